@@ -1,0 +1,367 @@
+"""Benchmark: RGB-D 640x480 frames/sec of the splat-observation hot path (BASELINE.json metric).
+
+Default workload = BASELINE config 2: a 1M-gaussian room scene (8 x 8 x 3 m) plus 4 skinned
+avatars (50k gaussians, 24 joints each), 64 environments per GPU, one 640x480 90 deg camera per env
+at 1.25 m, near 0.1 / far 100 (the reference agent-camera defaults, scene.py:23-24). A step =
+one batch: per-env avatar pose sampling + fused LBS, scene pass and avatar-layer pass
+(projection, SH, depth sort, tile binning, blend, composite) for all envs. Every step uses a fresh
+set of camera poses and sim times (pre-generated), so nothing is cached across steps; the scene
+(236 MB) and per-step buffers exceed the 126 MB L2.
+
+Multi-GPU (torchrun): each rank renders its own 64 envs against a replica of the scene (weak
+scaling, no data-path collective); timing is the max over ranks of CUDA-event time.
+
+--impl reference: the reference's algorithm on the host CPU (oracle/, the C restatement pinned to
+the reference) on all host threads, on a bounded sample of envs per step; rank 0 only.
+"""
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "RGB-D frames/sec (640×480) vs gaussian count & avatar count at 1/2/4/8 B200"
+STAGES = ("pose", "count", "scan", "emit", "depth_sort", "permute", "pair_scan", "duplicate", "pair_sort", "ranges",
+          "blend")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--envs", type=int, default=64, help="environments per GPU")
+    p.add_argument("--gaussians", type=int, default=1_000_000)
+    p.add_argument("--avatars", type=int, default=4)
+    p.add_argument("--near", type=float, default=0.1)
+    p.add_argument("--width", type=int, default=640)
+    p.add_argument("--height", type=int, default=480)
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-envs", type=int, default=0, help="env sample for the CPU baseline (0 = auto)")
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload(args, world, rank, n_sets):
+    """Scene + avatars (identical on every rank) and n_sets per-step (cameras, times) for this rank."""
+    from paper_2604_12626_b200 import synthetic as S
+    box = S.room_box(args.gaussians)
+    scene = S.make_scene(args.gaussians, box[0], box[1], seed=args.seed)
+    bundles = [S.make_avatar(50_000, seed=args.seed + 100 + i, floor_lo=box[0][:2], floor_hi=box[1][:2])
+               for i in range(args.avatars)]
+    sets = []
+    for s in range(n_sets):
+        cams = S.room_cameras(args.envs, box, seed=10_000 + (s * world + rank) * 7 + args.seed, width=args.width,
+                              height=args.height, near=args.near)
+        rng = np.random.default_rng(20_000 + s * world + rank)
+        times = rng.uniform(0.0, 2.0, size=args.envs)
+        sets.append((cams, times))
+    return scene, bundles, box, sets
+
+
+def start_offsets(n):
+    return [0.37 * i for i in range(n)]
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (median SM clock, throttle reasons)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None or not self.path or not os.path.exists(self.path):
+            return None
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx = max(mx, float(parts[2]))
+                except ValueError:
+                    continue
+                for name, flag in zip(names, parts[5:9]):
+                    if flag.lower() == "active":
+                        reasons.add(name)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def algorithmic_bytes(stage, pass_id, n_gauss, n_avatar_gauss, work, n_pix_total, n_steps):
+    """Minimum HBM bytes of one step's launches of `stage` (SURVEY.md 8(d) per-unit figures)."""
+    vis, pairs, loads = work[pass_id][0] / n_steps, work[pass_id][1] / n_steps, work[pass_id][2] / n_steps
+    n = n_gauss if pass_id == 0 else n_avatar_gauss
+    per_gauss_in = 48 if pass_id == 0 else 134  # packed params (+ skin influences for avatars)
+    if stage == "count":
+        return n * (per_gauss_in + 8)
+    if stage == "emit":
+        return n * (8 + per_gauss_in + 192) + vis * 88
+    if stage == "depth_sort":
+        return vis * 24
+    if stage == "permute":
+        return vis * 160
+    if stage == "pair_scan":
+        return vis * 12
+    if stage == "duplicate":
+        return vis * 16 + pairs * 8
+    if stage == "pair_sort":
+        return pairs * 16
+    if stage == "ranges":
+        return pairs * 4
+    if stage == "blend":
+        return loads * 68 + n_pix_total * (20 + (8 if pass_id == 0 else 24))
+    return 0.0
+
+
+def cpu_baseline(args, scene, bundles, sets, n_envs_sample):
+    """The reference algorithm (C oracle, pinned to the reference) on all host threads."""
+    from oracle import oracle as O
+    cams, times = sets[0]
+    cams = cams[:n_envs_sample]
+    times = times[:n_envs_sample]
+    threads = os.cpu_count() or 1
+    offs = start_offsets(len(bundles))
+    t0 = time.perf_counter()
+    per_env = []
+    for e in range(len(cams)):  # AvatarRuntime.deformed_cloud per env and avatar (tasks.py:501)
+        clouds = []
+        for a, b in enumerate(bundles):
+            t = offs[a] + float(times[e])
+            t = math.fmod(t, b.trajectory.duration)
+            q, tr = O.sample_pose(b.trajectory.quats, b.trajectory.trans, b.trajectory.fps, t)
+            pos, rot = O.lbs_deform(b.canonical.positions, b.canonical.rotations, b.lbs_weights, b.inv_bind, q, tr)
+            c = b.canonical
+            clouds.append(type(c)(pos, c.sh_coeffs, c.opacities, c.log_scales, rot))
+        per_env.append(O.concat_clouds(clouds) if clouds else None)
+    O.render_batch(scene, per_env if bundles else None, cams, np.ones(3), threads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": len(cams) / dt, "unit": "frames/s", "cores": threads, "kind": "port",
+            "sample": f"{len(cams)} envs of the same workload (scene {args.gaussians} gaussians, {len(bundles)} "
+                      f"avatars, {args.width}x{args.height}), LBS + render_observation per env, {dt:.1f} s wall"}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n_sample = args.cpu_envs or max(2, min(args.envs, threads))
+    scene, bundles, box, sets = workload(args, 1, 0, 1)
+    for _ in range(args.warmup):
+        cpu_baseline(args, scene, bundles, sets, min(n_sample, 2))
+    t0 = time.perf_counter()
+    frames = 0
+    for _ in range(args.steps):
+        r = cpu_baseline(args, scene, bundles, sets, n_sample)
+        frames += n_sample
+    dt = time.perf_counter() - t0
+    value = frames / dt
+    line = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE config 2 distributions, seeded)",
+        "impl": "reference",
+        "config": {"workload": f"config2: {args.gaussians} scene + {args.avatars}x50k avatars, "
+                               f"{args.width}x{args.height}, near {args.near}", "envs_per_step": n_sample},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "port",
+                         "sample": r["sample"]},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2604_12626_b200 import _native as N
+    from paper_2604_12626_b200.batch import BatchRenderer
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n_sets = args.warmup + args.steps
+    scene, bundles, box, sets = workload(args, world, rank, n_sets)
+    br = BatchRenderer(scene, bundles, start_offsets=start_offsets(len(bundles)), background=(1.0, 1.0, 1.0))
+    stage_ms = np.zeros(2 * len(STAGES))
+    work = np.zeros(8, dtype=np.int64)
+
+    def step(i, timed):
+        cams, times = sets[i]
+        from paper_2604_12626_b200.renderer import render_frames
+        opts = dict(avatars=br.avatars, sim_times=times, context=br.context, stats=False)
+        if timed:
+            opts["stage_ms"] = stage_ms
+            opts["work"] = work
+        return render_frames(br.scene, cams, br.background, **opts)
+
+    for i in range(args.warmup):
+        step(i, False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        ev0.record()
+        for i in range(args.steps):
+            step(args.warmup + i, True)
+        ev1.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    frames = args.envs * world * args.steps
+    value = frames / (ms_max / 1e3)
+
+    # end to end through the public API with host buffers: camera/time structs go host->device,
+    # frames come back to pinned host memory every step
+    e2e = None
+    if not args.no_e2e:
+        host_out = None
+        br.render_to_host(sets[0][0], sets[0][1])
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(args.steps):
+            cams, times = sets[args.warmup + i]
+            host_out = br.render_to_host(cams, times, host_out)
+        e1.record()
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        te = torch.tensor([ems], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        h, w = args.height, args.width
+        e2e = {"value": frames / (float(te.item()) / 1e3), "unit": "frames/s",
+               "h2d_bytes_per_step": args.envs * (192 + 8), "d2h_bytes_per_step": args.envs * h * w * (12 + 4 + 4)}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peak, peak_kind = measured_peaks()
+    stage = stage_ms.reshape(2, len(STAGES))
+    w2 = work.reshape(2, 4)
+    n_pix = args.envs * args.width * args.height
+    n_av = sum(b.canonical.n for b in bundles)
+    per_stage = {}
+    for p, name in ((0, "scene"), (1, "layer")):
+        for k, sname in enumerate(STAGES):
+            if stage[p, k] > 0:
+                per_stage[f"{name}.{sname}"] = stage[p, k] / args.steps
+    dom = max(per_stage, key=per_stage.get)
+    pname, sname = dom.split(".")
+    pid = 0 if pname == "scene" else 1
+    alg = algorithmic_bytes(sname, pid, args.gaussians, n_av, w2, n_pix, args.steps)
+    achieved = alg / (per_stage[dom] / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                "alg_bytes_per_step": alg, "ms_per_step": per_stage[dom],
+                "share_of_step": per_stage[dom] / (ms_max / args.steps)}
+    line = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64 geometry/decisions, f32 colour", "data": "synthetic (seeded, BASELINE distributions)",
+        "config": {"workload": f"config2: {args.gaussians} scene gaussians + {args.avatars}x50k skinned avatars, "
+                               f"{args.envs} envs/GPU, {args.width}x{args.height}, near {args.near}",
+                   "envs_per_gpu": args.envs, "n_gaussians": args.gaussians, "n_avatars": args.avatars,
+                   "l2": "inputs larger than L2 (236 MB scene + per-step buffers), fresh cameras every step",
+                   "parallelism": f"env-sharded x{world}"},
+        "gpu_launches": None, "roofline": roofline, "e2e": e2e,
+        "stages_ms_per_step": {k: round(v, 4) for k, v in per_stage.items()},
+        "work_per_step": {"scene_visible": int(w2[0, 0] / args.steps), "scene_pairs": int(w2[0, 1] / args.steps),
+                          "scene_records_loaded": int(w2[0, 2] / args.steps),
+                          "layer_visible": int(w2[1, 0] / args.steps), "layer_pairs": int(w2[1, 1] / args.steps)},
+        "clocks": clocks.summary(),
+    }
+    line["gpu_launches"] = launches_per_step(args) * args.steps
+    if world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        line["cpu_baseline"] = cpu_baseline(args, scene, bundles, sets, args.cpu_envs or max(2, min(args.envs, threads)))
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def launches_per_step(args):
+    """Kernels sn_render launches per step (ours only; CUB sorts/scans counted as library launches
+    separately): per pass: count, block scan, env offsets, emit, permute, duplicate, ranges, blend
+    (+ pose kernel for the avatar layer)."""
+    chunks = -(-args.envs // 64)
+    per_pass = 8
+    return chunks * per_pass * (2 if args.avatars else 1) + (1 if args.avatars else 0)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,209 @@
+/*
+ * splatnav_b200.h -- C ABI of the B200-native splat-observation hot path.
+ *
+ * This is the drop-in boundary for the reference package "splatnav"
+ * (/root/reference/pkg/src/splatnav). Plain C: no torch or CUDA C++ types. Memory arguments
+ * are DEVICE pointers unless a parameter says "host". Every function returns SN_OK (0) or an
+ * error code; sn_last_error() gives a thread-local message. Launches are asynchronous on the
+ * given stream. sn_render() synchronizes the stream internally to size its workspace (twice
+ * per pass).
+ *
+ * Reference interfaces replaced (file:line under /root/reference/pkg/src/splatnav):
+ *   sn_render ................ renderer.render_observation (renderer.py:169-177) batched over
+ *                              E environments; with no avatars it is renderer.rasterize
+ *                              (renderer.py:135); opts.tiled=0 gives rasterize_reference (:145)
+ *   sn_blend_tile_range ...... raster._kernels_cy.blend_tile_range (_kernels_cy.pyx:89-114), the
+ *                              reference's only FFI, same arguments (HOST buffers), for
+ *                              raster.get_kernel("cuda") (raster/__init__.py:26-36)
+ *   sn_composite ............. renderer.composite (renderer.py:151-166)
+ *   sn_sample_pose ........... rig.sample_pose (rig.py:78-104) + AvatarRuntime.clock
+ *                              (tasks.py:299-305), batched
+ *   sn_skin_lbs .............. rig.lbs_deform (rig.py:107-146)
+ *   sn_get_* ................. harness views of intermediates the reference computes inside
+ *                              project_cloud (projection.py:184 sorted ids) and _bin_tiles
+ *                              (renderer.py:80-101 tile CSR)
+ */
+#ifndef SPLATNAV_B200_H
+#define SPLATNAV_B200_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SN_ABI_VERSION 1
+
+enum {
+    SN_OK = 0,
+    SN_ERR_INVALID = 1, /* bad argument / contract violation (python: ContractViolation) */
+    SN_ERR_CUDA = 2,    /* CUDA runtime error */
+    SN_ERR_NOMEM = 3    /* device allocation failed */
+};
+
+enum { SN_FLOAT32 = 0, SN_FLOAT64 = 1 };
+
+/* Pinhole camera (camera.py:16-56). 192 bytes. `center` is Camera.center as the host computes it
+ * (-R^T t, camera.py:43-48); has_background = 0 selects layer mode (renderer.py:69-71). */
+typedef struct sn_camera {
+    double fx, fy, cx, cy, near_, far_;
+    double rot[9];   /* world_to_camera[:3,:3], row-major */
+    double trans[3]; /* world_to_camera[:3,3] */
+    double center[3];
+    double background[3];
+    int32_t width, height, has_background, pad;
+} sn_camera;
+
+/* RenderStats (projection.py:30-36), one per environment. */
+typedef struct sn_stats {
+    int64_t n_input, n_culled_depth, n_culled_frame, n_degenerate, n_drawn;
+} sn_stats;
+
+/* Device-resident scene cloud, packed once at load:
+ *   pos_opacity (n,4): x, y, z, opacity logit      -- float or double (dtype)
+ *   log_scales  (n,4): s0, s1, s2, unused          -- dtype
+ *   rotations   (n,4): w, x, y, z (raw, renormalized on use like build_cov3d)  -- dtype
+ *   sh          (K*3, n) float32, structure-of-arrays (coefficient k, channel c at row 3k+c) */
+typedef struct sn_cloud {
+    int64_t n;
+    int32_t sh_k;
+    int32_t dtype;
+    const void *pos_opacity;
+    const void *log_scales;
+    const void *rotations;
+    const float *sh;
+} sn_cloud;
+
+/* Device-resident avatar set: A avatars concatenated (render_observation's concat_clouds
+ * order), canonical data in float64, skinning as up to 4 (joint, weight) influences per
+ * gaussian in ascending joint order (the dense N x J rows of the bundle, avatar.py:127-178).
+ *   pos_opacity (n,4) f64, log_scales (n,4) f64, rotations (n,4) f64, sh (K*3, n) f32
+ *   joints (n) uint32: 4 x uint8 joint ids, weights (n,4) f64 (zero = unused slot)
+ *   avatar_of (n) uint16
+ *   inv_bind (A, J, 16) f64, traj_q (sum_a T_a*(J+1)*4) f64, traj_t (sum_a T_a*(J+1)*3) f64
+ *   traj_offset (A) int64 frame offsets into traj_*, n_frames (A) int32, fps (A) f64,
+ *   start_offset (A) f64, loop (A) int32    -- AvatarRuntime fields (tasks.py:290-297) */
+typedef struct sn_avatars {
+    int64_t n;
+    int32_t n_avatars;
+    int32_t n_joints;
+    int32_t sh_k;
+    int32_t pad;
+    const double *pos_opacity;
+    const double *log_scales;
+    const double *rotations;
+    const float *sh;
+    const uint32_t *joints;
+    const double *weights;
+    const uint16_t *avatar_of;
+    const double *inv_bind;
+    const double *traj_q;
+    const double *traj_t;
+    const int64_t *traj_offset;
+    const int32_t *n_frames;
+    const double *fps;
+    const double *start_offset;
+    const int32_t *loop;
+} sn_avatars;
+
+/* Stages timed by sn_render_opts.stage_ms (per pass: 0 = scene, 1 = layer). */
+enum {
+    SN_STAGE_POSE = 0,      /* sample_pose + joint matrices (layer pass only) */
+    SN_STAGE_COUNT = 1,     /* (skin +) project + cull + visibility counts */
+    SN_STAGE_SCAN = 2,      /* per-env block scan */
+    SN_STAGE_EMIT = 3,      /* (skin +) project + SH + record write */
+    SN_STAGE_DEPTH_SORT = 4,
+    SN_STAGE_PERMUTE = 5,
+    SN_STAGE_PAIR_SCAN = 6,
+    SN_STAGE_DUPLICATE = 7,
+    SN_STAGE_PAIR_SORT = 8,
+    SN_STAGE_RANGES = 9,
+    SN_STAGE_BLEND = 10,
+    SN_N_STAGES = 11
+};
+
+/* Per-call options. Null pointers disable the corresponding output. */
+typedef struct sn_render_opts {
+    int32_t tiled;          /* 1: tile pipeline (rasterize); 0: rasterize_reference semantics */
+    int32_t pad0;
+    const uint8_t *avatar_active; /* device (E, A) 0/1, NULL = all active */
+    int32_t *contrib_scene; /* device (E,H,W): splats accumulated per pixel, scene pass */
+    int32_t *contrib_layer; /* device (E,H,W): avatar-layer pass */
+    sn_stats *stats;        /* device (E): RenderStats accumulated over both passes */
+    double *stage_ms;       /* HOST (2 x SN_N_STAGES): GPU ms per stage (CUDA events), accumulated */
+    int64_t *work;          /* HOST (2 x 4): visible splats, tile pairs, records gathered by the
+                               blend, blend CTAs -- per pass, accumulated */
+} sn_render_opts;
+
+typedef struct sn_context sn_context;
+
+int sn_abi_version(void);
+const char *sn_last_error(void);
+
+/* One context per (device, thread). Owns the workspace; grows it on demand. */
+int sn_context_create(sn_context **ctx);
+int sn_context_destroy(sn_context *ctx);
+/* Bytes of device workspace currently held. */
+int sn_context_workspace_bytes(const sn_context *ctx, size_t *bytes);
+
+/*
+ * Render E environments: scene pass with the cameras' background (layer mode when the cameras
+ * have none), then one layer pass depth-composited over it (render_observation):
+ *   layer != NULL   -- an already-deformed cloud (concat_clouds of the avatar clouds), same for
+ *                      every env;
+ *   avatars != NULL -- the avatar set, skinned on device at each env's sim time (fused LBS).
+ * At most one of the two. All cameras must share width/height and background mode. cams and
+ * sim_times are HOST arrays (E entries). Outputs are device float32: color (E,H,W,3),
+ * alpha (E,H,W), depth (E,H,W).
+ */
+int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, const sn_avatars *avatars,
+              const sn_camera *cams, const double *sim_times, int32_t n_envs, const sn_render_opts *opts,
+              float *color, float *alpha, float *depth, void *stream);
+
+/* Intermediates of the last sn_render pass (0 = scene, 1 = avatar layer) for env e, copied to
+ * HOST buffers. sn_get_counts: visible splats and tile pairs. sorted_ids: original gaussian
+ * index per depth rank (projection.py:184). tile_starts (T+1) / pair_splat (P): the tile CSR
+ * with depth ranks as values (renderer.py:80-101). */
+int sn_get_counts(sn_context *ctx, int32_t pass, int32_t env, int64_t *n_visible, int64_t *n_pairs);
+int sn_get_sorted_ids(sn_context *ctx, int32_t pass, int32_t env, int32_t *ids_host, int64_t capacity);
+int sn_get_tile_csr(sn_context *ctx, int32_t pass, int32_t env, int64_t *tile_starts_host, int32_t *pair_splat_host,
+                    int64_t capacity);
+/* Depth-sorted per-splat projection outputs of the last pass for env e (HOST, capacity M):
+ * means2d (M,2), conics (M,3), depths (M), colors (M,3), alphas (M) -- project_cloud's arrays. */
+int sn_get_projection(sn_context *ctx, int32_t pass, int32_t env, double *means2d, double *conics, double *depths,
+                      double *colors, double *alphas, int64_t capacity);
+
+/*
+ * sample_pose + joint preparation for E x A (env, avatar) pairs at HOST sim_times (E):
+ * writes device pose_q (E*A, J+1, 4) and pose_t (E*A, J+1, 3), root last, exactly as
+ * rig.sample_pose returns them (after AvatarRuntime.clock). Returns SN_ERR_INVALID for a
+ * negative sample time (rig.py:80-81).
+ */
+int sn_sample_pose(sn_context *ctx, const sn_avatars *avatars, const double *sim_times, int32_t n_envs,
+                   double *pose_q, double *pose_t, void *stream);
+
+/* lbs_deform for avatar `avatar`, whose gaussians are [g_begin, g_begin + g_count) of the set, at
+ * explicit device poses pose_q (J+1,4) / pose_t (J+1,3), root last: writes device float64
+ * positions (g_count,3) and rotations (g_count,4). */
+int sn_skin_lbs(sn_context *ctx, const sn_avatars *avatars, int32_t avatar, int64_t g_begin, int64_t g_count,
+                const double *pose_q, const double *pose_t, double *out_positions, double *out_rotations,
+                void *stream);
+
+/* blend_tile_range with the reference's exact argument list; all buffers are HOST memory
+ * (float64 / int64 / int32 as in _kernels_cy.pyx:89-114); accumulates into the caller's buffers. */
+int sn_blend_tile_range(int32_t t_begin, int32_t t_end, int32_t tiles_x, int32_t tile_size, int32_t width,
+                        int32_t height, const int64_t *tile_starts, int64_t n_tiles_plus1, const int32_t *pair_splat,
+                        int64_t n_pairs, const double *means2d, const double *conics, const double *depths,
+                        const double *colors, const double *alphas, int64_t n_splats, double *color_acc,
+                        double *alpha_acc, double *trans, double *depth_acc);
+
+/* composite(front, back) on device float64 frames of npix pixels (renderer.py:151-166). */
+int sn_composite(int64_t npix, const double *front_color, const double *front_alpha, const double *front_depth,
+                 const double *back_color, const double *back_alpha, const double *back_depth, double *out_color,
+                 double *out_alpha, double *out_depth, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

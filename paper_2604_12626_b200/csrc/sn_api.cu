@@ -1,0 +1,713 @@
+// sn_api.cu -- the C ABI (include/splatnav_b200.h): context/workspace and pass orchestration.
+//
+// A pass (scene, or the concatenated avatar layer) over a chunk of <= 64 envs is:
+//   count -> per-env block scan -> [sync: visible total] -> emit -> depth sort -> permute
+//   -> pair-offset scan -> [sync: pair total] -> duplicate -> pair sort -> ranges -> blend.
+// The two host syncs size the workspace; buffers only grow, so a steady-state batch loop
+// allocates nothing.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sn_common.cuh"
+#include "sn_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string &msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define SN_CUDA(expr)                                                                                      \
+    do {                                                                                                   \
+        cudaError_t _e = (expr);                                                                           \
+        if (_e != cudaSuccess)                                                                             \
+            return fail(SN_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));                  \
+    } while (0)
+
+#define SN_CHECK(cond, msg)                         \
+    do {                                            \
+        if (!(cond)) return fail(SN_ERR_INVALID, msg); \
+    } while (0)
+
+struct Buf {
+    void *p = nullptr;
+    size_t cap = 0;
+    template <typename T>
+    T *as() const {
+        return static_cast<T *>(p);
+    }
+};
+
+int ensure(Buf &b, size_t bytes) {
+    if (bytes <= b.cap && b.p != nullptr) return SN_OK;
+    size_t want = std::max<size_t>(bytes + bytes / 4, 256);
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+    cudaError_t e = cudaMalloc(&b.p, want);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SN_ERR_NOMEM, std::string("cudaMalloc(") + std::to_string(want) + "): " + cudaGetErrorString(e));
+    }
+    b.cap = want;
+    return SN_OK;
+}
+
+#define SN_ENSURE(buf, bytes)                 \
+    do {                                      \
+        int _r = ensure((buf), (bytes));      \
+        if (_r != SN_OK) return _r;           \
+    } while (0)
+
+int bit_length(uint64_t v) { return v == 0 ? 0 : 64 - __builtin_clzll(v); }
+
+uint64_t dbits(double d) {
+    uint64_t u;
+    std::memcpy(&u, &d, 8);
+    return u;
+}
+
+struct PassWs {
+    Buf vismask, blk_counts, env_off, keys_un, keys_s, vals_un, vals_s, recs_un, recs, gid_un, gid, rects_un, rects,
+        tiles, pair_off, pkeys_a, pkeys_b, pvals_a, pvals_b, ranges, temp;
+    // metadata of the last chunk rendered by this pass
+    int32_t e0 = 0, ec = 0, tiles_x = 0, tiles_y = 0, tile_bits = 0, tiled = 1, valid = 0;
+    int64_t n_vis = 0, n_pairs = 0;
+};
+
+}  // namespace
+
+struct sn_context {
+    PassWs pass[2];
+    Buf cams, times, depth64, jm, eq, root, err, pose_q, pose_t, loads;
+    uint64_t *h_tot = nullptr;  // pinned
+    int32_t *h_err = nullptr;   // pinned
+    cudaEvent_t ev[2 * SN_N_STAGES] = {};
+    bool have_events = false;
+};
+
+namespace {
+
+// Stage timer: CUDA events around each stage on the render stream (only when requested).
+// Elapsed times are resolved in flush() once the pass is queued, so timing adds no host sync
+// between stages beyond the ones the pass already has.
+struct StageTimer {
+    sn_context *ctx;
+    cudaStream_t st;
+    double *ms;  // host (SN_N_STAGES) for this pass, or null
+    int open = -1;
+    bool pending[SN_N_STAGES] = {};
+    void begin(int stage) {
+        if (!ms) return;
+        if (pending[stage]) flush();
+        open = stage;
+        cudaEventRecord(ctx->ev[2 * stage], st);
+    }
+    void end() {
+        if (!ms || open < 0) return;
+        cudaEventRecord(ctx->ev[2 * open + 1], st);
+        pending[open] = true;
+        open = -1;
+    }
+    void flush() {
+        if (!ms) return;
+        for (int s = 0; s < SN_N_STAGES; ++s) {
+            if (!pending[s]) continue;
+            cudaEventSynchronize(ctx->ev[2 * s + 1]);
+            float t = 0.0f;
+            if (cudaEventElapsedTime(&t, ctx->ev[2 * s], ctx->ev[2 * s + 1]) == cudaSuccess) ms[s] += t;
+            pending[s] = false;
+        }
+    }
+    ~StageTimer() { flush(); }
+};
+
+}  // namespace
+
+namespace {
+
+using namespace sn;
+
+struct PassSpec {
+    const sn_cloud *scene = nullptr;
+    const sn_avatars *avatars = nullptr;
+    PoseView pose{};
+    const uint8_t *avatar_active = nullptr;
+    int mode = 0;
+};
+
+int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, int width, int height, int tiled,
+             uint64_t z_base, int z_bits, const sn_render_opts *opts, float *color, float *alpha, float *depth,
+             double *depth64, cudaStream_t st) {
+    PassWs &w = ctx->pass[pass_id];
+    StageTimer tm{ctx, st, opts && opts->stage_ms ? opts->stage_ms + pass_id * SN_N_STAGES : nullptr};
+    int64_t *work = opts && opts->work ? opts->work + pass_id * 4 : nullptr;
+    const int64_t n = sp.scene ? sp.scene->n : sp.avatars->n;
+    const int tiles_x = tiles_of(width), tiles_y = tiles_of(height);
+    const int n_tiles = tiles_x * tiles_y;
+    const int tile_bits = std::max(1, bit_length((uint64_t)(n_tiles - 1)));
+    const int env_bits = bit_length((uint64_t)(ec - 1));
+    const int32_t n_blocks = (int32_t)std::max<int64_t>(1, (n + kBlock - 1) / kBlock);
+
+    SN_ENSURE(w.vismask, sizeof(uint64_t) * std::max<int64_t>(n, 1));
+    SN_ENSURE(w.blk_counts, sizeof(uint32_t) * (size_t)ec * n_blocks);
+    SN_ENSURE(w.env_off, sizeof(uint64_t) * (ec + 1));
+    SN_CUDA(cudaMemsetAsync(w.env_off.p, 0, sizeof(uint64_t) * (ec + 1), st));
+
+    PrepArgs a{};
+    a.cams = ctx->cams.as<sn_camera>();
+    a.e0 = e0;
+    a.ec = ec;
+    a.n_blocks = n_blocks;
+    a.vismask = w.vismask.as<uint64_t>();
+    a.blk_counts = w.blk_counts.as<uint32_t>();
+    a.stats = opts && opts->stats ? reinterpret_cast<unsigned long long *>(opts->stats) : nullptr;
+    a.avatar_active = sp.avatar_active;
+    a.tiles_x = tiles_x;
+    a.tiles_y = tiles_y;
+    a.z_base = z_base;
+    a.z_bits = z_bits;
+
+    int64_t V = 0;
+    if (n > 0) {
+        tm.begin(SN_STAGE_COUNT);
+        if (sp.scene)
+            SN_CUDA(launch_scene_count(*sp.scene, a, st));
+        else
+            SN_CUDA(launch_avatar_count(*sp.avatars, sp.pose, a, st));
+        tm.end();
+        tm.begin(SN_STAGE_SCAN);
+        SN_CUDA(launch_block_scan(a.blk_counts, n_blocks, ec, w.env_off.as<uint64_t>(), st));
+        tm.end();
+        SN_CUDA(cudaMemcpyAsync(ctx->h_tot, w.env_off.as<uint64_t>() + ec, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        SN_CUDA(cudaStreamSynchronize(st));
+        V = (int64_t)ctx->h_tot[0];
+    }
+    SN_CHECK(V < (int64_t)0xffffffffLL, "too many visible splats in one env chunk (limit 2^32)");
+    const size_t v1 = (size_t)V + 1;
+    SN_ENSURE(w.keys_un, sizeof(uint64_t) * v1);
+    SN_ENSURE(w.keys_s, sizeof(uint64_t) * v1);
+    SN_ENSURE(w.vals_un, sizeof(uint32_t) * v1);
+    SN_ENSURE(w.vals_s, sizeof(uint32_t) * v1);
+    SN_ENSURE(w.recs_un, sizeof(SplatRec) * v1);
+    SN_ENSURE(w.recs, sizeof(SplatRec) * v1);
+    SN_ENSURE(w.gid_un, sizeof(uint32_t) * v1);
+    SN_ENSURE(w.gid, sizeof(uint32_t) * v1);
+    SN_ENSURE(w.rects_un, sizeof(ushort4) * v1);
+    SN_ENSURE(w.rects, sizeof(ushort4) * v1);
+    SN_ENSURE(w.tiles, sizeof(uint32_t) * v1);
+    SN_ENSURE(w.pair_off, sizeof(uint64_t) * v1);
+
+    a.env_off = w.env_off.as<uint64_t>();
+    a.keys = w.keys_un.as<unsigned long long>();
+    a.vals = w.vals_un.as<uint32_t>();
+    a.recs = w.recs_un.as<SplatRec>();
+    a.gid = w.gid_un.as<uint32_t>();
+    a.rects = w.rects_un.as<ushort4>();
+
+    BinArgs b{};
+    b.ec = ec;
+    b.tiles_x = tiles_x;
+    b.tiles_y = tiles_y;
+    b.tile_bits = tile_bits;
+    b.z_bits = z_bits;
+    b.n_vis = V;
+    b.keys_sorted = w.keys_s.as<unsigned long long>();
+    b.vals_sorted = w.vals_s.as<uint32_t>();
+    b.recs_in = w.recs_un.as<SplatRec>();
+    b.gid_in = w.gid_un.as<uint32_t>();
+    b.rects_in = w.rects_un.as<ushort4>();
+    b.env_off = w.env_off.as<uint64_t>();
+    b.recs_out = w.recs.as<SplatRec>();
+    b.gid_out = w.gid.as<uint32_t>();
+    b.rects_out = w.rects.as<ushort4>();
+    b.tiles_touched = w.tiles.as<uint32_t>();
+    b.pair_off = w.pair_off.as<uint64_t>();
+
+    int64_t P = 0;
+    if (V > 0) {
+        size_t tb = std::max(sort_u64_temp_bytes(V), scan_temp_bytes(V + 1));
+        SN_ENSURE(w.temp, tb);
+        tm.begin(SN_STAGE_EMIT);
+        if (sp.scene)
+            SN_CUDA(launch_scene_emit(*sp.scene, a, st));
+        else
+            SN_CUDA(launch_avatar_emit(*sp.avatars, sp.pose, a, st));
+        tm.end();
+        tm.begin(SN_STAGE_DEPTH_SORT);
+        SN_CUDA(sort_u64_pairs(w.temp.p, w.temp.cap, w.keys_un.as<unsigned long long>(),
+                               w.keys_s.as<unsigned long long>(), w.vals_un.as<uint32_t>(), w.vals_s.as<uint32_t>(), V,
+                               z_bits + env_bits, st));
+        tm.end();
+        tm.begin(SN_STAGE_PERMUTE);
+        SN_CUDA(launch_permute(b, st));
+        tm.end();
+        if (tiled) {
+            SN_CUDA(cudaMemsetAsync(w.tiles.as<uint32_t>() + V, 0, sizeof(uint32_t), st));
+            tm.begin(SN_STAGE_PAIR_SCAN);
+            SN_CUDA(scan_tiles(w.temp.p, w.temp.cap, w.tiles.as<uint32_t>(), w.pair_off.as<uint64_t>(), V + 1, st));
+            tm.end();
+            SN_CUDA(cudaMemcpyAsync(ctx->h_tot, w.pair_off.as<uint64_t>() + V, sizeof(uint64_t),
+                                    cudaMemcpyDeviceToHost, st));
+            SN_CUDA(cudaStreamSynchronize(st));
+            P = (int64_t)ctx->h_tot[0];
+            SN_CHECK(P < (int64_t)0x7fffffffLL, "too many tile pairs in one env chunk (limit 2^31)");
+        }
+    }
+    const size_t n_ranges = (size_t)ec << tile_bits;
+    SN_ENSURE(w.ranges, sizeof(uint2) * n_ranges);
+    SN_CUDA(cudaMemsetAsync(w.ranges.p, 0, sizeof(uint2) * n_ranges, st));
+    if (P > 0) {
+        SN_ENSURE(w.pkeys_a, sizeof(uint32_t) * P);
+        SN_ENSURE(w.pkeys_b, sizeof(uint32_t) * P);
+        SN_ENSURE(w.pvals_a, sizeof(uint32_t) * P);
+        SN_ENSURE(w.pvals_b, sizeof(uint32_t) * P);
+        size_t tb = sort_u32_temp_bytes(P);
+        SN_ENSURE(w.temp, tb);
+        b.pair_keys = w.pkeys_a.as<uint32_t>();
+        b.pair_vals = w.pvals_a.as<uint32_t>();
+        tm.begin(SN_STAGE_DUPLICATE);
+        SN_CUDA(launch_duplicate(b, st));
+        tm.end();
+        tm.begin(SN_STAGE_PAIR_SORT);
+        SN_CUDA(sort_u32_pairs(w.temp.p, w.temp.cap, w.pkeys_a.as<uint32_t>(), w.pkeys_b.as<uint32_t>(),
+                               w.pvals_a.as<uint32_t>(), w.pvals_b.as<uint32_t>(), P, env_bits + tile_bits, st));
+        tm.end();
+        tm.begin(SN_STAGE_RANGES);
+        SN_CUDA(launch_ranges(w.pkeys_b.as<uint32_t>(), P, w.ranges.as<uint2>(), st));
+        tm.end();
+    }
+
+    BlendArgs bl{};
+    bl.cams = ctx->cams.as<sn_camera>();
+    bl.e0 = e0;
+    bl.ec = ec;
+    bl.width = width;
+    bl.height = height;
+    bl.tiles_x = tiles_x;
+    bl.tile_bits = tile_bits;
+    bl.brute = tiled ? 0 : 1;
+    bl.mode = sp.mode;
+    bl.ranges = w.ranges.as<uint2>();
+    bl.pair_vals = w.pvals_b.as<uint32_t>();
+    bl.env_off = w.env_off.as<uint64_t>();
+    bl.recs = w.recs.as<SplatRec>();
+    bl.color = color;
+    bl.alpha = alpha;
+    bl.depth = depth;
+    bl.depth64 = depth64;
+    bl.contrib = opts ? (pass_id == 0 ? opts->contrib_scene : opts->contrib_layer) : nullptr;
+    if (work) {
+        SN_ENSURE(ctx->loads, sizeof(unsigned long long));
+        SN_CUDA(cudaMemsetAsync(ctx->loads.p, 0, sizeof(unsigned long long), st));
+        bl.loads = ctx->loads.as<unsigned long long>();
+    }
+    tm.begin(SN_STAGE_BLEND);
+    SN_CUDA(launch_blend(bl, st));
+    tm.end();
+    if (work) {
+        SN_CUDA(cudaMemcpyAsync(ctx->h_tot + 1, ctx->loads.p, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        SN_CUDA(cudaStreamSynchronize(st));
+        work[0] += V;
+        work[1] += P;
+        work[2] += (int64_t)ctx->h_tot[1];
+        work[3] += (int64_t)ec * tiles_x * tiles_y;
+    }
+
+    w.e0 = e0;
+    w.ec = ec;
+    w.tiles_x = tiles_x;
+    w.tiles_y = tiles_y;
+    w.tile_bits = tile_bits;
+    w.tiled = tiled;
+    w.n_vis = V;
+    w.n_pairs = P;
+    w.valid = 1;
+    return SN_OK;
+}
+
+int check_cloud(const sn_cloud *c) {
+    SN_CHECK(c != nullptr, "scene cloud is null");
+    SN_CHECK(c->n >= 0, "negative gaussian count");
+    SN_CHECK(c->n == 0 || (c->pos_opacity && c->log_scales && c->rotations && c->sh), "null scene buffer");
+    SN_CHECK(c->sh_k == 1 || c->sh_k == 4 || c->sh_k == 9 || c->sh_k == 16, "sh_k must be 1, 4, 9 or 16");
+    SN_CHECK(c->dtype == SN_FLOAT32 || c->dtype == SN_FLOAT64, "dtype must be SN_FLOAT32 or SN_FLOAT64");
+    SN_CHECK(c->n < (int64_t)0xffffffffLL, "scene too large for 32-bit splat ids");
+    return SN_OK;
+}
+
+int check_avatars(const sn_avatars *av) {
+    SN_CHECK(av->n >= 0 && av->n_avatars >= 1, "avatar set needs at least one avatar");
+    SN_CHECK(av->n_joints >= 1 && av->n_joints <= 255, "n_joints must be in [1, 255]");
+    SN_CHECK(av->sh_k == 1 || av->sh_k == 4 || av->sh_k == 9 || av->sh_k == 16, "sh_k must be 1, 4, 9 or 16");
+    SN_CHECK(av->n == 0 || (av->pos_opacity && av->log_scales && av->rotations && av->sh && av->joints &&
+                            av->weights && av->avatar_of),
+             "null avatar buffer");
+    SN_CHECK(av->inv_bind && av->traj_q && av->traj_t && av->traj_offset && av->n_frames && av->fps &&
+                 av->start_offset && av->loop,
+             "null avatar trajectory buffer");
+    return SN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sn_abi_version(void) { return SN_ABI_VERSION; }
+
+const char *sn_last_error(void) { return g_last_error.c_str(); }
+
+int sn_context_create(sn_context **out) {
+    SN_CHECK(out != nullptr, "null output pointer");
+    sn_context *ctx = new sn_context();
+    cudaError_t e = cudaMallocHost(&ctx->h_tot, sizeof(uint64_t) * 4);
+    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_err, sizeof(int32_t) * 4);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return fail(SN_ERR_CUDA, std::string("cudaMallocHost: ") + cudaGetErrorString(e));
+    }
+    *out = ctx;
+    return SN_OK;
+}
+
+int sn_context_destroy(sn_context *ctx) {
+    if (!ctx) return SN_OK;
+    cudaDeviceSynchronize();
+    auto free_buf = [](Buf &b) {
+        if (b.p) cudaFree(b.p);
+        b.p = nullptr;
+    };
+    for (auto &w : ctx->pass) {
+        for (Buf *b : {&w.vismask, &w.blk_counts, &w.env_off, &w.keys_un, &w.keys_s, &w.vals_un, &w.vals_s, &w.recs_un,
+                       &w.recs, &w.gid_un, &w.gid, &w.rects_un, &w.rects, &w.tiles, &w.pair_off, &w.pkeys_a,
+                       &w.pkeys_b, &w.pvals_a, &w.pvals_b, &w.ranges, &w.temp})
+            free_buf(*b);
+    }
+    for (Buf *b : {&ctx->cams, &ctx->times, &ctx->depth64, &ctx->jm, &ctx->eq, &ctx->root, &ctx->err, &ctx->pose_q,
+                   &ctx->pose_t, &ctx->loads})
+        free_buf(*b);
+    if (ctx->have_events)
+        for (auto &ev : ctx->ev) cudaEventDestroy(ev);
+    if (ctx->h_tot) cudaFreeHost(ctx->h_tot);
+    if (ctx->h_err) cudaFreeHost(ctx->h_err);
+    delete ctx;
+    return SN_OK;
+}
+
+int sn_context_workspace_bytes(const sn_context *ctx, size_t *bytes) {
+    SN_CHECK(ctx && bytes, "null argument");
+    size_t t = 0;
+    for (const auto &w : ctx->pass)
+        for (const Buf *b : {&w.vismask, &w.blk_counts, &w.env_off, &w.keys_un, &w.keys_s, &w.vals_un, &w.vals_s,
+                             &w.recs_un, &w.recs, &w.gid_un, &w.gid, &w.rects_un, &w.rects, &w.tiles, &w.pair_off,
+                             &w.pkeys_a, &w.pkeys_b, &w.pvals_a, &w.pvals_b, &w.ranges, &w.temp})
+            t += b->cap;
+    for (const Buf *b : {&ctx->cams, &ctx->times, &ctx->depth64, &ctx->jm, &ctx->eq, &ctx->root, &ctx->err,
+                         &ctx->pose_q, &ctx->pose_t})
+        t += b->cap;
+    *bytes = t;
+    return SN_OK;
+}
+
+int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, const sn_avatars *avatars,
+              const sn_camera *cams, const double *sim_times, int32_t n_envs, const sn_render_opts *opts, float *color,
+              float *alpha, float *depth, void *stream) {
+    SN_CHECK(ctx != nullptr, "null context");
+    SN_CHECK(n_envs >= 1, "need at least one environment");
+    SN_CHECK(cams != nullptr && color && alpha && depth, "null camera or output buffer");
+    int r = check_cloud(scene);
+    if (r != SN_OK) return r;
+    SN_CHECK(layer == nullptr || avatars == nullptr, "pass either a layer cloud or an avatar set, not both");
+    const bool with_layer = layer != nullptr && layer->n > 0;
+    if (layer) {
+        r = check_cloud(layer);
+        if (r != SN_OK) return r;
+    }
+    const bool with_avatars = avatars != nullptr && avatars->n > 0;
+    if (with_avatars) {
+        r = check_avatars(avatars);
+        if (r != SN_OK) return r;
+        SN_CHECK(sim_times != nullptr, "avatars need per-env sim_times");
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int W = cams[0].width, H = cams[0].height;
+    SN_CHECK(W >= 1 && H >= 1, "camera size must be at least 1x1");
+    SN_CHECK(tiles_of(W) <= 65535 && tiles_of(H) <= 65535 && tiles_of(W) * tiles_of(H) <= (1 << 16),
+             "frame too large (at most 65536 tiles)");
+    uint64_t z_lo = ~0ull, z_hi = 0;
+    for (int e = 0; e < n_envs; ++e) {
+        const sn_camera &c = cams[e];
+        SN_CHECK(c.width == W && c.height == H, "all cameras of a batch must share width/height");
+        SN_CHECK(c.has_background == cams[0].has_background, "all cameras of a batch must share the background mode");
+        SN_CHECK(c.fx > 0 && c.fy > 0, "focal lengths must be positive");
+        SN_CHECK(c.near_ > 0 && c.near_ < c.far_, "need 0 < near < far");
+        z_lo = std::min(z_lo, dbits(c.near_));
+        z_hi = std::max(z_hi, dbits(c.far_));
+    }
+    const int z_bits = std::max(1, bit_length(z_hi - z_lo));
+    const int free_bits = 64 - z_bits;
+    const int chunk = free_bits >= 6 ? kMaxEnvChunk : (1 << free_bits);
+    const int tiled = opts ? opts->tiled : 1;
+    if (opts && opts->stage_ms && !ctx->have_events) {
+        for (auto &ev : ctx->ev) SN_CUDA(cudaEventCreate(&ev));
+        ctx->have_events = true;
+    }
+
+    SN_ENSURE(ctx->cams, sizeof(sn_camera) * n_envs);
+    SN_CUDA(cudaMemcpyAsync(ctx->cams.p, cams, sizeof(sn_camera) * n_envs, cudaMemcpyHostToDevice, st));
+    double *depth64 = nullptr;
+    if (with_avatars || with_layer) {
+        SN_ENSURE(ctx->depth64, sizeof(double) * (size_t)n_envs * W * H);
+        depth64 = ctx->depth64.as<double>();
+    }
+    if (opts && opts->stats) SN_CUDA(cudaMemsetAsync(opts->stats, 0, sizeof(sn_stats) * n_envs, st));
+
+    PassSpec scene_spec;
+    scene_spec.scene = scene;
+    scene_spec.mode = cams[0].has_background ? 0 : 1;
+    for (int e0 = 0; e0 < n_envs; e0 += chunk) {
+        int ec = std::min(chunk, n_envs - e0);
+        r = run_pass(ctx, 0, scene_spec, e0, ec, W, H, tiled, z_lo, z_bits, opts, color, alpha, depth, depth64, st);
+        if (r != SN_OK) return r;
+    }
+    if (with_layer) {
+        PassSpec layer_spec;
+        layer_spec.scene = layer;
+        layer_spec.mode = 2;
+        for (int e0 = 0; e0 < n_envs; e0 += chunk) {
+            int ec = std::min(chunk, n_envs - e0);
+            r = run_pass(ctx, 1, layer_spec, e0, ec, W, H, tiled, z_lo, z_bits, opts, color, alpha, depth, depth64,
+                         st);
+            if (r != SN_OK) return r;
+        }
+        return SN_OK;
+    }
+    if (!with_avatars) return SN_OK;
+
+    const int A = avatars->n_avatars, J = avatars->n_joints;
+    SN_ENSURE(ctx->times, sizeof(double) * n_envs);
+    SN_CUDA(cudaMemcpyAsync(ctx->times.p, sim_times, sizeof(double) * n_envs, cudaMemcpyHostToDevice, st));
+    SN_ENSURE(ctx->jm, sizeof(double) * (size_t)n_envs * A * J * 12);
+    SN_ENSURE(ctx->eq, sizeof(double) * (size_t)n_envs * A * J * 4);
+    SN_ENSURE(ctx->root, sizeof(double) * (size_t)n_envs * A * 12);
+    SN_ENSURE(ctx->err, sizeof(int32_t));
+    SN_CUDA(cudaMemsetAsync(ctx->err.p, 0, sizeof(int32_t), st));
+    StageTimer ptm{ctx, st, opts && opts->stage_ms ? opts->stage_ms + SN_N_STAGES : nullptr};
+    ptm.begin(SN_STAGE_POSE);
+    SN_CUDA(launch_pose(*avatars, ctx->times.as<double>(), n_envs, nullptr, nullptr, ctx->jm.as<double>(),
+                        ctx->eq.as<double>(), ctx->root.as<double>(), ctx->err.as<int32_t>(), st));
+    ptm.end();
+    SN_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->err.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    SN_CUDA(cudaStreamSynchronize(st));
+    SN_CHECK(ctx->h_err[0] == 0, "sample time must be nonnegative");
+
+    PassSpec av_spec;
+    av_spec.avatars = avatars;
+    av_spec.pose = PoseView{ctx->jm.as<double>(), ctx->eq.as<double>(), ctx->root.as<double>(), J, A};
+    av_spec.avatar_active = opts ? opts->avatar_active : nullptr;
+    av_spec.mode = 2;
+    for (int e0 = 0; e0 < n_envs; e0 += chunk) {
+        int ec = std::min(chunk, n_envs - e0);
+        r = run_pass(ctx, 1, av_spec, e0, ec, W, H, tiled, z_lo, z_bits, opts, color, alpha, depth, depth64, st);
+        if (r != SN_OK) return r;
+    }
+    return SN_OK;
+}
+
+static int pass_env(sn_context *ctx, int32_t pass, int32_t env, PassWs *&w, int &el, std::vector<uint64_t> &off) {
+    SN_CHECK(ctx != nullptr && (pass == 0 || pass == 1), "bad context or pass");
+    w = &ctx->pass[pass];
+    SN_CHECK(w->valid, "no render recorded for this pass");
+    SN_CHECK(env >= w->e0 && env < w->e0 + w->ec, "env not in the last rendered chunk of this pass");
+    el = env - w->e0;
+    off.resize(w->ec + 1);
+    SN_CUDA(cudaDeviceSynchronize());
+    SN_CUDA(cudaMemcpy(off.data(), w->env_off.p, sizeof(uint64_t) * (w->ec + 1), cudaMemcpyDeviceToHost));
+    return SN_OK;
+}
+
+int sn_get_counts(sn_context *ctx, int32_t pass, int32_t env, int64_t *n_visible, int64_t *n_pairs) {
+    PassWs *w;
+    int el;
+    std::vector<uint64_t> off;
+    int r = pass_env(ctx, pass, env, w, el, off);
+    if (r != SN_OK) return r;
+    int64_t v0 = (int64_t)off[el], v1 = (int64_t)off[el + 1];
+    if (n_visible) *n_visible = v1 - v0;
+    if (n_pairs) {
+        *n_pairs = 0;
+        if (w->tiled && w->n_vis > 0) {
+            uint64_t p[2];
+            SN_CUDA(cudaMemcpy(&p[0], w->pair_off.as<uint64_t>() + v0, 8, cudaMemcpyDeviceToHost));
+            SN_CUDA(cudaMemcpy(&p[1], w->pair_off.as<uint64_t>() + v1, 8, cudaMemcpyDeviceToHost));
+            *n_pairs = (int64_t)(p[1] - p[0]);
+        }
+    }
+    return SN_OK;
+}
+
+int sn_get_sorted_ids(sn_context *ctx, int32_t pass, int32_t env, int32_t *ids_host, int64_t capacity) {
+    PassWs *w;
+    int el;
+    std::vector<uint64_t> off;
+    int r = pass_env(ctx, pass, env, w, el, off);
+    if (r != SN_OK) return r;
+    int64_t m = (int64_t)(off[el + 1] - off[el]);
+    SN_CHECK(capacity >= m, "ids buffer too small");
+    if (m) SN_CUDA(cudaMemcpy(ids_host, w->gid.as<uint32_t>() + off[el], sizeof(int32_t) * m, cudaMemcpyDeviceToHost));
+    return SN_OK;
+}
+
+int sn_get_tile_csr(sn_context *ctx, int32_t pass, int32_t env, int64_t *tile_starts_host, int32_t *pair_splat_host,
+                    int64_t capacity) {
+    PassWs *w;
+    int el;
+    std::vector<uint64_t> off;
+    int r = pass_env(ctx, pass, env, w, el, off);
+    if (r != SN_OK) return r;
+    SN_CHECK(w->tiled, "last pass was not tiled");
+    const int n_tiles = w->tiles_x * w->tiles_y;
+    std::vector<uint2> rng(n_tiles);
+    SN_CUDA(cudaMemcpy(rng.data(), w->ranges.as<uint2>() + ((size_t)el << w->tile_bits), sizeof(uint2) * n_tiles,
+                       cudaMemcpyDeviceToHost));
+    int64_t p0 = 0, p1 = 0;
+    if (w->n_vis > 0) {
+        uint64_t pp[2];
+        SN_CUDA(cudaMemcpy(&pp[0], w->pair_off.as<uint64_t>() + off[el], 8, cudaMemcpyDeviceToHost));
+        SN_CUDA(cudaMemcpy(&pp[1], w->pair_off.as<uint64_t>() + off[el + 1], 8, cudaMemcpyDeviceToHost));
+        p0 = (int64_t)pp[0];
+        p1 = (int64_t)pp[1];
+    }
+    SN_CHECK(capacity >= p1 - p0, "pair buffer too small");
+    tile_starts_host[0] = 0;
+    for (int t = 0; t < n_tiles; ++t) tile_starts_host[t + 1] = tile_starts_host[t] + (int64_t)(rng[t].y - rng[t].x);
+    SN_CHECK(tile_starts_host[n_tiles] == p1 - p0, "tile ranges do not cover the env's pairs");
+    if (p1 > p0) {
+        std::vector<uint32_t> v((size_t)(p1 - p0));
+        SN_CUDA(cudaMemcpy(v.data(), w->pvals_b.as<uint32_t>() + p0, sizeof(uint32_t) * v.size(), cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < v.size(); ++i) pair_splat_host[i] = (int32_t)(v[i] - off[el]);
+    }
+    return SN_OK;
+}
+
+int sn_get_projection(sn_context *ctx, int32_t pass, int32_t env, double *means2d, double *conics, double *depths,
+                      double *colors, double *alphas, int64_t capacity) {
+    PassWs *w;
+    int el;
+    std::vector<uint64_t> off;
+    int r = pass_env(ctx, pass, env, w, el, off);
+    if (r != SN_OK) return r;
+    int64_t m = (int64_t)(off[el + 1] - off[el]);
+    SN_CHECK(capacity >= m, "projection buffers too small");
+    std::vector<SplatRec> recs((size_t)m);
+    if (m) SN_CUDA(cudaMemcpy(recs.data(), w->recs.as<SplatRec>() + off[el], sizeof(SplatRec) * m, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < m; ++i) {
+        const SplatRec &s = recs[i];
+        means2d[2 * i] = s.mx;
+        means2d[2 * i + 1] = s.my;
+        conics[3 * i] = s.ca;
+        conics[3 * i + 1] = s.cb2 * 0.5;
+        conics[3 * i + 2] = s.cc;
+        depths[i] = s.z;
+        for (int c = 0; c < 3; ++c)
+            colors[3 * i + c] = (double)((s.rgb >> (21 * c)) & 0x1FFFFFull) * (1.0 / 2097151.0);
+        alphas[i] = s.alpha;
+    }
+    return SN_OK;
+}
+
+int sn_sample_pose(sn_context *ctx, const sn_avatars *avatars, const double *sim_times, int32_t n_envs,
+                   double *pose_q, double *pose_t, void *stream) {
+    SN_CHECK(ctx && avatars && sim_times && pose_q && pose_t && n_envs >= 1, "null argument");
+    int r = check_avatars(avatars);
+    if (r != SN_OK) return r;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    SN_ENSURE(ctx->times, sizeof(double) * n_envs);
+    SN_CUDA(cudaMemcpyAsync(ctx->times.p, sim_times, sizeof(double) * n_envs, cudaMemcpyHostToDevice, st));
+    SN_ENSURE(ctx->err, sizeof(int32_t));
+    SN_CUDA(cudaMemsetAsync(ctx->err.p, 0, sizeof(int32_t), st));
+    SN_CUDA(launch_pose(*avatars, ctx->times.as<double>(), n_envs, pose_q, pose_t, nullptr, nullptr, nullptr,
+                        ctx->err.as<int32_t>(), st));
+    SN_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->err.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    SN_CUDA(cudaStreamSynchronize(st));
+    SN_CHECK(ctx->h_err[0] == 0, "sample time must be nonnegative");
+    return SN_OK;
+}
+
+int sn_skin_lbs(sn_context *ctx, const sn_avatars *avatars, int32_t avatar, int64_t g_begin, int64_t g_count,
+                const double *pose_q, const double *pose_t, double *out_positions, double *out_rotations,
+                void *stream) {
+    SN_CHECK(ctx && avatars && pose_q && pose_t, "null argument");
+    int r = check_avatars(avatars);
+    if (r != SN_OK) return r;
+    SN_CHECK(avatar >= 0 && avatar < avatars->n_avatars, "avatar index out of range");
+    SN_CHECK(g_begin >= 0 && g_count >= 0 && g_begin + g_count <= avatars->n, "gaussian range out of bounds");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int J = avatars->n_joints;
+    SN_ENSURE(ctx->pose_q, sizeof(double) * (J * 12 + J * 4 + 12));
+    double *jm = ctx->pose_q.as<double>(), *eq = jm + J * 12, *root = eq + J * 4;
+    SN_CUDA(launch_joint_prep(*avatars, avatar, pose_q, pose_t, jm, eq, root, st));
+    PoseView pv{jm, eq, root, J, 1};
+    SN_CUDA(launch_skin_range(*avatars, g_begin, g_count, pv, out_positions, out_rotations, st));
+    return SN_OK;
+}
+
+int sn_blend_tile_range(int32_t t_begin, int32_t t_end, int32_t tiles_x, int32_t tile_size, int32_t width,
+                        int32_t height, const int64_t *tile_starts, int64_t n_tiles_plus1, const int32_t *pair_splat,
+                        int64_t n_pairs, const double *means2d, const double *conics, const double *depths,
+                        const double *colors, const double *alphas, int64_t n_splats, double *color_acc,
+                        double *alpha_acc, double *trans, double *depth_acc) {
+    SN_CHECK(t_begin >= 0 && t_end >= t_begin && t_end < n_tiles_plus1, "tile range out of bounds");
+    SN_CHECK(tiles_x >= 1 && tile_size >= 1 && width >= 1 && height >= 1, "bad tiling");
+    if (t_end == t_begin) return SN_OK;
+    const size_t npix = (size_t)width * height;
+    const size_t ms = (size_t)std::max<int64_t>(n_splats, 1), np = (size_t)std::max<int64_t>(n_pairs, 1);
+    size_t sizes[] = {sizeof(int64_t) * n_tiles_plus1, sizeof(int32_t) * np, 16 * ms, 24 * ms, 8 * ms, 24 * ms,
+                      8 * ms, 24 * npix, 8 * npix, 8 * npix, 8 * npix};
+    size_t total = 0;
+    for (size_t s : sizes) total += (s + 255) & ~(size_t)255;
+    char *base = nullptr;
+    SN_CUDA(cudaMalloc(&base, total));
+    void *d[11];
+    size_t o = 0;
+    for (int i = 0; i < 11; ++i) {
+        d[i] = base + o;
+        o += (sizes[i] + 255) & ~(size_t)255;
+    }
+    const void *src[] = {tile_starts, pair_splat, means2d, conics, depths, colors, alphas, color_acc, alpha_acc,
+                         trans, depth_acc};
+    int rc = SN_OK;
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < 11 && e == cudaSuccess; ++i)
+        if (i != 1 || n_pairs > 0) e = cudaMemcpy(d[i], src[i], i < 7 && i >= 2 ? sizes[i] / ms * n_splats : sizes[i],
+                                                  cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = launch_blend_tile_range(t_begin, t_end, tiles_x, tile_size, width, height, (const int64_t *)d[0],
+                                    (const int32_t *)d[1], (const double *)d[2], (const double *)d[3],
+                                    (const double *)d[4], (const double *)d[5], (const double *)d[6], (double *)d[7],
+                                    (double *)d[8], (double *)d[9], (double *)d[10], 0);
+    if (e == cudaSuccess) e = cudaMemcpy(color_acc, d[7], sizes[7], cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(alpha_acc, d[8], sizes[8], cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(trans, d[9], sizes[9], cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(depth_acc, d[10], sizes[10], cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = fail(SN_ERR_CUDA, std::string("sn_blend_tile_range: ") + cudaGetErrorString(e));
+    cudaFree(base);
+    return rc;
+}
+
+int sn_composite(int64_t npix, const double *front_color, const double *front_alpha, const double *front_depth,
+                 const double *back_color, const double *back_alpha, const double *back_depth, double *out_color,
+                 double *out_alpha, double *out_depth, void *stream) {
+    SN_CHECK(npix >= 0, "negative pixel count");
+    SN_CUDA(launch_composite64(npix, front_color, front_alpha, front_depth, back_color, back_alpha, back_depth,
+                               out_color, out_alpha, out_depth, static_cast<cudaStream_t>(stream)));
+    return SN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,146 @@
+// sn_bin.cu -- K3-K6: depth sort, permute into depth order, tile-pair duplication, pair sort,
+// tile-range extraction.
+//
+// Order contract (renderer.py:80-101 + projection.py:184): within each (env, tile) the splats
+// appear in (z, original index) order. The emit stage writes records env-major in index order;
+// a stable radix sort on the 64-bit key (env | z_bits - z_base) therefore yields the exact
+// lexsort order. Pairs are then emitted in (env, depth-rank) order and a stable sort on the
+// (env | tile) key alone (17 bits at 64 envs x 1,200 tiles) keeps depth order inside each tile,
+// which is the semantics of a 64-bit (env | tile | depth) key without sorting the depth bits
+// twice.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "sn_common.cuh"
+#include "sn_internal.h"
+
+namespace sn {
+
+namespace {
+
+__global__ void __launch_bounds__(kBlock) permute_kernel(BinArgs b) {
+    int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (i >= b.n_vis) return;
+    uint32_t slot = b.vals_sorted[i];
+    const uint4 *src = reinterpret_cast<const uint4 *>(b.recs_in + slot);
+    uint4 *dst = reinterpret_cast<uint4 *>(b.recs_out + i);
+    uint4 v0 = __ldg(src), v1 = __ldg(src + 1), v2 = __ldg(src + 2), v3 = __ldg(src + 3);
+    dst[0] = v0;
+    dst[1] = v1;
+    dst[2] = v2;
+    dst[3] = v3;
+    b.gid_out[i] = __ldg(b.gid_in + slot);
+    ushort4 r = b.rects_in[slot];
+    b.rects_out[i] = r;
+    b.tiles_touched[i] = (uint32_t)(r.y - r.x + 1) * (uint32_t)(r.w - r.z + 1);
+}
+
+// Load-balanced pair emission: a CTA owns 256 consecutive depth-sorted splats and spreads
+// their (tile) pairs evenly over its threads, so a splat covering all 1,200 tiles does not
+// serialize one thread. Writes are contiguous.
+__global__ void __launch_bounds__(kBlock) duplicate_kernel(BinArgs b) {
+    __shared__ uint64_t s_off[kBlock + 1];
+    __shared__ ushort4 s_rect[kBlock];
+    __shared__ uint32_t s_env[kBlock];
+    int64_t i0 = (int64_t)blockIdx.x * kBlock;
+    int t = threadIdx.x;
+    int64_t i = i0 + t;
+    int cnt = (int)min((int64_t)kBlock, b.n_vis - i0);
+    if (t < cnt) {
+        s_off[t] = b.pair_off[i];
+        s_rect[t] = b.rects_out[i];
+        s_env[t] = (uint32_t)(b.keys_sorted[i] >> b.z_bits);
+    }
+    if (t == 0) s_off[cnt] = b.pair_off[i0 + cnt];
+    __syncthreads();
+    uint64_t base = s_off[0];
+    uint64_t total = s_off[cnt] - base;
+    for (uint64_t k = t; k < total; k += kBlock) {
+        uint64_t gk = base + k;
+        int lo = 0, hi = cnt - 1;  // last splat with s_off <= gk
+        while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (s_off[mid] <= gk)
+                lo = mid;
+            else
+                hi = mid - 1;
+        }
+        ushort4 r = s_rect[lo];
+        uint32_t local = (uint32_t)(gk - s_off[lo]);
+        uint32_t span = (uint32_t)(r.y - r.x + 1);
+        uint32_t tx = r.x + local % span, ty = r.z + local / span;
+        uint32_t tile = ty * (uint32_t)b.tiles_x + tx;
+        b.pair_keys[gk] = (s_env[lo] << b.tile_bits) | tile;
+        b.pair_vals[gk] = (uint32_t)(i0 + lo);
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) ranges_kernel(const uint32_t *keys, int64_t n, uint2 *ranges) {
+    int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n) return;
+    uint32_t k = keys[i];
+    if (i == 0 || keys[i - 1] != k) ranges[k].x = (uint32_t)i;
+    if (i == n - 1 || keys[i + 1] != k) ranges[k].y = (uint32_t)(i + 1);
+}
+
+}  // namespace
+
+cudaError_t launch_permute(const BinArgs &b, cudaStream_t s) {
+    if (b.n_vis == 0) return cudaSuccess;
+    permute_kernel<<<(unsigned)((b.n_vis + kBlock - 1) / kBlock), kBlock, 0, s>>>(b);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_duplicate(const BinArgs &b, cudaStream_t s) {
+    if (b.n_vis == 0) return cudaSuccess;
+    duplicate_kernel<<<(unsigned)((b.n_vis + kBlock - 1) / kBlock), kBlock, 0, s>>>(b);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ranges(const uint32_t *keys_sorted, int64_t n_pairs, uint2 *ranges, cudaStream_t s) {
+    if (n_pairs == 0) return cudaSuccess;
+    ranges_kernel<<<(unsigned)((n_pairs + kBlock - 1) / kBlock), kBlock, 0, s>>>(keys_sorted, n_pairs, ranges);
+    return cudaGetLastError();
+}
+
+size_t sort_u64_temp_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const unsigned long long *)nullptr,
+                                    (unsigned long long *)nullptr, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                    (int64_t)n, 0, 64);
+    return bytes;
+}
+
+cudaError_t sort_u64_pairs(void *temp, size_t temp_bytes, const unsigned long long *k_in, unsigned long long *k_out,
+                           const uint32_t *v_in, uint32_t *v_out, int64_t n, int bits, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k_in, k_out, v_in, v_out, n, 0, bits, s);
+}
+
+size_t sort_u32_temp_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                    (const uint32_t *)nullptr, (uint32_t *)nullptr, (int64_t)n, 0, 32);
+    return bytes;
+}
+
+cudaError_t sort_u32_pairs(void *temp, size_t temp_bytes, const uint32_t *k_in, uint32_t *k_out, const uint32_t *v_in,
+                           uint32_t *v_out, int64_t n, int bits, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k_in, k_out, v_in, v_out, n, 0, bits, s);
+}
+
+size_t scan_temp_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveScan(nullptr, bytes, (const uint32_t *)nullptr, (uint64_t *)nullptr, cub::Sum(),
+                                   (uint64_t)0, (int64_t)n);
+    return bytes;
+}
+
+cudaError_t scan_tiles(void *temp, size_t temp_bytes, const uint32_t *tiles_touched, uint64_t *pair_off, int64_t n,
+                       cudaStream_t s) {
+    // pair_off has n + 1 entries: scan n + 1 inputs where the last reads a zero pad
+    return cub::DeviceScan::ExclusiveScan(temp, temp_bytes, tiles_touched, pair_off, cub::Sum(), (uint64_t)0, n, s);
+}
+
+}  // namespace sn

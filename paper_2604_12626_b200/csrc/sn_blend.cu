@@ -1,0 +1,219 @@
+// sn_blend.cu -- K7/K8: per-tile front-to-back compositing with fused finalize / composite.
+//
+// One 256-thread CTA per (tile, env); thread = pixel. The tile's depth-ordered splat list is
+// walked in batches of 256: each thread gathers one 64-byte record into shared memory, then all
+// pixels evaluate the batch from shared memory (broadcast reads, no bank conflicts). A CTA-wide
+// vote (__syncthreads_count) stops the walk once every pixel's transmittance fell below 1e-4.
+//
+// Per-pixel semantics are _kernels_cy.pyx:64-86 in float64 for the decision chain (d2 test,
+// alpha, transmittance) so contributor counts equal the reference's; colour accumulates in fp32.
+// The epilogue is _finalize (renderer.py:67-77) and, for the avatar layer, composite
+// (renderer.py:151-166) against the scene frame already in the output buffers.
+#include "sn_common.cuh"
+#include "sn_internal.h"
+
+namespace sn {
+
+namespace {
+
+template <int MODE>
+__global__ void __launch_bounds__(kBlock) blend_kernel(BlendArgs b) {
+    __shared__ SplatRec s_rec[kBlock];
+    const int tile = blockIdx.x, el = blockIdx.y, env = b.e0 + el;
+    const int tx = tile % b.tiles_x, ty = tile / b.tiles_x;
+    const int px_i = tx * kTile + (threadIdx.x & (kTile - 1));
+    const int py_i = ty * kTile + (threadIdx.x / kTile);
+    const bool inside = px_i < b.width && py_i < b.height;
+    const double px = px_i + 0.5, py = py_i + 0.5;
+
+    uint32_t s0, s1;
+    if (b.brute) {
+        s0 = (uint32_t)b.env_off[el];
+        s1 = (uint32_t)b.env_off[el + 1];
+    } else {
+        uint2 r = b.ranges[((uint32_t)el << b.tile_bits) | (uint32_t)tile];
+        s0 = r.x;
+        s1 = r.y;
+    }
+
+    double T = 1.0, A = 0.0, D = 0.0;
+    float cr = 0.0f, cg = 0.0f, cb = 0.0f;
+    int nc = 0;
+    bool done = !inside;
+    uint32_t loaded = 0;
+    for (uint32_t base = s0; base < s1; base += kBlock) {
+        if (__syncthreads_count(!done) == 0) break;  // also guards s_rec reuse
+        loaded += min((uint32_t)kBlock, s1 - base);
+        uint32_t idx = base + threadIdx.x;
+        if (idx < s1) {
+            uint32_t rid = b.brute ? idx : __ldg(b.pair_vals + idx);
+            const uint4 *src = reinterpret_cast<const uint4 *>(b.recs + rid);
+            uint4 *dst = reinterpret_cast<uint4 *>(s_rec + threadIdx.x);
+            uint4 v0 = __ldg(src), v1 = __ldg(src + 1), v2 = __ldg(src + 2), v3 = __ldg(src + 3);
+            dst[0] = v0;
+            dst[1] = v1;
+            dst[2] = v2;
+            dst[3] = v3;
+        }
+        __syncthreads();
+        if (!done) {
+            const int cnt = (int)min((uint32_t)kBlock, s1 - base);
+            for (int j = 0; j < cnt; ++j) {
+                if (T < kTCutoff) break;
+                const SplatRec &s = s_rec[j];
+                double dx = s.mx - px, dy = s.my - py;
+                double d2 = (s.ca * dx * dx + s.cb2 * dx * dy) + s.cc * dy * dy;
+                if (d2 > kSupportD2) continue;
+                double a = s.alpha * exp(-0.5 * d2);
+                if (a > kAlphaClip) a = kAlphaClip;
+                double w = a * T;
+                float rgb[3];
+                unpack_rgb21(s.rgb, rgb);
+                float wf = (float)w;
+                cr = __fmaf_rn(rgb[0], wf, cr);
+                cg = __fmaf_rn(rgb[1], wf, cg);
+                cb = __fmaf_rn(rgb[2], wf, cb);
+                A = A + w;
+                D = D + s.z * w;
+                T = T * (1.0 - a);
+                ++nc;
+            }
+            done = T < kTCutoff;
+        }
+    }
+    if (b.loads && threadIdx.x == 0 && loaded) atomicAdd(b.loads, (unsigned long long)loaded);
+    if (!inside) return;
+
+    const sn_camera &cam = b.cams[env];
+    const int64_t pix = ((int64_t)env * b.height + py_i) * b.width + px_i;
+    if (b.contrib) b.contrib[pix] = nc;
+    const double alpha = A < 1.0 ? A : 1.0;
+    const double depth = A > 0.0 ? D / A : cam.far_;
+    float *oc = b.color + 3 * pix;
+    if (MODE == 0) {
+        oc[0] = (float)np_clip((double)cr + cam.background[0] * T, 0.0, 1.0);
+        oc[1] = (float)np_clip((double)cg + cam.background[1] * T, 0.0, 1.0);
+        oc[2] = (float)np_clip((double)cb + cam.background[2] * T, 0.0, 1.0);
+        b.alpha[pix] = (float)alpha;
+        b.depth[pix] = (float)depth;
+        if (b.depth64) b.depth64[pix] = depth;
+        return;
+    }
+    double fc0 = 0.0, fc1 = 0.0, fc2 = 0.0;
+    if (A > 0.0) {
+        fc0 = np_clip((double)cr / A, 0.0, 1.0);
+        fc1 = np_clip((double)cg / A, 0.0, 1.0);
+        fc2 = np_clip((double)cb / A, 0.0, 1.0);
+    }
+    if (MODE == 1) {
+        oc[0] = (float)fc0;
+        oc[1] = (float)fc1;
+        oc[2] = (float)fc2;
+        b.alpha[pix] = (float)alpha;
+        b.depth[pix] = (float)depth;
+        return;
+    }
+    // MODE 2: composite(front = this layer, back = scene frame in the outputs)
+    const double bd = b.depth64 ? b.depth64[pix] : (double)b.depth[pix];
+    if (depth < bd) {
+        const double ba = b.alpha[pix];
+        oc[0] = (float)(fc0 * alpha + (double)oc[0] * (1.0 - alpha));
+        oc[1] = (float)(fc1 * alpha + (double)oc[1] * (1.0 - alpha));
+        oc[2] = (float)(fc2 * alpha + (double)oc[2] * (1.0 - alpha));
+        b.alpha[pix] = (float)(alpha + ba * (1.0 - alpha));
+        if (alpha >= 0.5) b.depth[pix] = (float)depth;
+    }
+}
+
+__global__ void composite64_kernel(int64_t npix, const double *fc, const double *fa, const double *fd,
+                                   const double *bc, const double *ba, const double *bd, double *oc, double *oa,
+                                   double *od) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= npix) return;
+    bool use_front = fd[i] < bd[i];
+    double a = fa[i];
+    for (int c = 0; c < 3; ++c) {
+        double blended = fc[3 * i + c] * a + bc[3 * i + c] * (1.0 - a);
+        oc[3 * i + c] = use_front ? blended : bc[3 * i + c];
+    }
+    od[i] = (use_front && a >= 0.5) ? fd[i] : bd[i];
+    oa[i] = use_front ? a + ba[i] * (1.0 - a) : ba[i];
+}
+
+// blend_tile_range with the reference's float64 buffers (_kernels_cy.pyx:21-86), exact.
+__global__ void blend_tile_range_kernel(int t_begin, int tiles_x, int tile_size, int width, int height,
+                                        const int64_t *tile_starts, const int32_t *pair_splat, const double *means2d,
+                                        const double *conics, const double *depths, const double *colors,
+                                        const double *alphas, double *color_acc, double *alpha_acc, double *trans,
+                                        double *depth_acc) {
+    int t = t_begin + blockIdx.x;
+    int64_t s0 = tile_starts[t], s1 = tile_starts[t + 1];
+    if (s0 == s1) return;
+    int x0 = (t % tiles_x) * tile_size, y0 = (t / tiles_x) * tile_size;
+    int tw = min(tile_size, width - x0), th = min(tile_size, height - y0);
+    if (tw <= 0 || th <= 0) return;
+    for (int k = threadIdx.x; k < tw * th; k += blockDim.x) {
+        int py_i = y0 + k / tw, px_i = x0 + k % tw;
+        double px = px_i + 0.5, py = py_i + 0.5;
+        int64_t p = (int64_t)py_i * width + px_i;
+        double c0 = color_acc[3 * p], c1 = color_acc[3 * p + 1], c2 = color_acc[3 * p + 2];
+        double A = alpha_acc[p], D = depth_acc[p], T = 1.0;
+        for (int64_t s = s0; s < s1; ++s) {
+            if (T < kTCutoff) break;
+            int sid = pair_splat[s];
+            double dx = means2d[2 * sid] - px, dy = means2d[2 * sid + 1] - py;
+            double ca = conics[3 * sid], cbv = conics[3 * sid + 1], cc = conics[3 * sid + 2];
+            double d2 = ca * dx * dx + 2.0 * cbv * dx * dy + cc * dy * dy;
+            if (d2 > kSupportD2) continue;
+            double a = alphas[sid] * exp(-0.5 * d2);
+            if (a > kAlphaClip) a = kAlphaClip;
+            double w = a * T;
+            c0 = c0 + colors[3 * sid] * w;
+            c1 = c1 + colors[3 * sid + 1] * w;
+            c2 = c2 + colors[3 * sid + 2] * w;
+            A = A + w;
+            D = D + depths[sid] * w;
+            T = T * (1.0 - a);
+        }
+        color_acc[3 * p] = c0;
+        color_acc[3 * p + 1] = c1;
+        color_acc[3 * p + 2] = c2;
+        alpha_acc[p] = A;
+        depth_acc[p] = D;
+        trans[p] = T;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_blend(const BlendArgs &b, cudaStream_t s) {
+    dim3 grid((unsigned)(tiles_of(b.width) * tiles_of(b.height)), (unsigned)b.ec);
+    if (b.mode == 0)
+        blend_kernel<0><<<grid, kBlock, 0, s>>>(b);
+    else if (b.mode == 1)
+        blend_kernel<1><<<grid, kBlock, 0, s>>>(b);
+    else
+        blend_kernel<2><<<grid, kBlock, 0, s>>>(b);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_composite64(int64_t npix, const double *fc, const double *fa, const double *fd, const double *bc,
+                               const double *ba, const double *bd, double *oc, double *oa, double *od, cudaStream_t s) {
+    if (npix == 0) return cudaSuccess;
+    composite64_kernel<<<(unsigned)((npix + 255) / 256), 256, 0, s>>>(npix, fc, fa, fd, bc, ba, bd, oc, oa, od);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_blend_tile_range(int t_begin, int t_end, int tiles_x, int tile_size, int width, int height,
+                                    const int64_t *tile_starts, const int32_t *pair_splat, const double *means2d,
+                                    const double *conics, const double *depths, const double *colors,
+                                    const double *alphas, double *color_acc, double *alpha_acc, double *trans,
+                                    double *depth_acc, cudaStream_t s) {
+    if (t_end <= t_begin) return cudaSuccess;
+    blend_tile_range_kernel<<<t_end - t_begin, 256, 0, s>>>(t_begin, tiles_x, tile_size, width, height, tile_starts,
+                                                            pair_splat, means2d, conics, depths, colors, alphas,
+                                                            color_acc, alpha_acc, trans, depth_acc);
+    return cudaGetLastError();
+}
+
+}  // namespace sn

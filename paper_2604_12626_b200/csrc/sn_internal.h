@@ -1,0 +1,118 @@
+// sn_internal.h -- host-side declarations shared by the .cu translation units (not exported).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/splatnav_b200.h"
+
+namespace sn {
+
+struct SplatRec;
+
+// Per-(env, avatar) pose block produced by the pose kernel and read by the skinning code:
+// joint_mats (J x 12, rows of the 3x4 M_j = rigid(T_j) B_j^-1), eff_q (J x 4 effective joint
+// quats q_root * q(M_j)), root (12: root rotation 3x3 row-major, root translation).
+struct PoseView {
+    const double *joint_mats;
+    const double *eff_q;
+    const double *root;
+    int32_t n_joints;
+    int32_t n_avatars;
+};
+
+// Launch parameters for one preprocess pass over an env chunk [e0, e0 + ec).
+struct PrepArgs {
+    const sn_camera *cams;  // device, indexed by global env id
+    int32_t e0, ec;
+    int32_t n_blocks;
+    uint64_t *vismask;      // (n) bit e set: gaussian visible in env e0 + e
+    uint32_t *blk_counts;   // (ec, n_blocks) -> exclusive offsets after scan
+    unsigned long long *stats;  // (E, 5) device, may be null
+    const uint8_t *avatar_active;  // (E, A), avatars only, may be null
+    // emit outputs (unsorted, env-major, index order within env)
+    const uint64_t *env_off;  // (ec + 1)
+    unsigned long long *keys;  // depth keys
+    uint32_t *vals;            // identity positions
+    SplatRec *recs;
+    uint32_t *gid;
+    ushort4 *rects;
+    int32_t tiles_x, tiles_y;
+    uint64_t z_base;
+    int32_t z_bits;
+};
+
+// sn_preprocess.cu
+cudaError_t launch_scene_count(const sn_cloud &c, const PrepArgs &a, cudaStream_t s);
+cudaError_t launch_scene_emit(const sn_cloud &c, const PrepArgs &a, cudaStream_t s);
+cudaError_t launch_avatar_count(const sn_avatars &av, const PoseView &pv, const PrepArgs &a, cudaStream_t s);
+cudaError_t launch_avatar_emit(const sn_avatars &av, const PoseView &pv, const PrepArgs &a, cudaStream_t s);
+cudaError_t launch_block_scan(uint32_t *blk_counts, int32_t n_blocks, int32_t ec, uint64_t *env_off,
+                              cudaStream_t s);
+cudaError_t launch_skin_range(const sn_avatars &av, int64_t g0, int64_t n, const PoseView &pv, double *out_pos,
+                              double *out_rot, cudaStream_t s);
+
+// sn_rig.cu
+cudaError_t launch_pose(const sn_avatars &av, const double *sim_times, int32_t n_envs, double *pose_q, double *pose_t,
+                        double *joint_mats, double *eff_q, double *root, int32_t *err_flag, cudaStream_t s);
+cudaError_t launch_joint_prep(const sn_avatars &av, int32_t avatar, const double *pose_q, const double *pose_t,
+                              double *joint_mats, double *eff_q, double *root, cudaStream_t s);
+
+// sn_bin.cu
+struct BinArgs {
+    int32_t ec, tiles_x, tiles_y, tile_bits, z_bits;
+    int64_t n_vis;
+    const unsigned long long *keys_sorted;
+    const uint32_t *vals_sorted;
+    const SplatRec *recs_in;
+    const uint32_t *gid_in;
+    const ushort4 *rects_in;
+    const uint64_t *env_off;
+    SplatRec *recs_out;
+    uint32_t *gid_out;
+    ushort4 *rects_out;
+    uint32_t *tiles_touched;
+    uint64_t *pair_off;      // (n_vis + 1)
+    uint32_t *pair_keys;
+    uint32_t *pair_vals;
+    uint2 *ranges;           // (ec << tile_bits)
+};
+cudaError_t launch_permute(const BinArgs &b, cudaStream_t s);
+cudaError_t launch_duplicate(const BinArgs &b, cudaStream_t s);
+cudaError_t launch_ranges(const uint32_t *keys_sorted, int64_t n_pairs, uint2 *ranges, cudaStream_t s);
+size_t sort_u64_temp_bytes(int64_t n);
+cudaError_t sort_u64_pairs(void *temp, size_t temp_bytes, const unsigned long long *k_in, unsigned long long *k_out,
+                           const uint32_t *v_in, uint32_t *v_out, int64_t n, int bits, cudaStream_t s);
+size_t sort_u32_temp_bytes(int64_t n);
+cudaError_t sort_u32_pairs(void *temp, size_t temp_bytes, const uint32_t *k_in, uint32_t *k_out, const uint32_t *v_in,
+                           uint32_t *v_out, int64_t n, int bits, cudaStream_t s);
+size_t scan_temp_bytes(int64_t n);
+cudaError_t scan_tiles(void *temp, size_t temp_bytes, const uint32_t *tiles_touched, uint64_t *pair_off, int64_t n,
+                       cudaStream_t s);
+
+// sn_blend.cu
+struct BlendArgs {
+    const sn_camera *cams;
+    int32_t e0, ec, width, height, tiles_x, tile_bits;
+    int32_t brute;          // rasterize_reference: every tile walks the env's whole depth order
+    int32_t mode;           // 0 scene (background), 1 layer only, 2 layer composited over outputs
+    const uint2 *ranges;
+    const uint32_t *pair_vals;
+    const uint64_t *env_off;
+    const SplatRec *recs;
+    float *color, *alpha, *depth;  // (E,H,W,[3]) outputs, indexed by global env
+    double *depth64;        // scene pass: exact depth for the compositor (may be null)
+    int32_t *contrib;       // (E,H,W) may be null
+    unsigned long long *loads;  // device counter: records gathered into shared memory (may be null)
+};
+cudaError_t launch_blend(const BlendArgs &b, cudaStream_t s);
+cudaError_t launch_composite64(int64_t npix, const double *fc, const double *fa, const double *fd, const double *bc,
+                               const double *ba, const double *bd, double *oc, double *oa, double *od, cudaStream_t s);
+cudaError_t launch_blend_tile_range(int t_begin, int t_end, int tiles_x, int tile_size, int width, int height,
+                                    const int64_t *tile_starts, const int32_t *pair_splat, const double *means2d,
+                                    const double *conics, const double *depths, const double *colors,
+                                    const double *alphas, double *color_acc, double *alpha_acc, double *trans,
+                                    double *depth_acc, cudaStream_t s);
+
+}  // namespace sn

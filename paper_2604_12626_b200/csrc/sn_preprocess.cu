@@ -1,0 +1,450 @@
+// sn_preprocess.cu -- K1/K2: (skinning +) projection, culling, SH colour and stream compaction.
+//
+// One thread per gaussian, looping over the env chunk's cameras, so a scene gaussian's
+// parameters and its 3D covariance are read/built once per chunk instead of once per env.
+// Two launches per pass:
+//   count: visibility bitmask per gaussian + per-(env, block) visible counts + RenderStats
+//          (warp ballots, aggregated in shared memory, one global atomic per block and field);
+//   emit:  recomputes geometry only for visible (gaussian, env) pairs and writes 64-byte splat
+//          records at order-preserving positions (env-major, gaussian index order within env),
+//          so a stable depth sort reproduces np.lexsort((idx, z)) (projection.py:184).
+// Avatars (sn_avatars) run the same pipeline with LBS skinning fused in front of the
+// projection (rig.py:107-146): skinned positions/rotations never touch HBM.
+#include <cub/block/block_scan.cuh>
+
+#include "sn_common.cuh"
+#include "sn_internal.h"
+
+namespace sn {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+template <typename T>
+__device__ __forceinline__ void load4(const T *p, double o[4]);
+template <>
+__device__ __forceinline__ void load4<float>(const float *p, double o[4]) {
+    float4 v = __ldg(reinterpret_cast<const float4 *>(p));
+    o[0] = v.x;
+    o[1] = v.y;
+    o[2] = v.z;
+    o[3] = v.w;
+}
+template <>
+__device__ __forceinline__ void load4<double>(const double *p, double o[4]) {
+    double2 a = __ldg(reinterpret_cast<const double2 *>(p));
+    double2 b = __ldg(reinterpret_cast<const double2 *>(p) + 1);
+    o[0] = a.x;
+    o[1] = a.y;
+    o[2] = b.x;
+    o[3] = b.y;
+}
+
+__device__ __forceinline__ double cam_z(const double p[3], const sn_camera &c) {
+    return dot3_fma(p[0], p[1], p[2], c.rot[6], c.rot[7], c.rot[8]) + c.trans[2];
+}
+
+// Warp-aggregated stats: one shared atomic per warp and field.
+__device__ __forceinline__ void tally(unsigned (*s_cnt)[5], int e, int code, bool input) {
+    int lane = threadIdx.x & 31;
+    unsigned b_in = __ballot_sync(kFull, input);
+    unsigned b_keep = __ballot_sync(kFull, code == kKeep);
+    unsigned b_depth = __ballot_sync(kFull, code == kCullDepth);
+    unsigned b_deg = __ballot_sync(kFull, code == kDegenerate);
+    unsigned b_frame = __ballot_sync(kFull, code == kCullFrame);
+    if (lane == 0) {
+        if (b_in) atomicAdd(&s_cnt[e][0], __popc(b_in));
+        if (b_depth) atomicAdd(&s_cnt[e][1], __popc(b_depth));
+        if (b_frame) atomicAdd(&s_cnt[e][2], __popc(b_frame));
+        if (b_deg) atomicAdd(&s_cnt[e][3], __popc(b_deg));
+        if (b_keep) atomicAdd(&s_cnt[e][4], __popc(b_keep));
+    }
+}
+
+__device__ __forceinline__ void flush_counts(unsigned (*s_cnt)[5], const PrepArgs &a) {
+    __syncthreads();
+    int t = threadIdx.x;
+    if (t < a.ec) a.blk_counts[(int64_t)t * a.n_blocks + blockIdx.x] = s_cnt[t][4];
+    if (a.stats != nullptr && t < a.ec * 5) {
+        int e = t / 5, f = t % 5;  // sn_stats field order: input, depth, frame, degenerate, drawn
+        unsigned v = s_cnt[e][f];
+        if (v) atomicAdd(a.stats + (int64_t)(a.e0 + e) * 5 + f, (unsigned long long)v);
+    }
+}
+
+__device__ __forceinline__ void init_counts(unsigned (*s_cnt)[5], int ec) {
+    for (int i = threadIdx.x; i < ec * 5; i += blockDim.x) s_cnt[i / 5][i % 5] = 0;
+    __syncthreads();
+}
+
+// Per-warp exclusive offsets for each env of the chunk; returns via s_woff.
+__device__ __forceinline__ void warp_offsets(uint64_t mask, int ec, unsigned (*s_woff)[kBlock / 32]) {
+    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int e = 0; e < ec; ++e) {
+        unsigned b = __ballot_sync(kFull, (mask >> e) & 1ull);
+        if (lane == 0) s_woff[e][warp] = __popc(b);
+    }
+    __syncthreads();
+    if (threadIdx.x < ec) {
+        unsigned run = 0;
+        for (int w = 0; w < kBlock / 32; ++w) {
+            unsigned c = s_woff[threadIdx.x][w];
+            s_woff[threadIdx.x][w] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void write_splat(const PrepArgs &a, int64_t pos, int e, const Geo &geo, double alpha,
+                                            const float rgb[3], uint32_t gid) {
+    SplatRec r;
+    r.mx = geo.mx;
+    r.my = geo.my;
+    r.ca = geo.ca;
+    r.cb2 = 2.0 * geo.cb;  // exact; _kernels_cy.pyx:73 evaluates (2.0 * cb) first
+    r.cc = geo.cc;
+    r.alpha = alpha;
+    r.z = geo.z;
+    r.rgb = pack_rgb21(rgb);
+    a.recs[pos] = r;
+    unsigned long long zb = (unsigned long long)__double_as_longlong(geo.z);
+    a.keys[pos] = ((unsigned long long)e << a.z_bits) | (zb - a.z_base);
+    a.vals[pos] = (uint32_t)pos;
+    a.gid[pos] = gid;
+    int rect[4];
+    tile_rect(geo.mx, geo.my, geo.radius, a.tiles_x, a.tiles_y, rect);
+    a.rects[pos] = make_ushort4((unsigned short)rect[0], (unsigned short)rect[1], (unsigned short)rect[2],
+                                (unsigned short)rect[3]);
+}
+
+// ------------------------------------------------------------------------------- scene
+
+template <typename T>
+__device__ __forceinline__ void load_scene(const sn_cloud &c, int64_t g, double p[3], double ls[3], double q[4],
+                                           double &opacity) {
+    double v[4];
+    load4<T>(static_cast<const T *>(c.pos_opacity) + 4 * g, v);
+    p[0] = v[0];
+    p[1] = v[1];
+    p[2] = v[2];
+    opacity = v[3];
+    load4<T>(static_cast<const T *>(c.log_scales) + 4 * g, v);
+    ls[0] = v[0];
+    ls[1] = v[1];
+    ls[2] = v[2];
+    load4<T>(static_cast<const T *>(c.rotations) + 4 * g, q);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) scene_count_kernel(sn_cloud c, PrepArgs a) {
+    __shared__ unsigned s_cnt[kMaxEnvChunk][5];
+    init_counts(s_cnt, a.ec);
+    int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    bool valid = g < c.n;
+    double p[3], ls[3], q[4], opacity, cov[6];
+    bool have_cov = false;
+    if (valid) load_scene<T>(c, g, p, ls, q, opacity);
+    uint64_t mask = 0;
+    for (int e = 0; e < a.ec; ++e) {
+        int code = -1;
+        if (valid) {
+            const sn_camera &cam = a.cams[a.e0 + e];
+            double z = cam_z(p, cam);
+            if (!((z > cam.near_) && (z < cam.far_))) {
+                code = kCullDepth;
+            } else {
+                if (!have_cov) {
+                    build_cov3d(ls, q, cov);
+                    have_cov = true;
+                }
+                Geo geo;
+                code = project_geo(p, cov, cam, geo);
+            }
+            if (code == kKeep) mask |= 1ull << e;
+        }
+        tally(s_cnt, e, code, valid);
+    }
+    if (valid) a.vismask[g] = mask;
+    flush_counts(s_cnt, a);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) scene_emit_kernel(sn_cloud c, PrepArgs a) {
+    __shared__ unsigned s_woff[kMaxEnvChunk][kBlock / 32];
+    int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    bool valid = g < c.n;
+    uint64_t mask = valid ? a.vismask[g] : 0ull;
+    warp_offsets(mask, a.ec, s_woff);
+    if (!__any_sync(kFull, mask != 0)) return;
+    double p[3], ls[3], q[4], opacity, cov[6], alpha = 0.0;
+    if (mask) {
+        load_scene<T>(c, g, p, ls, q, opacity);
+        build_cov3d(ls, q, cov);
+        alpha = sigmoid(opacity);
+    }
+    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned lt = (1u << lane) - 1u;
+    for (int e = 0; e < a.ec; ++e) {
+        bool vis = (mask >> e) & 1ull;
+        unsigned b = __ballot_sync(kFull, vis);
+        if (!vis) continue;
+        int64_t pos = (int64_t)a.env_off[e] + a.blk_counts[(int64_t)e * a.n_blocks + blockIdx.x] + s_woff[e][warp] +
+                      __popc(b & lt);
+        const sn_camera &cam = a.cams[a.e0 + e];
+        Geo geo;
+        project_geo(p, cov, cam, geo);
+        float d[3], rgb[3];
+        view_dir(p, cam, d);
+        eval_sh_f32(c.sh, c.n, g, c.sh_k, d[0], d[1], d[2], rgb);
+        write_splat(a, pos, e, geo, alpha, rgb, (uint32_t)g);
+    }
+}
+
+// ------------------------------------------------------------------------------- avatars
+
+// lbs_deform (rig.py:107-146) for one gaussian under one (env, avatar) pose. Sparse influences
+// in ascending joint order reproduce the dense N x J sums exactly: zero weights add +-0.
+__device__ __forceinline__ void skin_one(const sn_avatars &av, int64_t g, const double *jm, const double *eq,
+                                         const double *root, double p_out[3], double q_out[4]) {
+    double P[4], W[4], Q[4];
+    load4<double>(av.pos_opacity + 4 * g, P);
+    load4<double>(av.weights + 4 * g, W);
+    load4<double>(av.rotations + 4 * g, Q);
+    uint32_t J4 = __ldg(av.joints + g);
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+    int dom = -1;
+    double wmax = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        double w = W[k];
+        if (w == 0.0) continue;
+        int j = (J4 >> (8 * k)) & 0xff;
+        const double *M = jm + 12 * j;
+        // einsum("jab,nb->jna") as numpy evaluates it: (r0 p0 + r2 p2) + r1 p1, then + offset
+        double t0 = ((__ldg(M + 0) * P[0] + __ldg(M + 2) * P[2]) + __ldg(M + 1) * P[1]) + __ldg(M + 3);
+        double t1 = ((__ldg(M + 4) * P[0] + __ldg(M + 6) * P[2]) + __ldg(M + 5) * P[1]) + __ldg(M + 7);
+        double t2 = ((__ldg(M + 8) * P[0] + __ldg(M + 10) * P[2]) + __ldg(M + 9) * P[1]) + __ldg(M + 11);
+        acc0 = acc0 + w * (t0 - P[0]);
+        acc1 = acc1 + w * (t1 - P[1]);
+        acc2 = acc2 + w * (t2 - P[2]);
+        if (dom < 0 || w > wmax) {
+            wmax = w;
+            dom = j;
+        }
+    }
+    if (dom < 0) dom = 0;  // all-zero row: np.argmax picks joint 0
+    double b0 = P[0] + acc0, b1 = P[1] + acc1, b2 = P[2] + acc2;
+    p_out[0] = dot3_fma(b0, b1, b2, __ldg(root + 0), __ldg(root + 1), __ldg(root + 2)) + __ldg(root + 9);
+    p_out[1] = dot3_fma(b0, b1, b2, __ldg(root + 3), __ldg(root + 4), __ldg(root + 5)) + __ldg(root + 10);
+    p_out[2] = dot3_fma(b0, b1, b2, __ldg(root + 6), __ldg(root + 7), __ldg(root + 8)) + __ldg(root + 11);
+
+    double qd[4];
+    load4<double>(eq + 4 * dom, qd);
+    double bq[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        double w = W[k];
+        if (w == 0.0) continue;
+        int j = (J4 >> (8 * k)) & 0xff;
+        double qj[4];
+        load4<double>(eq + 4 * j, qj);
+        double dot = fma(qj[3], qd[3], fma(qj[2], qd[2], fma(qj[1], qd[1], qj[0] * qd[0])));
+        double ws = w * (dot < 0.0 ? -1.0 : 1.0);
+        bq[0] = fma(ws, qj[0], bq[0]);
+        bq[1] = fma(ws, qj[1], bq[1]);
+        bq[2] = fma(ws, qj[2], bq[2]);
+        bq[3] = fma(ws, qj[3], bq[3]);
+    }
+    if (norm4(bq[0], bq[1], bq[2], bq[3]) < 1e-12) {
+        bq[0] = qd[0];
+        bq[1] = qd[1];
+        bq[2] = qd[2];
+        bq[3] = qd[3];
+    }
+    double nn = norm4(bq[0], bq[1], bq[2], bq[3]);
+    double qn[4] = {bq[0] / nn, bq[1] / nn, bq[2] / nn, bq[3] / nn};
+    quat_multiply(qn, Q, q_out);
+}
+
+__device__ __forceinline__ void pose_ptrs(const PoseView &pv, int env, int avatar, const double *&jm,
+                                          const double *&eq, const double *&root) {
+    int64_t ea = (int64_t)env * pv.n_avatars + avatar;
+    jm = pv.joint_mats + ea * pv.n_joints * 12;
+    eq = pv.eff_q + ea * pv.n_joints * 4;
+    root = pv.root + ea * 12;
+}
+
+__device__ __forceinline__ bool avatar_on(const PrepArgs &a, int n_avatars, int env, int avatar) {
+    return a.avatar_active == nullptr || a.avatar_active[(int64_t)env * n_avatars + avatar] != 0;
+}
+
+__global__ void __launch_bounds__(kBlock) avatar_count_kernel(sn_avatars av, PoseView pv, PrepArgs a) {
+    __shared__ unsigned s_cnt[kMaxEnvChunk][5];
+    init_counts(s_cnt, a.ec);
+    int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    bool valid = g < av.n;
+    int avatar = valid ? av.avatar_of[g] : 0;
+    double ls[4];
+    if (valid) load4<double>(av.log_scales + 4 * g, ls);
+    uint64_t mask = 0;
+    for (int e = 0; e < a.ec; ++e) {
+        int env = a.e0 + e;
+        bool input = valid && avatar_on(a, av.n_avatars, env, avatar);
+        int code = -1;
+        if (input) {
+            const double *jm, *eq, *root;
+            pose_ptrs(pv, env, avatar, jm, eq, root);
+            double p[3], q[4];
+            skin_one(av, g, jm, eq, root, p, q);
+            const sn_camera &cam = a.cams[env];
+            double z = cam_z(p, cam);
+            if (!((z > cam.near_) && (z < cam.far_))) {
+                code = kCullDepth;
+            } else {
+                double cov[6];
+                build_cov3d(ls, q, cov);
+                Geo geo;
+                code = project_geo(p, cov, cam, geo);
+            }
+            if (code == kKeep) mask |= 1ull << e;
+        }
+        tally(s_cnt, e, code, input);
+    }
+    if (valid) a.vismask[g] = mask;
+    flush_counts(s_cnt, a);
+}
+
+__global__ void __launch_bounds__(kBlock) avatar_emit_kernel(sn_avatars av, PoseView pv, PrepArgs a) {
+    __shared__ unsigned s_woff[kMaxEnvChunk][kBlock / 32];
+    int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    bool valid = g < av.n;
+    uint64_t mask = valid ? a.vismask[g] : 0ull;
+    warp_offsets(mask, a.ec, s_woff);
+    if (!__any_sync(kFull, mask != 0)) return;
+    int avatar = valid ? av.avatar_of[g] : 0;
+    double ls[4], alpha = 0.0;
+    if (mask) {
+        load4<double>(av.log_scales + 4 * g, ls);
+        alpha = sigmoid(__ldg(av.pos_opacity + 4 * g + 3));
+    }
+    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned lt = (1u << lane) - 1u;
+    for (int e = 0; e < a.ec; ++e) {
+        bool vis = (mask >> e) & 1ull;
+        unsigned b = __ballot_sync(kFull, vis);
+        if (!vis) continue;
+        int env = a.e0 + e;
+        int64_t pos = (int64_t)a.env_off[e] + a.blk_counts[(int64_t)e * a.n_blocks + blockIdx.x] + s_woff[e][warp] +
+                      __popc(b & lt);
+        const double *jm, *eq, *root;
+        pose_ptrs(pv, env, avatar, jm, eq, root);
+        double p[3], q[4], cov[6];
+        skin_one(av, g, jm, eq, root, p, q);
+        build_cov3d(ls, q, cov);
+        const sn_camera &cam = a.cams[env];
+        Geo geo;
+        project_geo(p, cov, cam, geo);
+        float d[3], rgb[3];
+        view_dir(p, cam, d);
+        eval_sh_f32(av.sh, av.n, g, av.sh_k, d[0], d[1], d[2], rgb);
+        write_splat(a, pos, e, geo, alpha, rgb, (uint32_t)g);
+    }
+}
+
+// Standalone skinning (lbs_deform API): float64 positions/rotations of one avatar.
+__global__ void __launch_bounds__(kBlock) skin_kernel(sn_avatars av, int64_t g0, int64_t n, PoseView pv,
+                                                      double *out_pos, double *out_rot) {
+    int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n) return;
+    const double *jm, *eq, *root;
+    pose_ptrs(pv, 0, 0, jm, eq, root);
+    double p[3], q[4];
+    skin_one(av, g0 + i, jm, eq, root, p, q);
+    out_pos[3 * i] = p[0];
+    out_pos[3 * i + 1] = p[1];
+    out_pos[3 * i + 2] = p[2];
+    out_rot[4 * i] = q[0];
+    out_rot[4 * i + 1] = q[1];
+    out_rot[4 * i + 2] = q[2];
+    out_rot[4 * i + 3] = q[3];
+}
+
+// Per-env exclusive scan of the per-block visible counts (in place), then env offsets.
+constexpr int kScanThreads = 1024;
+__global__ void __launch_bounds__(kScanThreads) block_scan_kernel(uint32_t *blk_counts, int32_t n_blocks,
+                                                                  uint64_t *env_tot) {
+    using Scan = cub::BlockScan<uint32_t, kScanThreads>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ uint32_t carry;
+    uint32_t *row = blk_counts + (int64_t)blockIdx.x * n_blocks;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < n_blocks; base += kScanThreads) {
+        int i = base + threadIdx.x;
+        uint32_t v = i < n_blocks ? row[i] : 0u, ex, total;
+        Scan(tmp).ExclusiveSum(v, ex, total);
+        uint32_t c = carry;
+        if (i < n_blocks) row[i] = c + ex;
+        __syncthreads();
+        if (threadIdx.x == 0) carry = c + total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) env_tot[blockIdx.x] = carry;
+}
+
+__global__ void env_offsets_kernel(int32_t ec, uint64_t *env_off) {
+    // env_off holds per-env totals in [1..ec]; make it an exclusive prefix with env_off[0] = 0
+    uint64_t run = 0;
+    for (int e = 0; e < ec; ++e) {
+        uint64_t t = env_off[e + 1];
+        env_off[e] = run;
+        run += t;
+    }
+    env_off[ec] = run;
+}
+
+}  // namespace
+
+cudaError_t launch_scene_count(const sn_cloud &c, const PrepArgs &a, cudaStream_t s) {
+    if (c.dtype == SN_FLOAT64)
+        scene_count_kernel<double><<<a.n_blocks, kBlock, 0, s>>>(c, a);
+    else
+        scene_count_kernel<float><<<a.n_blocks, kBlock, 0, s>>>(c, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scene_emit(const sn_cloud &c, const PrepArgs &a, cudaStream_t s) {
+    if (c.dtype == SN_FLOAT64)
+        scene_emit_kernel<double><<<a.n_blocks, kBlock, 0, s>>>(c, a);
+    else
+        scene_emit_kernel<float><<<a.n_blocks, kBlock, 0, s>>>(c, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_avatar_count(const sn_avatars &av, const PoseView &pv, const PrepArgs &a, cudaStream_t s) {
+    avatar_count_kernel<<<a.n_blocks, kBlock, 0, s>>>(av, pv, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_avatar_emit(const sn_avatars &av, const PoseView &pv, const PrepArgs &a, cudaStream_t s) {
+    avatar_emit_kernel<<<a.n_blocks, kBlock, 0, s>>>(av, pv, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_block_scan(uint32_t *blk_counts, int32_t n_blocks, int32_t ec, uint64_t *env_off,
+                              cudaStream_t s) {
+    block_scan_kernel<<<ec, kScanThreads, 0, s>>>(blk_counts, n_blocks, env_off + 1);
+    env_offsets_kernel<<<1, 1, 0, s>>>(ec, env_off);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_skin_range(const sn_avatars &av, int64_t g0, int64_t n, const PoseView &pv, double *out_pos,
+                              double *out_rot, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    skin_kernel<<<(unsigned)((n + kBlock - 1) / kBlock), kBlock, 0, s>>>(av, g0, n, pv, out_pos, out_rot);
+    return cudaGetLastError();
+}
+
+}  // namespace sn

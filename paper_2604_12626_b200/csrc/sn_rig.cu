@@ -1,0 +1,200 @@
+// sn_rig.cu -- per-(env, avatar) pose sampling and joint preparation.
+//
+// AvatarRuntime.clock (tasks.py:299-305) -> sample_pose (rig.py:78-104, nlerp with hemisphere
+// correction, transforms.py:73-81) -> M_j = rigid(q_j, t_j) @ inv_bind_j (rig.py:116) and the
+// effective joint quaternions q_root * matrix_to_quat(M_j) (rig.py:127-128, Shepperd,
+// transforms.py:37-53). One CTA per (env, avatar), one thread per joint (+ root). The output
+// pose block is what the fused skin->project kernels read (a few KB per env and avatar).
+#include "sn_common.cuh"
+#include "sn_internal.h"
+
+namespace sn {
+
+namespace {
+
+__device__ __forceinline__ void matrix_to_quat(const double m[9], double q[4]) {
+    double t = (m[0] + m[4]) + m[8];
+    double s;
+    if (t > 0.0) {
+        s = sqrt(t + 1.0) * 2.0;
+        q[0] = 0.25 * s;
+        q[1] = (m[7] - m[5]) / s;
+        q[2] = (m[2] - m[6]) / s;
+        q[3] = (m[3] - m[1]) / s;
+    } else if (m[0] >= m[4] && m[0] >= m[8]) {
+        s = sqrt(((1.0 + m[0]) - m[4]) - m[8]) * 2.0;
+        q[0] = (m[7] - m[5]) / s;
+        q[1] = 0.25 * s;
+        q[2] = (m[1] + m[3]) / s;
+        q[3] = (m[2] + m[6]) / s;
+    } else if (m[4] >= m[8]) {
+        s = sqrt(((1.0 + m[4]) - m[0]) - m[8]) * 2.0;
+        q[0] = (m[2] - m[6]) / s;
+        q[1] = (m[1] + m[3]) / s;
+        q[2] = 0.25 * s;
+        q[3] = (m[5] + m[7]) / s;
+    } else {
+        s = sqrt(((1.0 + m[8]) - m[0]) - m[4]) * 2.0;
+        q[0] = (m[3] - m[1]) / s;
+        q[1] = (m[2] + m[6]) / s;
+        q[2] = (m[5] + m[7]) / s;
+        q[3] = 0.25 * s;
+    }
+    double n = norm4(q[0], q[1], q[2], q[3]);
+    q[0] /= n;
+    q[1] /= n;
+    q[2] /= n;
+    q[3] /= n;
+}
+
+// rigid(q, t) @ inv_bind (4x4 @ 4x4, FMA chain over k as OpenBLAS), rows 0..2 -> M (12);
+// then the effective quaternion q_root * q(M[:3,:3]).
+__device__ __forceinline__ void joint_prep(const double q[4], const double t[3], const double root_q[4],
+                                           const double *ib, double *jm_out, double *eq_out) {
+    double r[9];
+    quat_to_matrix(q[0], q[1], q[2], q[3], r);
+    double rm[12] = {r[0], r[1], r[2], t[0], r[3], r[4], r[5], t[1], r[6], r[7], r[8], t[2]};
+    double m[12];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+            m[a * 4 + b] = fma(rm[a * 4 + 3], ib[12 + b],
+                               fma(rm[a * 4 + 2], ib[8 + b], fma(rm[a * 4 + 1], ib[4 + b], rm[a * 4 + 0] * ib[b])));
+#pragma unroll
+    for (int i = 0; i < 12; ++i) jm_out[i] = m[i];
+    double m3[9] = {m[0], m[1], m[2], m[4], m[5], m[6], m[8], m[9], m[10]};
+    double mq[4];
+    matrix_to_quat(m3, mq);
+    double e[4];
+    quat_multiply(root_q, mq, e);
+    eq_out[0] = e[0];
+    eq_out[1] = e[1];
+    eq_out[2] = e[2];
+    eq_out[3] = e[3];
+}
+
+__device__ __forceinline__ void root_prep(const double q[4], const double t[3], double *root) {
+    double r[9];
+    quat_to_matrix(q[0], q[1], q[2], q[3], r);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) root[i] = r[i];
+    root[9] = t[0];
+    root[10] = t[1];
+    root[11] = t[2];
+}
+
+// sample_pose for joint j of one trajectory at time t (t >= 0 checked by the caller).
+__device__ __forceinline__ void sample_joint(const double *tq, const double *tt, int n_frames, int jp, double fps,
+                                             double t, int j, double q[4], double tr[3]) {
+    double pos = t * fps;
+    double ff = floor(pos);
+    int last = n_frames - 1;
+    if (ff >= (double)last) {
+        const double *a = tq + ((int64_t)last * jp + j) * 4;
+        const double *b = tt + ((int64_t)last * jp + j) * 3;
+        q[0] = a[0]; q[1] = a[1]; q[2] = a[2]; q[3] = a[3];
+        tr[0] = b[0]; tr[1] = b[1]; tr[2] = b[2];
+        return;
+    }
+    int f = (int)ff;
+    double lam = pos - ff;
+    const double *qa = tq + ((int64_t)f * jp + j) * 4, *qb = tq + ((int64_t)(f + 1) * jp + j) * 4;
+    const double *ta = tt + ((int64_t)f * jp + j) * 3, *tb = tt + ((int64_t)(f + 1) * jp + j) * 3;
+    if (lam == 0.0) {
+        q[0] = qa[0]; q[1] = qa[1]; q[2] = qa[2]; q[3] = qa[3];
+        tr[0] = ta[0]; tr[1] = ta[1]; tr[2] = ta[2];
+        return;
+    }
+    double dot = ((qa[0] * qb[0] + qa[1] * qb[1]) + qa[2] * qb[2]) + qa[3] * qb[3];
+    double v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        double bk = dot < 0.0 ? -qb[k] : qb[k];
+        v[k] = qa[k] + lam * (bk - qa[k]);
+    }
+    double n = norm4(v[0], v[1], v[2], v[3]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = v[k] / n;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) tr[k] = ta[k] + lam * (tb[k] - ta[k]);
+}
+
+__global__ void pose_kernel(sn_avatars av, const double *sim_times, double *pose_q, double *pose_t,
+                            double *joint_mats, double *eff_q, double *root, int32_t *err_flag) {
+    __shared__ double s_root_q[4];
+    int ea = blockIdx.x;
+    int A = av.n_avatars, J = av.n_joints, jp = J + 1;
+    int env = ea / A, a = ea % A;
+    int j = threadIdx.x;
+    // AvatarRuntime.clock (tasks.py:299-305)
+    double fps = av.fps[a];
+    int nf = av.n_frames[a];
+    double t = av.start_offset[a] + sim_times[env];
+    double duration = (double)nf / fps;
+    if (av.loop[a] && duration > 0)
+        t = fmod(t, duration);
+    else
+        t = t < duration ? t : duration;
+    bool bad = !(t >= 0.0);  // rig.py:80-81 (also rejects NaN)
+    const double *tq = av.traj_q + av.traj_offset[a] * jp * 4;
+    const double *tt = av.traj_t + av.traj_offset[a] * jp * 3;
+    double q[4] = {1.0, 0.0, 0.0, 0.0}, tr[3] = {0.0, 0.0, 0.0};
+    if (j <= J && !bad) sample_joint(tq, tt, nf, jp, fps, t, j, q, tr);
+    if (j == J) {
+        s_root_q[0] = q[0]; s_root_q[1] = q[1]; s_root_q[2] = q[2]; s_root_q[3] = q[3];
+    }
+    __syncthreads();
+    if (j > J) return;
+    if (bad) {
+        if (j == 0) atomicExch(err_flag, 1);
+        return;
+    }
+    if (pose_q) {
+        double *oq = pose_q + ((int64_t)ea * jp + j) * 4;
+        double *ot = pose_t + ((int64_t)ea * jp + j) * 3;
+        oq[0] = q[0]; oq[1] = q[1]; oq[2] = q[2]; oq[3] = q[3];
+        ot[0] = tr[0]; ot[1] = tr[1]; ot[2] = tr[2];
+    }
+    if (joint_mats == nullptr) return;
+    if (j < J) {
+        double rq[4] = {s_root_q[0], s_root_q[1], s_root_q[2], s_root_q[3]};
+        joint_prep(q, tr, rq, av.inv_bind + ((int64_t)a * J + j) * 16, joint_mats + ((int64_t)ea * J + j) * 12,
+                   eff_q + ((int64_t)ea * J + j) * 4);
+    } else {
+        root_prep(q, tr, root + (int64_t)ea * 12);
+    }
+}
+
+__global__ void joint_prep_kernel(sn_avatars av, int avatar, const double *pose_q, const double *pose_t,
+                                  double *joint_mats, double *eff_q, double *root) {
+    int J = av.n_joints, j = threadIdx.x;
+    if (j > J) return;
+    double q[4] = {pose_q[4 * j], pose_q[4 * j + 1], pose_q[4 * j + 2], pose_q[4 * j + 3]};
+    double t[3] = {pose_t[3 * j], pose_t[3 * j + 1], pose_t[3 * j + 2]};
+    if (j < J) {
+        double rq[4] = {pose_q[4 * J], pose_q[4 * J + 1], pose_q[4 * J + 2], pose_q[4 * J + 3]};
+        joint_prep(q, t, rq, av.inv_bind + ((int64_t)avatar * J + j) * 16, joint_mats + 12 * j, eff_q + 4 * j);
+    } else {
+        root_prep(q, t, root);
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_pose(const sn_avatars &av, const double *sim_times, int32_t n_envs, double *pose_q, double *pose_t,
+                        double *joint_mats, double *eff_q, double *root, int32_t *err_flag, cudaStream_t s) {
+    int threads = ((av.n_joints + 1 + 31) / 32) * 32;
+    pose_kernel<<<n_envs * av.n_avatars, threads, 0, s>>>(av, sim_times, pose_q, pose_t, joint_mats, eff_q, root,
+                                                           err_flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_joint_prep(const sn_avatars &av, int32_t avatar, const double *pose_q, const double *pose_t,
+                              double *joint_mats, double *eff_q, double *root, cudaStream_t s) {
+    int threads = ((av.n_joints + 1 + 31) / 32) * 32;
+    joint_prep_kernel<<<1, threads, 0, s>>>(av, avatar, pose_q, pose_t, joint_mats, eff_q, root);
+    return cudaGetLastError();
+}
+
+}  // namespace sn

@@ -1,0 +1,291 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the reference's golden
+fixtures on identical inputs.
+
+Bars (BASELINE.json north_star):
+* bit-exact: depth-sorted ids, tile CSR (tile_starts + per-tile depth ranks), per-pixel
+  contributor counts, RenderStats;
+* RGB max-abs error <= 2e-3; depth relative error <= 1e-4 (where alpha > 0; far elsewhere).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_cases
+from oracle import oracle as O
+from paper_2604_12626_b200 import synthetic as S
+
+pytestmark = pytest.mark.gpu
+
+RGB_TOL = 2e-3
+DEPTH_REL_TOL = 1e-4
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    from paper_2604_12626_b200 import build
+    build.build()
+
+
+def R():
+    from paper_2604_12626_b200 import renderer
+    return renderer
+
+
+def check_frame(color, alpha, depth, ref_color, ref_alpha, ref_depth, far):
+    color = np.asarray(color, dtype=np.float64)
+    depth = np.asarray(depth, dtype=np.float64)
+    assert np.abs(color - ref_color).max() <= RGB_TOL, np.abs(color - ref_color).max()
+    if ref_alpha is not None:
+        assert np.abs(np.asarray(alpha, dtype=np.float64) - ref_alpha).max() <= RGB_TOL
+    hit = ref_depth < far
+    rel = np.abs(depth - ref_depth) / np.maximum(np.abs(ref_depth), 1e-12)
+    assert rel[hit].max(initial=0.0) <= DEPTH_REL_TOL, rel[hit].max(initial=0.0)
+    np.testing.assert_array_equal(depth[~hit], ref_depth[~hit].astype(np.float32).astype(np.float64))
+
+
+def check_discrete(case_ids, tile_starts, pair_splat, contrib, pass_id, env, n_tiles):
+    r = R()
+    inter = r.pass_intermediates(pass_id, env)
+    np.testing.assert_array_equal(inter["ids"], case_ids)
+    if tile_starts is not None:
+        ts, ps = r.tile_csr(n_tiles, pass_id, env)
+        np.testing.assert_array_equal(ts, tile_starts)
+        if pair_splat is not None:
+            np.testing.assert_array_equal(ps, pair_splat)
+    return inter
+
+
+def render_case(case, cloud, cam):
+    r = R()
+    out = r.render_frames(cloud, [cam], case.background(), contrib=True)
+    return {k: v.cpu().numpy() for k, v in out.items() if isinstance(v, torch.Tensor)}
+
+
+def _check_golden_case(case, cloud, cam):
+    out = render_case(case, cloud, cam)
+    tiles_x, tiles_y = O.tiles_for(cam.width, cam.height)
+    inter = check_discrete(case["ids"], case["tile_starts"], case.get("pair_splat"), None, 0, 0, tiles_x * tiles_y)
+    np.testing.assert_array_equal(out["contrib_scene"][0], case["contrib"].astype(np.int32))
+    assert out["stats"][0].tolist() == case["stats"].tolist()
+    np.testing.assert_array_equal(inter["depths"], case["depths"])
+    if "means2d" in case and case["ids"].size:
+        np.testing.assert_array_equal(inter["means2d"], case["means2d"])
+        assert np.abs(inter["colors"] - case["colors"]).max() <= 1e-5
+    check_frame(out["color"][0], out["alpha"][0] if "alpha" in case else None, out["depth"][0], case["color"],
+                case.get("alpha"), case["depth"], cam.far)
+
+
+@pytest.mark.parametrize("name", ["c1_scenes", "edges"])
+def test_golden_small(name):
+    for case in load_cases(name):
+        _check_golden_case(case, case.cloud(), case.camera())
+
+
+def test_golden_config0():
+    (case,) = load_cases("config0")
+    scene, cam = S.config0()
+    _check_golden_case(case, scene, cam)
+
+
+def test_golden_room_batched():
+    cases = load_cases("room")
+    box = S.room_box(1_000_000)
+    scene = S.make_scene(100_000, box[0], box[1], seed=5)
+    cams = S.room_cameras(2, box, seed=6)
+    out = R().render_frames(scene, cams, np.array([1.0, 1.0, 1.0]), contrib=True)
+    tiles_x, tiles_y = O.tiles_for(640, 480)
+    for e, case in enumerate(cases):
+        check_discrete(case["ids"], case["tile_starts"], None, None, 0, e, tiles_x * tiles_y)
+        np.testing.assert_array_equal(out["contrib_scene"][e].cpu().numpy(), case["contrib"].astype(np.int32))
+        check_frame(out["color"][e].cpu().numpy(), None, out["depth"][e].cpu().numpy(), case["color"], None,
+                    case["depth"].astype(np.float64), cams[e].far)
+
+
+def _oracle_check_env(out, e, cloud, cam, bg, pass_id=0, layer_mode=False):
+    o = O.rasterize(cloud, cam, None if layer_mode else bg)
+    proj = O.project_cloud(cloud, cam)
+    tiles_x, tiles_y = O.tiles_for(cam.width, cam.height)
+    ts, ps = O.bin_tiles(proj.means2d, proj.radii, tiles_x, tiles_y)
+    check_discrete(proj.ids.astype(np.int32), ts, ps, None, pass_id, e, tiles_x * tiles_y)
+    key = "contrib_scene" if pass_id == 0 else "contrib_layer"
+    np.testing.assert_array_equal(out[key][e].cpu().numpy(), o.contrib)
+    return o
+
+
+def test_batched_envs_match_oracle_near_001_and_01():
+    box = S.room_box(1_000_000)
+    scene = S.make_scene(150_000, box[0], box[1], seed=21)
+    for near in (0.1, 0.01):
+        cams = S.room_cameras(6, box, seed=22, near=near)
+        bg = np.array([0.3, 0.6, 0.9])
+        out = R().render_frames(scene, cams, bg, contrib=True)
+        for e in (0, 3, 5):
+            o = _oracle_check_env(out, e, scene, cams[e], bg)
+            check_frame(out["color"][e].cpu().numpy(), out["alpha"][e].cpu().numpy(), out["depth"][e].cpu().numpy(),
+                        o.color, o.alpha, o.depth, cams[e].far)
+            assert out["stats"][e].tolist() == [o.stats[k] for k in ("n_input", "n_culled_depth", "n_culled_frame",
+                                                                     "n_degenerate", "n_drawn")]
+
+
+def test_float64_cloud_and_layer_mode():
+    box = S.room_box(1_000_000)
+    scene = S.make_scene(30_000, box[0], box[1], seed=31)
+    scene.positions = scene.positions.astype(np.float64) + 1e-9  # not float32-representable -> f64 path
+    cams = S.room_cameras(2, box, seed=32, width=160, height=120)
+    out = R().render_frames(scene, cams, None, contrib=True)
+    for e in range(2):
+        o = _oracle_check_env(out, e, scene, cams[e], None, layer_mode=True)
+        check_frame(out["color"][e].cpu().numpy(), out["alpha"][e].cpu().numpy(), out["depth"][e].cpu().numpy(),
+                    o.color, o.alpha, o.depth, cams[e].far)
+
+
+def test_rasterize_reference_equals_tiled():
+    case = load_cases("c1_scenes")[3]
+    r = R()
+    cloud, cam, bg = case.cloud(), case.camera(), case.background()
+    a = r.render_frames(cloud, [cam], bg, tiled=True, contrib=True)
+    b = r.render_frames(cloud, [cam], bg, tiled=False, contrib=True)
+    assert torch.equal(a["color"], b["color"]) and torch.equal(a["depth"], b["depth"])
+    assert torch.equal(a["contrib_scene"], b["contrib_scene"])
+    ref = r.rasterize_reference(cloud, cam, bg)
+    assert np.abs(ref.color - case["color"]).max() <= RGB_TOL
+
+
+def test_drop_in_rasterize_and_stats():
+    from paper_2604_12626_b200.renderer import RenderStats
+    case = load_cases("edges")[2]  # degenerate splats
+    stats = RenderStats()
+    frame = R().rasterize(case.cloud(), case.camera(), case.background(), stats=stats)
+    assert [stats.n_input, stats.n_culled_depth, stats.n_culled_frame, stats.n_degenerate, stats.n_drawn] == \
+        case["stats"].tolist()
+    assert frame.color.dtype == np.float64 and frame.shape == (64, 64)
+    assert np.abs(frame.color - case["color"]).max() <= RGB_TOL
+
+
+def test_determinism_bit_identical():
+    box = S.room_box(1_000_000)
+    scene = S.make_scene(50_000, box[0], box[1], seed=41)
+    cams = S.room_cameras(3, box, seed=42)
+    r = R()
+    a = r.render_frames(scene, cams, np.ones(3))
+    b = r.render_frames(scene, cams, np.ones(3))
+    for k in ("color", "alpha", "depth"):
+        assert torch.equal(a[k], b[k])
+
+
+# ------------------------------------------------------------------------------ avatars
+
+
+def _avatar_setup(n_avatars=2, n_gauss=3000, seed=50):
+    box = S.room_box(1_000_000)
+    bundles = [S.make_avatar(n_gauss, seed=seed + i, n_frames=12, floor_lo=(1.0, 1.0), floor_hi=(7.0, 7.0))
+               for i in range(n_avatars)]
+    return box, bundles
+
+
+def test_sample_pose_and_lbs_bit_exact_vs_oracle():
+    from paper_2604_12626_b200 import rig
+    _, bundles = _avatar_setup(1)
+    b = bundles[0]
+    for t in (0.0, 0.1, 0.137, 0.2, 99.0):
+        pose = rig.sample_pose(b.trajectory, t)
+        oq, ot = O.sample_pose(b.trajectory.quats, b.trajectory.trans, b.trajectory.fps, t)
+        np.testing.assert_array_equal(np.concatenate([pose.quats, pose.root_quat[None]]), oq)
+        np.testing.assert_array_equal(np.concatenate([pose.trans, pose.root_trans[None]]), ot)
+        cloud = rig.lbs_deform(b, pose)
+        op, orr = O.lbs_deform(b.canonical.positions, b.canonical.rotations, b.lbs_weights, b.inv_bind, oq, ot)
+        assert np.abs(cloud.positions - op).max() <= 1e-12
+        assert np.abs(cloud.rotations - orr).max() <= 1e-12
+
+
+def test_lbs_golden_fixtures():
+    from paper_2604_12626_b200 import rig
+    from paper_2604_12626_b200.avatar import AvatarBundle, Skeleton, Trajectory
+    from paper_2604_12626_b200.cloud import GaussianCloud
+    for case in load_cases("lbs"):
+        traj = Trajectory(float(case["fps"]), case["traj_quats"], case["traj_trans"])
+        pose = rig.sample_pose(traj, float(case["t"]))
+        np.testing.assert_array_equal(np.concatenate([pose.quats, pose.root_quat[None]]), case["pose_quats"])
+        np.testing.assert_array_equal(np.concatenate([pose.trans, pose.root_trans[None]]), case["pose_trans"])
+        n, j = case["weights"].shape
+        canon = GaussianCloud(case["canon_positions"], np.zeros((n, 1, 3), np.float32), np.zeros(n, np.float32),
+                              np.zeros((n, 3), np.float32), case["canon_rotations"])
+        bundle = AvatarBundle(canon, case["weights"], case["inv_bind"],
+                              Skeleton(np.array([-1] + [0] * (j - 1)), np.zeros((j, 3))), traj)
+        out = rig.lbs_deform(bundle, pose)
+        assert np.abs(out.positions - case["out_positions"]).max() <= 1e-12
+        assert np.abs(out.rotations - case["out_rotations"]).max() <= 1e-12
+
+
+def test_render_observation_golden():
+    r = R()
+    for case in load_cases("observation"):
+        avatars = [case.cloud(f"avatar{i}_") for i in range(int(case["n_avatars"]))]
+        frame = r.render_observation(case.cloud("scene_"), avatars, case.camera(), case["background"])
+        check_frame(frame.color, frame.alpha, frame.depth, case["color"], case["alpha"], case["depth"],
+                    case.camera().far)
+
+
+def test_fused_avatar_batch_matches_oracle():
+    """Batched scene + 2 skinned avatars at per-env times vs the oracle fed the GPU-skinned clouds."""
+    from paper_2604_12626_b200 import rig
+    from paper_2604_12626_b200.batch import BatchRenderer
+    from paper_2604_12626_b200.cloud import concat_clouds
+    box, bundles = _avatar_setup(2, 4000)
+    scene = S.make_scene(60_000, box[0], box[1], seed=61)
+    cams = S.room_cameras(5, box, seed=62, width=320, height=240)
+    # point two cameras at the avatars so the layer is non-trivial
+    times = np.array([0.0, 0.05, 0.133, 0.21, 0.3])
+    br = BatchRenderer(scene, bundles, start_offsets=[0.0, 0.1], loops=[1, 0], background=(0.2, 0.3, 0.4))
+    out = br.render(cams, times, contrib=True, stats=True)
+    for e in range(len(cams)):
+        clouds = []
+        for a, b in enumerate(bundles):
+            rt = rig.AvatarRuntime(b, start_offset=[0.0, 0.1][a], loop=[True, False][a])
+            clouds.append(rt.deformed_cloud(float(times[e])))
+        layer = concat_clouds(clouds)
+        o = O.render_observation(scene, clouds, cams[e], np.array([0.2, 0.3, 0.4]))
+        check_frame(out["color"][e].cpu().numpy(), out["alpha"][e].cpu().numpy(), out["depth"][e].cpu().numpy(),
+                    o.color, o.alpha, o.depth, cams[e].far)
+        # discrete parity of the avatar layer pass
+        lo = O.rasterize(layer, cams[e], None)
+        np.testing.assert_array_equal(out["contrib_layer"][e].cpu().numpy(), lo.contrib)
+        proj = O.project_cloud(layer, cams[e])
+        inter = R().pass_intermediates(1, e)
+        np.testing.assert_array_equal(inter["ids"], proj.ids.astype(np.int32))
+
+
+def test_composite_kernel_exact():
+    rng = np.random.default_rng(3)
+    h, w = 17, 23
+
+    def frame():
+        return R().FrameRGBD(rng.uniform(size=(h, w, 3)), rng.uniform(size=(h, w)), rng.uniform(0.5, 5, size=(h, w)))
+
+    f, b = frame(), frame()
+    f.alpha[0, :5] = 0.5
+    got = R().composite(f, b)
+    ref = O.composite(f, b)
+    np.testing.assert_array_equal(got.color, ref.color)
+    np.testing.assert_array_equal(got.depth, ref.depth)
+    np.testing.assert_array_equal(got.alpha, ref.alpha)
+
+
+def test_blend_tile_range_plugin():
+    from paper_2604_12626_b200 import raster
+    case = load_cases("c1_scenes")[5]
+    k = raster.get_kernel("cuda")
+    assert k.KERNEL_NAME == "cuda"
+    with pytest.raises(ValueError):
+        raster.get_kernel("python")
+    proj = O.project_cloud(case.cloud(), case.camera())
+    ts, ps = O.bin_tiles(proj.means2d, proj.radii, 4, 4)
+    acc = [np.zeros((64, 64, 3)), np.zeros((64, 64)), np.ones((64, 64)), np.zeros((64, 64))]
+    k.blend_tile_range(0, 16, 4, 16, 64, 64, ts, ps, proj.means2d, proj.conics, proj.depths, proj.colors,
+                       proj.alphas, *acc)
+    ref = O.blend(4, 16, 64, 64, ts, ps, proj.means2d, proj.conics, proj.depths, proj.colors, proj.alphas)
+    for a, b in zip(acc, ref[:4]):
+        assert np.abs(a - b).max() <= 1e-12
