@@ -44,7 +44,7 @@ enum {
 
 enum { SN_FLOAT32 = 0, SN_FLOAT64 = 1 };
 
-/* Pinhole camera (camera.py:16-56). 192 bytes. `center` is Camera.center as the host computes it
+/* Pinhole camera (camera.py:16-56). 208 bytes. `center` is Camera.center as the host computes it
  * (-R^T t, camera.py:43-48); has_background = 0 selects layer mode (renderer.py:69-71). */
 typedef struct sn_camera {
     double fx, fy, cx, cy, near_, far_;

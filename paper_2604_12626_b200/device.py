@@ -183,7 +183,7 @@ class DeviceAvatars:
 
 CAMERA_DTYPE = np.dtype([("intr", "<f8", 6), ("rot", "<f8", 9), ("trans", "<f8", 3), ("center", "<f8", 3),
                          ("background", "<f8", 3), ("size", "<i4", 2), ("has_background", "<i4"), ("pad", "<i4")])
-assert CAMERA_DTYPE.itemsize == 192
+assert CAMERA_DTYPE.itemsize == 208
 
 
 def camera_array(cameras, background):

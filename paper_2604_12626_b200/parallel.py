@@ -42,7 +42,7 @@ def gather_observations(rgb, depth, n_envs, dst=0, group=None):
             return t.contiguous()
         return torch.cat([t, t.new_zeros((pad,) + tuple(t.shape[1:]))]).contiguous()
 
-    send_rgb, send_depth = padded(rgb), padded(depth.view(torch.int16))
+    send_rgb, send_depth = padded(rgb), padded(depth.contiguous().view(torch.uint8))  # fp16 as bytes
     if rank == dst:
         rgb_list = [torch.empty_like(send_rgb) for _ in range(world)]
         depth_list = [torch.empty_like(send_depth) for _ in range(world)]

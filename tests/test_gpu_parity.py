@@ -254,7 +254,7 @@ def test_fused_avatar_batch_matches_oracle():
         lo = O.rasterize(layer, cams[e], None)
         np.testing.assert_array_equal(out["contrib_layer"][e].cpu().numpy(), lo.contrib)
         proj = O.project_cloud(layer, cams[e])
-        inter = R().pass_intermediates(1, e)
+        inter = R().pass_intermediates(1, e, context=br.context)
         np.testing.assert_array_equal(inter["ids"], proj.ids.astype(np.int32))
 
 
