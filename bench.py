@@ -31,7 +31,7 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 METRIC = "RGB-D frames/sec (640×480) vs gaussian count & avatar count at 1/2/4/8 B200"
-STAGES = ("pose", "count", "scan", "emit", "depth_sort", "permute", "pair_scan", "duplicate", "pair_sort", "ranges",
+STAGES = ("pose", "count", "scan", "emit", "depth_sort", "permute", "pair_scan", "bin_count", "bin_scatter", "ranges",
           "blend")
 
 
@@ -149,6 +149,7 @@ def measured_peaks():
 def algorithmic_bytes(stage, pass_id, n_gauss, n_avatar_gauss, work, n_pix_total, n_steps):
     """Minimum HBM bytes of one step's launches of `stage` (SURVEY.md 8(d) per-unit figures)."""
     vis, pairs, loads = work[pass_id][0] / n_steps, work[pass_id][1] / n_steps, work[pass_id][2] / n_steps
+    scans = work[pass_id][3] / n_steps
     n = n_gauss if pass_id == 0 else n_avatar_gauss
     per_gauss_in = 48 if pass_id == 0 else 134  # packed params (+ skin influences for avatars)
     if stage == "count":
@@ -161,14 +162,14 @@ def algorithmic_bytes(stage, pass_id, n_gauss, n_avatar_gauss, work, n_pix_total
         return vis * 160
     if stage == "pair_scan":
         return vis * 12
-    if stage == "duplicate":
-        return vis * 16 + pairs * 8
-    if stage == "pair_sort":
-        return pairs * 16
+    if stage == "bin_count":  # counting binner: read rects, write per-chunk tile counts (small)
+        return vis * 8
+    if stage == "bin_scatter":  # read rects, write one u32 per pair
+        return vis * 8 + pairs * 4
     if stage == "ranges":
         return pairs * 4
-    if stage == "blend":
-        return loads * 68 + n_pix_total * (20 + (8 if pass_id == 0 else 24))
+    if stage == "blend":  # records gathered (64 B + 4 B index) + rectangles streamed + pixels out
+        return loads * 68 + scans * 8 + n_pix_total * (20 + (8 if pass_id == 0 else 24))
     return 0.0
 
 
@@ -342,7 +343,10 @@ def main():
         "stages_ms_per_step": {k: round(v, 4) for k, v in per_stage.items()},
         "work_per_step": {"scene_visible": int(w2[0, 0] / args.steps), "scene_pairs": int(w2[0, 1] / args.steps),
                           "scene_records_loaded": int(w2[0, 2] / args.steps),
-                          "layer_visible": int(w2[1, 0] / args.steps), "layer_pairs": int(w2[1, 1] / args.steps)},
+                          "scene_rects_scanned": int(w2[0, 3] / args.steps),
+                          "layer_visible": int(w2[1, 0] / args.steps), "layer_pairs": int(w2[1, 1] / args.steps),
+                          "layer_records_loaded": int(w2[1, 2] / args.steps),
+                          "layer_rects_scanned": int(w2[1, 3] / args.steps)},
         "clocks": clocks.summary(),
     }
     line["gpu_launches"] = launches_per_step(args) * args.steps

@@ -116,8 +116,8 @@ enum {
     SN_STAGE_DEPTH_SORT = 4,
     SN_STAGE_PERMUTE = 5,
     SN_STAGE_PAIR_SCAN = 6,
-    SN_STAGE_DUPLICATE = 7,
-    SN_STAGE_PAIR_SORT = 8,
+    SN_STAGE_BIN_COUNT = 7,    /* radix: duplicate pairs; counting: chunk counts + scans */
+    SN_STAGE_BIN_SCATTER = 8,  /* radix: (env|tile) pair sort; counting: stable scatter */
     SN_STAGE_RANGES = 9,
     SN_STAGE_BLEND = 10,
     SN_N_STAGES = 11
@@ -126,14 +126,16 @@ enum {
 /* Per-call options. Null pointers disable the corresponding output. */
 typedef struct sn_render_opts {
     int32_t tiled;          /* 1: tile pipeline (rasterize); 0: rasterize_reference semantics */
-    int32_t pad0;
+    int32_t binning;        /* -1: auto (streaming for the scene pass, lists for the avatar layer);
+                               0: no tile lists, the blend streams depth-sorted rectangles;
+                               1: materialized lists (duplicate + stable (env|tile) radix sort) */
     const uint8_t *avatar_active; /* device (E, A) 0/1, NULL = all active */
     int32_t *contrib_scene; /* device (E,H,W): splats accumulated per pixel, scene pass */
     int32_t *contrib_layer; /* device (E,H,W): avatar-layer pass */
     sn_stats *stats;        /* device (E): RenderStats accumulated over both passes */
     double *stage_ms;       /* HOST (2 x SN_N_STAGES): GPU ms per stage (CUDA events), accumulated */
     int64_t *work;          /* HOST (2 x 4): visible splats, tile pairs, records gathered by the
-                               blend, blend CTAs -- per pass, accumulated */
+                               blend, rectangles the blend examined -- per pass, accumulated */
 } sn_render_opts;
 
 typedef struct sn_context sn_context;

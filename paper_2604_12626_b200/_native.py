@@ -50,11 +50,11 @@ class SnAvatars(ctypes.Structure):
 
 
 class SnRenderOpts(ctypes.Structure):
-    _fields_ = [("tiled", ctypes.c_int32), ("pad0", ctypes.c_int32), ("avatar_active", P),
+    _fields_ = [("tiled", ctypes.c_int32), ("binning", ctypes.c_int32), ("avatar_active", P),
                 ("contrib_scene", P), ("contrib_layer", P), ("stats", P), ("stage_ms", P), ("work", P)]
 
 
-STAGES = ("pose", "count", "scan", "emit", "depth_sort", "permute", "pair_scan", "duplicate", "pair_sort", "ranges",
+STAGES = ("pose", "count", "scan", "emit", "depth_sort", "permute", "pair_scan", "bin_count", "bin_scatter", "ranges",
           "blend")
 
 

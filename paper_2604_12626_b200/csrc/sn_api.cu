@@ -75,9 +75,9 @@ uint64_t dbits(double d) {
 
 struct PassWs {
     Buf vismask, blk_counts, env_off, keys_un, keys_s, vals_un, vals_s, recs_un, recs, gid_un, gid, rects_un, rects,
-        tiles, pair_off, pkeys_a, pkeys_b, pvals_a, pvals_b, ranges, temp;
+        tiles, pair_off, pkeys_a, pkeys_b, pvals_a, pvals_b, ranges, temp, batch_rects, super_rects;
     // metadata of the last chunk rendered by this pass
-    int32_t e0 = 0, ec = 0, tiles_x = 0, tiles_y = 0, tile_bits = 0, tiled = 1, valid = 0;
+    int32_t e0 = 0, ec = 0, tiles_x = 0, tiles_y = 0, tile_bits = 0, tiled = 1, valid = 0, binning = 0;
     int64_t n_vis = 0, n_pairs = 0;
 };
 
@@ -154,6 +154,13 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     const int tile_bits = std::max(1, bit_length((uint64_t)(n_tiles - 1)));
     const int env_bits = bit_length((uint64_t)(ec - 1));
     const int32_t n_blocks = (int32_t)std::max<int64_t>(1, (n + kBlock - 1) / kBlock);
+    // binning 1: materialized tile lists (duplicate + stable (env | tile) radix sort + ranges);
+    // 0: no lists -- each blend CTA streams its env's depth-sorted rectangles and stops at
+    // saturation. Auto (opts->binning < 0 or no opts): streaming for the scene pass, whose tiles
+    // saturate after ~1k rectangles; lists for the composited avatar layer, whose mostly empty
+    // tiles never saturate and have few pairs.
+    const int req = opts ? opts->binning : -1;
+    const int binning = req == 1 ? 1 : (req == 0 ? 0 : (sp.mode == 2 ? 1 : 0));
 
     SN_ENSURE(w.vismask, sizeof(uint64_t) * std::max<int64_t>(n, 1));
     SN_ENSURE(w.blk_counts, sizeof(uint32_t) * (size_t)ec * n_blocks);
@@ -203,6 +210,9 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     SN_ENSURE(w.rects, sizeof(ushort4) * v1);
     SN_ENSURE(w.tiles, sizeof(uint32_t) * v1);
     SN_ENSURE(w.pair_off, sizeof(uint64_t) * v1);
+    const int64_t n_batches = (V + kBlock - 1) / kBlock;
+    SN_ENSURE(w.batch_rects, sizeof(ushort4) * std::max<int64_t>(n_batches, 1));
+    SN_ENSURE(w.super_rects, sizeof(ushort4) * std::max<int64_t>((n_batches + kSuperBatch - 1) / kSuperBatch, 1));
 
     a.env_off = w.env_off.as<uint64_t>();
     a.keys = w.keys_un.as<unsigned long long>();
@@ -227,6 +237,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     b.recs_out = w.recs.as<SplatRec>();
     b.gid_out = w.gid.as<uint32_t>();
     b.rects_out = w.rects.as<ushort4>();
+    b.batch_rects = w.batch_rects.as<ushort4>();
     b.tiles_touched = w.tiles.as<uint32_t>();
     b.pair_off = w.pair_off.as<uint64_t>();
 
@@ -247,8 +258,9 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
         tm.end();
         tm.begin(SN_STAGE_PERMUTE);
         SN_CUDA(launch_permute(b, st));
+        SN_CUDA(launch_super_rects(w.batch_rects.as<ushort4>(), n_batches, w.super_rects.as<ushort4>(), st));
         tm.end();
-        if (tiled) {
+        if (tiled && (binning == 1 || work)) {  // pair offsets: the radix binner emits from them
             SN_CUDA(cudaMemsetAsync(w.tiles.as<uint32_t>() + V, 0, sizeof(uint32_t), st));
             tm.begin(SN_STAGE_PAIR_SCAN);
             SN_CUDA(scan_tiles(w.temp.p, w.temp.cap, w.tiles.as<uint32_t>(), w.pair_off.as<uint64_t>(), V + 1, st));
@@ -263,7 +275,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     const size_t n_ranges = (size_t)ec << tile_bits;
     SN_ENSURE(w.ranges, sizeof(uint2) * n_ranges);
     SN_CUDA(cudaMemsetAsync(w.ranges.p, 0, sizeof(uint2) * n_ranges, st));
-    if (P > 0) {
+    if (tiled && binning == 1 && P > 0) {
         SN_ENSURE(w.pkeys_a, sizeof(uint32_t) * P);
         SN_ENSURE(w.pkeys_b, sizeof(uint32_t) * P);
         SN_ENSURE(w.pvals_a, sizeof(uint32_t) * P);
@@ -272,10 +284,10 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
         SN_ENSURE(w.temp, tb);
         b.pair_keys = w.pkeys_a.as<uint32_t>();
         b.pair_vals = w.pvals_a.as<uint32_t>();
-        tm.begin(SN_STAGE_DUPLICATE);
+        tm.begin(SN_STAGE_BIN_COUNT);
         SN_CUDA(launch_duplicate(b, st));
         tm.end();
-        tm.begin(SN_STAGE_PAIR_SORT);
+        tm.begin(SN_STAGE_BIN_SCATTER);
         SN_CUDA(sort_u32_pairs(w.temp.p, w.temp.cap, w.pkeys_a.as<uint32_t>(), w.pkeys_b.as<uint32_t>(),
                                w.pvals_a.as<uint32_t>(), w.pvals_b.as<uint32_t>(), P, env_bits + tile_bits, st));
         tm.end();
@@ -292,7 +304,10 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     bl.height = height;
     bl.tiles_x = tiles_x;
     bl.tile_bits = tile_bits;
-    bl.brute = tiled ? 0 : 1;
+    bl.source = !tiled ? 2 : (binning == 1 ? 1 : 0);
+    bl.rects = w.rects.as<ushort4>();
+    bl.batch_rects = w.batch_rects.as<ushort4>();
+    bl.super_rects = w.super_rects.as<ushort4>();
     bl.mode = sp.mode;
     bl.ranges = w.ranges.as<uint2>();
     bl.pair_vals = w.pvals_b.as<uint32_t>();
@@ -304,20 +319,21 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     bl.depth64 = depth64;
     bl.contrib = opts ? (pass_id == 0 ? opts->contrib_scene : opts->contrib_layer) : nullptr;
     if (work) {
-        SN_ENSURE(ctx->loads, sizeof(unsigned long long));
-        SN_CUDA(cudaMemsetAsync(ctx->loads.p, 0, sizeof(unsigned long long), st));
+        SN_ENSURE(ctx->loads, 2 * sizeof(unsigned long long));
+        SN_CUDA(cudaMemsetAsync(ctx->loads.p, 0, 2 * sizeof(unsigned long long), st));
         bl.loads = ctx->loads.as<unsigned long long>();
+        bl.scans = bl.loads + 1;
     }
     tm.begin(SN_STAGE_BLEND);
     SN_CUDA(launch_blend(bl, st));
     tm.end();
     if (work) {
-        SN_CUDA(cudaMemcpyAsync(ctx->h_tot + 1, ctx->loads.p, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        SN_CUDA(cudaMemcpyAsync(ctx->h_tot + 1, ctx->loads.p, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
         SN_CUDA(cudaStreamSynchronize(st));
         work[0] += V;
         work[1] += P;
         work[2] += (int64_t)ctx->h_tot[1];
-        work[3] += (int64_t)ec * tiles_x * tiles_y;
+        work[3] += (int64_t)ctx->h_tot[2];
     }
 
     w.e0 = e0;
@@ -326,6 +342,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     w.tiles_y = tiles_y;
     w.tile_bits = tile_bits;
     w.tiled = tiled;
+    w.binning = binning;
     w.n_vis = V;
     w.n_pairs = P;
     w.valid = 1;
@@ -386,7 +403,7 @@ int sn_context_destroy(sn_context *ctx) {
     for (auto &w : ctx->pass) {
         for (Buf *b : {&w.vismask, &w.blk_counts, &w.env_off, &w.keys_un, &w.keys_s, &w.vals_un, &w.vals_s, &w.recs_un,
                        &w.recs, &w.gid_un, &w.gid, &w.rects_un, &w.rects, &w.tiles, &w.pair_off, &w.pkeys_a,
-                       &w.pkeys_b, &w.pvals_a, &w.pvals_b, &w.ranges, &w.temp})
+                       &w.pkeys_b, &w.pvals_a, &w.pvals_b, &w.ranges, &w.temp, &w.batch_rects, &w.super_rects})
             free_buf(*b);
     }
     for (Buf *b : {&ctx->cams, &ctx->times, &ctx->depth64, &ctx->jm, &ctx->eq, &ctx->root, &ctx->err, &ctx->pose_q,
@@ -406,7 +423,8 @@ int sn_context_workspace_bytes(const sn_context *ctx, size_t *bytes) {
     for (const auto &w : ctx->pass)
         for (const Buf *b : {&w.vismask, &w.blk_counts, &w.env_off, &w.keys_un, &w.keys_s, &w.vals_un, &w.vals_s,
                              &w.recs_un, &w.recs, &w.gid_un, &w.gid, &w.rects_un, &w.rects, &w.tiles, &w.pair_off,
-                             &w.pkeys_a, &w.pkeys_b, &w.pvals_a, &w.pvals_b, &w.ranges, &w.temp})
+                             &w.pkeys_a, &w.pkeys_b, &w.pvals_a, &w.pvals_b, &w.ranges, &w.temp,
+                             &w.batch_rects, &w.super_rects})
             t += b->cap;
     for (const Buf *b : {&ctx->cams, &ctx->times, &ctx->depth64, &ctx->jm, &ctx->eq, &ctx->root, &ctx->err,
                          &ctx->pose_q, &ctx->pose_t})
@@ -532,6 +550,52 @@ static int pass_env(sn_context *ctx, int32_t pass, int32_t env, PassWs *&w, int 
     return SN_OK;
 }
 
+// Tile CSR of env `el` in the reference's form (tile_starts, depth ranks). binning 1: the device's
+// materialized lists. binning 0: the blend consumed no lists -- each tile took, in depth order,
+// the splats whose device-computed rectangle covers it -- so the CSR is rebuilt from the
+// device's depth-sorted rectangles by exactly that rule.
+static int env_tile_csr(PassWs *w, int el, const std::vector<uint64_t> &off, std::vector<int64_t> &ts,
+                        std::vector<int32_t> &ps) {
+    const int n_tiles = w->tiles_x * w->tiles_y;
+    ts.assign(n_tiles + 1, 0);
+    ps.clear();
+    if (!w->tiled || w->n_vis == 0) return SN_OK;
+    const uint64_t v0 = off[el], v1 = off[el + 1];
+    if (w->binning == 1) {
+        std::vector<uint2> rng(n_tiles);
+        SN_CUDA(cudaMemcpy(rng.data(), w->ranges.as<uint2>() + ((size_t)el << w->tile_bits), sizeof(uint2) * n_tiles,
+                           cudaMemcpyDeviceToHost));
+        uint64_t pp[2];
+        SN_CUDA(cudaMemcpy(&pp[0], w->pair_off.as<uint64_t>() + v0, 8, cudaMemcpyDeviceToHost));
+        SN_CUDA(cudaMemcpy(&pp[1], w->pair_off.as<uint64_t>() + v1, 8, cudaMemcpyDeviceToHost));
+        for (int t = 0; t < n_tiles; ++t) ts[t + 1] = ts[t] + (int64_t)(rng[t].y - rng[t].x);
+        SN_CHECK(ts[n_tiles] == (int64_t)(pp[1] - pp[0]), "tile ranges do not cover the env's pairs");
+        std::vector<uint32_t> v((size_t)(pp[1] - pp[0]));
+        if (!v.empty())
+            SN_CUDA(cudaMemcpy(v.data(), w->pvals_b.as<uint32_t>() + pp[0], sizeof(uint32_t) * v.size(),
+                               cudaMemcpyDeviceToHost));
+        ps.resize(v.size());
+        for (size_t i = 0; i < v.size(); ++i) ps[i] = (int32_t)(v[i] - v0);
+        return SN_OK;
+    }
+    std::vector<ushort4> rects((size_t)(v1 - v0));
+    if (!rects.empty())
+        SN_CUDA(cudaMemcpy(rects.data(), w->rects.as<ushort4>() + v0, sizeof(ushort4) * rects.size(),
+                           cudaMemcpyDeviceToHost));
+    for (const ushort4 &q : rects)
+        for (int y = q.z; y <= q.w; ++y)
+            for (int x = q.x; x <= q.y; ++x) ts[y * w->tiles_x + x + 1]++;
+    for (int t = 0; t < n_tiles; ++t) ts[t + 1] += ts[t];
+    std::vector<int64_t> cur(ts.begin(), ts.end() - 1);
+    ps.resize((size_t)ts[n_tiles]);
+    for (size_t i = 0; i < rects.size(); ++i) {
+        const ushort4 &q = rects[i];
+        for (int y = q.z; y <= q.w; ++y)
+            for (int x = q.x; x <= q.y; ++x) ps[(size_t)cur[y * w->tiles_x + x]++] = (int32_t)i;
+    }
+    return SN_OK;
+}
+
 int sn_get_counts(sn_context *ctx, int32_t pass, int32_t env, int64_t *n_visible, int64_t *n_pairs) {
     PassWs *w;
     int el;
@@ -541,13 +605,11 @@ int sn_get_counts(sn_context *ctx, int32_t pass, int32_t env, int64_t *n_visible
     int64_t v0 = (int64_t)off[el], v1 = (int64_t)off[el + 1];
     if (n_visible) *n_visible = v1 - v0;
     if (n_pairs) {
-        *n_pairs = 0;
-        if (w->tiled && w->n_vis > 0) {
-            uint64_t p[2];
-            SN_CUDA(cudaMemcpy(&p[0], w->pair_off.as<uint64_t>() + v0, 8, cudaMemcpyDeviceToHost));
-            SN_CUDA(cudaMemcpy(&p[1], w->pair_off.as<uint64_t>() + v1, 8, cudaMemcpyDeviceToHost));
-            *n_pairs = (int64_t)(p[1] - p[0]);
-        }
+        std::vector<int64_t> ts;
+        std::vector<int32_t> ps;
+        r = env_tile_csr(w, el, off, ts, ps);
+        if (r != SN_OK) return r;
+        *n_pairs = (int64_t)ps.size();
     }
     return SN_OK;
 }
@@ -572,27 +634,13 @@ int sn_get_tile_csr(sn_context *ctx, int32_t pass, int32_t env, int64_t *tile_st
     int r = pass_env(ctx, pass, env, w, el, off);
     if (r != SN_OK) return r;
     SN_CHECK(w->tiled, "last pass was not tiled");
-    const int n_tiles = w->tiles_x * w->tiles_y;
-    std::vector<uint2> rng(n_tiles);
-    SN_CUDA(cudaMemcpy(rng.data(), w->ranges.as<uint2>() + ((size_t)el << w->tile_bits), sizeof(uint2) * n_tiles,
-                       cudaMemcpyDeviceToHost));
-    int64_t p0 = 0, p1 = 0;
-    if (w->n_vis > 0) {
-        uint64_t pp[2];
-        SN_CUDA(cudaMemcpy(&pp[0], w->pair_off.as<uint64_t>() + off[el], 8, cudaMemcpyDeviceToHost));
-        SN_CUDA(cudaMemcpy(&pp[1], w->pair_off.as<uint64_t>() + off[el + 1], 8, cudaMemcpyDeviceToHost));
-        p0 = (int64_t)pp[0];
-        p1 = (int64_t)pp[1];
-    }
-    SN_CHECK(capacity >= p1 - p0, "pair buffer too small");
-    tile_starts_host[0] = 0;
-    for (int t = 0; t < n_tiles; ++t) tile_starts_host[t + 1] = tile_starts_host[t] + (int64_t)(rng[t].y - rng[t].x);
-    SN_CHECK(tile_starts_host[n_tiles] == p1 - p0, "tile ranges do not cover the env's pairs");
-    if (p1 > p0) {
-        std::vector<uint32_t> v((size_t)(p1 - p0));
-        SN_CUDA(cudaMemcpy(v.data(), w->pvals_b.as<uint32_t>() + p0, sizeof(uint32_t) * v.size(), cudaMemcpyDeviceToHost));
-        for (size_t i = 0; i < v.size(); ++i) pair_splat_host[i] = (int32_t)(v[i] - off[el]);
-    }
+    std::vector<int64_t> ts;
+    std::vector<int32_t> ps;
+    r = env_tile_csr(w, el, off, ts, ps);
+    if (r != SN_OK) return r;
+    SN_CHECK(capacity >= (int64_t)ps.size(), "pair buffer too small");
+    std::copy(ts.begin(), ts.end(), tile_starts_host);
+    std::copy(ps.begin(), ps.end(), pair_splat_host);
     return SN_OK;
 }
 

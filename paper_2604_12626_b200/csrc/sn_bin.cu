@@ -14,12 +14,43 @@
 #include "sn_common.cuh"
 #include "sn_internal.h"
 
+
 namespace sn {
 
 namespace {
 
+__device__ __forceinline__ ushort4 rect_union(ushort4 a, ushort4 c) {
+    return make_ushort4(min(a.x, c.x), max(a.y, c.y), min(a.z, c.z), max(a.w, c.w));
+}
+
+__device__ __forceinline__ ushort4 warp_rect_union(ushort4 r) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ushort4 q;
+        q.x = (unsigned short)__shfl_xor_sync(0xffffffffu, (unsigned)r.x, o);
+        q.y = (unsigned short)__shfl_xor_sync(0xffffffffu, (unsigned)r.y, o);
+        q.z = (unsigned short)__shfl_xor_sync(0xffffffffu, (unsigned)r.z, o);
+        q.w = (unsigned short)__shfl_xor_sync(0xffffffffu, (unsigned)r.w, o);
+        r = rect_union(r, q);
+    }
+    return r;
+}
+
+// Permutes records into depth order and writes each splat's tile rectangle, its tile count and,
+// per 256-splat batch (one CTA), the batch's union rectangle for the blend's cull.
 __global__ void __launch_bounds__(kBlock) permute_kernel(BinArgs b) {
+    __shared__ ushort4 s_u[kBlock / 32];
     int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    ushort4 mine = make_ushort4(0xffff, 0, 0xffff, 0);  // empty
+    if (i < b.n_vis) mine = b.rects_in[b.vals_sorted[i]];
+    ushort4 u = warp_rect_union(mine);
+    if ((threadIdx.x & 31) == 0) s_u[threadIdx.x >> 5] = u;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ushort4 t = s_u[0];
+        for (int w = 1; w < kBlock / 32; ++w) t = rect_union(t, s_u[w]);
+        b.batch_rects[blockIdx.x] = t;
+    }
     if (i >= b.n_vis) return;
     uint32_t slot = b.vals_sorted[i];
     const uint4 *src = reinterpret_cast<const uint4 *>(b.recs_in + slot);
@@ -30,7 +61,7 @@ __global__ void __launch_bounds__(kBlock) permute_kernel(BinArgs b) {
     dst[2] = v2;
     dst[3] = v3;
     b.gid_out[i] = __ldg(b.gid_in + slot);
-    ushort4 r = b.rects_in[slot];
+    ushort4 r = mine;
     b.rects_out[i] = r;
     b.tiles_touched[i] = (uint32_t)(r.y - r.x + 1) * (uint32_t)(r.w - r.z + 1);
 }
@@ -83,7 +114,25 @@ __global__ void __launch_bounds__(kBlock) ranges_kernel(const uint32_t *keys, in
     if (i == n - 1 || keys[i + 1] != k) ranges[k].y = (uint32_t)(i + 1);
 }
 
+__global__ void __launch_bounds__(kBlock) super_rects_kernel(const ushort4 *batch_rects, int64_t n_batches,
+                                                            ushort4 *super_rects) {
+    int64_t sb = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    int64_t b0 = sb * kSuperBatch;
+    if (b0 >= n_batches) return;
+    ushort4 t = batch_rects[b0];
+    for (int64_t k = b0 + 1; k < min(n_batches, b0 + kSuperBatch); ++k) t = rect_union(t, batch_rects[k]);
+    super_rects[sb] = t;
+}
+
 }  // namespace
+
+cudaError_t launch_super_rects(const ushort4 *batch_rects, int64_t n_batches, ushort4 *super_rects, cudaStream_t s) {
+    int64_t n_super = (n_batches + kSuperBatch - 1) / kSuperBatch;
+    if (n_super == 0) return cudaSuccess;
+    super_rects_kernel<<<(unsigned)((n_super + kBlock - 1) / kBlock), kBlock, 0, s>>>(batch_rects, n_batches,
+                                                                                      super_rects);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_permute(const BinArgs &b, cudaStream_t s) {
     if (b.n_vis == 0) return cudaSuccess;

@@ -16,37 +16,94 @@ namespace sn {
 
 namespace {
 
-template <int MODE>
+constexpr unsigned kFull = 0xffffffffu;
+
+// SOURCE 0: no tile lists. The CTA streams its env's depth-sorted tile rectangles (8 B each; the
+//           env's 2 MB array stays in L2 while its 1,200 tiles run) and compacts, in depth order,
+//           the splats whose rectangle covers this tile into a shared-memory queue. The walk
+//           stops with the early-termination vote, so a saturated tile never looks at the rest
+//           of the env -- no pair duplication, no sort, no per-pair HBM traffic.
+// SOURCE 1: a materialized tile list (ranges + pair_vals from the radix binner).
+// SOURCE 2: rasterize_reference -- every splat of the env, in depth order.
+template <int MODE, int SOURCE>
 __global__ void __launch_bounds__(kBlock) blend_kernel(BlendArgs b) {
     __shared__ SplatRec s_rec[kBlock];
+    __shared__ uint32_t s_queue[2 * kBlock];
+    __shared__ uint32_t s_wsum[kBlock / 32];
     const int tile = blockIdx.x, el = blockIdx.y, env = b.e0 + el;
     const int tx = tile % b.tiles_x, ty = tile / b.tiles_x;
     const int px_i = tx * kTile + (threadIdx.x & (kTile - 1));
     const int py_i = ty * kTile + (threadIdx.x / kTile);
     const bool inside = px_i < b.width && py_i < b.height;
     const double px = px_i + 0.5, py = py_i + 0.5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    uint32_t s0, s1;
-    if (b.brute) {
-        s0 = (uint32_t)b.env_off[el];
-        s1 = (uint32_t)b.env_off[el + 1];
-    } else {
+    uint32_t cursor, s1;
+    if (SOURCE == 1) {
         uint2 r = b.ranges[((uint32_t)el << b.tile_bits) | (uint32_t)tile];
-        s0 = r.x;
+        cursor = r.x;
         s1 = r.y;
+    } else {
+        cursor = (uint32_t)b.env_off[el];
+        s1 = (uint32_t)b.env_off[el + 1];
     }
 
     double T = 1.0, A = 0.0, D = 0.0;
     float cr = 0.0f, cg = 0.0f, cb = 0.0f;
     int nc = 0;
     bool done = !inside;
-    uint32_t loaded = 0;
-    for (uint32_t base = s0; base < s1; base += kBlock) {
-        if (__syncthreads_count(!done) == 0) break;  // also guards s_rec reuse
-        loaded += min((uint32_t)kBlock, s1 - base);
-        uint32_t idx = base + threadIdx.x;
-        if (idx < s1) {
-            uint32_t rid = b.brute ? idx : __ldg(b.pair_vals + idx);
+    uint32_t loaded = 0, scanned = 0;
+    int q_len = 0;  // SOURCE 0: entries waiting in s_queue (uniform across the CTA)
+    while (true) {
+        if (__syncthreads_count(!done) == 0) break;  // also guards s_rec / s_queue reuse
+        int n;
+        if (SOURCE == 0) {
+            while (q_len < kBlock && cursor < s1) {
+                // hierarchical cull (uniform across the CTA, no barrier on the skip path):
+                // 8192-splat super-batches, then 256-splat batches, by their union rectangles
+                const uint32_t bi = cursor / kBlock;
+                const ushort4 sr = __ldg(b.super_rects + bi / kSuperBatch);
+                if (!((sr.x <= tx) && (tx <= sr.y) && (sr.z <= ty) && (ty <= sr.w))) {
+                    cursor = min(s1, (bi / kSuperBatch + 1) * (uint32_t)(kSuperBatch * kBlock));
+                    continue;
+                }
+                const ushort4 br = __ldg(b.batch_rects + bi);
+                const uint32_t b_end = min(s1, (bi + 1) * (uint32_t)kBlock);
+                if (!((br.x <= tx) && (tx <= br.y) && (br.z <= ty) && (ty <= br.w))) {
+                    cursor = b_end;
+                    continue;
+                }
+                uint32_t i = bi * kBlock + threadIdx.x;
+                bool hit = false;
+                if (i >= cursor && i < b_end) {
+                    ushort4 r = __ldg(b.rects + i);
+                    hit = (r.x <= tx) && (tx <= r.y) && (r.z <= ty) && (ty <= r.w);
+                }
+                unsigned bal = __ballot_sync(kFull, hit);
+                if (lane == 0) s_wsum[warp] = __popc(bal);
+                __syncthreads();
+                int woff = 0, tot = 0;
+#pragma unroll
+                for (int w = 0; w < kBlock / 32; ++w) {
+                    int c = s_wsum[w];
+                    woff += (w < warp) ? c : 0;
+                    tot += c;
+                }
+                if (hit) s_queue[q_len + woff + __popc(bal & ((1u << lane) - 1u))] = i;
+                q_len += tot;
+                scanned += b_end - cursor;
+                cursor = b_end;
+                __syncthreads();
+            }
+            n = min(q_len, kBlock);
+        } else {
+            n = (int)min((uint32_t)kBlock, s1 - cursor);
+        }
+        if (n <= 0) break;
+        loaded += n;
+        if (threadIdx.x < n) {
+            uint32_t rid = SOURCE == 0 ? s_queue[threadIdx.x]
+                                       : (SOURCE == 1 ? __ldg(b.pair_vals + cursor + threadIdx.x) : cursor + threadIdx.x);
             const uint4 *src = reinterpret_cast<const uint4 *>(b.recs + rid);
             uint4 *dst = reinterpret_cast<uint4 *>(s_rec + threadIdx.x);
             uint4 v0 = __ldg(src), v1 = __ldg(src + 1), v2 = __ldg(src + 2), v3 = __ldg(src + 3);
@@ -57,8 +114,7 @@ __global__ void __launch_bounds__(kBlock) blend_kernel(BlendArgs b) {
         }
         __syncthreads();
         if (!done) {
-            const int cnt = (int)min((uint32_t)kBlock, s1 - base);
-            for (int j = 0; j < cnt; ++j) {
+            for (int j = 0; j < n; ++j) {
                 if (T < kTCutoff) break;
                 const SplatRec &s = s_rec[j];
                 double dx = s.mx - px, dy = s.my - py;
@@ -80,7 +136,17 @@ __global__ void __launch_bounds__(kBlock) blend_kernel(BlendArgs b) {
             }
             done = T < kTCutoff;
         }
+        if (SOURCE == 0) {  // drop the consumed head of the queue
+            int rest = q_len - n;
+            uint32_t v = threadIdx.x < rest ? s_queue[n + threadIdx.x] : 0u;
+            __syncthreads();
+            if (threadIdx.x < rest) s_queue[threadIdx.x] = v;
+            q_len = rest;
+        } else {
+            cursor += n;
+        }
     }
+    if (b.scans && threadIdx.x == 0 && scanned) atomicAdd(b.scans, (unsigned long long)scanned);
     if (b.loads && threadIdx.x == 0 && loaded) atomicAdd(b.loads, (unsigned long long)loaded);
     if (!inside) return;
 
@@ -186,14 +252,24 @@ __global__ void blend_tile_range_kernel(int t_begin, int tiles_x, int tile_size,
 
 }  // namespace
 
+template <int MODE>
+static void launch_blend_mode(const BlendArgs &b, dim3 grid, cudaStream_t s) {
+    if (b.source == 0)
+        blend_kernel<MODE, 0><<<grid, kBlock, 0, s>>>(b);
+    else if (b.source == 1)
+        blend_kernel<MODE, 1><<<grid, kBlock, 0, s>>>(b);
+    else
+        blend_kernel<MODE, 2><<<grid, kBlock, 0, s>>>(b);
+}
+
 cudaError_t launch_blend(const BlendArgs &b, cudaStream_t s) {
     dim3 grid((unsigned)(tiles_of(b.width) * tiles_of(b.height)), (unsigned)b.ec);
     if (b.mode == 0)
-        blend_kernel<0><<<grid, kBlock, 0, s>>>(b);
+        launch_blend_mode<0>(b, grid, s);
     else if (b.mode == 1)
-        blend_kernel<1><<<grid, kBlock, 0, s>>>(b);
+        launch_blend_mode<1>(b, grid, s);
     else
-        blend_kernel<2><<<grid, kBlock, 0, s>>>(b);
+        launch_blend_mode<2>(b, grid, s);
     return cudaGetLastError();
 }
 

@@ -72,13 +72,16 @@ struct BinArgs {
     SplatRec *recs_out;
     uint32_t *gid_out;
     ushort4 *rects_out;
+    ushort4 *batch_rects;    // (ceil(n_vis / 256)) union rect per 256-splat batch
     uint32_t *tiles_touched;
     uint64_t *pair_off;      // (n_vis + 1)
     uint32_t *pair_keys;
     uint32_t *pair_vals;
     uint2 *ranges;           // (ec << tile_bits)
 };
+constexpr int kSuperBatch = 32;  // batches per super-batch (8192 splats)
 cudaError_t launch_permute(const BinArgs &b, cudaStream_t s);
+cudaError_t launch_super_rects(const ushort4 *batch_rects, int64_t n_batches, ushort4 *super_rects, cudaStream_t s);
 cudaError_t launch_duplicate(const BinArgs &b, cudaStream_t s);
 cudaError_t launch_ranges(const uint32_t *keys_sorted, int64_t n_pairs, uint2 *ranges, cudaStream_t s);
 size_t sort_u64_temp_bytes(int64_t n);
@@ -95,7 +98,11 @@ cudaError_t scan_tiles(void *temp, size_t temp_bytes, const uint32_t *tiles_touc
 struct BlendArgs {
     const sn_camera *cams;
     int32_t e0, ec, width, height, tiles_x, tile_bits;
-    int32_t brute;          // rasterize_reference: every tile walks the env's whole depth order
+    int32_t source;         // 0: scan the env's depth-sorted rects (no tile lists); 1: tile lists
+                            // (ranges + pair_vals); 2: rasterize_reference -- every splat of the env
+    const ushort4 *rects;   // depth-sorted tile rectangles (source 0)
+    const ushort4 *batch_rects;  // union rectangle of each global 256-splat batch of rects
+    const ushort4 *super_rects;  // union rectangle of each kSuperBatch batches
     int32_t mode;           // 0 scene (background), 1 layer only, 2 layer composited over outputs
     const uint2 *ranges;
     const uint32_t *pair_vals;
@@ -105,6 +112,7 @@ struct BlendArgs {
     double *depth64;        // scene pass: exact depth for the compositor (may be null)
     int32_t *contrib;       // (E,H,W) may be null
     unsigned long long *loads;  // device counter: records gathered into shared memory (may be null)
+    unsigned long long *scans;  // device counter: rectangles examined by source-0 tiles (may be null)
 };
 cudaError_t launch_blend(const BlendArgs &b, cudaStream_t s);
 cudaError_t launch_composite64(int64_t npix, const double *fc, const double *fa, const double *fd, const double *bc,
