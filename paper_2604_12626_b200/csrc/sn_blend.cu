@@ -18,6 +18,50 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Shared-memory form of a record: a float32 copy of the geometry relative to the tile origin for
+// the pre-filter, the float64 decision-chain fields, colour unpacked to float. 96 bytes.
+struct __align__(16) BlendRec {
+    float mxr, myr, caf, cb2f;  // mean - tile origin, conic (a, 2b) in float32
+    float ccf, r, g, b;
+    double mx, my, ca, cb2, cc, alpha, z, pad;
+};
+
+// 2^(j/64), j = 0..63 (round to nearest)
+__constant__ double kExp2Tbl[64] = {
+    1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284, 1.0442737824274138, 1.0556451783605572,
+    1.0671404006768237, 1.0787607977571199, 1.0905077326652577, 1.102382583307841, 1.1143867425958924,
+    1.1265216186082418, 1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812,
+    1.189207115002721, 1.202156731452703, 1.215247359980469, 1.22848053610687, 1.241857812073484, 1.255380757024691,
+    1.2690509571917332, 1.2828700160787783, 1.2968395546510096, 1.3109612115247644, 1.3252366431597413,
+    1.339667524053303, 1.3542555469368927, 1.3690024229745905, 1.383909881963832, 1.3989796725383112,
+    1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647, 1.4768261459394993,
+    1.4929077282912648, 1.5091644275934228, 1.5255981507445384, 1.5422108254079407, 1.559004400237837,
+    1.5759808451078865, 1.593142151342267, 1.6104903319492543, 1.6280274218573478, 1.645755478153965,
+    1.6636765803267364, 1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062,
+    1.7562521603732995, 1.7753764925265212, 1.7947090750031072, 1.8142521755003989, 1.8340080864093424,
+    1.8539791250833855, 1.8741676341103, 1.8945759815869656, 1.9152065613971474, 1.9360617934922943,
+    1.9571441241754002, 1.978456026387951};
+
+// exp(x) for the blend's argument range x = -d2/2, d2 in [~0, 9]: 2^(n/64) * e^r with a 64-entry
+// table in shared memory and a degree-5 polynomial, |r| <= ln2/128 (+ the slack of a 21-bit scale).
+// Max error 2 ulp (numpy's, libm's and CUDA's exp also differ by ulps). Constants whose low word is
+// zero encode as instruction immediates, so the loop does not re-materialize them.
+#define SN_EXP_BLEND(x, tbl, out)                                                                  \
+    do {                                                                                           \
+        const double _t = fma((x), 92.33245849609375, 6755399441055744.0); /* ~64/ln2 (21 bits), 1.5*2^52 */ \
+        const int _n = __double2loint(_t);                                                         \
+        const double _nd = _t - 6755399441055744.0;                                                \
+        double _r = fma(_nd, -0.010830417275428772, (x)); /* ln2/64 hi: 21 bits */                                           \
+        _r = fma(_nd, -7.420820373486988e-09, _r);                                                \
+        double _p = fma(_r, 0.008333333333333333, 0.041666666666666664);                           \
+        _p = fma(_p, _r, 0.16666666666666666);                                                     \
+        _p = fma(_p, _r, 0.5);                                                                     \
+        _p = fma(_p, _r, 1.0);                                                                     \
+        _p = fma(_p, _r, 1.0);                                                                     \
+        const double _v = (tbl)[_n & 63] * _p;                                                     \
+        (out) = __hiloint2double(__double2hiint(_v) + ((_n >> 6) << 20), __double2loint(_v));    \
+    } while (0)
+
 // SOURCE 0: no tile lists. The CTA streams its env's depth-sorted tile rectangles (8 B each; the
 //           env's 2 MB array stays in L2 while its 1,200 tiles run) and compacts, in depth order,
 //           the splats whose rectangle covers this tile into a shared-memory queue. The walk
@@ -27,16 +71,23 @@ constexpr unsigned kFull = 0xffffffffu;
 // SOURCE 2: rasterize_reference -- every splat of the env, in depth order.
 template <int MODE, int SOURCE>
 __global__ void __launch_bounds__(kBlock) blend_kernel(BlendArgs b) {
-    __shared__ SplatRec s_rec[kBlock];
+    __shared__ BlendRec s_rec[kBlock];
+    __shared__ double s_exp[64];
     __shared__ uint32_t s_queue[2 * kBlock];
     __shared__ uint32_t s_wsum[kBlock / 32];
     const int tile = blockIdx.x, el = blockIdx.y, env = b.e0 + el;
     const int tx = tile % b.tiles_x, ty = tile / b.tiles_x;
-    const int px_i = tx * kTile + (threadIdx.x & (kTile - 1));
-    const int py_i = ty * kTile + (threadIdx.x / kTile);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // each warp shades an 8 x 4 pixel block (compact footprint: splats that miss the block skip
+    // the float64 path for the whole warp more often than with 16 x 2 rows)
+    const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
+    const int px_i = tx * kTile + lx;
+    const int py_i = ty * kTile + ly;
     const bool inside = px_i < b.width && py_i < b.height;
     const double px = px_i + 0.5, py = py_i + 0.5;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double x0 = tx * kTile, y0 = ty * kTile;
+    const float lxf = (float)lx + 0.5f, lyf = (float)ly + 0.5f;
+    if (threadIdx.x < 64) s_exp[threadIdx.x] = kExp2Tbl[threadIdx.x];
 
     uint32_t cursor, s1;
     if (SOURCE == 1) {
@@ -104,35 +155,58 @@ __global__ void __launch_bounds__(kBlock) blend_kernel(BlendArgs b) {
         if (threadIdx.x < n) {
             uint32_t rid = SOURCE == 0 ? s_queue[threadIdx.x]
                                        : (SOURCE == 1 ? __ldg(b.pair_vals + cursor + threadIdx.x) : cursor + threadIdx.x);
-            const uint4 *src = reinterpret_cast<const uint4 *>(b.recs + rid);
-            uint4 *dst = reinterpret_cast<uint4 *>(s_rec + threadIdx.x);
-            uint4 v0 = __ldg(src), v1 = __ldg(src + 1), v2 = __ldg(src + 2), v3 = __ldg(src + 3);
-            dst[0] = v0;
-            dst[1] = v1;
-            dst[2] = v2;
-            dst[3] = v3;
+            const double2 *src = reinterpret_cast<const double2 *>(b.recs + rid);
+            double2 m = __ldg(src), c01 = __ldg(src + 1), c2a = __ldg(src + 2), zr = __ldg(src + 3);
+            BlendRec &d = s_rec[threadIdx.x];
+            d.mxr = (float)(m.x - x0);
+            d.myr = (float)(m.y - y0);
+            d.caf = (float)c01.x;
+            d.cb2f = (float)c01.y;
+            d.ccf = (float)c2a.x;
+            float rgb[3];
+            unpack_rgb21((unsigned long long)__double_as_longlong(zr.y), rgb);
+            d.r = rgb[0];
+            d.g = rgb[1];
+            d.b = rgb[2];
+            d.mx = m.x;
+            d.my = m.y;
+            d.ca = c01.x;
+            d.cb2 = c01.y;
+            d.cc = c2a.x;
+            d.alpha = c2a.y;
+            d.z = zr.x;
         }
         __syncthreads();
         if (!done) {
             for (int j = 0; j < n; ++j) {
-                if (T < kTCutoff) break;
-                const SplatRec &s = s_rec[j];
+                const BlendRec &s = s_rec[j];
+                // float32 pre-filter: d2f = dx (a dx + 2b dy) + c dy^2 with FMAs. For a positive
+                // definite conic |2b dx dy| <= a dx^2 + c dy^2, so every term is bounded by
+                // M = 2 (a dx^2 + c dy^2); the float error is far below 2^-14 M + 1e-3, and a splat
+                // clearing 9 by that margin is certainly outside the support. Survivors take the
+                // exact float64 test.
+                const float dxf = s.mxr - lxf, dyf = s.myr - lyf;
+                const float cyf = s.ccf * dyf;
+                const float d2f = __fmaf_rn(dxf, __fmaf_rn(s.caf, dxf, s.cb2f * dyf), cyf * dyf);
+                const float mag = __fmaf_rn(s.caf * dxf, dxf, cyf * dyf);
+                if (d2f > __fmaf_rn(mag, 1.220703125e-04f, 9.001f)) continue;
                 double dx = s.mx - px, dy = s.my - py;
                 double d2 = (s.ca * dx * dx + s.cb2 * dx * dy) + s.cc * dy * dy;
                 if (d2 > kSupportD2) continue;
-                double a = s.alpha * exp(-0.5 * d2);
+                double e;
+                SN_EXP_BLEND(d2 * -0.5, s_exp, e);
+                double a = s.alpha * e;
                 if (a > kAlphaClip) a = kAlphaClip;
                 double w = a * T;
-                float rgb[3];
-                unpack_rgb21(s.rgb, rgb);
                 float wf = (float)w;
-                cr = __fmaf_rn(rgb[0], wf, cr);
-                cg = __fmaf_rn(rgb[1], wf, cg);
-                cb = __fmaf_rn(rgb[2], wf, cb);
+                cr = __fmaf_rn(s.r, wf, cr);
+                cg = __fmaf_rn(s.g, wf, cg);
+                cb = __fmaf_rn(s.b, wf, cb);
                 A = A + w;
                 D = D + s.z * w;
                 T = T * (1.0 - a);
                 ++nc;
+                if (T < kTCutoff) break;  // T only falls on contributions (_kernels_cy.pyx:65-66)
             }
             done = T < kTCutoff;
         }
