@@ -137,68 +137,145 @@ __device__ __forceinline__ void load_scene(const sn_cloud &c, int64_t g, double 
     load4<T>(static_cast<const T *>(c.rotations) + 4 * g, q);
 }
 
+// Visible (gaussian, env) items of a warp, compacted per round of kEmitRound envs so the
+// float64 projection + SH run with full lanes (a scene gaussian is visible in ~1/4 of the envs;
+// walking envs per lane would leave ~3/4 of the lanes idle). Item = lane | env << 5 | rank << 11,
+// rank = position among the warp's visible lanes for that env (order-preserving output slot).
+constexpr int kEmitRound = 8;
+
+__device__ __forceinline__ int build_round(uint64_t mask, int e_begin, int e_end, uint16_t *q) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    int n = 0;
+    for (int e = e_begin; e < e_end; ++e) {
+        bool vis = (mask >> e) & 1ull;
+        unsigned bal = __ballot_sync(kFull, vis);
+        unsigned r = __popc(bal & lt);
+        if (vis) q[n + r] = (uint16_t)(lane | (e << 5) | (r << 11));
+        n += __popc(bal);
+    }
+    __syncwarp();
+    return n;
+}
+
+// Per-item stats with warp aggregation: lanes holding the same (env, field) add once.
+__device__ __forceinline__ void tally_item(unsigned (*s_cnt)[5], unsigned active, int e, int field) {
+    unsigned same = __match_any_sync(active, e * 8 + field);
+    int leader = __ffs(same) - 1;
+    if ((int)(threadIdx.x & 31) == leader) atomicAdd(&s_cnt[e][field], __popc(same));
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kBlock) scene_count_kernel(sn_cloud c, PrepArgs a) {
     __shared__ unsigned s_cnt[kMaxEnvChunk][5];
+    __shared__ double s_geo[kBlock][9];  // position (3), cov3d (6)
+    __shared__ unsigned long long s_vis[kBlock];
+    __shared__ uint16_t s_q[kBlock / 32][32 * kEmitRound];
     init_counts(s_cnt, a.ec);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     bool valid = g < c.n;
-    double p[3], ls[3], q[4], opacity, cov[6];
-    bool have_cov = false;
-    if (valid) load_scene<T>(c, g, p, ls, q, opacity);
-    uint64_t mask = 0;
+    double p[3] = {0.0, 0.0, 0.0};
+    if (valid) {
+        double ls[3], q[4], opacity, cov[6];
+        load_scene<T>(c, g, p, ls, q, opacity);
+        build_cov3d(ls, q, cov);
+        double *d = s_geo[threadIdx.x];
+        d[0] = p[0];
+        d[1] = p[1];
+        d[2] = p[2];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) d[3 + k] = cov[k];
+    }
+    s_vis[threadIdx.x] = 0ull;
+    // depth cull for every env (4 fp64 ops per env), then full geometry only for in-depth items
+    uint64_t in_depth = 0;
     for (int e = 0; e < a.ec; ++e) {
-        int code = -1;
+        bool in = false;
         if (valid) {
             const sn_camera &cam = a.cams[a.e0 + e];
             double z = cam_z(p, cam);
-            if (!((z > cam.near_) && (z < cam.far_))) {
-                code = kCullDepth;
-            } else {
-                if (!have_cov) {
-                    build_cov3d(ls, q, cov);
-                    have_cov = true;
-                }
-                Geo geo;
-                code = project_geo(p, cov, cam, geo);
-            }
-            if (code == kKeep) mask |= 1ull << e;
+            in = (z > cam.near_) && (z < cam.far_);
         }
-        tally(s_cnt, e, code, valid);
+        in_depth |= (uint64_t)in << e;
+        unsigned b_in = __ballot_sync(kFull, valid), b_out = __ballot_sync(kFull, valid && !in);
+        if (lane == 0) {
+            if (b_in) atomicAdd(&s_cnt[e][0], __popc(b_in));
+            if (b_out) atomicAdd(&s_cnt[e][1], __popc(b_out));
+        }
     }
-    if (valid) a.vismask[g] = mask;
+    const int64_t g0 = (int64_t)blockIdx.x * kBlock + warp * 32;
+    uint16_t *qq = s_q[warp];
+    for (int eb = 0; eb < a.ec; eb += kEmitRound) {
+        const int n = build_round(in_depth, eb, min(eb + kEmitRound, a.ec), qq);
+        for (int k0 = 0; k0 < n; k0 += 32) {
+            const int k = k0 + lane;
+            const unsigned active = __ballot_sync(kFull, k < n);
+            if (k >= n) continue;
+            const unsigned it = qq[k];
+            const int l = it & 31, e = (it >> 5) & 63;
+            const double *d = s_geo[warp * 32 + l];
+            const double pp[3] = {d[0], d[1], d[2]};
+            const double cov[6] = {d[3], d[4], d[5], d[6], d[7], d[8]};
+            Geo geo;
+            const int code = project_geo(pp, cov, a.cams[a.e0 + e], geo);
+            // field: 2 frame, 3 degenerate, 4 drawn (sn_stats order)
+            const int field = code == kKeep ? 4 : (code == kDegenerate ? 3 : 2);
+            tally_item(s_cnt, active, e, field);
+            if (code == kKeep) atomicOr(&s_vis[warp * 32 + l], 1ull << e);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    if (valid) a.vismask[g] = s_vis[threadIdx.x];
+    (void)g0;
     flush_counts(s_cnt, a);
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kBlock) scene_emit_kernel(sn_cloud c, PrepArgs a) {
     __shared__ unsigned s_woff[kMaxEnvChunk][kBlock / 32];
+    __shared__ double s_geo[kBlock][10];  // position (3), cov3d (6), alpha
+    __shared__ uint16_t s_q[kBlock / 32][32 * kEmitRound];
     int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     bool valid = g < c.n;
     uint64_t mask = valid ? a.vismask[g] : 0ull;
     warp_offsets(mask, a.ec, s_woff);
     if (!__any_sync(kFull, mask != 0)) return;
-    double p[3], ls[3], q[4], opacity, cov[6], alpha = 0.0;
+    const int warp = threadIdx.x >> 5;
     if (mask) {
+        double p[3], ls[3], q[4], opacity, cov[6];
         load_scene<T>(c, g, p, ls, q, opacity);
         build_cov3d(ls, q, cov);
-        alpha = sigmoid(opacity);
+        double *d = s_geo[threadIdx.x];
+        d[0] = p[0];
+        d[1] = p[1];
+        d[2] = p[2];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) d[3 + k] = cov[k];
+        d[9] = sigmoid(opacity);
     }
-    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned lt = (1u << lane) - 1u;
-    for (int e = 0; e < a.ec; ++e) {
-        bool vis = (mask >> e) & 1ull;
-        unsigned b = __ballot_sync(kFull, vis);
-        if (!vis) continue;
-        int64_t pos = (int64_t)a.env_off[e] + a.blk_counts[(int64_t)e * a.n_blocks + blockIdx.x] + s_woff[e][warp] +
-                      __popc(b & lt);
-        const sn_camera &cam = a.cams[a.e0 + e];
-        Geo geo;
-        project_geo(p, cov, cam, geo);
-        float d[3], rgb[3];
-        view_dir(p, cam, d);
-        eval_sh_f32(c.sh, c.n, g, c.sh_k, d[0], d[1], d[2], rgb);
-        write_splat(a, pos, e, geo, alpha, rgb, (uint32_t)g);
+    const int64_t g0 = (int64_t)blockIdx.x * kBlock + warp * 32;
+    uint16_t *q = s_q[warp];
+    for (int eb = 0; eb < a.ec; eb += kEmitRound) {
+        const int n = build_round(mask, eb, min(eb + kEmitRound, a.ec), q);
+        for (int k = threadIdx.x & 31; k < n; k += 32) {
+            const unsigned it = q[k];
+            const int l = it & 31, e = (it >> 5) & 63, rank = it >> 11;
+            const double *d = s_geo[warp * 32 + l];
+            const double p[3] = {d[0], d[1], d[2]};
+            const double cov[6] = {d[3], d[4], d[5], d[6], d[7], d[8]};
+            const int64_t pos =
+                (int64_t)a.env_off[e] + a.blk_counts[(int64_t)e * a.n_blocks + blockIdx.x] + s_woff[e][warp] + rank;
+            const sn_camera &cam = a.cams[a.e0 + e];
+            Geo geo;
+            project_geo(p, cov, cam, geo);
+            float dir[3], rgb[3];
+            view_dir(p, cam, dir);
+            eval_sh_f32(c.sh, c.n, g0 + l, c.sh_k, dir[0], dir[1], dir[2], rgb);
+            write_splat(a, pos, e, geo, d[9], rgb, (uint32_t)(g0 + l));
+        }
+        __syncwarp();
     }
 }
 
@@ -318,38 +395,40 @@ __global__ void __launch_bounds__(kBlock) avatar_count_kernel(sn_avatars av, Pos
 
 __global__ void __launch_bounds__(kBlock) avatar_emit_kernel(sn_avatars av, PoseView pv, PrepArgs a) {
     __shared__ unsigned s_woff[kMaxEnvChunk][kBlock / 32];
+    __shared__ uint16_t s_q[kBlock / 32][32 * kEmitRound];
     int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     bool valid = g < av.n;
     uint64_t mask = valid ? a.vismask[g] : 0ull;
     warp_offsets(mask, a.ec, s_woff);
     if (!__any_sync(kFull, mask != 0)) return;
-    int avatar = valid ? av.avatar_of[g] : 0;
-    double ls[4], alpha = 0.0;
-    if (mask) {
-        load4<double>(av.log_scales + 4 * g, ls);
-        alpha = sigmoid(__ldg(av.pos_opacity + 4 * g + 3));
-    }
-    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned lt = (1u << lane) - 1u;
-    for (int e = 0; e < a.ec; ++e) {
-        bool vis = (mask >> e) & 1ull;
-        unsigned b = __ballot_sync(kFull, vis);
-        if (!vis) continue;
-        int env = a.e0 + e;
-        int64_t pos = (int64_t)a.env_off[e] + a.blk_counts[(int64_t)e * a.n_blocks + blockIdx.x] + s_woff[e][warp] +
-                      __popc(b & lt);
-        const double *jm, *eq, *root;
-        pose_ptrs(pv, env, avatar, jm, eq, root);
-        double p[3], q[4], cov[6];
-        skin_one(av, g, jm, eq, root, p, q);
-        build_cov3d(ls, q, cov);
-        const sn_camera &cam = a.cams[env];
-        Geo geo;
-        project_geo(p, cov, cam, geo);
-        float d[3], rgb[3];
-        view_dir(p, cam, d);
-        eval_sh_f32(av.sh, av.n, g, av.sh_k, d[0], d[1], d[2], rgb);
-        write_splat(a, pos, e, geo, alpha, rgb, (uint32_t)g);
+    const int warp = threadIdx.x >> 5;
+    const int64_t g0 = (int64_t)blockIdx.x * kBlock + warp * 32;
+    uint16_t *q = s_q[warp];
+    for (int eb = 0; eb < a.ec; eb += kEmitRound) {
+        const int n = build_round(mask, eb, min(eb + kEmitRound, a.ec), q);
+        for (int k = threadIdx.x & 31; k < n; k += 32) {
+            const unsigned it = q[k];
+            const int l = it & 31, e = (it >> 5) & 63, rank = it >> 11;
+            const int64_t gi = g0 + l;
+            const int env = a.e0 + e;
+            const int avatar = av.avatar_of[gi];
+            const int64_t pos =
+                (int64_t)a.env_off[e] + a.blk_counts[(int64_t)e * a.n_blocks + blockIdx.x] + s_woff[e][warp] + rank;
+            const double *jm, *eq, *root;
+            pose_ptrs(pv, env, avatar, jm, eq, root);
+            double p[3], qr[4], ls[4], cov[6];
+            skin_one(av, gi, jm, eq, root, p, qr);
+            load4<double>(av.log_scales + 4 * gi, ls);
+            build_cov3d(ls, qr, cov);
+            const sn_camera &cam = a.cams[env];
+            Geo geo;
+            project_geo(p, cov, cam, geo);
+            float dir[3], rgb[3];
+            view_dir(p, cam, dir);
+            eval_sh_f32(av.sh, av.n, gi, av.sh_k, dir[0], dir[1], dir[2], rgb);
+            write_splat(a, pos, e, geo, sigmoid(__ldg(av.pos_opacity + 4 * gi + 3)), rgb, (uint32_t)gi);
+        }
+        __syncwarp();
     }
 }
 
