@@ -74,7 +74,7 @@ uint64_t dbits(double d) {
 }
 
 struct PassWs {
-    Buf vismask, blk_counts, env_off, keys_un, keys_s, vals_un, vals_s, recs_un, recs, gid_un, gid, rects_un, rects,
+    Buf vismask, blk_counts, env_off, keys_un, keys_s, vals_un, vals_s, recs_un, gid_un, rects_un, rects,
         tiles, pair_off, pkeys_a, pkeys_b, pvals_a, pvals_b, ranges, temp, batch_rects, super_rects;
     // metadata of the last chunk rendered by this pass
     int32_t e0 = 0, ec = 0, tiles_x = 0, tiles_y = 0, tile_bits = 0, tiled = 1, valid = 0, binning = 0;
@@ -153,6 +153,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     const int n_tiles = tiles_x * tiles_y;
     const int tile_bits = std::max(1, bit_length((uint64_t)(n_tiles - 1)));
     const int env_bits = bit_length((uint64_t)(ec - 1));
+    const int key_bits = z_bits + env_bits;
     const int32_t n_blocks = (int32_t)std::max<int64_t>(1, (n + kBlock - 1) / kBlock);
     // binning 1: materialized tile lists (duplicate + stable (env | tile) radix sort + ranges);
     // 0: no lists -- each blend CTA streams its env's depth-sorted rectangles and stops at
@@ -198,14 +199,12 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     }
     SN_CHECK(V < (int64_t)0xffffffffLL, "too many visible splats in one env chunk (limit 2^32)");
     const size_t v1 = (size_t)V + 1;
-    SN_ENSURE(w.keys_un, sizeof(uint64_t) * v1);
-    SN_ENSURE(w.keys_s, sizeof(uint64_t) * v1);
+    SN_ENSURE(w.keys_un, sizeof(uint32_t) * v1);
+    SN_ENSURE(w.keys_s, sizeof(uint32_t) * v1);
     SN_ENSURE(w.vals_un, sizeof(uint32_t) * v1);
     SN_ENSURE(w.vals_s, sizeof(uint32_t) * v1);
     SN_ENSURE(w.recs_un, sizeof(SplatRec) * v1);
-    SN_ENSURE(w.recs, sizeof(SplatRec) * v1);
     SN_ENSURE(w.gid_un, sizeof(uint32_t) * v1);
-    SN_ENSURE(w.gid, sizeof(uint32_t) * v1);
     SN_ENSURE(w.rects_un, sizeof(ushort4) * v1);
     SN_ENSURE(w.rects, sizeof(ushort4) * v1);
     SN_ENSURE(w.tiles, sizeof(uint32_t) * v1);
@@ -215,7 +214,8 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     SN_ENSURE(w.super_rects, sizeof(ushort4) * std::max<int64_t>((n_batches + kSuperBatch - 1) / kSuperBatch, 1));
 
     a.env_off = w.env_off.as<uint64_t>();
-    a.keys = w.keys_un.as<unsigned long long>();
+    a.keys = w.keys_un.as<uint32_t>();
+    a.key_shift = key_bits > 32 ? key_bits - 32 : 0;
     a.vals = w.vals_un.as<uint32_t>();
     a.recs = w.recs_un.as<SplatRec>();
     a.gid = w.gid_un.as<uint32_t>();
@@ -228,14 +228,11 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     b.tile_bits = tile_bits;
     b.z_bits = z_bits;
     b.n_vis = V;
-    b.keys_sorted = w.keys_s.as<unsigned long long>();
+    b.keys_sorted = w.keys_s.as<uint32_t>();
     b.vals_sorted = w.vals_s.as<uint32_t>();
-    b.recs_in = w.recs_un.as<SplatRec>();
-    b.gid_in = w.gid_un.as<uint32_t>();
+    b.recs_un = w.recs_un.as<SplatRec>();
     b.rects_in = w.rects_un.as<ushort4>();
     b.env_off = w.env_off.as<uint64_t>();
-    b.recs_out = w.recs.as<SplatRec>();
-    b.gid_out = w.gid.as<uint32_t>();
     b.rects_out = w.rects.as<ushort4>();
     b.batch_rects = w.batch_rects.as<ushort4>();
     b.tiles_touched = w.tiles.as<uint32_t>();
@@ -243,7 +240,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
 
     int64_t P = 0;
     if (V > 0) {
-        size_t tb = std::max(sort_u64_temp_bytes(V), scan_temp_bytes(V + 1));
+        size_t tb = std::max(sort_u32_temp_bytes(V), scan_temp_bytes(V + 1));
         SN_ENSURE(w.temp, tb);
         tm.begin(SN_STAGE_EMIT);
         if (sp.scene)
@@ -252,9 +249,10 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
             SN_CUDA(launch_avatar_emit(*sp.avatars, sp.pose, a, st));
         tm.end();
         tm.begin(SN_STAGE_DEPTH_SORT);
-        SN_CUDA(sort_u64_pairs(w.temp.p, w.temp.cap, w.keys_un.as<unsigned long long>(),
-                               w.keys_s.as<unsigned long long>(), w.vals_un.as<uint32_t>(), w.vals_s.as<uint32_t>(), V,
-                               z_bits + env_bits, st));
+        // 32-bit keys (env + top z bits) in 4 radix passes, then an exact fix of equal-key runs
+        SN_CUDA(sort_u32_pairs(w.temp.p, w.temp.cap, w.keys_un.as<uint32_t>(), w.keys_s.as<uint32_t>(),
+                               w.vals_un.as<uint32_t>(), w.vals_s.as<uint32_t>(), V, std::min(key_bits, 32), st));
+        if (key_bits > 32) SN_CUDA(launch_depth_tie_fix(b, st));
         tm.end();
         tm.begin(SN_STAGE_PERMUTE);
         SN_CUDA(launch_permute(b, st));
@@ -312,7 +310,8 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     bl.ranges = w.ranges.as<uint2>();
     bl.pair_vals = w.pvals_b.as<uint32_t>();
     bl.env_off = w.env_off.as<uint64_t>();
-    bl.recs = w.recs.as<SplatRec>();
+    bl.recs = w.recs_un.as<SplatRec>();
+    bl.order = w.vals_s.as<uint32_t>();
     bl.color = color;
     bl.alpha = alpha;
     bl.depth = depth;
@@ -402,7 +401,7 @@ int sn_context_destroy(sn_context *ctx) {
     };
     for (auto &w : ctx->pass) {
         for (Buf *b : {&w.vismask, &w.blk_counts, &w.env_off, &w.keys_un, &w.keys_s, &w.vals_un, &w.vals_s, &w.recs_un,
-                       &w.recs, &w.gid_un, &w.gid, &w.rects_un, &w.rects, &w.tiles, &w.pair_off, &w.pkeys_a,
+                       &w.gid_un, &w.rects_un, &w.rects, &w.tiles, &w.pair_off, &w.pkeys_a,
                        &w.pkeys_b, &w.pvals_a, &w.pvals_b, &w.ranges, &w.temp, &w.batch_rects, &w.super_rects})
             free_buf(*b);
     }
@@ -422,7 +421,7 @@ int sn_context_workspace_bytes(const sn_context *ctx, size_t *bytes) {
     size_t t = 0;
     for (const auto &w : ctx->pass)
         for (const Buf *b : {&w.vismask, &w.blk_counts, &w.env_off, &w.keys_un, &w.keys_s, &w.vals_un, &w.vals_s,
-                             &w.recs_un, &w.recs, &w.gid_un, &w.gid, &w.rects_un, &w.rects, &w.tiles, &w.pair_off,
+                             &w.recs_un, &w.gid_un, &w.rects_un, &w.rects, &w.tiles, &w.pair_off,
                              &w.pkeys_a, &w.pkeys_b, &w.pvals_a, &w.pvals_b, &w.ranges, &w.temp,
                              &w.batch_rects, &w.super_rects})
             t += b->cap;
@@ -622,7 +621,12 @@ int sn_get_sorted_ids(sn_context *ctx, int32_t pass, int32_t env, int32_t *ids_h
     if (r != SN_OK) return r;
     int64_t m = (int64_t)(off[el + 1] - off[el]);
     SN_CHECK(capacity >= m, "ids buffer too small");
-    if (m) SN_CUDA(cudaMemcpy(ids_host, w->gid.as<uint32_t>() + off[el], sizeof(int32_t) * m, cudaMemcpyDeviceToHost));
+    if (m) {
+        std::vector<uint32_t> order((size_t)m), gid((size_t)m);
+        SN_CUDA(cudaMemcpy(order.data(), w->vals_s.as<uint32_t>() + off[el], sizeof(uint32_t) * m, cudaMemcpyDeviceToHost));
+        SN_CUDA(cudaMemcpy(gid.data(), w->gid_un.as<uint32_t>() + off[el], sizeof(uint32_t) * m, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < m; ++i) ids_host[i] = (int32_t)gid[order[i] - off[el]];
+    }
     return SN_OK;
 }
 
@@ -654,9 +658,13 @@ int sn_get_projection(sn_context *ctx, int32_t pass, int32_t env, double *means2
     int64_t m = (int64_t)(off[el + 1] - off[el]);
     SN_CHECK(capacity >= m, "projection buffers too small");
     std::vector<SplatRec> recs((size_t)m);
-    if (m) SN_CUDA(cudaMemcpy(recs.data(), w->recs.as<SplatRec>() + off[el], sizeof(SplatRec) * m, cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> order((size_t)m);
+    if (m) {
+        SN_CUDA(cudaMemcpy(recs.data(), w->recs_un.as<SplatRec>() + off[el], sizeof(SplatRec) * m, cudaMemcpyDeviceToHost));
+        SN_CUDA(cudaMemcpy(order.data(), w->vals_s.as<uint32_t>() + off[el], sizeof(uint32_t) * m, cudaMemcpyDeviceToHost));
+    }
     for (int64_t i = 0; i < m; ++i) {
-        const SplatRec &s = recs[i];
+        const SplatRec &s = recs[order[i] - off[el]];
         means2d[2 * i] = s.mx;
         means2d[2 * i + 1] = s.my;
         conics[3 * i] = s.ca;

@@ -36,8 +36,9 @@ __device__ __forceinline__ ushort4 warp_rect_union(ushort4 r) {
     return r;
 }
 
-// Permutes records into depth order and writes each splat's tile rectangle, its tile count and,
-// per 256-splat batch (one CTA), the batch's union rectangle for the blend's cull.
+// Writes each depth-sorted splat's tile rectangle and tile count and, per 256-splat batch (one
+// CTA), the batch's union rectangle for the blend's cull. The 64-byte records themselves stay
+// where the emit wrote them: the blend gathers them through the sort's index.
 __global__ void __launch_bounds__(kBlock) permute_kernel(BinArgs b) {
     __shared__ ushort4 s_u[kBlock / 32];
     int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
@@ -52,15 +53,6 @@ __global__ void __launch_bounds__(kBlock) permute_kernel(BinArgs b) {
         b.batch_rects[blockIdx.x] = t;
     }
     if (i >= b.n_vis) return;
-    uint32_t slot = b.vals_sorted[i];
-    const uint4 *src = reinterpret_cast<const uint4 *>(b.recs_in + slot);
-    uint4 *dst = reinterpret_cast<uint4 *>(b.recs_out + i);
-    uint4 v0 = __ldg(src), v1 = __ldg(src + 1), v2 = __ldg(src + 2), v3 = __ldg(src + 3);
-    dst[0] = v0;
-    dst[1] = v1;
-    dst[2] = v2;
-    dst[3] = v3;
-    b.gid_out[i] = __ldg(b.gid_in + slot);
     ushort4 r = mine;
     b.rects_out[i] = r;
     b.tiles_touched[i] = (uint32_t)(r.y - r.x + 1) * (uint32_t)(r.w - r.z + 1);
@@ -80,7 +72,9 @@ __global__ void __launch_bounds__(kBlock) duplicate_kernel(BinArgs b) {
     if (t < cnt) {
         s_off[t] = b.pair_off[i];
         s_rect[t] = b.rects_out[i];
-        s_env[t] = (uint32_t)(b.keys_sorted[i] >> b.z_bits);
+        uint32_t e = 0;
+        while (e + 1 < (uint32_t)b.ec && b.env_off[e + 1] <= (uint64_t)i) ++e;
+        s_env[t] = e;
     }
     if (t == 0) s_off[cnt] = b.pair_off[i0 + cnt];
     __syncthreads();
@@ -124,7 +118,65 @@ __global__ void __launch_bounds__(kBlock) super_rects_kernel(const ushort4 *batc
     super_rects[sb] = t;
 }
 
+// The depth sort ran on 32-bit keys (env + top bits of z). Splats whose 32-bit keys tie are
+// re-ordered here by the full float64 z, then by slot (= original index, the emit writes in index
+// order): the exact np.lexsort((idx, z)) order. Runs are almost always 1-3 long; long runs
+// (pathological exact-depth planes) fall back to an in-place heap sort.
+__device__ __forceinline__ bool z_less(const SplatRec *recs, uint32_t a, uint32_t c) {
+    double za = recs[a].z, zc = recs[c].z;
+    return za < zc || (za == zc && a < c);
+}
+
+__global__ void __launch_bounds__(kBlock) tie_fix_kernel(BinArgs b) {
+    int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (i >= b.n_vis) return;
+    const uint32_t k = b.keys_sorted[i];
+    if (i > 0 && b.keys_sorted[i - 1] == k) return;  // not a run start
+    int64_t e = i + 1;
+    while (e < b.n_vis && b.keys_sorted[e] == k) ++e;
+    const int64_t L = e - i;
+    if (L < 2) return;
+    uint32_t *v = b.vals_sorted + i;
+    if (L <= 32) {
+        for (int64_t x = 1; x < L; ++x) {  // insertion sort
+            uint32_t cur = v[x];
+            int64_t y = x - 1;
+            while (y >= 0 && z_less(b.recs_un, cur, v[y])) {
+                v[y + 1] = v[y];
+                --y;
+            }
+            v[y + 1] = cur;
+        }
+        return;
+    }
+    // heap sort (max-heap by z_less)
+    auto sift = [&](int64_t root, int64_t end) {
+        while (2 * root + 1 < end) {
+            int64_t c = 2 * root + 1;
+            if (c + 1 < end && z_less(b.recs_un, v[c], v[c + 1])) ++c;
+            if (!z_less(b.recs_un, v[root], v[c])) return;
+            uint32_t t = v[root];
+            v[root] = v[c];
+            v[c] = t;
+            root = c;
+        }
+    };
+    for (int64_t r = L / 2 - 1; r >= 0; --r) sift(r, L);
+    for (int64_t end = L - 1; end > 0; --end) {
+        uint32_t t = v[0];
+        v[0] = v[end];
+        v[end] = t;
+        sift(0, end);
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_depth_tie_fix(const BinArgs &b, cudaStream_t s) {
+    if (b.n_vis == 0) return cudaSuccess;
+    tie_fix_kernel<<<(unsigned)((b.n_vis + kBlock - 1) / kBlock), kBlock, 0, s>>>(b);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_super_rects(const ushort4 *batch_rects, int64_t n_batches, ushort4 *super_rects, cudaStream_t s) {
     int64_t n_super = (n_batches + kSuperBatch - 1) / kSuperBatch;
@@ -150,20 +202,6 @@ cudaError_t launch_ranges(const uint32_t *keys_sorted, int64_t n_pairs, uint2 *r
     if (n_pairs == 0) return cudaSuccess;
     ranges_kernel<<<(unsigned)((n_pairs + kBlock - 1) / kBlock), kBlock, 0, s>>>(keys_sorted, n_pairs, ranges);
     return cudaGetLastError();
-}
-
-size_t sort_u64_temp_bytes(int64_t n) {
-    size_t bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const unsigned long long *)nullptr,
-                                    (unsigned long long *)nullptr, (const uint32_t *)nullptr, (uint32_t *)nullptr,
-                                    (int64_t)n, 0, 64);
-    return bytes;
-}
-
-cudaError_t sort_u64_pairs(void *temp, size_t temp_bytes, const unsigned long long *k_in, unsigned long long *k_out,
-                           const uint32_t *v_in, uint32_t *v_out, int64_t n, int bits, cudaStream_t s) {
-    if (n == 0) return cudaSuccess;
-    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k_in, k_out, v_in, v_out, n, 0, bits, s);
 }
 
 size_t sort_u32_temp_bytes(int64_t n) {

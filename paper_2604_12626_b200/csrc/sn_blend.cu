@@ -42,21 +42,22 @@ __constant__ double kExp2Tbl[64] = {
     1.8539791250833855, 1.8741676341103, 1.8945759815869656, 1.9152065613971474, 1.9360617934922943,
     1.9571441241754002, 1.978456026387951};
 
-// exp(x) for the blend's argument range x = -d2/2, d2 in [~0, 9]: 2^(n/64) * e^r with a 64-entry
-// table in shared memory and a degree-5 polynomial, |r| <= ln2/128 (+ the slack of a 21-bit scale).
-// Max error 2 ulp (numpy's, libm's and CUDA's exp also differ by ulps). Constants whose low word is
-// zero encode as instruction immediates, so the loop does not re-materialize them.
-#define SN_EXP_BLEND(x, tbl, out)                                                                  \
+// e^(-d2/2) for the blend's argument range d2 in [~0, 9]: 2^(n/64) * e^r with a 64-entry table in
+// shared memory and a degree-5 polynomial in r2 = 2r, |r| <= ln2/128 (+ the slack of a 21-bit
+// scale). The -1/2 is folded into the reduction (exact power-of-two scaling). Max error 2 ulp
+// (numpy's, libm's and CUDA's exp also differ by ulps). Constants whose low word is zero encode as
+// instruction immediates; only ln2/32-lo and 1/48 need full 64-bit operands.
+#define SN_EXP_NEG_HALF(d2, tbl, out)                                                              \
     do {                                                                                           \
-        const double _t = fma((x), 92.33245849609375, 6755399441055744.0); /* ~64/ln2 (21 bits), 1.5*2^52 */ \
+        const double _t = fma((d2), -46.166229248046875, 6755399441055744.0);                     \
         const int _n = __double2loint(_t);                                                         \
         const double _nd = _t - 6755399441055744.0;                                                \
-        double _r = fma(_nd, -0.010830417275428772, (x)); /* ln2/64 hi: 21 bits */                                           \
-        _r = fma(_nd, -7.420820373486988e-09, _r);                                                \
-        double _p = fma(_r, 0.008333333333333333, 0.041666666666666664);                           \
-        _p = fma(_p, _r, 0.16666666666666666);                                                     \
+        double _r = fma(_nd, -0.021660834550857544, -(d2));                                       \
+        _r = fma(_nd, -1.4841640746973977e-08, _r);                                                \
+        double _p = fma(_r, 0.00026041665114462376, 0.0026041660457849503);                       \
+        _p = fma(_p, _r, 0.020833333333333332);                                                    \
+        _p = fma(_p, _r, 0.125);                                                                   \
         _p = fma(_p, _r, 0.5);                                                                     \
-        _p = fma(_p, _r, 1.0);                                                                     \
         _p = fma(_p, _r, 1.0);                                                                     \
         const double _v = (tbl)[_n & 63] * _p;                                                     \
         (out) = __hiloint2double(__double2hiint(_v) + ((_n >> 6) << 20), __double2loint(_v));    \
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(kBlock) blend_kernel(BlendArgs b) {
         if (threadIdx.x < n) {
             uint32_t rid = SOURCE == 0 ? s_queue[threadIdx.x]
                                        : (SOURCE == 1 ? __ldg(b.pair_vals + cursor + threadIdx.x) : cursor + threadIdx.x);
-            const double2 *src = reinterpret_cast<const double2 *>(b.recs + rid);
+            const double2 *src = reinterpret_cast<const double2 *>(b.recs + __ldg(b.order + rid));
             double2 m = __ldg(src), c01 = __ldg(src + 1), c2a = __ldg(src + 2), zr = __ldg(src + 3);
             BlendRec &d = s_rec[threadIdx.x];
             d.mxr = (float)(m.x - x0);
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(kBlock) blend_kernel(BlendArgs b) {
                 double d2 = (s.ca * dx * dx + s.cb2 * dx * dy) + s.cc * dy * dy;
                 if (d2 > kSupportD2) continue;
                 double e;
-                SN_EXP_BLEND(d2 * -0.5, s_exp, e);
+                SN_EXP_NEG_HALF(d2, s_exp, e);
                 double a = s.alpha * e;
                 if (a > kAlphaClip) a = kAlphaClip;
                 double w = a * T;

@@ -33,7 +33,8 @@ struct PrepArgs {
     const uint8_t *avatar_active;  // (E, A), avatars only, may be null
     // emit outputs (unsorted, env-major, index order within env)
     const uint64_t *env_off;  // (ec + 1)
-    unsigned long long *keys;  // depth keys
+    uint32_t *keys;            // 32-bit depth keys: top bits of (env << z_bits | z_bits - z_base)
+    int32_t key_shift;         // right shift that turns the 64-bit key into the 32-bit one
     uint32_t *vals;            // identity positions
     SplatRec *recs;
     uint32_t *gid;
@@ -63,14 +64,11 @@ cudaError_t launch_joint_prep(const sn_avatars &av, int32_t avatar, const double
 struct BinArgs {
     int32_t ec, tiles_x, tiles_y, tile_bits, z_bits;
     int64_t n_vis;
-    const unsigned long long *keys_sorted;
-    const uint32_t *vals_sorted;
-    const SplatRec *recs_in;
-    const uint32_t *gid_in;
+    const uint32_t *keys_sorted;   // 32-bit depth keys after the sort
+    uint32_t *vals_sorted;         // depth order -> unsorted record slot (tie-fixed in place)
+    const SplatRec *recs_un;       // unsorted records (z for the tie fix)
     const ushort4 *rects_in;
     const uint64_t *env_off;
-    SplatRec *recs_out;
-    uint32_t *gid_out;
     ushort4 *rects_out;
     ushort4 *batch_rects;    // (ceil(n_vis / 256)) union rect per 256-splat batch
     uint32_t *tiles_touched;
@@ -81,12 +79,10 @@ struct BinArgs {
 };
 constexpr int kSuperBatch = 32;  // batches per super-batch (8192 splats)
 cudaError_t launch_permute(const BinArgs &b, cudaStream_t s);
+cudaError_t launch_depth_tie_fix(const BinArgs &b, cudaStream_t s);
 cudaError_t launch_super_rects(const ushort4 *batch_rects, int64_t n_batches, ushort4 *super_rects, cudaStream_t s);
 cudaError_t launch_duplicate(const BinArgs &b, cudaStream_t s);
 cudaError_t launch_ranges(const uint32_t *keys_sorted, int64_t n_pairs, uint2 *ranges, cudaStream_t s);
-size_t sort_u64_temp_bytes(int64_t n);
-cudaError_t sort_u64_pairs(void *temp, size_t temp_bytes, const unsigned long long *k_in, unsigned long long *k_out,
-                           const uint32_t *v_in, uint32_t *v_out, int64_t n, int bits, cudaStream_t s);
 size_t sort_u32_temp_bytes(int64_t n);
 cudaError_t sort_u32_pairs(void *temp, size_t temp_bytes, const uint32_t *k_in, uint32_t *k_out, const uint32_t *v_in,
                            uint32_t *v_out, int64_t n, int bits, cudaStream_t s);
@@ -107,7 +103,8 @@ struct BlendArgs {
     const uint2 *ranges;
     const uint32_t *pair_vals;
     const uint64_t *env_off;
-    const SplatRec *recs;
+    const SplatRec *recs;   // unsorted records
+    const uint32_t *order;  // depth-sorted index -> record slot
     float *color, *alpha, *depth;  // (E,H,W,[3]) outputs, indexed by global env
     double *depth64;        // scene pass: exact depth for the compositor (may be null)
     int32_t *contrib;       // (E,H,W) may be null

@@ -110,7 +110,7 @@ __device__ __forceinline__ void write_splat(const PrepArgs &a, int64_t pos, int 
     r.rgb = pack_rgb21(rgb);
     a.recs[pos] = r;
     unsigned long long zb = (unsigned long long)__double_as_longlong(geo.z);
-    a.keys[pos] = ((unsigned long long)e << a.z_bits) | (zb - a.z_base);
+    a.keys[pos] = (uint32_t)((((unsigned long long)e << a.z_bits) | (zb - a.z_base)) >> a.key_shift);
     a.vals[pos] = (uint32_t)pos;
     a.gid[pos] = gid;
     int rect[4];
