@@ -134,8 +134,11 @@ typedef struct sn_render_opts {
     int32_t *contrib_layer; /* device (E,H,W): avatar-layer pass */
     sn_stats *stats;        /* device (E): RenderStats accumulated over both passes */
     double *stage_ms;       /* HOST (2 x SN_N_STAGES): GPU ms per stage (CUDA events), accumulated */
-    int64_t *work;          /* HOST (2 x 4): visible splats, tile pairs, records gathered by the
-                               blend, rectangles the blend examined -- per pass, accumulated */
+    int64_t *work;          /* HOST (2 x 4): visible splats, tile pairs (when computed), records
+                               gathered by the blend, rectangles the blend examined -- per pass,
+                               accumulated. Both arrays are filled asynchronously: they are complete
+                               after the next sn_render on the context or sn_context_sync_stats(),
+                               and must stay valid until then. */
 } sn_render_opts;
 
 typedef struct sn_context sn_context;
@@ -146,6 +149,8 @@ const char *sn_last_error(void);
 /* One context per (device, thread). Owns the workspace; grows it on demand. */
 int sn_context_create(sn_context **ctx);
 int sn_context_destroy(sn_context *ctx);
+/* Folds pending stage timings / work counters into the arrays last passed in sn_render_opts. */
+int sn_context_sync_stats(sn_context *ctx);
 /* Bytes of device workspace currently held. */
 int sn_context_workspace_bytes(const sn_context *ctx, size_t *bytes);
 

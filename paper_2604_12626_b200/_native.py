@@ -61,6 +61,7 @@ STAGES = ("pose", "count", "scan", "emit", "depth_sort", "permute", "pair_scan",
 # every symbol include/splatnav_b200.h declares (tests check the library exports all of them)
 EXPORTS = (
     "sn_abi_version", "sn_last_error", "sn_context_create", "sn_context_destroy", "sn_context_workspace_bytes",
+    "sn_context_sync_stats",
     "sn_render", "sn_get_counts", "sn_get_sorted_ids", "sn_get_tile_csr", "sn_get_projection", "sn_sample_pose",
     "sn_skin_lbs", "sn_blend_tile_range", "sn_composite",
 )
@@ -88,6 +89,7 @@ def load():
             "sn_context_create": ([ctypes.POINTER(P)], ctypes.c_int),
             "sn_context_destroy": ([P], ctypes.c_int),
             "sn_context_workspace_bytes": ([P, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
+            "sn_context_sync_stats": ([P], ctypes.c_int),
             "sn_render": ([P, ctypes.POINTER(SnCloud), ctypes.POINTER(SnCloud), ctypes.POINTER(SnAvatars), P, P, i32,
                            ctypes.POINTER(SnRenderOpts), P, P, P, P], ctypes.c_int),
             "sn_get_counts": ([P, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)], ctypes.c_int),
@@ -135,6 +137,9 @@ class Context:
             except Exception:
                 pass
             self.handle = None
+
+    def sync_stats(self):
+        check(self._lib.sn_context_sync_stats(self.handle))
 
     def workspace_bytes(self):
         v = ctypes.c_size_t()

@@ -88,44 +88,59 @@ struct sn_context {
     Buf cams, times, depth64, jm, eq, root, err, pose_q, pose_t, loads;
     uint64_t *h_tot = nullptr;  // pinned
     int32_t *h_err = nullptr;   // pinned
-    cudaEvent_t ev[2 * SN_N_STAGES] = {};
+    uint64_t *h_work = nullptr; // pinned (2 passes x 2 counters)
+    // lazily resolved instrumentation: CUDA events per (pass, stage) and the blend's counters,
+    // folded into the caller's arrays at the next sn_render / sn_context_sync_stats, so timing
+    // adds no host synchronization inside a render
+    cudaEvent_t ev[2][SN_N_STAGES][2] = {};
+    cudaEvent_t ev_work[2] = {};
+    double *ms_dst[2][SN_N_STAGES] = {};
+    int64_t *work_dst[2] = {};
     bool have_events = false;
 };
 
 namespace {
 
+void resolve_stage(sn_context *ctx, int pass, int stage) {
+    double *dst = ctx->ms_dst[pass][stage];
+    if (!dst) return;
+    cudaEventSynchronize(ctx->ev[pass][stage][1]);
+    float t = 0.0f;
+    if (cudaEventElapsedTime(&t, ctx->ev[pass][stage][0], ctx->ev[pass][stage][1]) == cudaSuccess) *dst += t;
+    ctx->ms_dst[pass][stage] = nullptr;
+}
+
+void resolve_all(sn_context *ctx) {
+    for (int p = 0; p < 2; ++p) {
+        for (int s = 0; s < SN_N_STAGES; ++s) resolve_stage(ctx, p, s);
+        if (ctx->work_dst[p]) {
+            cudaEventSynchronize(ctx->ev_work[p]);
+            ctx->work_dst[p][2] += (int64_t)ctx->h_work[2 * p];
+            ctx->work_dst[p][3] += (int64_t)ctx->h_work[2 * p + 1];
+            ctx->work_dst[p] = nullptr;
+        }
+    }
+}
+
 // Stage timer: CUDA events around each stage on the render stream (only when requested).
-// Elapsed times are resolved in flush() once the pass is queued, so timing adds no host sync
-// between stages beyond the ones the pass already has.
 struct StageTimer {
     sn_context *ctx;
     cudaStream_t st;
     double *ms;  // host (SN_N_STAGES) for this pass, or null
+    int pass;
     int open = -1;
-    bool pending[SN_N_STAGES] = {};
     void begin(int stage) {
         if (!ms) return;
-        if (pending[stage]) flush();
+        resolve_stage(ctx, pass, stage);  // the event pair is about to be reused (multi-chunk renders)
         open = stage;
-        cudaEventRecord(ctx->ev[2 * stage], st);
+        cudaEventRecord(ctx->ev[pass][stage][0], st);
     }
     void end() {
         if (!ms || open < 0) return;
-        cudaEventRecord(ctx->ev[2 * open + 1], st);
-        pending[open] = true;
+        cudaEventRecord(ctx->ev[pass][open][1], st);
+        ctx->ms_dst[pass][open] = ms + open;
         open = -1;
     }
-    void flush() {
-        if (!ms) return;
-        for (int s = 0; s < SN_N_STAGES; ++s) {
-            if (!pending[s]) continue;
-            cudaEventSynchronize(ctx->ev[2 * s + 1]);
-            float t = 0.0f;
-            if (cudaEventElapsedTime(&t, ctx->ev[2 * s], ctx->ev[2 * s + 1]) == cudaSuccess) ms[s] += t;
-            pending[s] = false;
-        }
-    }
-    ~StageTimer() { flush(); }
 };
 
 }  // namespace
@@ -146,7 +161,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
              uint64_t z_base, int z_bits, const sn_render_opts *opts, float *color, float *alpha, float *depth,
              double *depth64, cudaStream_t st) {
     PassWs &w = ctx->pass[pass_id];
-    StageTimer tm{ctx, st, opts && opts->stage_ms ? opts->stage_ms + pass_id * SN_N_STAGES : nullptr};
+    StageTimer tm{ctx, st, opts && opts->stage_ms ? opts->stage_ms + pass_id * SN_N_STAGES : nullptr, pass_id};
     int64_t *work = opts && opts->work ? opts->work + pass_id * 4 : nullptr;
     const int64_t n = sp.scene ? sp.scene->n : sp.avatars->n;
     const int tiles_x = tiles_of(width), tiles_y = tiles_of(height);
@@ -258,7 +273,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
         SN_CUDA(launch_permute(b, st));
         SN_CUDA(launch_super_rects(w.batch_rects.as<ushort4>(), n_batches, w.super_rects.as<ushort4>(), st));
         tm.end();
-        if (tiled && (binning == 1 || work)) {  // pair offsets: the radix binner emits from them
+        if (tiled && binning == 1) {  // pair offsets: the radix binner emits from them
             SN_CUDA(cudaMemsetAsync(w.tiles.as<uint32_t>() + V, 0, sizeof(uint32_t), st));
             tm.begin(SN_STAGE_PAIR_SCAN);
             SN_CUDA(scan_tiles(w.temp.p, w.temp.cap, w.tiles.as<uint32_t>(), w.pair_off.as<uint64_t>(), V + 1, st));
@@ -318,21 +333,26 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     bl.depth64 = depth64;
     bl.contrib = opts ? (pass_id == 0 ? opts->contrib_scene : opts->contrib_layer) : nullptr;
     if (work) {
-        SN_ENSURE(ctx->loads, 2 * sizeof(unsigned long long));
-        SN_CUDA(cudaMemsetAsync(ctx->loads.p, 0, 2 * sizeof(unsigned long long), st));
-        bl.loads = ctx->loads.as<unsigned long long>();
+        if (ctx->work_dst[pass_id]) {  // previous chunk's counters still in flight
+            cudaEventSynchronize(ctx->ev_work[pass_id]);
+            ctx->work_dst[pass_id][2] += (int64_t)ctx->h_work[2 * pass_id];
+            ctx->work_dst[pass_id][3] += (int64_t)ctx->h_work[2 * pass_id + 1];
+            ctx->work_dst[pass_id] = nullptr;
+        }
+        SN_ENSURE(ctx->loads, 4 * sizeof(unsigned long long));
+        bl.loads = ctx->loads.as<unsigned long long>() + 2 * pass_id;
         bl.scans = bl.loads + 1;
+        SN_CUDA(cudaMemsetAsync(bl.loads, 0, 2 * sizeof(unsigned long long), st));
     }
     tm.begin(SN_STAGE_BLEND);
     SN_CUDA(launch_blend(bl, st));
     tm.end();
     if (work) {
-        SN_CUDA(cudaMemcpyAsync(ctx->h_tot + 1, ctx->loads.p, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-        SN_CUDA(cudaStreamSynchronize(st));
+        SN_CUDA(cudaMemcpyAsync(ctx->h_work + 2 * pass_id, bl.loads, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        SN_CUDA(cudaEventRecord(ctx->ev_work[pass_id], st));
+        ctx->work_dst[pass_id] = work;
         work[0] += V;
         work[1] += P;
-        work[2] += (int64_t)ctx->h_tot[1];
-        work[3] += (int64_t)ctx->h_tot[2];
     }
 
     w.e0 = e0;
@@ -384,6 +404,7 @@ int sn_context_create(sn_context **out) {
     sn_context *ctx = new sn_context();
     cudaError_t e = cudaMallocHost(&ctx->h_tot, sizeof(uint64_t) * 4);
     if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_err, sizeof(int32_t) * 4);
+    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_work, sizeof(uint64_t) * 4);
     if (e != cudaSuccess) {
         delete ctx;
         return fail(SN_ERR_CUDA, std::string("cudaMallocHost: ") + cudaGetErrorString(e));
@@ -408,11 +429,22 @@ int sn_context_destroy(sn_context *ctx) {
     for (Buf *b : {&ctx->cams, &ctx->times, &ctx->depth64, &ctx->jm, &ctx->eq, &ctx->root, &ctx->err, &ctx->pose_q,
                    &ctx->pose_t, &ctx->loads})
         free_buf(*b);
-    if (ctx->have_events)
-        for (auto &ev : ctx->ev) cudaEventDestroy(ev);
+    if (ctx->have_events) {
+        for (auto &p : ctx->ev)
+            for (auto &st2 : p)
+                for (auto &ev : st2) cudaEventDestroy(ev);
+        for (auto &ev : ctx->ev_work) cudaEventDestroy(ev);
+    }
+    if (ctx->h_work) cudaFreeHost(ctx->h_work);
     if (ctx->h_tot) cudaFreeHost(ctx->h_tot);
     if (ctx->h_err) cudaFreeHost(ctx->h_err);
     delete ctx;
+    return SN_OK;
+}
+
+int sn_context_sync_stats(sn_context *ctx) {
+    SN_CHECK(ctx != nullptr, "null context");
+    resolve_all(ctx);
     return SN_OK;
 }
 
@@ -471,8 +503,12 @@ int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, con
     const int free_bits = 64 - z_bits;
     const int chunk = free_bits >= 6 ? kMaxEnvChunk : (1 << free_bits);
     const int tiled = opts ? opts->tiled : 1;
-    if (opts && opts->stage_ms && !ctx->have_events) {
-        for (auto &ev : ctx->ev) SN_CUDA(cudaEventCreate(&ev));
+    resolve_all(ctx);
+    if (opts && (opts->stage_ms || opts->work) && !ctx->have_events) {
+        for (auto &p : ctx->ev)
+            for (auto &st2 : p)
+                for (auto &ev : st2) SN_CUDA(cudaEventCreate(&ev));
+        for (auto &ev : ctx->ev_work) SN_CUDA(cudaEventCreate(&ev));
         ctx->have_events = true;
     }
 
@@ -515,7 +551,7 @@ int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, con
     SN_ENSURE(ctx->root, sizeof(double) * (size_t)n_envs * A * 12);
     SN_ENSURE(ctx->err, sizeof(int32_t));
     SN_CUDA(cudaMemsetAsync(ctx->err.p, 0, sizeof(int32_t), st));
-    StageTimer ptm{ctx, st, opts && opts->stage_ms ? opts->stage_ms + SN_N_STAGES : nullptr};
+    StageTimer ptm{ctx, st, opts && opts->stage_ms ? opts->stage_ms + SN_N_STAGES : nullptr, 1};
     ptm.begin(SN_STAGE_POSE);
     SN_CUDA(launch_pose(*avatars, ctx->times.as<double>(), n_envs, nullptr, nullptr, ctx->jm.as<double>(),
                         ctx->eq.as<double>(), ctx->root.as<double>(), ctx->err.as<int32_t>(), st));

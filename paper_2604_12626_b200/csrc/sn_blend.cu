@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kBlock) blend_kernel(BlendArgs b) {
                 cg = __fmaf_rn(s.g, wf, cg);
                 cb = __fmaf_rn(s.b, wf, cb);
                 A = A + w;
-                D = D + s.z * w;
+                D = fma(s.z, w, D);  // one rounding instead of two: ulp-level, inside the depth tolerance
                 T = T * (1.0 - a);
                 ++nc;
                 if (T < kTCutoff) break;  // T only falls on contributions (_kernels_cy.pyx:65-66)
