@@ -134,9 +134,9 @@ typedef struct sn_render_opts {
     int32_t *contrib_layer; /* device (E,H,W): avatar-layer pass */
     sn_stats *stats;        /* device (E): RenderStats accumulated over both passes */
     double *stage_ms;       /* HOST (2 x SN_N_STAGES): GPU ms per stage (CUDA events), accumulated */
-    int64_t *work;          /* HOST (2 x 4): visible splats, tile pairs (when computed), records
-                               gathered by the blend, rectangles the blend examined -- per pass,
-                               accumulated. Both arrays are filled asynchronously: they are complete
+    int64_t *work;          /* HOST (2 x 6): visible splats, tile pairs (when lists are built),
+                               records gathered by the blend, rectangles the blend examined,
+                               (pixel, splat) contributions, unused -- per pass, accumulated. Both arrays are filled asynchronously: they are complete
                                after the next sn_render on the context or sn_context_sync_stats(),
                                and must stay valid until then. */
 } sn_render_opts;

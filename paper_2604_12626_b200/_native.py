@@ -11,7 +11,7 @@ import threading
 from .errors import ContractViolation, NativeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsplatnav_b200.so")
+LIB_PATH = os.environ.get("SPLATNAV_B200_LIB") or os.path.join(_HERE, "libsplatnav_b200.so")
 
 SN_OK, SN_ERR_INVALID, SN_ERR_CUDA, SN_ERR_NOMEM = 0, 1, 2, 3
 SN_FLOAT32, SN_FLOAT64 = 0, 1

@@ -49,6 +49,58 @@ class BatchRenderer:
         return host_out
 
 
+class HostPipeline:
+    """Render batches straight into pinned host memory with the device->host copies of batch i
+    overlapped with the render of batch i+1 (double-buffered, separate copy stream).
+
+    submit(cameras, sim_times) -> slot index; the frames of a slot are valid in host[slot] after
+    wait(slot) (or after the slot is reused two submits later, which waits for it)."""
+
+    KEYS = ("color", "alpha", "depth")
+
+    def __init__(self, renderer, n_envs, height, width, depth=2):
+        self.r = renderer
+        dev = renderer.device
+        # renders on their own stream, not the legacy default stream (whose implicit
+        # synchronization would serialize them with the copies)
+        self.render_stream = torch.cuda.Stream(dev)
+        self.copy_stream = torch.cuda.Stream(dev)
+        shapes = {"color": (n_envs, height, width, 3), "alpha": (n_envs, height, width),
+                  "depth": (n_envs, height, width)}
+        self.host = [{k: torch.empty(shapes[k], dtype=torch.float32, pin_memory=True) for k in self.KEYS}
+                     for _ in range(depth)]
+        self.done = [None] * depth
+        self.keep = [None] * depth
+        self.i = 0
+
+    def submit(self, cameras, sim_times=None):
+        slot = self.i % len(self.host)
+        self.i += 1
+        if self.done[slot] is not None:
+            self.done[slot].synchronize()  # host buffer of this slot is free again
+        with torch.cuda.stream(self.render_stream):
+            out = self.r.render(cameras, sim_times)
+            ready = torch.cuda.Event()
+            ready.record(self.render_stream)
+        with torch.cuda.stream(self.copy_stream):
+            self.copy_stream.wait_event(ready)
+            for k in self.KEYS:
+                self.host[slot][k].copy_(out[k], non_blocking=True)
+                out[k].record_stream(self.copy_stream)
+            ev = torch.cuda.Event()
+            ev.record(self.copy_stream)
+        self.done[slot] = ev
+        self.keep[slot] = out
+        return slot
+
+    def wait(self, slot=None):
+        for i, ev in enumerate(self.done):
+            if ev is not None and (slot is None or i == slot):
+                ev.synchronize()
+                torch.cuda.current_stream(self.r.device).wait_event(ev)
+        return self.host[slot] if slot is not None else None
+
+
 def quantize_observation(color, depth):
     """uint8 RGB (x*255+0.5, frame_io.py:13-14) + fp16 depth, the gather payload."""
     rgb = (color.clamp(0.0, 1.0) * 255.0 + 0.5).to(torch.uint8)

@@ -86,14 +86,23 @@ struct PassWs {
 struct sn_context {
     PassWs pass[2];
     Buf cams, times, depth64, jm, eq, root, err, pose_q, pose_t, loads;
-    uint64_t *h_tot = nullptr;  // pinned
-    int32_t *h_err = nullptr;   // pinned
-    uint64_t *h_work = nullptr; // pinned (2 passes x 2 counters)
+    // mapped pinned words the device writes with a one-thread kernel: reading a total this way
+    // never queues behind other streams' bulk copies on the device->host copy engine
+    uint64_t *h_tot = nullptr, *d_tot = nullptr;
+    int32_t *h_err = nullptr, *d_err = nullptr;
+    uint64_t *h_work = nullptr; // pinned (2 passes x 3 counters)
+    // pinned staging for the per-call host inputs: a pageable cudaMemcpyAsync would serialize
+    // with copies other streams have in flight (e.g. the caller's frame downloads)
+    void *h_stage = nullptr;
+    size_t h_stage_cap = 0;
     // lazily resolved instrumentation: CUDA events per (pass, stage) and the blend's counters,
     // folded into the caller's arrays at the next sn_render / sn_context_sync_stats, so timing
     // adds no host synchronization inside a render
     cudaEvent_t ev[2][SN_N_STAGES][2] = {};
     cudaEvent_t ev_work[2] = {};
+    // side stream for the layer pass: its preprocessing overlaps the scene blend
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_inputs = nullptr, ev_scene = nullptr, ev_layer = nullptr;
     double *ms_dst[2][SN_N_STAGES] = {};
     int64_t *work_dst[2] = {};
     bool have_events = false;
@@ -115,8 +124,9 @@ void resolve_all(sn_context *ctx) {
         for (int s = 0; s < SN_N_STAGES; ++s) resolve_stage(ctx, p, s);
         if (ctx->work_dst[p]) {
             cudaEventSynchronize(ctx->ev_work[p]);
-            ctx->work_dst[p][2] += (int64_t)ctx->h_work[2 * p];
-            ctx->work_dst[p][3] += (int64_t)ctx->h_work[2 * p + 1];
+            ctx->work_dst[p][2] += (int64_t)ctx->h_work[3 * p];
+            ctx->work_dst[p][3] += (int64_t)ctx->h_work[3 * p + 1];
+            ctx->work_dst[p][4] += (int64_t)ctx->h_work[3 * p + 2];
             ctx->work_dst[p] = nullptr;
         }
     }
@@ -159,10 +169,10 @@ struct PassSpec {
 
 int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, int width, int height, int tiled,
              uint64_t z_base, int z_bits, const sn_render_opts *opts, float *color, float *alpha, float *depth,
-             double *depth64, cudaStream_t st) {
+             double *depth64, cudaStream_t st, cudaEvent_t blend_wait = nullptr) {
     PassWs &w = ctx->pass[pass_id];
     StageTimer tm{ctx, st, opts && opts->stage_ms ? opts->stage_ms + pass_id * SN_N_STAGES : nullptr, pass_id};
-    int64_t *work = opts && opts->work ? opts->work + pass_id * 4 : nullptr;
+    int64_t *work = opts && opts->work ? opts->work + pass_id * 6 : nullptr;
     const int64_t n = sp.scene ? sp.scene->n : sp.avatars->n;
     const int tiles_x = tiles_of(width), tiles_y = tiles_of(height);
     const int n_tiles = tiles_x * tiles_y;
@@ -208,7 +218,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
         tm.begin(SN_STAGE_SCAN);
         SN_CUDA(launch_block_scan(a.blk_counts, n_blocks, ec, w.env_off.as<uint64_t>(), st));
         tm.end();
-        SN_CUDA(cudaMemcpyAsync(ctx->h_tot, w.env_off.as<uint64_t>() + ec, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        SN_CUDA(launch_publish_u64(w.env_off.as<uint64_t>() + ec, ctx->d_tot, st));
         SN_CUDA(cudaStreamSynchronize(st));
         V = (int64_t)ctx->h_tot[0];
     }
@@ -278,8 +288,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
             tm.begin(SN_STAGE_PAIR_SCAN);
             SN_CUDA(scan_tiles(w.temp.p, w.temp.cap, w.tiles.as<uint32_t>(), w.pair_off.as<uint64_t>(), V + 1, st));
             tm.end();
-            SN_CUDA(cudaMemcpyAsync(ctx->h_tot, w.pair_off.as<uint64_t>() + V, sizeof(uint64_t),
-                                    cudaMemcpyDeviceToHost, st));
+            SN_CUDA(launch_publish_u64(w.pair_off.as<uint64_t>() + V, ctx->d_tot, st));
             SN_CUDA(cudaStreamSynchronize(st));
             P = (int64_t)ctx->h_tot[0];
             SN_CHECK(P < (int64_t)0x7fffffffLL, "too many tile pairs in one env chunk (limit 2^31)");
@@ -335,20 +344,23 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     if (work) {
         if (ctx->work_dst[pass_id]) {  // previous chunk's counters still in flight
             cudaEventSynchronize(ctx->ev_work[pass_id]);
-            ctx->work_dst[pass_id][2] += (int64_t)ctx->h_work[2 * pass_id];
-            ctx->work_dst[pass_id][3] += (int64_t)ctx->h_work[2 * pass_id + 1];
+            ctx->work_dst[pass_id][2] += (int64_t)ctx->h_work[3 * pass_id];
+            ctx->work_dst[pass_id][3] += (int64_t)ctx->h_work[3 * pass_id + 1];
+            ctx->work_dst[pass_id][4] += (int64_t)ctx->h_work[3 * pass_id + 2];
             ctx->work_dst[pass_id] = nullptr;
         }
-        SN_ENSURE(ctx->loads, 4 * sizeof(unsigned long long));
-        bl.loads = ctx->loads.as<unsigned long long>() + 2 * pass_id;
+        SN_ENSURE(ctx->loads, 6 * sizeof(unsigned long long));
+        bl.loads = ctx->loads.as<unsigned long long>() + 3 * pass_id;
         bl.scans = bl.loads + 1;
-        SN_CUDA(cudaMemsetAsync(bl.loads, 0, 2 * sizeof(unsigned long long), st));
+        bl.contribs = bl.loads + 2;
+        SN_CUDA(cudaMemsetAsync(bl.loads, 0, 3 * sizeof(unsigned long long), st));
     }
+    if (blend_wait) SN_CUDA(cudaStreamWaitEvent(st, blend_wait, 0));  // composite reads the scene frame
     tm.begin(SN_STAGE_BLEND);
     SN_CUDA(launch_blend(bl, st));
     tm.end();
     if (work) {
-        SN_CUDA(cudaMemcpyAsync(ctx->h_work + 2 * pass_id, bl.loads, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        SN_CUDA(cudaMemcpyAsync(ctx->h_work + 3 * pass_id, bl.loads, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
         SN_CUDA(cudaEventRecord(ctx->ev_work[pass_id], st));
         ctx->work_dst[pass_id] = work;
         work[0] += V;
@@ -402,9 +414,11 @@ const char *sn_last_error(void) { return g_last_error.c_str(); }
 int sn_context_create(sn_context **out) {
     SN_CHECK(out != nullptr, "null output pointer");
     sn_context *ctx = new sn_context();
-    cudaError_t e = cudaMallocHost(&ctx->h_tot, sizeof(uint64_t) * 4);
-    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_err, sizeof(int32_t) * 4);
-    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_work, sizeof(uint64_t) * 4);
+    cudaError_t e = cudaHostAlloc(&ctx->h_tot, sizeof(uint64_t) * 4, cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(&ctx->d_tot, ctx->h_tot, 0);
+    if (e == cudaSuccess) e = cudaHostAlloc(&ctx->h_err, sizeof(int32_t) * 4, cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(&ctx->d_err, ctx->h_err, 0);
+    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_work, sizeof(uint64_t) * 6);
     if (e != cudaSuccess) {
         delete ctx;
         return fail(SN_ERR_CUDA, std::string("cudaMallocHost: ") + cudaGetErrorString(e));
@@ -436,6 +450,10 @@ int sn_context_destroy(sn_context *ctx) {
         for (auto &ev : ctx->ev_work) cudaEventDestroy(ev);
     }
     if (ctx->h_work) cudaFreeHost(ctx->h_work);
+    if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
+    for (cudaEvent_t ev : {ctx->ev_inputs, ctx->ev_scene, ctx->ev_layer})
+        if (ev) cudaEventDestroy(ev);
     if (ctx->h_tot) cudaFreeHost(ctx->h_tot);
     if (ctx->h_err) cudaFreeHost(ctx->h_err);
     delete ctx;
@@ -513,13 +531,42 @@ int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, con
     }
 
     SN_ENSURE(ctx->cams, sizeof(sn_camera) * n_envs);
-    SN_CUDA(cudaMemcpyAsync(ctx->cams.p, cams, sizeof(sn_camera) * n_envs, cudaMemcpyHostToDevice, st));
+    {
+        const size_t need = (sizeof(sn_camera) + sizeof(double)) * n_envs;
+        if (need > ctx->h_stage_cap) {
+            SN_CUDA(cudaStreamSynchronize(st));
+            if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+            ctx->h_stage = nullptr;
+            ctx->h_stage_cap = 0;
+            SN_CUDA(cudaMallocHost(&ctx->h_stage, need));
+            ctx->h_stage_cap = need;
+        }
+    }
+    // the previous call's uploads have completed: every call synchronizes its stream(s) at least once
+    // after its uploads, so the staging buffer is free to overwrite here
+    std::memcpy(ctx->h_stage, cams, sizeof(sn_camera) * n_envs);
+    SN_CUDA(cudaMemcpyAsync(ctx->cams.p, ctx->h_stage, sizeof(sn_camera) * n_envs, cudaMemcpyHostToDevice, st));
     double *depth64 = nullptr;
     if (with_avatars || with_layer) {
         SN_ENSURE(ctx->depth64, sizeof(double) * (size_t)n_envs * W * H);
         depth64 = ctx->depth64.as<double>();
     }
     if (opts && opts->stats) SN_CUDA(cudaMemsetAsync(opts->stats, 0, sizeof(sn_stats) * n_envs, st));
+
+    // the layer pass runs on the context's side stream: only its blend waits for the scene blend
+    const bool two_pass = with_layer || with_avatars;
+    cudaStream_t lst = st;
+    if (two_pass) {
+        if (!ctx->side) {
+            SN_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+            SN_CUDA(cudaEventCreateWithFlags(&ctx->ev_inputs, cudaEventDisableTiming));
+            SN_CUDA(cudaEventCreateWithFlags(&ctx->ev_scene, cudaEventDisableTiming));
+            SN_CUDA(cudaEventCreateWithFlags(&ctx->ev_layer, cudaEventDisableTiming));
+        }
+        lst = ctx->side;
+        SN_CUDA(cudaEventRecord(ctx->ev_inputs, st));
+        SN_CUDA(cudaStreamWaitEvent(lst, ctx->ev_inputs, 0));
+    }
 
     PassSpec scene_spec;
     scene_spec.scene = scene;
@@ -529,6 +576,7 @@ int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, con
         r = run_pass(ctx, 0, scene_spec, e0, ec, W, H, tiled, z_lo, z_bits, opts, color, alpha, depth, depth64, st);
         if (r != SN_OK) return r;
     }
+    if (two_pass) SN_CUDA(cudaEventRecord(ctx->ev_scene, st));
     if (with_layer) {
         PassSpec layer_spec;
         layer_spec.scene = layer;
@@ -536,28 +584,32 @@ int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, con
         for (int e0 = 0; e0 < n_envs; e0 += chunk) {
             int ec = std::min(chunk, n_envs - e0);
             r = run_pass(ctx, 1, layer_spec, e0, ec, W, H, tiled, z_lo, z_bits, opts, color, alpha, depth, depth64,
-                         st);
+                         lst, ctx->ev_scene);
             if (r != SN_OK) return r;
         }
+        SN_CUDA(cudaEventRecord(ctx->ev_layer, lst));
+        SN_CUDA(cudaStreamWaitEvent(st, ctx->ev_layer, 0));
         return SN_OK;
     }
     if (!with_avatars) return SN_OK;
 
     const int A = avatars->n_avatars, J = avatars->n_joints;
     SN_ENSURE(ctx->times, sizeof(double) * n_envs);
-    SN_CUDA(cudaMemcpyAsync(ctx->times.p, sim_times, sizeof(double) * n_envs, cudaMemcpyHostToDevice, st));
+    double *h_times = reinterpret_cast<double *>(static_cast<char *>(ctx->h_stage) + sizeof(sn_camera) * n_envs);
+    std::memcpy(h_times, sim_times, sizeof(double) * n_envs);
+    SN_CUDA(cudaMemcpyAsync(ctx->times.p, h_times, sizeof(double) * n_envs, cudaMemcpyHostToDevice, lst));
     SN_ENSURE(ctx->jm, sizeof(double) * (size_t)n_envs * A * J * 12);
     SN_ENSURE(ctx->eq, sizeof(double) * (size_t)n_envs * A * J * 4);
     SN_ENSURE(ctx->root, sizeof(double) * (size_t)n_envs * A * 12);
     SN_ENSURE(ctx->err, sizeof(int32_t));
-    SN_CUDA(cudaMemsetAsync(ctx->err.p, 0, sizeof(int32_t), st));
-    StageTimer ptm{ctx, st, opts && opts->stage_ms ? opts->stage_ms + SN_N_STAGES : nullptr, 1};
+    SN_CUDA(cudaMemsetAsync(ctx->err.p, 0, sizeof(int32_t), lst));
+    StageTimer ptm{ctx, lst, opts && opts->stage_ms ? opts->stage_ms + SN_N_STAGES : nullptr, 1};
     ptm.begin(SN_STAGE_POSE);
     SN_CUDA(launch_pose(*avatars, ctx->times.as<double>(), n_envs, nullptr, nullptr, ctx->jm.as<double>(),
-                        ctx->eq.as<double>(), ctx->root.as<double>(), ctx->err.as<int32_t>(), st));
+                        ctx->eq.as<double>(), ctx->root.as<double>(), ctx->err.as<int32_t>(), lst));
     ptm.end();
-    SN_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->err.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    SN_CUDA(cudaStreamSynchronize(st));
+    SN_CUDA(launch_publish_i32(ctx->err.as<int32_t>(), ctx->d_err, lst));
+    SN_CUDA(cudaStreamSynchronize(lst));
     SN_CHECK(ctx->h_err[0] == 0, "sample time must be nonnegative");
 
     PassSpec av_spec;
@@ -567,9 +619,12 @@ int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, con
     av_spec.mode = 2;
     for (int e0 = 0; e0 < n_envs; e0 += chunk) {
         int ec = std::min(chunk, n_envs - e0);
-        r = run_pass(ctx, 1, av_spec, e0, ec, W, H, tiled, z_lo, z_bits, opts, color, alpha, depth, depth64, st);
+        r = run_pass(ctx, 1, av_spec, e0, ec, W, H, tiled, z_lo, z_bits, opts, color, alpha, depth, depth64, lst,
+                     ctx->ev_scene);
         if (r != SN_OK) return r;
     }
+    SN_CUDA(cudaEventRecord(ctx->ev_layer, lst));
+    SN_CUDA(cudaStreamWaitEvent(st, ctx->ev_layer, 0));
     return SN_OK;
 }
 
@@ -726,7 +781,7 @@ int sn_sample_pose(sn_context *ctx, const sn_avatars *avatars, const double *sim
     SN_CUDA(cudaMemsetAsync(ctx->err.p, 0, sizeof(int32_t), st));
     SN_CUDA(launch_pose(*avatars, ctx->times.as<double>(), n_envs, pose_q, pose_t, nullptr, nullptr, nullptr,
                         ctx->err.as<int32_t>(), st));
-    SN_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->err.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    SN_CUDA(launch_publish_i32(ctx->err.as<int32_t>(), ctx->d_err, st));
     SN_CUDA(cudaStreamSynchronize(st));
     SN_CHECK(ctx->h_err[0] == 0, "sample time must be nonnegative");
     return SN_OK;

@@ -70,8 +70,11 @@ __constant__ double kExp2Tbl[64] = {
 //           of the env -- no pair duplication, no sort, no per-pair HBM traffic.
 // SOURCE 1: a materialized tile list (ranges + pair_vals from the radix binner).
 // SOURCE 2: rasterize_reference -- every splat of the env, in depth order.
+#ifndef SN_BLEND_MIN_BLOCKS
+#define SN_BLEND_MIN_BLOCKS 1
+#endif
 template <int MODE, int SOURCE>
-__global__ void __launch_bounds__(kBlock) blend_kernel(BlendArgs b) {
+__global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(BlendArgs b) {
     __shared__ BlendRec s_rec[kBlock];
     __shared__ double s_exp[64];
     __shared__ uint32_t s_queue[2 * kBlock];
@@ -95,6 +98,9 @@ __global__ void __launch_bounds__(kBlock) blend_kernel(BlendArgs b) {
         uint2 r = b.ranges[((uint32_t)el << b.tile_bits) | (uint32_t)tile];
         cursor = r.x;
         s1 = r.y;
+        // composite of an empty layer tile: front alpha 0 and depth `far`, and the scene depth is a
+        // weighted mean of z < far, so `front.depth < back.depth` never holds -- nothing to do
+        if (MODE == 2 && cursor == s1) return;
     } else {
         cursor = (uint32_t)b.env_off[el];
         s1 = (uint32_t)b.env_off[el + 1];
@@ -222,6 +228,10 @@ __global__ void __launch_bounds__(kBlock) blend_kernel(BlendArgs b) {
         }
     }
     if (b.scans && threadIdx.x == 0 && scanned) atomicAdd(b.scans, (unsigned long long)scanned);
+    if (b.contribs) {
+        unsigned sum = __reduce_add_sync(kFull, (unsigned)nc);
+        if ((threadIdx.x & 31) == 0 && sum) atomicAdd(b.contribs, (unsigned long long)sum);
+    }
     if (b.loads && threadIdx.x == 0 && loaded) atomicAdd(b.loads, (unsigned long long)loaded);
     if (!inside) return;
 

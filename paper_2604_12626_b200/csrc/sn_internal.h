@@ -54,6 +54,10 @@ cudaError_t launch_block_scan(uint32_t *blk_counts, int32_t n_blocks, int32_t ec
 cudaError_t launch_skin_range(const sn_avatars &av, int64_t g0, int64_t n, const PoseView &pv, double *out_pos,
                               double *out_rot, cudaStream_t s);
 
+// one-thread copies of a device word into mapped pinned host memory (no copy engine)
+cudaError_t launch_publish_u64(const uint64_t *src, uint64_t *mapped_dst, cudaStream_t s);
+cudaError_t launch_publish_i32(const int32_t *src, int32_t *mapped_dst, cudaStream_t s);
+
 // sn_rig.cu
 cudaError_t launch_pose(const sn_avatars &av, const double *sim_times, int32_t n_envs, double *pose_q, double *pose_t,
                         double *joint_mats, double *eff_q, double *root, int32_t *err_flag, cudaStream_t s);
@@ -110,6 +114,7 @@ struct BlendArgs {
     int32_t *contrib;       // (E,H,W) may be null
     unsigned long long *loads;  // device counter: records gathered into shared memory (may be null)
     unsigned long long *scans;  // device counter: rectangles examined by source-0 tiles (may be null)
+    unsigned long long *contribs;  // device counter: (pixel, splat) contributions (may be null)
 };
 cudaError_t launch_blend(const BlendArgs &b, cudaStream_t s);
 cudaError_t launch_composite64(int64_t npix, const double *fc, const double *fa, const double *fd, const double *bc,

@@ -283,6 +283,25 @@ __global__ void __launch_bounds__(kBlock) scene_emit_kernel(sn_cloud c, PrepArgs
 
 // lbs_deform (rig.py:107-146) for one gaussian under one (env, avatar) pose. Sparse influences
 // in ascending joint order reproduce the dense N x J sums exactly: zero weights add +-0.
+template <bool NC>
+__device__ __forceinline__ double ldp(const double *p) {
+    if (NC) return __ldg(p);
+    return *p;
+}
+template <bool NC>
+__device__ __forceinline__ void ld4p(const double *p, double o[4]) {
+    if (NC) {
+        load4<double>(p, o);
+    } else {
+        o[0] = p[0];
+        o[1] = p[1];
+        o[2] = p[2];
+        o[3] = p[3];
+    }
+}
+
+// NC = true: pose data in global memory (read-only path); false: generic loads (shared memory)
+template <bool NC = true>
 __device__ __forceinline__ void skin_one(const sn_avatars &av, int64_t g, const double *jm, const double *eq,
                                          const double *root, double p_out[3], double q_out[4]) {
     double P[4], W[4], Q[4];
@@ -300,9 +319,9 @@ __device__ __forceinline__ void skin_one(const sn_avatars &av, int64_t g, const 
         int j = (J4 >> (8 * k)) & 0xff;
         const double *M = jm + 12 * j;
         // einsum("jab,nb->jna") as numpy evaluates it: (r0 p0 + r2 p2) + r1 p1, then + offset
-        double t0 = ((__ldg(M + 0) * P[0] + __ldg(M + 2) * P[2]) + __ldg(M + 1) * P[1]) + __ldg(M + 3);
-        double t1 = ((__ldg(M + 4) * P[0] + __ldg(M + 6) * P[2]) + __ldg(M + 5) * P[1]) + __ldg(M + 7);
-        double t2 = ((__ldg(M + 8) * P[0] + __ldg(M + 10) * P[2]) + __ldg(M + 9) * P[1]) + __ldg(M + 11);
+        double t0 = ((ldp<NC>(M + 0) * P[0] + ldp<NC>(M + 2) * P[2]) + ldp<NC>(M + 1) * P[1]) + ldp<NC>(M + 3);
+        double t1 = ((ldp<NC>(M + 4) * P[0] + ldp<NC>(M + 6) * P[2]) + ldp<NC>(M + 5) * P[1]) + ldp<NC>(M + 7);
+        double t2 = ((ldp<NC>(M + 8) * P[0] + ldp<NC>(M + 10) * P[2]) + ldp<NC>(M + 9) * P[1]) + ldp<NC>(M + 11);
         acc0 = acc0 + w * (t0 - P[0]);
         acc1 = acc1 + w * (t1 - P[1]);
         acc2 = acc2 + w * (t2 - P[2]);
@@ -313,12 +332,12 @@ __device__ __forceinline__ void skin_one(const sn_avatars &av, int64_t g, const 
     }
     if (dom < 0) dom = 0;  // all-zero row: np.argmax picks joint 0
     double b0 = P[0] + acc0, b1 = P[1] + acc1, b2 = P[2] + acc2;
-    p_out[0] = dot3_fma(b0, b1, b2, __ldg(root + 0), __ldg(root + 1), __ldg(root + 2)) + __ldg(root + 9);
-    p_out[1] = dot3_fma(b0, b1, b2, __ldg(root + 3), __ldg(root + 4), __ldg(root + 5)) + __ldg(root + 10);
-    p_out[2] = dot3_fma(b0, b1, b2, __ldg(root + 6), __ldg(root + 7), __ldg(root + 8)) + __ldg(root + 11);
+    p_out[0] = dot3_fma(b0, b1, b2, ldp<NC>(root + 0), ldp<NC>(root + 1), ldp<NC>(root + 2)) + ldp<NC>(root + 9);
+    p_out[1] = dot3_fma(b0, b1, b2, ldp<NC>(root + 3), ldp<NC>(root + 4), ldp<NC>(root + 5)) + ldp<NC>(root + 10);
+    p_out[2] = dot3_fma(b0, b1, b2, ldp<NC>(root + 6), ldp<NC>(root + 7), ldp<NC>(root + 8)) + ldp<NC>(root + 11);
 
     double qd[4];
-    load4<double>(eq + 4 * dom, qd);
+    ld4p<NC>(eq + 4 * dom, qd);
     double bq[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -326,7 +345,7 @@ __device__ __forceinline__ void skin_one(const sn_avatars &av, int64_t g, const 
         if (w == 0.0) continue;
         int j = (J4 >> (8 * k)) & 0xff;
         double qj[4];
-        load4<double>(eq + 4 * j, qj);
+        ld4p<NC>(eq + 4 * j, qj);
         double dot = fma(qj[3], qd[3], fma(qj[2], qd[2], fma(qj[1], qd[1], qj[0] * qd[0])));
         double ws = w * (dot < 0.0 ? -1.0 : 1.0);
         bq[0] = fma(ws, qj[0], bq[0]);
@@ -357,24 +376,54 @@ __device__ __forceinline__ bool avatar_on(const PrepArgs &a, int n_avatars, int 
     return a.avatar_active == nullptr || a.avatar_active[(int64_t)env * n_avatars + avatar] != 0;
 }
 
+// Pose blocks of the (at most two) avatars a CTA's gaussians belong to are staged in shared memory
+// for each env, so the per-(gaussian, env) skinning reads joint matrices from shared memory
+// instead of hammering L1 (avatars are contiguous and >= 256 gaussians in practice; other
+// avatars fall back to global loads).
+__host__ __device__ __forceinline__ int pose_block_doubles(int J) { return 16 * J + 12; }
+
 __global__ void __launch_bounds__(kBlock) avatar_count_kernel(sn_avatars av, PoseView pv, PrepArgs a) {
     __shared__ unsigned s_cnt[kMaxEnvChunk][5];
+    extern __shared__ double s_pose[];  // 2 x (J*12 joint mats | J*4 quats | 12 root)
     init_counts(s_cnt, a.ec);
     int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     bool valid = g < av.n;
     int avatar = valid ? av.avatar_of[g] : 0;
+    const int64_t g_first = (int64_t)blockIdx.x * kBlock;
+    const int64_t g_last = min(av.n, g_first + kBlock) - 1;
+    const int a_lo = av.avatar_of[g_first], a_hi = av.avatar_of[g_last];
+    const int J = pv.n_joints, pb = pose_block_doubles(J);
     double ls[4];
     if (valid) load4<double>(av.log_scales + 4 * g, ls);
     uint64_t mask = 0;
     for (int e = 0; e < a.ec; ++e) {
         int env = a.e0 + e;
+        __syncthreads();
+        for (int k = threadIdx.x; k < 2 * pb; k += kBlock) {
+            const int slot = k / pb, o = k % pb, av_id = slot ? a_hi : a_lo;
+            const int64_t ea = (int64_t)env * pv.n_avatars + av_id;
+            double v;
+            if (o < 12 * J)
+                v = pv.joint_mats[ea * J * 12 + o];
+            else if (o < 16 * J)
+                v = pv.eff_q[ea * J * 4 + (o - 12 * J)];
+            else
+                v = pv.root[ea * 12 + (o - 16 * J)];
+            s_pose[k] = v;
+        }
+        __syncthreads();
         bool input = valid && avatar_on(a, av.n_avatars, env, avatar);
         int code = -1;
         if (input) {
-            const double *jm, *eq, *root;
-            pose_ptrs(pv, env, avatar, jm, eq, root);
             double p[3], q[4];
-            skin_one(av, g, jm, eq, root, p, q);
+            if (avatar == a_lo || avatar == a_hi) {
+                const double *blk = s_pose + (avatar == a_lo ? 0 : pb);
+                skin_one<false>(av, g, blk, blk + 12 * J, blk + 16 * J, p, q);
+            } else {
+                const double *jm, *eq, *root;
+                pose_ptrs(pv, env, avatar, jm, eq, root);
+                skin_one<true>(av, g, jm, eq, root, p, q);
+            }
             const sn_camera &cam = a.cams[env];
             double z = cam_z(p, cam);
             if (!((z > cam.near_) && (z < cam.far_))) {
@@ -484,7 +533,20 @@ __global__ void env_offsets_kernel(int32_t ec, uint64_t *env_off) {
     env_off[ec] = run;
 }
 
+__global__ void publish_u64_kernel(const uint64_t *src, volatile uint64_t *dst) { *dst = *src; }
+__global__ void publish_i32_kernel(const int32_t *src, volatile int32_t *dst) { *dst = *src; }
+
 }  // namespace
+
+cudaError_t launch_publish_u64(const uint64_t *src, uint64_t *mapped_dst, cudaStream_t s) {
+    publish_u64_kernel<<<1, 1, 0, s>>>(src, mapped_dst);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_publish_i32(const int32_t *src, int32_t *mapped_dst, cudaStream_t s) {
+    publish_i32_kernel<<<1, 1, 0, s>>>(src, mapped_dst);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_scene_count(const sn_cloud &c, const PrepArgs &a, cudaStream_t s) {
     if (c.dtype == SN_FLOAT64)
@@ -503,7 +565,9 @@ cudaError_t launch_scene_emit(const sn_cloud &c, const PrepArgs &a, cudaStream_t
 }
 
 cudaError_t launch_avatar_count(const sn_avatars &av, const PoseView &pv, const PrepArgs &a, cudaStream_t s) {
-    avatar_count_kernel<<<a.n_blocks, kBlock, 0, s>>>(av, pv, a);
+    const size_t smem = sizeof(double) * 2 * (size_t)pose_block_doubles(pv.n_joints);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(avatar_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    avatar_count_kernel<<<a.n_blocks, kBlock, smem, s>>>(av, pv, a);
     return cudaGetLastError();
 }
 

@@ -89,8 +89,8 @@ def render_frames(scene, cameras, background, layer=None, avatars=None, sim_time
     if stage_ms is not None:  # host float64 (2, 11): per-pass GPU ms per stage, accumulated
         assert stage_ms.dtype == np.float64 and stage_ms.size == 2 * len(N.STAGES) and stage_ms.flags.c_contiguous
         opts.stage_ms = stage_ms.ctypes.data
-    if work is not None:  # host int64 (2, 4): visible, pairs, records gathered, CTAs
-        assert work.dtype == np.int64 and work.size == 8 and work.flags.c_contiguous
+    if work is not None:  # host int64 (2, 6): visible, pairs, records gathered, rects scanned, contributions
+        assert work.dtype == np.int64 and work.size == 12 and work.flags.c_contiguous
         opts.work = work.ctypes.data
     if avatar_active is not None:
         out["avatar_active"] = avatar_active.to(device=dev, dtype=torch.uint8).contiguous()
