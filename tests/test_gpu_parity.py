@@ -320,3 +320,85 @@ def test_layer_pass_both_binners_agree():
     for o in outs[1:]:
         for k in ("color", "alpha", "depth", "contrib_scene", "contrib_layer"):
             assert torch.equal(outs[0][k], o[k]), k
+
+
+def test_env_chunking_beyond_64_envs():
+    """E > 64 runs in env chunks (key space); every env must still match the oracle exactly."""
+    box = S.room_box(1_000_000)
+    scene = S.make_scene(25_000, box[0], box[1], seed=91)
+    cams = S.room_cameras(70, box, seed=92, width=48, height=40)
+    bg = np.array([0.1, 0.2, 0.3])
+    out = R().render_frames(scene, cams, bg, contrib=True)
+    for e in range(70):
+        o = O.rasterize(scene, cams[e], bg)
+        np.testing.assert_array_equal(out["contrib_scene"][e].cpu().numpy(), o.contrib)
+        check_frame(out["color"][e].cpu().numpy(), out["alpha"][e].cpu().numpy(), out["depth"][e].cpu().numpy(),
+                    o.color, o.alpha, o.depth, cams[e].far)
+
+
+def test_avatar_active_mask_and_clock():
+    from paper_2604_12626_b200 import rig
+    from paper_2604_12626_b200.batch import BatchRenderer
+    box, bundles = _avatar_setup(3, 2500, seed=95)
+    scene = S.make_scene(30_000, box[0], box[1], seed=96)
+    cams = S.room_cameras(4, box, seed=97, width=160, height=120)
+    times = np.array([0.05, 0.5, 1.7, 3.3])  # past the 12-frame trajectories: loop vs clamp
+    offs, loops = [0.0, 0.25, 0.6], [1, 0, 1]
+    active = torch.tensor([[1, 1, 1], [0, 1, 0], [1, 0, 1], [0, 0, 0]], dtype=torch.uint8)
+    br = BatchRenderer(scene, bundles, start_offsets=offs, loops=loops, background=(0.5, 0.4, 0.3))
+    out = br.render(cams, times, avatar_active=active, contrib=True)
+    for e in range(4):
+        clouds = [rig.AvatarRuntime(b, start_offset=offs[a], loop=bool(loops[a])).deformed_cloud(float(times[e]))
+                  for a, b in enumerate(bundles) if active[e, a]]
+        o = O.render_observation(scene, clouds, cams[e], np.array([0.5, 0.4, 0.3]))
+        check_frame(out["color"][e].cpu().numpy(), out["alpha"][e].cpu().numpy(), out["depth"][e].cpu().numpy(),
+                    o.color, o.alpha, o.depth, cams[e].far)
+
+
+def test_negative_sample_time_is_a_contract_violation():
+    from paper_2604_12626_b200 import rig
+    from paper_2604_12626_b200.batch import BatchRenderer
+    from paper_2604_12626_b200.errors import ContractViolation
+    box, bundles = _avatar_setup(1, 500, seed=98)
+    br = BatchRenderer(S.make_scene(1000, box[0], box[1], seed=1), bundles, loops=[0])
+    cams = S.room_cameras(1, box, seed=2, width=32, height=32)
+    with pytest.raises(ContractViolation):
+        br.render(cams, np.array([-0.5]))
+    with pytest.raises(ContractViolation):
+        rig.sample_pose(bundles[0].trajectory, -0.1)
+
+
+def test_full_size_config2_spot_check():
+    """BASELINE config 2 at full size (1M scene, 4 x 50k avatars, 64 envs, 640x480): two envs
+    against the oracle, discrete outputs exact."""
+    from paper_2604_12626_b200 import rig
+    from paper_2604_12626_b200.batch import BatchRenderer
+    cfg = S.baseline_config(2, seed=0)
+    offs = [0.37 * i for i in range(4)]
+    br = BatchRenderer(cfg["scene"], cfg["avatars"], start_offsets=offs, background=(1.0, 1.0, 1.0))
+    times = np.random.default_rng(5).uniform(0.0, 2.0, size=64)
+    out = br.render(cfg["cameras"], times, contrib=True, stats=True)
+    for e in (0, 41):
+        cam = cfg["cameras"][e]
+        clouds = [rig.AvatarRuntime(b, start_offset=offs[a]).deformed_cloud(float(times[e]))
+                  for a, b in enumerate(cfg["avatars"])]
+        o = O.render_observation(cfg["scene"], clouds, cam, np.ones(3))
+        check_frame(out["color"][e].cpu().numpy(), out["alpha"][e].cpu().numpy(), out["depth"][e].cpu().numpy(),
+                    o.color, o.alpha, o.depth, cam.far)
+        np.testing.assert_array_equal(out["contrib_scene"][e].cpu().numpy(), o.scene.contrib)
+        np.testing.assert_array_equal(out["contrib_layer"][e].cpu().numpy(), o.layer.contrib)
+        proj = O.project_cloud(cfg["scene"], cam)
+        inter = R().pass_intermediates(0, e, context=br.context)
+        np.testing.assert_array_equal(inter["ids"], proj.ids.astype(np.int32))
+
+
+def test_3m_scene_spot_check():
+    """BASELINE config 3/4 scale (3M gaussians in a 3x-area room): one env exact vs the oracle."""
+    box = S.room_box(3_000_000)
+    scene = S.make_scene(3_000_000, box[0], box[1], seed=7)
+    cams = S.room_cameras(8, box, seed=8)
+    out = R().render_frames(scene, cams, np.ones(3), contrib=True)
+    o = O.rasterize(scene, cams[5], np.ones(3))
+    np.testing.assert_array_equal(out["contrib_scene"][5].cpu().numpy(), o.contrib)
+    check_frame(out["color"][5].cpu().numpy(), out["alpha"][5].cpu().numpy(), out["depth"][5].cpu().numpy(),
+                o.color, o.alpha, o.depth, cams[5].far)
