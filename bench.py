@@ -265,6 +265,7 @@ def main():
     if world > 1:
         dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = br.context.kernel_launches()
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
         ev0.record()
@@ -273,6 +274,7 @@ def main():
         ev1.record()
         torch.cuda.synchronize()
     br.context.sync_stats()  # stage timings / work counters are folded in lazily (no syncs while timing)
+    launches = br.context.kernel_launches() - launches0
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
@@ -367,22 +369,13 @@ def main():
                           "layer_contributions": int(w2[1, 4] / args.steps)},
         "clocks": clocks.summary(),
     }
-    line["gpu_launches"] = launches_per_step(args) * args.steps
+    line["gpu_launches"] = launches  # this library's kernels in the timed region (CUB sort/scan kernels excluded)
     if world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         line["cpu_baseline"] = cpu_baseline(args, scene, bundles, sets, args.cpu_envs or max(2, min(args.envs, threads)))
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
-
-
-def launches_per_step(args):
-    """Kernels sn_render launches per step (ours only; CUB sorts/scans counted as library launches
-    separately): per pass: count, block scan, env offsets, emit, permute, duplicate, ranges, blend
-    (+ pose kernel for the avatar layer)."""
-    chunks = -(-args.envs // 64)
-    per_pass = 8
-    return chunks * per_pass * (2 if args.avatars else 1) + (1 if args.avatars else 0)
 
 
 if __name__ == "__main__":

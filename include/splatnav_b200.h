@@ -149,6 +149,9 @@ const char *sn_last_error(void);
 /* One context per (device, thread). Owns the workspace; grows it on demand. */
 int sn_context_create(sn_context **ctx);
 int sn_context_destroy(sn_context *ctx);
+/* Cumulative number of this library's kernels launched through the context (CUB's radix sort and
+ * scan kernels excluded). */
+int sn_context_kernel_launches(const sn_context *ctx, int64_t *n);
 /* Folds pending stage timings / work counters into the arrays last passed in sn_render_opts. */
 int sn_context_sync_stats(sn_context *ctx);
 /* Bytes of device workspace currently held. */

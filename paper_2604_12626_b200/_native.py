@@ -61,7 +61,7 @@ STAGES = ("pose", "count", "scan", "emit", "depth_sort", "permute", "pair_scan",
 # every symbol include/splatnav_b200.h declares (tests check the library exports all of them)
 EXPORTS = (
     "sn_abi_version", "sn_last_error", "sn_context_create", "sn_context_destroy", "sn_context_workspace_bytes",
-    "sn_context_sync_stats",
+    "sn_context_sync_stats", "sn_context_kernel_launches",
     "sn_render", "sn_get_counts", "sn_get_sorted_ids", "sn_get_tile_csr", "sn_get_projection", "sn_sample_pose",
     "sn_skin_lbs", "sn_blend_tile_range", "sn_composite",
 )
@@ -90,6 +90,7 @@ def load():
             "sn_context_destroy": ([P], ctypes.c_int),
             "sn_context_workspace_bytes": ([P, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
             "sn_context_sync_stats": ([P], ctypes.c_int),
+            "sn_context_kernel_launches": ([P, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
             "sn_render": ([P, ctypes.POINTER(SnCloud), ctypes.POINTER(SnCloud), ctypes.POINTER(SnAvatars), P, P, i32,
                            ctypes.POINTER(SnRenderOpts), P, P, P, P], ctypes.c_int),
             "sn_get_counts": ([P, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)], ctypes.c_int),
@@ -140,6 +141,11 @@ class Context:
 
     def sync_stats(self):
         check(self._lib.sn_context_sync_stats(self.handle))
+
+    def kernel_launches(self):
+        v = ctypes.c_int64()
+        check(self._lib.sn_context_kernel_launches(self.handle, ctypes.byref(v)))
+        return int(v.value)
 
     def workspace_bytes(self):
         v = ctypes.c_size_t()

@@ -103,6 +103,7 @@ struct sn_context {
     // side stream for the layer pass: its preprocessing overlaps the scene blend
     cudaStream_t side = nullptr;
     cudaEvent_t ev_inputs = nullptr, ev_scene = nullptr, ev_layer = nullptr;
+    int64_t launches = 0;  // kernels of this library launched through the context (not CUB's)
     double *ms_dst[2][SN_N_STAGES] = {};
     int64_t *work_dst[2] = {};
     bool have_events = false;
@@ -210,14 +211,17 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     int64_t V = 0;
     if (n > 0) {
         tm.begin(SN_STAGE_COUNT);
+        ctx->launches += 1;
         if (sp.scene)
             SN_CUDA(launch_scene_count(*sp.scene, a, st));
         else
             SN_CUDA(launch_avatar_count(*sp.avatars, sp.pose, a, st));
         tm.end();
         tm.begin(SN_STAGE_SCAN);
+        ctx->launches += 2;
         SN_CUDA(launch_block_scan(a.blk_counts, n_blocks, ec, w.env_off.as<uint64_t>(), st));
         tm.end();
+        ctx->launches += 1;
         SN_CUDA(launch_publish_u64(w.env_off.as<uint64_t>() + ec, ctx->d_tot, st));
         SN_CUDA(cudaStreamSynchronize(st));
         V = (int64_t)ctx->h_tot[0];
@@ -268,6 +272,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
         size_t tb = std::max(sort_u32_temp_bytes(V), scan_temp_bytes(V + 1));
         SN_ENSURE(w.temp, tb);
         tm.begin(SN_STAGE_EMIT);
+        ctx->launches += 1;
         if (sp.scene)
             SN_CUDA(launch_scene_emit(*sp.scene, a, st));
         else
@@ -277,10 +282,15 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
         // 32-bit keys (env + top z bits) in 4 radix passes, then an exact fix of equal-key runs
         SN_CUDA(sort_u32_pairs(w.temp.p, w.temp.cap, w.keys_un.as<uint32_t>(), w.keys_s.as<uint32_t>(),
                                w.vals_un.as<uint32_t>(), w.vals_s.as<uint32_t>(), V, std::min(key_bits, 32), st));
-        if (key_bits > 32) SN_CUDA(launch_depth_tie_fix(b, st));
+        if (key_bits > 32) {
+            ctx->launches += 1;
+            SN_CUDA(launch_depth_tie_fix(b, st));
+        }
         tm.end();
         tm.begin(SN_STAGE_PERMUTE);
+        ctx->launches += 1;
         SN_CUDA(launch_permute(b, st));
+        ctx->launches += 1;
         SN_CUDA(launch_super_rects(w.batch_rects.as<ushort4>(), n_batches, w.super_rects.as<ushort4>(), st));
         tm.end();
         if (tiled && binning == 1) {  // pair offsets: the radix binner emits from them
@@ -288,6 +298,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
             tm.begin(SN_STAGE_PAIR_SCAN);
             SN_CUDA(scan_tiles(w.temp.p, w.temp.cap, w.tiles.as<uint32_t>(), w.pair_off.as<uint64_t>(), V + 1, st));
             tm.end();
+            ctx->launches += 1;
             SN_CUDA(launch_publish_u64(w.pair_off.as<uint64_t>() + V, ctx->d_tot, st));
             SN_CUDA(cudaStreamSynchronize(st));
             P = (int64_t)ctx->h_tot[0];
@@ -307,6 +318,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
         b.pair_keys = w.pkeys_a.as<uint32_t>();
         b.pair_vals = w.pvals_a.as<uint32_t>();
         tm.begin(SN_STAGE_BIN_COUNT);
+        ctx->launches += 1;
         SN_CUDA(launch_duplicate(b, st));
         tm.end();
         tm.begin(SN_STAGE_BIN_SCATTER);
@@ -314,6 +326,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
                                w.pvals_a.as<uint32_t>(), w.pvals_b.as<uint32_t>(), P, env_bits + tile_bits, st));
         tm.end();
         tm.begin(SN_STAGE_RANGES);
+        ctx->launches += 1;
         SN_CUDA(launch_ranges(w.pkeys_b.as<uint32_t>(), P, w.ranges.as<uint2>(), st));
         tm.end();
     }
@@ -357,6 +370,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     }
     if (blend_wait) SN_CUDA(cudaStreamWaitEvent(st, blend_wait, 0));  // composite reads the scene frame
     tm.begin(SN_STAGE_BLEND);
+    ctx->launches += 1;
     SN_CUDA(launch_blend(bl, st));
     tm.end();
     if (work) {
@@ -457,6 +471,12 @@ int sn_context_destroy(sn_context *ctx) {
     if (ctx->h_tot) cudaFreeHost(ctx->h_tot);
     if (ctx->h_err) cudaFreeHost(ctx->h_err);
     delete ctx;
+    return SN_OK;
+}
+
+int sn_context_kernel_launches(const sn_context *ctx, int64_t *n) {
+    SN_CHECK(ctx && n, "null argument");
+    *n = ctx->launches;
     return SN_OK;
 }
 
@@ -605,9 +625,11 @@ int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, con
     SN_CUDA(cudaMemsetAsync(ctx->err.p, 0, sizeof(int32_t), lst));
     StageTimer ptm{ctx, lst, opts && opts->stage_ms ? opts->stage_ms + SN_N_STAGES : nullptr, 1};
     ptm.begin(SN_STAGE_POSE);
+    ctx->launches += 1;
     SN_CUDA(launch_pose(*avatars, ctx->times.as<double>(), n_envs, nullptr, nullptr, ctx->jm.as<double>(),
                         ctx->eq.as<double>(), ctx->root.as<double>(), ctx->err.as<int32_t>(), lst));
     ptm.end();
+    ctx->launches += 1;
     SN_CUDA(launch_publish_i32(ctx->err.as<int32_t>(), ctx->d_err, lst));
     SN_CUDA(cudaStreamSynchronize(lst));
     SN_CHECK(ctx->h_err[0] == 0, "sample time must be nonnegative");
@@ -779,8 +801,10 @@ int sn_sample_pose(sn_context *ctx, const sn_avatars *avatars, const double *sim
     SN_CUDA(cudaMemcpyAsync(ctx->times.p, sim_times, sizeof(double) * n_envs, cudaMemcpyHostToDevice, st));
     SN_ENSURE(ctx->err, sizeof(int32_t));
     SN_CUDA(cudaMemsetAsync(ctx->err.p, 0, sizeof(int32_t), st));
+    ctx->launches += 1;
     SN_CUDA(launch_pose(*avatars, ctx->times.as<double>(), n_envs, pose_q, pose_t, nullptr, nullptr, nullptr,
                         ctx->err.as<int32_t>(), st));
+    ctx->launches += 1;
     SN_CUDA(launch_publish_i32(ctx->err.as<int32_t>(), ctx->d_err, st));
     SN_CUDA(cudaStreamSynchronize(st));
     SN_CHECK(ctx->h_err[0] == 0, "sample time must be nonnegative");
@@ -799,8 +823,10 @@ int sn_skin_lbs(sn_context *ctx, const sn_avatars *avatars, int32_t avatar, int6
     const int J = avatars->n_joints;
     SN_ENSURE(ctx->pose_q, sizeof(double) * (J * 12 + J * 4 + 12));
     double *jm = ctx->pose_q.as<double>(), *eq = jm + J * 12, *root = eq + J * 4;
+    ctx->launches += 1;
     SN_CUDA(launch_joint_prep(*avatars, avatar, pose_q, pose_t, jm, eq, root, st));
     PoseView pv{jm, eq, root, J, 1};
+    ctx->launches += 1;
     SN_CUDA(launch_skin_range(*avatars, g_begin, g_count, pv, out_positions, out_rotations, st));
     return SN_OK;
 }
