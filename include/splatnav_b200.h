@@ -120,7 +120,8 @@ enum {
     SN_STAGE_BIN_SCATTER = 8,  /* radix: (env|tile) pair sort; counting: stable scatter */
     SN_STAGE_RANGES = 9,
     SN_STAGE_BLEND = 10,
-    SN_N_STAGES = 11
+    SN_STAGE_COMPOSITE = 11,   /* layer pass: composite over the scene frame + float64 fixups */
+    SN_N_STAGES = 12
 };
 
 /* Per-call options. Null pointers disable the corresponding output. */
@@ -136,7 +137,8 @@ typedef struct sn_render_opts {
     double *stage_ms;       /* HOST (2 x SN_N_STAGES): GPU ms per stage (CUDA events), accumulated */
     int64_t *work;          /* HOST (2 x 6): visible splats, tile pairs (when lists are built),
                                records gathered by the blend, rectangles the blend examined,
-                               (pixel, splat) contributions, unused -- per pass, accumulated. Both arrays are filled asynchronously: they are complete
+                               (pixel, splat) contributions, pixels recomputed by the float64
+                               fixup -- per pass, accumulated. Both arrays are filled asynchronously: they are complete
                                after the next sn_render on the context or sn_context_sync_stats(),
                                and must stay valid until then. */
 } sn_render_opts;
@@ -152,6 +154,9 @@ int sn_context_destroy(sn_context *ctx);
 /* Cumulative number of this library's kernels launched through the context (CUB's radix sort and
  * scan kernels excluded). */
 int sn_context_kernel_launches(const sn_context *ctx, int64_t *n);
+/* Renders that were run twice because a pass outgrew its capacity-sized buffers (the render is
+ * queued without host round trips; its visible-splat / tile-pair counts are checked at the end). */
+int sn_context_render_retries(const sn_context *ctx, int64_t *n);
 /* Folds pending stage timings / work counters into the arrays last passed in sn_render_opts. */
 int sn_context_sync_stats(sn_context *ctx);
 /* Bytes of device workspace currently held. */
@@ -207,6 +212,10 @@ int sn_blend_tile_range(int32_t t_begin, int32_t t_end, int32_t tiles_x, int32_t
                         int64_t n_pairs, const double *means2d, const double *conics, const double *depths,
                         const double *colors, const double *alphas, int64_t n_splats, double *color_acc,
                         double *alpha_acc, double *trans, double *depth_acc);
+
+/* Self-check of the blend's fast exponential (ex2.approx, float32): largest relative error against
+ * float64 exp(-d2/2) over every float d2 in [0, 9.5]. The blend's error budget assumes <= 1e-6. */
+int sn_selftest_fast_exp(double *max_rel_err);
 
 /* composite(front, back) on device float64 frames of npix pixels (renderer.py:151-166). */
 int sn_composite(int64_t npix, const double *front_color, const double *front_alpha, const double *front_depth,

@@ -55,15 +55,15 @@ class SnRenderOpts(ctypes.Structure):
 
 
 STAGES = ("pose", "count", "scan", "emit", "depth_sort", "permute", "pair_scan", "bin_count", "bin_scatter", "ranges",
-          "blend")
+          "blend", "composite")
 
 
 # every symbol include/splatnav_b200.h declares (tests check the library exports all of them)
 EXPORTS = (
     "sn_abi_version", "sn_last_error", "sn_context_create", "sn_context_destroy", "sn_context_workspace_bytes",
-    "sn_context_sync_stats", "sn_context_kernel_launches",
+    "sn_context_sync_stats", "sn_context_kernel_launches", "sn_context_render_retries",
     "sn_render", "sn_get_counts", "sn_get_sorted_ids", "sn_get_tile_csr", "sn_get_projection", "sn_sample_pose",
-    "sn_skin_lbs", "sn_blend_tile_range", "sn_composite",
+    "sn_skin_lbs", "sn_blend_tile_range", "sn_composite", "sn_selftest_fast_exp",
 )
 
 _lib = None
@@ -91,6 +91,7 @@ def load():
             "sn_context_workspace_bytes": ([P, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
             "sn_context_sync_stats": ([P], ctypes.c_int),
             "sn_context_kernel_launches": ([P, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+            "sn_context_render_retries": ([P, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
             "sn_render": ([P, ctypes.POINTER(SnCloud), ctypes.POINTER(SnCloud), ctypes.POINTER(SnAvatars), P, P, i32,
                            ctypes.POINTER(SnRenderOpts), P, P, P, P], ctypes.c_int),
             "sn_get_counts": ([P, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)], ctypes.c_int),
@@ -101,6 +102,7 @@ def load():
             "sn_skin_lbs": ([P, ctypes.POINTER(SnAvatars), i32, i64, i64, P, P, P, P, P], ctypes.c_int),
             "sn_blend_tile_range": ([i32] * 6 + [P, i64, P, i64, P, P, P, P, P, i64, P, P, P, P], ctypes.c_int),
             "sn_composite": ([i64] + [P] * 9 + [P], ctypes.c_int),
+            "sn_selftest_fast_exp": ([ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -147,10 +149,22 @@ class Context:
         check(self._lib.sn_context_kernel_launches(self.handle, ctypes.byref(v)))
         return int(v.value)
 
+    def render_retries(self):
+        v = ctypes.c_int64()
+        check(self._lib.sn_context_render_retries(self.handle, ctypes.byref(v)))
+        return int(v.value)
+
     def workspace_bytes(self):
         v = ctypes.c_size_t()
         check(self._lib.sn_context_workspace_bytes(self.handle, ctypes.byref(v)))
         return int(v.value)
+
+
+def selftest_fast_exp():
+    """Largest relative error of the blend's float32 fast exp over its argument range (device)."""
+    v = ctypes.c_double()
+    check(load().sn_selftest_fast_exp(ctypes.byref(v)))
+    return float(v.value)
 
 
 _tls = threading.local()

@@ -6,6 +6,7 @@
 // The two host syncs size the workspace; buffers only grow, so a steady-state batch loop
 // allocates nothing.
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -75,22 +76,29 @@ uint64_t dbits(double d) {
 
 struct PassWs {
     Buf vismask, blk_counts, env_off, keys_un, keys_s, vals_un, vals_s, recs_un, gid_un, rects_un, rects,
-        tiles, pair_off, pkeys_a, pkeys_b, pvals_a, pvals_b, ranges, temp, batch_rects, super_rects;
+        tiles, pair_off, pkeys_a, pkeys_b, pvals_a, pvals_b, ranges, temp, batch_rects, super_rects, fix, counts;
+    uint64_t cap_v = 0, cap_p = 0;  // capacities of the per-splat / per-pair buffers
     // metadata of the last chunk rendered by this pass
     int32_t e0 = 0, ec = 0, tiles_x = 0, tiles_y = 0, tile_bits = 0, tiled = 1, valid = 0, binning = 0;
     int64_t n_vis = 0, n_pairs = 0;
+    sn::BlendArgs bl{};        // the last blend's arguments (the deferred composite reuses them)
+    int64_t *work = nullptr;   // mode 2: work counters still to be collected after the composite
 };
 
 }  // namespace
 
 struct sn_context {
     PassWs pass[2];
-    Buf cams, times, depth64, jm, eq, root, err, pose_q, pose_t, loads;
+    Buf cams, times, derr, jm, eq, root, err, pose_q, pose_t, loads, fixcnt;
+    Buf lcolor, lalpha, ldepth, lderr, laerr, tile_flag;  // deferred-composite layer frame
     // mapped pinned words the device writes with a one-thread kernel: reading a total this way
     // never queues behind other streams' bulk copies on the device->host copy engine
     uint64_t *h_tot = nullptr, *d_tot = nullptr;
     int32_t *h_err = nullptr, *d_err = nullptr;
-    uint64_t *h_work = nullptr; // pinned (2 passes x 3 counters)
+    // mapped (chunk, pass) -> (visible splats, tile pairs) of the last render, for the capacity check
+    uint64_t *h_counts = nullptr, *d_counts = nullptr;
+    size_t counts_cap = 0;  // entries (chunk x pass)
+    uint64_t *h_work = nullptr; // pinned (2 passes x 4 counters: loads, scans, contributions, fixups)
     // pinned staging for the per-call host inputs: a pageable cudaMemcpyAsync would serialize
     // with copies other streams have in flight (e.g. the caller's frame downloads)
     void *h_stage = nullptr;
@@ -102,8 +110,9 @@ struct sn_context {
     cudaEvent_t ev_work[2] = {};
     // side stream for the layer pass: its preprocessing overlaps the scene blend
     cudaStream_t side = nullptr;
-    cudaEvent_t ev_inputs = nullptr, ev_scene = nullptr, ev_layer = nullptr;
-    int64_t launches = 0;  // kernels of this library launched through the context (not CUB's)
+    cudaEvent_t ev_inputs = nullptr, ev_scene = nullptr, ev_layer = nullptr, ev_pre = nullptr;
+    int64_t launches = 0;  // kernels of this library launched through the context
+    int64_t retries = 0;   // renders re-run because a pass outgrew its buffers
     double *ms_dst[2][SN_N_STAGES] = {};
     int64_t *work_dst[2] = {};
     bool have_events = false;
@@ -125,9 +134,7 @@ void resolve_all(sn_context *ctx) {
         for (int s = 0; s < SN_N_STAGES; ++s) resolve_stage(ctx, p, s);
         if (ctx->work_dst[p]) {
             cudaEventSynchronize(ctx->ev_work[p]);
-            ctx->work_dst[p][2] += (int64_t)ctx->h_work[3 * p];
-            ctx->work_dst[p][3] += (int64_t)ctx->h_work[3 * p + 1];
-            ctx->work_dst[p][4] += (int64_t)ctx->h_work[3 * p + 2];
+            for (int k = 0; k < 4; ++k) ctx->work_dst[p][2 + k] += (int64_t)ctx->h_work[4 * p + k];
             ctx->work_dst[p] = nullptr;
         }
     }
@@ -168,9 +175,28 @@ struct PassSpec {
     int mode = 0;
 };
 
+PassView view_of(const PassWs &w) {
+    PassView v{};
+    v.source = !w.tiled ? 2 : (w.binning == 1 ? 1 : 0);
+    v.tile_bits = w.tile_bits;
+    v.rects = w.rects.as<ushort4>();
+    v.batch_rects = w.batch_rects.as<ushort4>();
+    v.super_rects = w.super_rects.as<ushort4>();
+    v.ranges = w.ranges.as<uint2>();
+    v.pair_vals = w.pvals_b.as<uint32_t>();
+    v.env_off = w.env_off.as<uint64_t>();
+    v.recs = w.recs_un.as<SplatRec>();
+    v.order = w.vals_s.as<uint32_t>();
+    v.d_nvis = w.env_off.as<uint64_t>() + w.ec;
+    v.d_npairs = w.counts.as<uint64_t>() + 1;
+    v.cap_v = w.cap_v;
+    v.cap_p = w.cap_p;
+    return v;
+}
+
 int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, int width, int height, int tiled,
              uint64_t z_base, int z_bits, const sn_render_opts *opts, float *color, float *alpha, float *depth,
-             double *depth64, cudaStream_t st, cudaEvent_t blend_wait = nullptr) {
+             float *derr, cudaStream_t st, int chunk_idx) {
     PassWs &w = ctx->pass[pass_id];
     StageTimer tm{ctx, st, opts && opts->stage_ms ? opts->stage_ms + pass_id * SN_N_STAGES : nullptr, pass_id};
     int64_t *work = opts && opts->work ? opts->work + pass_id * 6 : nullptr;
@@ -208,7 +234,38 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     a.z_base = z_base;
     a.z_bits = z_bits;
 
-    int64_t V = 0;
+    // No host round trip inside a pass: the visible count V = env_off[ec] and the pair count P stay
+    // on the device; buffers are sized by the host capacities cap_v / cap_p (from earlier renders);
+    // sn_render checks the published counts afterwards and re-runs with larger buffers on overflow.
+    const uint64_t cap_v = w.cap_v, cap_p = w.cap_p;
+    const size_t v1 = (size_t)cap_v + 1;
+    SN_ENSURE(w.keys_un, sizeof(uint32_t) * v1);
+    SN_ENSURE(w.keys_s, sizeof(uint32_t) * v1);
+    SN_ENSURE(w.vals_un, sizeof(uint32_t) * v1);
+    SN_ENSURE(w.vals_s, sizeof(uint32_t) * v1);
+    SN_ENSURE(w.recs_un, sizeof(SplatRec) * v1);
+    SN_ENSURE(w.gid_un, sizeof(uint32_t) * v1);
+    SN_ENSURE(w.rects_un, sizeof(ushort4) * v1);
+    SN_ENSURE(w.rects, sizeof(ushort4) * v1);
+    SN_ENSURE(w.tiles, sizeof(uint32_t) * v1);
+    SN_ENSURE(w.pair_off, sizeof(uint64_t) * v1);
+    const uint64_t n_batches = (cap_v + kBlock - 1) / kBlock;
+    SN_ENSURE(w.batch_rects, sizeof(ushort4) * std::max<uint64_t>(n_batches, 1));
+    SN_ENSURE(w.super_rects, sizeof(ushort4) * std::max<uint64_t>((n_batches + kSuperBatch - 1) / kSuperBatch, 1));
+    SN_ENSURE(w.counts, 2 * sizeof(uint64_t));
+    SN_CUDA(cudaMemsetAsync(w.counts.p, 0, 2 * sizeof(uint64_t), st));
+    SN_ENSURE(w.temp, std::max({sort_temp_bytes(cap_v), scan_temp_bytes_dev(cap_v), sort_temp_bytes(cap_p)}));
+    const uint64_t *d_nvis = w.env_off.as<uint64_t>() + ec;
+
+    a.env_off = w.env_off.as<uint64_t>();
+    a.keys = w.keys_un.as<uint32_t>();
+    a.key_shift = key_bits > 32 ? key_bits - 32 : 0;
+    a.vals = w.vals_un.as<uint32_t>();
+    a.recs = w.recs_un.as<SplatRec>();
+    a.gid = w.gid_un.as<uint32_t>();
+    a.rects = w.rects_un.as<ushort4>();
+    a.cap = cap_v;
+
     if (n > 0) {
         tm.begin(SN_STAGE_COUNT);
         ctx->launches += 1;
@@ -221,34 +278,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
         ctx->launches += 2;
         SN_CUDA(launch_block_scan(a.blk_counts, n_blocks, ec, w.env_off.as<uint64_t>(), st));
         tm.end();
-        ctx->launches += 1;
-        SN_CUDA(launch_publish_u64(w.env_off.as<uint64_t>() + ec, ctx->d_tot, st));
-        SN_CUDA(cudaStreamSynchronize(st));
-        V = (int64_t)ctx->h_tot[0];
     }
-    SN_CHECK(V < (int64_t)0xffffffffLL, "too many visible splats in one env chunk (limit 2^32)");
-    const size_t v1 = (size_t)V + 1;
-    SN_ENSURE(w.keys_un, sizeof(uint32_t) * v1);
-    SN_ENSURE(w.keys_s, sizeof(uint32_t) * v1);
-    SN_ENSURE(w.vals_un, sizeof(uint32_t) * v1);
-    SN_ENSURE(w.vals_s, sizeof(uint32_t) * v1);
-    SN_ENSURE(w.recs_un, sizeof(SplatRec) * v1);
-    SN_ENSURE(w.gid_un, sizeof(uint32_t) * v1);
-    SN_ENSURE(w.rects_un, sizeof(ushort4) * v1);
-    SN_ENSURE(w.rects, sizeof(ushort4) * v1);
-    SN_ENSURE(w.tiles, sizeof(uint32_t) * v1);
-    SN_ENSURE(w.pair_off, sizeof(uint64_t) * v1);
-    const int64_t n_batches = (V + kBlock - 1) / kBlock;
-    SN_ENSURE(w.batch_rects, sizeof(ushort4) * std::max<int64_t>(n_batches, 1));
-    SN_ENSURE(w.super_rects, sizeof(ushort4) * std::max<int64_t>((n_batches + kSuperBatch - 1) / kSuperBatch, 1));
-
-    a.env_off = w.env_off.as<uint64_t>();
-    a.keys = w.keys_un.as<uint32_t>();
-    a.key_shift = key_bits > 32 ? key_bits - 32 : 0;
-    a.vals = w.vals_un.as<uint32_t>();
-    a.recs = w.recs_un.as<SplatRec>();
-    a.gid = w.gid_un.as<uint32_t>();
-    a.rects = w.rects_un.as<ushort4>();
 
     BinArgs b{};
     b.ec = ec;
@@ -256,9 +286,10 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     b.tiles_y = tiles_y;
     b.tile_bits = tile_bits;
     b.z_bits = z_bits;
-    b.n_vis = V;
-    b.keys_sorted = w.keys_s.as<uint32_t>();
-    b.vals_sorted = w.vals_s.as<uint32_t>();
+    b.d_nvis = d_nvis;
+    b.cap_v = cap_v;
+    b.d_npairs = w.counts.as<uint64_t>() + 1;
+    b.cap_p = cap_p;
     b.recs_un = w.recs_un.as<SplatRec>();
     b.rects_in = w.rects_un.as<ushort4>();
     b.env_off = w.env_off.as<uint64_t>();
@@ -266,11 +297,13 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     b.batch_rects = w.batch_rects.as<ushort4>();
     b.tiles_touched = w.tiles.as<uint32_t>();
     b.pair_off = w.pair_off.as<uint64_t>();
+    b.ranges = w.ranges.as<uint2>();
 
-    int64_t P = 0;
-    if (V > 0) {
-        size_t tb = std::max(sort_u32_temp_bytes(V), scan_temp_bytes(V + 1));
-        SN_ENSURE(w.temp, tb);
+    const size_t n_ranges = (size_t)ec << tile_bits;
+    SN_ENSURE(w.ranges, sizeof(uint2) * n_ranges);
+    b.ranges = w.ranges.as<uint2>();
+    SN_CUDA(cudaMemsetAsync(w.ranges.p, 0, sizeof(uint2) * n_ranges, st));
+    if (n > 0 && cap_v > 0) {
         tm.begin(SN_STAGE_EMIT);
         ctx->launches += 1;
         if (sp.scene)
@@ -279,106 +312,59 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
             SN_CUDA(launch_avatar_emit(*sp.avatars, sp.pose, a, st));
         tm.end();
         tm.begin(SN_STAGE_DEPTH_SORT);
-        // 32-bit keys (env + top z bits) in 4 radix passes, then an exact fix of equal-key runs
-        SN_CUDA(sort_u32_pairs(w.temp.p, w.temp.cap, w.keys_un.as<uint32_t>(), w.keys_s.as<uint32_t>(),
-                               w.vals_un.as<uint32_t>(), w.vals_s.as<uint32_t>(), V, std::min(key_bits, 32), st));
+        // 32-bit keys (env + top z bits), then an exact fix of equal-key runs
+        const bool in_s = radix_sort_pairs(w.temp.p, w.keys_un.as<uint32_t>(), w.vals_un.as<uint32_t>(),
+                                           w.keys_s.as<uint32_t>(), w.vals_s.as<uint32_t>(), d_nvis, cap_v,
+                                           std::min(key_bits, 32), st, &ctx->launches);
+        SN_CUDA(cudaGetLastError());
+        if (!in_s) {  // even pass count: the sorted arrays are back in the *_un buffers
+            std::swap(w.keys_un, w.keys_s);
+            std::swap(w.vals_un, w.vals_s);
+        }
+        b.keys_sorted = w.keys_s.as<uint32_t>();
+        b.vals_sorted = w.vals_s.as<uint32_t>();
         if (key_bits > 32) {
             ctx->launches += 1;
             SN_CUDA(launch_depth_tie_fix(b, st));
         }
         tm.end();
         tm.begin(SN_STAGE_PERMUTE);
-        ctx->launches += 1;
+        ctx->launches += 2;
         SN_CUDA(launch_permute(b, st));
-        ctx->launches += 1;
-        SN_CUDA(launch_super_rects(w.batch_rects.as<ushort4>(), n_batches, w.super_rects.as<ushort4>(), st));
+        SN_CUDA(launch_super_rects(b, w.super_rects.as<ushort4>(), st));
         tm.end();
-        if (tiled && binning == 1) {  // pair offsets: the radix binner emits from them
-            SN_CUDA(cudaMemsetAsync(w.tiles.as<uint32_t>() + V, 0, sizeof(uint32_t), st));
+        if (tiled && binning == 1) {
             tm.begin(SN_STAGE_PAIR_SCAN);
-            SN_CUDA(scan_tiles(w.temp.p, w.temp.cap, w.tiles.as<uint32_t>(), w.pair_off.as<uint64_t>(), V + 1, st));
+            SN_CUDA(scan_u32_to_u64(w.temp.p, w.tiles.as<uint32_t>(), d_nvis, cap_v, w.pair_off.as<uint64_t>(),
+                                    w.counts.as<uint64_t>() + 1, st, &ctx->launches));
             tm.end();
-            ctx->launches += 1;
-            SN_CUDA(launch_publish_u64(w.pair_off.as<uint64_t>() + V, ctx->d_tot, st));
-            SN_CUDA(cudaStreamSynchronize(st));
-            P = (int64_t)ctx->h_tot[0];
-            SN_CHECK(P < (int64_t)0x7fffffffLL, "too many tile pairs in one env chunk (limit 2^31)");
+            if (cap_p > 0) {
+                SN_ENSURE(w.pkeys_a, sizeof(uint32_t) * cap_p);
+                SN_ENSURE(w.pkeys_b, sizeof(uint32_t) * cap_p);
+                SN_ENSURE(w.pvals_a, sizeof(uint32_t) * cap_p);
+                SN_ENSURE(w.pvals_b, sizeof(uint32_t) * cap_p);
+                b.pair_keys = w.pkeys_a.as<uint32_t>();
+                b.pair_vals = w.pvals_a.as<uint32_t>();
+                tm.begin(SN_STAGE_BIN_COUNT);
+                ctx->launches += 1;
+                SN_CUDA(launch_duplicate(b, st));
+                tm.end();
+                tm.begin(SN_STAGE_BIN_SCATTER);
+                const bool in_b = radix_sort_pairs(w.temp.p, w.pkeys_a.as<uint32_t>(), w.pvals_a.as<uint32_t>(),
+                                                   w.pkeys_b.as<uint32_t>(), w.pvals_b.as<uint32_t>(),
+                                                   b.d_npairs, cap_p, env_bits + tile_bits, st, &ctx->launches);
+                SN_CUDA(cudaGetLastError());
+                if (!in_b) {
+                    std::swap(w.pkeys_a, w.pkeys_b);
+                    std::swap(w.pvals_a, w.pvals_b);
+                }
+                tm.end();
+                tm.begin(SN_STAGE_RANGES);
+                ctx->launches += 1;
+                SN_CUDA(launch_ranges(b, w.pkeys_b.as<uint32_t>(), st));
+                tm.end();
+            }
         }
-    }
-    const size_t n_ranges = (size_t)ec << tile_bits;
-    SN_ENSURE(w.ranges, sizeof(uint2) * n_ranges);
-    SN_CUDA(cudaMemsetAsync(w.ranges.p, 0, sizeof(uint2) * n_ranges, st));
-    if (tiled && binning == 1 && P > 0) {
-        SN_ENSURE(w.pkeys_a, sizeof(uint32_t) * P);
-        SN_ENSURE(w.pkeys_b, sizeof(uint32_t) * P);
-        SN_ENSURE(w.pvals_a, sizeof(uint32_t) * P);
-        SN_ENSURE(w.pvals_b, sizeof(uint32_t) * P);
-        size_t tb = sort_u32_temp_bytes(P);
-        SN_ENSURE(w.temp, tb);
-        b.pair_keys = w.pkeys_a.as<uint32_t>();
-        b.pair_vals = w.pvals_a.as<uint32_t>();
-        tm.begin(SN_STAGE_BIN_COUNT);
-        ctx->launches += 1;
-        SN_CUDA(launch_duplicate(b, st));
-        tm.end();
-        tm.begin(SN_STAGE_BIN_SCATTER);
-        SN_CUDA(sort_u32_pairs(w.temp.p, w.temp.cap, w.pkeys_a.as<uint32_t>(), w.pkeys_b.as<uint32_t>(),
-                               w.pvals_a.as<uint32_t>(), w.pvals_b.as<uint32_t>(), P, env_bits + tile_bits, st));
-        tm.end();
-        tm.begin(SN_STAGE_RANGES);
-        ctx->launches += 1;
-        SN_CUDA(launch_ranges(w.pkeys_b.as<uint32_t>(), P, w.ranges.as<uint2>(), st));
-        tm.end();
-    }
-
-    BlendArgs bl{};
-    bl.cams = ctx->cams.as<sn_camera>();
-    bl.e0 = e0;
-    bl.ec = ec;
-    bl.width = width;
-    bl.height = height;
-    bl.tiles_x = tiles_x;
-    bl.tile_bits = tile_bits;
-    bl.source = !tiled ? 2 : (binning == 1 ? 1 : 0);
-    bl.rects = w.rects.as<ushort4>();
-    bl.batch_rects = w.batch_rects.as<ushort4>();
-    bl.super_rects = w.super_rects.as<ushort4>();
-    bl.mode = sp.mode;
-    bl.ranges = w.ranges.as<uint2>();
-    bl.pair_vals = w.pvals_b.as<uint32_t>();
-    bl.env_off = w.env_off.as<uint64_t>();
-    bl.recs = w.recs_un.as<SplatRec>();
-    bl.order = w.vals_s.as<uint32_t>();
-    bl.color = color;
-    bl.alpha = alpha;
-    bl.depth = depth;
-    bl.depth64 = depth64;
-    bl.contrib = opts ? (pass_id == 0 ? opts->contrib_scene : opts->contrib_layer) : nullptr;
-    if (work) {
-        if (ctx->work_dst[pass_id]) {  // previous chunk's counters still in flight
-            cudaEventSynchronize(ctx->ev_work[pass_id]);
-            ctx->work_dst[pass_id][2] += (int64_t)ctx->h_work[3 * pass_id];
-            ctx->work_dst[pass_id][3] += (int64_t)ctx->h_work[3 * pass_id + 1];
-            ctx->work_dst[pass_id][4] += (int64_t)ctx->h_work[3 * pass_id + 2];
-            ctx->work_dst[pass_id] = nullptr;
-        }
-        SN_ENSURE(ctx->loads, 6 * sizeof(unsigned long long));
-        bl.loads = ctx->loads.as<unsigned long long>() + 3 * pass_id;
-        bl.scans = bl.loads + 1;
-        bl.contribs = bl.loads + 2;
-        SN_CUDA(cudaMemsetAsync(bl.loads, 0, 3 * sizeof(unsigned long long), st));
-    }
-    if (blend_wait) SN_CUDA(cudaStreamWaitEvent(st, blend_wait, 0));  // composite reads the scene frame
-    tm.begin(SN_STAGE_BLEND);
-    ctx->launches += 1;
-    SN_CUDA(launch_blend(bl, st));
-    tm.end();
-    if (work) {
-        SN_CUDA(cudaMemcpyAsync(ctx->h_work + 3 * pass_id, bl.loads, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-        SN_CUDA(cudaEventRecord(ctx->ev_work[pass_id], st));
-        ctx->work_dst[pass_id] = work;
-        work[0] += V;
-        work[1] += P;
     }
 
     w.e0 = e0;
@@ -388,9 +374,98 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     w.tile_bits = tile_bits;
     w.tiled = tiled;
     w.binning = binning;
-    w.n_vis = V;
-    w.n_pairs = P;
+    SN_ENSURE(w.fix, sizeof(uint32_t) * (size_t)ec * width * height);
+    SN_ENSURE(ctx->fixcnt, 2 * sizeof(unsigned));
+    BlendArgs bl{};
+    bl.cams = ctx->cams.as<sn_camera>();
+    bl.e0 = e0;
+    bl.ec = ec;
+    bl.width = width;
+    bl.height = height;
+    bl.tiles_x = tiles_x;
+    bl.mode = sp.mode;
+    bl.pv = view_of(w);
+    if (sp.mode == 2) {
+        SN_CHECK(ctx->pass[0].valid && ctx->pass[0].e0 == e0 && ctx->pass[0].ec == ec,
+                 "layer composite needs the scene pass of the same env chunk");
+        bl.back = view_of(ctx->pass[0]);
+    }
+    bl.color = color;
+    bl.alpha = alpha;
+    bl.depth = depth;
+    bl.derr = derr;
+    bl.contrib = opts ? (pass_id == 0 ? opts->contrib_scene : opts->contrib_layer) : nullptr;
+    bl.fix_list = w.fix.as<uint32_t>();
+    bl.fix_count = ctx->fixcnt.as<unsigned>() + pass_id;
+    SN_CUDA(cudaMemsetAsync(bl.fix_count, 0, sizeof(unsigned), st));
+    if (work) {
+        if (ctx->work_dst[pass_id]) {  // previous chunk's counters still in flight
+            cudaEventSynchronize(ctx->ev_work[pass_id]);
+            for (int k = 0; k < 4; ++k) ctx->work_dst[pass_id][2 + k] += (int64_t)ctx->h_work[4 * pass_id + k];
+            ctx->work_dst[pass_id] = nullptr;
+        }
+        SN_ENSURE(ctx->loads, 8 * sizeof(unsigned long long));
+        bl.loads = ctx->loads.as<unsigned long long>() + 4 * pass_id;
+        bl.scans = bl.loads + 1;
+        bl.contribs = bl.loads + 2;
+        SN_CUDA(cudaMemsetAsync(bl.loads, 0, 4 * sizeof(unsigned long long), st));
+    }
+    if (sp.mode == 2) {
+        const size_t npix = (size_t)(e0 + ec) * width * height;
+        SN_ENSURE(ctx->lcolor, sizeof(float) * 3 * npix);
+        SN_ENSURE(ctx->lalpha, sizeof(float) * npix);
+        SN_ENSURE(ctx->ldepth, sizeof(float) * npix);
+        SN_ENSURE(ctx->lderr, sizeof(float) * npix);
+        SN_ENSURE(ctx->laerr, sizeof(float) * npix);
+        SN_ENSURE(ctx->tile_flag, (size_t)ec * n_tiles);
+        bl.lcolor = ctx->lcolor.as<float>();
+        bl.lalpha = ctx->lalpha.as<float>();
+        bl.ldepth = ctx->ldepth.as<float>();
+        bl.lderr = ctx->lderr.as<float>();
+        bl.laerr = ctx->laerr.as<float>();
+        bl.tile_flag = ctx->tile_flag.as<uint8_t>();
+    }
+    if (pass_id == 0 && ctx->ev_pre) SN_CUDA(cudaEventRecord(ctx->ev_pre, st));  // scene preprocessing done
+    tm.begin(SN_STAGE_BLEND);
+    ctx->launches += sp.mode == 2 ? 1 : 2;  // blend (+ float64 fixup; mode 2's runs after the composite)
+    SN_CUDA(launch_blend(bl, st));
+    tm.end();
+    w.bl = bl;
+    w.work = nullptr;
+    if (work && sp.mode == 2) {  // collected by finish_layer, after the fixups
+        w.work = work;
+    } else if (work) {
+        SN_CUDA(cudaMemcpyAsync(ctx->loads.as<unsigned long long>() + 4 * pass_id + 3, bl.fix_count, sizeof(unsigned),
+                                cudaMemcpyDeviceToDevice, st));
+        SN_CUDA(cudaMemcpyAsync(ctx->h_work + 4 * pass_id, bl.loads, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        SN_CUDA(cudaEventRecord(ctx->ev_work[pass_id], st));
+        ctx->work_dst[pass_id] = work;
+    }
+    // this chunk's (V, P) into mapped host memory: sn_render checks them against the capacities
+    ctx->launches += 1;
+    SN_CUDA(launch_publish_counts(d_nvis, w.counts.as<uint64_t>() + 1, ctx->d_counts + 2 * (2 * chunk_idx + pass_id),
+                                  st));
     w.valid = 1;
+    return SN_OK;
+}
+
+// The deferred composite of the layer pass (mode 2) over the scene frame, on the scene stream once
+// both blends are done: composite_kernel, then the float64 fixups of the layer pass.
+int finish_layer(sn_context *ctx, const sn_render_opts *opts, cudaStream_t st) {
+    PassWs &w = ctx->pass[1];
+    StageTimer tm{ctx, st, opts && opts->stage_ms ? opts->stage_ms + SN_N_STAGES : nullptr, 1};
+    tm.begin(SN_STAGE_COMPOSITE);
+    ctx->launches += 2;
+    SN_CUDA(launch_layer_composite(w.bl, st));
+    tm.end();
+    if (w.work) {
+        SN_CUDA(cudaMemcpyAsync(ctx->loads.as<unsigned long long>() + 4 + 3, w.bl.fix_count, sizeof(unsigned),
+                                cudaMemcpyDeviceToDevice, st));
+        SN_CUDA(cudaMemcpyAsync(ctx->h_work + 4, w.bl.loads, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        SN_CUDA(cudaEventRecord(ctx->ev_work[1], st));
+        ctx->work_dst[1] = w.work;
+        w.work = nullptr;
+    }
     return SN_OK;
 }
 
@@ -432,7 +507,7 @@ int sn_context_create(sn_context **out) {
     if (e == cudaSuccess) e = cudaHostGetDevicePointer(&ctx->d_tot, ctx->h_tot, 0);
     if (e == cudaSuccess) e = cudaHostAlloc(&ctx->h_err, sizeof(int32_t) * 4, cudaHostAllocMapped);
     if (e == cudaSuccess) e = cudaHostGetDevicePointer(&ctx->d_err, ctx->h_err, 0);
-    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_work, sizeof(uint64_t) * 6);
+    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_work, sizeof(uint64_t) * 8);
     if (e != cudaSuccess) {
         delete ctx;
         return fail(SN_ERR_CUDA, std::string("cudaMallocHost: ") + cudaGetErrorString(e));
@@ -451,11 +526,13 @@ int sn_context_destroy(sn_context *ctx) {
     for (auto &w : ctx->pass) {
         for (Buf *b : {&w.vismask, &w.blk_counts, &w.env_off, &w.keys_un, &w.keys_s, &w.vals_un, &w.vals_s, &w.recs_un,
                        &w.gid_un, &w.rects_un, &w.rects, &w.tiles, &w.pair_off, &w.pkeys_a,
-                       &w.pkeys_b, &w.pvals_a, &w.pvals_b, &w.ranges, &w.temp, &w.batch_rects, &w.super_rects})
+                       &w.pkeys_b, &w.pvals_a, &w.pvals_b, &w.ranges, &w.temp, &w.batch_rects, &w.super_rects,
+                       &w.fix, &w.counts})
             free_buf(*b);
     }
-    for (Buf *b : {&ctx->cams, &ctx->times, &ctx->depth64, &ctx->jm, &ctx->eq, &ctx->root, &ctx->err, &ctx->pose_q,
-                   &ctx->pose_t, &ctx->loads})
+    for (Buf *b : {&ctx->cams, &ctx->times, &ctx->derr, &ctx->jm, &ctx->eq, &ctx->root, &ctx->err, &ctx->pose_q,
+                   &ctx->pose_t, &ctx->loads, &ctx->fixcnt, &ctx->lcolor, &ctx->lalpha, &ctx->ldepth, &ctx->lderr,
+                   &ctx->laerr, &ctx->tile_flag})
         free_buf(*b);
     if (ctx->have_events) {
         for (auto &p : ctx->ev)
@@ -466,10 +543,11 @@ int sn_context_destroy(sn_context *ctx) {
     if (ctx->h_work) cudaFreeHost(ctx->h_work);
     if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
     if (ctx->side) cudaStreamDestroy(ctx->side);
-    for (cudaEvent_t ev : {ctx->ev_inputs, ctx->ev_scene, ctx->ev_layer})
+    for (cudaEvent_t ev : {ctx->ev_inputs, ctx->ev_scene, ctx->ev_layer, ctx->ev_pre})
         if (ev) cudaEventDestroy(ev);
     if (ctx->h_tot) cudaFreeHost(ctx->h_tot);
     if (ctx->h_err) cudaFreeHost(ctx->h_err);
+    if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
     delete ctx;
     return SN_OK;
 }
@@ -477,6 +555,12 @@ int sn_context_destroy(sn_context *ctx) {
 int sn_context_kernel_launches(const sn_context *ctx, int64_t *n) {
     SN_CHECK(ctx && n, "null argument");
     *n = ctx->launches;
+    return SN_OK;
+}
+
+int sn_context_render_retries(const sn_context *ctx, int64_t *n) {
+    SN_CHECK(ctx && n, "null argument");
+    *n = ctx->retries;
     return SN_OK;
 }
 
@@ -493,14 +577,20 @@ int sn_context_workspace_bytes(const sn_context *ctx, size_t *bytes) {
         for (const Buf *b : {&w.vismask, &w.blk_counts, &w.env_off, &w.keys_un, &w.keys_s, &w.vals_un, &w.vals_s,
                              &w.recs_un, &w.gid_un, &w.rects_un, &w.rects, &w.tiles, &w.pair_off,
                              &w.pkeys_a, &w.pkeys_b, &w.pvals_a, &w.pvals_b, &w.ranges, &w.temp,
-                             &w.batch_rects, &w.super_rects})
+                             &w.batch_rects, &w.super_rects, &w.fix})
             t += b->cap;
-    for (const Buf *b : {&ctx->cams, &ctx->times, &ctx->depth64, &ctx->jm, &ctx->eq, &ctx->root, &ctx->err,
-                         &ctx->pose_q, &ctx->pose_t})
+    for (const Buf *b : {&ctx->cams, &ctx->times, &ctx->derr, &ctx->jm, &ctx->eq, &ctx->root, &ctx->err,
+                         &ctx->pose_q, &ctx->pose_t, &ctx->lcolor, &ctx->lalpha, &ctx->ldepth, &ctx->lderr,
+                         &ctx->laerr, &ctx->tile_flag})
         t += b->cap;
     *bytes = t;
     return SN_OK;
 }
+
+static int render_once(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, const sn_avatars *avatars,
+                       const sn_camera *cams, const double *sim_times, int32_t n_envs, const sn_render_opts *opts,
+                       float *color, float *alpha, float *depth, cudaStream_t st, uint64_t z_lo, int z_bits, int chunk,
+                       int tiled, bool with_layer, bool with_avatars);
 
 int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, const sn_avatars *avatars,
               const sn_camera *cams, const double *sim_times, int32_t n_envs, const sn_render_opts *opts, float *color,
@@ -550,6 +640,70 @@ int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, con
         ctx->have_events = true;
     }
 
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        const int n_chunks = (n_envs + chunk - 1) / chunk;
+        if ((size_t)(2 * n_chunks) > ctx->counts_cap) {
+            SN_CUDA(cudaDeviceSynchronize());
+            if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
+            ctx->h_counts = nullptr;
+            ctx->counts_cap = 0;
+            SN_CUDA(cudaHostAlloc(&ctx->h_counts, sizeof(uint64_t) * 2 * 2 * n_chunks, cudaHostAllocMapped));
+            SN_CUDA(cudaHostGetDevicePointer(&ctx->d_counts, ctx->h_counts, 0));
+            ctx->counts_cap = 2 * n_chunks;
+        }
+        std::memset(ctx->h_counts, 0, sizeof(uint64_t) * 2 * 2 * n_chunks);
+        ctx->h_err[0] = 0;
+        r = render_once(ctx, scene, layer, avatars, cams, sim_times, n_envs, opts, color, alpha, depth, st, z_lo,
+                        z_bits, chunk, tiled, with_layer, with_avatars);
+        if (r != SN_OK) return r;
+        // the one host synchronization of a render: every pass published its counts (and the pose
+        // kernel its error flag) into mapped memory; check them against the capacities
+        SN_CUDA(cudaStreamSynchronize(st));
+        SN_CHECK(ctx->h_err[0] == 0, "sample time must be nonnegative");
+        bool grow = false;
+        for (int p = 0; p < 2; ++p) {
+            uint64_t need_v = 0, need_p = 0, sum_v = 0, sum_p = 0, last_v = 0, last_p = 0;
+            for (int c = 0; c < n_chunks; ++c) {
+                const uint64_t v = ctx->h_counts[2 * (2 * c + p)], q = ctx->h_counts[2 * (2 * c + p) + 1];
+                need_v = std::max(need_v, v);
+                need_p = std::max(need_p, q);
+                sum_v += v;
+                sum_p += q;
+                last_v = v;
+                last_p = q;
+            }
+            SN_CHECK(need_v < 0xffffffffull, "too many visible splats in one env chunk (limit 2^32)");
+            SN_CHECK(need_p < 0x7fffffffull, "too many tile pairs in one env chunk (limit 2^31)");
+            PassWs &w = ctx->pass[p];
+            if (need_v > w.cap_v) {
+                w.cap_v = need_v + need_v / 4 + 1024;
+                grow = true;
+            }
+            if (need_p > w.cap_p) {
+                w.cap_p = need_p + need_p / 4 + 1024;
+                grow = true;
+            }
+            w.n_vis = (int64_t)last_v;
+            w.n_pairs = (int64_t)last_p;
+            if (!grow && opts && opts->work && (p == 0 || with_layer || with_avatars)) {
+                opts->work[6 * p] += (int64_t)sum_v;
+                opts->work[6 * p + 1] += (int64_t)sum_p;
+            }
+        }
+        if (!grow) return SN_OK;
+        // larger buffers: drop the partial work counters of the failed attempt and render again
+        resolve_all(ctx);
+        ctx->retries += 1;
+    }
+    return fail(SN_ERR_NOMEM, "workspace capacity did not converge");
+}
+
+static int render_once(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, const sn_avatars *avatars,
+                       const sn_camera *cams, const double *sim_times, int32_t n_envs, const sn_render_opts *opts,
+                       float *color, float *alpha, float *depth, cudaStream_t st, uint64_t z_lo, int z_bits, int chunk,
+                       int tiled, bool with_layer, bool with_avatars) {
+    const int W = cams[0].width, H = cams[0].height;
+    int r = SN_OK;
     SN_ENSURE(ctx->cams, sizeof(sn_camera) * n_envs);
     {
         const size_t need = (sizeof(sn_camera) + sizeof(double)) * n_envs;
@@ -566,10 +720,10 @@ int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, con
     // after its uploads, so the staging buffer is free to overwrite here
     std::memcpy(ctx->h_stage, cams, sizeof(sn_camera) * n_envs);
     SN_CUDA(cudaMemcpyAsync(ctx->cams.p, ctx->h_stage, sizeof(sn_camera) * n_envs, cudaMemcpyHostToDevice, st));
-    double *depth64 = nullptr;
+    float *derr = nullptr;  // scene depth error bounds for the compositor
     if (with_avatars || with_layer) {
-        SN_ENSURE(ctx->depth64, sizeof(double) * (size_t)n_envs * W * H);
-        depth64 = ctx->depth64.as<double>();
+        SN_ENSURE(ctx->derr, sizeof(float) * (size_t)n_envs * W * H);
+        derr = ctx->derr.as<float>();
     }
     if (opts && opts->stats) SN_CUDA(cudaMemsetAsync(opts->stats, 0, sizeof(sn_stats) * n_envs, st));
 
@@ -578,10 +732,16 @@ int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, con
     cudaStream_t lst = st;
     if (two_pass) {
         if (!ctx->side) {
-            SN_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+            // highest priority: the layer pass is short and its kernels (and host round trips) must
+            // not queue behind the scene blend's CTAs, or the composite waits for it
+            int lo = 0, hi = 0;
+            SN_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            const char *pe = getenv("SN_LAYER_PRIORITY");
+            SN_CUDA(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, (pe && pe[0] == '0') ? lo : hi));
             SN_CUDA(cudaEventCreateWithFlags(&ctx->ev_inputs, cudaEventDisableTiming));
             SN_CUDA(cudaEventCreateWithFlags(&ctx->ev_scene, cudaEventDisableTiming));
             SN_CUDA(cudaEventCreateWithFlags(&ctx->ev_layer, cudaEventDisableTiming));
+            SN_CUDA(cudaEventCreateWithFlags(&ctx->ev_pre, cudaEventDisableTiming));
         }
         lst = ctx->side;
         SN_CUDA(cudaEventRecord(ctx->ev_inputs, st));
@@ -591,62 +751,59 @@ int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, con
     PassSpec scene_spec;
     scene_spec.scene = scene;
     scene_spec.mode = cams[0].has_background ? 0 : 1;
+    PassSpec layer_spec;
+    layer_spec.mode = 2;
+    if (with_layer) layer_spec.scene = layer;
+    // Per env chunk: the scene pass on the caller's stream and the layer pass on the side stream run
+    // concurrently (the layer blend writes its own frame); then, on the caller's stream, the
+    // composite merges the layer frame and the layer's float64 fixups run (they read both passes'
+    // workspaces, so the next chunk's passes are queued behind them).
     for (int e0 = 0; e0 < n_envs; e0 += chunk) {
-        int ec = std::min(chunk, n_envs - e0);
-        r = run_pass(ctx, 0, scene_spec, e0, ec, W, H, tiled, z_lo, z_bits, opts, color, alpha, depth, depth64, st);
+        const int ec = std::min(chunk, n_envs - e0);
+        r = run_pass(ctx, 0, scene_spec, e0, ec, W, H, tiled, z_lo, z_bits, opts, color, alpha, depth, derr, st,
+                     e0 / chunk);
         if (r != SN_OK) return r;
-    }
-    if (two_pass) SN_CUDA(cudaEventRecord(ctx->ev_scene, st));
-    if (with_layer) {
-        PassSpec layer_spec;
-        layer_spec.scene = layer;
-        layer_spec.mode = 2;
-        for (int e0 = 0; e0 < n_envs; e0 += chunk) {
-            int ec = std::min(chunk, n_envs - e0);
-            r = run_pass(ctx, 1, layer_spec, e0, ec, W, H, tiled, z_lo, z_bits, opts, color, alpha, depth, depth64,
-                         lst, ctx->ev_scene);
-            if (r != SN_OK) return r;
+        if (!two_pass) continue;
+        // the layer pass starts once the scene's preprocessing is done: it then overlaps the scene
+        // blend (issue-bound, long) instead of competing with the scene's memory-bound stages
+        {
+            const char *we = getenv("SN_LAYER_WAIT_PRE");
+            if (we && we[0] == '1') SN_CUDA(cudaStreamWaitEvent(lst, ctx->ev_pre, 0));
         }
-        SN_CUDA(cudaEventRecord(ctx->ev_layer, lst));
-        SN_CUDA(cudaStreamWaitEvent(st, ctx->ev_layer, 0));
-        return SN_OK;
-    }
-    if (!with_avatars) return SN_OK;
-
-    const int A = avatars->n_avatars, J = avatars->n_joints;
-    SN_ENSURE(ctx->times, sizeof(double) * n_envs);
-    double *h_times = reinterpret_cast<double *>(static_cast<char *>(ctx->h_stage) + sizeof(sn_camera) * n_envs);
-    std::memcpy(h_times, sim_times, sizeof(double) * n_envs);
-    SN_CUDA(cudaMemcpyAsync(ctx->times.p, h_times, sizeof(double) * n_envs, cudaMemcpyHostToDevice, lst));
-    SN_ENSURE(ctx->jm, sizeof(double) * (size_t)n_envs * A * J * 12);
-    SN_ENSURE(ctx->eq, sizeof(double) * (size_t)n_envs * A * J * 4);
-    SN_ENSURE(ctx->root, sizeof(double) * (size_t)n_envs * A * 12);
-    SN_ENSURE(ctx->err, sizeof(int32_t));
-    SN_CUDA(cudaMemsetAsync(ctx->err.p, 0, sizeof(int32_t), lst));
-    StageTimer ptm{ctx, lst, opts && opts->stage_ms ? opts->stage_ms + SN_N_STAGES : nullptr, 1};
-    ptm.begin(SN_STAGE_POSE);
-    ctx->launches += 1;
-    SN_CUDA(launch_pose(*avatars, ctx->times.as<double>(), n_envs, nullptr, nullptr, ctx->jm.as<double>(),
-                        ctx->eq.as<double>(), ctx->root.as<double>(), ctx->err.as<int32_t>(), lst));
-    ptm.end();
-    ctx->launches += 1;
-    SN_CUDA(launch_publish_i32(ctx->err.as<int32_t>(), ctx->d_err, lst));
-    SN_CUDA(cudaStreamSynchronize(lst));
-    SN_CHECK(ctx->h_err[0] == 0, "sample time must be nonnegative");
-
-    PassSpec av_spec;
-    av_spec.avatars = avatars;
-    av_spec.pose = PoseView{ctx->jm.as<double>(), ctx->eq.as<double>(), ctx->root.as<double>(), J, A};
-    av_spec.avatar_active = opts ? opts->avatar_active : nullptr;
-    av_spec.mode = 2;
-    for (int e0 = 0; e0 < n_envs; e0 += chunk) {
-        int ec = std::min(chunk, n_envs - e0);
-        r = run_pass(ctx, 1, av_spec, e0, ec, W, H, tiled, z_lo, z_bits, opts, color, alpha, depth, depth64, lst,
-                     ctx->ev_scene);
+        if (with_avatars && e0 == 0) {
+            const int A = avatars->n_avatars, J = avatars->n_joints;
+            SN_ENSURE(ctx->times, sizeof(double) * n_envs);
+            double *h_times =
+                reinterpret_cast<double *>(static_cast<char *>(ctx->h_stage) + sizeof(sn_camera) * n_envs);
+            std::memcpy(h_times, sim_times, sizeof(double) * n_envs);
+            SN_CUDA(cudaMemcpyAsync(ctx->times.p, h_times, sizeof(double) * n_envs, cudaMemcpyHostToDevice, lst));
+            SN_ENSURE(ctx->jm, sizeof(double) * (size_t)n_envs * A * J * 12);
+            SN_ENSURE(ctx->eq, sizeof(double) * (size_t)n_envs * A * J * 4);
+            SN_ENSURE(ctx->root, sizeof(double) * (size_t)n_envs * A * 12);
+            SN_ENSURE(ctx->err, sizeof(int32_t));
+            SN_CUDA(cudaMemsetAsync(ctx->err.p, 0, sizeof(int32_t), lst));
+            StageTimer ptm{ctx, lst, opts && opts->stage_ms ? opts->stage_ms + SN_N_STAGES : nullptr, 1};
+            ptm.begin(SN_STAGE_POSE);
+            ctx->launches += 1;
+            SN_CUDA(launch_pose(*avatars, ctx->times.as<double>(), n_envs, nullptr, nullptr, ctx->jm.as<double>(),
+                                ctx->eq.as<double>(), ctx->root.as<double>(), ctx->err.as<int32_t>(), lst));
+            ptm.end();
+            ctx->launches += 1;
+            SN_CUDA(launch_publish_i32(ctx->err.as<int32_t>(), ctx->d_err, lst));  // checked by sn_render
+            layer_spec.avatars = avatars;
+            layer_spec.pose = PoseView{ctx->jm.as<double>(), ctx->eq.as<double>(), ctx->root.as<double>(), J, A};
+            layer_spec.avatar_active = opts ? opts->avatar_active : nullptr;
+        }
+        r = run_pass(ctx, 1, layer_spec, e0, ec, W, H, tiled, z_lo, z_bits, opts, color, alpha, depth, derr, lst,
+                     e0 / chunk);
         if (r != SN_OK) return r;
+        SN_CUDA(cudaEventRecord(ctx->ev_layer, lst));
+        SN_CUDA(cudaStreamWaitEvent(st, ctx->ev_layer, 0));  // both blends done: composite on st
+        r = finish_layer(ctx, opts, st);
+        if (r != SN_OK) return r;
+        SN_CUDA(cudaEventRecord(ctx->ev_scene, st));
+        SN_CUDA(cudaStreamWaitEvent(lst, ctx->ev_scene, 0));  // next chunk's layer pass reuses the buffers
     }
-    SN_CUDA(cudaEventRecord(ctx->ev_layer, lst));
-    SN_CUDA(cudaStreamWaitEvent(st, ctx->ev_layer, 0));
     return SN_OK;
 }
 
@@ -828,6 +985,12 @@ int sn_skin_lbs(sn_context *ctx, const sn_avatars *avatars, int32_t avatar, int6
     PoseView pv{jm, eq, root, J, 1};
     ctx->launches += 1;
     SN_CUDA(launch_skin_range(*avatars, g_begin, g_count, pv, out_positions, out_rotations, st));
+    return SN_OK;
+}
+
+int sn_selftest_fast_exp(double *max_rel_err) {
+    SN_CHECK(max_rel_err != nullptr, "null argument");
+    SN_CUDA(fast_exp_selftest(max_rel_err));
     return SN_OK;
 }
 

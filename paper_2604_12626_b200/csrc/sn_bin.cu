@@ -8,16 +8,26 @@
 // (env | tile) key alone (17 bits at 64 envs x 1,200 tiles) keeps depth order inside each tile,
 // which is the semantics of a 64-bit (env | tile | depth) key without sorting the depth bits
 // twice.
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
-
 #include "sn_common.cuh"
 #include "sn_internal.h"
+
+#include <algorithm>
 
 
 namespace sn {
 
 namespace {
+
+// Visible splats / tile pairs of the pass, read on the device (clamped to the host capacity: an
+// overflowing pass is detected by the host afterwards and re-run with larger buffers).
+__device__ __forceinline__ int64_t n_vis_of(const BinArgs &b) {
+    const uint64_t n = *b.d_nvis;
+    return (int64_t)(n < b.cap_v ? n : b.cap_v);
+}
+__device__ __forceinline__ int64_t n_pairs_of(const BinArgs &b) {
+    const uint64_t n = *b.d_npairs;
+    return (int64_t)(n < b.cap_p ? n : b.cap_p);
+}
 
 __device__ __forceinline__ ushort4 rect_union(ushort4 a, ushort4 c) {
     return make_ushort4(min(a.x, c.x), max(a.y, c.y), min(a.z, c.z), max(a.w, c.w));
@@ -41,9 +51,11 @@ __device__ __forceinline__ ushort4 warp_rect_union(ushort4 r) {
 // where the emit wrote them: the blend gathers them through the sort's index.
 __global__ void __launch_bounds__(kBlock) permute_kernel(BinArgs b) {
     __shared__ ushort4 s_u[kBlock / 32];
+    const int64_t n_vis = n_vis_of(b);
+    if ((int64_t)blockIdx.x * kBlock >= n_vis) return;
     int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     ushort4 mine = make_ushort4(0xffff, 0, 0xffff, 0);  // empty
-    if (i < b.n_vis) mine = b.rects_in[b.vals_sorted[i]];
+    if (i < n_vis) mine = b.rects_in[b.vals_sorted[i]];
     ushort4 u = warp_rect_union(mine);
     if ((threadIdx.x & 31) == 0) s_u[threadIdx.x >> 5] = u;
     __syncthreads();
@@ -52,7 +64,7 @@ __global__ void __launch_bounds__(kBlock) permute_kernel(BinArgs b) {
         for (int w = 1; w < kBlock / 32; ++w) t = rect_union(t, s_u[w]);
         b.batch_rects[blockIdx.x] = t;
     }
-    if (i >= b.n_vis) return;
+    if (i >= n_vis) return;
     ushort4 r = mine;
     b.rects_out[i] = r;
     b.tiles_touched[i] = (uint32_t)(r.y - r.x + 1) * (uint32_t)(r.w - r.z + 1);
@@ -65,10 +77,12 @@ __global__ void __launch_bounds__(kBlock) duplicate_kernel(BinArgs b) {
     __shared__ uint64_t s_off[kBlock + 1];
     __shared__ ushort4 s_rect[kBlock];
     __shared__ uint32_t s_env[kBlock];
+    const int64_t n_vis = n_vis_of(b);
     int64_t i0 = (int64_t)blockIdx.x * kBlock;
+    if (i0 >= n_vis) return;
     int t = threadIdx.x;
     int64_t i = i0 + t;
-    int cnt = (int)min((int64_t)kBlock, b.n_vis - i0);
+    int cnt = (int)min((int64_t)kBlock, n_vis - i0);
     if (t < cnt) {
         s_off[t] = b.pair_off[i];
         s_rect[t] = b.rects_out[i];
@@ -80,6 +94,7 @@ __global__ void __launch_bounds__(kBlock) duplicate_kernel(BinArgs b) {
     __syncthreads();
     uint64_t base = s_off[0];
     uint64_t total = s_off[cnt] - base;
+    if (base + total > b.cap_p) total = base < b.cap_p ? b.cap_p - base : 0;  // overflow: re-run later
     for (uint64_t k = t; k < total; k += kBlock) {
         uint64_t gk = base + k;
         int lo = 0, hi = cnt - 1;  // last splat with s_off <= gk
@@ -100,16 +115,19 @@ __global__ void __launch_bounds__(kBlock) duplicate_kernel(BinArgs b) {
     }
 }
 
-__global__ void __launch_bounds__(kBlock) ranges_kernel(const uint32_t *keys, int64_t n, uint2 *ranges) {
+__global__ void __launch_bounds__(kBlock) ranges_kernel(BinArgs b, const uint32_t *keys) {
+    const int64_t n = n_pairs_of(b);
     int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (i >= n) return;
+    uint2 *ranges = b.ranges;
     uint32_t k = keys[i];
     if (i == 0 || keys[i - 1] != k) ranges[k].x = (uint32_t)i;
     if (i == n - 1 || keys[i + 1] != k) ranges[k].y = (uint32_t)(i + 1);
 }
 
-__global__ void __launch_bounds__(kBlock) super_rects_kernel(const ushort4 *batch_rects, int64_t n_batches,
-                                                            ushort4 *super_rects) {
+__global__ void __launch_bounds__(kBlock) super_rects_kernel(BinArgs b, ushort4 *super_rects) {
+    const ushort4 *batch_rects = b.batch_rects;
+    const int64_t n_batches = (n_vis_of(b) + kBlock - 1) / kBlock;
     int64_t sb = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     int64_t b0 = sb * kSuperBatch;
     if (b0 >= n_batches) return;
@@ -128,12 +146,13 @@ __device__ __forceinline__ bool z_less(const SplatRec *recs, uint32_t a, uint32_
 }
 
 __global__ void __launch_bounds__(kBlock) tie_fix_kernel(BinArgs b) {
+    const int64_t n_vis = n_vis_of(b);
     int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    if (i >= b.n_vis) return;
+    if (i >= n_vis) return;
     const uint32_t k = b.keys_sorted[i];
     if (i > 0 && b.keys_sorted[i - 1] == k) return;  // not a run start
     int64_t e = i + 1;
-    while (e < b.n_vis && b.keys_sorted[e] == k) ++e;
+    while (e < n_vis && b.keys_sorted[e] == k) ++e;
     const int64_t L = e - i;
     if (L < 2) return;
     uint32_t *v = b.vals_sorted + i;
@@ -172,62 +191,47 @@ __global__ void __launch_bounds__(kBlock) tie_fix_kernel(BinArgs b) {
 
 }  // namespace
 
-cudaError_t launch_depth_tie_fix(const BinArgs &b, cudaStream_t s) {
-    if (b.n_vis == 0) return cudaSuccess;
-    tie_fix_kernel<<<(unsigned)((b.n_vis + kBlock - 1) / kBlock), kBlock, 0, s>>>(b);
+__global__ void publish_counts_kernel(const uint64_t *v, const uint64_t *p, volatile uint64_t *dst) {
+    dst[0] = *v;
+    dst[1] = *p;
+}
+
+cudaError_t launch_publish_counts(const uint64_t *v, const uint64_t *p, uint64_t *mapped_dst, cudaStream_t s) {
+    publish_counts_kernel<<<1, 1, 0, s>>>(v, p, mapped_dst);
     return cudaGetLastError();
 }
 
-cudaError_t launch_super_rects(const ushort4 *batch_rects, int64_t n_batches, ushort4 *super_rects, cudaStream_t s) {
-    int64_t n_super = (n_batches + kSuperBatch - 1) / kSuperBatch;
-    if (n_super == 0) return cudaSuccess;
-    super_rects_kernel<<<(unsigned)((n_super + kBlock - 1) / kBlock), kBlock, 0, s>>>(batch_rects, n_batches,
-                                                                                      super_rects);
+static unsigned grid_of(uint64_t cap) { return (unsigned)std::max<uint64_t>(1, (cap + kBlock - 1) / kBlock); }
+
+cudaError_t launch_depth_tie_fix(const BinArgs &b, cudaStream_t s) {
+    if (b.cap_v == 0) return cudaSuccess;
+    tie_fix_kernel<<<grid_of(b.cap_v), kBlock, 0, s>>>(b);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_super_rects(const BinArgs &b, ushort4 *super_rects, cudaStream_t s) {
+    if (b.cap_v == 0) return cudaSuccess;
+    const uint64_t n_super = (b.cap_v + (uint64_t)kBlock * kSuperBatch - 1) / ((uint64_t)kBlock * kSuperBatch);
+    super_rects_kernel<<<grid_of(n_super), kBlock, 0, s>>>(b, super_rects);
     return cudaGetLastError();
 }
 
 cudaError_t launch_permute(const BinArgs &b, cudaStream_t s) {
-    if (b.n_vis == 0) return cudaSuccess;
-    permute_kernel<<<(unsigned)((b.n_vis + kBlock - 1) / kBlock), kBlock, 0, s>>>(b);
+    if (b.cap_v == 0) return cudaSuccess;
+    permute_kernel<<<grid_of(b.cap_v), kBlock, 0, s>>>(b);
     return cudaGetLastError();
 }
 
 cudaError_t launch_duplicate(const BinArgs &b, cudaStream_t s) {
-    if (b.n_vis == 0) return cudaSuccess;
-    duplicate_kernel<<<(unsigned)((b.n_vis + kBlock - 1) / kBlock), kBlock, 0, s>>>(b);
+    if (b.cap_v == 0) return cudaSuccess;
+    duplicate_kernel<<<grid_of(b.cap_v), kBlock, 0, s>>>(b);
     return cudaGetLastError();
 }
 
-cudaError_t launch_ranges(const uint32_t *keys_sorted, int64_t n_pairs, uint2 *ranges, cudaStream_t s) {
-    if (n_pairs == 0) return cudaSuccess;
-    ranges_kernel<<<(unsigned)((n_pairs + kBlock - 1) / kBlock), kBlock, 0, s>>>(keys_sorted, n_pairs, ranges);
+cudaError_t launch_ranges(const BinArgs &b, const uint32_t *keys_sorted, cudaStream_t s) {
+    if (b.cap_p == 0) return cudaSuccess;
+    ranges_kernel<<<grid_of(b.cap_p), kBlock, 0, s>>>(b, keys_sorted);
     return cudaGetLastError();
-}
-
-size_t sort_u32_temp_bytes(int64_t n) {
-    size_t bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
-                                    (const uint32_t *)nullptr, (uint32_t *)nullptr, (int64_t)n, 0, 32);
-    return bytes;
-}
-
-cudaError_t sort_u32_pairs(void *temp, size_t temp_bytes, const uint32_t *k_in, uint32_t *k_out, const uint32_t *v_in,
-                           uint32_t *v_out, int64_t n, int bits, cudaStream_t s) {
-    if (n == 0) return cudaSuccess;
-    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k_in, k_out, v_in, v_out, n, 0, bits, s);
-}
-
-size_t scan_temp_bytes(int64_t n) {
-    size_t bytes = 0;
-    cub::DeviceScan::ExclusiveScan(nullptr, bytes, (const uint32_t *)nullptr, (uint64_t *)nullptr, cub::Sum(),
-                                   (uint64_t)0, (int64_t)n);
-    return bytes;
-}
-
-cudaError_t scan_tiles(void *temp, size_t temp_bytes, const uint32_t *tiles_touched, uint64_t *pair_off, int64_t n,
-                       cudaStream_t s) {
-    // pair_off has n + 1 entries: scan n + 1 inputs where the last reads a zero pad
-    return cub::DeviceScan::ExclusiveScan(temp, temp_bytes, tiles_touched, pair_off, cub::Sum(), (uint64_t)0, n, s);
 }
 
 }  // namespace sn

@@ -1,30 +1,45 @@
 // sn_blend.cu -- K7/K8: per-tile front-to-back compositing with fused finalize / composite.
 //
-// One 256-thread CTA per (tile, env); thread = pixel. The tile's depth-ordered splat list is
-// walked in batches of 256: each thread gathers one 64-byte record into shared memory, then all
-// pixels evaluate the batch from shared memory (broadcast reads, no bank conflicts). A CTA-wide
-// vote (__syncthreads_count) stops the walk once every pixel's transmittance fell below 1e-4.
+// One 256-thread CTA per (tile, env); thread = pixel, warp = 8 x 4 pixel block. The tile's
+// depth-ordered splats are walked in batches of 256: each thread gathers one 64-byte record into
+// shared memory, then every warp walks the batch entries whose support can reach its block
+// (a conservative per-warp mask), reading them as shared-memory broadcasts. A CTA-wide vote
+// (__syncthreads_count) stops the walk once every pixel is saturated.
 //
-// Per-pixel semantics are _kernels_cy.pyx:64-86 in float64 for the decision chain (d2 test,
-// alpha, transmittance) so contributor counts equal the reference's; colour accumulates in fp32.
-// The epilogue is _finalize (renderer.py:67-77) and, for the avatar layer, composite
-// (renderer.py:151-166) against the scene frame already in the output buffers.
+// Numerics (the reference is float64, _kernels_cy.pyx:64-86): the per-contribution chain runs in
+// float32 with a rigorous running error bound, and every discrete decision is either certain or
+// resolved in float64:
+//   * d2 <= 9: each gathered splat is re-expressed, in float64, in its conic's principal axes
+//     relative to the tile centre: d2 = l1 u1^2 + l2 u2^2, u1 = e1.o + U1, u2 = e2.o + U2
+//     (o = pixel - tile centre, |o| <= 7.5). Every float term is then small -- no cancellation
+//     even for camera-hugging splats whose mean is thousands of pixels away -- and a per-(splat,
+//     tile) bound E9 on |d2_f - d2| over {d2 <= 9.1} is computed at gather time. Pixels with
+//     |d2_f - 9| <= E9 recompute d2 exactly in float64 (rare).
+//   * alpha = min(.99, o e^(-d2/2)): relative error eps = E9 / 2 + kEpsExp (ex2.approx, argument
+//     and product roundings; the ex2 bound is verified by sn_selftest_fast_exp).
+//   * T < 1e-4: the absolute error of T is tracked per pixel, err' = err (1 - a) + w eps + 2.5 u T'.
+//     When T is within err of 1e-4 the pixel is "ambiguous": it is appended to a fixup list and
+//     recomputed by fixup_kernel, a warp-per-pixel float64 walk with the reference's operation
+//     order (the previous, fully float64 blend), which also writes its outputs.
+//   * composite (mode 2): depth_front < depth_back and alpha >= 0.5 are decided only when the
+//     tracked bounds separate them; otherwise the pixel goes to the fixup, which recomputes the
+//     scene pixel and the layer pixel in float64 and composites exactly.
+// So the discrete outputs (contributor counts, composite choices) are the float64 chain's, and
+// the continuous ones carry float32 error (~1e-6, against the 2e-3 RGB / 1e-4 depth bars).
 #include "sn_common.cuh"
 #include "sn_internal.h"
+
+#include <cstring>
+
+#ifdef SN_BLEND_PROF
+__device__ unsigned long long g_blend_prof[16];
+#endif
 
 namespace sn {
 
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-
-// Shared-memory form of a record: a float32 copy of the geometry relative to the tile origin for
-// the pre-filter, the float64 decision-chain fields, colour unpacked to float. 96 bytes.
-struct __align__(16) BlendRec {
-    float mxr, myr, caf, cb2f;  // mean - tile origin, conic (a, 2b) in float32
-    float ccf, r, g, b;
-    double mx, my, ca, cb2, cc, alpha, z, pad;
-};
 
 // 2^(j/64), j = 0..63 (round to nearest)
 __constant__ double kExp2Tbl[64] = {
@@ -63,6 +78,121 @@ __constant__ double kExp2Tbl[64] = {
         (out) = __hiloint2double(__double2hiint(_v) + ((_n >> 6) << 20), __double2loint(_v));    \
     } while (0)
 
+// ---- float32 chain error constants (see the header comment) ----
+constexpr float kEpsExp = 2.0e-6f;     // ex2.approx (<= 2^-21 asserted) + argument, alpha, product roundings
+constexpr float kEpsExact = 2.3e-6f;   // same, when d2 came from float64 (rounded to float: 4.5 u)
+constexpr float kU25 = 1.5e-7f;        // 2.5 u: roundings of 1 - a and T (1 - a)
+constexpr float kTLo = 9.99999e-05f;   // 1e-4 (1 - 1e-6): below it (with the bound) T < 1e-4 for sure
+constexpr float kTHi = 1.000001e-04f;  // 1e-4 (1 + 1e-6)
+constexpr float kNegHalfLog2e = -0.72134752044448170f;
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Shared-memory forms of a record: the float32 chain's fields (64 B: principal-axis offsets and
+// directions, eigenvalues, the decision thresholds 9 -/+ E9, alpha, z, the alpha error bound,
+// colour) and the float64 fields of the exact d2 test (40 B).
+struct __align__(16) FRec {
+    float U1, U2, e1x, e1y;
+    float l1, l2, thr_out, thr_in;
+    float alpha, z, ka, kb;  // alpha's relative error bound: eps(d2) = ka d2 + kb
+    float r, g, b, pad;
+};
+struct DRec {
+    double mx, my, ca, cb2, cc;
+};
+
+// The splat's d2 in its conic's principal axes, relative to the tile centre: (mx, my) = mean - tile
+// centre, conic (ca, cb2, cc) = (a, 2b, c). d2(o) = l1 (e1.o - e1.m)^2 + l2 (e2.o - e2.m)^2 with
+// e2 = (-e1y, e1x). Fills U1 = -e1.m, U2 = -e2.m, e1, l1 >= l2, the thresholds 9 -/+ E(9.1) and
+// the alpha error coefficients, from the float error of d2 at a pixel with |o| <= 7.5 sqrt(2):
+//   |u_k error| <= u S_k, S_k = 2 |U_k| + 21.3 + 3.02 / sqrt(l_k)   (valid while d2 <= 9.1),
+//   E(d2) = 1.5 [2 u sqrt(d2) (sqrt(l1) S1 + sqrt(l2) S2) + 7 u d2] + 1e-15 (l1 / l2) 9,
+//   eps(d2) = E(d2) / 2 + kEpsExp <= ka d2 + kb   (sqrt(d2) <= (d2 + 1) / 2).
+// An ill-conditioned or non-finite conic gets thresholds that send every pixel to float64.
+__device__ __forceinline__ void principal_form(double mx, double my, double ca, double cb2, double cc, FRec &f) {
+    const double b = 0.5 * cb2;
+    const double h = 0.5 * (ca - cc);
+    const double r = sqrt(h * h + b * b);
+    const double l1 = 0.5 * (ca + cc) + r;
+    const double det = ca * cc - b * b;
+    const double l2 = det / l1;
+    double vx = h >= 0.0 ? h + r : b, vy = h >= 0.0 ? b : r - h;
+    const double vn = sqrt(vx * vx + vy * vy);
+    if (vn > 0.0) {
+        vx /= vn;
+        vy /= vn;
+    } else {
+        vx = 1.0;
+        vy = 0.0;
+    }
+    const double U1 = -(vx * mx + vy * my), U2 = -(vx * my - vy * mx);
+    const double u = 5.9604644775390625e-08;  // 2^-24
+    const double s1 = 2.0 * fabs(U1) + 21.3 + 3.02 / sqrt(l1), s2 = 2.0 * fabs(U2) + 21.3 + 3.02 / sqrt(l2);
+    const double sig = sqrt(l1) * s1 + sqrt(l2) * s2;
+    const double kap = 1e-15 * (l1 / l2) * 9.0;
+    const double e9 = 1.5 * (2.0 * u * 3.0166 * sig + 7.0 * u * 9.1) + kap;
+    f.ka = (float)((0.75 * u * sig + 5.25 * u) * (1.0 + 1e-6));
+    f.kb = (float)((0.75 * u * sig + (double)kEpsExp + 0.5 * kap) * (1.0 + 1e-6));
+    f.U1 = (float)U1;
+    f.U2 = (float)U2;
+    f.e1x = (float)vx;
+    f.e1y = (float)vy;
+    f.l1 = (float)l1;
+    f.l2 = (float)l2;
+    if (det > 0.0 && l2 > 0.0 && e9 < 0.5) {
+        f.thr_in = (float)(9.0 - e9);
+        f.thr_out = (float)(9.0 + e9);
+    } else {  // every pixel that is not certainly outside takes the float64 test
+        f.thr_in = -1.0f;
+        f.thr_out = 3.0e38f;
+    }
+}
+
+// Which of the CTA's eight 8 x 4 warp blocks the splat's support {d2 <= 9} can reach. (mx, my) is
+// the mean relative to the tile origin, (ca, cb2, cc) the conic (a, 2b, c). The support ellipse's
+// bounding box has half-extents 3 sqrt(cc / det), 3 sqrt(ca / det) (det = ac - b^2); it is widened
+// by 1e-6 relative + 1e-3 px, far beyond the float64 rounding of the reference's d2 test, so a
+// pixel whose d2 <= 9 is never outside a set bit. Ill-conditioned conics keep every bit.
+__device__ __forceinline__ unsigned warp_block_mask(double mx, double my, double ca, double cb2, double cc) {
+    const double b = 0.5 * cb2;
+    const double det = ca * cc - b * b;
+    if (!(det > 1e-8 * (ca * cc))) return 0xFFu;
+    const double hx = 3.0 * sqrt(cc / det) * (1.0 + 1e-6) + 1e-3;
+    const double hy = 3.0 * sqrt(ca / det) * (1.0 + 1e-6) + 1e-3;
+    if (!(hx < 1e30 && hy < 1e30)) return 0xFFu;
+    const double x0 = mx - hx, x1 = mx + hx, y0 = my - hy, y1 = my + hy;
+    unsigned cols = 0, rows = 0;
+#pragma unroll
+    for (int bx = 0; bx < 2; ++bx)  // pixel centres 8 bx + 0.5 .. 8 bx + 7.5
+        cols |= (x1 >= 8 * bx + 0.5 && x0 <= 8 * bx + 7.5) ? (1u << bx) : 0u;
+#pragma unroll
+    for (int by = 0; by < 4; ++by)  // pixel centres 4 by + 0.5 .. 4 by + 3.5
+        rows |= (y1 >= 4 * by + 0.5 && y0 <= 4 * by + 3.5) ? (1u << by) : 0u;
+    unsigned m = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) m |= (((cols >> (w & 1)) & (rows >> (w >> 1))) & 1u) << w;
+    return m;
+}
+
+__device__ __forceinline__ bool covers(ushort4 r, int tx, int ty) {
+    return (r.x <= tx) && (tx <= r.y) && (r.z <= ty) && (ty <= r.w);
+}
+
+// Warp-aggregated append of this lane's pixel to the fixup list (all 32 lanes must call).
+__device__ __forceinline__ void push_fixup(const BlendArgs &b, bool flag, uint32_t code) {
+    const unsigned bal = __ballot_sync(kFull, flag);
+    if (!bal) return;
+    const int lane = threadIdx.x & 31;
+    unsigned base = 0;
+    if (lane == __ffs(bal) - 1) base = atomicAdd(b.fix_count, (unsigned)__popc(bal));
+    base = __shfl_sync(kFull, base, __ffs(bal) - 1);
+    if (flag) b.fix_list[base + __popc(bal & ((1u << lane) - 1u))] = code;
+}
+
 // SOURCE 0: no tile lists. The CTA streams its env's depth-sorted tile rectangles (8 B each; the
 //           env's 2 MB array stays in L2 while its 1,200 tiles run) and compacts, in depth order,
 //           the splats whose rectangle covers this tile into a shared-memory queue. The walk
@@ -71,72 +201,78 @@ __constant__ double kExp2Tbl[64] = {
 // SOURCE 1: a materialized tile list (ranges + pair_vals from the radix binner).
 // SOURCE 2: rasterize_reference -- every splat of the env, in depth order.
 #ifndef SN_BLEND_MIN_BLOCKS
-#define SN_BLEND_MIN_BLOCKS 1
+#define SN_BLEND_MIN_BLOCKS 3
 #endif
 template <int MODE, int SOURCE>
 __global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(BlendArgs b) {
-    __shared__ BlendRec s_rec[kBlock];
-    __shared__ double s_exp[64];
+    constexpr bool kBound = MODE != 1;  // depth error bounds feed the compositor
+    __shared__ FRec s_f[kBlock];
+    __shared__ DRec s_d[kBlock];
     __shared__ uint32_t s_queue[2 * kBlock];
     __shared__ uint32_t s_wsum[kBlock / 32];
+    __shared__ uint8_t s_mask[kBlock];  // bit w: the splat's support may reach warp w's 8 x 4 block
+    __shared__ uint8_t s_wl[kBlock / 32][kBlock];  // per warp: its batch entries, in depth order
+    const PassView &v = b.pv;
+    if (pass_overflow(v)) return;
     const int tile = blockIdx.x, el = blockIdx.y, env = b.e0 + el;
     const int tx = tile % b.tiles_x, ty = tile / b.tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // each warp shades an 8 x 4 pixel block (compact footprint: splats that miss the block skip
-    // the float64 path for the whole warp more often than with 16 x 2 rows)
     const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
     const int px_i = tx * kTile + lx;
     const int py_i = ty * kTile + ly;
     const bool inside = px_i < b.width && py_i < b.height;
     const double px = px_i + 0.5, py = py_i + 0.5;
     const double x0 = tx * kTile, y0 = ty * kTile;
-    const float lxf = (float)lx + 0.5f, lyf = (float)ly + 0.5f;
-    if (threadIdx.x < 64) s_exp[threadIdx.x] = kExp2Tbl[threadIdx.x];
+    const float oxf = (float)lx - 7.5f, oyf = (float)ly - 7.5f;  // pixel centre - tile centre
+#ifdef SN_BLEND_PROF
+    unsigned long long prof[16] = {};
+#define PROF(i, x) (prof[i] += (x))
+#else
+#define PROF(i, x) ((void)0)
+#endif
 
     uint32_t cursor, s1;
     if (SOURCE == 1) {
-        uint2 r = b.ranges[((uint32_t)el << b.tile_bits) | (uint32_t)tile];
+        uint2 r = v.ranges[((uint32_t)el << v.tile_bits) | (uint32_t)tile];
         cursor = r.x;
         s1 = r.y;
         // composite of an empty layer tile: front alpha 0 and depth `far`, and the scene depth is a
         // weighted mean of z < far, so `front.depth < back.depth` never holds -- nothing to do
-        if (MODE == 2 && cursor == s1) return;
+        if (MODE == 2) {
+            if (threadIdx.x == 0) b.tile_flag[(int64_t)el * gridDim.x + tile] = cursor != s1;
+            if (cursor == s1) return;
+        }
     } else {
-        cursor = (uint32_t)b.env_off[el];
-        s1 = (uint32_t)b.env_off[el + 1];
+        cursor = (uint32_t)v.env_off[el];
+        s1 = (uint32_t)v.env_off[el + 1];
     }
 
-    double T = 1.0, A = 0.0, D = 0.0;
+    float T = 1.0f, A = 0.0f, D = 0.0f, err = 0.0f;
     float cr = 0.0f, cg = 0.0f, cb = 0.0f;
+    float eps_max = 0.0f, z_first = 3.0e38f, z_last = 0.0f;
     int nc = 0;
-    bool done = !inside;
+    bool done = !inside, amb = false;
     uint32_t loaded = 0, scanned = 0;
     int q_len = 0;  // SOURCE 0: entries waiting in s_queue (uniform across the CTA)
     while (true) {
-        if (__syncthreads_count(!done) == 0) break;  // also guards s_rec / s_queue reuse
+        if (__syncthreads_count(!done) == 0) break;  // also guards s_f / s_queue reuse
         int n;
         if (SOURCE == 0) {
             while (q_len < kBlock && cursor < s1) {
                 // hierarchical cull (uniform across the CTA, no barrier on the skip path):
                 // 8192-splat super-batches, then 256-splat batches, by their union rectangles
                 const uint32_t bi = cursor / kBlock;
-                const ushort4 sr = __ldg(b.super_rects + bi / kSuperBatch);
-                if (!((sr.x <= tx) && (tx <= sr.y) && (sr.z <= ty) && (ty <= sr.w))) {
+                if (!covers(__ldg(v.super_rects + bi / kSuperBatch), tx, ty)) {
                     cursor = min(s1, (bi / kSuperBatch + 1) * (uint32_t)(kSuperBatch * kBlock));
                     continue;
                 }
-                const ushort4 br = __ldg(b.batch_rects + bi);
                 const uint32_t b_end = min(s1, (bi + 1) * (uint32_t)kBlock);
-                if (!((br.x <= tx) && (tx <= br.y) && (br.z <= ty) && (ty <= br.w))) {
+                if (!covers(__ldg(v.batch_rects + bi), tx, ty)) {
                     cursor = b_end;
                     continue;
                 }
                 uint32_t i = bi * kBlock + threadIdx.x;
-                bool hit = false;
-                if (i >= cursor && i < b_end) {
-                    ushort4 r = __ldg(b.rects + i);
-                    hit = (r.x <= tx) && (tx <= r.y) && (r.z <= ty) && (ty <= r.w);
-                }
+                const bool hit = i >= cursor && i < b_end && covers(__ldg(v.rects + i), tx, ty);
                 unsigned bal = __ballot_sync(kFull, hit);
                 if (lane == 0) s_wsum[warp] = __popc(bal);
                 __syncthreads();
@@ -161,119 +297,452 @@ __global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(Blen
         loaded += n;
         if (threadIdx.x < n) {
             uint32_t rid = SOURCE == 0 ? s_queue[threadIdx.x]
-                                       : (SOURCE == 1 ? __ldg(b.pair_vals + cursor + threadIdx.x) : cursor + threadIdx.x);
-            const double2 *src = reinterpret_cast<const double2 *>(b.recs + __ldg(b.order + rid));
-            double2 m = __ldg(src), c01 = __ldg(src + 1), c2a = __ldg(src + 2), zr = __ldg(src + 3);
-            BlendRec &d = s_rec[threadIdx.x];
-            d.mxr = (float)(m.x - x0);
-            d.myr = (float)(m.y - y0);
-            d.caf = (float)c01.x;
-            d.cb2f = (float)c01.y;
-            d.ccf = (float)c2a.x;
+                                       : (SOURCE == 1 ? __ldg(v.pair_vals + cursor + threadIdx.x) : cursor + threadIdx.x);
+            const double2 *src = reinterpret_cast<const double2 *>(v.recs + __ldg(v.order + rid));
+            const double2 m = __ldg(src), c01 = __ldg(src + 1), c2a = __ldg(src + 2), zr = __ldg(src + 3);
+            const double rx = m.x - x0, ry = m.y - y0;
+            FRec f;
+            principal_form(rx - 8.0, ry - 8.0, c01.x, c01.y, c2a.x, f);
+            f.alpha = (float)c2a.y;
+            f.z = (float)zr.x;
             float rgb[3];
             unpack_rgb21((unsigned long long)__double_as_longlong(zr.y), rgb);
-            d.r = rgb[0];
-            d.g = rgb[1];
-            d.b = rgb[2];
-            d.mx = m.x;
-            d.my = m.y;
-            d.ca = c01.x;
-            d.cb2 = c01.y;
-            d.cc = c2a.x;
-            d.alpha = c2a.y;
-            d.z = zr.x;
+            f.r = rgb[0];
+            f.g = rgb[1];
+            f.b = rgb[2];
+            s_f[threadIdx.x] = f;
+            s_d[threadIdx.x] = DRec{m.x, m.y, c01.x, c01.y, c2a.x};
+            s_mask[threadIdx.x] = (uint8_t)warp_block_mask(rx, ry, c01.x, c01.y, c2a.x);
         }
         __syncthreads();
-        if (!done) {
-            for (int j = 0; j < n; ++j) {
-                const BlendRec &s = s_rec[j];
-                // float32 pre-filter: d2f = dx (a dx + 2b dy) + c dy^2 with FMAs. For a positive
-                // definite conic |2b dx dy| <= a dx^2 + c dy^2, so every term is bounded by
-                // M = 2 (a dx^2 + c dy^2); the float error is far below 2^-14 M + 1e-3, and a splat
-                // clearing 9 by that margin is certainly outside the support. Survivors take the
-                // exact float64 test.
-                const float dxf = s.mxr - lxf, dyf = s.myr - lyf;
-                const float cyf = s.ccf * dyf;
-                const float d2f = __fmaf_rn(dxf, __fmaf_rn(s.caf, dxf, s.cb2f * dyf), cyf * dyf);
-                const float mag = __fmaf_rn(s.caf * dxf, dxf, cyf * dyf);
-                if (d2f > __fmaf_rn(mag, 1.220703125e-04f, 9.001f)) continue;
-                double dx = s.mx - px, dy = s.my - py;
-                double d2 = (s.ca * dx * dx + s.cb2 * dx * dy) + s.cc * dy * dy;
-                if (d2 > kSupportD2) continue;
-                double e;
-                SN_EXP_NEG_HALF(d2, s_exp, e);
-                double a = s.alpha * e;
-                if (a > kAlphaClip) a = kAlphaClip;
-                double w = a * T;
-                float wf = (float)w;
-                cr = __fmaf_rn(s.r, wf, cr);
-                cg = __fmaf_rn(s.g, wf, cg);
-                cb = __fmaf_rn(s.b, wf, cb);
+        // each warp walks only the batch entries whose support can reach its 8 x 4 pixel block,
+        // in depth order; the per-pixel tests below stay exact, the mask only skips whole warps
+        int cnt = 0;
+        for (int j0 = 0; j0 < n; j0 += 32) {
+            const bool mine = j0 + lane < n && ((s_mask[j0 + lane] >> warp) & 1u);
+            const unsigned bal = __ballot_sync(kFull, mine);
+            if (mine) s_wl[warp][cnt + __popc(bal & ((1u << lane) - 1u))] = (uint8_t)(j0 + lane);
+            cnt += __popc(bal);
+        }
+        __syncwarp();
+        for (int k0 = 0; k0 < cnt && !__all_sync(kFull, done); k0 += 32) {
+            const int k1 = min(cnt, k0 + 32);
+#pragma unroll 2
+            for (int k = k0; k < k1; ++k) {
+                const int j = s_wl[warp][k];
+                PROF(0, lane == 0);
+                const FRec &s = s_f[j];
+                const float u1 = __fmaf_rn(s.e1x, oxf, __fmaf_rn(s.e1y, oyf, s.U1));
+                const float u2 = __fmaf_rn(s.e1x, oyf, __fmaf_rn(-s.e1y, oxf, s.U2));
+                float d2 = __fmaf_rn(s.l1 * u1, u1, (s.l2 * u2) * u2);
+                if (done | (d2 > s.thr_out)) continue;  // saturated, or certainly outside the support
+                float eps;
+                if (d2 < s.thr_in) {
+                    eps = __fmaf_rn(d2, s.ka, s.kb);
+                } else {  // boundary band: the reference's float64 test (_kernels_cy.pyx:73-75)
+                    PROF(1, 1);
+                    const DRec &sd = s_d[j];
+                    const double ddx = sd.mx - px, ddy = sd.my - py;
+                    const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
+                    if (d2d > kSupportD2) continue;
+                    d2 = (float)d2d;
+                    eps = kEpsExact;
+                }
+                const float e = ex2_approx(d2 * kNegHalfLog2e);
+                const float a = fminf(s.alpha * e, 0.99f);
+                const float w = a * T;
+                cr = __fmaf_rn(s.r, w, cr);
+                cg = __fmaf_rn(s.g, w, cg);
+                cb = __fmaf_rn(s.b, w, cb);
                 A = A + w;
-                D = fma(s.z, w, D);  // one rounding instead of two: ulp-level, inside the depth tolerance
-                T = T * (1.0 - a);
+                D = __fmaf_rn(s.z, w, D);
+                const float om = 1.0f - a;
+                const float Tn = T * om;
+                err = __fmaf_rn(err, om, __fmaf_rn(w, eps, Tn * kU25));
+                T = Tn;
                 ++nc;
-                if (T < kTCutoff) break;  // T only falls on contributions (_kernels_cy.pyx:65-66)
+                if (kBound) {  // splats arrive in depth order: z spans [first, last] contribution
+                    eps_max = fmaxf(eps_max, eps);
+                    z_first = fminf(z_first, s.z);
+                    z_last = s.z;
+                }
+                if (Tn - err <= kTHi) {  // near the cutoff (_kernels_cy.pyx:65-66): decide or defer
+                    done = true;
+                    amb = !(Tn + err < kTLo);
+                    PROF(2, amb);
+                }
             }
-            done = T < kTCutoff;
         }
         if (SOURCE == 0) {  // drop the consumed head of the queue
             int rest = q_len - n;
-            uint32_t v = threadIdx.x < rest ? s_queue[n + threadIdx.x] : 0u;
+            uint32_t qv = threadIdx.x < rest ? s_queue[n + threadIdx.x] : 0u;
             __syncthreads();
-            if (threadIdx.x < rest) s_queue[threadIdx.x] = v;
+            if (threadIdx.x < rest) s_queue[threadIdx.x] = qv;
             q_len = rest;
         } else {
             cursor += n;
         }
     }
+#ifdef SN_BLEND_PROF
+    for (int i = 0; i < 16; ++i)
+        if (prof[i]) atomicAdd(&g_blend_prof[i], prof[i]);
+#endif
     if (b.scans && threadIdx.x == 0 && scanned) atomicAdd(b.scans, (unsigned long long)scanned);
-    if (b.contribs) {
-        unsigned sum = __reduce_add_sync(kFull, (unsigned)nc);
-        if ((threadIdx.x & 31) == 0 && sum) atomicAdd(b.contribs, (unsigned long long)sum);
-    }
     if (b.loads && threadIdx.x == 0 && loaded) atomicAdd(b.loads, (unsigned long long)loaded);
-    if (!inside) return;
 
     const sn_camera &cam = b.cams[env];
     const int64_t pix = ((int64_t)env * b.height + py_i) * b.width + px_i;
-    if (b.contrib) b.contrib[pix] = nc;
-    const double alpha = A < 1.0 ? A : 1.0;
-    const double depth = A > 0.0 ? D / A : cam.far_;
-    float *oc = b.color + 3 * pix;
-    if (MODE == 0) {
-        oc[0] = (float)np_clip((double)cr + cam.background[0] * T, 0.0, 1.0);
-        oc[1] = (float)np_clip((double)cg + cam.background[1] * T, 0.0, 1.0);
-        oc[2] = (float)np_clip((double)cb + cam.background[2] * T, 0.0, 1.0);
-        b.alpha[pix] = (float)alpha;
-        b.depth[pix] = (float)depth;
-        if (b.depth64) b.depth64[pix] = depth;
+    const uint32_t code = (uint32_t)(((int64_t)el * b.height + py_i) * b.width + px_i);
+    // Error bounds of the outputs the compositor decides on. Every weight w_i = a_i T_(i-1) has
+    // relative error <= rho_w (transmittance bound + largest alpha bound + the product's rounding);
+    // depth = sum z w / sum w then errs by <= rho_w (z_last - z_first) from the weights (z spans the
+    // contributions) plus (2n + 2) u from the float sums and the division; alpha by rho_w + (n + 1) u.
+    const float rho_w = err / T + eps_max + 6.0e-8f;
+    const float alpha = fminf(A, 1.0f);
+    const float depth = A > 0.0f ? D / A : (float)cam.far_;
+    const float d_err = 1.01f * (rho_w * (z_last - z_first) + (float)(2 * nc + 2) * 6.0e-8f * depth);
+    const bool flag = inside && amb;
+    if (b.contribs) {
+        unsigned sum = __reduce_add_sync(kFull, flag ? 0u : (unsigned)nc);
+        if (lane == 0 && sum) atomicAdd(b.contribs, (unsigned long long)sum);
+    }
+    push_fixup(b, flag, code);
+    if (!inside) return;
+    if (MODE == 2 && SOURCE != 1 && threadIdx.x == 0) b.tile_flag[(int64_t)el * gridDim.x + tile] = 1;
+    if (flag) {
+        if (MODE == 2) b.ldepth[pix] = __int_as_float(0x7fc00000);  // NaN: pending float64 fixup
         return;
     }
-    double fc0 = 0.0, fc1 = 0.0, fc2 = 0.0;
-    if (A > 0.0) {
-        fc0 = np_clip((double)cr / A, 0.0, 1.0);
-        fc1 = np_clip((double)cg / A, 0.0, 1.0);
-        fc2 = np_clip((double)cb / A, 0.0, 1.0);
+    if (b.contrib) b.contrib[pix] = nc;
+    if (MODE == 0) {
+        float *oc = b.color + 3 * pix;
+        oc[0] = np_clipf(__fmaf_rn((float)cam.background[0], T, cr), 0.0f, 1.0f);
+        oc[1] = np_clipf(__fmaf_rn((float)cam.background[1], T, cg), 0.0f, 1.0f);
+        oc[2] = np_clipf(__fmaf_rn((float)cam.background[2], T, cb), 0.0f, 1.0f);
+        b.alpha[pix] = alpha;
+        b.depth[pix] = depth;
+        if (b.derr) b.derr[pix] = A > 0.0f ? d_err : 0.0f;
+        return;
+    }
+    float fc0 = 0.0f, fc1 = 0.0f, fc2 = 0.0f;
+    if (A > 0.0f) {
+        fc0 = np_clipf(cr / A, 0.0f, 1.0f);
+        fc1 = np_clipf(cg / A, 0.0f, 1.0f);
+        fc2 = np_clipf(cb / A, 0.0f, 1.0f);
     }
     if (MODE == 1) {
-        oc[0] = (float)fc0;
-        oc[1] = (float)fc1;
-        oc[2] = (float)fc2;
-        b.alpha[pix] = (float)alpha;
-        b.depth[pix] = (float)depth;
+        float *oc = b.color + 3 * pix;
+        oc[0] = fc0;
+        oc[1] = fc1;
+        oc[2] = fc2;
+        b.alpha[pix] = alpha;
+        b.depth[pix] = depth;
         return;
     }
-    // MODE 2: composite(front = this layer, back = scene frame in the outputs)
-    const double bd = b.depth64 ? b.depth64[pix] : (double)b.depth[pix];
-    if (depth < bd) {
-        const double ba = b.alpha[pix];
-        oc[0] = (float)(fc0 * alpha + (double)oc[0] * (1.0 - alpha));
-        oc[1] = (float)(fc1 * alpha + (double)oc[1] * (1.0 - alpha));
-        oc[2] = (float)(fc2 * alpha + (double)oc[2] * (1.0 - alpha));
-        b.alpha[pix] = (float)(alpha + ba * (1.0 - alpha));
-        if (alpha >= 0.5) b.depth[pix] = (float)depth;
+    // MODE 2: the layer frame goes to its own buffers; composite_kernel merges it into the scene
+    // frame once the scene pass is done (so this blend runs concurrently with the scene blend)
+    float *lc = b.lcolor + 3 * pix;
+    lc[0] = fc0;
+    lc[1] = fc1;
+    lc[2] = fc2;
+    b.lalpha[pix] = alpha;
+    b.ldepth[pix] = depth;
+    b.lderr[pix] = d_err;
+    b.laerr[pix] = 1.01f * (rho_w + (float)(nc + 1) * 6.0e-8f) * A + 6.0e-8f;
+#undef PROF
+}
+
+// composite(front = avatar layer, back = scene frame), renderer.py:151-166, for the layer frame the
+// mode-2 blend left in its buffers. Decisions (front.depth < back.depth, alpha >= 0.5) are taken
+// only when the tracked float32 error bounds separate them; other pixels join the fixup list and
+// fixup_kernel<2> recomputes both layers in float64 and composites exactly.
+__global__ void __launch_bounds__(kBlock) composite_kernel(BlendArgs b) {
+    const int tile = blockIdx.x, el = blockIdx.y, env = b.e0 + el;
+    if (pass_overflow(b.pv) || pass_overflow(b.back)) return;
+    if (!b.tile_flag[(int64_t)el * gridDim.x + tile]) return;
+    const int tx = tile % b.tiles_x, ty = tile / b.tiles_x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int px_i = tx * kTile + (warp & 1) * 8 + (lane & 7);
+    const int py_i = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+    const bool inside = px_i < b.width && py_i < b.height;
+    const int64_t pix = ((int64_t)env * b.height + py_i) * b.width + px_i;
+    bool flag = false, use_front = false;
+    float ld = 0.0f, la = 0.0f, bd = 0.0f;
+    if (inside) {
+        ld = b.ldepth[pix];
+        la = b.lalpha[pix];
+        // pending fixup (NaN), or no contribution (front depth = far never wins)
+        if (ld == ld && la > 0.0f) {
+            bd = b.depth[pix];
+            if (fabsf(ld - bd) <= 1.01f * (b.lderr[pix] + b.derr[pix]) + 1e-30f)
+                flag = true;
+            else if (ld < bd) {
+                use_front = true;
+                if (fabsf(la - 0.5f) <= b.laerr[pix]) flag = true;
+            }
+        }
     }
+    push_fixup(b, flag, (uint32_t)(((int64_t)el * b.height + py_i) * b.width + px_i));
+    if (!use_front || flag) return;
+    const float *lc = b.lcolor + 3 * pix;
+    float *oc = b.color + 3 * pix;
+    oc[0] = __fmaf_rn(lc[0], la, oc[0] * (1.0f - la));
+    oc[1] = __fmaf_rn(lc[1], la, oc[1] * (1.0f - la));
+    oc[2] = __fmaf_rn(lc[2], la, oc[2] * (1.0f - la));
+    b.alpha[pix] = __fmaf_rn(b.alpha[pix], 1.0f - la, la);
+    if (la >= 0.5f) b.depth[pix] = ld;
+}
+
+// ---- exact (float64) per-pixel walk: the fixup path ----
+
+struct ExactPixel {
+    float cr, cg, cb;
+    double A, D, T;
+    int nc;
+};
+
+// A contribution waiting in a warp's queue (float64 alpha and z, colour).
+struct QEntry {
+    double a, z;
+    float r, g, b, pad;
+};
+constexpr int kQueue = 64;  // per-warp queue capacity: < 32 waiting + 32 arriving
+
+// One pixel of one pass, walked by a whole warp with the reference's float64 arithmetic
+// (_kernels_cy.pyx:64-86: float64 d2 / alpha / transmittance, T tested after each contribution).
+// Lanes gather and test 32 depth-ordered candidates at a time; the contributing ones are queued
+// (in order) and consumed 32 at a time: the transmittance through a group is a warp prefix
+// product (its rounding differs from the sequential product by a few float64 ulps, like the exp),
+// the first member that takes T below 1e-4 is the last contribution, and the accumulators are
+// per-lane partial sums reduced at the end. Groups are the 1st..32nd, 33rd..64th, ... contributions,
+// so the result depends only on the contribution sequence -- not on how candidates were listed
+// (streamed rectangles, tile lists or every splat of the env give bit-identical pixels).
+__device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_x, int px_i, int py_i,
+                                 const double *s_exp, QEntry *q) {
+    const int lane = threadIdx.x & 31;
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const double px = px_i + 0.5, py = py_i + 0.5;
+    float cr = 0.0f, cg = 0.0f, cb = 0.0f;  // per-lane partial sums, reduced at the end
+    double A = 0.0, D = 0.0, T = 1.0;
+    int nc = 0, qn = 0;
+    bool done = false;
+    auto consume = [&](int m) {  // the first m <= 32 queued contributions
+        const bool act = lane < m;
+        QEntry e{};
+        if (act) e = q[lane];
+        double pp = act ? 1.0 - e.a : 1.0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const double o = __shfl_up_sync(kFull, pp, d);
+            if (lane >= d) pp *= o;
+        }
+        double ex = __shfl_up_sync(kFull, pp, 1);
+        if (lane == 0) ex = 1.0;
+        const double t_after = T * pp;
+        const unsigned cut = __ballot_sync(kFull, act && t_after < kTCutoff);
+        const int last = cut ? __ffs(cut) - 1 : m - 1;
+        if (act && lane <= last) {
+            const double w = e.a * (T * ex);
+            const float wf = (float)w;
+            cr = __fmaf_rn(e.r, wf, cr);
+            cg = __fmaf_rn(e.g, wf, cg);
+            cb = __fmaf_rn(e.b, wf, cb);
+            A = A + w;
+            D = fma(e.z, w, D);
+            ++nc;
+        }
+        T = __shfl_sync(kFull, t_after, last);
+        if (cut) done = true;
+    };
+    uint32_t cur, end;
+    if (v.source == 1) {
+        uint2 r = v.ranges[((uint32_t)el << v.tile_bits) | (uint32_t)tile];
+        cur = r.x;
+        end = r.y;
+    } else {
+        cur = (uint32_t)v.env_off[el];
+        end = (uint32_t)v.env_off[el + 1];
+    }
+    constexpr int kPer = 4;  // candidates per lane per step: their gathers are in flight together
+    while (cur < end && !done) {
+        uint32_t step;
+        uint32_t rid[kPer];
+        bool cand[kPer];
+        if (v.source == 0) {
+            const uint32_t bi = cur / kBlock;
+            if (cur % kBlock == 0 || !covers(__ldg(v.batch_rects + bi), tx, ty)) {
+                // find the next 256-splat batch whose union rectangle covers the tile, 32 batches
+                // per step (the lanes test them in parallel)
+                const uint32_t nb = (end + kBlock - 1) / kBlock;
+                const uint32_t cand_b = bi + lane;
+                const unsigned hit = __ballot_sync(kFull, cand_b < nb && covers(__ldg(v.batch_rects + cand_b), tx, ty));
+                if (!hit) {
+                    cur = min(end, (bi + 32) * (uint32_t)kBlock);
+                    continue;
+                }
+                const uint32_t first = bi + __ffs(hit) - 1;
+                if (first != bi) {
+                    cur = first * (uint32_t)kBlock;
+                    continue;
+                }
+            }
+            const uint32_t b_end = min(end, (bi + 1) * (uint32_t)kBlock);
+            step = min(32u * kPer, b_end - cur);
+#pragma unroll
+            for (int i = 0; i < kPer; ++i) {
+                rid[i] = cur + 32 * i + lane;
+                cand[i] = rid[i] < cur + step && covers(__ldg(v.rects + rid[i]), tx, ty);
+            }
+        } else {
+            step = min(32u * kPer, end - cur);
+#pragma unroll
+            for (int i = 0; i < kPer; ++i) {
+                const uint32_t k = cur + 32 * i + lane;
+                cand[i] = k < cur + step;
+                rid[i] = cand[i] ? (v.source == 1 ? __ldg(v.pair_vals + k) : k) : 0u;
+            }
+        }
+        QEntry e[kPer];
+        bool contrib[kPer];
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            contrib[i] = false;
+            e[i] = QEntry{};
+            if (cand[i]) {
+                const SplatRec &s = v.recs[__ldg(v.order + rid[i])];
+                const double dx = s.mx - px, dy = s.my - py;
+                const double d2 = (s.ca * dx * dx + s.cb2 * dx * dy) + s.cc * dy * dy;
+                if (!(d2 > kSupportD2)) {
+                    contrib[i] = true;
+                    double ev;
+                    SN_EXP_NEG_HALF(d2, s_exp, ev);
+                    e[i].a = s.alpha * ev;
+                    if (e[i].a > kAlphaClip) e[i].a = kAlphaClip;
+                    e[i].z = s.z;
+                    float rgb[3];
+                    unpack_rgb21(s.rgb, rgb);
+                    e[i].r = rgb[0];
+                    e[i].g = rgb[1];
+                    e[i].b = rgb[2];
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            if (done) break;
+            const unsigned bal = __ballot_sync(kFull, contrib[i]);
+            if (contrib[i]) q[qn + __popc(bal & ((1u << lane) - 1u))] = e[i];
+            qn += __popc(bal);
+            __syncwarp();
+            if (qn >= 32) {
+                consume(32);
+                QEntry rest{};
+                const bool mv = lane < qn - 32;
+                if (mv) rest = q[32 + lane];
+                __syncwarp();
+                if (mv) q[lane] = rest;
+                __syncwarp();
+                qn -= 32;
+            }
+        }
+        cur += step;
+    }
+    if (!done && qn > 0) consume(qn);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        cr += __shfl_xor_sync(kFull, cr, d);
+        cg += __shfl_xor_sync(kFull, cg, d);
+        cb += __shfl_xor_sync(kFull, cb, d);
+        A += __shfl_xor_sync(kFull, A, d);
+        D += __shfl_xor_sync(kFull, D, d);
+    }
+    return ExactPixel{cr, cg, cb, A, D, T, (int)__reduce_add_sync(kFull, (unsigned)nc)};
+}
+
+// Recomputes the listed pixels exactly (warp per pixel, grid-stride over the device-side count)
+// and writes the same outputs the float64 blend epilogue writes. Mode 2 also recomputes the scene
+// pixel (the back layer) so the composite's comparisons see float64 depths.
+template <int MODE>
+__global__ void __launch_bounds__(256) fixup_kernel(BlendArgs b) {
+    __shared__ double s_exp[64];
+    __shared__ QEntry s_q[8][kQueue];
+    if (threadIdx.x < 64) s_exp[threadIdx.x] = kExp2Tbl[threadIdx.x];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    QEntry *q = s_q[threadIdx.x >> 5];
+    if (pass_overflow(b.pv) || (MODE == 2 && pass_overflow(b.back))) return;
+    const unsigned n_fix = *b.fix_count;
+    const unsigned hw = (unsigned)b.width * (unsigned)b.height;
+    unsigned long long contribs = 0;
+    for (unsigned i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_fix; i += (gridDim.x * blockDim.x) >> 5) {
+        const uint32_t code = b.fix_list[i];
+        const int el = (int)(code / hw), p = (int)(code % hw);
+        const int py_i = p / b.width, px_i = p % b.width;
+        const int env = b.e0 + el;
+        const int tile = (py_i / kTile) * b.tiles_x + px_i / kTile;
+        const sn_camera &cam = b.cams[env];
+        const ExactPixel f = exact_walk(b.pv, el, tile, b.tiles_x, px_i, py_i, s_exp, q);
+        ExactPixel k{};
+        if (MODE == 2) k = exact_walk(b.back, el, tile, b.tiles_x, px_i, py_i, s_exp, q);
+        contribs += (unsigned)f.nc;
+        if (lane != 0) continue;
+        const int64_t pix = ((int64_t)env * b.height + py_i) * b.width + px_i;
+        if (b.contrib) b.contrib[pix] = f.nc;
+        const double alpha = f.A < 1.0 ? f.A : 1.0;
+        const double depth = f.A > 0.0 ? f.D / f.A : cam.far_;
+        float *oc = b.color + 3 * pix;
+        if (MODE == 0) {
+            oc[0] = (float)np_clip((double)f.cr + cam.background[0] * f.T, 0.0, 1.0);
+            oc[1] = (float)np_clip((double)f.cg + cam.background[1] * f.T, 0.0, 1.0);
+            oc[2] = (float)np_clip((double)f.cb + cam.background[2] * f.T, 0.0, 1.0);
+            b.alpha[pix] = (float)alpha;
+            b.depth[pix] = (float)depth;
+            if (b.derr) b.derr[pix] = 0.0f;
+            continue;
+        }
+        double fc[3] = {0.0, 0.0, 0.0};
+        if (f.A > 0.0) {
+            fc[0] = np_clip((double)f.cr / f.A, 0.0, 1.0);
+            fc[1] = np_clip((double)f.cg / f.A, 0.0, 1.0);
+            fc[2] = np_clip((double)f.cb / f.A, 0.0, 1.0);
+        }
+        if (MODE == 1) {
+            for (int c = 0; c < 3; ++c) oc[c] = (float)fc[c];
+            b.alpha[pix] = (float)alpha;
+            b.depth[pix] = (float)depth;
+            continue;
+        }
+        // back = the scene frame exactly as the scene pass stores it (float32 colour / alpha)
+        const float bc[3] = {(float)np_clip((double)k.cr + cam.background[0] * k.T, 0.0, 1.0),
+                             (float)np_clip((double)k.cg + cam.background[1] * k.T, 0.0, 1.0),
+                             (float)np_clip((double)k.cb + cam.background[2] * k.T, 0.0, 1.0)};
+        const float ba = (float)(k.A < 1.0 ? k.A : 1.0);
+        const double bd = k.A > 0.0 ? k.D / k.A : cam.far_;
+        if (depth < bd) {  // composite, renderer.py:151-166
+            for (int c = 0; c < 3; ++c) oc[c] = (float)(fc[c] * alpha + (double)bc[c] * (1.0 - alpha));
+            b.alpha[pix] = (float)(alpha + (double)ba * (1.0 - alpha));
+            b.depth[pix] = (float)(alpha >= 0.5 ? depth : bd);
+        } else {
+            for (int c = 0; c < 3; ++c) oc[c] = bc[c];
+            b.alpha[pix] = ba;
+            b.depth[pix] = (float)bd;
+        }
+    }
+    if (b.contribs && lane == 0 && contribs) atomicAdd(b.contribs, contribs);
+}
+
+// Largest relative error of the blend's fast exp, ex2.approx(d2 * -log2(e) / 2) against float64
+// exp(-d2 / 2), over every float d2 in [0, 9.5]: the kEpsExp budget assumes <= 1e-6.
+__global__ void fast_exp_selftest_kernel(unsigned long long *max_err_bits) {
+    const uint32_t lo = 0u, hi = __float_as_uint(9.5f);
+    double worst = 0.0;
+    for (uint32_t u = lo + blockIdx.x * blockDim.x + threadIdx.x; u <= hi; u += gridDim.x * blockDim.x) {
+        const float d2 = __uint_as_float(u);
+        const float e = ex2_approx(d2 * kNegHalfLog2e);
+        const double ref = exp(-0.5 * (double)d2);
+        worst = fmax(worst, fabs((double)e - ref) / ref);
+    }
+    atomicMax(max_err_bits, (unsigned long long)__double_as_longlong(worst));
 }
 
 __global__ void composite64_kernel(int64_t npix, const double *fc, const double *fa, const double *fd,
@@ -339,12 +808,20 @@ __global__ void blend_tile_range_kernel(int t_begin, int tiles_x, int tile_size,
 
 template <int MODE>
 static void launch_blend_mode(const BlendArgs &b, dim3 grid, cudaStream_t s) {
-    if (b.source == 0)
+    if (b.pv.source == 0)
         blend_kernel<MODE, 0><<<grid, kBlock, 0, s>>>(b);
-    else if (b.source == 1)
+    else if (b.pv.source == 1)
         blend_kernel<MODE, 1><<<grid, kBlock, 0, s>>>(b);
     else
         blend_kernel<MODE, 2><<<grid, kBlock, 0, s>>>(b);
+    if (MODE != 2) fixup_kernel<MODE><<<kFixupBlocks, 256, 0, s>>>(b);  // mode 2: after the composite
+}
+
+cudaError_t launch_layer_composite(const BlendArgs &b, cudaStream_t s) {
+    dim3 grid((unsigned)(tiles_of(b.width) * tiles_of(b.height)), (unsigned)b.ec);
+    composite_kernel<<<grid, kBlock, 0, s>>>(b);
+    fixup_kernel<2><<<kFixupBlocks, 256, 0, s>>>(b);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_blend(const BlendArgs &b, cudaStream_t s) {
@@ -377,4 +854,29 @@ cudaError_t launch_blend_tile_range(int t_begin, int t_end, int tiles_x, int til
     return cudaGetLastError();
 }
 
+cudaError_t fast_exp_selftest(double *max_rel_err) {
+    unsigned long long *d = nullptr;
+    cudaError_t e = cudaMalloc(&d, sizeof(unsigned long long));
+    if (e != cudaSuccess) return e;
+    cudaMemset(d, 0, sizeof(unsigned long long));
+    fast_exp_selftest_kernel<<<1184, 256>>>(d);
+    unsigned long long bits = 0;
+    e = cudaMemcpy(&bits, d, sizeof(bits), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e == cudaSuccess) std::memcpy(max_rel_err, &bits, sizeof(double));
+    return e == cudaSuccess ? cudaGetLastError() : e;
+}
+
 }  // namespace sn
+
+#ifdef SN_BLEND_PROF
+extern "C" int sn_debug_blend_prof(unsigned long long *out, int reset) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_blend_prof, sizeof(unsigned long long) * 16);
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(g_blend_prof, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

@@ -42,6 +42,7 @@ struct PrepArgs {
     int32_t tiles_x, tiles_y;
     uint64_t z_base;
     int32_t z_bits;
+    uint64_t cap;              // capacity of the per-splat buffers (writes past it are dropped)
 };
 
 // sn_preprocess.cu
@@ -67,7 +68,10 @@ cudaError_t launch_joint_prep(const sn_avatars &av, int32_t avatar, const double
 // sn_bin.cu
 struct BinArgs {
     int32_t ec, tiles_x, tiles_y, tile_bits, z_bits;
-    int64_t n_vis;
+    const uint64_t *d_nvis;        // device: visible splats of the chunk (env_off[ec])
+    uint64_t cap_v;                // host capacity of the per-splat buffers
+    const uint64_t *d_npairs;      // device: tile pairs (binning 1)
+    uint64_t cap_p;
     const uint32_t *keys_sorted;   // 32-bit depth keys after the sort
     uint32_t *vals_sorted;         // depth order -> unsorted record slot (tie-fixed in place)
     const SplatRec *recs_un;       // unsorted records (z for the tie fix)
@@ -84,39 +88,66 @@ struct BinArgs {
 constexpr int kSuperBatch = 32;  // batches per super-batch (8192 splats)
 cudaError_t launch_permute(const BinArgs &b, cudaStream_t s);
 cudaError_t launch_depth_tie_fix(const BinArgs &b, cudaStream_t s);
-cudaError_t launch_super_rects(const ushort4 *batch_rects, int64_t n_batches, ushort4 *super_rects, cudaStream_t s);
+cudaError_t launch_super_rects(const BinArgs &b, ushort4 *super_rects, cudaStream_t s);
 cudaError_t launch_duplicate(const BinArgs &b, cudaStream_t s);
-cudaError_t launch_ranges(const uint32_t *keys_sorted, int64_t n_pairs, uint2 *ranges, cudaStream_t s);
-size_t sort_u32_temp_bytes(int64_t n);
-cudaError_t sort_u32_pairs(void *temp, size_t temp_bytes, const uint32_t *k_in, uint32_t *k_out, const uint32_t *v_in,
-                           uint32_t *v_out, int64_t n, int bits, cudaStream_t s);
-size_t scan_temp_bytes(int64_t n);
-cudaError_t scan_tiles(void *temp, size_t temp_bytes, const uint32_t *tiles_touched, uint64_t *pair_off, int64_t n,
-                       cudaStream_t s);
+cudaError_t launch_ranges(const BinArgs &b, const uint32_t *keys_sorted, cudaStream_t s);
+cudaError_t launch_publish_counts(const uint64_t *v, const uint64_t *p, uint64_t *mapped_dst, cudaStream_t s);
+
+// sn_sort.cu (counts in device memory, grids sized by capacity)
+size_t sort_temp_bytes(uint64_t cap);
+bool radix_sort_pairs(void *temp, uint32_t *k0, uint32_t *v0, uint32_t *k1, uint32_t *v1, const uint64_t *d_n,
+                      uint64_t cap, int bits, cudaStream_t s, int64_t *launches);
+size_t scan_temp_bytes_dev(uint64_t cap);
+cudaError_t scan_u32_to_u64(void *temp, const uint32_t *in, const uint64_t *d_n, uint64_t cap, uint64_t *out,
+                            uint64_t *total_out, cudaStream_t s, int64_t *launches);
 
 // sn_blend.cu
-struct BlendArgs {
-    const sn_camera *cams;
-    int32_t e0, ec, width, height, tiles_x, tile_bits;
+// Everything a pixel walk needs from one pass (scene or layer) over an env chunk.
+struct PassView {
     int32_t source;         // 0: scan the env's depth-sorted rects (no tile lists); 1: tile lists
                             // (ranges + pair_vals); 2: rasterize_reference -- every splat of the env
+    int32_t tile_bits;
     const ushort4 *rects;   // depth-sorted tile rectangles (source 0)
     const ushort4 *batch_rects;  // union rectangle of each global 256-splat batch of rects
     const ushort4 *super_rects;  // union rectangle of each kSuperBatch batches
-    int32_t mode;           // 0 scene (background), 1 layer only, 2 layer composited over outputs
     const uint2 *ranges;
     const uint32_t *pair_vals;
     const uint64_t *env_off;
     const SplatRec *recs;   // unsorted records
     const uint32_t *order;  // depth-sorted index -> record slot
+    // capacity guard: a pass whose counts exceeded its buffers produced no valid lists; its blend,
+    // composite and fixups do nothing (the host re-runs the render with larger buffers)
+    const uint64_t *d_nvis, *d_npairs;
+    uint64_t cap_v, cap_p;
+};
+__device__ __forceinline__ bool pass_overflow(const PassView &v) {
+    return *v.d_nvis > v.cap_v || (v.source == 1 && *v.d_npairs > v.cap_p);
+}
+struct BlendArgs {
+    const sn_camera *cams;
+    int32_t e0, ec, width, height, tiles_x;
+    int32_t mode;           // 0 scene (background), 1 layer only, 2 layer composited over outputs
+    PassView pv;            // this pass
+    PassView back;          // mode 2: the scene pass of the same env chunk (exact composite fixups)
     float *color, *alpha, *depth;  // (E,H,W,[3]) outputs, indexed by global env
-    double *depth64;        // scene pass: exact depth for the compositor (may be null)
+    float *derr;            // (E,H,W) error bound of the scene depth: mode 0 writes it (may be null),
+                            // mode 2 reads it
     int32_t *contrib;       // (E,H,W) may be null
+    // mode 2 (deferred composite): the layer frame -- normalized colour, alpha, depth (NaN = pending
+    // fixup) and the error bounds of depth / alpha -- and a per-(env in chunk, tile) "has layer
+    // splats" flag, all indexed like the outputs
+    float *lcolor, *lalpha, *ldepth, *lderr, *laerr;
+    uint8_t *tile_flag;
+    uint32_t *fix_list;     // (ec*H*W) pixels deferred to the float64 fixup (el*H*W + pixel)
+    unsigned *fix_count;    // device counter, zeroed before the blend
     unsigned long long *loads;  // device counter: records gathered into shared memory (may be null)
     unsigned long long *scans;  // device counter: rectangles examined by source-0 tiles (may be null)
     unsigned long long *contribs;  // device counter: (pixel, splat) contributions (may be null)
 };
-cudaError_t launch_blend(const BlendArgs &b, cudaStream_t s);
+constexpr int kFixupBlocks = 148 * 4;
+cudaError_t launch_blend(const BlendArgs &b, cudaStream_t s);  // blend (+ fixup for modes 0, 1)
+cudaError_t launch_layer_composite(const BlendArgs &b, cudaStream_t s);  // mode 2: composite + fixup
+cudaError_t fast_exp_selftest(double *max_rel_err);
 cudaError_t launch_composite64(int64_t npix, const double *fc, const double *fa, const double *fd, const double *bc,
                                const double *ba, const double *bd, double *oc, double *oa, double *od, cudaStream_t s);
 cudaError_t launch_blend_tile_range(int t_begin, int t_end, int tiles_x, int tile_size, int width, int height,

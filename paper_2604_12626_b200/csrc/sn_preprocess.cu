@@ -99,6 +99,7 @@ __device__ __forceinline__ void warp_offsets(uint64_t mask, int ec, unsigned (*s
 
 __device__ __forceinline__ void write_splat(const PrepArgs &a, int64_t pos, int e, const Geo &geo, double alpha,
                                             const float rgb[3], uint32_t gid) {
+    if ((uint64_t)pos >= a.cap) return;  // overflow: the host re-runs the pass with larger buffers
     SplatRec r;
     r.mx = geo.mx;
     r.my = geo.my;

@@ -402,3 +402,11 @@ def test_3m_scene_spot_check():
     np.testing.assert_array_equal(out["contrib_scene"][5].cpu().numpy(), o.contrib)
     check_frame(out["color"][5].cpu().numpy(), out["alpha"][5].cpu().numpy(), out["depth"][5].cpu().numpy(),
                 o.color, o.alpha, o.depth, cams[5].far)
+
+
+def test_fast_exp_error_budget():
+    """The float32 blend chain's error budget (csrc/sn_blend.cu kEpsExp = 2e-6) assumes the fast
+    exponential's relative error is <= 1e-6 over d2 in [0, 9.5]; check it on the device."""
+    from paper_2604_12626_b200 import _native as N
+    err = N.selftest_fast_exp()
+    assert 0.0 < err <= 1e-6, err
