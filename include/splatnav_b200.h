@@ -214,7 +214,7 @@ int sn_blend_tile_range(int32_t t_begin, int32_t t_end, int32_t tiles_x, int32_t
                         double *alpha_acc, double *trans, double *depth_acc);
 
 /* Self-check of the blend's fast exponential (ex2.approx, float32): largest relative error against
- * float64 exp(-d2/2) over every float d2 in [0, 9.5]. The blend's error budget assumes <= 1e-6. */
+ * float64 exp(-d2/2) over every float d2 in [0, 9.5]. The blend's error budget assumes <= 3.5e-7. */
 int sn_selftest_fast_exp(double *max_rel_err);
 
 /* composite(front, back) on device float64 frames of npix pixels (renderer.py:151-166). */

@@ -75,7 +75,7 @@ uint64_t dbits(double d) {
 }
 
 struct PassWs {
-    Buf vismask, blk_counts, env_off, keys_un, keys_s, vals_un, vals_s, recs_un, gid_un, rects_un, rects,
+    Buf vismask, blk_counts, env_off, keys_un, keys_s, vals_un, vals_s, recs_un, geo_un, gid_un, rects_un, rects,
         tiles, pair_off, pkeys_a, pkeys_b, pvals_a, pvals_b, ranges, temp, batch_rects, super_rects, fix, counts;
     uint64_t cap_v = 0, cap_p = 0;  // capacities of the per-splat / per-pair buffers
     // metadata of the last chunk rendered by this pass
@@ -186,6 +186,7 @@ PassView view_of(const PassWs &w) {
     v.pair_vals = w.pvals_b.as<uint32_t>();
     v.env_off = w.env_off.as<uint64_t>();
     v.recs = w.recs_un.as<SplatRec>();
+    v.geo = w.geo_un.as<BlendGeo>();
     v.order = w.vals_s.as<uint32_t>();
     v.d_nvis = w.env_off.as<uint64_t>() + w.ec;
     v.d_npairs = w.counts.as<uint64_t>() + 1;
@@ -244,6 +245,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     SN_ENSURE(w.vals_un, sizeof(uint32_t) * v1);
     SN_ENSURE(w.vals_s, sizeof(uint32_t) * v1);
     SN_ENSURE(w.recs_un, sizeof(SplatRec) * v1);
+    SN_ENSURE(w.geo_un, sizeof(BlendGeo) * v1);
     SN_ENSURE(w.gid_un, sizeof(uint32_t) * v1);
     SN_ENSURE(w.rects_un, sizeof(ushort4) * v1);
     SN_ENSURE(w.rects, sizeof(ushort4) * v1);
@@ -310,6 +312,8 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
             SN_CUDA(launch_scene_emit(*sp.scene, a, st));
         else
             SN_CUDA(launch_avatar_emit(*sp.avatars, sp.pose, a, st));
+        ctx->launches += 1;
+        SN_CUDA(launch_blend_geo(w.recs_un.as<SplatRec>(), w.geo_un.as<BlendGeo>(), d_nvis, cap_v, st));
         tm.end();
         tm.begin(SN_STAGE_DEPTH_SORT);
         // 32-bit keys (env + top z bits), then an exact fix of equal-key runs
@@ -524,7 +528,7 @@ int sn_context_destroy(sn_context *ctx) {
         b.p = nullptr;
     };
     for (auto &w : ctx->pass) {
-        for (Buf *b : {&w.vismask, &w.blk_counts, &w.env_off, &w.keys_un, &w.keys_s, &w.vals_un, &w.vals_s, &w.recs_un,
+        for (Buf *b : {&w.vismask, &w.blk_counts, &w.env_off, &w.keys_un, &w.keys_s, &w.vals_un, &w.vals_s, &w.recs_un, &w.geo_un,
                        &w.gid_un, &w.rects_un, &w.rects, &w.tiles, &w.pair_off, &w.pkeys_a,
                        &w.pkeys_b, &w.pvals_a, &w.pvals_b, &w.ranges, &w.temp, &w.batch_rects, &w.super_rects,
                        &w.fix, &w.counts})
@@ -575,7 +579,7 @@ int sn_context_workspace_bytes(const sn_context *ctx, size_t *bytes) {
     size_t t = 0;
     for (const auto &w : ctx->pass)
         for (const Buf *b : {&w.vismask, &w.blk_counts, &w.env_off, &w.keys_un, &w.keys_s, &w.vals_un, &w.vals_s,
-                             &w.recs_un, &w.gid_un, &w.rects_un, &w.rects, &w.tiles, &w.pair_off,
+                             &w.recs_un, &w.geo_un, &w.gid_un, &w.rects_un, &w.rects, &w.tiles, &w.pair_off,
                              &w.pkeys_a, &w.pkeys_b, &w.pvals_a, &w.pvals_b, &w.ranges, &w.temp,
                              &w.batch_rects, &w.super_rects, &w.fix})
             t += b->cap;

@@ -79,8 +79,10 @@ __constant__ double kExp2Tbl[64] = {
     } while (0)
 
 // ---- float32 chain error constants (see the header comment) ----
-constexpr float kEpsExp = 2.0e-6f;     // ex2.approx (<= 2^-21 asserted) + argument, alpha, product roundings
-constexpr float kEpsExact = 2.3e-6f;   // same, when d2 came from float64 (rounded to float: 4.5 u)
+// ex2.approx incl. its argument's rounding (measured max 2.76e-7 over d2 in [0, 9.5] by
+// sn_selftest_fast_exp; the GPU test asserts <= 3.5e-7) + the roundings of alpha and alpha * e
+constexpr float kEpsExp = 5.0e-7f;
+constexpr float kEpsExact = 8.0e-7f;   // same, when d2 came from float64 (rounded to float: 4.5 u)
 constexpr float kU25 = 1.5e-7f;        // 2.5 u: roundings of 1 - a and T (1 - a)
 constexpr float kTLo = 9.99999e-05f;   // 1e-4 (1 - 1e-6): below it (with the bound) T < 1e-4 for sure
 constexpr float kTHi = 1.000001e-04f;  // 1e-4 (1 + 1e-6)
@@ -92,90 +94,88 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
-// Shared-memory forms of a record: the float32 chain's fields (64 B: principal-axis offsets and
-// directions, eigenvalues, the decision thresholds 9 -/+ E9, alpha, z, the alpha error bound,
-// colour) and the float64 fields of the exact d2 test (40 B).
+// Shared-memory form of a gathered splat for the float32 chain (64 B): principal-axis offsets and
+// directions, eigenvalues, the decision thresholds 9 -/+ E(9.1), alpha, z, the alpha error bound
+// coefficients, colour.
 struct __align__(16) FRec {
     float U1, U2, e1x, e1y;
     float l1, l2, thr_out, thr_in;
     float alpha, z, ka, kb;  // alpha's relative error bound: eps(d2) = ka d2 + kb
     float r, g, b, pad;
 };
-struct DRec {
-    double mx, my, ca, cb2, cc;
-};
 
-// The splat's d2 in its conic's principal axes, relative to the tile centre: (mx, my) = mean - tile
-// centre, conic (ca, cb2, cc) = (a, 2b, c). d2(o) = l1 (e1.o - e1.m)^2 + l2 (e2.o - e2.m)^2 with
-// e2 = (-e1y, e1x). Fills U1 = -e1.m, U2 = -e2.m, e1, l1 >= l2, the thresholds 9 -/+ E(9.1) and
-// the alpha error coefficients, from the float error of d2 at a pixel with |o| <= 7.5 sqrt(2):
-//   |u_k error| <= u S_k, S_k = 2 |U_k| + 21.3 + 3.02 / sqrt(l_k)   (valid while d2 <= 9.1),
-//   E(d2) = 1.5 [2 u sqrt(d2) (sqrt(l1) S1 + sqrt(l2) S2) + 7 u d2] + 1e-15 (l1 / l2) 9,
-//   eps(d2) = E(d2) / 2 + kEpsExp <= ka d2 + kb   (sqrt(d2) <= (d2 + 1) / 2).
-// An ill-conditioned or non-finite conic gets thresholds that send every pixel to float64.
-__device__ __forceinline__ void principal_form(double mx, double my, double ca, double cb2, double cc, FRec &f) {
-    const double b = 0.5 * cb2;
-    const double h = 0.5 * (ca - cc);
-    const double r = sqrt(h * h + b * b);
-    const double l1 = 0.5 * (ca + cc) + r;
-    const double det = ca * cc - b * b;
-    const double l2 = det / l1;
-    double vx = h >= 0.0 ? h + r : b, vy = h >= 0.0 ? b : r - h;
-    const double vn = sqrt(vx * vx + vy * vy);
-    if (vn > 0.0) {
-        vx /= vn;
-        vy /= vn;
-    } else {
-        vx = 1.0;
-        vy = 0.0;
-    }
-    const double U1 = -(vx * mx + vy * my), U2 = -(vx * my - vy * mx);
-    const double u = 5.9604644775390625e-08;  // 2^-24
-    const double s1 = 2.0 * fabs(U1) + 21.3 + 3.02 / sqrt(l1), s2 = 2.0 * fabs(U2) + 21.3 + 3.02 / sqrt(l2);
-    const double sig = sqrt(l1) * s1 + sqrt(l2) * s2;
-    const double kap = 1e-15 * (l1 / l2) * 9.0;
-    const double e9 = 1.5 * (2.0 * u * 3.0166 * sig + 7.0 * u * 9.1) + kap;
-    f.ka = (float)((0.75 * u * sig + 5.25 * u) * (1.0 + 1e-6));
-    f.kb = (float)((0.75 * u * sig + (double)kEpsExp + 0.5 * kap) * (1.0 + 1e-6));
-    f.U1 = (float)U1;
-    f.U2 = (float)U2;
-    f.e1x = (float)vx;
-    f.e1y = (float)vy;
-    f.l1 = (float)l1;
-    f.l2 = (float)l2;
-    if (det > 0.0 && l2 > 0.0 && e9 < 0.5) {
-        f.thr_in = (float)(9.0 - e9);
-        f.thr_out = (float)(9.0 + e9);
-    } else {  // every pixel that is not certainly outside takes the float64 test
-        f.thr_in = -1.0f;
-        f.thr_out = 3.0e38f;
-    }
-}
-
-// Which of the CTA's eight 8 x 4 warp blocks the splat's support {d2 <= 9} can reach. (mx, my) is
-// the mean relative to the tile origin, (ca, cb2, cc) the conic (a, 2b, c). The support ellipse's
-// bounding box has half-extents 3 sqrt(cc / det), 3 sqrt(ca / det) (det = ac - b^2); it is widened
-// by 1e-6 relative + 1e-3 px, far beyond the float64 rounding of the reference's d2 test, so a
-// pixel whose d2 <= 9 is never outside a set bit. Ill-conditioned conics keep every bit.
-__device__ __forceinline__ unsigned warp_block_mask(double mx, double my, double ca, double cb2, double cc) {
-    const double b = 0.5 * cb2;
-    const double det = ca * cc - b * b;
-    if (!(det > 1e-8 * (ca * cc))) return 0xFFu;
-    const double hx = 3.0 * sqrt(cc / det) * (1.0 + 1e-6) + 1e-3;
-    const double hy = 3.0 * sqrt(ca / det) * (1.0 + 1e-6) + 1e-3;
-    if (!(hx < 1e30 && hy < 1e30)) return 0xFFu;
-    const double x0 = mx - hx, x1 = mx + hx, y0 = my - hy, y1 = my + hy;
+// Which of the CTA's eight 8 x 4 warp blocks the splat's support {d2 <= 9} can reach: (mx, my) is
+// the mean relative to the tile origin, (hx, hy) the support ellipse's bounding-box half-extents
+// (already widened far beyond the float rounding of the reference's d2 test), so a pixel whose
+// d2 <= 9 is never outside a set bit.
+__device__ __forceinline__ unsigned warp_block_mask(float mx, float my, float hx, float hy) {
+    const float x0 = mx - hx, x1 = mx + hx, y0 = my - hy, y1 = my + hy;
     unsigned cols = 0, rows = 0;
 #pragma unroll
     for (int bx = 0; bx < 2; ++bx)  // pixel centres 8 bx + 0.5 .. 8 bx + 7.5
-        cols |= (x1 >= 8 * bx + 0.5 && x0 <= 8 * bx + 7.5) ? (1u << bx) : 0u;
+        cols |= (x1 >= 8 * bx + 0.5f && x0 <= 8 * bx + 7.5f) ? (1u << bx) : 0u;
 #pragma unroll
     for (int by = 0; by < 4; ++by)  // pixel centres 4 by + 0.5 .. 4 by + 3.5
-        rows |= (y1 >= 4 * by + 0.5 && y0 <= 4 * by + 3.5) ? (1u << by) : 0u;
+        rows |= (y1 >= 4 * by + 0.5f && y0 <= 4 * by + 3.5f) ? (1u << by) : 0u;
     unsigned m = 0;
 #pragma unroll
     for (int w = 0; w < 8; ++w) m |= (((cols >> (w & 1)) & (rows >> (w >> 1))) & 1u) << w;
     return m;
+}
+
+// A gathered splat's float32 blend form for this tile, from its BlendGeo (make_blend_geo): d2 in the
+// conic's principal axes relative to the tile centre (cx, cy), d2(o) = l1 (e1.o + U1)^2 +
+// l2 (e2.o + U2)^2 with U_k = e_k.(centre - mean) formed in float64, the thresholds 9 -/+ E(9.1) and
+// the alpha error coefficients, from the float error of d2 at a pixel with |o| <= 7.5 sqrt(2):
+//   |u_k error| <= u S_k, S_k = 2 |U_k| + 21.3 + 3.02 / sqrt(l_k)   (valid while d2 <= 9.1),
+//   E(d2) = 1.5 [2 u sqrt(d2) (sqrt(l1) S1 + sqrt(l2) S2) + 7 u d2] + 1e-15 (l1 / l2) 9,
+//   eps(d2) = E(d2) / 2 + kEpsExp <= ka d2 + kb   (sqrt(d2) <= (d2 + 1) / 2),
+// all evaluated in float with a 1% margin. A degenerate conic (l2 <= 0) gets thresholds that send
+// every pixel to the float64 test. Returns the 8-bit warp-block mask (warp_block_mask).
+__device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1, double p2, float4 gl, float4 gr,
+                                               double cx, double cy, FRec &f) {
+    const double U1 = fma(e1x, cx, fma(e1y, cy, -p1));
+    const double U2 = fma(-e1y, cx, fma(e1x, cy, -p2));
+    const float l1 = gl.x, l2 = gl.y;
+    f.U1 = (float)U1;
+    f.U2 = (float)U2;
+    f.e1x = (float)e1x;
+    f.e1y = (float)e1y;
+    f.l1 = l1;
+    f.l2 = l2;
+    f.alpha = gl.z;
+    f.z = gl.w;
+    float rgb[3];
+    unpack_rgb21(((unsigned long long)__float_as_uint(gr.y) << 32) | __float_as_uint(gr.x), rgb);
+    f.r = rgb[0];
+    f.g = rgb[1];
+    f.b = rgb[2];
+    f.pad = 0.0f;
+    const float u = 5.9604644775390625e-08f;  // 2^-24
+    const float aU1 = fabsf(f.U1), aU2 = fabsf(f.U2);
+    bool ok = l2 > 0.0f;
+    if (ok) {
+        const float r1 = rsqrtf(l1), r2 = rsqrtf(l2);
+        const float s1 = 2.0f * aU1 + 21.3f + 3.02f * r1, s2 = 2.0f * aU2 + 21.3f + 3.02f * r2;
+        const float sig = (l1 * r1) * s1 + (l2 * r2) * s2;
+        const float kap = 9.0e-15f * fminf(l1 / l2, 1e30f);
+        const float e9 = 1.01f * (1.5f * (2.0f * u * 3.0166f * sig + 7.0f * u * 9.1f) + kap);
+        ok = e9 < 0.5f;
+        f.thr_in = 9.0f - e9;
+        f.thr_out = 9.0f + e9;
+        f.ka = 1.01f * (0.75f * u * sig + 5.25f * u);
+        f.kb = 1.01f * (0.75f * u * sig + kEpsExp + 0.5f * kap);
+    }
+    if (!ok) {  // every pixel that is not certainly outside takes the float64 test
+        f.thr_in = -1.0f;
+        f.thr_out = 3.0e38f;
+        f.ka = 0.0f;
+        f.kb = kEpsExact;
+    }
+    // mean - tile origin, from the principal-axis offsets (float error ~ 2u (|U1| + |U2|))
+    const float mx = 8.0f - (f.U1 * f.e1x - f.U2 * f.e1y), my = 8.0f - (f.U1 * f.e1y + f.U2 * f.e1x);
+    const float slack = 1e-3f + 4.0f * u * (aU1 + aU2);
+    return warp_block_mask(mx, my, gr.z * 1.00001f + slack, gr.w * 1.00001f + slack);
 }
 
 __device__ __forceinline__ bool covers(ushort4 r, int tx, int ty) {
@@ -201,13 +201,13 @@ __device__ __forceinline__ void push_fixup(const BlendArgs &b, bool flag, uint32
 // SOURCE 1: a materialized tile list (ranges + pair_vals from the radix binner).
 // SOURCE 2: rasterize_reference -- every splat of the env, in depth order.
 #ifndef SN_BLEND_MIN_BLOCKS
-#define SN_BLEND_MIN_BLOCKS 3
+#define SN_BLEND_MIN_BLOCKS 4
 #endif
 template <int MODE, int SOURCE>
 __global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(BlendArgs b) {
     constexpr bool kBound = MODE != 1;  // depth error bounds feed the compositor
     __shared__ FRec s_f[kBlock];
-    __shared__ DRec s_d[kBlock];
+    __shared__ uint32_t s_slot[kBlock];  // record slot (the exact fallback reads the SplatRec)
     __shared__ uint32_t s_queue[2 * kBlock];
     __shared__ uint32_t s_wsum[kBlock / 32];
     __shared__ uint8_t s_mask[kBlock];  // bit w: the splat's support may reach warp w's 8 x 4 block
@@ -298,21 +298,16 @@ __global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(Blen
         if (threadIdx.x < n) {
             uint32_t rid = SOURCE == 0 ? s_queue[threadIdx.x]
                                        : (SOURCE == 1 ? __ldg(v.pair_vals + cursor + threadIdx.x) : cursor + threadIdx.x);
-            const double2 *src = reinterpret_cast<const double2 *>(v.recs + __ldg(v.order + rid));
-            const double2 m = __ldg(src), c01 = __ldg(src + 1), c2a = __ldg(src + 2), zr = __ldg(src + 3);
-            const double rx = m.x - x0, ry = m.y - y0;
+            const uint32_t slot = __ldg(v.order + rid);
+            const double2 *src = reinterpret_cast<const double2 *>(v.geo + slot);
+            const double2 ge = __ldg(src), gp = __ldg(src + 1);
+            const float4 gl = __ldg(reinterpret_cast<const float4 *>(src + 2));
+            const float4 gr = __ldg(reinterpret_cast<const float4 *>(src + 3));
             FRec f;
-            principal_form(rx - 8.0, ry - 8.0, c01.x, c01.y, c2a.x, f);
-            f.alpha = (float)c2a.y;
-            f.z = (float)zr.x;
-            float rgb[3];
-            unpack_rgb21((unsigned long long)__double_as_longlong(zr.y), rgb);
-            f.r = rgb[0];
-            f.g = rgb[1];
-            f.b = rgb[2];
+            unsigned msk = tile_entry(ge.x, ge.y, gp.x, gp.y, gl, gr, x0 + 8.0, y0 + 8.0, f);
             s_f[threadIdx.x] = f;
-            s_d[threadIdx.x] = DRec{m.x, m.y, c01.x, c01.y, c2a.x};
-            s_mask[threadIdx.x] = (uint8_t)warp_block_mask(rx, ry, c01.x, c01.y, c2a.x);
+            s_slot[threadIdx.x] = slot;
+            s_mask[threadIdx.x] = (uint8_t)msk;
         }
         __syncthreads();
         // each warp walks only the batch entries whose support can reach its 8 x 4 pixel block,
@@ -341,7 +336,7 @@ __global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(Blen
                     eps = __fmaf_rn(d2, s.ka, s.kb);
                 } else {  // boundary band: the reference's float64 test (_kernels_cy.pyx:73-75)
                     PROF(1, 1);
-                    const DRec &sd = s_d[j];
+                    const SplatRec &sd = v.recs[s_slot[j]];
                     const double ddx = sd.mx - px, ddy = sd.my - py;
                     const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
                     if (d2d > kSupportD2) continue;
@@ -517,6 +512,7 @@ constexpr int kQueue = 64;  // per-warp queue capacity: < 32 waiting + 32 arrivi
 // per-lane partial sums reduced at the end. Groups are the 1st..32nd, 33rd..64th, ... contributions,
 // so the result depends only on the contribution sequence -- not on how candidates were listed
 // (streamed rectangles, tile lists or every splat of the env give bit-identical pixels).
+template <int kPer>  // candidates per lane per step: their gathers are in flight together
 __device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_x, int px_i, int py_i,
                                  const double *s_exp, QEntry *q) {
     const int lane = threadIdx.x & 31;
@@ -563,7 +559,6 @@ __device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_
         cur = (uint32_t)v.env_off[el];
         end = (uint32_t)v.env_off[el + 1];
     }
-    constexpr int kPer = 4;  // candidates per lane per step: their gathers are in flight together
     while (cur < end && !done) {
         uint32_t step;
         uint32_t rid[kPer];
@@ -681,15 +676,51 @@ __global__ void __launch_bounds__(256) fixup_kernel(BlendArgs b) {
         const int env = b.e0 + el;
         const int tile = (py_i / kTile) * b.tiles_x + px_i / kTile;
         const sn_camera &cam = b.cams[env];
-        const ExactPixel f = exact_walk(b.pv, el, tile, b.tiles_x, px_i, py_i, s_exp, q);
-        ExactPixel k{};
-        if (MODE == 2) k = exact_walk(b.back, el, tile, b.tiles_x, px_i, py_i, s_exp, q);
+        // mode 2 fixups are few and each walks long, unsaturated lists: more gathers in flight
+        const ExactPixel f = exact_walk<MODE == 2 ? 8 : 4>(b.pv, el, tile, b.tiles_x, px_i, py_i, s_exp, q);
         contribs += (unsigned)f.nc;
-        if (lane != 0) continue;
         const int64_t pix = ((int64_t)env * b.height + py_i) * b.width + px_i;
-        if (b.contrib) b.contrib[pix] = f.nc;
         const double alpha = f.A < 1.0 ? f.A : 1.0;
         const double depth = f.A > 0.0 ? f.D / f.A : cam.far_;
+        if (MODE == 2) {
+            // composite(front = this layer, back = the scene frame), renderer.py:151-166. The back
+            // depth in the frame is within derr of the float64 value: only when the exact front
+            // depth falls inside that band is the scene pixel recomputed in float64 as well.
+            if (lane == 0 && b.contrib) b.contrib[pix] = f.nc;
+            if (!(f.A > 0.0)) continue;  // front depth = far: the back is kept
+            double bd = (double)b.depth[pix];
+            bool exact_back = false;
+            ExactPixel k{};
+            if (fabs(depth - bd) <= 1.01 * (double)b.derr[pix] + 1e-30) {
+                k = exact_walk<4>(b.back, el, tile, b.tiles_x, px_i, py_i, s_exp, q);
+                bd = k.A > 0.0 ? k.D / k.A : cam.far_;
+                exact_back = true;
+            }
+            if (lane != 0) continue;
+            float *oc = b.color + 3 * pix;
+            float bc[3] = {oc[0], oc[1], oc[2]};
+            float ba = b.alpha[pix];
+            if (exact_back) {  // the scene frame exactly as the scene pass stores it (float32)
+                bc[0] = (float)np_clip((double)k.cr + cam.background[0] * k.T, 0.0, 1.0);
+                bc[1] = (float)np_clip((double)k.cg + cam.background[1] * k.T, 0.0, 1.0);
+                bc[2] = (float)np_clip((double)k.cb + cam.background[2] * k.T, 0.0, 1.0);
+                ba = (float)(k.A < 1.0 ? k.A : 1.0);
+            }
+            if (depth < bd) {
+                const double fc[3] = {np_clip((double)f.cr / f.A, 0.0, 1.0), np_clip((double)f.cg / f.A, 0.0, 1.0),
+                                      np_clip((double)f.cb / f.A, 0.0, 1.0)};
+                for (int c = 0; c < 3; ++c) oc[c] = (float)(fc[c] * alpha + (double)bc[c] * (1.0 - alpha));
+                b.alpha[pix] = (float)(alpha + (double)ba * (1.0 - alpha));
+                b.depth[pix] = (float)(alpha >= 0.5 ? depth : bd);
+            } else if (exact_back) {
+                for (int c = 0; c < 3; ++c) oc[c] = bc[c];
+                b.alpha[pix] = ba;
+                b.depth[pix] = (float)bd;
+            }
+            continue;
+        }
+        if (lane != 0) continue;
+        if (b.contrib) b.contrib[pix] = f.nc;
         float *oc = b.color + 3 * pix;
         if (MODE == 0) {
             oc[0] = (float)np_clip((double)f.cr + cam.background[0] * f.T, 0.0, 1.0);
@@ -706,33 +737,15 @@ __global__ void __launch_bounds__(256) fixup_kernel(BlendArgs b) {
             fc[1] = np_clip((double)f.cg / f.A, 0.0, 1.0);
             fc[2] = np_clip((double)f.cb / f.A, 0.0, 1.0);
         }
-        if (MODE == 1) {
-            for (int c = 0; c < 3; ++c) oc[c] = (float)fc[c];
-            b.alpha[pix] = (float)alpha;
-            b.depth[pix] = (float)depth;
-            continue;
-        }
-        // back = the scene frame exactly as the scene pass stores it (float32 colour / alpha)
-        const float bc[3] = {(float)np_clip((double)k.cr + cam.background[0] * k.T, 0.0, 1.0),
-                             (float)np_clip((double)k.cg + cam.background[1] * k.T, 0.0, 1.0),
-                             (float)np_clip((double)k.cb + cam.background[2] * k.T, 0.0, 1.0)};
-        const float ba = (float)(k.A < 1.0 ? k.A : 1.0);
-        const double bd = k.A > 0.0 ? k.D / k.A : cam.far_;
-        if (depth < bd) {  // composite, renderer.py:151-166
-            for (int c = 0; c < 3; ++c) oc[c] = (float)(fc[c] * alpha + (double)bc[c] * (1.0 - alpha));
-            b.alpha[pix] = (float)(alpha + (double)ba * (1.0 - alpha));
-            b.depth[pix] = (float)(alpha >= 0.5 ? depth : bd);
-        } else {
-            for (int c = 0; c < 3; ++c) oc[c] = bc[c];
-            b.alpha[pix] = ba;
-            b.depth[pix] = (float)bd;
-        }
+        for (int c = 0; c < 3; ++c) oc[c] = (float)fc[c];
+        b.alpha[pix] = (float)alpha;
+        b.depth[pix] = (float)depth;
     }
     if (b.contribs && lane == 0 && contribs) atomicAdd(b.contribs, contribs);
 }
 
 // Largest relative error of the blend's fast exp, ex2.approx(d2 * -log2(e) / 2) against float64
-// exp(-d2 / 2), over every float d2 in [0, 9.5]: the kEpsExp budget assumes <= 1e-6.
+// exp(-d2 / 2), over every float d2 in [0, 9.5]: the kEpsExp budget assumes <= 3.5e-7.
 __global__ void fast_exp_selftest_kernel(unsigned long long *max_err_bits) {
     const uint32_t lo = 0u, hi = __float_as_uint(9.5f);
     double worst = 0.0;

@@ -41,6 +41,53 @@ struct __align__(16) SplatRec {
 };
 static_assert(sizeof(SplatRec) == 64, "SplatRec must stay 64 bytes");
 
+// The blend's view of a splat, written next to its SplatRec by the emit stage: the conic in its
+// principal axes (float64 major-axis direction e1 and the projections p1 = e1.mean, p2 = e2.mean,
+// e2 = (-e1y, e1x); eigenvalues l1 >= l2) so a tile only has to form e1.(centre - mean) in
+// float64, plus the support ellipse's bounding-box half-extents and the float blend inputs.
+struct __align__(16) BlendGeo {
+    double e1x, e1y;
+    double p1, p2;
+    float l1, l2;          // l2 <= 0: degenerate -- the blend tests every pixel in float64
+    float alpha, z;
+    unsigned long long rgb;
+    float hx, hy;          // 3 sqrt(e1x^2 / l1 + e1y^2 / l2), 3 sqrt(e1y^2 / l1 + e1x^2 / l2)
+};
+static_assert(sizeof(BlendGeo) == 64, "BlendGeo must stay 64 bytes");
+
+__device__ __forceinline__ BlendGeo make_blend_geo(double mx, double my, double ca, double cb2, double cc,
+                                                   double alpha, double z, unsigned long long rgb) {
+    BlendGeo g;
+    const double b = 0.5 * cb2;
+    const double h = 0.5 * (ca - cc);
+    const double r = sqrt(h * h + b * b);
+    const double l1 = 0.5 * (ca + cc) + r;
+    const double det = ca * cc - b * b;
+    const double l2 = det / l1;
+    double vx = h >= 0.0 ? h + r : b, vy = h >= 0.0 ? b : r - h;
+    const double vn = sqrt(vx * vx + vy * vy);
+    if (vn > 0.0) {
+        vx /= vn;
+        vy /= vn;
+    } else {
+        vx = 1.0;
+        vy = 0.0;
+    }
+    g.e1x = vx;
+    g.e1y = vy;
+    g.p1 = vx * mx + vy * my;
+    g.p2 = vx * my - vy * mx;
+    const bool ok = det > 0.0 && l2 > 0.0 && l1 < 1e30;
+    g.l1 = (float)l1;
+    g.l2 = ok ? (float)l2 : 0.0f;
+    g.alpha = (float)alpha;
+    g.z = (float)z;
+    g.rgb = rgb;
+    g.hx = ok ? (float)(3.0 * sqrt(vx * vx / l1 + vy * vy / l2)) : 3.0e38f;
+    g.hy = ok ? (float)(3.0 * sqrt(vy * vy / l1 + vx * vx / l2)) : 3.0e38f;
+    return g;
+}
+
 __host__ __device__ inline int tiles_of(int px) { return (px + kTile - 1) / kTile; }
 
 // numpy.maximum(x, 0.0) / numpy.clip: NaN propagates (fmax would drop it)

@@ -10,6 +10,7 @@
 namespace sn {
 
 struct SplatRec;
+struct BlendGeo;
 
 // Per-(env, avatar) pose block produced by the pose kernel and read by the skinning code:
 // joint_mats (J x 12, rows of the 3x4 M_j = rigid(T_j) B_j^-1), eff_q (J x 4 effective joint
@@ -91,6 +92,8 @@ cudaError_t launch_depth_tie_fix(const BinArgs &b, cudaStream_t s);
 cudaError_t launch_super_rects(const BinArgs &b, ushort4 *super_rects, cudaStream_t s);
 cudaError_t launch_duplicate(const BinArgs &b, cudaStream_t s);
 cudaError_t launch_ranges(const BinArgs &b, const uint32_t *keys_sorted, cudaStream_t s);
+// BlendGeo of every record of the pass (reads the SplatRecs the emit wrote)
+cudaError_t launch_blend_geo(const SplatRec *recs, BlendGeo *geo, const uint64_t *d_nvis, uint64_t cap, cudaStream_t s);
 cudaError_t launch_publish_counts(const uint64_t *v, const uint64_t *p, uint64_t *mapped_dst, cudaStream_t s);
 
 // sn_sort.cu (counts in device memory, grids sized by capacity)
@@ -114,6 +117,7 @@ struct PassView {
     const uint32_t *pair_vals;
     const uint64_t *env_off;
     const SplatRec *recs;   // unsorted records
+    const BlendGeo *geo;    // their blend views (same slots)
     const uint32_t *order;  // depth-sorted index -> record slot
     // capacity guard: a pass whose counts exceeded its buffers produced no valid lists; its blend,
     // composite and fixups do nothing (the host re-runs the render with larger buffers)

@@ -405,8 +405,9 @@ def test_3m_scene_spot_check():
 
 
 def test_fast_exp_error_budget():
-    """The float32 blend chain's error budget (csrc/sn_blend.cu kEpsExp = 2e-6) assumes the fast
-    exponential's relative error is <= 1e-6 over d2 in [0, 9.5]; check it on the device."""
+    """The float32 blend chain's error budget (csrc/sn_blend.cu kEpsExp = 5e-7) assumes the fast
+    exponential's relative error, argument rounding included, is <= 3.5e-7 over d2 in [0, 9.5]
+    (measured: 2.76e-7); check it on the device."""
     from paper_2604_12626_b200 import _native as N
     err = N.selftest_fast_exp()
-    assert 0.0 < err <= 1e-6, err
+    assert 0.0 < err <= 3.5e-7, err
