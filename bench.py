@@ -169,9 +169,21 @@ def algorithmic_bytes(stage, pass_id, n_gauss, n_avatar_gauss, work, n_pix_total
         return vis * 8 + pairs * 4
     if stage == "ranges":
         return pairs * 4
-    if stage == "blend":  # records gathered (64 B + 4 B index) + rectangles streamed + pixels out
-        return loads * 68 + scans * 8 + n_pix_total * (20 + (8 if pass_id == 0 else 24))
+    if stage == "blend":  # BlendGeo records gathered (64 B + 4 B index) + rectangles streamed + pixels out
+        # scene: RGB + alpha + depth (20 B) + the depth error bound (4 B); layer: its own frame (28 B)
+        return loads * 68 + scans * 8 + n_pix_total * (24 if pass_id == 0 else 28)
     return 0.0
+
+
+def measured_traffic(kernel_stage):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+    (profiles/ncu_traffic.json, written by scripts/ncu_traffic.py from the .ncu-rep)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        return d.get(kernel_stage)
+    except (OSError, ValueError):
+        return None
 
 
 def cpu_baseline(args, scene, bundles, sets, n_envs_sample):
@@ -344,20 +356,31 @@ def main():
                 "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
                 "alg_bytes_per_step": alg, "ms_per_step": per_stage[dom],
                 "share_of_step": per_stage[dom] / (ms_max / args.steps)}
+    traffic = measured_traffic(dom)
+    if traffic is not None:
+        roofline["traffic"] = traffic["dram_bytes_per_launch"] * traffic["launches_per_step"]
+        roofline["traffic_source"] = traffic["source"]
     if sname == "blend":
-        # the blend is fp64-issue-bound, not HBM-bound: report its float64 work too. FLOPs per
-        # contribution counted from the SASS of the contribution path: d2 (2 DADD + 6 DMUL + 2 DADD),
-        # exp (7 DFMA + 1 DADD + 1 DMUL), alpha/weights (DMUL, DMUL, DADD, DFMA, DADD, DMUL)
-        flops_per_contrib = 10 + (7 * 2 + 2) + (6 + 1)
+        # The blend is not HBM-bound (records and rectangles are L2 hits, DRAM traffic is the
+        # frames): it is issue-bound on its float32 contribution chain. FP32-pipe instructions per
+        # contribution, counted from the SASS of blend_kernel<0,0>: d2 (4 FFMA + 3 FMUL + 1 FFMA),
+        # alpha error (1 FFMA), exp argument (1 FMUL; the EX2 itself is on the MUFU pipe), alpha
+        # (FMUL, FMNMX), weight (FMUL), colour (3 FFMA), A (FADD), D (FFMA), transmittance (FADD,
+        # FMUL), its error bound (FMUL, 2 FFMA), bound tracking (2 FMNMX), cutoff test (FADD).
+        per_contrib = 8 + 1 + 1 + 2 + 1 + 3 + 1 + 1 + 2 + 3 + 2 + 1
         contribs = w2[pid, 4] / args.steps
-        roofline["fp64"] = {"contributions_per_step": int(contribs), "flops_per_contribution": flops_per_contrib,
-                            "achieved_tflops": contribs * flops_per_contrib / (per_stage[dom] / 1e3) / 1e12,
-                            "peak_tflops": 37.0, "peak_kind": "nominal B200 FP64 (not in MEASURED_PEAKS.json)"}
-        roofline["fp64"]["frac"] = roofline["fp64"]["achieved_tflops"] / 37.0
+        clk = (clocks.summary() or {}).get("sm_mhz") or 1965.0
+        peak_t = 148 * 128 * clk * 1e6 / 1e12  # FP32 lane-instructions per second (1 FFMA = 1)
+        achieved_t = contribs * per_contrib / (per_stage[dom] / 1e3) / 1e12
+        roofline["compute"] = {"pipe": "fp32", "contributions_per_step": int(contribs),
+                               "fp32_inst_per_contribution": per_contrib,
+                               "achieved_tinst_per_s": achieved_t, "peak_tinst_per_s": peak_t,
+                               "peak_kind": f"148 SMs x 128 FP32 lanes x {clk:.0f} MHz (measured SM clock)",
+                               "frac": achieved_t / peak_t}
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64 geometry/decisions, f32 colour", "data": "synthetic (seeded, BASELINE distributions)",
+        "vs_baseline": None, "dtype": "f64 geometry + exact decisions (f32 blend chain with error bounds, f64 fixups)", "data": "synthetic (seeded, BASELINE distributions)",
         "config": {"workload": f"config2: {args.gaussians} scene gaussians + {args.avatars}x50k skinned avatars, "
                                f"{args.envs} envs/GPU, {args.width}x{args.height}, near {args.near}",
                    "envs_per_gpu": args.envs, "n_gaussians": args.gaussians, "n_avatars": args.avatars,
