@@ -296,6 +296,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     b.rects_in = w.rects_un.as<ushort4>();
     b.env_off = w.env_off.as<uint64_t>();
     b.rects_out = w.rects.as<ushort4>();
+    b.geo_out = w.geo_un.as<BlendGeo>();
     b.batch_rects = w.batch_rects.as<ushort4>();
     b.tiles_touched = w.tiles.as<uint32_t>();
     b.pair_off = w.pair_off.as<uint64_t>();
@@ -312,8 +313,6 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
             SN_CUDA(launch_scene_emit(*sp.scene, a, st));
         else
             SN_CUDA(launch_avatar_emit(*sp.avatars, sp.pose, a, st));
-        ctx->launches += 1;
-        SN_CUDA(launch_blend_geo(w.recs_un.as<SplatRec>(), w.geo_un.as<BlendGeo>(), d_nvis, cap_v, st));
         tm.end();
         tm.begin(SN_STAGE_DEPTH_SORT);
         // 32-bit keys (env + top z bits), then an exact fix of equal-key runs

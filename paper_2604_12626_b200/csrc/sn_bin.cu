@@ -67,6 +67,12 @@ __global__ void __launch_bounds__(kBlock) permute_kernel(BinArgs b) {
     if (i >= n_vis) return;
     ushort4 r = mine;
     b.rects_out[i] = r;
+    {  // the blend's view of the splat, in depth order (the blend then reads it without the index)
+        const double2 *src = reinterpret_cast<const double2 *>(b.recs_un + b.vals_sorted[i]);
+        const double2 m = __ldg(src), c01 = __ldg(src + 1), c2a = __ldg(src + 2), zr = __ldg(src + 3);
+        b.geo_out[i] = make_blend_geo(m.x, m.y, c01.x, c01.y, c2a.x, c2a.y, zr.x,
+                                      (unsigned long long)__double_as_longlong(zr.y));
+    }
     b.tiles_touched[i] = (uint32_t)(r.y - r.x + 1) * (uint32_t)(r.w - r.z + 1);
 }
 
@@ -190,24 +196,6 @@ __global__ void __launch_bounds__(kBlock) tie_fix_kernel(BinArgs b) {
 }
 
 }  // namespace
-
-__global__ void __launch_bounds__(kBlock) blend_geo_kernel(const SplatRec *recs, BlendGeo *geo, const uint64_t *d_nvis,
-                                                          uint64_t cap) {
-    const uint64_t n = min(*d_nvis, cap);
-    const uint64_t i = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
-    if (i >= n) return;
-    const double2 *src = reinterpret_cast<const double2 *>(recs + i);
-    const double2 m = __ldg(src), c01 = __ldg(src + 1), c2a = __ldg(src + 2), zr = __ldg(src + 3);
-    geo[i] = make_blend_geo(m.x, m.y, c01.x, c01.y, c2a.x, c2a.y, zr.x,
-                            (unsigned long long)__double_as_longlong(zr.y));
-}
-
-cudaError_t launch_blend_geo(const SplatRec *recs, BlendGeo *geo, const uint64_t *d_nvis, uint64_t cap,
-                             cudaStream_t s) {
-    if (cap == 0) return cudaSuccess;
-    blend_geo_kernel<<<(unsigned)((cap + kBlock - 1) / kBlock), kBlock, 0, s>>>(recs, geo, d_nvis, cap);
-    return cudaGetLastError();
-}
 
 __global__ void publish_counts_kernel(const uint64_t *v, const uint64_t *p, volatile uint64_t *dst) {
     dst[0] = *v;

@@ -207,7 +207,7 @@ template <int MODE, int SOURCE>
 __global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(BlendArgs b) {
     constexpr bool kBound = MODE != 1;  // depth error bounds feed the compositor
     __shared__ FRec s_f[kBlock];
-    __shared__ uint32_t s_slot[kBlock];  // record slot (the exact fallback reads the SplatRec)
+    __shared__ uint32_t s_slot[kBlock];  // depth-sorted index (the exact fallback reads the SplatRec)
     __shared__ uint32_t s_queue[2 * kBlock];
     __shared__ uint32_t s_wsum[kBlock / 32];
     __shared__ uint8_t s_mask[kBlock];  // bit w: the splat's support may reach warp w's 8 x 4 block
@@ -298,15 +298,14 @@ __global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(Blen
         if (threadIdx.x < n) {
             uint32_t rid = SOURCE == 0 ? s_queue[threadIdx.x]
                                        : (SOURCE == 1 ? __ldg(v.pair_vals + cursor + threadIdx.x) : cursor + threadIdx.x);
-            const uint32_t slot = __ldg(v.order + rid);
-            const double2 *src = reinterpret_cast<const double2 *>(v.geo + slot);
+            const double2 *src = reinterpret_cast<const double2 *>(v.geo + rid);
             const double2 ge = __ldg(src), gp = __ldg(src + 1);
             const float4 gl = __ldg(reinterpret_cast<const float4 *>(src + 2));
             const float4 gr = __ldg(reinterpret_cast<const float4 *>(src + 3));
             FRec f;
             unsigned msk = tile_entry(ge.x, ge.y, gp.x, gp.y, gl, gr, x0 + 8.0, y0 + 8.0, f);
             s_f[threadIdx.x] = f;
-            s_slot[threadIdx.x] = slot;
+            s_slot[threadIdx.x] = rid;
             s_mask[threadIdx.x] = (uint8_t)msk;
         }
         __syncthreads();
@@ -336,7 +335,7 @@ __global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(Blen
                     eps = __fmaf_rn(d2, s.ka, s.kb);
                 } else {  // boundary band: the reference's float64 test (_kernels_cy.pyx:73-75)
                     PROF(1, 1);
-                    const SplatRec &sd = v.recs[s_slot[j]];
+                    const SplatRec &sd = v.recs[v.order[s_slot[j]]];
                     const double ddx = sd.mx - px, ddy = sd.my - py;
                     const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
                     if (d2d > kSupportD2) continue;

@@ -79,6 +79,7 @@ struct BinArgs {
     const ushort4 *rects_in;
     const uint64_t *env_off;
     ushort4 *rects_out;
+    BlendGeo *geo_out;       // (n_vis) BlendGeo in depth order
     ushort4 *batch_rects;    // (ceil(n_vis / 256)) union rect per 256-splat batch
     uint32_t *tiles_touched;
     uint64_t *pair_off;      // (n_vis + 1)
@@ -92,8 +93,6 @@ cudaError_t launch_depth_tie_fix(const BinArgs &b, cudaStream_t s);
 cudaError_t launch_super_rects(const BinArgs &b, ushort4 *super_rects, cudaStream_t s);
 cudaError_t launch_duplicate(const BinArgs &b, cudaStream_t s);
 cudaError_t launch_ranges(const BinArgs &b, const uint32_t *keys_sorted, cudaStream_t s);
-// BlendGeo of every record of the pass (reads the SplatRecs the emit wrote)
-cudaError_t launch_blend_geo(const SplatRec *recs, BlendGeo *geo, const uint64_t *d_nvis, uint64_t cap, cudaStream_t s);
 cudaError_t launch_publish_counts(const uint64_t *v, const uint64_t *p, uint64_t *mapped_dst, cudaStream_t s);
 
 // sn_sort.cu (counts in device memory, grids sized by capacity)
@@ -117,7 +116,7 @@ struct PassView {
     const uint32_t *pair_vals;
     const uint64_t *env_off;
     const SplatRec *recs;   // unsorted records
-    const BlendGeo *geo;    // their blend views (same slots)
+    const BlendGeo *geo;    // blend views in depth order (indexed like order)
     const uint32_t *order;  // depth-sorted index -> record slot
     // capacity guard: a pass whose counts exceeded its buffers produced no valid lists; its blend,
     // composite and fixups do nothing (the host re-runs the render with larger buffers)

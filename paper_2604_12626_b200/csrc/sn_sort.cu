@@ -6,8 +6,8 @@
 //   upsweep   -- each 2048-item tile builds its digit histogram (per-warp shared-memory counters);
 //   rowscan   -- one CTA per digit scans that digit's per-tile counts (exclusive) and its total;
 //   downsweep -- each tile ranks its items stably (warp __match_any_sync peers + per-warp running
-//                counts, then a prefix over the tile's warps) and scatters keys and values to
-//                digit base + tile offset + rank.
+//                counts, then a prefix over the tile's warps), stages them in digit order in shared
+//                memory and writes each digit's run to digit base + tile offset, coalesced.
 // Stable at every level (lane order within a round, round order within a warp's 256-item segment,
 // warp order within a tile, tile order in the scan), hence a stable LSD sort. Traffic per pass:
 // 4 B/item read (upsweep) + 8 B read + 8 B written (downsweep).
@@ -106,8 +106,10 @@ __global__ void __launch_bounds__(kSortThreads) sort_downsweep(const uint32_t *k
                                                                int shift, int dbits, const uint32_t *hist,
                                                                const uint32_t *totals, int n_tiles) {
     __shared__ uint32_t s_base[256];
+    __shared__ uint32_t s_tstart[256];
     __shared__ uint32_t s_cnt[kSortThreads / 32][256];
     __shared__ uint32_t s_w[kSortThreads / 32];
+    __shared__ uint32_t s_k[kSortTile], s_v[kSortTile];
     const uint64_t n = clamp_n(d_n, cap);
     const uint64_t base = (uint64_t)blockIdx.x * kSortTile;
     if (base >= n) return;
@@ -146,24 +148,41 @@ __global__ void __launch_bounds__(kSortThreads) sort_downsweep(const uint32_t *k
         pos[r] = before + rank;
     }
     __syncthreads();
-    if (threadIdx.x < bins) {  // per digit: prefix over the tile's warps
-        uint32_t run = 0;
+    uint32_t tile_cnt = 0;
+    if (threadIdx.x < bins) {  // per digit: prefix over the tile's warps, and the tile's count
 #pragma unroll
         for (int w = 0; w < kSortThreads / 32; ++w) {
             const uint32_t c = s_cnt[w][threadIdx.x];
-            s_cnt[w][threadIdx.x] = run;
-            run += c;
+            s_cnt[w][threadIdx.x] = tile_cnt;
+            tile_cnt += c;
         }
     }
     __syncthreads();
+    {  // where each digit's run starts inside the tile
+        uint32_t ex;
+        block_exclusive_scan<kSortThreads>(threadIdx.x < bins ? tile_cnt : 0u, ex, s_w);
+        if (threadIdx.x < bins) s_tstart[threadIdx.x] = ex;
+    }
+    __syncthreads();
+    // stage the tile in digit order in shared memory, then write each digit's run out with
+    // consecutive threads on consecutive addresses (coalesced)
 #pragma unroll
     for (int r = 0; r < kSortRounds; ++r) {
         const uint64_t i = seg + (uint64_t)r * 32 + lane;
         if (i >= n) continue;
         const uint32_t d = (k[r] >> shift) & mask;
-        const uint32_t g = s_base[d] + s_cnt[warp][d] + pos[r];
-        kout[g] = k[r];
-        vout[g] = v[r];
+        const uint32_t l = s_tstart[d] + s_cnt[warp][d] + pos[r];
+        s_k[l] = k[r];
+        s_v[l] = v[r];
+    }
+    __syncthreads();
+    const int tile_n = (int)min((uint64_t)kSortTile, n - base);
+    for (int l = threadIdx.x; l < tile_n; l += kSortThreads) {
+        const uint32_t key = s_k[l];
+        const uint32_t d = (key >> shift) & mask;
+        const uint32_t g = s_base[d] + (uint32_t)l - s_tstart[d];
+        kout[g] = key;
+        vout[g] = s_v[l];
     }
 }
 
