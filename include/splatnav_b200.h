@@ -5,8 +5,9 @@
  * (/root/reference/pkg/src/splatnav). Plain C: no torch or CUDA C++ types. Memory arguments
  * are DEVICE pointers unless a parameter says "host". Every function returns SN_OK (0) or an
  * error code; sn_last_error() gives a thread-local message. Launches are asynchronous on the
- * given stream. sn_render() synchronizes the stream internally to size its workspace (twice
- * per pass).
+ * given stream. sn_render() queues both passes without a host round trip (capacity-sized
+ * workspace, counts kept on the device) and synchronizes the stream once, at the end, to check
+ * the counts against the capacities (re-running the render with larger buffers if one overflowed).
  *
  * Reference interfaces replaced (file:line under /root/reference/pkg/src/splatnav):
  *   sn_render ................ renderer.render_observation (renderer.py:169-177) batched over
@@ -141,6 +142,9 @@ typedef struct sn_render_opts {
                                fixup -- per pass, accumulated. Both arrays are filled asynchronously: they are complete
                                after the next sn_render on the context or sn_context_sync_stats(),
                                and must stay valid until then. */
+    int32_t exact;          /* 1: every pixel takes the float64 path (the blend's fixup walk) instead of
+                               the float32 chain with error bounds -- validation / reference mode */
+    int32_t pad;
 } sn_render_opts;
 
 typedef struct sn_context sn_context;

@@ -30,12 +30,13 @@ class BatchRenderer:
     def device(self):
         return self.scene.device
 
-    def render(self, cameras, sim_times=None, avatar_active=None, tiled=True, contrib=False, stats=False):
+    def render(self, cameras, sim_times=None, avatar_active=None, tiled=True, contrib=False, stats=False,
+               exact=False):
         if self.avatars is not None and sim_times is None:
             sim_times = np.zeros(len(cameras))
         return render_frames(self.scene, cameras, self.background, avatars=self.avatars, sim_times=sim_times,
                              tiled=tiled, context=self.context, contrib=contrib, stats=stats,
-                             avatar_active=avatar_active)
+                             avatar_active=avatar_active, exact=exact)
 
     def render_to_host(self, cameras, sim_times=None, host_out=None):
         """render() followed by a device->host copy into pinned buffers (the end-to-end path)."""

@@ -400,6 +400,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     bl.contrib = opts ? (pass_id == 0 ? opts->contrib_scene : opts->contrib_layer) : nullptr;
     bl.fix_list = w.fix.as<uint32_t>();
     bl.fix_count = ctx->fixcnt.as<unsigned>() + pass_id;
+    bl.force_exact = opts ? opts->exact : 0;
     SN_CUDA(cudaMemsetAsync(bl.fix_count, 0, sizeof(unsigned), st));
     if (work) {
         if (ctx->work_dst[pass_id]) {  // previous chunk's counters still in flight

@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(Blen
     float cr = 0.0f, cg = 0.0f, cb = 0.0f;
     float eps_max = 0.0f, z_first = 3.0e38f, z_last = 0.0f;
     int nc = 0;
-    bool done = !inside, amb = false;
+    bool done = !inside || b.force_exact, amb = inside && b.force_exact;
     uint32_t loaded = 0, scanned = 0;
     int q_len = 0;  // SOURCE 0: entries waiting in s_queue (uniform across the CTA)
     while (true) {

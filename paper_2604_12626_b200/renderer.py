@@ -58,7 +58,7 @@ def _nonempty(c):
 
 def render_frames(scene, cameras, background, layer=None, avatars=None, sim_times=None, tiled=True,
                   context=None, contrib=False, stats=True, avatar_active=None, stage_ms=None, work=None,
-                  binning=-1):
+                  binning=-1, exact=False):
     """One sn_render call over E cameras. Returns a dict of device tensors:
     color (E,H,W,3), alpha (E,H,W), depth (E,H,W) float32; stats (E,5) int64; optionally
     contrib_scene / contrib_layer (E,H,W) int32. The context keeps the pass intermediates for
@@ -78,6 +78,7 @@ def render_frames(scene, cameras, background, layer=None, avatars=None, sim_time
     opts = N.SnRenderOpts()
     opts.tiled = 1 if tiled else 0
     opts.binning = int(binning)
+    opts.exact = 1 if exact else 0
     if stats:
         out["stats"] = torch.zeros((e, 5), dtype=torch.int64, device=dev)
         opts.stats = out["stats"].data_ptr()

@@ -46,12 +46,12 @@ def check_frame(color, alpha, depth, ref_color, ref_alpha, ref_depth, far):
     np.testing.assert_array_equal(depth[~hit], ref_depth[~hit].astype(np.float32).astype(np.float64))
 
 
-def check_discrete(case_ids, tile_starts, pair_splat, contrib, pass_id, env, n_tiles):
+def check_discrete(case_ids, tile_starts, pair_splat, contrib, pass_id, env, n_tiles, context=None):
     r = R()
-    inter = r.pass_intermediates(pass_id, env)
+    inter = r.pass_intermediates(pass_id, env, context=context)
     np.testing.assert_array_equal(inter["ids"], case_ids)
     if tile_starts is not None:
-        ts, ps = r.tile_csr(n_tiles, pass_id, env)
+        ts, ps = r.tile_csr(n_tiles, pass_id, env, context=context)
         np.testing.assert_array_equal(ts, tile_starts)
         if pair_splat is not None:
             np.testing.assert_array_equal(ps, pair_splat)
@@ -104,12 +104,12 @@ def test_golden_room_batched():
                     case["depth"].astype(np.float64), cams[e].far)
 
 
-def _oracle_check_env(out, e, cloud, cam, bg, pass_id=0, layer_mode=False):
+def _oracle_check_env(out, e, cloud, cam, bg, pass_id=0, layer_mode=False, context=None):
     o = O.rasterize(cloud, cam, None if layer_mode else bg)
     proj = O.project_cloud(cloud, cam)
     tiles_x, tiles_y = O.tiles_for(cam.width, cam.height)
     ts, ps = O.bin_tiles(proj.means2d, proj.radii, tiles_x, tiles_y)
-    check_discrete(proj.ids.astype(np.int32), ts, ps, None, pass_id, e, tiles_x * tiles_y)
+    check_discrete(proj.ids.astype(np.int32), ts, ps, None, pass_id, e, tiles_x * tiles_y, context=context)
     key = "contrib_scene" if pass_id == 0 else "contrib_layer"
     np.testing.assert_array_equal(out[key][e].cpu().numpy(), o.contrib)
     return o
@@ -229,8 +229,11 @@ def test_render_observation_golden():
                     case.camera().far)
 
 
-def test_fused_avatar_batch_matches_oracle():
-    """Batched scene + 2 skinned avatars at per-env times vs the oracle fed the GPU-skinned clouds."""
+@pytest.mark.parametrize("exact", [False, True])
+def test_fused_avatar_batch_matches_oracle(exact):
+    """Batched scene + 2 skinned avatars at per-env times vs the oracle fed the GPU-skinned clouds,
+    through the float32 chain with bounds (exact=False) and through the float64 walk for every
+    pixel (exact=True)."""
     from paper_2604_12626_b200 import rig
     from paper_2604_12626_b200.batch import BatchRenderer
     from paper_2604_12626_b200.cloud import concat_clouds
@@ -240,7 +243,7 @@ def test_fused_avatar_batch_matches_oracle():
     # point two cameras at the avatars so the layer is non-trivial
     times = np.array([0.0, 0.05, 0.133, 0.21, 0.3])
     br = BatchRenderer(scene, bundles, start_offsets=[0.0, 0.1], loops=[1, 0], background=(0.2, 0.3, 0.4))
-    out = br.render(cams, times, contrib=True, stats=True)
+    out = br.render(cams, times, contrib=True, stats=True, exact=exact)
     for e in range(len(cams)):
         clouds = []
         for a, b in enumerate(bundles):
@@ -411,3 +414,43 @@ def test_fast_exp_error_budget():
     from paper_2604_12626_b200 import _native as N
     err = N.selftest_fast_exp()
     assert 0.0 < err <= 3.5e-7, err
+
+
+def test_exact_mode_agrees_with_fast_path():
+    """The float32 chain's discrete outputs equal the all-float64 walk's, pixel for pixel; the
+    continuous ones differ by float32 rounding only."""
+    box = S.room_box(1_000_000)
+    scene = S.make_scene(200_000, box[0], box[1], seed=71)
+    cams = S.room_cameras(4, box, seed=72)
+    bg = np.array([1.0, 1.0, 1.0])
+    from paper_2604_12626_b200 import _native as N
+    ctx_fast, ctx_exact = N.Context(), N.Context()
+    fast = R().render_frames(scene, cams, bg, contrib=True, context=ctx_fast)
+    ex = R().render_frames(scene, cams, bg, contrib=True, context=ctx_exact, exact=True)
+    assert torch.equal(fast["contrib_scene"], ex["contrib_scene"])
+    assert float((fast["color"] - ex["color"]).abs().max()) <= 1e-5
+    rel = ((fast["depth"] - ex["depth"]).abs() / ex["depth"]).max()
+    assert float(rel) <= 1e-5
+    o = _oracle_check_env(ex, 1, scene, cams[1], bg, context=ctx_exact)
+    check_frame(ex["color"][1].cpu().numpy(), ex["alpha"][1].cpu().numpy(), ex["depth"][1].cpu().numpy(),
+                o.color, o.alpha, o.depth, cams[1].far)
+
+
+def test_capacity_growth_rerenders_exactly():
+    """A context sized by a small render must grow (one re-run) for a larger one and still give the
+    oracle's discrete outputs."""
+    from paper_2604_12626_b200 import _native as N
+    box = S.room_box(1_000_000)
+    small = S.make_scene(5_000, box[0], box[1], seed=81)
+    big = S.make_scene(120_000, box[0], box[1], seed=82)
+    cams = S.room_cameras(2, box, seed=83, width=320, height=240)
+    bg = np.array([0.5, 0.5, 0.5])
+    ctx = N.Context()
+    R().render_frames(small, cams, bg, context=ctx)
+    r0 = ctx.render_retries()
+    out = R().render_frames(big, cams, bg, contrib=True, context=ctx)
+    assert ctx.render_retries() > r0
+    for e in range(2):
+        o = _oracle_check_env(out, e, big, cams[e], bg, context=ctx)
+        check_frame(out["color"][e].cpu().numpy(), out["alpha"][e].cpu().numpy(), out["depth"][e].cpu().numpy(),
+                    o.color, o.alpha, o.depth, cams[e].far)

@@ -39,13 +39,31 @@ def test_library_exports_every_declared_symbol():
     assert N.load().sn_abi_version() == 1
 
 
-def test_struct_layouts_match_header():
-    assert ctypes.sizeof(N.SnCamera) == 208 == CAMERA_DTYPE.itemsize
-    assert N.SnCamera.width.offset == 6 * 8 + 18 * 8
-    assert ctypes.sizeof(N.SnStats) == 40
-    assert ctypes.sizeof(N.SnCloud) == 8 + 4 + 4 + 4 * 8
-    assert ctypes.sizeof(N.SnAvatars) == 8 + 4 * 4 + 15 * 8
-    assert ctypes.sizeof(N.SnRenderOpts) == 8 + 6 * 8
+def _c_layout(struct, fields):
+    """sizeof / offsetof of a header struct, from a C program compiled against the header."""
+    import subprocess
+    import tempfile
+    body = f'printf("%zu", sizeof({struct}));' + "".join(
+        f'printf(" %zu", offsetof({struct}, {f}));' for f in fields)
+    src = f'#include <stdio.h>\n#include "splatnav_b200.h"\nint main(void) {{ {body} return 0; }}\n'
+    with tempfile.TemporaryDirectory() as d:
+        c, exe = os.path.join(d, "t.c"), os.path.join(d, "t")
+        open(c, "w").write(src)
+        subprocess.run(["gcc", "-std=c11", "-I", os.path.dirname(HEADER), c, "-o", exe], check=True)
+        vals = [int(x) for x in subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split()]
+    return vals[0], vals[1:]
+
+
+@pytest.mark.parametrize("cls,struct", [(N.SnCamera, "sn_camera"), (N.SnStats, "sn_stats"), (N.SnCloud, "sn_cloud"),
+                                        (N.SnAvatars, "sn_avatars"), (N.SnRenderOpts, "sn_render_opts")])
+def test_struct_layouts_match_header(cls, struct):
+    """The ctypes mirrors have the C compiler's size and field offsets for every header struct."""
+    names = [f[0] for f in cls._fields_]
+    size, offs = _c_layout(struct, names)
+    assert ctypes.sizeof(cls) == size
+    assert [getattr(cls, f).offset for f in names] == offs
+    if cls is N.SnCamera:
+        assert size == CAMERA_DTYPE.itemsize
 
 
 def test_camera_array_packs_reference_centre():
