@@ -217,6 +217,31 @@ int sn_blend_tile_range(int32_t t_begin, int32_t t_end, int32_t tiles_x, int32_t
                         const double *colors, const double *alphas, int64_t n_splats, double *color_acc,
                         double *alpha_acc, double *trans, double *depth_acc);
 
+/*
+ * Asset ingest on the device. Validation counters (DEVICE, 10 x uint64, zeroed by
+ * the caller): [0..4] rows with non-finite positions / sh / opacity / log-scales / rotations,
+ * [5] zero-norm rotations, [6] max |quat norm - 1| (float bits), [7] rows with negative weights,
+ * [8] rows with more than 4 nonzero weights, [9] max |weight row sum - 1| (double bits); flags
+ * (DEVICE, n bytes): per-row bits in the same order (bit 6 negative weight, bit 7 > 4 weights).
+ * Rotations are renormalized in float32 exactly as GaussianCloud.validate (cloud.py:80-86) does.
+ *
+ * sn_unpack_ply -- ply.load_gaussian_ply (ply.py:76-120): `table` is the DEVICE copy of the
+ *   row-major float32 vertex payload (n x n_props); cols (HOST, 14 + 3(K-1) int32) are the column
+ *   indices of x y z f_dc_0..2 opacity scale_0..2 rot_0..3 f_rest_0..; outputs are the sn_cloud
+ *   float32 buffers (pos+opacity (n,4), log-scales (n,4), rotations (n,4), sh (K*3, n)).
+ * sn_unpack_bundle -- avatar.load_avatar_bundle (avatar.py:191-254) + AvatarBundle.validate
+ *   (:155-176): canonical.f32 and weights.f32 (DEVICE copies) -> rows [row0, row0 + n) of the
+ *   sn_avatars float64 canonical buffers, SH SoA (K*3, sh_stride), packed joints and (n,4) float64
+ *   influence weights; row_sums (DEVICE, n) receives the numpy-order float64 row sums.
+ */
+int sn_unpack_ply(int64_t n, int32_t n_props, const float *table, const int32_t *cols, int32_t sh_k,
+                  float *pos_opacity, float *log_scales, float *rotations, float *sh, uint8_t *flags,
+                  uint64_t *counters, void *stream);
+int sn_unpack_bundle(int64_t n, int32_t sh_k, int32_t n_joints, const float *canonical, const float *weights,
+                     int64_t row0, int64_t sh_stride, double *pos_opacity, double *log_scales, double *rotations,
+                     float *sh, uint32_t *joints, double *weights4, double *row_sums, uint8_t *flags,
+                     uint64_t *counters, void *stream);
+
 /* Self-check of the blend's fast exponential (ex2.approx, float32): largest relative error against
  * float64 exp(-d2/2) over every float d2 in [0, 9.5]. The blend's error budget assumes <= 3.5e-7. */
 int sn_selftest_fast_exp(double *max_rel_err);

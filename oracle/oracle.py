@@ -328,3 +328,53 @@ def render_batch(scene_cloud, avatar_clouds_per_env, cameras, background, thread
 
 def tiles_for(width, height):
     return math.ceil(width / TILE_SIZE), math.ceil(height / TILE_SIZE)
+
+
+# ---------------------------------------------------------------------------------------------
+# Asset loaders: numpy restatements of the reference's readers, used as the CPU
+# baseline of scripts/bench_assets.py and as a second checker in tests. ply.py:76-120 +
+# cloud.py:50-87 (float32 quaternion renormalization when any norm is off by more than 1e-5).
+
+def load_gaussian_ply_numpy(path):
+    """ply.load_gaussian_ply: returns (positions, sh (n,K,3), opacities, log_scales, rotations)."""
+    with open(path, "rb") as f:
+        props, n = [], None
+        while True:
+            line = f.readline().decode("ascii").strip()
+            if line == "end_header":
+                break
+            parts = line.split()
+            if parts and parts[0] == "element":
+                if parts[1] == "vertex":
+                    n = int(parts[2])
+                    in_vertex = True
+                else:
+                    in_vertex = False
+            elif parts and parts[0] == "property" and in_vertex:
+                props.append(parts[2])
+        data = f.read(n * len(props) * 4)
+    table = np.frombuffer(data, dtype="<f4").reshape(n, len(props))
+    col = {name: i for i, name in enumerate(props)}
+    rest = sorted([p for p in props if p.startswith("f_rest_")], key=lambda s: int(s.rsplit("_", 1)[1]))
+    k = (len(rest) // 3) + 1
+
+    def cols(names):
+        return table[:, [col[c] for c in names]]
+
+    positions = cols(["x", "y", "z"]).copy()
+    sh = np.zeros((n, k, 3), dtype=np.float32)
+    sh[:, 0, :] = cols(["f_dc_0", "f_dc_1", "f_dc_2"])
+    if rest:
+        sh[:, 1:, :] = cols(rest).reshape(n, 3, k - 1).transpose(0, 2, 1)
+    opacities = table[:, col["opacity"]].copy()
+    log_scales = cols(["scale_0", "scale_1", "scale_2"]).copy()
+    rotations = cols(["rot_0", "rot_1", "rot_2", "rot_3"]).copy()
+    for a in (positions, sh, opacities, log_scales, rotations):
+        if not np.isfinite(a).all():
+            raise ValueError("non-finite values")
+    norms = np.linalg.norm(rotations, axis=1)
+    if (norms <= 0).any():
+        raise ValueError("zero-norm rotation")
+    if np.abs(norms - 1.0).max() > 1e-5:
+        rotations = rotations / norms[:, None]
+    return positions, sh, opacities, log_scales, rotations

@@ -64,7 +64,8 @@ EXPORTS = (
     "sn_abi_version", "sn_last_error", "sn_context_create", "sn_context_destroy", "sn_context_workspace_bytes",
     "sn_context_sync_stats", "sn_context_kernel_launches", "sn_context_render_retries",
     "sn_render", "sn_get_counts", "sn_get_sorted_ids", "sn_get_tile_csr", "sn_get_projection", "sn_sample_pose",
-    "sn_skin_lbs", "sn_blend_tile_range", "sn_composite", "sn_selftest_fast_exp",
+    "sn_skin_lbs", "sn_blend_tile_range", "sn_composite", "sn_selftest_fast_exp", "sn_unpack_ply",
+    "sn_unpack_bundle",
 )
 
 _lib = None
@@ -104,6 +105,8 @@ def load():
             "sn_blend_tile_range": ([i32] * 6 + [P, i64, P, i64, P, P, P, P, P, i64, P, P, P, P], ctypes.c_int),
             "sn_composite": ([i64] + [P] * 9 + [P], ctypes.c_int),
             "sn_selftest_fast_exp": ([ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+            "sn_unpack_ply": ([i64, i32, P, P, i32, P, P, P, P, P, P, P], ctypes.c_int),
+            "sn_unpack_bundle": ([i64, i32, i32, P, P, i64, i64, P, P, P, P, P, P, P, P, P, P], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

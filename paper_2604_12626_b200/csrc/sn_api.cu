@@ -992,6 +992,34 @@ int sn_skin_lbs(sn_context *ctx, const sn_avatars *avatars, int32_t avatar, int6
     return SN_OK;
 }
 
+int sn_unpack_ply(int64_t n, int32_t n_props, const float *table, const int32_t *cols, int32_t sh_k,
+                  float *pos_opacity, float *log_scales, float *rotations, float *sh, uint8_t *flags,
+                  uint64_t *counters, void *stream) {
+    SN_CHECK(n >= 0 && n_props >= 14 && cols != nullptr, "bad PLY table description");
+    SN_CHECK(sh_k == 1 || sh_k == 4 || sh_k == 9 || sh_k == 16, "sh_k must be 1, 4, 9 or 16");
+    for (int i = 0; i < 14 + 3 * (sh_k - 1); ++i) SN_CHECK(cols[i] >= 0 && cols[i] < n_props, "column out of range");
+    SN_CHECK(n == 0 || (table && pos_opacity && log_scales && rotations && sh && flags && counters), "null buffer");
+    SN_CUDA(launch_unpack_ply(n, n_props, table, cols, sh_k, pos_opacity, log_scales, rotations, sh, flags,
+                              reinterpret_cast<unsigned long long *>(counters), static_cast<cudaStream_t>(stream)));
+    return SN_OK;
+}
+
+int sn_unpack_bundle(int64_t n, int32_t sh_k, int32_t n_joints, const float *canonical, const float *weights,
+                     int64_t row0, int64_t sh_stride, double *pos_opacity, double *log_scales, double *rotations,
+                     float *sh, uint32_t *joints, double *weights4, double *row_sums, uint8_t *flags,
+                     uint64_t *counters, void *stream) {
+    SN_CHECK(n >= 0 && row0 >= 0 && sh_stride >= row0 + n, "bad bundle slice");
+    SN_CHECK(sh_k == 1 || sh_k == 4 || sh_k == 9 || sh_k == 16, "sh_k must be 1, 4, 9 or 16");
+    SN_CHECK(n_joints >= 1 && n_joints <= 255, "n_joints must be in [1, 255]");
+    SN_CHECK(n == 0 || (canonical && weights && pos_opacity && log_scales && rotations && sh && joints && weights4 &&
+                        row_sums && flags && counters),
+             "null buffer");
+    SN_CUDA(launch_unpack_bundle(n, sh_k, n_joints, canonical, weights, row0, sh_stride, pos_opacity, log_scales,
+                                 rotations, sh, joints, weights4, row_sums, flags,
+                                 reinterpret_cast<unsigned long long *>(counters), static_cast<cudaStream_t>(stream)));
+    return SN_OK;
+}
+
 int sn_selftest_fast_exp(double *max_rel_err) {
     SN_CHECK(max_rel_err != nullptr, "null argument");
     SN_CUDA(fast_exp_selftest(max_rel_err));

@@ -160,4 +160,13 @@ cudaError_t launch_blend_tile_range(int t_begin, int t_end, int tiles_x, int til
                                     const double *alphas, double *color_acc, double *alpha_acc, double *trans,
                                     double *depth_acc, cudaStream_t s);
 
+// sn_assets.cu
+cudaError_t launch_unpack_ply(int64_t n, int32_t n_props, const float *table, const int32_t *cols_host, int32_t sh_k,
+                              float *pos_opacity, float *log_scales, float *rotations, float *sh, uint8_t *flags,
+                              unsigned long long *cnt, cudaStream_t s);
+cudaError_t launch_unpack_bundle(int64_t n, int32_t sh_k, int32_t J, const float *canonical, const float *weights,
+                                 int64_t row0, int64_t sh_stride, double *pos_opacity, double *log_scales,
+                                 double *rotations, float *sh, uint32_t *joints, double *wts, double *sums,
+                                 uint8_t *flags, unsigned long long *cnt, cudaStream_t s);
+
 }  // namespace sn

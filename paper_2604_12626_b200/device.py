@@ -69,6 +69,25 @@ class DeviceCloud:
     def wrap(cls, cloud, device=None):
         return cloud if isinstance(cloud, DeviceCloud) else cls(cloud, device)
 
+    @classmethod
+    def from_device(cls, pos_opacity, log_scales, rotations, sh, sh_k, dtype, device):
+        """Wrap buffers already in the sn_cloud layout (e.g. unpacked by assets.load_gaussian_ply)."""
+        self = cls.__new__(cls)
+        self.n = int(pos_opacity.shape[0])
+        self.sh_k = int(sh_k)
+        self.dtype = dtype
+        self.device = device
+        self.pos_opacity, self.log_scales, self.rotations, self.sh = pos_opacity, log_scales, rotations, sh
+        self._struct = N.SnCloud(self.n, self.sh_k, dtype, pos_opacity.data_ptr(), log_scales.data_ptr(),
+                                 rotations.data_ptr(), sh.data_ptr())
+        return self
+
+    def to_host(self):
+        """(positions (n,3), sh_coeffs (n,K,3), opacities (n,), log_scales (n,3), rotations (n,4))"""
+        po = self.pos_opacity.cpu().numpy()
+        sh = self.sh.cpu().numpy().T.reshape(self.n, self.sh_k, 3)
+        return po[:, :3], sh, po[:, 3], self.log_scales.cpu().numpy()[:, :3], self.rotations.cpu().numpy()
+
     def struct(self):
         return self._struct
 
@@ -155,14 +174,43 @@ class DeviceAvatars:
             nf.append(q.shape[0])
             fps.append(float(traj.fps))
             frame_off += q.shape[0]
+        t = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+        self._finish(t(po), t(ls), t(rot), t(sh.reshape(n, k * 3).T), t(jpk.view(np.int32)), t(wts), counts, ib,
+                     tq, tt, toff, nf, fps, j, k, start_offsets, loops, dev)
+
+    @classmethod
+    def from_device(cls, po, ls, rot, sh, joints, weights, counts, specs, j, k, start_offsets, loops, device):
+        """Canonical buffers already on the device (assets.load_avatar_bundles); specs carry each
+        bundle's inv_bind and trajectory (host, float64)."""
+        self = cls.__new__(cls)
+        ib = np.stack([np.asarray(s.inv_bind, dtype=np.float64).reshape(j, 16) for s in specs])
+        tq, tt, toff, nf, fps = [], [], [], [], []
+        frame_off = 0
+        for s in specs:
+            q = np.asarray(s.trajectory.quats, dtype=np.float64)
+            tq.append(q.reshape(-1))
+            tt.append(np.asarray(s.trajectory.trans, dtype=np.float64).reshape(-1))
+            toff.append(frame_off)
+            nf.append(q.shape[0])
+            fps.append(float(s.trajectory.fps))
+            frame_off += q.shape[0]
+        self._finish(po, ls, rot, sh, joints, weights, counts, ib, tq, tt, toff, nf, fps, j, k, start_offsets, loops,
+                     device)
+        return self
+
+    def _finish(self, po, ls, rot, sh, joints, weights, counts, ib, tq, tt, toff, nf, fps, j, k, start_offsets, loops,
+                dev):
+        a = len(counts)
+        n = int(sum(counts))
+        self.offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        owner = np.repeat(np.arange(a, dtype=np.uint16), counts)
         so = np.zeros(a) if start_offsets is None else np.asarray(start_offsets, dtype=np.float64)
         lp = np.ones(a, dtype=np.int32) if loops is None else np.asarray(loops, dtype=np.int32)
         t = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)
         self.n, self.n_avatars, self.n_joints, self.sh_k, self.device = n, a, j, k, dev
-        self.counts = counts
-        self.pos_opacity, self.log_scales, self.rotations = t(po), t(ls), t(rot)
-        self.sh = t(sh.reshape(n, k * 3).T)
-        self.joints, self.weights, self.avatar_of = t(jpk.view(np.int32)), t(wts), t(owner.view(np.int16))
+        self.counts = list(counts)
+        self.pos_opacity, self.log_scales, self.rotations, self.sh = po, ls, rot, sh
+        self.joints, self.weights, self.avatar_of = joints, weights, t(owner.view(np.int16))
         self.inv_bind = t(ib)
         self.traj_q, self.traj_t = t(np.concatenate(tq)), t(np.concatenate(tt))
         self.traj_offset = t(np.asarray(toff, dtype=np.int64))

@@ -20,3 +20,15 @@ class ContractViolation(SplatNavError, ValueError):
 
 class NativeError(SplatNavError, RuntimeError):
     """The CUDA extension reported an error (message comes from sn_last_error())."""
+
+
+class PlyParseError(SplatNavError, ValueError):
+    """Malformed PLY header or payload; message names the offending part."""
+
+
+class UnsupportedLayoutError(SplatNavError, ValueError):
+    """PLY field layout does not match any supported SH degree."""
+
+
+class SchemaError(SplatNavError, ValueError):
+    """Config or manifest JSON is missing required keys or has wrong types."""
