@@ -242,6 +242,13 @@ int sn_unpack_bundle(int64_t n, int32_t sh_k, int32_t n_joints, const float *can
                      float *sh, uint32_t *joints, double *weights4, double *row_sums, uint8_t *flags,
                      uint64_t *counters, void *stream);
 
+/* Observation payload / frame export (frame_io.py:11-31): uint8 RGB exactly as save_color_png
+ * evaluates it on the same values (clip, x*255+0.5 in float64, truncation) and fp16 depth; depth16
+ * may be NULL. sn_flip_rows writes (frames, H, W) float32 images bottom-to-top (the PFM row order). */
+int sn_quantize_frames(int64_t npix, const float *color, const float *depth, uint8_t *rgb8, uint16_t *depth16,
+                       void *stream);
+int sn_flip_rows(int64_t frames, int32_t height, int32_t width, const float *src, float *dst, void *stream);
+
 /* Self-check of the blend's fast exponential (ex2.approx, float32): largest relative error against
  * float64 exp(-d2/2) over every float d2 in [0, 9.5]. The blend's error budget assumes <= 3.5e-7. */
 int sn_selftest_fast_exp(double *max_rel_err);

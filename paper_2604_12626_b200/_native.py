@@ -65,7 +65,7 @@ EXPORTS = (
     "sn_context_sync_stats", "sn_context_kernel_launches", "sn_context_render_retries",
     "sn_render", "sn_get_counts", "sn_get_sorted_ids", "sn_get_tile_csr", "sn_get_projection", "sn_sample_pose",
     "sn_skin_lbs", "sn_blend_tile_range", "sn_composite", "sn_selftest_fast_exp", "sn_unpack_ply",
-    "sn_unpack_bundle",
+    "sn_unpack_bundle", "sn_quantize_frames", "sn_flip_rows",
 )
 
 _lib = None
@@ -106,6 +106,8 @@ def load():
             "sn_composite": ([i64] + [P] * 9 + [P], ctypes.c_int),
             "sn_selftest_fast_exp": ([ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
             "sn_unpack_ply": ([i64, i32, P, P, i32, P, P, P, P, P, P, P], ctypes.c_int),
+            "sn_quantize_frames": ([i64, P, P, P, P, P], ctypes.c_int),
+            "sn_flip_rows": ([i64, i32, i32, P, P, P], ctypes.c_int),
             "sn_unpack_bundle": ([i64, i32, i32, P, P, i64, i64, P, P, P, P, P, P, P, P, P, P], ctypes.c_int),
         }
         for name, (args, res) in sig.items():

@@ -103,6 +103,7 @@ class HostPipeline:
 
 
 def quantize_observation(color, depth):
-    """uint8 RGB (x*255+0.5, frame_io.py:13-14) + fp16 depth, the gather payload."""
-    rgb = (color.clamp(0.0, 1.0) * 255.0 + 0.5).to(torch.uint8)
-    return rgb, depth.to(torch.float16)
+    """uint8 RGB (x*255+0.5, frame_io.py:13-14) + fp16 depth, the gather payload (one CUDA kernel,
+    sn_quantize_frames)."""
+    from .frame_io import quantize
+    return quantize(color, depth)

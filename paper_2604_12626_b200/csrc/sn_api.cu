@@ -1020,6 +1020,21 @@ int sn_unpack_bundle(int64_t n, int32_t sh_k, int32_t n_joints, const float *can
     return SN_OK;
 }
 
+int sn_quantize_frames(int64_t npix, const float *color, const float *depth, uint8_t *rgb8, uint16_t *depth16,
+                       void *stream) {
+    SN_CHECK(npix >= 0, "negative pixel count");
+    SN_CHECK(npix == 0 || (color && rgb8 && (depth16 == nullptr || depth != nullptr)), "null buffer");
+    SN_CUDA(launch_quantize(npix, color, depth, rgb8, depth16, static_cast<cudaStream_t>(stream)));
+    return SN_OK;
+}
+
+int sn_flip_rows(int64_t frames, int32_t height, int32_t width, const float *src, float *dst, void *stream) {
+    SN_CHECK(frames >= 0 && height >= 0 && width >= 0 && (frames * height * width == 0 || (src && dst && src != dst)),
+             "bad frame buffers");
+    SN_CUDA(launch_flip_rows(frames, height, width, src, dst, static_cast<cudaStream_t>(stream)));
+    return SN_OK;
+}
+
 int sn_selftest_fast_exp(double *max_rel_err) {
     SN_CHECK(max_rel_err != nullptr, "null argument");
     SN_CUDA(fast_exp_selftest(max_rel_err));

@@ -18,6 +18,8 @@
 #include "sn_common.cuh"
 #include "sn_internal.h"
 
+#include <cuda_fp16.h>
+
 namespace sn {
 
 namespace {
@@ -261,6 +263,55 @@ cudaError_t launch_unpack_bundle(int64_t n, int32_t sh_k, int32_t J, const float
     renorm_rot_kernel<<<grid_for(n), 256, 0, s>>>(n, d, cnt);
     pack_weights_kernel<<<grid_for(n), 256, 0, s>>>(n, J, weights, row0, joints, wts, sums, flags, cnt);
     renorm_weights_kernel<<<grid_for(n), 256, 0, s>>>(n, row0, wts, sums, cnt);
+    return cudaGetLastError();
+}
+
+}  // namespace sn
+
+// ---- frame export (frame_io.py:11-58) and the observation payload ----
+
+namespace sn {
+
+namespace {
+
+// uint8 colour exactly as frame_io.save_color_png (frame_io.py:13-14) evaluates it on the same
+// values: clip to [0, 1], x * 255 + 0.5 in float64, truncation; fp16 depth (round to nearest).
+__global__ void __launch_bounds__(256) quantize_kernel(int64_t npix, const float *color, const float *depth,
+                                                       uint8_t *rgb8, __half *depth16) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= npix) return;
+    for (int c = 0; c < 3; ++c) {
+        double x = (double)color[3 * i + c];
+        x = x < 0.0 ? 0.0 : (x > 1.0 ? 1.0 : x);
+        rgb8[3 * i + c] = (uint8_t)(x * 255.0 + 0.5);
+    }
+    if (depth16) depth16[i] = __float2half_rn(depth[i]);
+}
+
+// frame_io.save_depth_pfm (:23-31): rows bottom-to-top, little-endian float32
+__global__ void __launch_bounds__(256) flip_rows_kernel(int64_t frames, int32_t h, int32_t w, const float *src,
+                                                        float *dst) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t hw = (int64_t)h * w;
+    if (i >= frames * hw) return;
+    const int64_t f = i / hw, p = i % hw, y = p / w, x = p % w;
+    dst[f * hw + (int64_t)(h - 1 - y) * w + x] = src[i];
+}
+
+}  // namespace
+
+cudaError_t launch_quantize(int64_t npix, const float *color, const float *depth, uint8_t *rgb8, uint16_t *depth16,
+                            cudaStream_t s) {
+    if (npix == 0) return cudaSuccess;
+    quantize_kernel<<<(unsigned)((npix + 255) / 256), 256, 0, s>>>(npix, color, depth, rgb8,
+                                                                   reinterpret_cast<__half *>(depth16));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_flip_rows(int64_t frames, int32_t h, int32_t w, const float *src, float *dst, cudaStream_t s) {
+    const int64_t n = frames * h * w;
+    if (n == 0) return cudaSuccess;
+    flip_rows_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(frames, h, w, src, dst);
     return cudaGetLastError();
 }
 
