@@ -31,12 +31,12 @@ class BatchRenderer:
         return self.scene.device
 
     def render(self, cameras, sim_times=None, avatar_active=None, tiled=True, contrib=False, stats=False,
-               exact=False):
+               exact=False, out=None):
         if self.avatars is not None and sim_times is None:
             sim_times = np.zeros(len(cameras))
         return render_frames(self.scene, cameras, self.background, avatars=self.avatars, sim_times=sim_times,
                              tiled=tiled, context=self.context, contrib=contrib, stats=stats,
-                             avatar_active=avatar_active, exact=exact)
+                             avatar_active=avatar_active, exact=exact, out=out)
 
     def render_to_host(self, cameras, sim_times=None, host_out=None):
         """render() followed by a device->host copy into pinned buffers (the end-to-end path)."""
@@ -70,8 +70,11 @@ class HostPipeline:
                   "depth": (n_envs, height, width)}
         self.host = [{k: torch.empty(shapes[k], dtype=torch.float32, pin_memory=True) for k in self.KEYS}
                      for _ in range(depth)]
+        # device frames of each slot, rendered into in place: no allocation per step (a caching-
+        # allocator miss would cudaMalloc / cudaFree and serialize the render with the copies)
+        self.dev = [{k: torch.empty(shapes[k], dtype=torch.float32, device=dev) for k in self.KEYS}
+                    for _ in range(depth)]
         self.done = [None] * depth
-        self.keep = [None] * depth
         self.i = 0
 
     def submit(self, cameras, sim_times=None):
@@ -80,18 +83,16 @@ class HostPipeline:
         if self.done[slot] is not None:
             self.done[slot].synchronize()  # host buffer of this slot is free again
         with torch.cuda.stream(self.render_stream):
-            out = self.r.render(cameras, sim_times)
+            out = self.r.render(cameras, sim_times, out=dict(self.dev[slot]))
             ready = torch.cuda.Event()
             ready.record(self.render_stream)
         with torch.cuda.stream(self.copy_stream):
             self.copy_stream.wait_event(ready)
             for k in self.KEYS:
                 self.host[slot][k].copy_(out[k], non_blocking=True)
-                out[k].record_stream(self.copy_stream)
             ev = torch.cuda.Event()
             ev.record(self.copy_stream)
         self.done[slot] = ev
-        self.keep[slot] = out
         return slot
 
     def wait(self, slot=None):

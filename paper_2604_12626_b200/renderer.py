@@ -58,7 +58,7 @@ def _nonempty(c):
 
 def render_frames(scene, cameras, background, layer=None, avatars=None, sim_times=None, tiled=True,
                   context=None, contrib=False, stats=True, avatar_active=None, stage_ms=None, work=None,
-                  binning=-1, exact=False):
+                  binning=-1, exact=False, out=None):
     """One sn_render call over E cameras. Returns a dict of device tensors:
     color (E,H,W,3), alpha (E,H,W), depth (E,H,W) float32; stats (E,5) int64; optionally
     contrib_scene / contrib_layer (E,H,W) int32. The context keeps the pass intermediates for
@@ -70,11 +70,13 @@ def render_frames(scene, cameras, background, layer=None, avatars=None, sim_time
     e = len(cameras)
     h, w = int(cameras[0].height), int(cameras[0].width)
     cams = camera_array(cameras, background)
-    out = {
-        "color": torch.empty((e, h, w, 3), dtype=torch.float32, device=dev),
-        "alpha": torch.empty((e, h, w), dtype=torch.float32, device=dev),
-        "depth": torch.empty((e, h, w), dtype=torch.float32, device=dev),
-    }
+    if out is None:  # caller-owned outputs (e.g. HostPipeline's ring) avoid per-call allocations
+        out = {}
+    shapes = {"color": (e, h, w, 3), "alpha": (e, h, w), "depth": (e, h, w)}
+    for k, shp in shapes.items():
+        t = out.get(k)
+        if t is None or tuple(t.shape) != shp or t.dtype != torch.float32 or t.device != dev or not t.is_contiguous():
+            out[k] = torch.empty(shp, dtype=torch.float32, device=dev)
     opts = N.SnRenderOpts()
     opts.tiled = 1 if tiled else 0
     opts.binning = int(binning)
