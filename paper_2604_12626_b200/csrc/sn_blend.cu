@@ -175,7 +175,26 @@ __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1
     // mean - tile origin, from the principal-axis offsets (float error ~ 2u (|U1| + |U2|))
     const float mx = 8.0f - (f.U1 * f.e1x - f.U2 * f.e1y), my = 8.0f - (f.U1 * f.e1y + f.U2 * f.e1x);
     const float slack = 1e-3f + 4.0f * u * (aU1 + aU2);
-    return warp_block_mask(mx, my, gr.z * 1.00001f + slack, gr.w * 1.00001f + slack);
+    unsigned m = warp_block_mask(mx, my, gr.z * 1.00001f + slack, gr.w * 1.00001f + slack);
+    if (ok && m) {
+        // Separating axes along the ellipse's own axes (the support's oriented bounding box,
+        // |u_k| <= 3 / sqrt(l_k), against each 8 x 4 block of pixel centres projected on e_k):
+        // rotated, elongated splats whose axis-aligned box reaches a block often miss it.
+        const float ax = fabsf(f.e1x), ay = fabsf(f.e1y);
+        const float marg = 1e-3f + 8.0f * u * (aU1 + aU2 + 16.0f);
+        const float ext1 = 3.0f * rsqrtf(l1) * 1.00001f + marg + (3.5f * ax + 1.5f * ay);
+        const float ext2 = 3.0f * rsqrtf(l2) * 1.00001f + marg + (3.5f * ay + 1.5f * ax);
+        // u_k at the block centres (8 bx - 4, 4 by - 6) relative to the tile centre
+        const float u1b = f.U1 - 4.0f * f.e1x - 6.0f * f.e1y, u2b = f.U2 + 4.0f * f.e1y - 6.0f * f.e1x;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            const float bx = (float)(w & 1), by = (float)(w >> 1);
+            const float u1c = u1b + 8.0f * bx * f.e1x + 4.0f * by * f.e1y;
+            const float u2c = u2b - 8.0f * bx * f.e1y + 4.0f * by * f.e1x;
+            if (fabsf(u1c) > ext1 || fabsf(u2c) > ext2) m &= ~(1u << w);
+        }
+    }
+    return m;
 }
 
 __device__ __forceinline__ bool covers(ushort4 r, int tx, int ty) {
