@@ -672,6 +672,235 @@ __device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_
     return ExactPixel{cr, cg, cb, A, D, T, (int)__reduce_add_sync(kFull, (unsigned)nc)};
 }
 
+// exact_walk for one pixel by a whole CTA (long, unsaturated lists: avatar-layer fixups). The 8
+// warps gather and evaluate up to 1,024 candidates per step (256 per step on the streamed-rectangle
+// source), the contributions are compacted in candidate order into a shared queue, and warp 0
+// consumes them 32 at a time exactly as exact_walk does -- same groups, bit-identical result.
+// Returns the reduced pixel in warp 0 (other warps' return values are unspecified).
+constexpr int kCtaPer = 4;
+constexpr int kCtaQueue = kCtaPer * kBlock + 32;
+__device__ ExactPixel exact_walk_cta(const PassView &v, int el, int tile, int tiles_x, int px_i, int py_i,
+                                     const double *s_exp, QEntry *q, int *s_i) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const double px = px_i + 0.5, py = py_i + 0.5;
+    float cr = 0.0f, cg = 0.0f, cb = 0.0f;
+    double A = 0.0, D = 0.0, T = 1.0;
+    int nc = 0;
+    bool done = false;  // warp 0's view
+    int qn = 0;         // queued contributions (uniform)
+    auto consume = [&](int head, int m) {  // warp 0: q[head, head + m), m <= 32
+        const bool act = lane < m;
+        QEntry e{};
+        if (act) e = q[head + lane];
+        double pp = act ? 1.0 - e.a : 1.0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const double o = __shfl_up_sync(kFull, pp, d);
+            if (lane >= d) pp *= o;
+        }
+        double ex = __shfl_up_sync(kFull, pp, 1);
+        if (lane == 0) ex = 1.0;
+        const double t_after = T * pp;
+        const unsigned cut = __ballot_sync(kFull, act && t_after < kTCutoff);
+        const int last = cut ? __ffs(cut) - 1 : m - 1;
+        if (act && lane <= last) {
+            const double w = e.a * (T * ex);
+            const float wf = (float)w;
+            cr = __fmaf_rn(e.r, wf, cr);
+            cg = __fmaf_rn(e.g, wf, cg);
+            cb = __fmaf_rn(e.b, wf, cb);
+            A = A + w;
+            D = fma(e.z, w, D);
+            ++nc;
+        }
+        T = __shfl_sync(kFull, t_after, last);
+        if (cut) done = true;
+    };
+    uint32_t cur, end;
+    if (v.source == 1) {
+        uint2 r = v.ranges[((uint32_t)el << v.tile_bits) | (uint32_t)tile];
+        cur = r.x;
+        end = r.y;
+    } else {
+        cur = (uint32_t)v.env_off[el];
+        end = (uint32_t)v.env_off[el + 1];
+    }
+    int *s_cnt = s_i;           // [8] per-warp counts
+    int *s_flag = s_i + 8;      // [0] done, [1] next cursor (source 0 batch search)
+    while (cur < end) {
+        uint32_t step;
+        int per;
+        if (v.source == 0) {  // one 256-splat batch per step; warp 0 finds the next covering batch
+            if (warp == 0) {
+                uint32_t c = cur;
+                while (c < end) {
+                    const uint32_t bi = c / kBlock;
+                    const uint32_t nb = (end + kBlock - 1) / kBlock;
+                    const unsigned hit =
+                        __ballot_sync(kFull, bi + lane < nb && covers(__ldg(v.batch_rects + bi + lane), tx, ty));
+                    if (hit) {
+                        c = max(c, (bi + __ffs(hit) - 1) * (uint32_t)kBlock);
+                        break;
+                    }
+                    c = min(end, (bi + 32) * (uint32_t)kBlock);
+                }
+                if (lane == 0) s_flag[1] = (int)c;
+            }
+            __syncthreads();
+            cur = (uint32_t)s_flag[1];
+            if (cur >= end) break;
+            step = min((uint32_t)kBlock - cur % kBlock, end - cur);
+            per = 1;
+        } else {
+            step = min((uint32_t)(kCtaPer * kBlock), end - cur);
+            per = kCtaPer;
+        }
+        for (int i = 0; i < per; ++i) {
+            const uint32_t k = cur + (uint32_t)(i * kBlock) + threadIdx.x;
+            bool contrib = false;
+            QEntry e{};
+            if (k < cur + step) {
+                uint32_t rid = k;
+                bool cand = true;
+                if (v.source == 0) cand = covers(__ldg(v.rects + k), tx, ty);
+                else if (v.source == 1) rid = __ldg(v.pair_vals + k);
+                if (cand) {
+                    const SplatRec &sr = v.recs[__ldg(v.order + rid)];
+                    const double dx = sr.mx - px, dy = sr.my - py;
+                    const double d2 = (sr.ca * dx * dx + sr.cb2 * dx * dy) + sr.cc * dy * dy;
+                    if (!(d2 > kSupportD2)) {
+                        contrib = true;
+                        double ev;
+                        SN_EXP_NEG_HALF(d2, s_exp, ev);
+                        e.a = sr.alpha * ev;
+                        if (e.a > kAlphaClip) e.a = kAlphaClip;
+                        e.z = sr.z;
+                        float rgb[3];
+                        unpack_rgb21(sr.rgb, rgb);
+                        e.r = rgb[0];
+                        e.g = rgb[1];
+                        e.b = rgb[2];
+                    }
+                }
+            }
+            const unsigned bal = __ballot_sync(kFull, contrib);
+            if (lane == 0) s_cnt[warp] = __popc(bal);
+            __syncthreads();
+            int off = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < kBlock / 32; ++w) {
+                const int c = s_cnt[w];
+                off += w < warp ? c : 0;
+                tot += c;
+            }
+            if (contrib) q[qn + off + __popc(bal & ((1u << lane) - 1u))] = e;
+            qn += tot;
+            __syncthreads();
+        }
+        // warp 0 consumes whole groups of 32; the remainder moves to the queue's front
+        if (warp == 0) {
+            int head = 0;
+            while (!done && qn - head >= 32) {
+                consume(head, 32);
+                head += 32;
+            }
+            const int rest = done ? 0 : qn - head;
+            QEntry t{};
+            if (lane < rest) t = q[head + lane];
+            __syncwarp();
+            if (lane < rest) q[lane] = t;
+            if (lane == 0) {
+                s_flag[0] = done;
+                s_cnt[0] = rest;
+            }
+        }
+        __syncthreads();
+        qn = s_cnt[0];
+        const bool stop = s_flag[0] != 0;
+        __syncthreads();
+        if (stop) break;
+        cur += step;
+    }
+    if (warp == 0) {
+        if (!done && qn > 0) consume(0, qn);
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            cr += __shfl_xor_sync(kFull, cr, d);
+            cg += __shfl_xor_sync(kFull, cg, d);
+            cb += __shfl_xor_sync(kFull, cb, d);
+            A += __shfl_xor_sync(kFull, A, d);
+            D += __shfl_xor_sync(kFull, D, d);
+        }
+        nc = (int)__reduce_add_sync(kFull, (unsigned)nc);
+    }
+    __syncthreads();  // the queue and scratch are reused by the next walk
+    return ExactPixel{cr, cg, cb, A, D, T, nc};
+}
+
+// Layer fixups (mode 2): a CTA per listed pixel (their walks are long: near avatars' tile lists
+// run to tens of thousands of pairs and rarely saturate).
+__global__ void __launch_bounds__(256) fixup_layer_kernel(BlendArgs b) {
+    __shared__ double s_exp[64];
+    __shared__ QEntry s_q[kCtaQueue];
+    __shared__ int s_i[16];
+    __shared__ int s_back;
+    if (threadIdx.x < 64) s_exp[threadIdx.x] = kExp2Tbl[threadIdx.x];
+    __syncthreads();
+    if (pass_overflow(b.pv) || pass_overflow(b.back)) return;
+    const unsigned n_fix = *b.fix_count;
+    const unsigned hw = (unsigned)b.width * (unsigned)b.height;
+    unsigned long long contribs = 0;
+    for (unsigned i = blockIdx.x; i < n_fix; i += gridDim.x) {
+        const uint32_t code = b.fix_list[i];
+        const int el = (int)(code / hw), p = (int)(code % hw);
+        const int py_i = p / b.width, px_i = p % b.width;
+        const int env = b.e0 + el;
+        const int tile = (py_i / kTile) * b.tiles_x + px_i / kTile;
+        const sn_camera &cam = b.cams[env];
+        const ExactPixel f = exact_walk_cta(b.pv, el, tile, b.tiles_x, px_i, py_i, s_exp, s_q, s_i);
+        const int64_t pix = ((int64_t)env * b.height + py_i) * b.width + px_i;
+        const double alpha = f.A < 1.0 ? f.A : 1.0;
+        const double depth = f.A > 0.0 ? f.D / f.A : cam.far_;
+        if (threadIdx.x == 0) {
+            contribs += (unsigned)f.nc;
+            if (b.contrib) b.contrib[pix] = f.nc;
+            // the back depth in the frame is within derr of the float64 value: recompute the scene
+            // pixel only when the exact front depth falls inside that band
+            s_back = f.A > 0.0 && fabs(depth - (double)b.depth[pix]) <= 1.01 * (double)b.derr[pix] + 1e-30;
+        }
+        __syncthreads();
+        const bool exact_back = s_back != 0;
+        __syncthreads();
+        ExactPixel k{};
+        if (exact_back) k = exact_walk_cta(b.back, el, tile, b.tiles_x, px_i, py_i, s_exp, s_q, s_i);
+        if (threadIdx.x != 0 || !(f.A > 0.0)) continue;  // front depth = far: the back is kept
+        float *oc = b.color + 3 * pix;
+        float bc[3] = {oc[0], oc[1], oc[2]};
+        float ba = b.alpha[pix];
+        double bd = (double)b.depth[pix];
+        if (exact_back) {  // the scene frame exactly as the scene pass stores it (float32)
+            bc[0] = (float)np_clip((double)k.cr + cam.background[0] * k.T, 0.0, 1.0);
+            bc[1] = (float)np_clip((double)k.cg + cam.background[1] * k.T, 0.0, 1.0);
+            bc[2] = (float)np_clip((double)k.cb + cam.background[2] * k.T, 0.0, 1.0);
+            ba = (float)(k.A < 1.0 ? k.A : 1.0);
+            bd = k.A > 0.0 ? k.D / k.A : cam.far_;
+        }
+        if (depth < bd) {  // composite, renderer.py:151-166
+            const double fc[3] = {np_clip((double)f.cr / f.A, 0.0, 1.0), np_clip((double)f.cg / f.A, 0.0, 1.0),
+                                  np_clip((double)f.cb / f.A, 0.0, 1.0)};
+            for (int c = 0; c < 3; ++c) oc[c] = (float)(fc[c] * alpha + (double)bc[c] * (1.0 - alpha));
+            b.alpha[pix] = (float)(alpha + (double)ba * (1.0 - alpha));
+            b.depth[pix] = (float)(alpha >= 0.5 ? depth : bd);
+        } else if (exact_back) {
+            for (int c = 0; c < 3; ++c) oc[c] = bc[c];
+            b.alpha[pix] = ba;
+            b.depth[pix] = (float)bd;
+        }
+    }
+    if (b.contribs && threadIdx.x == 0 && contribs) atomicAdd(b.contribs, contribs);
+}
+
 // Recomputes the listed pixels exactly (warp per pixel, grid-stride over the device-side count)
 // and writes the same outputs the float64 blend epilogue writes. Mode 2 also recomputes the scene
 // pixel (the back layer) so the composite's comparisons see float64 depths.
@@ -851,7 +1080,7 @@ static void launch_blend_mode(const BlendArgs &b, dim3 grid, cudaStream_t s) {
 cudaError_t launch_layer_composite(const BlendArgs &b, cudaStream_t s) {
     dim3 grid((unsigned)(tiles_of(b.width) * tiles_of(b.height)), (unsigned)b.ec);
     composite_kernel<<<grid, kBlock, 0, s>>>(b);
-    fixup_kernel<2><<<kFixupBlocks, 256, 0, s>>>(b);
+    fixup_layer_kernel<<<kFixupBlocks, 256, 0, s>>>(b);
     return cudaGetLastError();
 }
 
