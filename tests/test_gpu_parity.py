@@ -454,3 +454,50 @@ def test_capacity_growth_rerenders_exactly():
         o = _oracle_check_env(out, e, big, cams[e], bg, context=ctx)
         check_frame(out["color"][e].cpu().numpy(), out["alpha"][e].cpu().numpy(), out["depth"][e].cpu().numpy(),
                     o.color, o.alpha, o.depth, cams[e].far)
+
+
+def test_env_chunking_with_avatar_layer():
+    """E > 64 with the avatar layer: chunks are rendered scene then layer (the layer's fixups read the
+    same chunk's scene workspace); every env's observation must match the oracle fed the GPU-skinned
+    clouds, and the layer's contributor counts must be exact."""
+    from paper_2604_12626_b200 import rig
+    from paper_2604_12626_b200.batch import BatchRenderer
+    from paper_2604_12626_b200.cloud import concat_clouds
+    box, bundles = _avatar_setup(2, 2500, seed=71)
+    scene = S.make_scene(20_000, box[0], box[1], seed=72)
+    cams = S.room_cameras(70, box, seed=73, width=48, height=40)
+    times = np.linspace(0.0, 0.35, 70)
+    br = BatchRenderer(scene, bundles, start_offsets=[0.0, 0.05], loops=[1, 1], background=(0.3, 0.3, 0.3))
+    out = br.render(cams, times, contrib=True)
+    for e in (0, 31, 63, 64, 69):
+        clouds = [rig.AvatarRuntime(b, start_offset=[0.0, 0.05][a], loop=True).deformed_cloud(float(times[e]))
+                  for a, b in enumerate(bundles)]
+        o = O.render_observation(scene, clouds, cams[e], np.array([0.3, 0.3, 0.3]))
+        check_frame(out["color"][e].cpu().numpy(), out["alpha"][e].cpu().numpy(), out["depth"][e].cpu().numpy(),
+                    o.color, o.alpha, o.depth, cams[e].far)
+        lo = O.rasterize(concat_clouds(clouds), cams[e], None)
+        np.testing.assert_array_equal(out["contrib_layer"][e].cpu().numpy(), lo.contrib)
+
+
+def test_degenerate_and_extreme_splats():
+    """Huge, needle-thin and non-finite-scale splats (the float32 chain's worst conditioning and the
+    degenerate path) against the oracle, fast path and exact mode."""
+    from paper_2604_12626_b200 import _native as N
+    box = S.room_box(1_000_000)
+    scene = S.make_scene(40_000, box[0], box[1], seed=81)
+    rng = np.random.default_rng(82)
+    ls = scene.log_scales.copy()
+    ls[:300] = np.stack([rng.uniform(-1.0, 0.5, 300), rng.uniform(-9.0, -7.0, 300), rng.uniform(-9, -7, 300)], 1)
+    ls[300:310] = 400.0  # overflow -> non-finite covariance -> degenerate (projection.py:44-51,154)
+    scene.log_scales = ls.astype(np.float32)
+    cams = S.room_cameras(3, box, seed=83, width=160, height=120, near=0.01)
+    bg = np.array([1.0, 1.0, 1.0])
+    for exact in (False, True):
+        ctx = N.Context()
+        out = R().render_frames(scene, cams, bg, contrib=True, context=ctx, exact=exact)
+        for e in range(3):
+            o = _oracle_check_env(out, e, scene, cams[e], bg, context=ctx)
+            check_frame(out["color"][e].cpu().numpy(), out["alpha"][e].cpu().numpy(), out["depth"][e].cpu().numpy(),
+                        o.color, o.alpha, o.depth, cams[e].far)
+            assert out["stats"][e].tolist() == [o.stats[k] for k in ("n_input", "n_culled_depth", "n_culled_frame",
+                                                                     "n_degenerate", "n_drawn")]
