@@ -89,7 +89,7 @@ struct PassWs {
 
 struct sn_context {
     PassWs pass[2];
-    Buf cams, times, derr, jm, eq, root, err, pose_q, pose_t, loads, fixcnt;
+    Buf cams, times, derr, jm, eq, root, err, pose_q, pose_t, loads, fixcnt, av_ext, av_cull, rpose_q, rpose_t;
     Buf lcolor, lalpha, ldepth, lderr, laerr, tile_flag;  // deferred-composite layer frame
     // mapped pinned words the device writes with a one-thread kernel: reading a total this way
     // never queues behind other streams' bulk copies on the device->host copy engine
@@ -172,6 +172,7 @@ struct PassSpec {
     const sn_avatars *avatars = nullptr;
     PoseView pose{};
     const uint8_t *avatar_active = nullptr;
+    const uint8_t *avatar_cull = nullptr;
     int mode = 0;
 };
 
@@ -230,6 +231,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     a.blk_counts = w.blk_counts.as<uint32_t>();
     a.stats = opts && opts->stats ? reinterpret_cast<unsigned long long *>(opts->stats) : nullptr;
     a.avatar_active = sp.avatar_active;
+    a.avatar_cull = sp.avatar_cull;
     a.tiles_x = tiles_x;
     a.tiles_y = tiles_y;
     a.z_base = z_base;
@@ -535,7 +537,7 @@ int sn_context_destroy(sn_context *ctx) {
             free_buf(*b);
     }
     for (Buf *b : {&ctx->cams, &ctx->times, &ctx->derr, &ctx->jm, &ctx->eq, &ctx->root, &ctx->err, &ctx->pose_q,
-                   &ctx->pose_t, &ctx->loads, &ctx->fixcnt, &ctx->lcolor, &ctx->lalpha, &ctx->ldepth, &ctx->lderr,
+                   &ctx->pose_t, &ctx->loads, &ctx->fixcnt, &ctx->av_ext, &ctx->av_cull, &ctx->rpose_q, &ctx->rpose_t, &ctx->lcolor, &ctx->lalpha, &ctx->ldepth, &ctx->lderr,
                    &ctx->laerr, &ctx->tile_flag})
         free_buf(*b);
     if (ctx->have_events) {
@@ -664,6 +666,13 @@ int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, con
         // kernel its error flag) into mapped memory; check them against the capacities
         SN_CUDA(cudaStreamSynchronize(st));
         SN_CHECK(ctx->h_err[0] == 0, "sample time must be nonnegative");
+        if (with_avatars && getenv("SN_DEBUG_CULL")) {
+            std::vector<uint8_t> codes((size_t)n_envs * avatars->n_avatars);
+            SN_CUDA(cudaMemcpy(codes.data(), ctx->av_cull.p, codes.size(), cudaMemcpyDeviceToHost));
+            int c[4] = {0, 0, 0, 0};
+            for (uint8_t v : codes) c[v & 3]++;
+            fprintf(stderr, "avatar cull: test %d depth %d frame %d\n", c[0], c[kCullDepth], c[kCullFrame]);
+        }
         bool grow = false;
         for (int p = 0; p < 2; ++p) {
             uint64_t need_v = 0, need_p = 0, sum_v = 0, sum_p = 0, last_v = 0, last_p = 0;
@@ -789,13 +798,22 @@ static int render_once(sn_context *ctx, const sn_cloud *scene, const sn_cloud *l
             StageTimer ptm{ctx, lst, opts && opts->stage_ms ? opts->stage_ms + SN_N_STAGES : nullptr, 1};
             ptm.begin(SN_STAGE_POSE);
             ctx->launches += 1;
-            SN_CUDA(launch_pose(*avatars, ctx->times.as<double>(), n_envs, nullptr, nullptr, ctx->jm.as<double>(),
-                                ctx->eq.as<double>(), ctx->root.as<double>(), ctx->err.as<int32_t>(), lst));
+            SN_ENSURE(ctx->rpose_q, sizeof(double) * (size_t)n_envs * A * (J + 1) * 4);
+            SN_ENSURE(ctx->rpose_t, sizeof(double) * (size_t)n_envs * A * (J + 1) * 3);
+            SN_CUDA(launch_pose(*avatars, ctx->times.as<double>(), n_envs, ctx->rpose_q.as<double>(),
+                                ctx->rpose_t.as<double>(), ctx->jm.as<double>(), ctx->eq.as<double>(),
+                                ctx->root.as<double>(), ctx->err.as<int32_t>(), lst));
             ptm.end();
             ctx->launches += 1;
             SN_CUDA(launch_publish_i32(ctx->err.as<int32_t>(), ctx->d_err, lst));  // checked by sn_render
             layer_spec.avatars = avatars;
             layer_spec.pose = PoseView{ctx->jm.as<double>(), ctx->eq.as<double>(), ctx->root.as<double>(), J, A};
+            SN_ENSURE(ctx->av_ext, sizeof(unsigned long long) * (2 + J) * A);
+            SN_ENSURE(ctx->av_cull, (size_t)n_envs * A);
+            ctx->launches += 2;
+            SN_CUDA(launch_avatar_cull(*avatars, layer_spec.pose, ctx->rpose_t.as<double>(), ctx->cams.as<sn_camera>(),
+                                       n_envs, ctx->av_ext.as<unsigned long long>(), ctx->av_cull.as<uint8_t>(), lst));
+            layer_spec.avatar_cull = ctx->av_cull.as<uint8_t>();
             layer_spec.avatar_active = opts ? opts->avatar_active : nullptr;
         }
         r = run_pass(ctx, 1, layer_spec, e0, ec, W, H, tiled, z_lo, z_bits, opts, color, alpha, depth, derr, lst,

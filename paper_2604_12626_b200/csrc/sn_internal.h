@@ -32,6 +32,7 @@ struct PrepArgs {
     uint32_t *blk_counts;   // (ec, n_blocks) -> exclusive offsets after scan
     unsigned long long *stats;  // (E, 5) device, may be null
     const uint8_t *avatar_active;  // (E, A), avatars only, may be null
+    const uint8_t *avatar_cull;    // (E, A) whole-avatar cull codes, avatars only, may be null
     // emit outputs (unsorted, env-major, index order within env)
     const uint64_t *env_off;  // (ec + 1)
     uint32_t *keys;            // 32-bit depth keys: top bits of (env << z_bits | z_bits - z_base)
@@ -63,6 +64,9 @@ cudaError_t launch_publish_i32(const int32_t *src, int32_t *mapped_dst, cudaStre
 // sn_rig.cu
 cudaError_t launch_pose(const sn_avatars &av, const double *sim_times, int32_t n_envs, double *pose_q, double *pose_t,
                         double *joint_mats, double *eff_q, double *root, int32_t *err_flag, cudaStream_t s);
+// (env, avatar) whole-avatar cull codes (0 test, kCullDepth, kCullFrame) after launch_pose
+cudaError_t launch_avatar_cull(const sn_avatars &av, const PoseView &pv, const double *pose_t, const sn_camera *cams,
+                               int32_t n_envs, unsigned long long *ext, uint8_t *codes, cudaStream_t s);
 cudaError_t launch_joint_prep(const sn_avatars &av, int32_t avatar, const double *pose_q, const double *pose_t,
                               double *joint_mats, double *eff_q, double *root, cudaStream_t s);
 

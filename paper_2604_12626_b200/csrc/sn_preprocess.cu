@@ -66,10 +66,12 @@ __device__ __forceinline__ void flush_counts(unsigned (*s_cnt)[5], const PrepArg
     __syncthreads();
     int t = threadIdx.x;
     if (t < a.ec) a.blk_counts[(int64_t)t * a.n_blocks + blockIdx.x] = s_cnt[t][4];
-    if (a.stats != nullptr && t < a.ec * 5) {
-        int e = t / 5, f = t % 5;  // sn_stats field order: input, depth, frame, degenerate, drawn
-        unsigned v = s_cnt[e][f];
-        if (v) atomicAdd(a.stats + (int64_t)(a.e0 + e) * 5 + f, (unsigned long long)v);
+    if (a.stats != nullptr) {
+        for (int i = t; i < a.ec * 5; i += blockDim.x) {  // ec * 5 can exceed the block (64 envs: 320)
+            int e = i / 5, f = i % 5;  // sn_stats field order: input, depth, frame, degenerate, drawn
+            unsigned v = s_cnt[e][f];
+            if (v) atomicAdd(a.stats + (int64_t)(a.e0 + e) * 5 + f, (unsigned long long)v);
+        }
     }
 }
 
@@ -399,8 +401,11 @@ __global__ void __launch_bounds__(kBlock) avatar_count_kernel(sn_avatars av, Pos
     uint64_t mask = 0;
     for (int e = 0; e < a.ec; ++e) {
         int env = a.e0 + e;
+        const uint8_t *cull = a.avatar_cull ? a.avatar_cull + (int64_t)env * av.n_avatars : nullptr;
+        // both avatars of this block culled whole for this env: no pose staging, no skinning
+        const bool stage = !(cull && cull[a_lo] && cull[a_hi]);
         __syncthreads();
-        for (int k = threadIdx.x; k < 2 * pb; k += kBlock) {
+        for (int k = threadIdx.x; stage && k < 2 * pb; k += kBlock) {
             const int slot = k / pb, o = k % pb, av_id = slot ? a_hi : a_lo;
             const int64_t ea = (int64_t)env * pv.n_avatars + av_id;
             double v;
@@ -415,7 +420,9 @@ __global__ void __launch_bounds__(kBlock) avatar_count_kernel(sn_avatars av, Pos
         __syncthreads();
         bool input = valid && avatar_on(a, av.n_avatars, env, avatar);
         int code = -1;
-        if (input) {
+        if (input && cull && cull[avatar]) {
+            code = cull[avatar];  // the whole avatar is depth- or frame-culled in this env
+        } else if (input) {
             double p[3], q[4];
             if (avatar == a_lo || avatar == a_hi) {
                 const double *blk = s_pose + (avatar == a_lo ? 0 : pb);

@@ -180,6 +180,101 @@ __global__ void joint_prep_kernel(sn_avatars av, int avatar, const double *pose_
     }
 }
 
+// Per avatar: the largest canonical position norm and the largest 3D standard deviation
+// exp(max log-scale); per (avatar, joint): d_j = the largest |inv_bind_j P| over the gaussians the
+// joint influences -- the inputs of the (env, avatar) culling bound below.
+// ext layout per avatar: [0] |P|max, [1] s_max, [2 .. 2 + J) d_j (non-negative doubles as bits)
+__global__ void avatar_extent_kernel(sn_avatars av, unsigned long long *ext) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= av.n) return;
+    const int a = av.avatar_of[g], J = av.n_joints;
+    unsigned long long *e = ext + (int64_t)a * (2 + J);
+    const double *p = av.pos_opacity + 4 * g, *l = av.log_scales + 4 * g;
+    const double r = sqrt((p[0] * p[0] + p[1] * p[1]) + p[2] * p[2]);
+    const double sm = exp(fmax(fmax(l[0], l[1]), l[2]));
+    // non-negative doubles order like their bit patterns; NaN/inf poison the bound (no culling)
+    atomicMax(e, (unsigned long long)__double_as_longlong(r == r ? r : INFINITY));
+    atomicMax(e + 1, (unsigned long long)__double_as_longlong(sm == sm ? sm : INFINITY));
+    const uint32_t j4 = av.joints[g];
+    for (int k = 0; k < 4; ++k) {
+        if (av.weights[4 * g + k] == 0.0) continue;
+        const int j = (j4 >> (8 * k)) & 0xff;
+        const double *ib = av.inv_bind + ((int64_t)a * J + j) * 16;
+        const double x = ((ib[0] * p[0] + ib[1] * p[1]) + ib[2] * p[2]) + ib[3];
+        const double y = ((ib[4] * p[0] + ib[5] * p[1]) + ib[6] * p[2]) + ib[7];
+        const double z = ((ib[8] * p[0] + ib[9] * p[1]) + ib[10] * p[2]) + ib[11];
+        const double d = sqrt((x * x + y * y) + z * z);
+        atomicMax(e + 2 + j, (unsigned long long)__double_as_longlong(d == d ? d : INFINITY));
+    }
+}
+
+// Whole-avatar culling per (env, avatar), conservative and exact in its RenderStats category.
+// Skinned position p' = R_root b + t_root with b = (1 - sum w) P + sum_j w_j rigid_j(inv_bind_j P),
+// 0 <= w, |sum w - 1| <= 1e-3 (AvatarBundle validation): rigid_j(inv_bind_j P) lies within d_j of
+// the joint's sampled translation t_j, so b lies within rho = max_j (|t_j - c| + d_j) + 1e-3 |P|max of
+// any centre c (c = centre of the joints' bounding box), and p' within rho of R_root c + t_root.
+// Code kCullDepth: the whole ball is at z <= near or z >= far (projection.py:128-135). Code
+// kCullFrame: the ball is strictly inside (near, far), every covariance is finite (so det > 1e-12:
+// cov2d >= 0.3 I), and even with the largest projected radius 3 sqrt(||J||_F^2 s_max^2 + 0.3)
+// (>= 3 sqrt(lambda_max)) every mean misses the frame on one side (projection.py:160-166).
+// 0: test every gaussian.
+__global__ void avatar_cull_kernel(sn_avatars av, PoseView pv, const double *pose_t, const sn_camera *cams,
+                                   const unsigned long long *ext, int n_envs, uint8_t *codes) {
+    const int ea = blockIdx.x * blockDim.x + threadIdx.x;
+    const int A = av.n_avatars, J = av.n_joints;
+    if (ea >= n_envs * A) return;
+    const int env = ea / A, a = ea % A;
+    const unsigned long long *e = ext + (int64_t)a * (2 + J);
+    const double pmax = __longlong_as_double((long long)e[0]);
+    const double smax = __longlong_as_double((long long)e[1]);
+    const double *tj = pose_t + (int64_t)ea * (J + 1) * 3, *root = pv.root + (int64_t)ea * 12;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int j = 0; j < J; ++j)
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = fmin(lo[k], tj[3 * j + k]);
+            hi[k] = fmax(hi[k], tj[3 * j + k]);
+        }
+    const double cb[3] = {0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2])};
+    double rb = 0.0;
+    for (int j = 0; j < J; ++j) {
+        const double dx = tj[3 * j] - cb[0], dy = tj[3 * j + 1] - cb[1], dz = tj[3 * j + 2] - cb[2];
+        rb = fmax(rb, sqrt((dx * dx + dy * dy) + dz * dz) + __longlong_as_double((long long)e[2 + j]));
+    }
+    uint8_t code = 0;
+    const double rho = (rb + 1e-3 * pmax) * (1.0 + 1e-9) + 1e-9;
+    if (rho < 1e30) {
+        // ball centre in the world: R_root cb + t_root
+        const double px = ((root[0] * cb[0] + root[1] * cb[1]) + root[2] * cb[2]) + root[9];
+        const double py = ((root[3] * cb[0] + root[4] * cb[1]) + root[5] * cb[2]) + root[10];
+        const double pz = ((root[6] * cb[0] + root[7] * cb[1]) + root[8] * cb[2]) + root[11];
+        const sn_camera &c = cams[env];
+        const double *w = c.rot;
+        const double xc = ((w[0] * px + w[1] * py) + w[2] * pz) + c.trans[0];
+        const double yc = ((w[3] * px + w[4] * py) + w[5] * pz) + c.trans[1];
+        const double zc = ((w[6] * px + w[7] * py) + w[8] * pz) + c.trans[2];
+        const double tol = 1e-9 * (1.0 + fabs(zc) + rho);
+        if (zc + rho < c.near_ - tol || zc - rho > c.far_ + tol) {
+            code = kCullDepth;
+        } else if (zc - rho > c.near_ + tol && zc + rho < c.far_ - tol && smax < 1e30) {
+            const double zl = zc - rho, zh = zc + rho;
+            const double xl = xc - rho, xh = xc + rho, yl = yc - rho, yh = yc + rho;
+            const double ax = fmax(fabs(xl), fabs(xh)), ay = fmax(fabs(yl), fabs(yh));
+            const double jf2 = (c.fx * c.fx + c.fy * c.fy) / (zl * zl) +
+                               (c.fx * c.fx * ax * ax + c.fy * c.fy * ay * ay) / (zl * zl * zl * zl);
+            const double r = 3.0 * sqrt(jf2 * smax * smax + 0.3) * (1.0 + 1e-9) + 1e-6;
+            const double mx_hi = (xh >= 0.0 ? c.fx * xh / zl : c.fx * xh / zh) + c.cx;
+            const double mx_lo = (xl <= 0.0 ? c.fx * xl / zl : c.fx * xl / zh) + c.cx;
+            const double my_hi = (yh >= 0.0 ? c.fy * yh / zl : c.fy * yh / zh) + c.cy;
+            const double my_lo = (yl <= 0.0 ? c.fy * yl / zl : c.fy * yl / zh) + c.cy;
+            const double mw = 1e-6 * (1.0 + fabs(mx_hi) + fabs(mx_lo) + fabs(my_hi) + fabs(my_lo));
+            if (mx_hi + r < -mw || mx_lo - r > (double)c.width + mw || my_hi + r < -mw ||
+                my_lo - r > (double)c.height + mw)
+                code = kCullFrame;
+        }
+    }
+    codes[ea] = code;
+}
+
 }  // namespace
 
 cudaError_t launch_pose(const sn_avatars &av, const double *sim_times, int32_t n_envs, double *pose_q, double *pose_t,
@@ -187,6 +282,15 @@ cudaError_t launch_pose(const sn_avatars &av, const double *sim_times, int32_t n
     int threads = ((av.n_joints + 1 + 31) / 32) * 32;
     pose_kernel<<<n_envs * av.n_avatars, threads, 0, s>>>(av, sim_times, pose_q, pose_t, joint_mats, eff_q, root,
                                                            err_flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_avatar_cull(const sn_avatars &av, const PoseView &pv, const double *pose_t, const sn_camera *cams,
+                               int32_t n_envs, unsigned long long *ext, uint8_t *codes, cudaStream_t s) {
+    cudaMemsetAsync(ext, 0, sizeof(unsigned long long) * (2 + av.n_joints) * av.n_avatars, s);
+    if (av.n > 0) avatar_extent_kernel<<<(unsigned)((av.n + 255) / 256), 256, 0, s>>>(av, ext);
+    const int n = n_envs * av.n_avatars;
+    avatar_cull_kernel<<<(n + 127) / 128, 128, 0, s>>>(av, pv, pose_t, cams, ext, n_envs, codes);
     return cudaGetLastError();
 }
 

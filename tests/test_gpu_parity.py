@@ -468,7 +468,8 @@ def test_env_chunking_with_avatar_layer():
     cams = S.room_cameras(70, box, seed=73, width=48, height=40)
     times = np.linspace(0.0, 0.35, 70)
     br = BatchRenderer(scene, bundles, start_offsets=[0.0, 0.05], loops=[1, 1], background=(0.3, 0.3, 0.3))
-    out = br.render(cams, times, contrib=True)
+    out = br.render(cams, times, contrib=True, stats=True)
+    keys = ("n_input", "n_culled_depth", "n_culled_frame", "n_degenerate", "n_drawn")
     for e in (0, 31, 63, 64, 69):
         clouds = [rig.AvatarRuntime(b, start_offset=[0.0, 0.05][a], loop=True).deformed_cloud(float(times[e]))
                   for a, b in enumerate(bundles)]
@@ -477,6 +478,9 @@ def test_env_chunking_with_avatar_layer():
                     o.color, o.alpha, o.depth, cams[e].far)
         lo = O.rasterize(concat_clouds(clouds), cams[e], None)
         np.testing.assert_array_equal(out["contrib_layer"][e].cpu().numpy(), lo.contrib)
+        # RenderStats over both passes (the whole-avatar culls are counted in their categories)
+        so = O.rasterize(scene, cams[e], np.array([0.3, 0.3, 0.3]))
+        assert out["stats"][e].tolist() == [so.stats[k] + lo.stats[k] for k in keys]
 
 
 def test_degenerate_and_extreme_splats():
