@@ -184,27 +184,45 @@ __global__ void joint_prep_kernel(sn_avatars av, int avatar, const double *pose_
 // exp(max log-scale); per (avatar, joint): d_j = the largest |inv_bind_j P| over the gaussians the
 // joint influences -- the inputs of the (env, avatar) culling bound below.
 // ext layout per avatar: [0] |P|max, [1] s_max, [2 .. 2 + J) d_j (non-negative doubles as bits)
-__global__ void avatar_extent_kernel(sn_avatars av, unsigned long long *ext) {
-    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= av.n) return;
-    const int a = av.avatar_of[g], J = av.n_joints;
-    unsigned long long *e = ext + (int64_t)a * (2 + J);
-    const double *p = av.pos_opacity + 4 * g, *l = av.log_scales + 4 * g;
-    const double r = sqrt((p[0] * p[0] + p[1] * p[1]) + p[2] * p[2]);
-    const double sm = exp(fmax(fmax(l[0], l[1]), l[2]));
-    // non-negative doubles order like their bit patterns; NaN/inf poison the bound (no culling)
-    atomicMax(e, (unsigned long long)__double_as_longlong(r == r ? r : INFINITY));
-    atomicMax(e + 1, (unsigned long long)__double_as_longlong(sm == sm ? sm : INFINITY));
-    const uint32_t j4 = av.joints[g];
-    for (int k = 0; k < 4; ++k) {
-        if (av.weights[4 * g + k] == 0.0) continue;
-        const int j = (j4 >> (8 * k)) & 0xff;
-        const double *ib = av.inv_bind + ((int64_t)a * J + j) * 16;
-        const double x = ((ib[0] * p[0] + ib[1] * p[1]) + ib[2] * p[2]) + ib[3];
-        const double y = ((ib[4] * p[0] + ib[5] * p[1]) + ib[6] * p[2]) + ib[7];
-        const double z = ((ib[8] * p[0] + ib[9] * p[1]) + ib[10] * p[2]) + ib[11];
-        const double d = sqrt((x * x + y * y) + z * z);
-        atomicMax(e + 2 + j, (unsigned long long)__double_as_longlong(d == d ? d : INFINITY));
+__global__ void __launch_bounds__(256) avatar_extent_kernel(sn_avatars av, unsigned long long *ext) {
+    // a block's 256 gaussians belong to at most two avatars (contiguous ranges): reduce the maxima
+    // in shared memory, then one global atomic per slot and block
+    extern __shared__ unsigned long long s_ext[];  // 2 x (2 + J)
+    const int J = av.n_joints, slots = 2 + J;
+    for (int i = threadIdx.x; i < 2 * slots; i += blockDim.x) s_ext[i] = 0ull;
+    __syncthreads();
+    const int64_t g0 = (int64_t)blockIdx.x * blockDim.x;
+    const int64_t g = g0 + threadIdx.x;
+    const int a_lo = av.avatar_of[g0];
+    if (g < av.n) {
+        const int a = av.avatar_of[g];
+        unsigned long long *e = s_ext + (a == a_lo ? 0 : slots);
+        const double *p = av.pos_opacity + 4 * g, *l = av.log_scales + 4 * g;
+        const double r = sqrt((p[0] * p[0] + p[1] * p[1]) + p[2] * p[2]);
+        const double sm = exp(fmax(fmax(l[0], l[1]), l[2]));
+        // non-negative doubles order like their bit patterns; NaN/inf poison the bound (no culling)
+        atomicMax(e, (unsigned long long)__double_as_longlong(r == r ? r : INFINITY));
+        atomicMax(e + 1, (unsigned long long)__double_as_longlong(sm == sm ? sm : INFINITY));
+        const uint32_t j4 = av.joints[g];
+        for (int k = 0; k < 4; ++k) {
+            if (av.weights[4 * g + k] == 0.0) continue;
+            const int j = (j4 >> (8 * k)) & 0xff;
+            const double *ib = av.inv_bind + ((int64_t)a * J + j) * 16;
+            const double x = ((ib[0] * p[0] + ib[1] * p[1]) + ib[2] * p[2]) + ib[3];
+            const double y = ((ib[4] * p[0] + ib[5] * p[1]) + ib[6] * p[2]) + ib[7];
+            const double z = ((ib[8] * p[0] + ib[9] * p[1]) + ib[10] * p[2]) + ib[11];
+            const double d = sqrt((x * x + y * y) + z * z);
+            atomicMax(e + 2 + j, (unsigned long long)__double_as_longlong(d == d ? d : INFINITY));
+        }
+    }
+    __syncthreads();
+    const int64_t g_last = min(av.n, g0 + (int64_t)blockDim.x) - 1;
+    const int a_hi = av.avatar_of[g_last];
+    for (int i = threadIdx.x; i < 2 * slots; i += blockDim.x) {
+        const int which = i / slots, slot = i % slots;
+        const int a = which ? a_hi : a_lo;
+        if (which && a_hi == a_lo) continue;
+        if (s_ext[i]) atomicMax(ext + (int64_t)a * slots + slot, s_ext[i]);
     }
 }
 
@@ -288,7 +306,9 @@ cudaError_t launch_pose(const sn_avatars &av, const double *sim_times, int32_t n
 cudaError_t launch_avatar_cull(const sn_avatars &av, const PoseView &pv, const double *pose_t, const sn_camera *cams,
                                int32_t n_envs, unsigned long long *ext, uint8_t *codes, cudaStream_t s) {
     cudaMemsetAsync(ext, 0, sizeof(unsigned long long) * (2 + av.n_joints) * av.n_avatars, s);
-    if (av.n > 0) avatar_extent_kernel<<<(unsigned)((av.n + 255) / 256), 256, 0, s>>>(av, ext);
+    if (av.n > 0)
+        avatar_extent_kernel<<<(unsigned)((av.n + 255) / 256), 256, sizeof(unsigned long long) * 2 * (2 + av.n_joints),
+                               s>>>(av, ext);
     const int n = n_envs * av.n_avatars;
     avatar_cull_kernel<<<(n + 127) / 128, 128, 0, s>>>(av, pv, pose_t, cams, ext, n_envs, codes);
     return cudaGetLastError();
