@@ -905,7 +905,13 @@ __global__ void __launch_bounds__(256) fixup_layer_kernel(BlendArgs b) {
 // and writes the same outputs the float64 blend epilogue writes. Mode 2 also recomputes the scene
 // pixel (the back layer) so the composite's comparisons see float64 depths.
 template <int MODE>
-__global__ void __launch_bounds__(256) fixup_kernel(BlendArgs b) {
+#ifndef SN_FIXUP_MIN_BLOCKS
+#define SN_FIXUP_MIN_BLOCKS 4
+#endif
+#ifndef SN_FIXUP_PER
+#define SN_FIXUP_PER 2
+#endif
+__global__ void __launch_bounds__(256, SN_FIXUP_MIN_BLOCKS) fixup_kernel(BlendArgs b) {
     __shared__ double s_exp[64];
     __shared__ QEntry s_q[8][kQueue];
     if (threadIdx.x < 64) s_exp[threadIdx.x] = kExp2Tbl[threadIdx.x];
@@ -924,7 +930,7 @@ __global__ void __launch_bounds__(256) fixup_kernel(BlendArgs b) {
         const int tile = (py_i / kTile) * b.tiles_x + px_i / kTile;
         const sn_camera &cam = b.cams[env];
         // mode 2 fixups are few and each walks long, unsaturated lists: more gathers in flight
-        const ExactPixel f = exact_walk<MODE == 2 ? 8 : 4>(b.pv, el, tile, b.tiles_x, px_i, py_i, s_exp, q);
+        const ExactPixel f = exact_walk<MODE == 2 ? 8 : SN_FIXUP_PER>(b.pv, el, tile, b.tiles_x, px_i, py_i, s_exp, q);
         contribs += (unsigned)f.nc;
         const int64_t pix = ((int64_t)env * b.height + py_i) * b.width + px_i;
         const double alpha = f.A < 1.0 ? f.A : 1.0;
