@@ -98,8 +98,8 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // directions, eigenvalues, the decision thresholds 9 -/+ E(9.1), alpha, z, the alpha error bound
 // coefficients, colour.
 struct __align__(16) FRec {
-    float U1, U2, e1x, e1y;
-    float l1, l2, thr_out, thr_in;
+    float a1x, a1y, V1, c2x;  // v1 = sqrt(l1) u1 = a1.o + V1, v2 = sqrt(l2) u2 = c2.o + V2, d2 = v1^2 + v2^2
+    float c2y, V2, thr_out, thr_in;
     float alpha, z, ka, kb;  // alpha's relative error bound: eps(d2) = ka d2 + kb
     float r, g, b, pad;
 };
@@ -137,12 +137,15 @@ __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1
     const double U1 = fma(e1x, cx, fma(e1y, cy, -p1));
     const double U2 = fma(-e1y, cx, fma(e1x, cy, -p2));
     const float l1 = gl.x, l2 = gl.y;
-    f.U1 = (float)U1;
-    f.U2 = (float)U2;
-    f.e1x = (float)e1x;
-    f.e1y = (float)e1y;
-    f.l1 = l1;
-    f.l2 = l2;
+    // the axes pre-scaled by sqrt(l_k) (float64 products, rounded once): d2 = v1^2 + v2^2
+    const double sl1 = sqrt((double)l1), sl2 = sqrt((double)fmaxf(l2, 0.0f));
+    f.a1x = (float)(sl1 * e1x);
+    f.a1y = (float)(sl1 * e1y);
+    f.V1 = (float)(sl1 * U1);
+    f.c2x = (float)(-sl2 * e1y);
+    f.c2y = (float)(sl2 * e1x);
+    f.V2 = (float)(sl2 * U2);
+    const float fU1 = (float)U1, fU2 = (float)U2, fe1x = (float)e1x, fe1y = (float)e1y;
     f.alpha = gl.z;
     f.z = gl.w;
     float rgb[3];
@@ -152,7 +155,7 @@ __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1
     f.b = rgb[2];
     f.pad = 0.0f;
     const float u = 5.9604644775390625e-08f;  // 2^-24
-    const float aU1 = fabsf(f.U1), aU2 = fabsf(f.U2);
+    const float aU1 = fabsf(fU1), aU2 = fabsf(fU2);
     bool ok = l2 > 0.0f;
     if (ok) {
         const float r1 = rsqrtf(l1), r2 = rsqrtf(l2);
@@ -173,24 +176,24 @@ __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1
         f.kb = kEpsExact;
     }
     // mean - tile origin, from the principal-axis offsets (float error ~ 2u (|U1| + |U2|))
-    const float mx = 8.0f - (f.U1 * f.e1x - f.U2 * f.e1y), my = 8.0f - (f.U1 * f.e1y + f.U2 * f.e1x);
+    const float mx = 8.0f - (fU1 * fe1x - fU2 * fe1y), my = 8.0f - (fU1 * fe1y + fU2 * fe1x);
     const float slack = 1e-3f + 4.0f * u * (aU1 + aU2);
     unsigned m = warp_block_mask(mx, my, gr.z * 1.00001f + slack, gr.w * 1.00001f + slack);
     if (ok && m) {
         // Separating axes along the ellipse's own axes (the support's oriented bounding box,
         // |u_k| <= 3 / sqrt(l_k), against each 8 x 4 block of pixel centres projected on e_k):
         // rotated, elongated splats whose axis-aligned box reaches a block often miss it.
-        const float ax = fabsf(f.e1x), ay = fabsf(f.e1y);
+        const float ax = fabsf(fe1x), ay = fabsf(fe1y);
         const float marg = 1e-3f + 8.0f * u * (aU1 + aU2 + 16.0f);
         const float ext1 = 3.0f * rsqrtf(l1) * 1.00001f + marg + (3.5f * ax + 1.5f * ay);
         const float ext2 = 3.0f * rsqrtf(l2) * 1.00001f + marg + (3.5f * ay + 1.5f * ax);
         // u_k at the block centres (8 bx - 4, 4 by - 6) relative to the tile centre
-        const float u1b = f.U1 - 4.0f * f.e1x - 6.0f * f.e1y, u2b = f.U2 + 4.0f * f.e1y - 6.0f * f.e1x;
+        const float u1b = fU1 - 4.0f * fe1x - 6.0f * fe1y, u2b = fU2 + 4.0f * fe1y - 6.0f * fe1x;
 #pragma unroll
         for (int w = 0; w < 8; ++w) {
             const float bx = (float)(w & 1), by = (float)(w >> 1);
-            const float u1c = u1b + 8.0f * bx * f.e1x + 4.0f * by * f.e1y;
-            const float u2c = u2b - 8.0f * bx * f.e1y + 4.0f * by * f.e1x;
+            const float u1c = u1b + 8.0f * bx * fe1x + 4.0f * by * fe1y;
+            const float u2c = u2b - 8.0f * bx * fe1y + 4.0f * by * fe1x;
             if (fabsf(u1c) > ext1 || fabsf(u2c) > ext2) m &= ~(1u << w);
         }
     }
@@ -271,6 +274,7 @@ __global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(Blen
     float eps_max = 0.0f, z_first = 3.0e38f, z_last = 0.0f;
     int nc = 0;
     bool done = !inside || b.force_exact, amb = inside && b.force_exact;
+    float dead = done ? INFINITY : 0.0f;  // added to d2: a finished pixel skips every splat
     uint32_t loaded = 0, scanned = 0;
     int q_len = 0;  // SOURCE 0: entries waiting in s_queue (uniform across the CTA)
     while (true) {
@@ -345,10 +349,10 @@ __global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(Blen
                 const int j = s_wl[warp][k];
                 PROF(0, lane == 0);
                 const FRec &s = s_f[j];
-                const float u1 = __fmaf_rn(s.e1x, oxf, __fmaf_rn(s.e1y, oyf, s.U1));
-                const float u2 = __fmaf_rn(s.e1x, oyf, __fmaf_rn(-s.e1y, oxf, s.U2));
-                float d2 = __fmaf_rn(s.l1 * u1, u1, (s.l2 * u2) * u2);
-                if (done | (d2 > s.thr_out)) continue;  // saturated, or certainly outside the support
+                const float v1 = __fmaf_rn(s.a1x, oxf, __fmaf_rn(s.a1y, oyf, s.V1));
+                const float v2 = __fmaf_rn(s.c2x, oxf, __fmaf_rn(s.c2y, oyf, s.V2));
+                float d2 = __fmaf_rn(v1, v1, v2 * v2);
+                if (d2 + dead > s.thr_out) continue;  // saturated (dead = inf), or certainly outside the support
                 float eps;
                 if (d2 < s.thr_in) {
                     eps = __fmaf_rn(d2, s.ka, s.kb);
@@ -381,6 +385,7 @@ __global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(Blen
                 }
                 if (Tn - err <= kTHi) {  // near the cutoff (_kernels_cy.pyx:65-66): decide or defer
                     done = true;
+                    dead = INFINITY;
                     amb = !(Tn + err < kTLo);
                     PROF(2, amb);
                 }
