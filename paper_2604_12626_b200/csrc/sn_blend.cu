@@ -94,14 +94,31 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
-// Shared-memory form of a gathered splat for the float32 chain (64 B): principal-axis offsets and
-// directions, eigenvalues, the decision thresholds 9 -/+ E(9.1), alpha, z, the alpha error bound
-// coefficients, colour.
+// Packed float32 pairs (sm_100 FFMA2: two IEEE fmas per issue slot, each rounded exactly like
+// __fmaf_rn; a scalar operand is broadcast to both halves without a move).
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pack2(float lo, float hi) {
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void unpack2(f32x2 v, float &lo, float &hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+    f32x2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+// Shared-memory form of a gathered splat for the float32 chain (64 B): the principal-axis rows as
+// (axis 1, axis 2) pairs, the decision thresholds 9 -/+ E(9.1), alpha, the alpha error bound
+// coefficients, colour and z (paired for the FFMA2 accumulation).
 struct __align__(16) FRec {
-    float a1x, a1y, V1, c2x;  // v1 = sqrt(l1) u1 = a1.o + V1, v2 = sqrt(l2) u2 = c2.o + V2, d2 = v1^2 + v2^2
-    float c2y, V2, thr_out, thr_in;
-    float alpha, z, ka, kb;  // alpha's relative error bound: eps(d2) = ka d2 + kb
-    float r, g, b, pad;
+    float a1x, c2x, a1y, c2y;  // (v1, v2) = (a1x, c2x) ox + (a1y, c2y) oy + (V1, V2), d2 = v1^2 + v2^2,
+    float V1, V2, thr_out, thr_in;  // v_k = sqrt(l_k) u_k
+    float ka, kb, alpha, pad;  // alpha's relative error bound: eps(d2) = ka d2 + kb
+    float r, g, b, z;
 };
 
 // Which of the CTA's eight 8 x 4 warp blocks the splat's support {d2 <= 9} can reach: (mx, my) is
@@ -269,16 +286,19 @@ __global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(Blen
         s1 = (uint32_t)v.env_off[el + 1];
     }
 
-    float T = 1.0f, A = 0.0f, D = 0.0f, err = 0.0f;
-    float cr = 0.0f, cg = 0.0f, cb = 0.0f;
+    float T = 1.0f, A = 0.0f, err = 0.0f;
+    f32x2 crg = 0ull, cbd = 0ull;  // (colour r, g), (colour b, depth sum)
+    const f32x2 o2x = pack2(oxf, oxf), o2y = pack2(oyf, oyf);
     float eps_max = 0.0f, z_first = 3.0e38f, z_last = 0.0f;
     int nc = 0;
-    bool done = !inside || b.force_exact, amb = inside && b.force_exact;
-    float dead = done ? INFINITY : 0.0f;  // added to d2: a finished pixel skips every splat
+    // added to d2: a finished pixel skips every splat. A pixel is finished when it is outside the
+    // frame, forced exact, or past the cutoff test (after which T and err never change, so the
+    // cutoff's ambiguity is re-derived from them after the walk)
+    float dead = (!inside || b.force_exact) ? INFINITY : 0.0f;
     uint32_t loaded = 0, scanned = 0;
     int q_len = 0;  // SOURCE 0: entries waiting in s_queue (uniform across the CTA)
     while (true) {
-        if (__syncthreads_count(!done) == 0) break;  // also guards s_f / s_queue reuse
+        if (__syncthreads_count(dead == 0.0f) == 0) break;  // also guards s_f / s_queue reuse
         int n;
         if (SOURCE == 0) {
             while (q_len < kBlock && cursor < s1) {
@@ -342,19 +362,21 @@ __global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(Blen
             cnt += __popc(bal);
         }
         __syncwarp();
-        for (int k0 = 0; k0 < cnt && !__all_sync(kFull, done); k0 += 32) {
+        for (int k0 = 0; k0 < cnt && !__all_sync(kFull, dead != 0.0f); k0 += 32) {
             const int k1 = min(cnt, k0 + 32);
 #pragma unroll 2
             for (int k = k0; k < k1; ++k) {
                 const int j = s_wl[warp][k];
                 PROF(0, lane == 0);
                 const FRec &s = s_f[j];
-                const float v1 = __fmaf_rn(s.a1x, oxf, __fmaf_rn(s.a1y, oyf, s.V1));
-                const float v2 = __fmaf_rn(s.c2x, oxf, __fmaf_rn(s.c2y, oyf, s.V2));
+                const float4 q0 = *reinterpret_cast<const float4 *>(&s.a1x);
+                const float4 q1 = *reinterpret_cast<const float4 *>(&s.V1);
+                float v1, v2;
+                unpack2(fma2(pack2(q0.x, q0.y), o2x, fma2(pack2(q0.z, q0.w), o2y, pack2(q1.x, q1.y))), v1, v2);
                 float d2 = __fmaf_rn(v1, v1, v2 * v2);
-                if (d2 + dead > s.thr_out) continue;  // saturated (dead = inf), or certainly outside the support
+                if (d2 + dead > q1.z) continue;  // saturated (dead = inf), or certainly outside the support
                 float eps;
-                if (d2 < s.thr_in) {
+                if (d2 < q1.w) {
                     eps = __fmaf_rn(d2, s.ka, s.kb);
                 } else {  // boundary band: the reference's float64 test (_kernels_cy.pyx:73-75)
                     PROF(1, 1);
@@ -368,11 +390,10 @@ __global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(Blen
                 const float e = ex2_approx(d2 * kNegHalfLog2e);
                 const float a = fminf(s.alpha * e, 0.99f);
                 const float w = a * T;
-                cr = __fmaf_rn(s.r, w, cr);
-                cg = __fmaf_rn(s.g, w, cg);
-                cb = __fmaf_rn(s.b, w, cb);
+                const float4 q3 = *reinterpret_cast<const float4 *>(&s.r);
+                crg = fma2(pack2(q3.x, q3.y), pack2(w, w), crg);
+                cbd = fma2(pack2(q3.z, q3.w), pack2(w, w), cbd);
                 A = A + w;
-                D = __fmaf_rn(s.z, w, D);
                 const float om = 1.0f - a;
                 const float Tn = T * om;
                 err = __fmaf_rn(err, om, __fmaf_rn(w, eps, Tn * kU25));
@@ -380,15 +401,11 @@ __global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(Blen
                 ++nc;
                 if (kBound) {  // splats arrive in depth order: z spans [first, last] contribution
                     eps_max = fmaxf(eps_max, eps);
-                    z_first = fminf(z_first, s.z);
-                    z_last = s.z;
+                    z_first = fminf(z_first, q3.w);
+                    z_last = q3.w;
                 }
-                if (Tn - err <= kTHi) {  // near the cutoff (_kernels_cy.pyx:65-66): decide or defer
-                    done = true;
-                    dead = INFINITY;
-                    amb = !(Tn + err < kTLo);
-                    PROF(2, amb);
-                }
+                // near the cutoff (_kernels_cy.pyx:65-66): stop; decided or deferred after the walk
+                if (Tn - err <= kTHi) dead = INFINITY;
             }
         }
         if (SOURCE == 0) {  // drop the consumed head of the queue
@@ -401,6 +418,12 @@ __global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(Blen
             cursor += n;
         }
     }
+    float cr, cg, cb, D;
+    unpack2(crg, cr, cg);
+    unpack2(cbd, cb, D);
+    // the cutoff fired (T - err <= 1e-4 (1 + 1e-6)) but T < 1e-4 is not certain: float64 fixup
+    const bool amb = inside && (b.force_exact || (T - err <= kTHi && !(T + err < kTLo)));
+    PROF(2, amb);
 #ifdef SN_BLEND_PROF
     for (int i = 0; i < 16; ++i)
         if (prof[i]) atomicAdd(&g_blend_prof[i], prof[i]);
