@@ -110,6 +110,11 @@ __device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
     return r;
 }
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
 
 // Shared-memory form of a gathered splat for the float32 chain (64 B): the principal-axis rows as
 // (axis 1, axis 2) pairs, the decision thresholds 9 -/+ E(9.1), alpha, the alpha error bound
@@ -373,8 +378,9 @@ __global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(Blen
                 const float4 q1 = *reinterpret_cast<const float4 *>(&s.V1);
                 float v1, v2;
                 unpack2(fma2(pack2(q0.x, q0.y), o2x, fma2(pack2(q0.z, q0.w), o2y, pack2(q1.x, q1.y))), v1, v2);
-                float d2 = __fmaf_rn(v1, v1, v2 * v2);
-                if (d2 + dead > q1.z) continue;  // saturated (dead = inf), or certainly outside the support
+                // + dead: exact (v2^2 + 0 rounds like v2 * v2), or +inf for a finished pixel
+                float d2 = __fmaf_rn(v1, v1, __fmaf_rn(v2, v2, dead));
+                if (d2 > q1.z) continue;  // saturated (dead = inf), or certainly outside the support
                 float eps;
                 if (d2 < q1.w) {
                     eps = __fmaf_rn(d2, s.ka, s.kb);
@@ -389,13 +395,13 @@ __global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(Blen
                 }
                 const float e = ex2_approx(d2 * kNegHalfLog2e);
                 const float a = fminf(s.alpha * e, 0.99f);
-                const float w = a * T;
+                const float om = 1.0f - a;
+                float w, Tn;  // a T, (1 - a) T
+                unpack2(mul2(pack2(a, om), pack2(T, T)), w, Tn);
                 const float4 q3 = *reinterpret_cast<const float4 *>(&s.r);
                 crg = fma2(pack2(q3.x, q3.y), pack2(w, w), crg);
                 cbd = fma2(pack2(q3.z, q3.w), pack2(w, w), cbd);
                 A = A + w;
-                const float om = 1.0f - a;
-                const float Tn = T * om;
                 err = __fmaf_rn(err, om, __fmaf_rn(w, eps, Tn * kU25));
                 T = Tn;
                 ++nc;
