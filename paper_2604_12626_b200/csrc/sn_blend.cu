@@ -17,7 +17,8 @@
 //     |d2_f - 9| <= E9 recompute d2 exactly in float64 (rare).
 //   * alpha = min(.99, o e^(-d2/2)): relative error eps = E9 / 2 + kEpsExp (ex2.approx, argument
 //     and product roundings; the ex2 bound is verified by sn_selftest_fast_exp).
-//   * T < 1e-4: the absolute error of T is tracked per pixel, err' = err (1 - a) + w eps + 2.5 u T'.
+//   * T < 1e-4: T' = fma(-a, T, T) (one rounding) and its absolute error is tracked per pixel,
+//     err' = err (1 - a) + w eps + 1.25 u T'.
 //     When T is within err of 1e-4 the pixel is "ambiguous": it is appended to a fixup list and
 //     recomputed by fixup_kernel, a warp-per-pixel float64 walk with the reference's operation
 //     order (the previous, fully float64 blend), which also writes its outputs.
@@ -83,7 +84,7 @@ __constant__ double kExp2Tbl[64] = {
 // sn_selftest_fast_exp; the GPU test asserts <= 3.5e-7) + the roundings of alpha and alpha * e
 constexpr float kEpsExp = 5.0e-7f;
 constexpr float kEpsExact = 8.0e-7f;   // same, when d2 came from float64 (rounded to float: 4.5 u)
-constexpr float kU25 = 1.5e-7f;        // 2.5 u: roundings of 1 - a and T (1 - a)
+constexpr float kU125 = 7.5e-8f;       // 1.25 u: the one rounding of T' = fma(-a, T, T) (+ the err sums')
 constexpr float kTLo = 9.99999e-05f;   // 1e-4 (1 - 1e-6): below it (with the bound) T < 1e-4 for sure
 constexpr float kTHi = 1.000001e-04f;  // 1e-4 (1 + 1e-6)
 constexpr float kNegHalfLog2e = -0.72134752044448170f;
@@ -395,14 +396,13 @@ __global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(Blen
                 }
                 const float e = ex2_approx(d2 * kNegHalfLog2e);
                 const float a = fminf(s.alpha * e, 0.99f);
-                const float om = 1.0f - a;
-                float w, Tn;  // a T, (1 - a) T
-                unpack2(mul2(pack2(a, om), pack2(T, T)), w, Tn);
+                const float w = a * T;
+                const float Tn = __fmaf_rn(-a, T, T);  // T (1 - a), rounded once
                 const float4 q3 = *reinterpret_cast<const float4 *>(&s.r);
                 crg = fma2(pack2(q3.x, q3.y), pack2(w, w), crg);
                 cbd = fma2(pack2(q3.z, q3.w), pack2(w, w), cbd);
                 A = A + w;
-                err = __fmaf_rn(err, om, __fmaf_rn(w, eps, Tn * kU25));
+                err = __fmaf_rn(-a, err, __fmaf_rn(w, eps, __fmaf_rn(Tn, kU125, err)));  // err (1 - a) + ...
                 T = Tn;
                 ++nc;
                 if (kBound) {  // splats arrive in depth order: z spans [first, last] contribution

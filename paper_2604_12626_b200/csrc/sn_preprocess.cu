@@ -21,6 +21,14 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// resident CTAs per SM the emit / avatar kernels are compiled for (register cap 65536 / (256 x N))
+#ifndef SN_EMIT_MIN_BLOCKS
+#define SN_EMIT_MIN_BLOCKS 4
+#endif
+#ifndef SN_AVATAR_MIN_BLOCKS
+#define SN_AVATAR_MIN_BLOCKS 3
+#endif
+
 template <typename T>
 __device__ __forceinline__ void load4(const T *p, double o[4]);
 template <>
@@ -236,7 +244,7 @@ __global__ void __launch_bounds__(kBlock) scene_count_kernel(sn_cloud c, PrepArg
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kBlock) scene_emit_kernel(sn_cloud c, PrepArgs a) {
+__global__ void __launch_bounds__(kBlock, SN_EMIT_MIN_BLOCKS) scene_emit_kernel(sn_cloud c, PrepArgs a) {
     __shared__ unsigned s_woff[kMaxEnvChunk][kBlock / 32];
     __shared__ double s_geo[kBlock][10];  // position (3), cov3d (6), alpha
     __shared__ uint16_t s_q[kBlock / 32][32 * kEmitRound];
@@ -385,7 +393,7 @@ __device__ __forceinline__ bool avatar_on(const PrepArgs &a, int n_avatars, int 
 // avatars fall back to global loads).
 __host__ __device__ __forceinline__ int pose_block_doubles(int J) { return 16 * J + 12; }
 
-__global__ void __launch_bounds__(kBlock) avatar_count_kernel(sn_avatars av, PoseView pv, PrepArgs a) {
+__global__ void __launch_bounds__(kBlock, SN_AVATAR_MIN_BLOCKS) avatar_count_kernel(sn_avatars av, PoseView pv, PrepArgs a) {
     __shared__ unsigned s_cnt[kMaxEnvChunk][5];
     extern __shared__ double s_pose[];  // 2 x (J*12 joint mats | J*4 quats | 12 root)
     init_counts(s_cnt, a.ec);
@@ -450,7 +458,7 @@ __global__ void __launch_bounds__(kBlock) avatar_count_kernel(sn_avatars av, Pos
     flush_counts(s_cnt, a);
 }
 
-__global__ void __launch_bounds__(kBlock) avatar_emit_kernel(sn_avatars av, PoseView pv, PrepArgs a) {
+__global__ void __launch_bounds__(kBlock, SN_AVATAR_MIN_BLOCKS) avatar_emit_kernel(sn_avatars av, PoseView pv, PrepArgs a) {
     __shared__ unsigned s_woff[kMaxEnvChunk][kBlock / 32];
     __shared__ uint16_t s_q[kBlock / 32][32 * kEmitRound];
     int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
