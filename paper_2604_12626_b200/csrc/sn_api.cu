@@ -300,7 +300,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     b.rects_out = w.rects.as<ushort4>();
     b.geo_out = w.geo_un.as<BlendGeo>();
     b.batch_rects = w.batch_rects.as<ushort4>();
-    b.tiles_touched = w.tiles.as<uint32_t>();
+    b.tiles_touched = binning == 1 ? w.tiles.as<uint32_t>() : nullptr;  // pair counts: tile lists only
     b.pair_off = w.pair_off.as<uint64_t>();
     b.ranges = w.ranges.as<uint2>();
 

@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(kBlock) permute_kernel(BinArgs b) {
         b.geo_out[i] = make_blend_geo(m.x, m.y, c01.x, c01.y, c2a.x, c2a.y, zr.x,
                                       (unsigned long long)__double_as_longlong(zr.y));
     }
-    b.tiles_touched[i] = (uint32_t)(r.y - r.x + 1) * (uint32_t)(r.w - r.z + 1);
+    if (b.tiles_touched) b.tiles_touched[i] = (uint32_t)(r.y - r.x + 1) * (uint32_t)(r.w - r.z + 1);
 }
 
 // Load-balanced pair emission: a CTA owns 256 consecutive depth-sorted splats and spreads
@@ -151,12 +151,9 @@ __device__ __forceinline__ bool z_less(const SplatRec *recs, uint32_t a, uint32_
     return za < zc || (za == zc && a < c);
 }
 
-__global__ void __launch_bounds__(kBlock) tie_fix_kernel(BinArgs b) {
-    const int64_t n_vis = n_vis_of(b);
-    int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    if (i >= n_vis) return;
+// Sorts the run of equal 32-bit keys starting at i by (exact z, index).
+__device__ __forceinline__ void tie_fix_run(const BinArgs &b, int64_t i, int64_t n_vis) {
     const uint32_t k = b.keys_sorted[i];
-    if (i > 0 && b.keys_sorted[i - 1] == k) return;  // not a run start
     int64_t e = i + 1;
     while (e < n_vis && b.keys_sorted[e] == k) ++e;
     const int64_t L = e - i;
@@ -193,6 +190,16 @@ __global__ void __launch_bounds__(kBlock) tie_fix_kernel(BinArgs b) {
         v[end] = t;
         sift(0, end);
     }
+}
+
+
+__global__ void __launch_bounds__(kBlock) tie_fix_kernel(BinArgs b) {
+    const int64_t n_vis = n_vis_of(b);
+    int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n_vis) return;
+    const uint32_t k = b.keys_sorted[i];
+    if (i > 0 && b.keys_sorted[i - 1] == k) return;  // not a run start
+    tie_fix_run(b, i, n_vis);
 }
 
 }  // namespace

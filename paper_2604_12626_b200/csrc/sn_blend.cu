@@ -111,11 +111,6 @@ __device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
     return r;
 }
-__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
-    f32x2 r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
 
 // Shared-memory form of a gathered splat for the float32 chain (64 B): the principal-axis rows as
 // (axis 1, axis 2) pairs, the decision thresholds 9 -/+ E(9.1), alpha, the alpha error bound

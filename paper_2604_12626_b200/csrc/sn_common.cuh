@@ -83,8 +83,11 @@ __device__ __forceinline__ BlendGeo make_blend_geo(double mx, double my, double 
     g.alpha = (float)alpha;
     g.z = (float)z;
     g.rgb = rgb;
-    g.hx = ok ? (float)(3.0 * sqrt(vx * vx / l1 + vy * vy / l2)) : 3.0e38f;
-    g.hy = ok ? (float)(3.0 * sqrt(vy * vy / l1 + vx * vx / l2)) : 3.0e38f;
+    // support half-extents in float (IEEE ops, relative error ~1e-7): the blend widens them by 1e-5
+    const float fx2 = (float)(vx * vx), fy2 = (float)(vy * vy);
+    const float il1 = __frcp_rn(g.l1), il2 = __frcp_rn(g.l2);
+    g.hx = ok ? 3.0f * __fsqrt_rn(__fmaf_rn(fx2, il1, fy2 * il2)) : 3.0e38f;
+    g.hy = ok ? 3.0f * __fsqrt_rn(__fmaf_rn(fy2, il1, fx2 * il2)) : 3.0e38f;
     return g;
 }
 
