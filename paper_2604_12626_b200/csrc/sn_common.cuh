@@ -220,9 +220,12 @@ __device__ __forceinline__ void tile_rect(double mx, double my, double r, int ti
 }
 
 // sh.py:20-49 in float32 (colour is tolerance-checked, not part of the decision chain).
-// sh: SoA (K*3, n) float32; dir: unit view direction.
-__device__ __forceinline__ void eval_sh_f32(const float *__restrict__ sh, int64_t n, int64_t g, int K, float x,
-                                            float y, float z, float rgb[3]) {
+// sh: SoA (K*3, n) float32; dir: unit view direction. K is a compile-time constant (1, 4, 9, 16) so
+// the basis stays in registers; coefficient rows are walked with a 32-bit element offset (one
+// IMAD.WIDE per load) while 3 K n < 2^32, else with 64-bit indices.
+template <int K>
+__device__ __forceinline__ void eval_sh_k(const float *__restrict__ sh, int64_t n, int64_t g, float x, float y,
+                                          float z, float rgb[3]) {
     const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
     float basis[16];
     basis[0] = C0;
@@ -248,11 +251,35 @@ __device__ __forceinline__ void eval_sh_f32(const float *__restrict__ sh, int64_
             basis[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
         }
     }
+    float acc[3] = {0.0f, 0.0f, 0.0f};
+    if ((uint64_t)(3 * K) * (uint64_t)n < (1ull << 32)) {
+        const uint32_t un = (uint32_t)n;
+        uint32_t off = (uint32_t)g;
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-        float acc = 0.0f;
-        for (int k = 0; k < K; ++k) acc = __fmaf_rn(basis[k], __ldg(sh + (int64_t)(3 * k + ch) * n + g), acc);
-        rgb[ch] = np_clipf(acc + 0.5f, 0.0f, 1.0f);
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+                acc[ch] = __fmaf_rn(basis[k], __ldg(sh + off), acc[ch]);
+                off += un;
+            }
+    } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch)
+                acc[ch] = __fmaf_rn(basis[k], __ldg(sh + (int64_t)(3 * k + ch) * n + g), acc[ch]);
+    }
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) rgb[ch] = np_clipf(acc[ch] + 0.5f, 0.0f, 1.0f);
+}
+
+__device__ __forceinline__ void eval_sh_f32(const float *__restrict__ sh, int64_t n, int64_t g, int K, float x,
+                                            float y, float z, float rgb[3]) {
+    switch (K) {
+        case 16: eval_sh_k<16>(sh, n, g, x, y, z, rgb); break;
+        case 9: eval_sh_k<9>(sh, n, g, x, y, z, rgb); break;
+        case 4: eval_sh_k<4>(sh, n, g, x, y, z, rgb); break;
+        default: eval_sh_k<1>(sh, n, g, x, y, z, rgb); break;
     }
 }
 
