@@ -49,7 +49,10 @@ __device__ __forceinline__ ushort4 warp_rect_union(ushort4 r) {
 // Writes each depth-sorted splat's tile rectangle and tile count and, per 256-splat batch (one
 // CTA), the batch's union rectangle for the blend's cull. The 64-byte records themselves stay
 // where the emit wrote them: the blend gathers them through the sort's index.
-__global__ void __launch_bounds__(kBlock) permute_kernel(BinArgs b) {
+#ifndef SN_PERMUTE_MIN_BLOCKS
+#define SN_PERMUTE_MIN_BLOCKS 5
+#endif
+__global__ void __launch_bounds__(kBlock, SN_PERMUTE_MIN_BLOCKS) permute_kernel(BinArgs b) {
     __shared__ ushort4 s_u[kBlock / 32];
     const int64_t n_vis = n_vis_of(b);
     if ((int64_t)blockIdx.x * kBlock >= n_vis) return;

@@ -243,8 +243,11 @@ __device__ __forceinline__ void push_fixup(const BlendArgs &b, bool flag, uint32
 #ifndef SN_BLEND_MIN_BLOCKS
 #define SN_BLEND_MIN_BLOCKS 4
 #endif
+#ifndef SN_LAYER_MIN_BLOCKS
+#define SN_LAYER_MIN_BLOCKS 4
+#endif
 template <int MODE, int SOURCE>
-__global__ void __launch_bounds__(kBlock, SN_BLEND_MIN_BLOCKS) blend_kernel(BlendArgs b) {
+__global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEND_MIN_BLOCKS) blend_kernel(BlendArgs b) {
     constexpr bool kBound = MODE != 1;  // depth error bounds feed the compositor
     __shared__ FRec s_f[kBlock];
     __shared__ uint32_t s_slot[kBlock];  // depth-sorted index (the exact fallback reads the SplatRec)

@@ -101,7 +101,10 @@ __global__ void __launch_bounds__(kRowThreads) sort_rowscan(uint32_t *hist, int 
     if (threadIdx.x == 0) totals[blockIdx.x] = run;
 }
 
-__global__ void __launch_bounds__(kSortThreads) sort_downsweep(const uint32_t *kin, const uint32_t *vin, uint32_t *kout,
+#ifndef SN_SORT_MIN_BLOCKS
+#define SN_SORT_MIN_BLOCKS 5
+#endif
+__global__ void __launch_bounds__(kSortThreads, SN_SORT_MIN_BLOCKS) sort_downsweep(const uint32_t *kin, const uint32_t *vin, uint32_t *kout,
                                                                uint32_t *vout, const uint64_t *d_n, uint64_t cap,
                                                                int shift, int dbits, const uint32_t *hist,
                                                                const uint32_t *totals, int n_tiles) {
