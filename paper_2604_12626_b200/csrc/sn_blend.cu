@@ -88,6 +88,9 @@ constexpr float kU125 = 7.5e-8f;       // 1.25 u: the one rounding of T' = fma(-
 constexpr float kTLo = 9.99999e-05f;   // 1e-4 (1 - 1e-6): below it (with the bound) T < 1e-4 for sure
 constexpr float kTHi = 1.000001e-04f;  // 1e-4 (1 + 1e-6)
 constexpr float kNegHalfLog2e = -0.72134752044448170f;
+// the blend works on h = d2 log2(e) / 2 (so e^(-d2/2) = 2^-h): its axes carry sqrt(log2(e) / 2)
+constexpr double kHalfLog2e = 0.72134752044448170;
+constexpr double kSqrtHalfLog2e = 0.84932180028801904272;
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
@@ -113,12 +116,13 @@ __device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
 }
 
 // Shared-memory form of a gathered splat for the float32 chain (64 B): the principal-axis rows as
-// (axis 1, axis 2) pairs, the decision thresholds 9 -/+ E(9.1), alpha, the alpha error bound
-// coefficients, colour and z (paired for the FFMA2 accumulation).
+// (axis 1, axis 2) pairs, the decision thresholds k (9 -/+ E(9.1)), alpha, the alpha error bound
+// coefficients, colour and z (paired for the FFMA2 accumulation). k = log2(e) / 2: the chain
+// works on h = k d2, so alpha = o 2^-h.
 struct __align__(16) FRec {
-    float a1x, c2x, a1y, c2y;  // (v1, v2) = (a1x, c2x) ox + (a1y, c2y) oy + (V1, V2), d2 = v1^2 + v2^2,
-    float V1, V2, thr_out, thr_in;  // v_k = sqrt(l_k) u_k
-    float ka, kb, alpha, pad;  // alpha's relative error bound: eps(d2) = ka d2 + kb
+    float a1x, c2x, a1y, c2y;  // (v1, v2) = (a1x, c2x) ox + (a1y, c2y) oy + (V1, V2), h = v1^2 + v2^2,
+    float V1, V2, thr_out, thr_in;  // v_j = sqrt(k l_j) u_j
+    float ka, kb, alpha, pad;  // alpha's relative error bound: eps = ka h + kb
     float r, g, b, z;
 };
 
@@ -155,8 +159,10 @@ __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1
     const double U1 = fma(e1x, cx, fma(e1y, cy, -p1));
     const double U2 = fma(-e1y, cx, fma(e1x, cy, -p2));
     const float l1 = gl.x, l2 = gl.y;
-    // the axes pre-scaled by sqrt(l_k) (float64 products, rounded once): d2 = v1^2 + v2^2
-    const double sl1 = sqrt((double)l1), sl2 = sqrt((double)fmaxf(l2, 0.0f));
+    // the axes pre-scaled by sqrt(l_k log2(e) / 2) (float64 products, rounded once):
+    // h = v1^2 + v2^2 = d2 log2(e) / 2, the exp argument itself; every float error of d2 scales by
+    // the same factor, so the d2 bounds below carry over with thresholds and ka scaled
+    const double sl1 = sqrt((double)l1) * kSqrtHalfLog2e, sl2 = sqrt((double)fmaxf(l2, 0.0f)) * kSqrtHalfLog2e;
     f.a1x = (float)(sl1 * e1x);
     f.a1y = (float)(sl1 * e1y);
     f.V1 = (float)(sl1 * U1);
@@ -182,9 +188,11 @@ __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1
         const float kap = 9.0e-15f * fminf(l1 / l2, 1e30f);
         const float e9 = 1.01f * (1.5f * (2.0f * u * 3.0166f * sig + 7.0f * u * 9.1f) + kap);
         ok = e9 < 0.5f;
-        f.thr_in = 9.0f - e9;
-        f.thr_out = 9.0f + e9;
-        f.ka = 1.01f * (0.75f * u * sig + 5.25f * u);
+        // k (9 -/+ e9) in h units, widened by 1e-6 for the float k and the products' roundings
+        const float kf = (float)kHalfLog2e;
+        f.thr_in = __fmaf_rn(-kf, e9, kf * 9.0f) - 1.0e-6f;
+        f.thr_out = __fmaf_rn(kf, e9, kf * 9.0f) + 1.0e-6f;
+        f.ka = 1.4003f * (0.75f * u * sig + 5.25f * u);  // 1.01 / k: eps = ka d2 + kb = ka' h + kb
         f.kb = 1.01f * (0.75f * u * sig + kEpsExp + 0.5f * kap);
     }
     if (!ok) {  // every pixel that is not certainly outside takes the float64 test
@@ -389,10 +397,10 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
                     const double ddx = sd.mx - px, ddy = sd.my - py;
                     const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
                     if (d2d > kSupportD2) continue;
-                    d2 = (float)d2d;
+                    d2 = (float)(d2d * kHalfLog2e);  // h, rounded once (within kEpsExact)
                     eps = kEpsExact;
                 }
-                const float e = ex2_approx(d2 * kNegHalfLog2e);
+                const float e = ex2_approx(-d2);  // 2^-h: the negation is an operand modifier
                 const float a = fminf(s.alpha * e, 0.99f);
                 const float w = a * T;
                 const float Tn = __fmaf_rn(-a, T, T);  // T (1 - a), rounded once
