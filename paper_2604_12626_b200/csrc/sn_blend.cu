@@ -257,6 +257,11 @@ __device__ __forceinline__ void push_fixup(const BlendArgs &b, bool flag, uint32
 template <int MODE, int SOURCE>
 __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEND_MIN_BLOCKS) blend_kernel(BlendArgs b) {
     constexpr bool kBound = MODE != 1;  // depth error bounds feed the compositor
+    // the layer tracks each pixel's largest alpha bound (it decides the compositor's depth choice);
+    // the scene pass uses the CTA's largest bound over every gathered splat -- looser, one
+    // instruction less per contribution
+    constexpr bool kPixBound = MODE == 2;
+    __shared__ unsigned s_epsmax;
     __shared__ FRec s_f[kBlock];
     __shared__ uint32_t s_slot[kBlock];  // depth-sorted index (the exact fallback reads the SplatRec)
     __shared__ uint32_t s_queue[2 * kBlock];
@@ -265,6 +270,7 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
     __shared__ uint8_t s_wl[kBlock / 32][kBlock];  // per warp: its batch entries, in depth order
     const PassView &v = b.pv;
     if (pass_overflow(v)) return;
+    if (threadIdx.x == 0) s_epsmax = __float_as_uint(kEpsExact);
     const int tile = blockIdx.x, el = blockIdx.y, env = b.e0 + el;
     const int tx = tile % b.tiles_x, ty = tile / b.tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -359,6 +365,8 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
             const float4 gr = __ldg(reinterpret_cast<const float4 *>(src + 3));
             FRec f;
             unsigned msk = tile_entry(ge.x, ge.y, gp.x, gp.y, gl, gr, x0 + 8.0, y0 + 8.0, f);
+            if (kBound && !kPixBound && msk)  // eps at the support edge bounds eps inside it
+                atomicMax(&s_epsmax, __float_as_uint(__fmaf_rn(f.ka, fminf(f.thr_out, 7.0f), f.kb)));
             s_f[threadIdx.x] = f;
             s_slot[threadIdx.x] = rid;
             s_mask[threadIdx.x] = (uint8_t)msk;
@@ -411,8 +419,8 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
                 err = __fmaf_rn(-a, err, __fmaf_rn(w, eps, __fmaf_rn(Tn, kU125, err)));  // err (1 - a) + ...
                 T = Tn;
                 ++nc;
+                if (kPixBound) eps_max = fmaxf(eps_max, eps);
                 if (kBound) {  // splats arrive in depth order: z spans [first, last] contribution
-                    eps_max = fmaxf(eps_max, eps);
                     z_first = fminf(z_first, q3.w);
                     z_last = q3.w;
                 }
@@ -450,6 +458,7 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
     // relative error <= rho_w (transmittance bound + largest alpha bound + the product's rounding);
     // depth = sum z w / sum w then errs by <= rho_w (z_last - z_first) from the weights (z spans the
     // contributions) plus (2n + 2) u from the float sums and the division; alpha by rho_w + (n + 1) u.
+    if (!kPixBound) eps_max = __uint_as_float(s_epsmax);
     const float rho_w = err / T + eps_max + 6.0e-8f;
     const float alpha = fminf(A, 1.0f);
     const float depth = A > 0.0f ? D / A : (float)cam.far_;
