@@ -110,7 +110,7 @@ struct sn_context {
     cudaEvent_t ev_work[2] = {};
     // side stream for the layer pass: its preprocessing overlaps the scene blend
     cudaStream_t side = nullptr;
-    cudaEvent_t ev_inputs = nullptr, ev_scene = nullptr, ev_layer = nullptr, ev_pre = nullptr;
+    cudaEvent_t ev_inputs = nullptr, ev_scene = nullptr, ev_layer = nullptr;
     int64_t launches = 0;  // kernels of this library launched through the context
     int64_t retries = 0;   // renders re-run because a pass outgrew its buffers
     double *ms_dst[2][SN_N_STAGES] = {};
@@ -431,7 +431,6 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
         bl.laerr = ctx->laerr.as<float>();
         bl.tile_flag = ctx->tile_flag.as<uint8_t>();
     }
-    if (pass_id == 0 && ctx->ev_pre) SN_CUDA(cudaEventRecord(ctx->ev_pre, st));  // scene preprocessing done
     tm.begin(SN_STAGE_BLEND);
     ctx->launches += sp.mode == 2 ? 1 : 2;  // blend (+ float64 fixup; mode 2's runs after the composite)
     SN_CUDA(launch_blend(bl, st));
@@ -549,7 +548,7 @@ int sn_context_destroy(sn_context *ctx) {
     if (ctx->h_work) cudaFreeHost(ctx->h_work);
     if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
     if (ctx->side) cudaStreamDestroy(ctx->side);
-    for (cudaEvent_t ev : {ctx->ev_inputs, ctx->ev_scene, ctx->ev_layer, ctx->ev_pre})
+    for (cudaEvent_t ev : {ctx->ev_inputs, ctx->ev_scene, ctx->ev_layer})
         if (ev) cudaEventDestroy(ev);
     if (ctx->h_tot) cudaFreeHost(ctx->h_tot);
     if (ctx->h_err) cudaFreeHost(ctx->h_err);
@@ -666,13 +665,6 @@ int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, con
         // kernel its error flag) into mapped memory; check them against the capacities
         SN_CUDA(cudaStreamSynchronize(st));
         SN_CHECK(ctx->h_err[0] == 0, "sample time must be nonnegative");
-        if (with_avatars && getenv("SN_DEBUG_CULL")) {
-            std::vector<uint8_t> codes((size_t)n_envs * avatars->n_avatars);
-            SN_CUDA(cudaMemcpy(codes.data(), ctx->av_cull.p, codes.size(), cudaMemcpyDeviceToHost));
-            int c[4] = {0, 0, 0, 0};
-            for (uint8_t v : codes) c[v & 3]++;
-            fprintf(stderr, "avatar cull: test %d depth %d frame %d\n", c[0], c[kCullDepth], c[kCullFrame]);
-        }
         bool grow = false;
         for (int p = 0; p < 2; ++p) {
             uint64_t need_v = 0, need_p = 0, sum_v = 0, sum_p = 0, last_v = 0, last_p = 0;
@@ -749,12 +741,10 @@ static int render_once(sn_context *ctx, const sn_cloud *scene, const sn_cloud *l
             // not queue behind the scene blend's CTAs, or the composite waits for it
             int lo = 0, hi = 0;
             SN_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-            const char *pe = getenv("SN_LAYER_PRIORITY");
-            SN_CUDA(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, (pe && pe[0] == '0') ? lo : hi));
+            SN_CUDA(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, hi));
             SN_CUDA(cudaEventCreateWithFlags(&ctx->ev_inputs, cudaEventDisableTiming));
             SN_CUDA(cudaEventCreateWithFlags(&ctx->ev_scene, cudaEventDisableTiming));
             SN_CUDA(cudaEventCreateWithFlags(&ctx->ev_layer, cudaEventDisableTiming));
-            SN_CUDA(cudaEventCreateWithFlags(&ctx->ev_pre, cudaEventDisableTiming));
         }
         lst = ctx->side;
         SN_CUDA(cudaEventRecord(ctx->ev_inputs, st));
@@ -777,12 +767,6 @@ static int render_once(sn_context *ctx, const sn_cloud *scene, const sn_cloud *l
                      e0 / chunk);
         if (r != SN_OK) return r;
         if (!two_pass) continue;
-        // the layer pass starts once the scene's preprocessing is done: it then overlaps the scene
-        // blend (issue-bound, long) instead of competing with the scene's memory-bound stages
-        {
-            const char *we = getenv("SN_LAYER_WAIT_PRE");
-            if (we && we[0] == '1') SN_CUDA(cudaStreamWaitEvent(lst, ctx->ev_pre, 0));
-        }
         if (with_avatars && e0 == 0) {
             const int A = avatars->n_avatars, J = avatars->n_joints;
             SN_ENSURE(ctx->times, sizeof(double) * n_envs);

@@ -21,7 +21,10 @@ namespace sn {
 namespace {
 
 constexpr int kSortThreads = 256;
-constexpr int kSortRounds = 8;  // items per thread
+#ifndef SN_SORT_ROUNDS
+#define SN_SORT_ROUNDS 8
+#endif
+constexpr int kSortRounds = SN_SORT_ROUNDS;  // items per thread
 constexpr int kSortTile = kSortThreads * kSortRounds;
 constexpr int kRowThreads = 1024;
 constexpr unsigned kAll = 0xffffffffu;
