@@ -266,6 +266,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     a.key_shift = key_bits > 32 ? key_bits - 32 : 0;
     a.vals = w.vals_un.as<uint32_t>();
     a.recs = w.recs_un.as<SplatRec>();
+    a.geo = w.geo_un.as<BlendGeo>();
     a.gid = w.gid_un.as<uint32_t>();
     a.rects = w.rects_un.as<ushort4>();
     a.cap = cap_v;
@@ -298,7 +299,6 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     b.rects_in = w.rects_un.as<ushort4>();
     b.env_off = w.env_off.as<uint64_t>();
     b.rects_out = w.rects.as<ushort4>();
-    b.geo_out = w.geo_un.as<BlendGeo>();
     b.batch_rects = w.batch_rects.as<ushort4>();
     b.tiles_touched = binning == 1 ? w.tiles.as<uint32_t>() : nullptr;  // pair counts: tile lists only
     b.pair_off = w.pair_off.as<uint64_t>();

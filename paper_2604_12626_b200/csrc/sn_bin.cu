@@ -70,12 +70,6 @@ __global__ void __launch_bounds__(kBlock, SN_PERMUTE_MIN_BLOCKS) permute_kernel(
     if (i >= n_vis) return;
     ushort4 r = mine;
     b.rects_out[i] = r;
-    {  // the blend's view of the splat, in depth order (the blend then reads it without the index)
-        const double2 *src = reinterpret_cast<const double2 *>(b.recs_un + b.vals_sorted[i]);
-        const double2 m = __ldg(src), c01 = __ldg(src + 1), c2a = __ldg(src + 2), zr = __ldg(src + 3);
-        b.geo_out[i] = make_blend_geo(m.x, m.y, c01.x, c01.y, c2a.x, c2a.y, zr.x,
-                                      (unsigned long long)__double_as_longlong(zr.y));
-    }
     if (b.tiles_touched) b.tiles_touched[i] = (uint32_t)(r.y - r.x + 1) * (uint32_t)(r.w - r.z + 1);
 }
 

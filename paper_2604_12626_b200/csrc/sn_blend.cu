@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
         if (threadIdx.x < n) {
             uint32_t rid = SOURCE == 0 ? s_queue[threadIdx.x]
                                        : (SOURCE == 1 ? __ldg(v.pair_vals + cursor + threadIdx.x) : cursor + threadIdx.x);
-            const double2 *src = reinterpret_cast<const double2 *>(v.geo + rid);
+            const double2 *src = reinterpret_cast<const double2 *>(v.geo + __ldg(v.order + rid));
             const double2 ge = __ldg(src), gp = __ldg(src + 1);
             const float4 gl = __ldg(reinterpret_cast<const float4 *>(src + 2));
             const float4 gr = __ldg(reinterpret_cast<const float4 *>(src + 3));

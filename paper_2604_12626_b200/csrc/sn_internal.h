@@ -39,6 +39,7 @@ struct PrepArgs {
     int32_t key_shift;         // right shift that turns the 64-bit key into the 32-bit one
     uint32_t *vals;            // identity positions
     SplatRec *recs;
+    BlendGeo *geo;             // the blend's view of each record (same slots as recs)
     uint32_t *gid;
     ushort4 *rects;
     int32_t tiles_x, tiles_y;
@@ -83,7 +84,6 @@ struct BinArgs {
     const ushort4 *rects_in;
     const uint64_t *env_off;
     ushort4 *rects_out;
-    BlendGeo *geo_out;       // (n_vis) BlendGeo in depth order
     ushort4 *batch_rects;    // (ceil(n_vis / 256)) union rect per 256-splat batch
     uint32_t *tiles_touched;
     uint64_t *pair_off;      // (n_vis + 1)

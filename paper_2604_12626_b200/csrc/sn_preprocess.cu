@@ -120,6 +120,7 @@ __device__ __forceinline__ void write_splat(const PrepArgs &a, int64_t pos, int 
     r.z = geo.z;
     r.rgb = pack_rgb21(rgb);
     a.recs[pos] = r;
+    a.geo[pos] = make_blend_geo(r.mx, r.my, r.ca, r.cb2, r.cc, r.alpha, r.z, r.rgb);
     unsigned long long zb = (unsigned long long)__double_as_longlong(geo.z);
     a.keys[pos] = (uint32_t)((((unsigned long long)e << a.z_bits) | (zb - a.z_base)) >> a.key_shift);
     a.vals[pos] = (uint32_t)pos;
