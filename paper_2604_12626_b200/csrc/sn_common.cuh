@@ -211,6 +211,35 @@ __device__ __forceinline__ int project_geo(const double p[3], const double cov[6
     return kKeep;
 }
 
+// The frame cull of project_geo for an in-depth gaussian, decided in float32 where that is certain
+// (-1: undecided, run project_geo). Camera coordinates are project_geo's own float64 values;
+// the mean's float32 projection errs by far less than `m`; the 3-sigma radius is at most
+// r^ = 3 sqrt(||J||_F^2 tr(cov3d) + 0.3) (lambda_max(J W S W^T J^T) <= ||J W||_2^2 lambda_max(S),
+// W orthonormal), and at least 0. While r^ < 3000 px the entries of cov2d stay below 1e6, so the
+// float64 determinant is >= 0.09 - 1e-4 and the reference's degenerate test cannot fire: a
+// mean inside the frame is kept, a footprint bound outside it is culled, anything else (and
+// any non-finite value) takes the float64 path.
+__device__ __forceinline__ int frame_prefilter(const double p[3], double tr_cov, const sn_camera &c) {
+    const double *w = c.rot;
+    const double z = dot3_fma(p[0], p[1], p[2], w[6], w[7], w[8]) + c.trans[2];
+    const double x = dot3_fma(p[0], p[1], p[2], w[0], w[1], w[2]) + c.trans[0];
+    const double y = dot3_fma(p[0], p[1], p[2], w[3], w[4], w[5]) + c.trans[1];
+    // approximate float ops (a few ulp each: the margins below are ~17 ulp and 0.03%)
+    const float iz = __frcp_rn((float)z), xz = (float)x * iz, yz = (float)y * iz;
+    const float fx = (float)c.fx, fy = (float)c.fy;
+    const float mx = __fmaf_rn(fx, xz, (float)c.cx), my = __fmaf_rn(fy, yz, (float)c.cy);
+    const float jx = fx * iz, jy = fy * iz;
+    const float jf2 = jx * jx * __fmaf_rn(xz, xz, 1.0f) + jy * jy * __fmaf_rn(yz, yz, 1.0f);
+    const float l = __fmaf_rn(jf2, (float)tr_cov, 0.3f);
+    const float r = 3.001f * (l * rsqrtf(l)) + 1e-3f;
+    if (!(r < 3000.0f) || !isfinite(mx) || !isfinite(my)) return -1;  // also catches NaN / inf
+    const float W = (float)c.width, H = (float)c.height;
+    const float m = 1e-3f + 1e-6f * (fabsf(mx) + fabsf(my) + W + H);
+    if (mx >= m && mx <= W - m && my >= m && my <= H - m) return kKeep;
+    if (mx + r < -m || mx - r > W + m || my + r < -m || my - r > H + m) return kCullFrame;
+    return -1;
+}
+
 // renderer.py:83-86: inclusive tile rectangle, clipped to the grid
 __device__ __forceinline__ void tile_rect(double mx, double my, double r, int tiles_x, int tiles_y, int rect[4]) {
     rect[0] = (int)np_clip(floor((mx - r) / kTile), 0.0, (double)(tiles_x - 1));

@@ -25,6 +25,9 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef SN_EMIT_MIN_BLOCKS
 #define SN_EMIT_MIN_BLOCKS 4
 #endif
+#ifndef SN_COUNT_MIN_BLOCKS
+#define SN_COUNT_MIN_BLOCKS 4
+#endif
 #ifndef SN_AVATAR_MIN_BLOCKS
 #define SN_AVATAR_MIN_BLOCKS 3
 #endif
@@ -178,11 +181,12 @@ __device__ __forceinline__ void tally_item(unsigned (*s_cnt)[5], unsigned active
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kBlock) scene_count_kernel(sn_cloud c, PrepArgs a) {
+__global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kernel(sn_cloud c, PrepArgs a) {
     __shared__ unsigned s_cnt[kMaxEnvChunk][5];
     __shared__ double s_geo[kBlock][9];  // position (3), cov3d (6)
     __shared__ unsigned long long s_vis[kBlock];
     __shared__ uint16_t s_q[kBlock / 32][32 * kEmitRound];
+    __shared__ uint16_t s_u[kBlock / 32][32 * kEmitRound];  // items the prefilter left undecided
     init_counts(s_cnt, a.ec);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
@@ -217,14 +221,41 @@ __global__ void __launch_bounds__(kBlock) scene_count_kernel(sn_cloud c, PrepArg
         }
     }
     const int64_t g0 = (int64_t)blockIdx.x * kBlock + warp * 32;
-    uint16_t *qq = s_q[warp];
+    uint16_t *qq = s_q[warp], *uq = s_u[warp];
     for (int eb = 0; eb < a.ec; eb += kEmitRound) {
         const int n = build_round(in_depth, eb, min(eb + kEmitRound, a.ec), qq);
+        // float32 prefilter on every item; the undecided ones are queued and take the float64
+        // geometry afterwards with full lanes (run in place, one undecided lane would hold the
+        // whole warp in project_geo)
+        int nu = 0;
         for (int k0 = 0; k0 < n; k0 += 32) {
             const int k = k0 + lane;
             const unsigned active = __ballot_sync(kFull, k < n);
-            if (k >= n) continue;
-            const unsigned it = qq[k];
+            int code = -2;
+            unsigned it = 0;
+            if (k < n) {
+                it = qq[k];
+                const int l = it & 31, e = (it >> 5) & 63;
+                const double *d = s_geo[warp * 32 + l];
+                const double pp[3] = {d[0], d[1], d[2]};
+                code = frame_prefilter(pp, (d[3] + d[6]) + d[8], a.cams[a.e0 + e]);
+            }
+            const unsigned und = __ballot_sync(kFull, code == -1);
+            if (code == -1) uq[nu + __popc(und & ((1u << lane) - 1u))] = (uint16_t)it;
+            nu += __popc(und);
+            const unsigned dec = active & ~und;
+            if (code >= 0) {
+                const int l = it & 31, e = (it >> 5) & 63;
+                tally_item(s_cnt, dec, e, code == kKeep ? 4 : 2);  // sn_stats fields: 2 frame, 4 drawn
+                if (code == kKeep) atomicOr(&s_vis[warp * 32 + l], 1ull << e);
+            }
+        }
+        __syncwarp();
+        for (int k0 = 0; k0 < nu; k0 += 32) {
+            const int k = k0 + lane;
+            const unsigned active = __ballot_sync(kFull, k < nu);
+            if (k >= nu) continue;
+            const unsigned it = uq[k];
             const int l = it & 31, e = (it >> 5) & 63;
             const double *d = s_geo[warp * 32 + l];
             const double pp[3] = {d[0], d[1], d[2]};
@@ -313,7 +344,9 @@ __device__ __forceinline__ void ld4p(const double *p, double o[4]) {
 }
 
 // NC = true: pose data in global memory (read-only path); false: generic loads (shared memory)
-template <bool NC = true>
+// ROT = false: the position only (q_out untouched) -- the count kernel's visibility test needs the
+// rotation only for the few items its float32 prefilter cannot decide.
+template <bool NC = true, bool ROT = true>
 __device__ __forceinline__ void skin_one(const sn_avatars &av, int64_t g, const double *jm, const double *eq,
                                          const double *root, double p_out[3], double q_out[4]) {
     double P[4], W[4], Q[4];
@@ -347,6 +380,7 @@ __device__ __forceinline__ void skin_one(const sn_avatars &av, int64_t g, const 
     p_out[0] = dot3_fma(b0, b1, b2, ldp<NC>(root + 0), ldp<NC>(root + 1), ldp<NC>(root + 2)) + ldp<NC>(root + 9);
     p_out[1] = dot3_fma(b0, b1, b2, ldp<NC>(root + 3), ldp<NC>(root + 4), ldp<NC>(root + 5)) + ldp<NC>(root + 10);
     p_out[2] = dot3_fma(b0, b1, b2, ldp<NC>(root + 6), ldp<NC>(root + 7), ldp<NC>(root + 8)) + ldp<NC>(root + 11);
+    if (!ROT) return;
 
     double qd[4];
     ld4p<NC>(eq + 4 * dom, qd);
@@ -406,7 +440,12 @@ __global__ void __launch_bounds__(kBlock, SN_AVATAR_MIN_BLOCKS) avatar_count_ker
     const int a_lo = av.avatar_of[g_first], a_hi = av.avatar_of[g_last];
     const int J = pv.n_joints, pb = pose_block_doubles(J);
     double ls[4];
-    if (valid) load4<double>(av.log_scales + 4 * g, ls);
+    double tr_cov = 0.0;  // trace of cov3d = sum of squared scales (rotation-invariant)
+    if (valid) {
+        load4<double>(av.log_scales + 4 * g, ls);
+        const double s0 = exp(ls[0]), s1 = exp(ls[1]), s2 = exp(ls[2]);
+        tr_cov = (s0 * s0 + s1 * s1) + s2 * s2;
+    }
     uint64_t mask = 0;
     for (int e = 0; e < a.ec; ++e) {
         int env = a.e0 + e;
@@ -433,19 +472,23 @@ __global__ void __launch_bounds__(kBlock, SN_AVATAR_MIN_BLOCKS) avatar_count_ker
             code = cull[avatar];  // the whole avatar is depth- or frame-culled in this env
         } else if (input) {
             double p[3], q[4];
-            if (avatar == a_lo || avatar == a_hi) {
-                const double *blk = s_pose + (avatar == a_lo ? 0 : pb);
-                skin_one<false>(av, g, blk, blk + 12 * J, blk + 16 * J, p, q);
-            } else {
-                const double *jm, *eq, *root;
-                pose_ptrs(pv, env, avatar, jm, eq, root);
-                skin_one<true>(av, g, jm, eq, root, p, q);
-            }
+            const bool staged = avatar == a_lo || avatar == a_hi;
+            const double *blk = s_pose + (avatar == a_lo ? 0 : pb);
+            const double *jm, *eq, *root;
+            pose_ptrs(pv, env, avatar, jm, eq, root);
+            if (staged)
+                skin_one<false, false>(av, g, blk, blk + 12 * J, blk + 16 * J, p, q);
+            else
+                skin_one<true, false>(av, g, jm, eq, root, p, q);
             const sn_camera &cam = a.cams[env];
             double z = cam_z(p, cam);
             if (!((z > cam.near_) && (z < cam.far_))) {
                 code = kCullDepth;
-            } else {
+            } else if ((code = frame_prefilter(p, tr_cov, cam)) < 0) {
+                if (staged)
+                    skin_one<false>(av, g, blk, blk + 12 * J, blk + 16 * J, p, q);
+                else
+                    skin_one<true>(av, g, jm, eq, root, p, q);
                 double cov[6];
                 build_cov3d(ls, q, cov);
                 Geo geo;
