@@ -34,6 +34,7 @@
 
 #ifdef SN_BLEND_PROF
 __device__ unsigned long long g_blend_prof[16];
+__device__ unsigned g_env_frac[64];  // per env: largest fraction (1/1000) of the depth list a tile consumed
 #endif
 
 namespace sn {
@@ -445,6 +446,14 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
     const bool amb = inside && (b.force_exact || (T - err <= kTHi && !(T + err < kTLo)));
     PROF(2, amb);
 #ifdef SN_BLEND_PROF
+    if (SOURCE == 0 && MODE == 0 && threadIdx.x == 0) {
+        const uint32_t st = (uint32_t)v.env_off[el], tot = s1 - st;
+        // consumed: the list position the walk had reached (queued-but-unwalked entries excluded)
+        const uint32_t used = (cursor - st) - (uint32_t)q_len;
+        const unsigned fr = tot ? (unsigned)((1000ull * used) / tot) : 0u;
+        atomicMax(&g_env_frac[el & 63], fr);
+        atomicAdd(&g_blend_prof[4 + min(11u, fr * 12u / 1001u)], 1ull);
+    }
     for (int i = 0; i < 16; ++i)
         if (prof[i]) atomicAdd(&g_blend_prof[i], prof[i]);
 #endif
@@ -1191,6 +1200,15 @@ extern "C" int sn_debug_blend_prof(unsigned long long *out, int reset) {
     if (reset) {
         unsigned long long z[16] = {};
         cudaMemcpyToSymbol(g_blend_prof, z, sizeof(z));
+    }
+    return 0;
+}
+extern "C" int sn_debug_env_frac(unsigned *out, int reset) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_env_frac, sizeof(unsigned) * 64);
+    if (reset) {
+        unsigned z[64] = {};
+        cudaMemcpyToSymbol(g_env_frac, z, sizeof(z));
     }
     return 0;
 }
