@@ -7,7 +7,9 @@
  * error code; sn_last_error() gives a thread-local message. Launches are asynchronous on the
  * given stream. sn_render() queues both passes without a host round trip (capacity-sized
  * workspace, counts kept on the device) and synchronizes the stream once, at the end, to check
- * the counts against the capacities (re-running the render with larger buffers if one overflowed).
+ * the counts against the capacities (re-running the render with larger buffers if one overflowed);
+ * sn_render_async / sn_render_wait split the two so the next render is queued before the host
+ * waits for the previous one.
  *
  * Reference interfaces replaced (file:line under /root/reference/pkg/src/splatnav):
  *   sn_render ................ renderer.render_observation (renderer.py:169-177) batched over
@@ -179,6 +181,20 @@ int sn_context_workspace_bytes(const sn_context *ctx, size_t *bytes);
 int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, const sn_avatars *avatars,
               const sn_camera *cams, const double *sim_times, int32_t n_envs, const sn_render_opts *opts,
               float *color, float *alpha, float *depth, void *stream);
+
+/*
+ * Pipelined form of sn_render: sn_render_async queues the render (same arguments) and returns
+ * without waiting; sn_render_wait waits for the OLDEST queued render and checks it. At most two
+ * renders are in flight per context (queue i + 1, then wait for i). *retry = 1 when a pass of that
+ * render outgrew the workspace: the buffers have been enlarged, its frames are invalid and it --
+ * like any render queued after it -- must be queued again. opts->work / stage_ms arrays must stay
+ * alive until the render has been waited for. sn_render itself requires that no async render is
+ * in flight.
+ */
+int sn_render_async(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, const sn_avatars *avatars,
+                    const sn_camera *cams, const double *sim_times, int32_t n_envs, const sn_render_opts *opts,
+                    float *color, float *alpha, float *depth, void *stream);
+int sn_render_wait(sn_context *ctx, int32_t *retry);
 
 /* Intermediates of the last sn_render pass (0 = scene, 1 = avatar layer) for env e, copied to
  * HOST buffers. sn_get_counts: visible splats and tile pairs. sorted_ids: original gaussian

@@ -63,7 +63,7 @@ STAGES = ("pose", "count", "scan", "emit", "depth_sort", "permute", "pair_scan",
 EXPORTS = (
     "sn_abi_version", "sn_last_error", "sn_context_create", "sn_context_destroy", "sn_context_workspace_bytes",
     "sn_context_sync_stats", "sn_context_kernel_launches", "sn_context_render_retries",
-    "sn_render", "sn_get_counts", "sn_get_sorted_ids", "sn_get_tile_csr", "sn_get_projection", "sn_sample_pose",
+    "sn_render", "sn_render_async", "sn_render_wait", "sn_get_counts", "sn_get_sorted_ids", "sn_get_tile_csr", "sn_get_projection", "sn_sample_pose",
     "sn_skin_lbs", "sn_blend_tile_range", "sn_composite", "sn_selftest_fast_exp", "sn_unpack_ply",
     "sn_unpack_bundle", "sn_quantize_frames", "sn_flip_rows",
 )
@@ -96,6 +96,9 @@ def load():
             "sn_context_render_retries": ([P, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
             "sn_render": ([P, ctypes.POINTER(SnCloud), ctypes.POINTER(SnCloud), ctypes.POINTER(SnAvatars), P, P, i32,
                            ctypes.POINTER(SnRenderOpts), P, P, P, P], ctypes.c_int),
+            "sn_render_async": ([P, ctypes.POINTER(SnCloud), ctypes.POINTER(SnCloud), ctypes.POINTER(SnAvatars), P, P,
+                                 i32, ctypes.POINTER(SnRenderOpts), P, P, P, P], ctypes.c_int),
+            "sn_render_wait": ([P, ctypes.POINTER(ctypes.c_int32)], ctypes.c_int),
             "sn_get_counts": ([P, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)], ctypes.c_int),
             "sn_get_sorted_ids": ([P, i32, i32, P, i64], ctypes.c_int),
             "sn_get_tile_csr": ([P, i32, i32, P, P, i64], ctypes.c_int),
@@ -154,6 +157,13 @@ class Context:
         v = ctypes.c_int64()
         check(self._lib.sn_context_kernel_launches(self.handle, ctypes.byref(v)))
         return int(v.value)
+
+    def render_wait(self):
+        """Wait for the oldest render queued with render_frames(..., wait=False) and check it.
+        Returns True when it must be queued again (the workspace grew; its frames are invalid)."""
+        r = ctypes.c_int32()
+        check(self._lib.sn_render_wait(self.handle, ctypes.byref(r)))
+        return bool(r.value)
 
     def render_retries(self):
         v = ctypes.c_int64()

@@ -31,12 +31,14 @@ class BatchRenderer:
         return self.scene.device
 
     def render(self, cameras, sim_times=None, avatar_active=None, tiled=True, contrib=False, stats=False,
-               exact=False, out=None):
+               exact=False, out=None, wait=True):
+        """wait=False: queue the render and return (see render_frames); pair every such call with
+        a later self.context.render_wait()."""
         if self.avatars is not None and sim_times is None:
             sim_times = np.zeros(len(cameras))
         return render_frames(self.scene, cameras, self.background, avatars=self.avatars, sim_times=sim_times,
                              tiled=tiled, context=self.context, contrib=contrib, stats=stats,
-                             avatar_active=avatar_active, exact=exact, out=out)
+                             avatar_active=avatar_active, exact=exact, out=out, wait=wait)
 
     def render_to_host(self, cameras, sim_times=None, host_out=None):
         """render() followed by a device->host copy into pinned buffers (the end-to-end path)."""
@@ -52,7 +54,10 @@ class BatchRenderer:
 
 class HostPipeline:
     """Render batches straight into pinned host memory with the device->host copies of batch i
-    overlapped with the render of batch i+1 (double-buffered, separate copy stream).
+    overlapped with the render of batch i+1 (double-buffered, separate copy stream). Renders are
+    queued with sn_render_async and checked one submit later, so the host never idles the GPU
+    between batches; a render whose check asks for a retry (workspace growth) is re-rendered
+    synchronously, with any render queued after it.
 
     submit(cameras, sim_times) -> slot index; the frames of a slot are valid in host[slot] after
     wait(slot) (or after the slot is reused two submits later, which waits for it)."""
@@ -75,6 +80,7 @@ class HostPipeline:
         self.dev = [{k: torch.empty(shapes[k], dtype=torch.float32, device=dev) for k in self.KEYS}
                     for _ in range(depth)]
         self.done = [None] * depth
+        self.pending = []  # (slot, cameras, sim_times, ready event) queued, not yet checked
         self.i = 0
 
     def submit(self, cameras, sim_times=None):
@@ -83,19 +89,46 @@ class HostPipeline:
         if self.done[slot] is not None:
             self.done[slot].synchronize()  # host buffer of this slot is free again
         with torch.cuda.stream(self.render_stream):
-            out = self.r.render(cameras, sim_times, out=dict(self.dev[slot]))
+            out = self.r.render(cameras, sim_times, out=dict(self.dev[slot]), wait=False)
             ready = torch.cuda.Event()
             ready.record(self.render_stream)
+        self.dev[slot] = {k: out[k] for k in self.KEYS}  # the tensors the render writes
+        self.pending.append((slot, cameras, sim_times, ready))
+        if len(self.pending) > 1:
+            self._retire()
+        return slot
+
+    def _copy(self, slot, ready):
         with torch.cuda.stream(self.copy_stream):
             self.copy_stream.wait_event(ready)
             for k in self.KEYS:
-                self.host[slot][k].copy_(out[k], non_blocking=True)
+                self.host[slot][k].copy_(self.dev[slot][k], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(self.copy_stream)
         self.done[slot] = ev
-        return slot
+
+    def _retire(self):
+        """Check the oldest queued render and start its download."""
+        slot, cams, times, ready = self.pending.pop(0)
+        if not self.r.context.render_wait():
+            self._copy(slot, ready)
+            return
+        # the workspace grew: this render and those queued after it ran on the old capacities
+        redo = [(slot, cams, times)] + [(s, c, t) for s, c, t, _ in self.pending]
+        for _ in self.pending:
+            self.r.context.render_wait()
+        self.pending = []
+        for s, c, t in redo:
+            with torch.cuda.stream(self.render_stream):
+                out = self.r.render(c, t, out=dict(self.dev[s]))
+                self.dev[s] = {k: out[k] for k in self.KEYS}
+                ev = torch.cuda.Event()
+                ev.record(self.render_stream)
+            self._copy(s, ev)
 
     def wait(self, slot=None):
+        while self.pending:
+            self._retire()
         for i, ev in enumerate(self.done):
             if ev is not None and (slot is None or i == slot):
                 ev.synchronize()

@@ -95,14 +95,28 @@ struct sn_context {
     // never queues behind other streams' bulk copies on the device->host copy engine
     uint64_t *h_tot = nullptr, *d_tot = nullptr;
     int32_t *h_err = nullptr, *d_err = nullptr;
-    // mapped (chunk, pass) -> (visible splats, tile pairs) of the last render, for the capacity check
-    uint64_t *h_counts = nullptr, *d_counts = nullptr;
-    size_t counts_cap = 0;  // entries (chunk x pass)
+    // Per-render host state, in a ring of two so a render can be queued while the previous one is
+    // still in flight (sn_render_async / sn_render_wait): mapped (chunk, pass) -> (visible splats,
+    // tile pairs) words and the pose kernel's error flag, checked after the render; pinned staging
+    // for the per-call host inputs (a pageable cudaMemcpyAsync would serialize with copies other
+    // streams have in flight, e.g. the caller's frame downloads).
+    struct Slot {
+        uint64_t *h_counts = nullptr, *d_counts = nullptr;
+        size_t counts_cap = 0;  // entries (chunk x pass)
+        int32_t *h_err = nullptr, *d_err = nullptr;
+        void *h_stage = nullptr;
+        size_t h_stage_cap = 0;
+        cudaEvent_t done = nullptr;
+        bool pending = false;
+        int64_t seq = 0;
+        int n_chunks = 0;
+        bool two_pass = false;
+        int64_t *work = nullptr;  // the caller's work counters (accumulated when the check passes)
+        uint64_t cap_v[2] = {0, 0}, cap_p[2] = {0, 0};  // the capacities the render ran with
+    } slot[2];
+    int cur = 0;          // slot of the render being queued
+    int64_t seq = 0;      // renders queued so far
     uint64_t *h_work = nullptr; // pinned (2 passes x 4 counters: loads, scans, contributions, fixups)
-    // pinned staging for the per-call host inputs: a pageable cudaMemcpyAsync would serialize
-    // with copies other streams have in flight (e.g. the caller's frame downloads)
-    void *h_stage = nullptr;
-    size_t h_stage_cap = 0;
     // lazily resolved instrumentation: CUDA events per (pass, stage) and the blend's counters,
     // folded into the caller's arrays at the next sn_render / sn_context_sync_stats, so timing
     // adds no host synchronization inside a render
@@ -448,8 +462,8 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     }
     // this chunk's (V, P) into mapped host memory: sn_render checks them against the capacities
     ctx->launches += 1;
-    SN_CUDA(launch_publish_counts(d_nvis, w.counts.as<uint64_t>() + 1, ctx->d_counts + 2 * (2 * chunk_idx + pass_id),
-                                  st));
+    SN_CUDA(launch_publish_counts(d_nvis, w.counts.as<uint64_t>() + 1,
+                                  ctx->slot[ctx->cur].d_counts + 2 * (2 * chunk_idx + pass_id), st));
     w.valid = 1;
     return SN_OK;
 }
@@ -546,13 +560,17 @@ int sn_context_destroy(sn_context *ctx) {
         for (auto &ev : ctx->ev_work) cudaEventDestroy(ev);
     }
     if (ctx->h_work) cudaFreeHost(ctx->h_work);
-    if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+    for (auto &S : ctx->slot) {
+        if (S.h_stage) cudaFreeHost(S.h_stage);
+        if (S.h_counts) cudaFreeHost(S.h_counts);
+        if (S.h_err) cudaFreeHost(S.h_err);
+        if (S.done) cudaEventDestroy(S.done);
+    }
     if (ctx->side) cudaStreamDestroy(ctx->side);
     for (cudaEvent_t ev : {ctx->ev_inputs, ctx->ev_scene, ctx->ev_layer})
         if (ev) cudaEventDestroy(ev);
     if (ctx->h_tot) cudaFreeHost(ctx->h_tot);
     if (ctx->h_err) cudaFreeHost(ctx->h_err);
-    if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
     delete ctx;
     return SN_OK;
 }
@@ -597,9 +615,10 @@ static int render_once(sn_context *ctx, const sn_cloud *scene, const sn_cloud *l
                        float *color, float *alpha, float *depth, cudaStream_t st, uint64_t z_lo, int z_bits, int chunk,
                        int tiled, bool with_layer, bool with_avatars);
 
-int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, const sn_avatars *avatars,
-              const sn_camera *cams, const double *sim_times, int32_t n_envs, const sn_render_opts *opts, float *color,
-              float *alpha, float *depth, void *stream) {
+// Validates a render's arguments and queues it on `stream` into the current slot; no host wait.
+static int render_queue(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, const sn_avatars *avatars,
+                        const sn_camera *cams, const double *sim_times, int32_t n_envs, const sn_render_opts *opts,
+                        float *color, float *alpha, float *depth, void *stream) {
     SN_CHECK(ctx != nullptr, "null context");
     SN_CHECK(n_envs >= 1, "need at least one environment");
     SN_CHECK(cams != nullptr && color && alpha && depth, "null camera or output buffer");
@@ -636,6 +655,8 @@ int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, con
     const int free_bits = 64 - z_bits;
     const int chunk = free_bits >= 6 ? kMaxEnvChunk : (1 << free_bits);
     const int tiled = opts ? opts->tiled : 1;
+    sn_context::Slot &S = ctx->slot[ctx->cur];
+    SN_CHECK(!S.pending, "two renders are already in flight: call sn_render_wait first");
     resolve_all(ctx);
     if (opts && (opts->stage_ms || opts->work) && !ctx->have_events) {
         for (auto &p : ctx->ev)
@@ -644,61 +665,117 @@ int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, con
         for (auto &ev : ctx->ev_work) SN_CUDA(cudaEventCreate(&ev));
         ctx->have_events = true;
     }
+    const int n_chunks = (n_envs + chunk - 1) / chunk;
+    if (!S.h_err) {
+        SN_CUDA(cudaHostAlloc(&S.h_err, sizeof(int32_t) * 4, cudaHostAllocMapped));
+        SN_CUDA(cudaHostGetDevicePointer(&S.d_err, S.h_err, 0));
+        SN_CUDA(cudaEventCreateWithFlags(&S.done, cudaEventDisableTiming));
+    }
+    if ((size_t)(2 * n_chunks) > S.counts_cap) {
+        SN_CUDA(cudaDeviceSynchronize());
+        if (S.h_counts) cudaFreeHost(S.h_counts);
+        S.h_counts = nullptr;
+        S.counts_cap = 0;
+        SN_CUDA(cudaHostAlloc(&S.h_counts, sizeof(uint64_t) * 2 * 2 * n_chunks, cudaHostAllocMapped));
+        SN_CUDA(cudaHostGetDevicePointer(&S.d_counts, S.h_counts, 0));
+        S.counts_cap = 2 * n_chunks;
+    }
+    std::memset(S.h_counts, 0, sizeof(uint64_t) * 2 * 2 * n_chunks);
+    S.h_err[0] = 0;
+    r = render_once(ctx, scene, layer, avatars, cams, sim_times, n_envs, opts, color, alpha, depth, st, z_lo, z_bits,
+                    chunk, tiled, with_layer, with_avatars);
+    if (r != SN_OK) return r;
+    SN_CUDA(cudaEventRecord(S.done, st));
+    for (int p = 0; p < 2; ++p) {
+        S.cap_v[p] = ctx->pass[p].cap_v;
+        S.cap_p[p] = ctx->pass[p].cap_p;
+    }
+    S.pending = true;
+    S.seq = ctx->seq++;
+    S.n_chunks = n_chunks;
+    S.two_pass = with_layer || with_avatars;
+    S.work = opts ? opts->work : nullptr;
+    ctx->cur ^= 1;
+    return SN_OK;
+}
 
-    for (int attempt = 0; attempt < 3; ++attempt) {
-        const int n_chunks = (n_envs + chunk - 1) / chunk;
-        if ((size_t)(2 * n_chunks) > ctx->counts_cap) {
-            SN_CUDA(cudaDeviceSynchronize());
-            if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
-            ctx->h_counts = nullptr;
-            ctx->counts_cap = 0;
-            SN_CUDA(cudaHostAlloc(&ctx->h_counts, sizeof(uint64_t) * 2 * 2 * n_chunks, cudaHostAllocMapped));
-            SN_CUDA(cudaHostGetDevicePointer(&ctx->d_counts, ctx->h_counts, 0));
-            ctx->counts_cap = 2 * n_chunks;
+// Waits for the oldest queued render and checks it: the pose kernel's error flag, and every pass's
+// published (visible, pairs) counts against the workspace capacities. *retry = 1: a pass outgrew
+// its buffers, which have been enlarged; that render's frames are invalid and it must be queued
+// again (as must any render queued after it with the old capacities).
+static int render_check(sn_context *ctx, int32_t *retry) {
+    *retry = 0;
+    sn_context::Slot *S = nullptr;
+    for (auto &c : ctx->slot)
+        if (c.pending && (!S || c.seq < S->seq)) S = &c;
+    SN_CHECK(S != nullptr, "no render in flight");
+    S->pending = false;
+    SN_CUDA(cudaEventSynchronize(S->done));
+    SN_CHECK(S->h_err[0] == 0, "sample time must be nonnegative");
+    bool grow = false;
+    for (int p = 0; p < 2; ++p) {
+        uint64_t need_v = 0, need_p = 0, sum_v = 0, sum_p = 0, last_v = 0, last_p = 0;
+        for (int c = 0; c < S->n_chunks; ++c) {
+            const uint64_t v = S->h_counts[2 * (2 * c + p)], q = S->h_counts[2 * (2 * c + p) + 1];
+            need_v = std::max(need_v, v);
+            need_p = std::max(need_p, q);
+            sum_v += v;
+            sum_p += q;
+            last_v = v;
+            last_p = q;
         }
-        std::memset(ctx->h_counts, 0, sizeof(uint64_t) * 2 * 2 * n_chunks);
-        ctx->h_err[0] = 0;
-        r = render_once(ctx, scene, layer, avatars, cams, sim_times, n_envs, opts, color, alpha, depth, st, z_lo,
-                        z_bits, chunk, tiled, with_layer, with_avatars);
-        if (r != SN_OK) return r;
-        // the one host synchronization of a render: every pass published its counts (and the pose
-        // kernel its error flag) into mapped memory; check them against the capacities
-        SN_CUDA(cudaStreamSynchronize(st));
-        SN_CHECK(ctx->h_err[0] == 0, "sample time must be nonnegative");
-        bool grow = false;
-        for (int p = 0; p < 2; ++p) {
-            uint64_t need_v = 0, need_p = 0, sum_v = 0, sum_p = 0, last_v = 0, last_p = 0;
-            for (int c = 0; c < n_chunks; ++c) {
-                const uint64_t v = ctx->h_counts[2 * (2 * c + p)], q = ctx->h_counts[2 * (2 * c + p) + 1];
-                need_v = std::max(need_v, v);
-                need_p = std::max(need_p, q);
-                sum_v += v;
-                sum_p += q;
-                last_v = v;
-                last_p = q;
-            }
-            SN_CHECK(need_v < 0xffffffffull, "too many visible splats in one env chunk (limit 2^32)");
-            SN_CHECK(need_p < 0x7fffffffull, "too many tile pairs in one env chunk (limit 2^31)");
-            PassWs &w = ctx->pass[p];
-            if (need_v > w.cap_v) {
-                w.cap_v = need_v + need_v / 4 + 1024;
-                grow = true;
-            }
-            if (need_p > w.cap_p) {
-                w.cap_p = need_p + need_p / 4 + 1024;
-                grow = true;
-            }
-            w.n_vis = (int64_t)last_v;
-            w.n_pairs = (int64_t)last_p;
-            if (!grow && opts && opts->work && (p == 0 || with_layer || with_avatars)) {
-                opts->work[6 * p] += (int64_t)sum_v;
-                opts->work[6 * p + 1] += (int64_t)sum_p;
-            }
+        SN_CHECK(need_v < 0xffffffffull, "too many visible splats in one env chunk (limit 2^32)");
+        SN_CHECK(need_p < 0x7fffffffull, "too many tile pairs in one env chunk (limit 2^31)");
+        // against the capacities this render ran with (a later check may have grown them already)
+        PassWs &w = ctx->pass[p];
+        if (need_v > S->cap_v[p]) {
+            w.cap_v = std::max(w.cap_v, need_v + need_v / 4 + 1024);
+            grow = true;
         }
-        if (!grow) return SN_OK;
-        // larger buffers: drop the partial work counters of the failed attempt and render again
+        if (need_p > S->cap_p[p]) {
+            w.cap_p = std::max(w.cap_p, need_p + need_p / 4 + 1024);
+            grow = true;
+        }
+        w.n_vis = (int64_t)last_v;
+        w.n_pairs = (int64_t)last_p;
+        if (!grow && S->work && (p == 0 || S->two_pass)) {
+            S->work[6 * p] += (int64_t)sum_v;
+            S->work[6 * p + 1] += (int64_t)sum_p;
+        }
+    }
+    if (grow) {
+        // larger buffers: drop the partial work counters of the failed attempt
         resolve_all(ctx);
         ctx->retries += 1;
+        *retry = 1;
+    }
+    return SN_OK;
+}
+
+int sn_render_async(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, const sn_avatars *avatars,
+                    const sn_camera *cams, const double *sim_times, int32_t n_envs, const sn_render_opts *opts,
+                    float *color, float *alpha, float *depth, void *stream) {
+    return render_queue(ctx, scene, layer, avatars, cams, sim_times, n_envs, opts, color, alpha, depth, stream);
+}
+
+int sn_render_wait(sn_context *ctx, int32_t *retry) {
+    SN_CHECK(ctx != nullptr && retry != nullptr, "null argument");
+    return render_check(ctx, retry);
+}
+
+int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, const sn_avatars *avatars,
+              const sn_camera *cams, const double *sim_times, int32_t n_envs, const sn_render_opts *opts, float *color,
+              float *alpha, float *depth, void *stream) {
+    SN_CHECK(ctx != nullptr, "null context");
+    SN_CHECK(!ctx->slot[0].pending && !ctx->slot[1].pending,
+             "renders queued with sn_render_async are in flight: call sn_render_wait first");
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        int r = render_queue(ctx, scene, layer, avatars, cams, sim_times, n_envs, opts, color, alpha, depth, stream);
+        if (r != SN_OK) return r;
+        int32_t retry = 0;
+        r = render_check(ctx, &retry);
+        if (r != SN_OK) return r;
+        if (!retry) return SN_OK;
     }
     return fail(SN_ERR_NOMEM, "workspace capacity did not converge");
 }
@@ -710,21 +787,22 @@ static int render_once(sn_context *ctx, const sn_cloud *scene, const sn_cloud *l
     const int W = cams[0].width, H = cams[0].height;
     int r = SN_OK;
     SN_ENSURE(ctx->cams, sizeof(sn_camera) * n_envs);
+    sn_context::Slot &S = ctx->slot[ctx->cur];
     {
         const size_t need = (sizeof(sn_camera) + sizeof(double)) * n_envs;
-        if (need > ctx->h_stage_cap) {
+        if (need > S.h_stage_cap) {
             SN_CUDA(cudaStreamSynchronize(st));
-            if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
-            ctx->h_stage = nullptr;
-            ctx->h_stage_cap = 0;
-            SN_CUDA(cudaMallocHost(&ctx->h_stage, need));
-            ctx->h_stage_cap = need;
+            if (S.h_stage) cudaFreeHost(S.h_stage);
+            S.h_stage = nullptr;
+            S.h_stage_cap = 0;
+            SN_CUDA(cudaMallocHost(&S.h_stage, need));
+            S.h_stage_cap = need;
         }
     }
-    // the previous call's uploads have completed: every call synchronizes its stream(s) at least once
-    // after its uploads, so the staging buffer is free to overwrite here
-    std::memcpy(ctx->h_stage, cams, sizeof(sn_camera) * n_envs);
-    SN_CUDA(cudaMemcpyAsync(ctx->cams.p, ctx->h_stage, sizeof(sn_camera) * n_envs, cudaMemcpyHostToDevice, st));
+    // the slot's previous render (two renders back) has been waited for, so its uploads are done
+    // and the staging buffer is free to overwrite here
+    std::memcpy(S.h_stage, cams, sizeof(sn_camera) * n_envs);
+    SN_CUDA(cudaMemcpyAsync(ctx->cams.p, S.h_stage, sizeof(sn_camera) * n_envs, cudaMemcpyHostToDevice, st));
     float *derr = nullptr;  // scene depth error bounds for the compositor
     if (with_avatars || with_layer) {
         SN_ENSURE(ctx->derr, sizeof(float) * (size_t)n_envs * W * H);
@@ -771,7 +849,7 @@ static int render_once(sn_context *ctx, const sn_cloud *scene, const sn_cloud *l
             const int A = avatars->n_avatars, J = avatars->n_joints;
             SN_ENSURE(ctx->times, sizeof(double) * n_envs);
             double *h_times =
-                reinterpret_cast<double *>(static_cast<char *>(ctx->h_stage) + sizeof(sn_camera) * n_envs);
+                reinterpret_cast<double *>(static_cast<char *>(S.h_stage) + sizeof(sn_camera) * n_envs);
             std::memcpy(h_times, sim_times, sizeof(double) * n_envs);
             SN_CUDA(cudaMemcpyAsync(ctx->times.p, h_times, sizeof(double) * n_envs, cudaMemcpyHostToDevice, lst));
             SN_ENSURE(ctx->jm, sizeof(double) * (size_t)n_envs * A * J * 12);
@@ -789,7 +867,7 @@ static int render_once(sn_context *ctx, const sn_cloud *scene, const sn_cloud *l
                                 ctx->root.as<double>(), ctx->err.as<int32_t>(), lst));
             ptm.end();
             ctx->launches += 1;
-            SN_CUDA(launch_publish_i32(ctx->err.as<int32_t>(), ctx->d_err, lst));  // checked by sn_render
+            SN_CUDA(launch_publish_i32(ctx->err.as<int32_t>(), S.d_err, lst));  // checked by sn_render_wait
             layer_spec.avatars = avatars;
             layer_spec.pose = PoseView{ctx->jm.as<double>(), ctx->eq.as<double>(), ctx->root.as<double>(), J, A};
             SN_ENSURE(ctx->av_ext, sizeof(unsigned long long) * (2 + J) * A);

@@ -58,11 +58,12 @@ def _nonempty(c):
 
 def render_frames(scene, cameras, background, layer=None, avatars=None, sim_times=None, tiled=True,
                   context=None, contrib=False, stats=True, avatar_active=None, stage_ms=None, work=None,
-                  binning=-1, exact=False, out=None):
+                  binning=-1, exact=False, out=None, wait=True):
     """One sn_render call over E cameras. Returns a dict of device tensors:
     color (E,H,W,3), alpha (E,H,W), depth (E,H,W) float32; stats (E,5) int64; optionally
     contrib_scene / contrib_layer (E,H,W) int32. The context keeps the pass intermediates for
-    the sn_get_* views."""
+    the sn_get_* views. wait=False queues the render (sn_render_async) and returns at once: the
+    frames are valid only after context.render_wait() for it returns False."""
     lib = N.load()
     ctx = context or N.default_context()
     dscene = DeviceCloud.wrap(scene)
@@ -75,7 +76,8 @@ def render_frames(scene, cameras, background, layer=None, avatars=None, sim_time
     shapes = {"color": (e, h, w, 3), "alpha": (e, h, w), "depth": (e, h, w)}
     for k, shp in shapes.items():
         t = out.get(k)
-        if t is None or tuple(t.shape) != shp or t.dtype != torch.float32 or t.device != dev or not t.is_contiguous():
+        same_dev = t is not None and t.device.type == dev.type and (t.device.index or 0) == (dev.index or 0)
+        if t is None or tuple(t.shape) != shp or t.dtype != torch.float32 or not same_dev or not t.is_contiguous():
             out[k] = torch.empty(shp, dtype=torch.float32, device=dev)
     opts = N.SnRenderOpts()
     opts.tiled = 1 if tiled else 0
@@ -103,7 +105,7 @@ def render_frames(scene, cameras, background, layer=None, avatars=None, sim_time
     if avatars is not None:
         times = np.ascontiguousarray(np.asarray(sim_times, dtype=np.float64).reshape(e))
     stream = torch.cuda.current_stream(dev).cuda_stream
-    N.check(lib.sn_render(
+    N.check((lib.sn_render if wait else lib.sn_render_async)(
         ctx.handle, ctypes.byref(dscene.struct()), ctypes.byref(dlayer.struct()) if dlayer is not None else None,
         ctypes.byref(avatars.struct()) if avatars is not None else None, cams,
         times.ctypes.data_as(ctypes.c_void_p) if times is not None else None, e, ctypes.byref(opts),

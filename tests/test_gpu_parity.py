@@ -505,3 +505,49 @@ def test_degenerate_and_extreme_splats():
                         o.color, o.alpha, o.depth, cams[e].far)
             assert out["stats"][e].tolist() == [o.stats[k] for k in ("n_input", "n_culled_depth", "n_culled_frame",
                                                                      "n_degenerate", "n_drawn")]
+
+
+def test_async_render_pipeline_matches_sync_and_retries():
+    """sn_render_async / sn_render_wait: renders queued back to back (the next one before the host
+    waits for the previous) give frames bit-identical to synchronous renders; on a fresh context the
+    first check asks for a retry (workspace growth) and the re-queued render matches; a
+    third render while two are in flight is refused."""
+    from paper_2604_12626_b200 import _native as N
+    from paper_2604_12626_b200.batch import BatchRenderer, HostPipeline
+    box, bundles = _avatar_setup(2, 2500, seed=91)
+    scene = S.make_scene(30_000, box[0], box[1], seed=92)
+    bg = (0.4, 0.4, 0.4)
+    sets = [(S.room_cameras(3, box, seed=93 + s, width=64, height=48), np.linspace(0.05 * s, 0.3, 3)) for s in range(4)]
+    ref = BatchRenderer(scene, bundles, start_offsets=[0.0, 0.1], loops=[1, 1], background=bg)
+    want = []
+    for cams, times in sets:
+        o = ref.render(cams, times)
+        want.append({k: o[k].clone() for k in ("color", "alpha", "depth")})
+    br = BatchRenderer(scene, bundles, start_offsets=[0.0, 0.1], loops=[1, 1], background=bg, context=N.Context())
+    outs = [{k: torch.empty_like(v) for k, v in w.items()} for w in want]
+    br.render(*sets[0], out=outs[0], wait=False)
+    assert br.context.render_wait()  # empty workspace: this render overflowed and must be re-queued
+    for cams, times in sets:  # grow the workspace to fit every set (synchronous renders retry inside)
+        br.render(cams, times)
+    br.render(*sets[0], out=outs[0], wait=False)
+    assert not br.context.render_wait()
+    br.render(*sets[1], out=outs[1], wait=False)
+    br.render(*sets[2], out=outs[2], wait=False)
+    from paper_2604_12626_b200.errors import ContractViolation
+    with pytest.raises(ContractViolation):
+        br.render(*sets[3], out=outs[3], wait=False)
+    assert not br.context.render_wait()
+    br.render(*sets[3], out=outs[3], wait=False)
+    assert not br.context.render_wait()
+    assert not br.context.render_wait()
+    for got, exp in zip(outs, want):
+        for k in exp:
+            assert torch.equal(got[k], exp[k]), k
+    # the host pipeline (async renders, downloads overlapped) delivers the same frames
+    pipe = HostPipeline(br, 3, 48, 64)
+    slots = [pipe.submit(*s) for s in sets]
+    pipe.wait()
+    for i, s in enumerate(slots[-2:]):
+        exp = want[len(sets) - 2 + i]
+        for k in exp:
+            assert torch.equal(pipe.host[s][k], exp[k].cpu()), k
