@@ -326,14 +326,16 @@ __device__ __forceinline__ void unpack_rgb21(unsigned long long v, float rgb[3])
     rgb[2] = (float)(unsigned)((v >> 42) & 0x1FFFFFull) * inv;
 }
 
-// View direction (projection.py:178-180) for SH, from float64 position and camera centre.
+// View direction (projection.py:178-180) for SH, from float64 position and camera centre. The
+// difference is float64; the normalization is float32 (colour is tolerance-checked: a direction
+// error of ~1e-7 moves an SH colour by far less than the 2e-3 bar).
 __device__ __forceinline__ void view_dir(const double p[3], const sn_camera &c, float d[3]) {
-    double v0 = p[0] - c.center[0], v1 = p[1] - c.center[1], v2 = p[2] - c.center[2];
-    double nv = sqrt((v0 * v0 + v1 * v1) + v2 * v2);
-    if (nv == 0.0) nv = 1.0;
-    d[0] = (float)(v0 / nv);
-    d[1] = (float)(v1 / nv);
-    d[2] = (float)(v2 / nv);
+    const float v0 = (float)(p[0] - c.center[0]), v1 = (float)(p[1] - c.center[1]), v2 = (float)(p[2] - c.center[2]);
+    const float n2 = __fmaf_rn(v0, v0, __fmaf_rn(v1, v1, v2 * v2));
+    const float inv = n2 > 0.0f ? rsqrtf(n2) : 1.0f;  // the reference divides by 1 for a zero vector
+    d[0] = v0 * inv;
+    d[1] = v1 * inv;
+    d[2] = v2 * inv;
 }
 
 __device__ __forceinline__ double sigmoid(double o) { return 1.0 / (1.0 + exp(-o)); }
