@@ -543,11 +543,17 @@ def test_async_render_pipeline_matches_sync_and_retries():
     for got, exp in zip(outs, want):
         for k in exp:
             assert torch.equal(got[k], exp[k]), k
-    # the host pipeline (async renders, downloads overlapped) delivers the same frames
-    pipe = HostPipeline(br, 3, 48, 64)
-    slots = [pipe.submit(*s) for s in sets]
-    pipe.wait()
-    for i, s in enumerate(slots[-2:]):
-        exp = want[len(sets) - 2 + i]
-        for k in exp:
-            assert torch.equal(pipe.host[s][k], exp[k].cpu()), k
+    # the host pipeline (async renders, downloads overlapped) delivers the same frames -- on a warm
+    # context, and on a fresh one whose first checks ask for retries (its re-render path)
+    fresh = BatchRenderer(scene, bundles, start_offsets=[0.0, 0.1], loops=[1, 1], background=bg, context=N.Context())
+    for renderer in (br, fresh):
+        pipe = HostPipeline(renderer, 3, 48, 64)
+        r0 = renderer.context.render_retries()
+        for st in sets:
+            pipe.submit(*st)
+        pipe.wait()
+        for i in (len(sets) - 2, len(sets) - 1):
+            for k in want[i]:
+                assert torch.equal(pipe.host[i % 2][k], want[i][k].cpu()), (k, i)
+        if renderer is fresh:
+            assert renderer.context.render_retries() > r0
