@@ -186,7 +186,6 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
     __shared__ double s_geo[kBlock][9];  // position (3), cov3d (6)
     __shared__ unsigned long long s_vis[kBlock];
     __shared__ uint16_t s_q[kBlock / 32][32 * kEmitRound];
-    __shared__ uint16_t s_u[kBlock / 32][32 * kEmitRound];  // items the prefilter left undecided
     init_counts(s_cnt, a.ec);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
@@ -221,41 +220,14 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
         }
     }
     const int64_t g0 = (int64_t)blockIdx.x * kBlock + warp * 32;
-    uint16_t *qq = s_q[warp], *uq = s_u[warp];
+    uint16_t *qq = s_q[warp];
     for (int eb = 0; eb < a.ec; eb += kEmitRound) {
         const int n = build_round(in_depth, eb, min(eb + kEmitRound, a.ec), qq);
-        // float32 prefilter on every item; the undecided ones are queued and take the float64
-        // geometry afterwards with full lanes (run in place, one undecided lane would hold the
-        // whole warp in project_geo)
-        int nu = 0;
         for (int k0 = 0; k0 < n; k0 += 32) {
             const int k = k0 + lane;
             const unsigned active = __ballot_sync(kFull, k < n);
-            int code = -2;
-            unsigned it = 0;
-            if (k < n) {
-                it = qq[k];
-                const int l = it & 31, e = (it >> 5) & 63;
-                const double *d = s_geo[warp * 32 + l];
-                const double pp[3] = {d[0], d[1], d[2]};
-                code = frame_prefilter(pp, (d[3] + d[6]) + d[8], a.cams[a.e0 + e]);
-            }
-            const unsigned und = __ballot_sync(kFull, code == -1);
-            if (code == -1) uq[nu + __popc(und & ((1u << lane) - 1u))] = (uint16_t)it;
-            nu += __popc(und);
-            const unsigned dec = active & ~und;
-            if (code >= 0) {
-                const int l = it & 31, e = (it >> 5) & 63;
-                tally_item(s_cnt, dec, e, code == kKeep ? 4 : 2);  // sn_stats fields: 2 frame, 4 drawn
-                if (code == kKeep) atomicOr(&s_vis[warp * 32 + l], 1ull << e);
-            }
-        }
-        __syncwarp();
-        for (int k0 = 0; k0 < nu; k0 += 32) {
-            const int k = k0 + lane;
-            const unsigned active = __ballot_sync(kFull, k < nu);
-            if (k >= nu) continue;
-            const unsigned it = uq[k];
+            if (k >= n) continue;
+            const unsigned it = qq[k];
             const int l = it & 31, e = (it >> 5) & 63;
             const double *d = s_geo[warp * 32 + l];
             const double pp[3] = {d[0], d[1], d[2]};
