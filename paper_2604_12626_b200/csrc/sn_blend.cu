@@ -182,8 +182,11 @@ __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1
     const float u = 5.9604644775390625e-08f;  // 2^-24
     const float aU1 = fabsf(fU1), aU2 = fabsf(fU2);
     bool ok = l2 > 0.0f;
+    float r1v = 0.0f, r2v = 0.0f;
     if (ok) {
         const float r1 = rsqrtf(l1), r2 = rsqrtf(l2);
+        r1v = r1;
+        r2v = r2;
         const float s1 = 2.0f * aU1 + 21.3f + 3.02f * r1, s2 = 2.0f * aU2 + 21.3f + 3.02f * r2;
         const float sig = (l1 * r1) * s1 + (l2 * r2) * s2;
         const float kap = 9.0e-15f * fminf(l1 / l2, 1e30f);
@@ -214,6 +217,16 @@ __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1
         const float marg = 1e-3f + 8.0f * u * (aU1 + aU2 + 16.0f);
         const float ext1 = 3.0f * rsqrtf(l1) * 1.00001f + marg + (3.5f * ax + 1.5f * ay);
         const float ext2 = 3.0f * rsqrtf(l2) * 1.00001f + marg + (3.5f * ay + 1.5f * ax);
+        // Two more axes, the diagonals of the support's normalized frame: with v_k = sqrt(l_k) u_k
+        // the support is the disc |v| <= 3 and a block is a parallelogram, which misses the disc if
+        // its projection on d = (1, +-1)/sqrt(2) stays beyond 3 -- the blocks near the corners of
+        // the oriented box, which pass the two tests above without holding a single pixel inside.
+        const float s1 = l1 * r1v, s2 = l2 * r2v;  // sqrt(l1), sqrt(l2)
+        const float hx1 = s1 * 3.5f * fe1x, hx2 = -s2 * 3.5f * fe1y;  // block half-edges in v space
+        const float hy1 = s1 * 1.5f * fe1y, hy2 = s2 * 1.5f * fe1x;
+        const float hwp = (fabsf(hx1 + hx2) + fabsf(hy1 + hy2)) * 0.70710678f;
+        const float hwm = (fabsf(hx1 - hx2) + fabsf(hy1 - hy2)) * 0.70710678f;
+        const float lim = 3.0f * 1.00001f + (s1 + s2) * marg;
         // u_k at the block centres (8 bx - 4, 4 by - 6) relative to the tile centre
         const float u1b = fU1 - 4.0f * fe1x - 6.0f * fe1y, u2b = fU2 + 4.0f * fe1y - 6.0f * fe1x;
 #pragma unroll
@@ -221,7 +234,11 @@ __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1
             const float bx = (float)(w & 1), by = (float)(w >> 1);
             const float u1c = u1b + 8.0f * bx * fe1x + 4.0f * by * fe1y;
             const float u2c = u2b - 8.0f * bx * fe1y + 4.0f * by * fe1x;
-            if (fabsf(u1c) > ext1 || fabsf(u2c) > ext2) m &= ~(1u << w);
+            const float v1c = s1 * u1c, v2c = s2 * u2c;
+            const float slack = lim + 1e-5f * (fabsf(v1c) + fabsf(v2c) + hwp + hwm);
+            if (fabsf(u1c) > ext1 || fabsf(u2c) > ext2 || fabsf(v1c + v2c) * 0.70710678f - hwp > slack ||
+                fabsf(v1c - v2c) * 0.70710678f - hwm > slack)
+                m &= ~(1u << w);
         }
     }
     return m;
