@@ -2,7 +2,8 @@
 avatar count'): frames/s and per-stage ms for the scene-complexity sweep (250k..6M gaussians, 256
 envs) and the avatar-count sweep (3M scene, 0..16 avatars x 50k, 1,024 envs), plus config 1 and the
 near=0.01 sensitivity row of config 2. Inputs are seeded synthetic stand-ins (synthetic.py). Each
-point: 2 untimed steps (workspace growth), then 3 timed steps with fresh cameras, CUDA events.
+point: 2 untimed steps (workspace growth), then 3 timed steps with fresh cameras, CUDA events, renders
+pipelined through sn_render_async / sn_render_wait as in bench.py; stage timers from a separate pass.
 Prints one JSON line per point."""
 import json
 import os
@@ -28,19 +29,37 @@ def point(config, n, a, e, near=0.1, steps=3, warm=2, seed=0):
             for s in range(warm + steps)]
     stage = np.zeros(2 * len(N.STAGES))
     work = np.zeros(12, dtype=np.int64)
-    for s in range(warm):
+    for s in range(warm + steps):  # untimed: grows the workspace to fit every timed step's views
         br.render(*sets[s])
     torch.cuda.synchronize()
+    shapes = {"color": (e, 480, 640, 3), "alpha": (e, 480, 640), "depth": (e, 480, 640)}
+    outs = [{k: torch.empty(v, device="cuda") for k, v in shapes.items()} for _ in range(2)]
+
+    def run(s, wait, **kw):
+        cams, times = sets[s]
+        return render_frames(br.scene, cams, br.background, avatars=br.avatars, sim_times=times if a else None,
+                             context=br.context, stats=False, out=dict(outs[s % 2]), wait=wait, **kw)
+
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
+    pending = []  # pipelined like bench.py: queue step s + 1, then check step s
     for s in range(warm, warm + steps):
-        cams, times = sets[s]
-        render_frames(br.scene, cams, br.background, avatars=br.avatars, sim_times=times if a else None,
-                      context=br.context, stats=False, stage_ms=stage, work=work)
+        run(s, False)
+        pending.append(s)
+        if len(pending) > 1 and br.context.render_wait():
+            raise RuntimeError("workspace grew inside the timed steps; raise the warm-up")
+        if len(pending) > 1:
+            pending.pop(0)
+    while pending:
+        if br.context.render_wait():
+            raise RuntimeError("workspace grew inside the timed steps; raise the warm-up")
+        pending.pop(0)
     e1.record()
     torch.cuda.synchronize()
-    br.context.sync_stats()
     ms = e0.elapsed_time(e1) / steps
+    for s in range(warm, warm + steps):  # stage timers and work counters: a separate, untimed pass
+        run(s, True, stage_ms=stage, work=work)
+    br.context.sync_stats()
     st = stage.reshape(2, -1) / steps
     names = list(N.STAGES)
     g = lambda p, *ks: float(sum(st[p, names.index(k)] for k in ks))
