@@ -12,6 +12,8 @@
 // projection (rig.py:107-146): skinned positions/rotations never touch HBM.
 #include <cub/block/block_scan.cuh>
 
+#include <algorithm>
+
 #include "sn_common.cuh"
 #include "sn_internal.h"
 
@@ -27,6 +29,9 @@ constexpr unsigned kFull = 0xffffffffu;
 #endif
 #ifndef SN_COUNT_MIN_BLOCKS
 #define SN_COUNT_MIN_BLOCKS 4
+#endif
+#ifndef SN_AVATAR_ENV_GROUP
+#define SN_AVATAR_ENV_GROUP 8  // envs whose pose blocks the avatar count kernel stages per barrier pair
 #endif
 #ifndef SN_AVATAR_MIN_BLOCKS
 #define SN_AVATAR_MIN_BLOCKS 3
@@ -400,9 +405,11 @@ __device__ __forceinline__ bool avatar_on(const PrepArgs &a, int n_avatars, int 
 // avatars fall back to global loads).
 __host__ __device__ __forceinline__ int pose_block_doubles(int J) { return 16 * J + 12; }
 
-__global__ void __launch_bounds__(kBlock, SN_AVATAR_MIN_BLOCKS) avatar_count_kernel(sn_avatars av, PoseView pv, PrepArgs a) {
+// Pose blocks are staged for `group` envs per barrier pair (group x 2 blocks in shared memory).
+__global__ void __launch_bounds__(kBlock, SN_AVATAR_MIN_BLOCKS) avatar_count_kernel(sn_avatars av, PoseView pv, PrepArgs a,
+                                                                                    int group) {
     __shared__ unsigned s_cnt[kMaxEnvChunk][5];
-    extern __shared__ double s_pose[];  // 2 x (J*12 joint mats | J*4 quats | 12 root)
+    extern __shared__ double s_pose[];  // group x 2 x (J*12 joint mats | J*4 quats | 12 root)
     init_counts(s_cnt, a.ec);
     int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     bool valid = g < av.n;
@@ -422,22 +429,28 @@ __global__ void __launch_bounds__(kBlock, SN_AVATAR_MIN_BLOCKS) avatar_count_ker
     for (int e = 0; e < a.ec; ++e) {
         int env = a.e0 + e;
         const uint8_t *cull = a.avatar_cull ? a.avatar_cull + (int64_t)env * av.n_avatars : nullptr;
-        // both avatars of this block culled whole for this env: no pose staging, no skinning
-        const bool stage = !(cull && cull[a_lo] && cull[a_hi]);
-        __syncthreads();
-        for (int k = threadIdx.x; stage && k < 2 * pb; k += kBlock) {
-            const int slot = k / pb, o = k % pb, av_id = slot ? a_hi : a_lo;
-            const int64_t ea = (int64_t)env * pv.n_avatars + av_id;
-            double v;
-            if (o < 12 * J)
-                v = pv.joint_mats[ea * J * 12 + o];
-            else if (o < 16 * J)
-                v = pv.eff_q[ea * J * 4 + (o - 12 * J)];
-            else
-                v = pv.root[ea * 12 + (o - 16 * J)];
-            s_pose[k] = v;
+        const int gs = e % group;  // this env's staging slot in the group
+        if (gs == 0) {  // stage the group's pose blocks (skipping envs whose two avatars are culled whole)
+            __syncthreads();
+            const int ge = min(group, a.ec - e);
+            for (int k = threadIdx.x; k < ge * 2 * pb; k += kBlock) {
+                const int eg = k / (2 * pb), kk = k % (2 * pb);
+                const int env_k = env + eg;
+                const uint8_t *cull_k = a.avatar_cull ? a.avatar_cull + (int64_t)env_k * av.n_avatars : nullptr;
+                if (cull_k && cull_k[a_lo] && cull_k[a_hi]) continue;
+                const int slot = kk / pb, o = kk % pb, av_id = slot ? a_hi : a_lo;
+                const int64_t ea = (int64_t)env_k * pv.n_avatars + av_id;
+                double v;
+                if (o < 12 * J)
+                    v = pv.joint_mats[ea * J * 12 + o];
+                else if (o < 16 * J)
+                    v = pv.eff_q[ea * J * 4 + (o - 12 * J)];
+                else
+                    v = pv.root[ea * 12 + (o - 16 * J)];
+                s_pose[k] = v;
+            }
+            __syncthreads();
         }
-        __syncthreads();
         bool input = valid && avatar_on(a, av.n_avatars, env, avatar);
         int code = -1;
         if (input && cull && cull[avatar]) {
@@ -445,7 +458,7 @@ __global__ void __launch_bounds__(kBlock, SN_AVATAR_MIN_BLOCKS) avatar_count_ker
         } else if (input) {
             double p[3], q[4];
             const bool staged = avatar == a_lo || avatar == a_hi;
-            const double *blk = s_pose + (avatar == a_lo ? 0 : pb);
+            const double *blk = s_pose + (size_t)gs * 2 * pb + (avatar == a_lo ? 0 : pb);
             const double *jm, *eq, *root;
             pose_ptrs(pv, env, avatar, jm, eq, root);
             if (staged)
@@ -597,9 +610,11 @@ cudaError_t launch_scene_emit(const sn_cloud &c, const PrepArgs &a, cudaStream_t
 }
 
 cudaError_t launch_avatar_count(const sn_avatars &av, const PoseView &pv, const PrepArgs &a, cudaStream_t s) {
-    const size_t smem = sizeof(double) * 2 * (size_t)pose_block_doubles(pv.n_joints);
+    const size_t blk = sizeof(double) * 2 * (size_t)pose_block_doubles(pv.n_joints);
+    const int group = (int)std::max<size_t>(1, std::min<size_t>(SN_AVATAR_ENV_GROUP, (40 * 1024) / blk));
+    const size_t smem = blk * group;
     if (smem > 48 * 1024) cudaFuncSetAttribute(avatar_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    avatar_count_kernel<<<a.n_blocks, kBlock, smem, s>>>(av, pv, a);
+    avatar_count_kernel<<<a.n_blocks, kBlock, smem, s>>>(av, pv, a, group);
     return cudaGetLastError();
 }
 
