@@ -401,6 +401,17 @@ def main():
         clk = (clocks.summary() or {}).get("sm_mhz") or 1965.0
         peak_t = 148 * 128 * clk * 1e6 / 1e12  # FP32 lane-instructions per second (1 FFMA = 1)
         achieved_t = contribs * per_contrib / (per_stage[dom] / 1e3) / 1e12
+        if traffic is not None and traffic.get("warp_inst_per_launch"):
+            # the bound that actually binds: instruction issue (4 schedulers per SM, 1 warp
+            # instruction per cycle each); instructions per launch from the committed ncu capture
+            # of the same command, divided by this run's live blend time
+            inst = traffic["warp_inst_per_launch"]
+            peak_i = 148 * 4 * clk * 1e6 / 1e9
+            ach_i = inst / (per_stage[dom] / 1e3) / 1e9
+            roofline["issue"] = {"warp_inst_per_launch": inst, "achieved_ginst_per_s": ach_i,
+                                 "peak_ginst_per_s": peak_i,
+                                 "peak_kind": f"148 SMs x 4 schedulers x {clk:.0f} MHz (measured SM clock)",
+                                 "frac": ach_i / peak_i, "source": traffic["source"]}
         roofline["compute"] = {"pipe": "fp32", "contributions_per_step": int(contribs),
                                "fp32_inst_per_contribution": per_contrib,
                                "achieved_tinst_per_s": achieved_t, "peak_tinst_per_s": peak_t,

@@ -43,7 +43,9 @@ def main():
             result[stage] = {"dram_bytes_per_launch": vals.get("dram__bytes_read.sum", 0.0) +
                              vals.get("dram__bytes_write.sum", 0.0),
                              "launches_per_step": 1, "source": f"ncu --set full ({rep.split('/')[-1]})",
-                             "ncu_ms": vals.get("gpu__time_duration.sum")}
+                             "ncu_ms": vals.get("gpu__time_duration.sum"),
+                             "warp_inst_per_launch": vals.get("smsp__inst_executed.sum"),
+                             "issue_active_pct": vals.get("smsp__issue_active.avg.pct_of_peak_sustained_active")}
     with open(out, "w") as f:
         json.dump(result, f, indent=1)
 
