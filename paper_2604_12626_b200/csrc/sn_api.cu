@@ -75,7 +75,7 @@ uint64_t dbits(double d) {
 }
 
 struct PassWs {
-    Buf vismask, blk_counts, env_off, keys_un, keys_s, vals_un, vals_s, recs_un, geo_un, gid_un, rects_un, rects,
+    Buf vismask, blk_counts, env_off, keys_un, keys_s, vals_un, vals_s, recs_un, geo_un, gid_un, rects_un, rects_tun, rects,
         tiles, pair_off, pkeys_a, pkeys_b, pvals_a, pvals_b, ranges, temp, batch_rects, super_rects, fix, counts;
     uint64_t cap_v = 0, cap_p = 0;  // capacities of the per-splat / per-pair buffers
     // metadata of the last chunk rendered by this pass
@@ -264,6 +264,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     SN_ENSURE(w.geo_un, sizeof(BlendGeo) * v1);
     SN_ENSURE(w.gid_un, sizeof(uint32_t) * v1);
     SN_ENSURE(w.rects_un, sizeof(ushort4) * v1);
+    SN_ENSURE(w.rects_tun, sizeof(ushort4) * v1);
     SN_ENSURE(w.rects, sizeof(ushort4) * v1);
     SN_ENSURE(w.tiles, sizeof(uint32_t) * v1);
     SN_ENSURE(w.pair_off, sizeof(uint64_t) * v1);
@@ -283,6 +284,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     a.geo = w.geo_un.as<BlendGeo>();
     a.gid = w.gid_un.as<uint32_t>();
     a.rects = w.rects_un.as<ushort4>();
+    a.rects_tight = w.rects_tun.as<ushort4>();
     a.cap = cap_v;
 
     if (n > 0) {
@@ -310,7 +312,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     b.d_npairs = w.counts.as<uint64_t>() + 1;
     b.cap_p = cap_p;
     b.recs_un = w.recs_un.as<SplatRec>();
-    b.rects_in = w.rects_un.as<ushort4>();
+    b.rects_in = w.rects_tun.as<ushort4>();  // the blend's (tight) rectangles into depth order
     b.env_off = w.env_off.as<uint64_t>();
     b.rects_out = w.rects.as<ushort4>();
     b.batch_rects = w.batch_rects.as<ushort4>();
@@ -544,7 +546,7 @@ int sn_context_destroy(sn_context *ctx) {
     };
     for (auto &w : ctx->pass) {
         for (Buf *b : {&w.vismask, &w.blk_counts, &w.env_off, &w.keys_un, &w.keys_s, &w.vals_un, &w.vals_s, &w.recs_un, &w.geo_un,
-                       &w.gid_un, &w.rects_un, &w.rects, &w.tiles, &w.pair_off, &w.pkeys_a,
+                       &w.gid_un, &w.rects_un, &w.rects_tun, &w.rects, &w.tiles, &w.pair_off, &w.pkeys_a,
                        &w.pkeys_b, &w.pvals_a, &w.pvals_b, &w.ranges, &w.temp, &w.batch_rects, &w.super_rects,
                        &w.fix, &w.counts})
             free_buf(*b);
@@ -598,7 +600,7 @@ int sn_context_workspace_bytes(const sn_context *ctx, size_t *bytes) {
     size_t t = 0;
     for (const auto &w : ctx->pass)
         for (const Buf *b : {&w.vismask, &w.blk_counts, &w.env_off, &w.keys_un, &w.keys_s, &w.vals_un, &w.vals_s,
-                             &w.recs_un, &w.geo_un, &w.gid_un, &w.rects_un, &w.rects, &w.tiles, &w.pair_off,
+                             &w.recs_un, &w.geo_un, &w.gid_un, &w.rects_un, &w.rects_tun, &w.rects, &w.tiles, &w.pair_off,
                              &w.pkeys_a, &w.pkeys_b, &w.pvals_a, &w.pvals_b, &w.ranges, &w.temp,
                              &w.batch_rects, &w.super_rects, &w.fix})
             t += b->cap;
@@ -903,10 +905,11 @@ static int pass_env(sn_context *ctx, int32_t pass, int32_t env, PassWs *&w, int 
     return SN_OK;
 }
 
-// Tile CSR of env `el` in the reference's form (tile_starts, depth ranks). binning 1: the device's
-// materialized lists. binning 0: the blend consumed no lists -- each tile took, in depth order,
-// the splats whose device-computed rectangle covers it -- so the CSR is rebuilt from the
-// device's depth-sorted rectangles by exactly that rule.
+// Tile CSR of env `el` in the reference's form (tile_starts, depth ranks): every depth-sorted splat
+// whose reference tile rectangle (renderer.py:83-86, computed on the device by the emit) covers
+// the tile, in depth order -- _bin_tiles' lists. The device's own lists / streamed rectangles are
+// the tighter subsets the blend consumes (tiles the support ellipse can reach), so the view is
+// rebuilt here from the device's reference rectangles and depth order.
 static int env_tile_csr(PassWs *w, int el, const std::vector<uint64_t> &off, std::vector<int64_t> &ts,
                         std::vector<int32_t> &ps) {
     const int n_tiles = w->tiles_x * w->tiles_y;
@@ -914,27 +917,18 @@ static int env_tile_csr(PassWs *w, int el, const std::vector<uint64_t> &off, std
     ps.clear();
     if (!w->tiled || w->n_vis == 0) return SN_OK;
     const uint64_t v0 = off[el], v1 = off[el + 1];
-    if (w->binning == 1) {
-        std::vector<uint2> rng(n_tiles);
-        SN_CUDA(cudaMemcpy(rng.data(), w->ranges.as<uint2>() + ((size_t)el << w->tile_bits), sizeof(uint2) * n_tiles,
+    std::vector<uint32_t> order((size_t)(v1 - v0));
+    std::vector<ushort4> ref((size_t)(v1 - v0)), rects((size_t)(v1 - v0));
+    if (!order.empty()) {
+        SN_CUDA(cudaMemcpy(order.data(), w->vals_s.as<uint32_t>() + v0, sizeof(uint32_t) * order.size(),
                            cudaMemcpyDeviceToHost));
-        uint64_t pp[2];
-        SN_CUDA(cudaMemcpy(&pp[0], w->pair_off.as<uint64_t>() + v0, 8, cudaMemcpyDeviceToHost));
-        SN_CUDA(cudaMemcpy(&pp[1], w->pair_off.as<uint64_t>() + v1, 8, cudaMemcpyDeviceToHost));
-        for (int t = 0; t < n_tiles; ++t) ts[t + 1] = ts[t] + (int64_t)(rng[t].y - rng[t].x);
-        SN_CHECK(ts[n_tiles] == (int64_t)(pp[1] - pp[0]), "tile ranges do not cover the env's pairs");
-        std::vector<uint32_t> v((size_t)(pp[1] - pp[0]));
-        if (!v.empty())
-            SN_CUDA(cudaMemcpy(v.data(), w->pvals_b.as<uint32_t>() + pp[0], sizeof(uint32_t) * v.size(),
-                               cudaMemcpyDeviceToHost));
-        ps.resize(v.size());
-        for (size_t i = 0; i < v.size(); ++i) ps[i] = (int32_t)(v[i] - v0);
-        return SN_OK;
+        SN_CUDA(cudaMemcpy(ref.data(), w->rects_un.as<ushort4>() + v0, sizeof(ushort4) * ref.size(),
+                           cudaMemcpyDeviceToHost));
     }
-    std::vector<ushort4> rects((size_t)(v1 - v0));
-    if (!rects.empty())
-        SN_CUDA(cudaMemcpy(rects.data(), w->rects.as<ushort4>() + v0, sizeof(ushort4) * rects.size(),
-                           cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < order.size(); ++i) {  // env-major emission: the env's slots are [v0, v1)
+        SN_CHECK(order[i] >= v0 && order[i] < v1, "depth order leaves the env's slots");
+        rects[i] = ref[order[i] - v0];
+    }
     for (const ushort4 &q : rects)
         for (int y = q.z; y <= q.w; ++y)
             for (int x = q.x; x <= q.y; ++x) ts[y * w->tiles_x + x + 1]++;

@@ -70,7 +70,8 @@ __global__ void __launch_bounds__(kBlock, SN_PERMUTE_MIN_BLOCKS) permute_kernel(
     if (i >= n_vis) return;
     ushort4 r = mine;
     b.rects_out[i] = r;
-    if (b.tiles_touched) b.tiles_touched[i] = (uint32_t)(r.y - r.x + 1) * (uint32_t)(r.w - r.z + 1);
+    if (b.tiles_touched)
+        b.tiles_touched[i] = r.x <= r.y && r.z <= r.w ? (uint32_t)(r.y - r.x + 1) * (uint32_t)(r.w - r.z + 1) : 0u;
 }
 
 // Load-balanced pair emission: a CTA owns 256 consecutive depth-sorted splats and spreads

@@ -40,6 +40,7 @@ struct PrepArgs {
     uint32_t *vals;            // identity positions
     SplatRec *recs;
     BlendGeo *geo;             // the blend's view of each record (same slots as recs)
+    ushort4 *rects_tight;      // tiles the support ellipse's bounding box reaches (within rects)
     uint32_t *gid;
     ushort4 *rects;
     int32_t tiles_x, tiles_y;

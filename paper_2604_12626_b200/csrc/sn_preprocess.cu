@@ -128,7 +128,8 @@ __device__ __forceinline__ void write_splat(const PrepArgs &a, int64_t pos, int 
     r.z = geo.z;
     r.rgb = pack_rgb21(rgb);
     a.recs[pos] = r;
-    a.geo[pos] = make_blend_geo(r.mx, r.my, r.ca, r.cb2, r.cc, r.alpha, r.z, r.rgb);
+    const BlendGeo bg = make_blend_geo(r.mx, r.my, r.ca, r.cb2, r.cc, r.alpha, r.z, r.rgb);
+    a.geo[pos] = bg;
     unsigned long long zb = (unsigned long long)__double_as_longlong(geo.z);
     a.keys[pos] = (uint32_t)((((unsigned long long)e << a.z_bits) | (zb - a.z_base)) >> a.key_shift);
     a.vals[pos] = (uint32_t)pos;
@@ -137,6 +138,23 @@ __device__ __forceinline__ void write_splat(const PrepArgs &a, int64_t pos, int 
     tile_rect(geo.mx, geo.my, geo.radius, a.tiles_x, a.tiles_y, rect);
     a.rects[pos] = make_ushort4((unsigned short)rect[0], (unsigned short)rect[1], (unsigned short)rect[2],
                                 (unsigned short)rect[3]);
+    // The tiles whose pixel centres the support {d2 <= 9} can reach: its bounding box mean +- (hx, hy)
+    // (BlendGeo, float, widened far beyond its rounding), intersected with the reference rectangle
+    // (3 sqrt(lambda_max) circle, renderer.py:83-86, which contains the ellipse). The reference's
+    // tile lists hold the other tiles of the rectangle too, but no pixel there passes d2 <= 9, so the
+    // blend and the exact walks skip them; the harness CSR views still report the reference lists.
+    int t0 = rect[0], t1 = rect[1], t2 = rect[2], t3 = rect[3];
+    if (bg.hx < 1e30f && bg.hy < 1e30f) {
+        const double ex = (double)bg.hx * (1.0 + 1e-5) + 1e-3, ey = (double)bg.hy * (1.0 + 1e-5) + 1e-3;
+        // pixel p has its centre p + 0.5 inside [m - e, m + e] iff p in [m - e - 0.5, m + e - 0.5]
+        t0 = max(t0, (int)floor((geo.mx - ex - 0.5) / kTile));
+        t1 = min(t1, (int)floor((geo.mx + ex - 0.5) / kTile));
+        t2 = max(t2, (int)floor((geo.my - ey - 0.5) / kTile));
+        t3 = min(t3, (int)floor((geo.my + ey - 0.5) / kTile));
+    }
+    a.rects_tight[pos] = t0 <= t1 && t2 <= t3 ? make_ushort4((unsigned short)t0, (unsigned short)t1, (unsigned short)t2,
+                                                             (unsigned short)t3)
+                                              : make_ushort4(0xffff, 0, 0xffff, 0);  // reaches no pixel
 }
 
 // ------------------------------------------------------------------------------- scene
