@@ -160,50 +160,20 @@ __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1
     const double U1 = fma(e1x, cx, fma(e1y, cy, -p1));
     const double U2 = fma(-e1y, cx, fma(e1x, cy, -p2));
     const float l1 = gl.x, l2 = gl.y;
-    // the axes pre-scaled by sqrt(l_k log2(e) / 2) (float64 products, rounded once):
-    // h = v1^2 + v2^2 = d2 log2(e) / 2, the exp argument itself; every float error of d2 scales by
-    // the same factor, so the d2 bounds below carry over with thresholds and ka scaled
-    const double sl1 = sqrt((double)l1) * kSqrtHalfLog2e, sl2 = sqrt((double)fmaxf(l2, 0.0f)) * kSqrtHalfLog2e;
-    f.a1x = (float)(sl1 * e1x);
-    f.a1y = (float)(sl1 * e1y);
-    f.V1 = (float)(sl1 * U1);
-    f.c2x = (float)(-sl2 * e1y);
-    f.c2y = (float)(sl2 * e1x);
-    f.V2 = (float)(sl2 * U2);
     const float fU1 = (float)U1, fU2 = (float)U2, fe1x = (float)e1x, fe1y = (float)e1y;
-    f.alpha = gl.z;
-    f.z = gl.w;
-    float rgb[3];
-    unpack_rgb21(((unsigned long long)__float_as_uint(gr.y) << 32) | __float_as_uint(gr.x), rgb);
-    f.r = rgb[0];
-    f.g = rgb[1];
-    f.b = rgb[2];
-    f.pad = 0.0f;
     const float u = 5.9604644775390625e-08f;  // 2^-24
     const float aU1 = fabsf(fU1), aU2 = fabsf(fU2);
     bool ok = l2 > 0.0f;
-    float r1v = 0.0f, r2v = 0.0f;
+    float r1v = 0.0f, r2v = 0.0f, sig = 0.0f, kap = 0.0f, e9 = 0.0f;
     if (ok) {
         const float r1 = rsqrtf(l1), r2 = rsqrtf(l2);
         r1v = r1;
         r2v = r2;
         const float s1 = 2.0f * aU1 + 21.3f + 3.02f * r1, s2 = 2.0f * aU2 + 21.3f + 3.02f * r2;
-        const float sig = (l1 * r1) * s1 + (l2 * r2) * s2;
-        const float kap = 9.0e-15f * fminf(l1 / l2, 1e30f);
-        const float e9 = 1.01f * (1.5f * (2.0f * u * 3.0166f * sig + 7.0f * u * 9.1f) + kap);
+        sig = (l1 * r1) * s1 + (l2 * r2) * s2;
+        kap = 9.0e-15f * fminf(l1 / l2, 1e30f);
+        e9 = 1.01f * (1.5f * (2.0f * u * 3.0166f * sig + 7.0f * u * 9.1f) + kap);
         ok = e9 < 0.5f;
-        // k (9 -/+ e9) in h units, widened by 1e-6 for the float k and the products' roundings
-        const float kf = (float)kHalfLog2e;
-        f.thr_in = __fmaf_rn(-kf, e9, kf * 9.0f) - 1.0e-6f;
-        f.thr_out = __fmaf_rn(kf, e9, kf * 9.0f) + 1.0e-6f;
-        f.ka = 1.4003f * (0.75f * u * sig + 5.25f * u);  // 1.01 / k: eps = ka d2 + kb = ka' h + kb
-        f.kb = 1.01f * (0.75f * u * sig + kEpsExp + 0.5f * kap);
-    }
-    if (!ok) {  // every pixel that is not certainly outside takes the float64 test
-        f.thr_in = -1.0f;
-        f.thr_out = 3.0e38f;
-        f.ka = 0.0f;
-        f.kb = kEpsExact;
     }
     // mean - tile origin, from the principal-axis offsets (float error ~ 2u (|U1| + |U2|))
     const float mx = 8.0f - (fU1 * fe1x - fU2 * fe1y), my = 8.0f - (fU1 * fe1y + fU2 * fe1x);
@@ -240,6 +210,38 @@ __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1
                 fabsf(v1c - v2c) * 0.70710678f - hwm > slack)
                 m &= ~(1u << w);
         }
+    }
+    if (!m) return 0u;  // reaches none of the CTA's warp blocks: the record is never read
+    // the axes pre-scaled by sqrt(l_k log2(e) / 2) (float64 products, rounded once):
+    // h = v1^2 + v2^2 = d2 log2(e) / 2, the exp argument itself; every float error of d2 scales by
+    // the same factor, so the d2 bounds carry over with thresholds and ka scaled
+    const double sl1 = sqrt((double)l1) * kSqrtHalfLog2e, sl2 = sqrt((double)fmaxf(l2, 0.0f)) * kSqrtHalfLog2e;
+    f.a1x = (float)(sl1 * e1x);
+    f.a1y = (float)(sl1 * e1y);
+    f.V1 = (float)(sl1 * U1);
+    f.c2x = (float)(-sl2 * e1y);
+    f.c2y = (float)(sl2 * e1x);
+    f.V2 = (float)(sl2 * U2);
+    f.alpha = gl.z;
+    f.z = gl.w;
+    float rgb[3];
+    unpack_rgb21(((unsigned long long)__float_as_uint(gr.y) << 32) | __float_as_uint(gr.x), rgb);
+    f.r = rgb[0];
+    f.g = rgb[1];
+    f.b = rgb[2];
+    f.pad = 0.0f;
+    if (ok) {
+        // k (9 -/+ e9) in h units, widened by 1e-6 for the float k and the products' roundings
+        const float kf = (float)kHalfLog2e;
+        f.thr_in = __fmaf_rn(-kf, e9, kf * 9.0f) - 1.0e-6f;
+        f.thr_out = __fmaf_rn(kf, e9, kf * 9.0f) + 1.0e-6f;
+        f.ka = 1.4003f * (0.75f * u * sig + 5.25f * u);  // 1.01 / k: eps = ka d2 + kb = ka' h + kb
+        f.kb = 1.01f * (0.75f * u * sig + kEpsExp + 0.5f * kap);
+    } else {  // every pixel that is not certainly outside takes the float64 test
+        f.thr_in = -1.0f;
+        f.thr_out = 3.0e38f;
+        f.ka = 0.0f;
+        f.kb = kEpsExact;
     }
     return m;
 }
@@ -385,7 +387,7 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
             unsigned msk = tile_entry(ge.x, ge.y, gp.x, gp.y, gl, gr, x0 + 8.0, y0 + 8.0, f);
             if (kBound && !kPixBound && msk)  // eps at the support edge bounds eps inside it
                 atomicMax(&s_epsmax, __float_as_uint(__fmaf_rn(f.ka, fminf(f.thr_out, 7.0f), f.kb)));
-            s_f[threadIdx.x] = f;
+            if (msk) s_f[threadIdx.x] = f;  // an entry no warp walks is never read
             s_slot[threadIdx.x] = rid;
             s_mask[threadIdx.x] = (uint8_t)msk;
         }
