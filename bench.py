@@ -37,8 +37,8 @@ STAGES = ("pose", "count", "scan", "emit", "depth_sort", "permute", "pair_scan",
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
-    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--steps", type=int, default=30)
+    p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--envs", type=int, default=64, help="environments per GPU")
     p.add_argument("--gaussians", type=int, default=1_000_000)

@@ -60,7 +60,7 @@ class HostPipeline:
     synchronously, with any render queued after it.
 
     submit(cameras, sim_times) -> slot index; the frames of a slot are valid in host[slot] after
-    wait(slot) (or after the slot is reused two submits later, which waits for it)."""
+    wait(slot), until the slot is reused two submits later."""
 
     KEYS = ("color", "alpha", "depth")
 
@@ -86,9 +86,11 @@ class HostPipeline:
     def submit(self, cameras, sim_times=None):
         slot = self.i % len(self.host)
         self.i += 1
-        if self.done[slot] is not None:
-            self.done[slot].synchronize()  # host buffer of this slot is free again
         with torch.cuda.stream(self.render_stream):
+            if self.done[slot] is not None:
+                # the render overwrites this slot's device frames once their download (two submits
+                # back) is done: a device-side wait, so the host keeps queueing ahead of the GPU
+                self.render_stream.wait_event(self.done[slot])
             out = self.r.render(cameras, sim_times, out=dict(self.dev[slot]), wait=False)
             ready = torch.cuda.Event()
             ready.record(self.render_stream)

@@ -5,7 +5,7 @@ set -u
 mkdir -p gpurun_out
 timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-B="python bench.py --steps 10 --warmup 3"
+B="python bench.py"
 timeout 900 $B > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 if [ "${SKIP_NCU:-0}" = "0" ]; then
   L="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
