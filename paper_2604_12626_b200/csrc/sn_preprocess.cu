@@ -33,6 +33,9 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef SN_AVATAR_ENV_GROUP
 #define SN_AVATAR_ENV_GROUP 8  // envs whose pose blocks the avatar count kernel stages per barrier pair
 #endif
+#ifndef SN_AVATAR_COUNT_MIN_BLOCKS
+#define SN_AVATAR_COUNT_MIN_BLOCKS 4
+#endif
 #ifndef SN_AVATAR_MIN_BLOCKS
 #define SN_AVATAR_MIN_BLOCKS 3
 #endif
@@ -424,7 +427,7 @@ __device__ __forceinline__ bool avatar_on(const PrepArgs &a, int n_avatars, int 
 __host__ __device__ __forceinline__ int pose_block_doubles(int J) { return 16 * J + 12; }
 
 // Pose blocks are staged for `group` envs per barrier pair (group x 2 blocks in shared memory).
-__global__ void __launch_bounds__(kBlock, SN_AVATAR_MIN_BLOCKS) avatar_count_kernel(sn_avatars av, PoseView pv, PrepArgs a,
+__global__ void __launch_bounds__(kBlock, SN_AVATAR_COUNT_MIN_BLOCKS) avatar_count_kernel(sn_avatars av, PoseView pv, PrepArgs a,
                                                                                     int group) {
     __shared__ unsigned s_cnt[kMaxEnvChunk][5];
     extern __shared__ double s_pose[];  // group x 2 x (J*12 joint mats | J*4 quats | 12 root)
