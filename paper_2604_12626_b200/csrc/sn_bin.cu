@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kBlock) duplicate_kernel(BinArgs b) {
         uint32_t tx = r.x + local % span, ty = r.z + local / span;
         uint32_t tile = ty * (uint32_t)b.tiles_x + tx;
         b.pair_keys[gk] = (s_env[lo] << b.tile_bits) | tile;
-        b.pair_vals[gk] = (uint32_t)(i0 + lo);
+        b.pair_vals[gk] = b.vals_sorted[i0 + lo];  // the record slot: the blend gathers it directly
     }
 }
 

@@ -266,7 +266,8 @@ __device__ __forceinline__ void push_fixup(const BlendArgs &b, bool flag, uint32
 //           the splats whose rectangle covers this tile into a shared-memory queue. The walk
 //           stops with the early-termination vote, so a saturated tile never looks at the rest
 //           of the env -- no pair duplication, no sort, no per-pair HBM traffic.
-// SOURCE 1: a materialized tile list (ranges + pair_vals from the radix binner).
+// SOURCE 1: a materialized tile list (ranges + pair_vals from the radix binner; the values are
+//           record slots, in depth order).
 // SOURCE 2: rasterize_reference -- every splat of the env, in depth order.
 #ifndef SN_BLEND_MIN_BLOCKS
 #define SN_BLEND_MIN_BLOCKS 4
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
     constexpr bool kPixBound = MODE == 2;
     __shared__ unsigned s_epsmax;
     __shared__ FRec s_f[kBlock];
-    __shared__ uint32_t s_slot[kBlock];  // depth-sorted index (the exact fallback reads the SplatRec)
+    __shared__ uint32_t s_slot[kBlock];  // record slot (the boundary band reads its SplatRec)
     __shared__ uint32_t s_queue[2 * kBlock];
     __shared__ uint32_t s_wsum[kBlock / 32];
     __shared__ uint8_t s_mask[kBlock];  // bit w: the splat's support may reach warp w's 8 x 4 block
@@ -377,9 +378,10 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
         if (n <= 0) break;
         loaded += n;
         if (threadIdx.x < n) {
-            uint32_t rid = SOURCE == 0 ? s_queue[threadIdx.x]
-                                       : (SOURCE == 1 ? __ldg(v.pair_vals + cursor + threadIdx.x) : cursor + threadIdx.x);
-            const double2 *src = reinterpret_cast<const double2 *>(v.geo + __ldg(v.order + rid));
+            // the record slot: tile lists hold slots; streamed / all-splat sources map depth ranks
+            const uint32_t rid = SOURCE == 1 ? __ldg(v.pair_vals + cursor + threadIdx.x)
+                                             : __ldg(v.order + (SOURCE == 0 ? s_queue[threadIdx.x] : cursor + threadIdx.x));
+            const double2 *src = reinterpret_cast<const double2 *>(v.geo + rid);
             const double2 ge = __ldg(src), gp = __ldg(src + 1);
             const float4 gl = __ldg(reinterpret_cast<const float4 *>(src + 2));
             const float4 gr = __ldg(reinterpret_cast<const float4 *>(src + 3));
@@ -421,7 +423,7 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
                     eps = __fmaf_rn(d2, s.ka, s.kb);
                 } else {  // boundary band: the reference's float64 test (_kernels_cy.pyx:73-75)
                     PROF(1, 1);
-                    const SplatRec &sd = v.recs[v.order[s_slot[j]]];
+                    const SplatRec &sd = v.recs[s_slot[j]];
                     const double ddx = sd.mx - px, ddy = sd.my - py;
                     const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
                     if (d2d > kSupportD2) continue;
@@ -699,7 +701,7 @@ __device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_
             contrib[i] = false;
             e[i] = QEntry{};
             if (cand[i]) {
-                const SplatRec &s = v.recs[__ldg(v.order + rid[i])];
+                const SplatRec &s = v.recs[v.source == 1 ? rid[i] : __ldg(v.order + rid[i])];
                 const double dx = s.mx - px, dy = s.my - py;
                 const double d2 = (s.ca * dx * dx + s.cb2 * dx * dy) + s.cc * dy * dy;
                 if (!(d2 > kSupportD2)) {
@@ -843,7 +845,7 @@ __device__ ExactPixel exact_walk_cta(const PassView &v, int el, int tile, int ti
                 if (v.source == 0) cand = covers(__ldg(v.rects + k), tx, ty);
                 else if (v.source == 1) rid = __ldg(v.pair_vals + k);
                 if (cand) {
-                    const SplatRec &sr = v.recs[__ldg(v.order + rid)];
+                    const SplatRec &sr = v.recs[v.source == 1 ? rid : __ldg(v.order + rid)];
                     const double dx = sr.mx - px, dy = sr.my - py;
                     const double d2 = (sr.ca * dx * dx + sr.cb2 * dx * dy) + sr.cc * dy * dy;
                     if (!(d2 > kSupportD2)) {
