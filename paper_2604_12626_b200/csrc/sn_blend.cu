@@ -89,6 +89,10 @@ constexpr float kU125 = 7.5e-8f;       // 1.25 u: the one rounding of T' = fma(-
 constexpr float kTLo = 9.99999e-05f;   // 1e-4 (1 - 1e-6): below it (with the bound) T < 1e-4 for sure
 constexpr float kTHi = 1.000001e-04f;  // 1e-4 (1 + 1e-6)
 constexpr float kNegHalfLog2e = -0.72134752044448170f;
+#ifndef SN_WALK_UNROLL
+#define SN_WALK_UNROLL 2
+#endif
+constexpr int kWalkUnroll = SN_WALK_UNROLL;  // walk loop unroll (entries per iteration)
 // the blend works on h = d2 log2(e) / 2 (so e^(-d2/2) = 2^-h): its axes carry sqrt(log2(e) / 2)
 constexpr double kHalfLog2e = 0.72134752044448170;
 constexpr double kSqrtHalfLog2e = 0.84932180028801904272;
@@ -406,7 +410,7 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
         __syncwarp();
         for (int k0 = 0; k0 < cnt && !__all_sync(kFull, dead != 0.0f); k0 += 32) {
             const int k1 = min(cnt, k0 + 32);
-#pragma unroll 2
+#pragma unroll kWalkUnroll
             for (int k = k0; k < k1; ++k) {
                 const int j = s_wl[warp][k];
                 PROF(0, lane == 0);
