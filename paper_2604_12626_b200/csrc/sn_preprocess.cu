@@ -99,6 +99,16 @@ __device__ __forceinline__ void init_counts(unsigned (*s_cnt)[5], int ec) {
     __syncthreads();
 }
 
+// The chunk's cameras into shared memory (read per (gaussian, env) item: broadcasts instead of
+// L1 round trips). Callers synchronize before use.
+__device__ __forceinline__ void stage_cams(const PrepArgs &a, sn_camera *s_cam) {
+    static_assert(sizeof(sn_camera) % sizeof(double) == 0, "sn_camera is copied as doubles");
+    const double *src = reinterpret_cast<const double *>(a.cams + a.e0);
+    double *dst = reinterpret_cast<double *>(s_cam);
+    const int nd = a.ec * (int)(sizeof(sn_camera) / sizeof(double));
+    for (int i = threadIdx.x; i < nd; i += blockDim.x) dst[i] = __ldg(src + i);
+}
+
 // Per-warp exclusive offsets for each env of the chunk; returns via s_woff.
 __device__ __forceinline__ void warp_offsets(uint64_t mask, int ec, unsigned (*s_woff)[kBlock / 32]) {
     int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -212,7 +222,9 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
     __shared__ double s_geo[kBlock][9];  // position (3), cov3d (6)
     __shared__ unsigned long long s_vis[kBlock];
     __shared__ uint16_t s_q[kBlock / 32][32 * kEmitRound];
-    init_counts(s_cnt, a.ec);
+    __shared__ sn_camera s_cam[kMaxEnvChunk];
+    stage_cams(a, s_cam);
+    init_counts(s_cnt, a.ec);  // (synchronizes)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     bool valid = g < c.n;
@@ -234,7 +246,7 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
     for (int e = 0; e < a.ec; ++e) {
         bool in = false;
         if (valid) {
-            const sn_camera &cam = a.cams[a.e0 + e];
+            const sn_camera &cam = s_cam[e];
             double z = cam_z(p, cam);
             in = (z > cam.near_) && (z < cam.far_);
         }
@@ -259,7 +271,7 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
             const double pp[3] = {d[0], d[1], d[2]};
             const double cov[6] = {d[3], d[4], d[5], d[6], d[7], d[8]};
             Geo geo;
-            const int code = project_geo(pp, cov, a.cams[a.e0 + e], geo);
+            const int code = project_geo(pp, cov, s_cam[e], geo);
             // field: 2 frame, 3 degenerate, 4 drawn (sn_stats order)
             const int field = code == kKeep ? 4 : (code == kDegenerate ? 3 : 2);
             tally_item(s_cnt, active, e, field);
@@ -278,10 +290,12 @@ __global__ void __launch_bounds__(kBlock, SN_EMIT_MIN_BLOCKS) scene_emit_kernel(
     __shared__ unsigned s_woff[kMaxEnvChunk][kBlock / 32];
     __shared__ double s_geo[kBlock][10];  // position (3), cov3d (6), alpha
     __shared__ uint16_t s_q[kBlock / 32][32 * kEmitRound];
+    __shared__ sn_camera s_cam[kMaxEnvChunk];
+    stage_cams(a, s_cam);
     int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     bool valid = g < c.n;
     uint64_t mask = valid ? a.vismask[g] : 0ull;
-    warp_offsets(mask, a.ec, s_woff);
+    warp_offsets(mask, a.ec, s_woff);  // (synchronizes)
     if (!__any_sync(kFull, mask != 0)) return;
     const int warp = threadIdx.x >> 5;
     if (mask) {
@@ -308,7 +322,7 @@ __global__ void __launch_bounds__(kBlock, SN_EMIT_MIN_BLOCKS) scene_emit_kernel(
             const double cov[6] = {d[3], d[4], d[5], d[6], d[7], d[8]};
             const int64_t pos =
                 (int64_t)a.env_off[e] + a.blk_counts[(int64_t)e * a.n_blocks + blockIdx.x] + s_woff[e][warp] + rank;
-            const sn_camera &cam = a.cams[a.e0 + e];
+            const sn_camera &cam = s_cam[e];
             Geo geo;
             project_geo(p, cov, cam, geo);
             float dir[3], rgb[3];
