@@ -444,8 +444,10 @@ __host__ __device__ __forceinline__ int pose_block_doubles(int J) { return 16 * 
 __global__ void __launch_bounds__(kBlock, SN_AVATAR_COUNT_MIN_BLOCKS) avatar_count_kernel(sn_avatars av, PoseView pv, PrepArgs a,
                                                                                     int group) {
     __shared__ unsigned s_cnt[kMaxEnvChunk][5];
+    __shared__ sn_camera s_cam[kMaxEnvChunk];
     extern __shared__ double s_pose[];  // group x 2 x (J*12 joint mats | J*4 quats | 12 root)
-    init_counts(s_cnt, a.ec);
+    stage_cams(a, s_cam);
+    init_counts(s_cnt, a.ec);  // (synchronizes)
     int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     bool valid = g < av.n;
     int avatar = valid ? av.avatar_of[g] : 0;
@@ -500,7 +502,7 @@ __global__ void __launch_bounds__(kBlock, SN_AVATAR_COUNT_MIN_BLOCKS) avatar_cou
                 skin_one<false, false>(av, g, blk, blk + 12 * J, blk + 16 * J, p, q);
             else
                 skin_one<true, false>(av, g, jm, eq, root, p, q);
-            const sn_camera &cam = a.cams[env];
+            const sn_camera &cam = s_cam[env - a.e0];
             double z = cam_z(p, cam);
             if (!((z > cam.near_) && (z < cam.far_))) {
                 code = kCullDepth;
@@ -525,6 +527,8 @@ __global__ void __launch_bounds__(kBlock, SN_AVATAR_COUNT_MIN_BLOCKS) avatar_cou
 __global__ void __launch_bounds__(kBlock, SN_AVATAR_MIN_BLOCKS) avatar_emit_kernel(sn_avatars av, PoseView pv, PrepArgs a) {
     __shared__ unsigned s_woff[kMaxEnvChunk][kBlock / 32];
     __shared__ uint16_t s_q[kBlock / 32][32 * kEmitRound];
+    __shared__ sn_camera s_cam[kMaxEnvChunk];
+    stage_cams(a, s_cam);
     int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     bool valid = g < av.n;
     uint64_t mask = valid ? a.vismask[g] : 0ull;
@@ -549,7 +553,7 @@ __global__ void __launch_bounds__(kBlock, SN_AVATAR_MIN_BLOCKS) avatar_emit_kern
             skin_one(av, gi, jm, eq, root, p, qr);
             load4<double>(av.log_scales + 4 * gi, ls);
             build_cov3d(ls, qr, cov);
-            const sn_camera &cam = a.cams[env];
+            const sn_camera &cam = s_cam[env - a.e0];
             Geo geo;
             project_geo(p, cov, cam, geo);
             float dir[3], rgb[3];
@@ -648,7 +652,13 @@ cudaError_t launch_avatar_count(const sn_avatars &av, const PoseView &pv, const 
     const size_t blk = sizeof(double) * 2 * (size_t)pose_block_doubles(pv.n_joints);
     const int group = (int)std::max<size_t>(1, std::min<size_t>(SN_AVATAR_ENV_GROUP, (40 * 1024) / blk));
     const size_t smem = blk * group;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(avatar_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // dynamic + static (cameras, counters) may pass the default 48 KB: opt in to the dynamic size
+    static size_t opted = 0;
+    if (smem > opted) {
+        cudaError_t e = cudaFuncSetAttribute(avatar_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        opted = smem;
+    }
     avatar_count_kernel<<<a.n_blocks, kBlock, smem, s>>>(av, pv, a, group);
     return cudaGetLastError();
 }
