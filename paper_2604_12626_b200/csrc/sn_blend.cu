@@ -467,8 +467,11 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
     float cr, cg, cb, D;
     unpack2(crg, cr, cg);
     unpack2(cbd, cb, D);
-    // the cutoff fired (T - err <= 1e-4 (1 + 1e-6)) but T < 1e-4 is not certain: float64 fixup
-    const bool amb = inside && (b.force_exact || (T - err <= kTHi && !(T + err < kTLo)));
+    // the cutoff fired (T - err <= 1e-4 (1 + 1e-6)) but T < 1e-4 is not certain: float64 fixup.
+    // Also when err > T / 16: the 0.25 u T' margin in kU125 covers the bound's own float roundings
+    // (<= 2u err per step) only while err <= T / 8, and err / T never decreases along the walk.
+    const bool cut = T - err <= kTHi;
+    const bool amb = inside && (b.force_exact || (cut && (!(T + err < kTLo) || err > 0.0625f * T)));
     PROF(2, amb);
 #ifdef SN_BLEND_PROF
     if (SOURCE == 0 && MODE == 0 && threadIdx.x == 0) {
