@@ -31,6 +31,7 @@
 #include "sn_internal.h"
 
 #include <cstring>
+#include <type_traits>
 
 #ifdef SN_BLEND_PROF
 __device__ unsigned long long g_blend_prof[16];
@@ -286,13 +287,18 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
     // the scene pass uses the CTA's largest bound over every gathered splat -- looser, one
     // instruction less per contribution
     constexpr bool kPixBound = MODE == 2;
+    // records per batch: tile lists (the avatar layer) take 2 per thread -- their warps' walks are
+    // very uneven (small splats in a few blocks), and fewer, larger batches wait less at barriers
+    constexpr int kPerT = SOURCE == 1 ? 2 : 1;
+    constexpr int kBatch = kBlock * kPerT;
+    using WlIndex = typename std::conditional<(kBatch > 256), uint16_t, uint8_t>::type;
     __shared__ unsigned s_epsmax;
-    __shared__ FRec s_f[kBlock];
-    __shared__ uint32_t s_slot[kBlock];  // record slot (the boundary band reads its SplatRec)
-    __shared__ uint32_t s_queue[2 * kBlock];
+    __shared__ FRec s_f[kBatch];
+    __shared__ uint32_t s_slot[kBatch];  // record slot (the boundary band reads its SplatRec)
+    __shared__ uint32_t s_queue[SOURCE == 0 ? 2 * kBlock : 1];
     __shared__ uint32_t s_wsum[kBlock / 32];
-    __shared__ uint8_t s_mask[kBlock];  // bit w: the splat's support may reach warp w's 8 x 4 block
-    __shared__ uint8_t s_wl[kBlock / 32][kBlock];  // per warp: its batch entries, in depth order
+    __shared__ uint8_t s_mask[kBatch];  // bit w: the splat's support may reach warp w's 8 x 4 block
+    __shared__ WlIndex s_wl[kBlock / 32][kBatch];  // per warp: its batch entries, in depth order
     const PassView &v = b.pv;
     if (pass_overflow(v)) return;
     if (threadIdx.x == 0) s_epsmax = __float_as_uint(kEpsExact);
@@ -377,14 +383,17 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
             }
             n = min(q_len, kBlock);
         } else {
-            n = (int)min((uint32_t)kBlock, s1 - cursor);
+            n = (int)min((uint32_t)kBatch, s1 - cursor);
         }
         if (n <= 0) break;
         loaded += n;
-        if (threadIdx.x < n) {
+#pragma unroll
+        for (int r = 0; r < kPerT; ++r) {
+            const int jt = threadIdx.x + r * kBlock;
+            if (jt >= n) break;
             // the record slot: tile lists hold slots; streamed / all-splat sources map depth ranks
-            const uint32_t rid = SOURCE == 1 ? __ldg(v.pair_vals + cursor + threadIdx.x)
-                                             : __ldg(v.order + (SOURCE == 0 ? s_queue[threadIdx.x] : cursor + threadIdx.x));
+            const uint32_t rid = SOURCE == 1 ? __ldg(v.pair_vals + cursor + jt)
+                                             : __ldg(v.order + (SOURCE == 0 ? s_queue[jt] : cursor + jt));
             const double2 *src = reinterpret_cast<const double2 *>(v.geo + rid);
             const double2 ge = __ldg(src), gp = __ldg(src + 1);
             const float4 gl = __ldg(reinterpret_cast<const float4 *>(src + 2));
@@ -393,9 +402,9 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
             unsigned msk = tile_entry(ge.x, ge.y, gp.x, gp.y, gl, gr, x0 + 8.0, y0 + 8.0, f);
             if (kBound && !kPixBound && msk)  // eps at the support edge bounds eps inside it
                 atomicMax(&s_epsmax, __float_as_uint(__fmaf_rn(f.ka, fminf(f.thr_out, 7.0f), f.kb)));
-            if (msk) s_f[threadIdx.x] = f;  // an entry no warp walks is never read
-            s_slot[threadIdx.x] = rid;
-            s_mask[threadIdx.x] = (uint8_t)msk;
+            if (msk) s_f[jt] = f;  // an entry no warp walks is never read
+            s_slot[jt] = rid;
+            s_mask[jt] = (uint8_t)msk;
         }
         __syncthreads();
         // each warp walks only the batch entries whose support can reach its 8 x 4 pixel block,
@@ -404,7 +413,7 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
         for (int j0 = 0; j0 < n; j0 += 32) {
             const bool mine = j0 + lane < n && ((s_mask[j0 + lane] >> warp) & 1u);
             const unsigned bal = __ballot_sync(kFull, mine);
-            if (mine) s_wl[warp][cnt + __popc(bal & ((1u << lane) - 1u))] = (uint8_t)(j0 + lane);
+            if (mine) s_wl[warp][cnt + __popc(bal & ((1u << lane) - 1u))] = (WlIndex)(j0 + lane);
             cnt += __popc(bal);
         }
         __syncwarp();
