@@ -289,13 +289,16 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
     constexpr bool kPixBound = MODE == 2;
     // records per batch: tile lists (the avatar layer) take 2 per thread -- their warps' walks are
     // very uneven (small splats in a few blocks), and fewer, larger batches wait less at barriers
-    constexpr int kPerT = SOURCE == 1 ? 2 : 1;
+#ifndef SN_STREAM_PER_THREAD
+#define SN_STREAM_PER_THREAD 1
+#endif
+    constexpr int kPerT = SOURCE == 1 ? 2 : (SOURCE == 0 ? SN_STREAM_PER_THREAD : 1);
     constexpr int kBatch = kBlock * kPerT;
     using WlIndex = typename std::conditional<(kBatch > 256), uint16_t, uint8_t>::type;
     __shared__ unsigned s_epsmax;
     __shared__ FRec s_f[kBatch];
     __shared__ uint32_t s_slot[kBatch];  // record slot (the boundary band reads its SplatRec)
-    __shared__ uint32_t s_queue[SOURCE == 0 ? 2 * kBlock : 1];
+    __shared__ uint32_t s_queue[SOURCE == 0 ? kBatch + kBlock : 1];
     __shared__ uint32_t s_wsum[kBlock / 32];
     __shared__ uint8_t s_mask[kBatch];  // bit w: the splat's support may reach warp w's 8 x 4 block
     __shared__ WlIndex s_wl[kBlock / 32][kBatch];  // per warp: its batch entries, in depth order
@@ -350,7 +353,7 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
         if (__syncthreads_count(dead == 0.0f) == 0) break;  // also guards s_f / s_queue reuse
         int n;
         if (SOURCE == 0) {
-            while (q_len < kBlock && cursor < s1) {
+            while (q_len < kBatch && cursor < s1) {
                 // hierarchical cull (uniform across the CTA, no barrier on the skip path):
                 // 8192-splat super-batches, then 256-splat batches, by their union rectangles
                 const uint32_t bi = cursor / kBlock;
@@ -381,7 +384,7 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
                 cursor = b_end;
                 __syncthreads();
             }
-            n = min(q_len, kBlock);
+            n = min(q_len, kBatch);
         } else {
             n = (int)min((uint32_t)kBatch, s1 - cursor);
         }
