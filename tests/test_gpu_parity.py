@@ -557,3 +557,25 @@ def test_async_render_pipeline_matches_sync_and_retries():
                 assert torch.equal(pipe.host[i % 2][k], want[i][k].cpu()), (k, i)
         if renderer is fresh:
             assert renderer.context.render_retries() > r0
+
+
+@pytest.mark.parametrize("seed", [101, 202, 303])
+def test_random_scale_spread_against_oracle(seed):
+    """Seeded scenes with a wide spread of scales and opacities (tiny to frame-filling splats, needle
+    and disc shapes) and small frames, near 0.1 and 0.01: the tight rectangles, the warp-block
+    separating axes and the float32 chain must leave every discrete output equal to the oracle's."""
+    box = S.room_box(1_000_000)
+    scene = S.make_scene(20_000, box[0], box[1], seed=seed)
+    rng = np.random.default_rng(seed + 1)
+    scene.log_scales = rng.normal(-3.0, 1.5, scene.log_scales.shape).astype(np.float32)
+    scene.opacities = rng.normal(0.5, 2.0, scene.opacities.shape).astype(np.float32)
+    for near in (0.1, 0.01):
+        cams = S.room_cameras(3, box, seed=seed + 2, width=96, height=80, near=near)
+        bg = np.array([0.2, 0.5, 0.8])
+        out = R().render_frames(scene, cams, bg, contrib=True)
+        for e in range(3):
+            o = _oracle_check_env(out, e, scene, cams[e], bg)
+            check_frame(out["color"][e].cpu().numpy(), out["alpha"][e].cpu().numpy(), out["depth"][e].cpu().numpy(),
+                        o.color, o.alpha, o.depth, cams[e].far)
+            assert out["stats"][e].tolist() == [o.stats[k] for k in ("n_input", "n_culled_depth", "n_culled_frame",
+                                                                     "n_degenerate", "n_drawn")]
