@@ -371,9 +371,12 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
                 SN_CUDA(launch_duplicate(b, st));
                 tm.end();
                 tm.begin(SN_STAGE_BIN_SCATTER);
+                // duplicate emits pairs env-major and, within an env, in depth order, so a stable sort on
+                // the tile bits alone leaves every (tile, env) group contiguous and depth-ordered; the env
+                // bits never need a radix pass.
                 const bool in_b = radix_sort_pairs(w.temp.p, w.pkeys_a.as<uint32_t>(), w.pvals_a.as<uint32_t>(),
                                                    w.pkeys_b.as<uint32_t>(), w.pvals_b.as<uint32_t>(),
-                                                   b.d_npairs, cap_p, env_bits + tile_bits, st, &ctx->launches);
+                                                   b.d_npairs, cap_p, tile_bits, st, &ctx->launches);
                 SN_CUDA(cudaGetLastError());
                 if (!in_b) {
                     std::swap(w.pkeys_a, w.pkeys_b);
