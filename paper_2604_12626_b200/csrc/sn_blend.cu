@@ -420,6 +420,9 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
             cnt += __popc(bal);
         }
         __syncwarp();
+        // a lower bound on the pixel's first contribution depth, once per batch instead of per
+        // contribution: the warp's entries arrive in depth order, so its first one is the nearest
+        if (kBound && cnt > 0) z_first = fminf(z_first, s_f[s_wl[warp][0]].z);
         for (int k0 = 0; k0 < cnt && !__all_sync(kFull, dead != 0.0f); k0 += 32) {
             const int k1 = min(cnt, k0 + 32);
 #pragma unroll kWalkUnroll
@@ -434,9 +437,10 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
                 // + dead: exact (v2^2 + 0 rounds like v2 * v2), or +inf for a finished pixel
                 float d2 = __fmaf_rn(v1, v1, __fmaf_rn(v2, v2, dead));
                 if (d2 > q1.z) continue;  // saturated (dead = inf), or certainly outside the support
+                const float4 q2 = *reinterpret_cast<const float4 *>(&s.ka);  // (ka, kb, alpha, -): one load
                 float eps;
                 if (d2 < q1.w) {
-                    eps = __fmaf_rn(d2, s.ka, s.kb);
+                    eps = __fmaf_rn(d2, q2.x, q2.y);
                 } else {  // boundary band: the reference's float64 test (_kernels_cy.pyx:73-75)
                     PROF(1, 1);
                     const SplatRec &sd = v.recs[s_slot[j]];
@@ -447,7 +451,7 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
                     eps = kEpsExact;
                 }
                 const float e = ex2_approx(-d2);  // 2^-h: the negation is an operand modifier
-                const float a = fminf(s.alpha * e, 0.99f);
+                const float a = fminf(q2.z * e, 0.99f);
                 const float w = a * T;
                 const float Tn = __fmaf_rn(-a, T, T);  // T (1 - a), rounded once
                 const float4 q3 = *reinterpret_cast<const float4 *>(&s.r);
@@ -458,10 +462,7 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
                 T = Tn;
                 ++nc;
                 if (kPixBound) eps_max = fmaxf(eps_max, eps);
-                if (kBound) {  // splats arrive in depth order: z spans [first, last] contribution
-                    z_first = fminf(z_first, q3.w);
-                    z_last = q3.w;
-                }
+                if (kBound) z_last = fmaxf(z_last, q3.w);  // one op into a fixed register (a copy would be two)
                 // near the cutoff (_kernels_cy.pyx:65-66): stop; decided or deferred after the walk
                 if (Tn - err <= kTHi) dead = INFINITY;
             }
@@ -508,6 +509,7 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
     // depth = sum z w / sum w then errs by <= rho_w (z_last - z_first) from the weights (z spans the
     // contributions) plus (2n + 2) u from the float sums and the division; alpha by rho_w + (n + 1) u.
     if (!kPixBound) eps_max = __uint_as_float(s_epsmax);
+    if (nc == 0) z_first = 3.0e38f;  // no contribution: the empty range, as before any batch
     const float rho_w = err / T + eps_max + 6.0e-8f;
     const float alpha = fminf(A, 1.0f);
     const float depth = A > 0.0f ? D / A : (float)cam.far_;
