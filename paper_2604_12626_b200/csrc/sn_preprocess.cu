@@ -25,7 +25,7 @@ constexpr unsigned kFull = 0xffffffffu;
 
 // resident CTAs per SM the emit / avatar kernels are compiled for (register cap 65536 / (256 x N))
 #ifndef SN_EMIT_MIN_BLOCKS
-#define SN_EMIT_MIN_BLOCKS 4
+#define SN_EMIT_MIN_BLOCKS 3
 #endif
 #ifndef SN_COUNT_MIN_BLOCKS
 #define SN_COUNT_MIN_BLOCKS 4
