@@ -31,7 +31,7 @@ constexpr unsigned kFull = 0xffffffffu;
 #define SN_COUNT_MIN_BLOCKS 4
 #endif
 #ifndef SN_AVATAR_ENV_GROUP
-#define SN_AVATAR_ENV_GROUP 8  // envs whose pose blocks the avatar count kernel stages per barrier pair
+#define SN_AVATAR_ENV_GROUP 4  // envs whose pose blocks the avatar count kernel stages per barrier pair
 #endif
 #ifndef SN_AVATAR_COUNT_MIN_BLOCKS
 #define SN_AVATAR_COUNT_MIN_BLOCKS 4
