@@ -777,7 +777,10 @@ __device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_
 // source), the contributions are compacted in candidate order into a shared queue, and warp 0
 // consumes them 32 at a time exactly as exact_walk does -- same groups, bit-identical result.
 // Returns the reduced pixel in warp 0 (other warps' return values are unspecified).
-constexpr int kCtaPer = 4;
+#ifndef SN_FIXUP_CTA_PER
+#define SN_FIXUP_CTA_PER 4
+#endif
+constexpr int kCtaPer = SN_FIXUP_CTA_PER;
 constexpr int kCtaQueue = kCtaPer * kBlock + 32;
 __device__ ExactPixel exact_walk_cta(const PassView &v, int el, int tile, int tiles_x, int px_i, int py_i,
                                      const double *s_exp, QEntry *q, int *s_i) {

@@ -92,7 +92,10 @@ struct BinArgs {
     uint32_t *pair_vals;
     uint2 *ranges;           // (ec << tile_bits)
 };
-constexpr int kSuperBatch = 32;  // batches per super-batch (8192 splats)
+#ifndef SN_SUPER_BATCH
+#define SN_SUPER_BATCH 32
+#endif
+constexpr int kSuperBatch = SN_SUPER_BATCH;  // batches per super-batch (8192 splats)
 cudaError_t launch_permute(const BinArgs &b, cudaStream_t s);
 cudaError_t launch_depth_tie_fix(const BinArgs &b, cudaStream_t s);
 cudaError_t launch_super_rects(const BinArgs &b, ushort4 *super_rects, cudaStream_t s);

@@ -192,7 +192,14 @@ __device__ __forceinline__ void load_scene(const sn_cloud &c, int64_t g, double 
 // float64 projection + SH run with full lanes (a scene gaussian is visible in ~1/4 of the envs;
 // walking envs per lane would leave ~3/4 of the lanes idle). Item = lane | env << 5 | rank << 11,
 // rank = position among the warp's visible lanes for that env (order-preserving output slot).
-constexpr int kEmitRound = 8;
+#ifndef SN_EMIT_ROUND
+#define SN_EMIT_ROUND 16
+#endif
+#ifndef SN_COUNT_ROUND
+#define SN_COUNT_ROUND 8
+#endif
+constexpr int kEmitRound = SN_EMIT_ROUND;
+constexpr int kCountRound = SN_COUNT_ROUND;  // the count kernel's rounds (in-depth items)
 
 __device__ __forceinline__ int build_round(uint64_t mask, int e_begin, int e_end, uint16_t *q) {
     const int lane = threadIdx.x & 31;
@@ -221,7 +228,7 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
     __shared__ unsigned s_cnt[kMaxEnvChunk][5];
     __shared__ double s_geo[kBlock][9];  // position (3), cov3d (6)
     __shared__ unsigned long long s_vis[kBlock];
-    __shared__ uint16_t s_q[kBlock / 32][32 * kEmitRound];
+    __shared__ uint16_t s_q[kBlock / 32][32 * kCountRound];
     __shared__ sn_camera s_cam[kMaxEnvChunk];
     stage_cams(a, s_cam);
     init_counts(s_cnt, a.ec);  // (synchronizes)
@@ -259,8 +266,8 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
     }
     const int64_t g0 = (int64_t)blockIdx.x * kBlock + warp * 32;
     uint16_t *qq = s_q[warp];
-    for (int eb = 0; eb < a.ec; eb += kEmitRound) {
-        const int n = build_round(in_depth, eb, min(eb + kEmitRound, a.ec), qq);
+    for (int eb = 0; eb < a.ec; eb += kCountRound) {
+        const int n = build_round(in_depth, eb, min(eb + kCountRound, a.ec), qq);
         for (int k0 = 0; k0 < n; k0 += 32) {
             const int k = k0 + lane;
             const unsigned active = __ballot_sync(kFull, k < n);
