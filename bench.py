@@ -34,6 +34,15 @@ STAGES = ("pose", "count", "scan", "emit", "depth_sort", "permute", "pair_scan",
           "blend", "composite")
 
 
+
+def workload_config(args, parallelism):
+    """The `config` object both arms print (the GPU arm and `--impl reference` share it)."""
+    return {"workload": f"config2: {args.gaussians} scene gaussians + {args.avatars}x50k skinned avatars, "
+                        f"{args.envs} envs/GPU, {args.width}x{args.height}, near {args.near}",
+            "envs_per_gpu": args.envs, "n_gaussians": args.gaussians, "n_avatars": args.avatars,
+            "l2": "inputs larger than L2 (236 MB scene + per-step buffers), fresh cameras every step",
+            "parallelism": parallelism}
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -234,8 +243,7 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE config 2 distributions, seeded)",
         "impl": "reference",
-        "config": {"workload": f"config2: {args.gaussians} scene + {args.avatars}x50k avatars, "
-                               f"{args.width}x{args.height}, near {args.near}", "envs_per_step": n_sample},
+        "config": dict(workload_config(args, f"host threads x{threads}"), sample_envs_per_step=n_sample),
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "port",
                          "sample": r["sample"]},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -421,11 +429,7 @@ def main():
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64 geometry + exact decisions (f32 blend chain with error bounds, f64 fixups)", "data": "synthetic (seeded, BASELINE distributions)",
-        "config": {"workload": f"config2: {args.gaussians} scene gaussians + {args.avatars}x50k skinned avatars, "
-                               f"{args.envs} envs/GPU, {args.width}x{args.height}, near {args.near}",
-                   "envs_per_gpu": args.envs, "n_gaussians": args.gaussians, "n_avatars": args.avatars,
-                   "l2": "inputs larger than L2 (236 MB scene + per-step buffers), fresh cameras every step",
-                   "parallelism": f"env-sharded x{world}"},
+        "config": workload_config(args, f"env-sharded x{world}"),
         "gpu_launches": None, "roofline": roofline, "e2e": e2e,
         "stages_ms_per_step": {k: round(v, 4) for k, v in per_stage.items()},
         "work_per_step": {"scene_visible": int(w2[0, 0] / args.steps),
