@@ -292,7 +292,10 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
 #ifndef SN_STREAM_PER_THREAD
 #define SN_STREAM_PER_THREAD 1
 #endif
-    constexpr int kPerT = SOURCE == 1 ? 2 : (SOURCE == 0 ? SN_STREAM_PER_THREAD : 1);
+#ifndef SN_LIST_PER_THREAD
+#define SN_LIST_PER_THREAD 2
+#endif
+    constexpr int kPerT = SOURCE == 1 ? SN_LIST_PER_THREAD : (SOURCE == 0 ? SN_STREAM_PER_THREAD : 1);
     constexpr int kBatch = kBlock * kPerT;
     using WlIndex = typename std::conditional<(kBatch > 256), uint16_t, uint8_t>::type;
     __shared__ unsigned s_epsmax;
