@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SN_ABI_VERSION 1
+#define SN_ABI_VERSION 2
 
 enum {
     SN_OK = 0,
@@ -79,10 +79,16 @@ typedef struct sn_cloud {
 } sn_cloud;
 
 /* Device-resident avatar set: A avatars concatenated (render_observation's concat_clouds
- * order), canonical data in float64, skinning as up to 4 (joint, weight) influences per
- * gaussian in ascending joint order (the dense N x J rows of the bundle, avatar.py:127-178).
+ * order), canonical data in float64, skinning as the nonzero (joint, weight) influences of each
+ * gaussian in ascending joint order (the dense N x J rows of the bundle, avatar.py:127-178;
+ * skipping a zero weight leaves the reference's sums unchanged, rig.py:119-132), in one of two
+ * layouts:
+ *   4-slot (infl_offset == NULL; every row has <= 4 nonzeros): joints (n) uint32 = 4 x uint8
+ *     joint ids, weights (n,4) f64 (zero = unused slot);
+ *   CSR (infl_offset != NULL; any row width, e.g. dense SMPL-X softmax weights over 55 joints):
+ *     row g's influences are [infl_offset[g], infl_offset[g+1]) of infl_joint (uint8) and
+ *     infl_weight (f64); joints / weights are then unused (may be NULL).
  *   pos_opacity (n,4) f64, log_scales (n,4) f64, rotations (n,4) f64, sh (K*3, n) f32
- *   joints (n) uint32: 4 x uint8 joint ids, weights (n,4) f64 (zero = unused slot)
  *   avatar_of (n) uint16
  *   inv_bind (A, J, 16) f64, traj_q (sum_a T_a*(J+1)*4) f64, traj_t (sum_a T_a*(J+1)*3) f64
  *   traj_offset (A) int64 frame offsets into traj_*, n_frames (A) int32, fps (A) f64,
@@ -108,6 +114,9 @@ typedef struct sn_avatars {
     const double *fps;
     const double *start_offset;
     const int32_t *loop;
+    const uint32_t *infl_offset; /* (n+1) CSR row offsets, or NULL for the 4-slot layout */
+    const uint8_t *infl_joint;   /* (nnz) */
+    const double *infl_weight;   /* (nnz) */
 } sn_avatars;
 
 /* Stages timed by sn_render_opts.stage_ms (per pass: 0 = scene, 1 = layer). */
@@ -257,6 +266,15 @@ int sn_unpack_bundle(int64_t n, int32_t sh_k, int32_t n_joints, const float *can
                      int64_t row0, int64_t sh_stride, double *pos_opacity, double *log_scales, double *rotations,
                      float *sh, uint32_t *joints, double *weights4, double *row_sums, uint8_t *flags,
                      uint64_t *counters, void *stream);
+
+/* Skins wider than 4 influences (the CSR layout of sn_avatars), after sn_unpack_bundle of the same
+ * rows: each row's nonzero weights.f32 entries (DEVICE, n x n_joints), ascending joint, written at
+ * offsets[row] (DEVICE, caller-computed row offsets into the set's CSR arrays) as uint8 joint ids
+ * and float64 weights, divided by row_sums when counters[9] (sn_unpack_bundle's largest row-sum
+ * deviation) exceeds 1e-5 -- AvatarBundle.validate's renormalization (avatar.py:169-170). */
+int sn_pack_influences(int64_t n, int32_t n_joints, const float *weights, const double *row_sums,
+                       const uint64_t *counters, const uint32_t *offsets, uint8_t *infl_joint, double *infl_weight,
+                       void *stream);
 
 /* Observation payload / frame export (frame_io.py:11-31): uint8 RGB exactly as save_color_png
  * evaluates it on the same values (clip, x*255+0.5 in float64, truncation) and fp16 depth; depth16

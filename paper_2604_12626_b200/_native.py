@@ -15,6 +15,7 @@ LIB_PATH = os.environ.get("SPLATNAV_B200_LIB") or os.path.join(_HERE, "libsplatn
 
 SN_OK, SN_ERR_INVALID, SN_ERR_CUDA, SN_ERR_NOMEM = 0, 1, 2, 3
 SN_FLOAT32, SN_FLOAT64 = 0, 1
+ABI_VERSION = 2
 
 c_double_p = ctypes.POINTER(ctypes.c_double)
 P = ctypes.c_void_p
@@ -46,7 +47,8 @@ class SnAvatars(ctypes.Structure):
                 ("sh_k", ctypes.c_int32), ("pad", ctypes.c_int32),
                 ("pos_opacity", P), ("log_scales", P), ("rotations", P), ("sh", P), ("joints", P), ("weights", P),
                 ("avatar_of", P), ("inv_bind", P), ("traj_q", P), ("traj_t", P), ("traj_offset", P),
-                ("n_frames", P), ("fps", P), ("start_offset", P), ("loop", P)]
+                ("n_frames", P), ("fps", P), ("start_offset", P), ("loop", P),
+                ("infl_offset", P), ("infl_joint", P), ("infl_weight", P)]
 
 
 class SnRenderOpts(ctypes.Structure):
@@ -65,7 +67,7 @@ EXPORTS = (
     "sn_context_sync_stats", "sn_context_kernel_launches", "sn_context_render_retries",
     "sn_render", "sn_render_async", "sn_render_wait", "sn_get_counts", "sn_get_sorted_ids", "sn_get_tile_csr", "sn_get_projection", "sn_sample_pose",
     "sn_skin_lbs", "sn_blend_tile_range", "sn_composite", "sn_selftest_fast_exp", "sn_unpack_ply",
-    "sn_unpack_bundle", "sn_quantize_frames", "sn_flip_rows",
+    "sn_unpack_bundle", "sn_pack_influences", "sn_quantize_frames", "sn_flip_rows",
 )
 
 _lib = None
@@ -112,13 +114,14 @@ def load():
             "sn_quantize_frames": ([i64, P, P, P, P, P], ctypes.c_int),
             "sn_flip_rows": ([i64, i32, i32, P, P, P], ctypes.c_int),
             "sn_unpack_bundle": ([i64, i32, i32, P, P, i64, i64, P, P, P, P, P, P, P, P, P, P], ctypes.c_int),
+            "sn_pack_influences": ([i64, i32, P, P, P, P, P, P, P], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = res
-        if L.sn_abi_version() != 1:
-            raise NativeError(f"ABI mismatch: library reports {L.sn_abi_version()}, binding expects 1")
+        if L.sn_abi_version() != ABI_VERSION:
+            raise NativeError(f"ABI mismatch: library reports {L.sn_abi_version()}, binding expects {ABI_VERSION}")
         _lib = L
     return _lib
 

@@ -8,8 +8,9 @@
 * load_avatar_bundles(paths) -> DeviceAvatars: the reference's bundle directory reader
   (splatnav/avatar.py:180-254: manifest schema, blob sizes, capsules) with canonical.f32 and
   weights.f32 unpacked on the device (sn_unpack_bundle): float64 canonical geometry, SH SoA, the
-  dense N x J weights -> up to 4 (joint, weight) influences with AvatarBundle.validate's checks
-  and float64 row renormalization in numpy's summation order.
+  dense N x J weights -> each row's nonzero (joint, weight) influences (4-slot, or CSR for wider
+  skins) with AvatarBundle.validate's checks and float64 row renormalization in numpy's summation
+  order; trajectory, inverse-bind and capsule-track checks on the host.
 
 Both raise the reference's exception types with the reference's messages.
 """
@@ -22,7 +23,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .avatar import Skeleton, Trajectory
+from .avatar import CapsuleTrack, Skeleton, Trajectory
 from .device import DeviceAvatars, DeviceCloud, _device
 from .errors import (ConsistencyError, ContractViolation, PlyParseError, SchemaError, UnsupportedLayoutError,
                      ValidationError)
@@ -209,18 +210,38 @@ def read_bundle_dir(path, require_capsules=True):
     inv_bind = _read_blob(path, "inv_bind.f32", j * 16).reshape(j, 4, 4).astype(np.float64)
     traj_raw = _read_blob(path, "trajectory.f32", t * (j + 1) * 7).reshape(t, j + 1, 7).astype(np.float64)
     trajectory = Trajectory(fps=fps, quats=traj_raw[:, :, :4], trans=traj_raw[:, :, 4:])
+    capsules = None
     if os.path.isfile(os.path.join(path, "capsules.f32")):
-        _read_blob(path, "capsules.f32", t * c * 7)
+        capsules = CapsuleTrack(_read_blob(path, "capsules.f32", t * c * 7).reshape(t, c, 7).astype(np.float64))
     elif require_capsules:
         raise FileNotFoundError(f"avatar bundle is missing blob 'capsules.f32' in {path}")
-    skeleton.validate()
-    trajectory.validate()
-    if inv_bind.shape != (j, 4, 4):
-        raise ConsistencyError(f"inv_bind shape {inv_bind.shape} != ({j}, 4, 4)")
-    if trajectory.n_joints != j:
-        raise ConsistencyError(f"trajectory has {trajectory.n_joints} joints, skeleton has {j}")
+    # validated by load_avatar_bundles in AvatarBundle.validate's order (canonical cloud first)
     return {"n": n, "j": j, "k": k, "canonical": canonical, "weights": weights, "inv_bind": inv_bind,
-            "trajectory": trajectory, "skeleton": skeleton}
+            "trajectory": trajectory, "skeleton": skeleton, "capsules": capsules}
+
+
+def _validate_host_parts(s):
+    """AvatarBundle.validate (avatar.py:155-178) for everything but the canonical cloud and the
+    weights (checked on the device): skeleton, trajectory (incl. non-finite data), shapes,
+    non-finite inverse binds. The capsule track is checked after the weights (_validate_capsules)."""
+    j = s["j"]
+    s["skeleton"].validate()
+    s["trajectory"].validate()
+    if s["inv_bind"].shape != (j, 4, 4):
+        raise ConsistencyError(f"inv_bind shape {s['inv_bind'].shape} != ({j}, 4, 4)")
+    if s["trajectory"].n_joints != j:
+        raise ConsistencyError(f"trajectory has {s['trajectory'].n_joints} joints, skeleton has {j}")
+    if not np.isfinite(s["inv_bind"]).all():
+        raise ValidationError("non-finite inverse bind matrices")
+
+
+def _validate_capsules(s):
+    cap = s["capsules"]
+    if cap is None:
+        return
+    cap.validate()
+    if cap.n_frames != s["trajectory"].n_frames:
+        raise ConsistencyError(f"capsule track has {cap.n_frames} frames, trajectory has {s['trajectory'].n_frames}")
 
 
 class _BundleSpec:
@@ -245,12 +266,25 @@ def load_avatar_bundles(paths, start_offsets=None, loops=None, device=None, requ
     k = max(s["k"] for s in specs)
     counts = [s["n"] for s in specs]
     n = sum(counts)
+    # skins with a row wider than 4 nonzero influences use the CSR layout for the whole set (row
+    # offsets counted here from the raw float32 rows; joints and weights are packed on the device)
+    widths = [(s["weights"].reshape(s["n"], j) != 0.0).sum(axis=1) for s in specs]
+    csr = any(w.size and int(w.max()) > 4 for w in widths)
     po = torch.zeros((n, 4), dtype=torch.float64, device=dev)
     ls = torch.zeros((n, 4), dtype=torch.float64, device=dev)
     rot = torch.zeros((n, 4), dtype=torch.float64, device=dev)
     sh = torch.zeros((k * 3, n), dtype=torch.float32, device=dev)
     jpk = torch.zeros(n, dtype=torch.int32, device=dev)
     wts = torch.zeros((n, 4), dtype=torch.float64, device=dev)
+    infl = None
+    if csr:
+        off = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(np.concatenate(widths), out=off[1:])
+        if off[-1] >= 2 ** 32:
+            raise ContractViolation("too many skinning influences for 32-bit offsets")
+        nnz = int(off[-1])
+        infl = (torch.from_numpy(off.astype(np.uint32).view(np.int32)).to(dev),
+                torch.zeros(nnz + 1, dtype=torch.uint8, device=dev), torch.zeros(nnz + 1, dtype=torch.float64, device=dev))
     st = torch.cuda.current_stream(dev)
     lib = N.load()
     row0 = 0
@@ -264,8 +298,13 @@ def load_avatar_bundles(paths, start_offsets=None, loops=None, device=None, requ
         N.check(lib.sn_unpack_bundle(m, s["k"], j, canon.data_ptr(), w.data_ptr(), row0, n, po.data_ptr(),
                                      ls.data_ptr(), rot.data_ptr(), sh.data_ptr(), jpk.data_ptr(), wts.data_ptr(),
                                      sums.data_ptr(), flags.data_ptr(), cnt.data_ptr(), st.cuda_stream))
+        if csr:
+            N.check(lib.sn_pack_influences(m, j, w.data_ptr(), sums.data_ptr(), cnt.data_ptr(),
+                                           infl[0].data_ptr() + 4 * row0, infl[1].data_ptr(), infl[2].data_ptr(),
+                                           st.cuda_stream))
         counters = cnt.cpu().numpy().view(np.uint64)
         _raise_cloud_errors(flags, counters)                      # AvatarBundle.validate: canonical first
+        _validate_host_parts(s)
         if m:
             if counters[7]:
                 raise ValidationError("negative skinning weights")
@@ -275,10 +314,7 @@ def load_avatar_bundles(paths, start_offsets=None, loops=None, device=None, requ
                 bad = int(np.argmax(dev_rows))
                 raise ValidationError(f"weight row {bad} sums to {sums[bad].item():.6f}; deviation exceeds "
                                       f"{WEIGHT_RENORM_TOL}")
-            if counters[8]:
-                rows = np.nonzero(flags.cpu().numpy()[:m] & 128)[0]
-                raise ContractViolation(f"weight row {int(rows[0])} has more than 4 nonzero joints; the skinning "
-                                        f"kernel supports at most 4")
+        _validate_capsules(s)
         row0 += m
     return DeviceAvatars.from_device(po, ls, rot, sh, jpk, wts, counts, [_BundleSpec(s) for s in specs], j, k,
-                                     start_offsets, loops, dev)
+                                     start_offsets, loops, dev, infl)

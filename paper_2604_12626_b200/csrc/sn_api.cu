@@ -507,9 +507,12 @@ int check_avatars(const sn_avatars *av) {
     SN_CHECK(av->n >= 0 && av->n_avatars >= 1, "avatar set needs at least one avatar");
     SN_CHECK(av->n_joints >= 1 && av->n_joints <= 255, "n_joints must be in [1, 255]");
     SN_CHECK(av->sh_k == 1 || av->sh_k == 4 || av->sh_k == 9 || av->sh_k == 16, "sh_k must be 1, 4, 9 or 16");
-    SN_CHECK(av->n == 0 || (av->pos_opacity && av->log_scales && av->rotations && av->sh && av->joints &&
-                            av->weights && av->avatar_of),
+    SN_CHECK(av->n == 0 || (av->pos_opacity && av->log_scales && av->rotations && av->sh && av->avatar_of),
              "null avatar buffer");
+    if (av->infl_offset)
+        SN_CHECK(av->n == 0 || (av->infl_joint && av->infl_weight), "null CSR influence buffer");
+    else
+        SN_CHECK(av->n == 0 || (av->joints && av->weights), "null 4-slot influence buffer");
     SN_CHECK(av->inv_bind && av->traj_q && av->traj_t && av->traj_offset && av->n_frames && av->fps &&
                  av->start_offset && av->loop,
              "null avatar trajectory buffer");
@@ -1094,6 +1097,16 @@ int sn_unpack_bundle(int64_t n, int32_t sh_k, int32_t n_joints, const float *can
     SN_CUDA(launch_unpack_bundle(n, sh_k, n_joints, canonical, weights, row0, sh_stride, pos_opacity, log_scales,
                                  rotations, sh, joints, weights4, row_sums, flags,
                                  reinterpret_cast<unsigned long long *>(counters), static_cast<cudaStream_t>(stream)));
+    return SN_OK;
+}
+
+int sn_pack_influences(int64_t n, int32_t n_joints, const float *weights, const double *row_sums,
+                       const uint64_t *counters, const uint32_t *offsets, uint8_t *infl_joint, double *infl_weight,
+                       void *stream) {
+    SN_CHECK(n >= 0 && n_joints >= 1 && n_joints <= 255, "bad influence table description");
+    SN_CHECK(n == 0 || (weights && row_sums && counters && offsets && infl_joint && infl_weight), "null buffer");
+    SN_CUDA(launch_pack_csr(n, n_joints, weights, row_sums, reinterpret_cast<const unsigned long long *>(counters),
+                            offsets, infl_joint, infl_weight, static_cast<cudaStream_t>(stream)));
     return SN_OK;
 }
 

@@ -231,6 +231,27 @@ __global__ void __launch_bounds__(256) renorm_weights_kernel(int64_t n, int64_t 
     for (int k = 0; k < 4; ++k) wts[4 * (row0 + row) + k] = wts[4 * (row0 + row) + k] / s;
 }
 
+// Skins wider than 4 influences: row `row` of weights.f32 -> its nonzeros (ascending joint) at
+// offsets[row] of the CSR arrays, float64, divided by the float64 row sum when any row of the
+// bundle deviated by more than 1e-5 (the same rule as renorm_weights_kernel).
+__global__ void __launch_bounds__(256) pack_csr_kernel(int64_t n, int32_t J, const float *w, const double *sums,
+                                                       const unsigned long long *cnt, const uint32_t *offsets,
+                                                       uint8_t *joint, double *weight) {
+    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= n) return;
+    const bool renorm = __longlong_as_double((long long)cnt[kCntSumDev]) > kWeightSumTol;
+    const double s = sums[row];
+    const float *r = w + row * J;
+    uint32_t o = offsets[row];
+    for (int j = 0; j < J; ++j) {
+        const float v = __ldg(r + j);
+        if (v == 0.0f) continue;
+        joint[o] = (uint8_t)j;
+        weight[o] = renorm ? (double)v / s : (double)v;
+        ++o;
+    }
+}
+
 unsigned grid_for(int64_t n) { return (unsigned)((n + 255) / 256); }
 
 }  // namespace
@@ -263,6 +284,14 @@ cudaError_t launch_unpack_bundle(int64_t n, int32_t sh_k, int32_t J, const float
     renorm_rot_kernel<<<grid_for(n), 256, 0, s>>>(n, d, cnt);
     pack_weights_kernel<<<grid_for(n), 256, 0, s>>>(n, J, weights, row0, joints, wts, sums, flags, cnt);
     renorm_weights_kernel<<<grid_for(n), 256, 0, s>>>(n, row0, wts, sums, cnt);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_csr(int64_t n, int32_t J, const float *weights, const double *sums,
+                            const unsigned long long *cnt, const uint32_t *offsets, uint8_t *joint, double *weight,
+                            cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    pack_csr_kernel<<<grid_for(n), 256, 0, s>>>(n, J, weights, sums, cnt, offsets, joint, weight);
     return cudaGetLastError();
 }
 

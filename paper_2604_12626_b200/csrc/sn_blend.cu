@@ -1087,7 +1087,11 @@ __global__ void __launch_bounds__(256, SN_FIXUP_MIN_BLOCKS) fixup_kernel(BlendAr
             oc[2] = (float)np_clip((double)f.cb + cam.background[2] * f.T, 0.0, 1.0);
             b.alpha[pix] = (float)alpha;
             b.depth[pix] = (float)depth;
-            if (b.derr) b.derr[pix] = 0.0f;
+            // the stored depth is the float64 walk's rounded to float32 (and the walk's prefix-product
+            // transmittance / table exp differ from the sequential reference by a few float64 ulps):
+            // a band of ~2 float ulps makes a layer fixup whose exact front depth falls inside it
+            // recompute this pixel in float64 (fixup_layer_kernel / fixup_kernel<2>)
+            if (b.derr) b.derr[pix] = f.A > 0.0 ? (float)(2.5e-7 * fabs(depth)) : 0.0f;
             continue;
         }
         double fc[3] = {0.0, 0.0, 0.0};

@@ -177,6 +177,10 @@ cudaError_t launch_unpack_bundle(int64_t n, int32_t sh_k, int32_t J, const float
                                  double *rotations, float *sh, uint32_t *joints, double *wts, double *sums,
                                  uint8_t *flags, unsigned long long *cnt, cudaStream_t s);
 
+cudaError_t launch_pack_csr(int64_t n, int32_t J, const float *weights, const double *sums,
+                            const unsigned long long *cnt, const uint32_t *offsets, uint8_t *joint, double *weight,
+                            cudaStream_t s);
+
 cudaError_t launch_quantize(int64_t npix, const float *color, const float *depth, uint8_t *rgb8, uint16_t *depth16,
                             cudaStream_t s);
 cudaError_t launch_flip_rows(int64_t frames, int32_t h, int32_t w, const float *src, float *dst, cudaStream_t s);

@@ -362,34 +362,32 @@ __device__ __forceinline__ void ld4p(const double *p, double o[4]) {
     }
 }
 
-// NC = true: pose data in global memory (read-only path); false: generic loads (shared memory)
-// ROT = false: the position only (q_out untouched) -- the count kernel's visibility test needs the
-// rotation only for the few items its float32 prefilter cannot decide.
-template <bool NC = true, bool ROT = true>
-__device__ __forceinline__ void skin_one(const sn_avatars &av, int64_t g, const double *jm, const double *eq,
-                                         const double *root, double p_out[3], double q_out[4]) {
-    double P[4], W[4], Q[4];
-    load4<double>(av.pos_opacity + 4 * g, P);
-    load4<double>(av.weights + 4 * g, W);
-    load4<double>(av.rotations + 4 * g, Q);
-    uint32_t J4 = __ldg(av.joints + g);
+// lbs_deform's per-gaussian sums over one influence list (get(k, j, w): the k-th nonzero influence,
+// ascending joint order). NC = true: pose data in global memory (read-only path); false: generic
+// loads (shared memory). ROT = false: the position only (q_out untouched) -- the count kernel's
+// visibility test needs the rotation only for the few items its float32 prefilter cannot decide.
+template <bool NC, bool ROT, typename Get>
+__device__ __forceinline__ void skin_core(int n, Get get, const double P[4], const double Q[4], const double *jm,
+                                          const double *eq, const double *root, double p_out[3], double q_out[4]) {
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
     int dom = -1;
     double wmax = 0.0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        double w = W[k];
+    for (int k = 0; k < n; ++k) {
+        int j;
+        double w;
+        get(k, j, w);
         if (w == 0.0) continue;
-        int j = (J4 >> (8 * k)) & 0xff;
         const double *M = jm + 12 * j;
-        // einsum("jab,nb->jna") as numpy evaluates it: (r0 p0 + r2 p2) + r1 p1, then + offset
+        // einsum("jab,nb->jna") as numpy evaluates it: (r0 p0 + r2 p2) + r1 p1, then + offset;
+        // einsum("nj,jnc->nc") accumulates over j sequentially, unfused (measured)
         double t0 = ((ldp<NC>(M + 0) * P[0] + ldp<NC>(M + 2) * P[2]) + ldp<NC>(M + 1) * P[1]) + ldp<NC>(M + 3);
         double t1 = ((ldp<NC>(M + 4) * P[0] + ldp<NC>(M + 6) * P[2]) + ldp<NC>(M + 5) * P[1]) + ldp<NC>(M + 7);
         double t2 = ((ldp<NC>(M + 8) * P[0] + ldp<NC>(M + 10) * P[2]) + ldp<NC>(M + 9) * P[1]) + ldp<NC>(M + 11);
         acc0 = acc0 + w * (t0 - P[0]);
         acc1 = acc1 + w * (t1 - P[1]);
         acc2 = acc2 + w * (t2 - P[2]);
-        if (dom < 0 || w > wmax) {
+        if (dom < 0 || w > wmax) {  // np.argmax: the first maximum
             wmax = w;
             dom = j;
         }
@@ -404,11 +402,15 @@ __device__ __forceinline__ void skin_one(const sn_avatars &av, int64_t g, const 
     double qd[4];
     ld4p<NC>(eq + 4 * dom, qd);
     double bq[4] = {0.0, 0.0, 0.0, 0.0};
+    // (weights * signs) @ eff_quats: an FMA chain over j (OpenBLAS at production sizes; for
+    // K >= 16 and up to ~1k rows OpenBLAS interleaves 8 accumulators instead -- a few-ulp
+    // difference before the normalization, inside the 1e-12 LBS tolerance)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        double w = W[k];
+    for (int k = 0; k < n; ++k) {
+        int j;
+        double w;
+        get(k, j, w);
         if (w == 0.0) continue;
-        int j = (J4 >> (8 * k)) & 0xff;
         double qj[4];
         ld4p<NC>(eq + 4 * j, qj);
         double dot = fma(qj[3], qd[3], fma(qj[2], qd[2], fma(qj[1], qd[1], qj[0] * qd[0])));
@@ -427,6 +429,40 @@ __device__ __forceinline__ void skin_one(const sn_avatars &av, int64_t g, const 
     double nn = norm4(bq[0], bq[1], bq[2], bq[3]);
     double qn[4] = {bq[0] / nn, bq[1] / nn, bq[2] / nn, bq[3] / nn};
     quat_multiply(qn, Q, q_out);
+}
+
+// lbs_deform (rig.py:107-146) for one gaussian under one (env, avatar) pose. The influences are
+// the row's nonzeros in ascending joint order, so the sums equal the dense N x J contractions
+// (a zero weight adds +-0): the 4-slot layout, or the CSR rows of an arbitrary-width skin.
+template <bool NC = true, bool ROT = true>
+__device__ __forceinline__ void skin_one(const sn_avatars &av, int64_t g, const double *jm, const double *eq,
+                                         const double *root, double p_out[3], double q_out[4]) {
+    double P[4], Q[4];
+    load4<double>(av.pos_opacity + 4 * g, P);
+    if (ROT) load4<double>(av.rotations + 4 * g, Q);
+    if (av.infl_offset == nullptr) {
+        double W[4];
+        load4<double>(av.weights + 4 * g, W);
+        const uint32_t J4 = __ldg(av.joints + g);
+        skin_core<NC, ROT>(
+            4,
+            [&](int k, int &j, double &w) {
+                j = (J4 >> (8 * k)) & 0xff;
+                w = W[k];
+            },
+            P, Q, jm, eq, root, p_out, q_out);
+    } else {
+        const uint32_t o0 = __ldg(av.infl_offset + g), o1 = __ldg(av.infl_offset + g + 1);
+        const uint8_t *js = av.infl_joint + o0;
+        const double *ws = av.infl_weight + o0;
+        skin_core<NC, ROT>(
+            (int)(o1 - o0),
+            [&](int k, int &j, double &w) {
+                j = __ldg(js + k);
+                w = __ldg(ws + k);
+            },
+            P, Q, jm, eq, root, p_out, q_out);
+    }
 }
 
 __device__ __forceinline__ void pose_ptrs(const PoseView &pv, int env, int avatar, const double *&jm,
@@ -660,11 +696,16 @@ cudaError_t launch_avatar_count(const sn_avatars &av, const PoseView &pv, const 
     const int group = (int)std::max<size_t>(1, std::min<size_t>(SN_AVATAR_ENV_GROUP, (40 * 1024) / blk));
     const size_t smem = blk * group;
     // dynamic + static (cameras, counters) may pass the default 48 KB: opt in to the dynamic size
-    static size_t opted = 0;
-    if (smem > opted) {
-        cudaError_t e = cudaFuncSetAttribute(avatar_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // (a function attribute is per device: remember the opted size per device ordinal)
+    constexpr int kMaxDevices = 64;
+    static size_t opted[kMaxDevices] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDevices || smem > opted[dev]) {
+        e = cudaFuncSetAttribute(avatar_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        opted = smem;
+        if (dev >= 0 && dev < kMaxDevices) opted[dev] = smem;
     }
     avatar_count_kernel<<<a.n_blocks, kBlock, smem, s>>>(av, pv, a, group);
     return cudaGetLastError();

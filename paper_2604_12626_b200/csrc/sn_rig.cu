@@ -203,10 +203,12 @@ __global__ void __launch_bounds__(256) avatar_extent_kernel(sn_avatars av, unsig
         // non-negative doubles order like their bit patterns; NaN/inf poison the bound (no culling)
         atomicMax(e, (unsigned long long)__double_as_longlong(r == r ? r : INFINITY));
         atomicMax(e + 1, (unsigned long long)__double_as_longlong(sm == sm ? sm : INFINITY));
-        const uint32_t j4 = av.joints[g];
-        for (int k = 0; k < 4; ++k) {
-            if (av.weights[4 * g + k] == 0.0) continue;
-            const int j = (j4 >> (8 * k)) & 0xff;
+        const bool csr = av.infl_offset != nullptr;
+        const uint32_t j4 = csr ? 0u : av.joints[g];
+        const int64_t k0 = csr ? (int64_t)av.infl_offset[g] : 0, k1 = csr ? (int64_t)av.infl_offset[g + 1] : 4;
+        for (int64_t k = k0; k < k1; ++k) {
+            if ((csr ? av.infl_weight[k] : av.weights[4 * g + k]) == 0.0) continue;
+            const int j = csr ? (int)av.infl_joint[k] : (int)((j4 >> (8 * k)) & 0xff);
             const double *ib = av.inv_bind + ((int64_t)a * J + j) * 16;
             const double x = ((ib[0] * p[0] + ib[1] * p[1]) + ib[2] * p[2]) + ib[3];
             const double y = ((ib[4] * p[0] + ib[5] * p[1]) + ib[6] * p[2]) + ib[7];

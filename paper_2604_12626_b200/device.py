@@ -92,8 +92,14 @@ class DeviceCloud:
         return self._struct
 
 
+def influence_widths(weights):
+    """Nonzero influences per row of dense (N, J) skinning weights."""
+    return (np.asarray(weights) != 0.0).sum(axis=1)
+
+
 def sparse_influences(weights, max_influences=MAX_INFLUENCES):
-    """Dense (N, J) skinning weights -> (joints uint32 packed 4 x uint8, weights (N, 4) float64).
+    """Dense (N, J) skinning weights -> (joints uint32 packed 4 x uint8, weights (N, 4) float64),
+    the 4-slot layout for rows with at most 4 nonzeros (csr_influences takes any width).
 
     Influences are the nonzero entries of each row in ascending joint order, so the kernel's
     running sums visit joints in the same order as the reference's dense contractions.
@@ -106,8 +112,8 @@ def sparse_influences(weights, max_influences=MAX_INFLUENCES):
     counts = nz.sum(axis=1)
     if n and counts.max() > max_influences:
         row = int(np.argmax(counts))
-        raise ContractViolation(f"weight row {row} has {int(counts[row])} nonzero joints; the skinning kernel "
-                                f"supports at most {max_influences}")
+        raise ContractViolation(f"weight row {row} has {int(counts[row])} nonzero joints; the 4-slot layout "
+                                f"holds at most {max_influences} (use csr_influences)")
     order = np.argsort(~nz, axis=1, kind="stable")[:, :max_influences]  # nonzeros first, ascending joint
     wk = np.take_along_axis(w, order, axis=1)
     slot_used = np.arange(max_influences)[None, :] < counts[:, None]
@@ -119,6 +125,24 @@ def sparse_influences(weights, max_influences=MAX_INFLUENCES):
         jk = np.pad(jk, ((0, 0), (0, pad)))
     packed = jk[:, 0] | (jk[:, 1] << 8) | (jk[:, 2] << 16) | (jk[:, 3] << 24)
     return packed.astype(np.uint32), np.ascontiguousarray(wk)
+
+
+def csr_influences(weights, row_offset=0):
+    """Dense (N, J) skinning weights -> CSR (offsets uint32 (N+1), joints uint8 (nnz), weights f64
+    (nnz)): each row's nonzeros in ascending joint order, any width (dense SMPL / SMPL-X skins).
+    `row_offset` is added to every offset (concatenating several bundles)."""
+    w = np.asarray(weights, dtype=np.float64)
+    n, j = w.shape
+    if j > 255:
+        raise ContractViolation(f"at most 255 joints are supported, got {j}")
+    rows, cols = np.nonzero(w)  # row-major: ascending joint within each row
+    counts = np.bincount(rows, minlength=n)
+    off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=off[1:])
+    off += row_offset
+    if off[-1] >= 2 ** 32:
+        raise ContractViolation("too many skinning influences for 32-bit offsets")
+    return off.astype(np.uint32), cols.astype(np.uint8), np.ascontiguousarray(w[rows, cols])
 
 
 class DeviceAvatars:
@@ -146,8 +170,12 @@ class DeviceAvatars:
         ls = np.zeros((n, 4))
         rot = np.zeros((n, 4))
         sh = np.zeros((n, k, 3), dtype=np.float32)
+        # 4-slot influences when every row has <= 4 nonzeros, else CSR rows for the whole set
+        csr = any(n_b and influence_widths(b.lbs_weights).max() > MAX_INFLUENCES
+                  for n_b, b in zip(counts, bundles))
         jpk = np.zeros(n, dtype=np.uint32)
         wts = np.zeros((n, 4))
+        c_off, c_j, c_w = [np.zeros(1, dtype=np.uint32)], [], []
         owner = np.zeros(n, dtype=np.uint16)
         ib = np.zeros((a, j, 16))
         tq, tt, toff, nf, fps = [], [], [], [], []
@@ -161,7 +189,13 @@ class DeviceAvatars:
             rot[s:e] = np.asarray(c.rotations, dtype=np.float64)
             cs = np.asarray(c.sh_coeffs, dtype=np.float32)
             sh[s:e, :cs.shape[1]] = cs
-            jpk[s:e], wts[s:e] = sparse_influences(b.lbs_weights)
+            if csr:
+                o, jj, ww = csr_influences(b.lbs_weights, row_offset=int(c_off[-1][-1]))
+                c_off.append(o[1:])
+                c_j.append(jj)
+                c_w.append(ww)
+            else:
+                jpk[s:e], wts[s:e] = sparse_influences(b.lbs_weights)
             owner[s:e] = i
             ib[i] = np.asarray(b.inv_bind, dtype=np.float64).reshape(j, 16)
             traj = b.trajectory
@@ -175,13 +209,21 @@ class DeviceAvatars:
             fps.append(float(traj.fps))
             frame_off += q.shape[0]
         t = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+        infl = None
+        if csr:
+            cj, cw = np.concatenate(c_j), np.concatenate(c_w)
+            # (one padding entry keeps the buffers non-null for an all-zero skin)
+            infl = (t(np.concatenate(c_off).view(np.int32)), t(np.concatenate([cj, np.zeros(1, np.uint8)])),
+                    t(np.concatenate([cw, np.zeros(1)])))
         self._finish(t(po), t(ls), t(rot), t(sh.reshape(n, k * 3).T), t(jpk.view(np.int32)), t(wts), counts, ib,
-                     tq, tt, toff, nf, fps, j, k, start_offsets, loops, dev)
+                     tq, tt, toff, nf, fps, j, k, start_offsets, loops, dev, infl)
 
     @classmethod
-    def from_device(cls, po, ls, rot, sh, joints, weights, counts, specs, j, k, start_offsets, loops, device):
+    def from_device(cls, po, ls, rot, sh, joints, weights, counts, specs, j, k, start_offsets, loops, device,
+                    infl=None):
         """Canonical buffers already on the device (assets.load_avatar_bundles); specs carry each
-        bundle's inv_bind and trajectory (host, float64)."""
+        bundle's inv_bind and trajectory (host, float64); infl = (offsets, joints, weights) CSR
+        device tensors for skins wider than 4 influences."""
         self = cls.__new__(cls)
         ib = np.stack([np.asarray(s.inv_bind, dtype=np.float64).reshape(j, 16) for s in specs])
         tq, tt, toff, nf, fps = [], [], [], [], []
@@ -195,11 +237,11 @@ class DeviceAvatars:
             fps.append(float(s.trajectory.fps))
             frame_off += q.shape[0]
         self._finish(po, ls, rot, sh, joints, weights, counts, ib, tq, tt, toff, nf, fps, j, k, start_offsets, loops,
-                     device)
+                     device, infl)
         return self
 
     def _finish(self, po, ls, rot, sh, joints, weights, counts, ib, tq, tt, toff, nf, fps, j, k, start_offsets, loops,
-                dev):
+                dev, infl=None):
         a = len(counts)
         n = int(sum(counts))
         self.offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
@@ -218,12 +260,14 @@ class DeviceAvatars:
         self.fps = t(np.asarray(fps, dtype=np.float64))
         self.start_offset = t(so)
         self.loop = t(lp)
+        self.infl = infl  # CSR (offsets, joints, weights) or None (4-slot layout)
         ptr = lambda x: x.data_ptr()
+        iptr = (None, None, None) if infl is None else tuple(x.data_ptr() for x in infl)
         self._struct = N.SnAvatars(
             n, a, j, k, 0, ptr(self.pos_opacity), ptr(self.log_scales), ptr(self.rotations), ptr(self.sh),
             ptr(self.joints), ptr(self.weights), ptr(self.avatar_of), ptr(self.inv_bind), ptr(self.traj_q),
             ptr(self.traj_t), ptr(self.traj_offset), ptr(self.n_frames), ptr(self.fps), ptr(self.start_offset),
-            ptr(self.loop))
+            ptr(self.loop), *iptr)
 
     def struct(self):
         return self._struct

@@ -112,20 +112,23 @@ def _sample_body(rng, n):
     return p0[which] + t[:, None] * (p1[which] - p0[which]) + r[which, None] * d
 
 
-def random_pose_trajectory(rng, n_frames, fps, floor_lo, floor_hi, sigma=0.3):
+def random_pose_trajectory(rng, n_frames, fps, floor_lo, floor_hi, sigma=0.3, parents=None, rest=None):
     """Per-frame local axis-angle ~ N(0, sigma) per joint, forward kinematics to world joint
-    transforms, plus a random floor translation and yaw for the root (index J)."""
-    j = 24
+    transforms, plus a random floor translation and yaw for the root (index J). Default skeleton:
+    the 24-joint SMPL-like tree."""
+    parents = SMPL_PARENTS if parents is None else np.asarray(parents)
+    rest = SMPL_REST if rest is None else np.asarray(rest)
+    j = parents.shape[0]
     quats = np.zeros((n_frames, j + 1, 4))
     trans = np.zeros((n_frames, j + 1, 3))
     local = axis_angle_to_quat(rng.normal(0.0, sigma, size=(n_frames, j, 3)))
     for f in range(n_frames):
         quats[f, 0] = local[f, 0]
-        trans[f, 0] = SMPL_REST[0]
+        trans[f, 0] = rest[0]
         for k in range(1, j):
-            p = SMPL_PARENTS[k]
+            p = parents[k]
             quats[f, k] = quat_multiply(quats[f, p], local[f, k])
-            trans[f, k] = trans[f, p] + rotate(quats[f, p], SMPL_REST[k] - SMPL_REST[p])
+            trans[f, k] = trans[f, p] + rotate(quats[f, p], rest[k] - rest[p])
     yaw = rng.uniform(-math.pi, math.pi, size=n_frames)
     quats[:, j] = np.stack([np.cos(yaw / 2), np.zeros(n_frames), np.zeros(n_frames), np.sin(yaw / 2)], axis=1)
     trans[:, j, :2] = rng.uniform(floor_lo, floor_hi, size=(n_frames, 2))
@@ -158,6 +161,56 @@ def make_avatar(n_gaussians=50_000, seed=0, n_frames=64, fps=30.0, floor_lo=(0.0
     inv_bind[:, :3, 3] = -SMPL_REST
     traj = random_pose_trajectory(rng, n_frames, fps, np.asarray(floor_lo), np.asarray(floor_hi))
     return AvatarBundle(canonical=cloud, lbs_weights=weights, inv_bind=inv_bind, skeleton=smpl_skeleton(),
+                        trajectory=traj).validate()
+
+
+def smplx_like_skeleton(n_joints=55):
+    """The 24-joint tree extended to n_joints (SMPL-X has 55: body, jaw/eyes, 2 x 15 finger joints):
+    extra joints hang as short 3-joint chains off the wrists (20, 21) and the head (15)."""
+    parents = list(SMPL_PARENTS)
+    rest = [list(r) for r in SMPL_REST]
+    anchors = [20, 21, 15]
+    k = 0
+    while len(parents) < n_joints:
+        a = anchors[k % 3]
+        base = rest[a]
+        for d in range(3):
+            if len(parents) >= n_joints:
+                break
+            parents.append(a if d == 0 else len(parents) - 1)
+            off = 0.02 * (d + 1)
+            rest.append([base[0] + off, base[1] + 0.01 * ((k // 3) - 2), base[2] - 0.01 * d])
+        k += 1
+    return Skeleton(parents=np.array(parents), rest_positions=np.array(rest)).validate()
+
+
+def make_dense_avatar(n_gaussians=2_000, n_joints=24, seed=0, n_frames=16, fps=30.0, temperature=0.02,
+                      floor_lo=(0.0, 0.0), floor_hi=(8.0, 8.0), sh_degree=1):
+    """An avatar whose skinning rows are dense: softmax(-|p - rest_j|^2 / temperature) over every
+    joint (the SMPL / SMPL-X style skins the reference's dense N x J blend accepts, rig.py:112-119)."""
+    rng = np.random.default_rng(seed)
+    skel = smpl_skeleton() if n_joints == 24 else smplx_like_skeleton(n_joints)
+    k = sh_coeff_count(sh_degree)
+    pos = _sample_body(rng, n_gaussians)
+    d2 = ((pos[:, None, :] - skel.rest_positions[None, :, :]) ** 2).sum(axis=2)
+    logits = -(d2 - d2.min(axis=1, keepdims=True)) / temperature
+    w = np.exp(logits)
+    w = np.maximum(w / w.sum(axis=1, keepdims=True), 1e-6)  # every joint nonzero
+    w = (w / w.sum(axis=1, keepdims=True)).astype(np.float32).astype(np.float64)
+    sh = np.empty((n_gaussians, k, 3))
+    sh[:, 0, :] = rng.normal(0.0, 0.5, size=(n_gaussians, 3))
+    if k > 1:
+        sh[:, 1:, :] = rng.normal(0.0, 0.05, size=(n_gaussians, k - 1, 3))
+    cloud = GaussianCloud(
+        positions=pos.astype(np.float32), sh_coeffs=sh.astype(np.float32),
+        opacities=rng.normal(2.0, 0.5, size=n_gaussians).astype(np.float32),
+        log_scales=rng.normal(-4.0, 0.3, size=(n_gaussians, 3)).astype(np.float32),
+        rotations=quat_normalize(rng.normal(size=(n_gaussians, 4))).astype(np.float32)).validate()
+    inv_bind = np.tile(np.eye(4), (n_joints, 1, 1))
+    inv_bind[:, :3, 3] = -skel.rest_positions
+    traj = random_pose_trajectory(rng, n_frames, fps, np.asarray(floor_lo), np.asarray(floor_hi),
+                                  parents=skel.parents, rest=skel.rest_positions)
+    return AvatarBundle(canonical=cloud, lbs_weights=w, inv_bind=inv_bind, skeleton=skel,
                         trajectory=traj).validate()
 
 
