@@ -1,15 +1,23 @@
 """Benchmark: RGB-D 640x480 frames/sec of the splat-observation hot path (BASELINE.json metric).
 
-Default workload = BASELINE config 2: a 1M-gaussian room scene (8 x 8 x 3 m) plus 4 skinned
-avatars (50k gaussians, 24 joints each), 64 environments per GPU, one 640x480 90 deg camera per env
-at 1.25 m, near 0.1 / far 100 (the reference agent-camera defaults, scene.py:23-24). A step =
-one batch: per-env avatar pose sampling + fused LBS, scene pass and avatar-layer pass
+Workloads (--config):
+* 2 (default): BASELINE config 2 -- a 1M-gaussian room scene (8 x 8 x 3 m) plus 4 skinned avatars
+  (50k gaussians, 24 joints each), 64 environments PER GPU (weak scaling), one 640x480 90 deg
+  camera per env at 1.25 m, near 0.1 / far 100 (the reference agent-camera defaults,
+  scene.py:23-24).
+* 4: BASELINE config 4 -- a 3M-gaussian scene, --avatars 0/1/4/8/16 skinned avatars, a FIXED batch
+  of 1,024 environments sharded across the N GPUs (strong scaling; env e -> rank floor(e N / E),
+  parallel.env_shard); each rank renders its shard in one call (chunks of 64 envs inside).
+A step = one batch: per-env avatar pose sampling + fused LBS, scene pass and avatar-layer pass
 (projection, SH, depth sort, tile binning, blend, composite) for all envs. Every step uses a fresh
 set of camera poses and sim times (pre-generated), so nothing is cached across steps; the scene
-(236 MB) and per-step buffers exceed the 126 MB L2.
+(236 MB at 1M) and the per-step buffers exceed the 126 MB L2.
 
-Multi-GPU (torchrun): each rank renders its own 64 envs against a replica of the scene (weak
-scaling, no data-path collective); timing is the max over ranks of CUDA-event time.
+--gpus N: one process per GPU. Without a torchrun environment, bench.py re-launches itself under
+`torch.distributed.run --nproc-per-node N` (127.0.0.1); under torchrun it refuses to run when
+WORLD_SIZE != N. Timing is CUDA events per rank, the max over ranks. --gather adds the optional
+observation gather of BASELINE config 4: the render's epilogues write uint8 RGB + fp16 depth
+(frame_io.py:13-14 rule) and every step they are gathered to rank 0 over NCCL (timed).
 
 --impl reference: the reference's algorithm on the host CPU (oracle/, the C restatement pinned to
 the reference) on all host threads, on a bounded sample of envs per step; rank 0 only.
@@ -19,6 +27,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -32,34 +41,49 @@ sys.path.insert(0, REPO)
 METRIC = "RGB-D frames/sec (640×480) vs gaussian count & avatar count at 1/2/4/8 B200"
 STAGES = ("pose", "count", "scan", "emit", "depth_sort", "permute", "pair_scan", "bin_count", "bin_scatter", "ranges",
           "blend", "composite")
+CAMERA_BYTES = 208  # sn_camera (include/splatnav_b200.h)
+TIME_BYTES = 8      # one float64 sim time per env
+# FP32-pipe floating-point operations per (pixel, splat) contribution of blend_kernel<0,0>, counted
+# from its SASS (an FFMA / FFMA2 lane is 2 flops, FMUL / FADD / FMNMX 1): the two principal-axis rows
+# (2 FFMA2 = 8) and h (2 FFMA = 4), alpha's error (FFMA, 2), alpha (FMUL + FMNMX, 2; the EX2 is on
+# the MUFU pipe), weight (FMUL, 1), transmittance (FFMA, 2), colour and depth sums (2 FFMA2 = 8),
+# A (FADD, 1), the transmittance error bound (3 FFMA, 6), z bound (FMNMX, 1), cutoff test (FADD, 1).
+BLEND_FLOPS_PER_CONTRIBUTION = 8 + 4 + 2 + 2 + 1 + 2 + 8 + 1 + 6 + 1 + 1
 
 
+def defaults_for(config):
+    if config == 4:
+        return {"gaussians": 3_000_000, "avatars": 4, "envs": 1024}
+    return {"gaussians": 1_000_000, "avatars": 4, "envs": 64}
 
-def workload_config(args, parallelism):
-    """The `config` object both arms print (the GPU arm and `--impl reference` share it)."""
-    return {"workload": f"config2: {args.gaussians} scene gaussians + {args.avatars}x50k skinned avatars, "
-                        f"{args.envs} envs/GPU, {args.width}x{args.height}, near {args.near}",
-            "envs_per_gpu": args.envs, "n_gaussians": args.gaussians, "n_avatars": args.avatars,
-            "l2": "inputs larger than L2 (236 MB scene + per-step buffers), fresh cameras every step",
-            "parallelism": parallelism}
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--envs", type=int, default=64, help="environments per GPU")
-    p.add_argument("--gaussians", type=int, default=1_000_000)
-    p.add_argument("--avatars", type=int, default=4)
+    p.add_argument("--config", type=int, default=2, choices=[2, 4],
+                   help="2: 64 envs per GPU (weak scaling); 4: a fixed 1,024-env batch sharded over the GPUs")
+    p.add_argument("--envs", type=int, default=None,
+                   help="config 2: environments per GPU (64); config 4: total environments (1024)")
+    p.add_argument("--gaussians", type=int, default=None)
+    p.add_argument("--avatars", type=int, default=None)
     p.add_argument("--near", type=float, default=0.1)
     p.add_argument("--width", type=int, default=640)
     p.add_argument("--height", type=int, default=480)
     p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--gather", action="store_true",
+                   help="write the uint8/fp16 observation payload and gather it to rank 0 every step (timed)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-envs", type=int, default=0, help="env sample for the CPU baseline (0 = auto)")
-    return p.parse_args()
+    a = p.parse_args(argv)
+    d = defaults_for(a.config)
+    for k, v in d.items():
+        if getattr(a, k) is None:
+            setattr(a, k, v)
+    return a
 
 
 def dist_env():
@@ -69,19 +93,64 @@ def dist_env():
     return world, rank, local
 
 
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_under_torchrun(args):
+    """--gpus N > 1 without a torchrun environment: run this script as N ranks on this node."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def workload_config(args, world):
+    """The `config` object both arms print (the GPU arm and `--impl reference` share it exactly)."""
+    if args.config == 4:
+        wl = (f"config4: {args.gaussians} scene gaussians + {args.avatars}x50k skinned avatars, {args.envs} envs "
+              f"sharded over {world} GPU(s), {args.width}x{args.height}, near {args.near}")
+        envs = {"total_envs": args.envs, "scaling": "strong"}
+    else:
+        wl = (f"config2: {args.gaussians} scene gaussians + {args.avatars}x50k skinned avatars, {args.envs} envs/GPU, "
+              f"{args.width}x{args.height}, near {args.near}")
+        envs = {"envs_per_gpu": args.envs, "scaling": "weak"}
+    cfg = {"workload": wl, "n_gaussians": args.gaussians, "n_avatars": args.avatars, **envs,
+           "l2": "inputs larger than L2 (scene + per-step buffers), fresh cameras every step",
+           "parallelism": f"env-sharded x{world}", "gather": bool(args.gather)}
+    return cfg
+
+
+def envs_of_rank(args, world, rank):
+    """(first global env, count) of this rank's batch."""
+    if args.config == 4:
+        from paper_2604_12626_b200.parallel import env_shard
+        a, b = env_shard(args.envs, world, rank)
+        return a, b - a
+    return rank * args.envs, args.envs
+
+
+def total_envs(args, world):
+    return args.envs if args.config == 4 else args.envs * world
+
+
 def workload(args, world, rank, n_sets):
-    """Scene + avatars (identical on every rank) and n_sets per-step (cameras, times) for this rank."""
+    """Scene + avatars (identical on every rank) and n_sets per-step (cameras, times) for this rank's
+    envs. Cameras of global env g at step s are the same whatever the rank count."""
     from paper_2604_12626_b200 import synthetic as S
     box = S.room_box(args.gaussians)
     scene = S.make_scene(args.gaussians, box[0], box[1], seed=args.seed)
     bundles = [S.make_avatar(50_000, seed=args.seed + 100 + i, floor_lo=box[0][:2], floor_hi=box[1][:2])
                for i in range(args.avatars)]
+    e0, ne = envs_of_rank(args, world, rank)
+    n_all = total_envs(args, world)
     sets = []
     for s in range(n_sets):
-        cams = S.room_cameras(args.envs, box, seed=10_000 + (s * world + rank) * 7 + args.seed, width=args.width,
-                              height=args.height, near=args.near)
-        rng = np.random.default_rng(20_000 + s * world + rank)
-        times = rng.uniform(0.0, 2.0, size=args.envs)
+        cams = S.room_cameras(n_all, box, seed=10_000 + 7 * s + args.seed, width=args.width, height=args.height,
+                              near=args.near)[e0:e0 + ne]
+        rng = np.random.default_rng(20_000 + s)
+        times = rng.uniform(0.0, 2.0, size=n_all)[e0:e0 + ne]
         sets.append((cams, times))
     return scene, bundles, box, sets
 
@@ -91,15 +160,13 @@ def start_offsets(n):
 
 
 class ClockSampler:
-    """SM clock and throttle reasons sampled every 5 ms during the timed region (NVML; falls back
-    to an nvidia-smi loop when NVML is unavailable)."""
+    """SM clock and throttle reasons sampled every 5 ms during the timed region (NVML)."""
 
     def __init__(self, gpu_index):
         self.gpu = gpu_index
         self.samples, self.max_mhz, self.reasons = [], 0.0, set()
         self._stop = threading.Event()
         self._thread = None
-        self._smi = None
 
     def _run_nvml(self, nv, h):
         names = {"hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
@@ -172,10 +239,10 @@ def algorithmic_bytes(stage, pass_id, n_gauss, n_avatar_gauss, work, n_pix_total
         return vis * 160
     if stage == "pair_scan":
         return vis * 12
-    if stage == "bin_count":  # counting binner: read rects, write per-chunk tile counts (small)
-        return vis * 8
-    if stage == "bin_scatter":  # read rects, write one u32 per pair
-        return vis * 8 + pairs * 4
+    if stage == "bin_count":
+        return vis * 8 + pairs * 8
+    if stage == "bin_scatter":  # one read + one write of each (key, value) pair
+        return pairs * 16
     if stage == "ranges":
         return pairs * 4
     if stage == "blend":  # BlendGeo records gathered (64 B + 4 B index) + rectangles streamed + pixels out
@@ -184,9 +251,9 @@ def algorithmic_bytes(stage, pass_id, n_gauss, n_avatar_gauss, work, n_pix_total
     return 0.0
 
 
-def measured_traffic(kernel_stage):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
-    (profiles/ncu_traffic.json, written by scripts/ncu_traffic.py from the .ncu-rep)."""
+def committed_ncu(kernel_stage):
+    """Per-launch DRAM bytes / warp instructions of a kernel from the committed ncu --set full capture
+    of the same bench command (profiles/ncu_traffic.json, written by scripts/ncu_traffic.py)."""
     try:
         with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as f:
             d = json.load(f)
@@ -218,8 +285,9 @@ def cpu_baseline(args, scene, bundles, sets, n_envs_sample):
     O.render_batch(scene, per_env if bundles else None, cams, np.ones(3), threads=threads)
     dt = time.perf_counter() - t0
     return {"value": len(cams) / dt, "unit": "frames/s", "cores": threads, "kind": "port",
-            "sample": f"{len(cams)} envs of the same workload (scene {args.gaussians} gaussians, {len(bundles)} "
-                      f"avatars, {args.width}x{args.height}), LBS + render_observation per env, {dt:.1f} s wall"}
+            "sample": f"{len(cams)} envs per step of the same workload (scene {args.gaussians} gaussians, "
+                      f"{len(bundles)} avatars, {args.width}x{args.height}), LBS + render_observation per env, "
+                      f"{dt:.1f} s wall"}
 
 
 def run_reference(args):
@@ -227,7 +295,7 @@ def run_reference(args):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    n_sample = args.cpu_envs or max(2, min(args.envs, threads))
+    n_sample = args.cpu_envs or max(2, min(16, threads))
     scene, bundles, box, sets = workload(args, 1, 0, 1)
     for _ in range(args.warmup):
         cpu_baseline(args, scene, bundles, sets, min(n_sample, 2))
@@ -240,10 +308,11 @@ def run_reference(args):
     value = frames / dt
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE config 2 distributions, seeded)",
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong" if args.config == 4 else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE distributions, seeded)",
         "impl": "reference",
-        "config": dict(workload_config(args, f"host threads x{threads}"), sample_envs_per_step=n_sample),
+        "config": workload_config(args, args.gpus),
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "port",
                          "sample": r["sample"]},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -251,39 +320,113 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def blend_roofline(per_stage, dom, pid, w2, args, clk, hbm_peak, peak_kind, n_pix, n_av, ms_step):
+    """The scene blend's roofline. It is a compute-side kernel (its records and rectangles are L2
+    hits; DRAM traffic is the frames): the headline is the FP32 pipe -- flops per contribution
+    (SASS-counted constant) x this run's contribution count / this run's blend time, against
+    148 SMs x 128 lanes x 2 x the measured SM clock. The issue-slot and HBM views are attached."""
+    ms = per_stage[dom]
+    contribs = w2[pid, 4] / args.steps
+    peak_f = 148 * 128 * 2 * clk * 1e6 / 1e12
+    ach_f = contribs * BLEND_FLOPS_PER_CONTRIBUTION / (ms / 1e3) / 1e12
+    alg = algorithmic_bytes("blend", pid, args.gaussians, n_av, w2, n_pix, args.steps)
+    ach_b = alg / (ms / 1e3) / 1e9
+    ncu = committed_ncu(dom)
+    roof = {"bound": "fp32", "kernel": dom, "achieved": ach_f, "peak": peak_f, "unit": "TFLOP/s",
+            "frac": ach_f / peak_f, "traffic": None,
+            "peak_kind": f"148 SMs x 128 FP32 lanes x 2 x {clk:.0f} MHz (this run's median SM clock)",
+            "flops_per_contribution": BLEND_FLOPS_PER_CONTRIBUTION, "contributions_per_step": int(contribs),
+            "ms_per_step": ms, "share_of_step": ms / ms_step,
+            "hbm": {"achieved": ach_b, "peak": hbm_peak, "unit": "GB/s", "frac": ach_b / hbm_peak,
+                    "peak_kind": peak_kind, "alg_bytes_per_step": alg}}
+    if ncu is not None:
+        roof["traffic"] = ncu["dram_bytes_per_launch"] * ncu["launches_per_step"]
+        roof["traffic_source"] = ncu["source"]
+        if ncu.get("warp_inst_per_launch"):
+            inst = ncu["warp_inst_per_launch"] * ncu["launches_per_step"]
+            peak_i = 148 * 4 * clk * 1e6 / 1e9
+            ach_i = inst / (ms / 1e3) / 1e9
+            roof["issue"] = {"warp_inst_per_step": inst, "achieved_ginst_per_s": ach_i, "peak_ginst_per_s": peak_i,
+                             "frac": ach_i / peak_i,
+                             "note": "instruction count from the committed ncu capture of this bench command "
+                                     f"({ncu['source']}), divided by this run's live blend time"}
+    return roof
+
+
+def hbm_roofline(per_stage, dom, sname, pid, w2, args, hbm_peak, peak_kind, n_pix, n_av, ms_step):
+    ms = per_stage[dom]
+    alg = algorithmic_bytes(sname, pid, args.gaussians, n_av, w2, n_pix, args.steps)
+    ach = alg / (ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+            "frac": ach / hbm_peak, "traffic": None, "peak_kind": peak_kind, "alg_bytes_per_step": alg,
+            "ms_per_step": ms, "share_of_step": ms / ms_step}
+    ncu = committed_ncu(dom)
+    if ncu is not None:
+        roof["traffic"] = ncu["dram_bytes_per_launch"] * ncu["launches_per_step"]
+        roof["traffic_source"] = ncu["source"]
+    return roof
+
+
 def main():
     args = parse()
+    world, rank, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; refusing to run", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args)
         return
     import torch
     import torch.distributed as dist
-    from paper_2604_12626_b200 import _native as N
-    from paper_2604_12626_b200.batch import BatchRenderer
+    from paper_2604_12626_b200.batch import BatchRenderer, HostPipeline
+    from paper_2604_12626_b200.parallel import gather_observations
 
-    world, rank, local = dist_env()
+    if torch.cuda.device_count() <= local:
+        print(f"bench.py: rank {rank} needs cuda:{local}, {torch.cuda.device_count()} visible", file=sys.stderr)
+        sys.exit(2)
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n_sets = args.warmup + args.steps
     scene, bundles, box, sets = workload(args, world, rank, n_sets)
+    n_local = len(sets[0][0])
+    n_all = total_envs(args, world)
     br = BatchRenderer(scene, bundles, start_offsets=start_offsets(len(bundles)), background=(1.0, 1.0, 1.0))
     stage_ms = np.zeros(2 * len(STAGES))
     work = np.zeros(12, dtype=np.int64)
-
-    from paper_2604_12626_b200.renderer import render_frames
-    shapes = {"color": (args.envs, args.height, args.width, 3), "alpha": (args.envs, args.height, args.width),
-              "depth": (args.envs, args.height, args.width)}
-    frames_out = [{k: torch.empty(v, dtype=torch.float32, device="cuda") for k, v in shapes.items()} for _ in range(2)]
+    payload = bool(args.gather)
+    shapes = {"color": ((n_local, args.height, args.width, 3), torch.float32),
+              "alpha": ((n_local, args.height, args.width), torch.float32),
+              "depth": ((n_local, args.height, args.width), torch.float32)}
+    if payload:
+        shapes.update({"rgb8": ((n_local, args.height, args.width, 3), torch.uint8),
+                       "depth16": ((n_local, args.height, args.width), torch.float16)})
+    frames_out = [{k: torch.empty(s, dtype=d, device="cuda") for k, (s, d) in shapes.items()} for _ in range(2)]
+    gather_stream = torch.cuda.Stream()
+    gather_ms = []
 
     def step(i, instrumented=False, wait=True):
         cams, times = sets[i]
-        opts = dict(avatars=br.avatars, sim_times=times, context=br.context, stats=False, wait=wait,
-                    out=dict(frames_out[i % 2]))
-        if instrumented:
-            opts["stage_ms"] = stage_ms
-            opts["work"] = work
-        return render_frames(br.scene, cams, br.background, **opts)
+        kw = dict(stats=False, wait=wait, out=dict(frames_out[i % 2]), payload=payload)
+        if instrumented:  # the layer pass serialized behind the scene pass: stage times add up
+            kw.update(stage_ms=stage_ms, work=work, serialize=True)
+        return br.render(cams, times, **kw)
+
+    def gather(i):
+        """The step's payload to rank 0 (NCCL) on a side stream, after the render (event)."""
+        ready = torch.cuda.Event()
+        ready.record()
+        with torch.cuda.stream(gather_stream):
+            gather_stream.wait_event(ready)
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record()
+            if world > 1:
+                f = frames_out[i % 2]
+                gather_observations(f["rgb8"], f["depth16"], n_all)
+            g1.record()
+            gather_ms.append((g0, g1))
 
     def retire(pending):
         """Check the oldest queued render; on a workspace-growth retry redo it and every later
@@ -296,10 +439,19 @@ def main():
             pending.clear()
             for j in redo:
                 step(j)
+            if payload:
+                for j in redo:
+                    gather(j)
+            return
+        if payload:
+            gather(i)
 
     for i in range(args.warmup):
         step(i)
+        if payload:
+            gather(i)
     torch.cuda.synchronize()
+    gather_ms.clear()
     if world > 1:
         dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -318,31 +470,40 @@ def main():
                 retire(pending)
         while pending:
             retire(pending)
+        torch.cuda.current_stream().wait_stream(gather_stream)
         ev1.record()
         torch.cuda.synchronize()
     launches = br.context.kernel_launches() - launches0
     retries_timed = br.context.render_retries() - retries_t0
+    g_ms = sum(a.elapsed_time(b) for a, b in gather_ms) / max(1, args.steps) if payload else 0.0
     # per-stage CUDA-event timers and work counters from a separate, untimed pass over the same
-    # steps (the timers' events and their resolution stay out of the timed region)
+    # steps, with the layer pass serialized on the render stream so the stages sum to the step
     for i in range(args.steps):
         step(args.warmup + i, instrumented=True)
     br.context.sync_stats()
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([ms, g_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    frames = args.envs * world * args.steps
+    ms_max, g_ms_max = float(t[0].item()), float(t[1].item())
+    frames = n_all * args.steps
     value = frames / (ms_max / 1e3)
+    per_rank_value = n_local * args.steps / (ms / 1e3)
+    pr = torch.tensor([per_rank_value], dtype=torch.float64, device="cuda")
+    per_rank = [pr.clone() for _ in range(world)]
+    if world > 1:
+        dist.all_gather(per_rank, pr)
+    per_rank = [float(x.item()) for x in per_rank]
 
     # end to end through the public API with host buffers: camera/time structs go host->device,
-    # frames come back to pinned host memory every step
+    # the step's frames (float32 RGB + alpha + depth; the uint8/fp16 payload with --gather or at
+    # config 4) come back to pinned host memory every step
     e2e = None
     if not args.no_e2e:
-        from paper_2604_12626_b200.batch import HostPipeline
-        pipe = HostPipeline(br, args.envs, args.height, args.width)
+        e2e_payload = payload or args.config == 4
+        pipe = HostPipeline(br, n_local, args.height, args.width, payload=e2e_payload)
         retries0 = br.context.render_retries()
         for i in range(max(args.warmup, 3)):  # the pipeline's buffers and allocator reach steady state
             pipe.submit(sets[i][0], sets[i][1])
@@ -363,9 +524,10 @@ def main():
         te = torch.tensor([ems], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        h, w = args.height, args.width
         e2e = {"value": frames / (float(te.item()) / 1e3), "unit": "frames/s", "render_retries": e2e_retries,
-               "h2d_bytes_per_step": args.envs * (192 + 8), "d2h_bytes_per_step": args.envs * h * w * (12 + 4 + 4)}
+               "h2d_bytes_per_step": n_local * (CAMERA_BYTES + (TIME_BYTES if bundles else 0)),
+               "d2h_bytes_per_step": pipe.bytes_per_submit,
+               "download": "uint8 RGB + fp16 depth payload" if e2e_payload else "float32 RGB + alpha + depth"}
 
     if rank != 0:
         if world > 1:
@@ -374,64 +536,35 @@ def main():
     peak, peak_kind = measured_peaks()
     stage = stage_ms.reshape(2, len(STAGES))
     w2 = work.reshape(2, 6)
-    n_pix = args.envs * args.width * args.height
+    n_pix = n_local * args.width * args.height
     n_av = sum(b.canonical.n for b in bundles)
     per_stage = {}
     for p, name in ((0, "scene"), (1, "layer")):
         for k, sname in enumerate(STAGES):
             if stage[p, k] > 0:
                 per_stage[f"{name}.{sname}"] = stage[p, k] / args.steps
-    # the layer pass's preprocessing runs on a side stream under the scene blend, so its stage
-    # times are overlapped wall times; the dominant kernel is chosen among serial stages
-    serial = {k: v for k, v in per_stage.items() if k.startswith("scene.") or k == "layer.composite"}
-    dom = max(serial, key=serial.get)
+    ms_step = ms_max / args.steps
+    dom = max(per_stage, key=per_stage.get)
     pname, sname = dom.split(".")
     pid = 0 if pname == "scene" else 1
-    alg = algorithmic_bytes(sname, pid, args.gaussians, n_av, w2, n_pix, args.steps)
-    achieved = alg / (per_stage[dom] / 1e3) / 1e9
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                "alg_bytes_per_step": alg, "ms_per_step": per_stage[dom],
-                "share_of_step": per_stage[dom] / (ms_max / args.steps)}
-    traffic = measured_traffic(dom)
-    if traffic is not None:
-        roofline["traffic"] = traffic["dram_bytes_per_launch"] * traffic["launches_per_step"]
-        roofline["traffic_source"] = traffic["source"]
+    clk = (clocks.summary() or {}).get("sm_mhz") or 1965.0
     if sname == "blend":
-        # The blend is not HBM-bound (records and rectangles are L2 hits, DRAM traffic is the
-        # frames): it is issue-bound on its float32 contribution chain. FP32-pipe lane operations
-        # per contribution, counted from the SASS of blend_kernel<0,0> (an FFMA2 is two): the two
-        # axis rows (2 FFMA2) and h (2 FFMA), alpha error (1 FFMA), alpha (FMUL, FMNMX; the EX2 is
-        # on the MUFU pipe), weight (FMUL), transmittance (FFMA), colour and depth sums (2 FFMA2),
-        # A (FADD), its error bound (3 FFMA), z bound (FMNMX), cutoff test (FADD).
-        per_contrib = 4 + 2 + 1 + 2 + 1 + 1 + 4 + 1 + 3 + 1 + 1
-        contribs = w2[pid, 4] / args.steps
-        clk = (clocks.summary() or {}).get("sm_mhz") or 1965.0
-        peak_t = 148 * 128 * clk * 1e6 / 1e12  # FP32 lane-instructions per second (1 FFMA = 1)
-        achieved_t = contribs * per_contrib / (per_stage[dom] / 1e3) / 1e12
-        if traffic is not None and traffic.get("warp_inst_per_launch"):
-            # the bound that actually binds: instruction issue (4 schedulers per SM, 1 warp
-            # instruction per cycle each); instructions per launch from the committed ncu capture
-            # of the same command, divided by this run's live blend time
-            inst = traffic["warp_inst_per_launch"]
-            peak_i = 148 * 4 * clk * 1e6 / 1e9
-            ach_i = inst / (per_stage[dom] / 1e3) / 1e9
-            roofline["issue"] = {"warp_inst_per_launch": inst, "achieved_ginst_per_s": ach_i,
-                                 "peak_ginst_per_s": peak_i,
-                                 "peak_kind": f"148 SMs x 4 schedulers x {clk:.0f} MHz (measured SM clock)",
-                                 "frac": ach_i / peak_i, "source": traffic["source"]}
-        roofline["compute"] = {"pipe": "fp32", "contributions_per_step": int(contribs),
-                               "fp32_inst_per_contribution": per_contrib,
-                               "achieved_tinst_per_s": achieved_t, "peak_tinst_per_s": peak_t,
-                               "peak_kind": f"148 SMs x 128 FP32 lanes x {clk:.0f} MHz (measured SM clock)",
-                               "frac": achieved_t / peak_t}
+        roofline = blend_roofline(per_stage, dom, pid, w2, args, clk, peak, peak_kind, n_pix, n_av, ms_step)
+    else:
+        roofline = hbm_roofline(per_stage, dom, sname, pid, w2, args, peak, peak_kind, n_pix, n_av, ms_step)
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64 geometry + exact decisions (f32 blend chain with error bounds, f64 fixups)", "data": "synthetic (seeded, BASELINE distributions)",
-        "config": workload_config(args, f"env-sharded x{world}"),
-        "gpu_launches": None, "roofline": roofline, "e2e": e2e,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong" if args.config == 4 else "weak", "vs_baseline": None,
+        "dtype": "f64 geometry + exact decisions (f32 blend chain with error bounds, f64 fixups)",
+        "data": "synthetic (seeded, BASELINE distributions)",
+        "config": workload_config(args, world),
+        "gpu_launches": launches, "roofline": roofline, "e2e": e2e,
+        "per_rank_frames_per_s": per_rank, "envs_per_rank": n_local,
         "stages_ms_per_step": {k: round(v, 4) for k, v in per_stage.items()},
+        "stages_note": "CUDA-event timers from a separate untimed pass with the avatar layer serialized "
+                       "behind the scene pass (in the timed steps the layer runs concurrently on a side stream)",
+        "stages_sum_ms": round(sum(per_stage.values()), 4),
         "work_per_step": {"scene_visible": int(w2[0, 0] / args.steps),
                           "scene_records_loaded": int(w2[0, 2] / args.steps),
                           "scene_rects_scanned": int(w2[0, 3] / args.steps),
@@ -443,12 +576,17 @@ def main():
                           "scene_fixup_pixels": int(w2[0, 5] / args.steps),
                           "layer_fixup_pixels": int(w2[1, 5] / args.steps)},
         "clocks": clocks.summary(),
+        "render_retries": retries_timed,  # renders re-run to grow capacity-sized buffers
     }
-    line["gpu_launches"] = launches
-    line["render_retries"] = retries_timed  # renders re-run to grow capacity-sized buffers
+    if payload:
+        per_frame = args.width * args.height * (3 + 2)
+        line["gather"] = {"communicator_size": world, "backend": "nccl" if world > 1 else "none (1 rank)",
+                          "ms_per_step_max_over_ranks": g_ms_max,
+                          "bytes_to_rank0_per_step": per_frame * (n_all - n_local) if world > 1 else 0,
+                          "payload_bytes_per_frame": per_frame}
     if world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        line["cpu_baseline"] = cpu_baseline(args, scene, bundles, sets, args.cpu_envs or max(2, min(args.envs, threads)))
+        line["cpu_baseline"] = cpu_baseline(args, scene, bundles, sets, args.cpu_envs or max(2, min(16, threads)))
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -155,7 +155,14 @@ typedef struct sn_render_opts {
                                and must stay valid until then. */
     int32_t exact;          /* 1: every pixel takes the float64 path (the blend's fixup walk) instead of
                                the float32 chain with error bounds -- validation / reference mode */
-    int32_t pad;
+    int32_t serialize;      /* 1: the avatar-layer pass runs on the caller's stream after the scene pass
+                               instead of concurrently on the context's side stream (stage_ms then sum
+                               to the render's time) */
+    uint8_t *rgb8;          /* device (E,H,W,3) or NULL: the observation payload's uint8 colour, written
+                               by the epilogues that finalize each pixel (blend, composite, fixups) with
+                               frame_io.save_color_png's rule (clip, x*255+0.5 in float64, truncation)
+                               on the float32 colour the frame holds */
+    uint16_t *depth16;      /* device (E,H,W) or NULL: fp16 depth (round to nearest) of the same pixels */
 } sn_render_opts;
 
 typedef struct sn_context sn_context;

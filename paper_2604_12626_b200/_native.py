@@ -54,7 +54,7 @@ class SnAvatars(ctypes.Structure):
 class SnRenderOpts(ctypes.Structure):
     _fields_ = [("tiled", ctypes.c_int32), ("binning", ctypes.c_int32), ("avatar_active", P),
                 ("contrib_scene", P), ("contrib_layer", P), ("stats", P), ("stage_ms", P), ("work", P),
-                ("exact", ctypes.c_int32), ("pad", ctypes.c_int32)]
+                ("exact", ctypes.c_int32), ("serialize", ctypes.c_int32), ("rgb8", P), ("depth16", P)]
 
 
 STAGES = ("pose", "count", "scan", "emit", "depth_sort", "permute", "pair_scan", "bin_count", "bin_scatter", "ranges",

@@ -31,14 +31,17 @@ class BatchRenderer:
         return self.scene.device
 
     def render(self, cameras, sim_times=None, avatar_active=None, tiled=True, contrib=False, stats=False,
-               exact=False, out=None, wait=True):
+               exact=False, out=None, wait=True, payload=False, serialize=False, stage_ms=None, work=None,
+               binning=-1):
         """wait=False: queue the render and return (see render_frames); pair every such call with
-        a later self.context.render_wait()."""
+        a later self.context.render_wait(). payload=True also returns the uint8 / fp16 observation
+        payload (rgb8, depth16) written by the render's epilogues."""
         if self.avatars is not None and sim_times is None:
             sim_times = np.zeros(len(cameras))
         return render_frames(self.scene, cameras, self.background, avatars=self.avatars, sim_times=sim_times,
                              tiled=tiled, context=self.context, contrib=contrib, stats=stats,
-                             avatar_active=avatar_active, exact=exact, out=out, wait=wait)
+                             avatar_active=avatar_active, exact=exact, out=out, wait=wait, payload=payload,
+                             serialize=serialize, stage_ms=stage_ms, work=work, binning=binning)
 
     def render_to_host(self, cameras, sim_times=None, host_out=None):
         """render() followed by a device->host copy into pinned buffers (the end-to-end path)."""
@@ -62,23 +65,31 @@ class HostPipeline:
     submit(cameras, sim_times) -> slot index; the frames of a slot are valid in host[slot] after
     wait(slot), until the slot is reused two submits later."""
 
-    KEYS = ("color", "alpha", "depth")
+    FRAME_KEYS = ("color", "alpha", "depth")
+    PAYLOAD_KEYS = ("rgb8", "depth16")
 
-    def __init__(self, renderer, n_envs, height, width, depth=2):
+    def __init__(self, renderer, n_envs, height, width, depth=2, payload=False):
+        """payload=True downloads the uint8 RGB + fp16 depth observation payload the render writes
+        (frame_io's rule) instead of the float32 frames."""
         self.r = renderer
+        self.payload = payload
+        self.KEYS = self.PAYLOAD_KEYS if payload else self.FRAME_KEYS
         dev = renderer.device
         # renders on their own stream, not the legacy default stream (whose implicit
         # synchronization would serialize them with the copies)
         self.render_stream = torch.cuda.Stream(dev)
         self.copy_stream = torch.cuda.Stream(dev)
-        shapes = {"color": (n_envs, height, width, 3), "alpha": (n_envs, height, width),
-                  "depth": (n_envs, height, width)}
-        self.host = [{k: torch.empty(shapes[k], dtype=torch.float32, pin_memory=True) for k in self.KEYS}
+        shapes = {"color": ((n_envs, height, width, 3), torch.float32), "alpha": ((n_envs, height, width), torch.float32),
+                  "depth": ((n_envs, height, width), torch.float32),
+                  "rgb8": ((n_envs, height, width, 3), torch.uint8), "depth16": ((n_envs, height, width), torch.float16)}
+        self.host = [{k: torch.empty(shapes[k][0], dtype=shapes[k][1], pin_memory=True) for k in self.KEYS}
                      for _ in range(depth)]
         # device frames of each slot, rendered into in place: no allocation per step (a caching-
         # allocator miss would cudaMalloc / cudaFree and serialize the render with the copies)
-        self.dev = [{k: torch.empty(shapes[k], dtype=torch.float32, device=dev) for k in self.KEYS}
+        dkeys = self.FRAME_KEYS + (self.PAYLOAD_KEYS if payload else ())
+        self.dev = [{k: torch.empty(shapes[k][0], dtype=shapes[k][1], device=dev) for k in dkeys}
                     for _ in range(depth)]
+        self.bytes_per_submit = sum(t.numel() * t.element_size() for t in self.host[0].values())
         self.done = [None] * depth
         self.pending = []  # (slot, cameras, sim_times, ready event) queued, not yet checked
         self.i = 0
@@ -91,10 +102,10 @@ class HostPipeline:
                 # the render overwrites this slot's device frames once their download (two submits
                 # back) is done: a device-side wait, so the host keeps queueing ahead of the GPU
                 self.render_stream.wait_event(self.done[slot])
-            out = self.r.render(cameras, sim_times, out=dict(self.dev[slot]), wait=False)
+            out = self.r.render(cameras, sim_times, out=dict(self.dev[slot]), wait=False, payload=self.payload)
             ready = torch.cuda.Event()
             ready.record(self.render_stream)
-        self.dev[slot] = {k: out[k] for k in self.KEYS}  # the tensors the render writes
+        self.dev[slot] = {k: out[k] for k in self.dev[slot]}  # the tensors the render writes
         self.pending.append((slot, cameras, sim_times, ready))
         if len(self.pending) > 1:
             self._retire()
@@ -122,8 +133,8 @@ class HostPipeline:
         self.pending = []
         for s, c, t in redo:
             with torch.cuda.stream(self.render_stream):
-                out = self.r.render(c, t, out=dict(self.dev[s]))
-                self.dev[s] = {k: out[k] for k in self.KEYS}
+                out = self.r.render(c, t, out=dict(self.dev[s]), payload=self.payload)
+                self.dev[s] = {k: out[k] for k in self.dev[s]}
                 ev = torch.cuda.Event()
                 ev.record(self.render_stream)
             self._copy(s, ev)

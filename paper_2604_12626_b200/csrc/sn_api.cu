@@ -422,6 +422,8 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     bl.fix_list = w.fix.as<uint32_t>();
     bl.fix_count = ctx->fixcnt.as<unsigned>() + pass_id;
     bl.force_exact = opts ? opts->exact : 0;
+    bl.rgb8 = opts ? opts->rgb8 : nullptr;
+    bl.depth16 = opts ? opts->depth16 : nullptr;
     SN_CUDA(cudaMemsetAsync(bl.fix_count, 0, sizeof(unsigned), st));
     if (work) {
         if (ctx->work_dst[pass_id]) {  // previous chunk's counters still in flight
@@ -821,7 +823,7 @@ static int render_once(sn_context *ctx, const sn_cloud *scene, const sn_cloud *l
     // the layer pass runs on the context's side stream: only its blend waits for the scene blend
     const bool two_pass = with_layer || with_avatars;
     cudaStream_t lst = st;
-    if (two_pass) {
+    if (two_pass && !(opts && opts->serialize)) {
         if (!ctx->side) {
             // highest priority: the layer pass is short and its kernels (and host round trips) must
             // not queue behind the scene blend's CTAs, or the composite waits for it
@@ -889,12 +891,16 @@ static int render_once(sn_context *ctx, const sn_cloud *scene, const sn_cloud *l
         r = run_pass(ctx, 1, layer_spec, e0, ec, W, H, tiled, z_lo, z_bits, opts, color, alpha, depth, derr, lst,
                      e0 / chunk);
         if (r != SN_OK) return r;
-        SN_CUDA(cudaEventRecord(ctx->ev_layer, lst));
-        SN_CUDA(cudaStreamWaitEvent(st, ctx->ev_layer, 0));  // both blends done: composite on st
+        if (lst != st) {
+            SN_CUDA(cudaEventRecord(ctx->ev_layer, lst));
+            SN_CUDA(cudaStreamWaitEvent(st, ctx->ev_layer, 0));  // both blends done: composite on st
+        }
         r = finish_layer(ctx, opts, st);
         if (r != SN_OK) return r;
-        SN_CUDA(cudaEventRecord(ctx->ev_scene, st));
-        SN_CUDA(cudaStreamWaitEvent(lst, ctx->ev_scene, 0));  // next chunk's layer pass reuses the buffers
+        if (lst != st) {
+            SN_CUDA(cudaEventRecord(ctx->ev_scene, st));
+            SN_CUDA(cudaStreamWaitEvent(lst, ctx->ev_scene, 0));  // next chunk's layer pass reuses the buffers
+        }
     }
     return SN_OK;
 }

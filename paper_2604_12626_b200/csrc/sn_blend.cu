@@ -30,6 +30,8 @@
 #include "sn_common.cuh"
 #include "sn_internal.h"
 
+#include <cuda_fp16.h>
+
 #include <cstring>
 #include <type_traits>
 
@@ -249,6 +251,26 @@ __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1
         f.kb = kEpsExact;
     }
     return m;
+}
+
+// The observation payload of a finished pixel (sn_render_opts.rgb8 / depth16), from the float32
+// values the frame holds: frame_io.save_color_png's uint8 rule (frame_io.py:13-14: clip, x * 255
+// + 0.5 in float64, truncation) and fp16 depth -- the same bytes sn_quantize_frames writes, fused
+// into each epilogue that finalizes a pixel so only the quantized frame leaves for the gather.
+__device__ __forceinline__ uint8_t quant8(float x) {
+    double v = (double)x;
+    v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+    return (uint8_t)(v * 255.0 + 0.5);
+}
+__device__ __forceinline__ void store_payload(const BlendArgs &b, int64_t pix, float r, float g, float bl,
+                                              float depth) {
+    if (b.rgb8) {
+        uint8_t *o = b.rgb8 + 3 * pix;
+        o[0] = quant8(r);
+        o[1] = quant8(g);
+        o[2] = quant8(bl);
+    }
+    if (b.depth16) b.depth16[pix] = __half_as_ushort(__float2half_rn(depth));
 }
 
 __device__ __forceinline__ bool covers(ushort4 r, int tx, int ty) {
@@ -532,12 +554,16 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
     if (b.contrib) b.contrib[pix] = nc;
     if (MODE == 0) {
         float *oc = b.color + 3 * pix;
-        oc[0] = np_clipf(__fmaf_rn((float)cam.background[0], T, cr), 0.0f, 1.0f);
-        oc[1] = np_clipf(__fmaf_rn((float)cam.background[1], T, cg), 0.0f, 1.0f);
-        oc[2] = np_clipf(__fmaf_rn((float)cam.background[2], T, cb), 0.0f, 1.0f);
+        const float o0 = np_clipf(__fmaf_rn((float)cam.background[0], T, cr), 0.0f, 1.0f);
+        const float o1 = np_clipf(__fmaf_rn((float)cam.background[1], T, cg), 0.0f, 1.0f);
+        const float o2 = np_clipf(__fmaf_rn((float)cam.background[2], T, cb), 0.0f, 1.0f);
+        oc[0] = o0;
+        oc[1] = o1;
+        oc[2] = o2;
         b.alpha[pix] = alpha;
         b.depth[pix] = depth;
         if (b.derr) b.derr[pix] = A > 0.0f ? d_err : 0.0f;
+        store_payload(b, pix, o0, o1, o2, depth);
         return;
     }
     float fc0 = 0.0f, fc1 = 0.0f, fc2 = 0.0f;
@@ -553,6 +579,7 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
         oc[2] = fc2;
         b.alpha[pix] = alpha;
         b.depth[pix] = depth;
+        store_payload(b, pix, fc0, fc1, fc2, depth);
         return;
     }
     // MODE 2: the layer frame goes to its own buffers; composite_kernel merges it into the scene
@@ -602,11 +629,15 @@ __global__ void __launch_bounds__(kBlock) composite_kernel(BlendArgs b) {
     if (!use_front || flag) return;
     const float *lc = b.lcolor + 3 * pix;
     float *oc = b.color + 3 * pix;
-    oc[0] = __fmaf_rn(lc[0], la, oc[0] * (1.0f - la));
-    oc[1] = __fmaf_rn(lc[1], la, oc[1] * (1.0f - la));
-    oc[2] = __fmaf_rn(lc[2], la, oc[2] * (1.0f - la));
+    const float o0 = __fmaf_rn(lc[0], la, oc[0] * (1.0f - la));
+    const float o1 = __fmaf_rn(lc[1], la, oc[1] * (1.0f - la));
+    const float o2 = __fmaf_rn(lc[2], la, oc[2] * (1.0f - la));
+    oc[0] = o0;
+    oc[1] = o1;
+    oc[2] = o2;
     b.alpha[pix] = __fmaf_rn(b.alpha[pix], 1.0f - la, la);
     if (la >= 0.5f) b.depth[pix] = ld;
+    store_payload(b, pix, o0, o1, o2, la >= 0.5f ? ld : bd);
 }
 
 // ---- exact (float64) per-pixel walk: the fixup path ----
@@ -998,10 +1029,12 @@ __global__ void __launch_bounds__(256) fixup_layer_kernel(BlendArgs b) {
             for (int c = 0; c < 3; ++c) oc[c] = (float)(fc[c] * alpha + (double)bc[c] * (1.0 - alpha));
             b.alpha[pix] = (float)(alpha + (double)ba * (1.0 - alpha));
             b.depth[pix] = (float)(alpha >= 0.5 ? depth : bd);
+            store_payload(b, pix, oc[0], oc[1], oc[2], b.depth[pix]);
         } else if (exact_back) {
             for (int c = 0; c < 3; ++c) oc[c] = bc[c];
             b.alpha[pix] = ba;
             b.depth[pix] = (float)bd;
+            store_payload(b, pix, bc[0], bc[1], bc[2], (float)bd);
         }
     }
     if (b.contribs && threadIdx.x == 0 && contribs) atomicAdd(b.contribs, contribs);
@@ -1071,10 +1104,12 @@ __global__ void __launch_bounds__(256, SN_FIXUP_MIN_BLOCKS) fixup_kernel(BlendAr
                 for (int c = 0; c < 3; ++c) oc[c] = (float)(fc[c] * alpha + (double)bc[c] * (1.0 - alpha));
                 b.alpha[pix] = (float)(alpha + (double)ba * (1.0 - alpha));
                 b.depth[pix] = (float)(alpha >= 0.5 ? depth : bd);
+                store_payload(b, pix, oc[0], oc[1], oc[2], b.depth[pix]);
             } else if (exact_back) {
                 for (int c = 0; c < 3; ++c) oc[c] = bc[c];
                 b.alpha[pix] = ba;
                 b.depth[pix] = (float)bd;
+                store_payload(b, pix, bc[0], bc[1], bc[2], (float)bd);
             }
             continue;
         }
@@ -1087,6 +1122,7 @@ __global__ void __launch_bounds__(256, SN_FIXUP_MIN_BLOCKS) fixup_kernel(BlendAr
             oc[2] = (float)np_clip((double)f.cb + cam.background[2] * f.T, 0.0, 1.0);
             b.alpha[pix] = (float)alpha;
             b.depth[pix] = (float)depth;
+            store_payload(b, pix, oc[0], oc[1], oc[2], (float)depth);
             // the stored depth is the float64 walk's rounded to float32 (and the walk's prefix-product
             // transmittance / table exp differ from the sequential reference by a few float64 ulps):
             // a band of ~2 float ulps makes a layer fixup whose exact front depth falls inside it
@@ -1103,6 +1139,7 @@ __global__ void __launch_bounds__(256, SN_FIXUP_MIN_BLOCKS) fixup_kernel(BlendAr
         for (int c = 0; c < 3; ++c) oc[c] = (float)fc[c];
         b.alpha[pix] = (float)alpha;
         b.depth[pix] = (float)depth;
+        store_payload(b, pix, oc[0], oc[1], oc[2], (float)depth);
     }
     if (b.contribs && lane == 0 && contribs) atomicAdd(b.contribs, contribs);
 }

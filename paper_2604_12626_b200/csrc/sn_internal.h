@@ -152,6 +152,8 @@ struct BlendArgs {
     uint32_t *fix_list;     // (ec*H*W) pixels deferred to the float64 fixup (el*H*W + pixel)
     unsigned *fix_count;    // device counter, zeroed before the blend
     int32_t force_exact;    // every pixel to the float64 fixup (sn_render_opts.exact)
+    uint8_t *rgb8;          // (E,H,W,3) observation payload colour, or null (written where a pixel is final)
+    uint16_t *depth16;      // (E,H,W) fp16 payload depth, or null
     unsigned long long *loads;  // device counter: records gathered into shared memory (may be null)
     unsigned long long *scans;  // device counter: rectangles examined by source-0 tiles (may be null)
     unsigned long long *contribs;  // device counter: (pixel, splat) contributions (may be null)

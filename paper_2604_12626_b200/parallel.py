@@ -55,3 +55,30 @@ def gather_observations(rgb, depth, n_envs, dst=0, group=None):
     rgb_all = torch.cat([t[:c] for t, c in zip(rgb_list, counts)])
     depth_all = torch.cat([t[:c] for t, c in zip(depth_list, counts)]).view(torch.float16)
     return rgb_all, depth_all
+
+
+def render_sharded(renderer, cameras, sim_times=None, gather=True, dst=0, group=None):
+    """One step of the env-sharded batch: this rank renders its contiguous block
+    env_shard(E, G, rank) of the E environments with `renderer` (a batch.BatchRenderer holding its
+    own replica of the scene and avatar set), the render's epilogues write the uint8 RGB + fp16 depth
+    payload, and -- when `gather` -- the payload of all E envs is gathered to rank `dst` in env order.
+
+    Returns (local, gathered): local = the render_frames dict of this rank's block (float frames +
+    payload), gathered = (rgb8 (E,H,W,3), depth16 (E,H,W)) on dst, None elsewhere. With the gloo
+    backend (CPU tests) the payload is staged through host memory; NCCL gathers device tensors.
+    """
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    n = len(cameras)
+    a, b = env_shard(n, world, rank)
+    times = None if sim_times is None else list(sim_times)[a:b]
+    local = renderer.render(list(cameras)[a:b], times, payload=True)
+    if not gather:
+        return local, None
+    if world == 1:
+        return local, (local["rgb8"], local["depth16"])
+    rgb, depth = local["rgb8"], local["depth16"]
+    if dist.get_backend(group) != "nccl":
+        rgb, depth = rgb.cpu(), depth.cpu()
+    out = gather_observations(rgb, depth, n, dst=dst, group=group)
+    return local, (out if rank == dst else None)

@@ -58,12 +58,15 @@ def _nonempty(c):
 
 def render_frames(scene, cameras, background, layer=None, avatars=None, sim_times=None, tiled=True,
                   context=None, contrib=False, stats=True, avatar_active=None, stage_ms=None, work=None,
-                  binning=-1, exact=False, out=None, wait=True):
+                  binning=-1, exact=False, out=None, wait=True, payload=False, serialize=False):
     """One sn_render call over E cameras. Returns a dict of device tensors:
     color (E,H,W,3), alpha (E,H,W), depth (E,H,W) float32; stats (E,5) int64; optionally
-    contrib_scene / contrib_layer (E,H,W) int32. The context keeps the pass intermediates for
-    the sn_get_* views. wait=False queues the render (sn_render_async) and returns at once: the
-    frames are valid only after context.render_wait() for it returns False."""
+    contrib_scene / contrib_layer (E,H,W) int32 and, with payload=True, the observation payload
+    rgb8 (E,H,W,3) uint8 + depth16 (E,H,W) float16 written by the render's own epilogues
+    (frame_io's uint8 rule). The context keeps the pass intermediates for the sn_get_* views.
+    wait=False queues the render (sn_render_async) and returns at once: the frames are valid only
+    after context.render_wait() for it returns False. serialize=True runs the avatar layer after
+    the scene pass on the same stream (per-stage timers then add up to the render)."""
     lib = N.load()
     ctx = context or N.default_context()
     dscene = DeviceCloud.wrap(scene)
@@ -73,16 +76,23 @@ def render_frames(scene, cameras, background, layer=None, avatars=None, sim_time
     cams = camera_array(cameras, background)
     if out is None:  # caller-owned outputs (e.g. HostPipeline's ring) avoid per-call allocations
         out = {}
-    shapes = {"color": (e, h, w, 3), "alpha": (e, h, w), "depth": (e, h, w)}
-    for k, shp in shapes.items():
+    shapes = {"color": ((e, h, w, 3), torch.float32), "alpha": ((e, h, w), torch.float32),
+              "depth": ((e, h, w), torch.float32)}
+    if payload:
+        shapes.update({"rgb8": ((e, h, w, 3), torch.uint8), "depth16": ((e, h, w), torch.float16)})
+    for k, (shp, dt) in shapes.items():
         t = out.get(k)
         same_dev = t is not None and t.device.type == dev.type and (t.device.index or 0) == (dev.index or 0)
-        if t is None or tuple(t.shape) != shp or t.dtype != torch.float32 or not same_dev or not t.is_contiguous():
-            out[k] = torch.empty(shp, dtype=torch.float32, device=dev)
+        if t is None or tuple(t.shape) != shp or t.dtype != dt or not same_dev or not t.is_contiguous():
+            out[k] = torch.empty(shp, dtype=dt, device=dev)
     opts = N.SnRenderOpts()
     opts.tiled = 1 if tiled else 0
     opts.binning = int(binning)
     opts.exact = 1 if exact else 0
+    opts.serialize = 1 if serialize else 0
+    if payload:
+        opts.rgb8 = out["rgb8"].data_ptr()
+        opts.depth16 = out["depth16"].data_ptr()
     if stats:
         out["stats"] = torch.zeros((e, 5), dtype=torch.int64, device=dev)
         opts.stats = out["stats"].data_ptr()
