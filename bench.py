@@ -251,15 +251,23 @@ def algorithmic_bytes(stage, pass_id, n_gauss, n_avatar_gauss, work, n_pix_total
     return 0.0
 
 
-def committed_ncu(kernel_stage):
+def workload_tag(args):
+    return (f"config{args.config}:{args.gaussians}:{args.avatars}:{args.envs}:{args.width}x{args.height}:"
+            f"near{args.near}")
+
+
+def committed_ncu(kernel_stage, args):
     """Per-launch DRAM bytes / warp instructions of a kernel from the committed ncu --set full capture
-    of the same bench command (profiles/ncu_traffic.json, written by scripts/ncu_traffic.py)."""
+    of the same bench command (profiles/ncu_traffic.json, written by scripts/ncu_traffic.py), only
+    when that capture was taken on this workload."""
     try:
         with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as f:
             d = json.load(f)
-        return d.get(kernel_stage)
     except (OSError, ValueError):
         return None
+    if d.get("_workload", workload_tag(parse([]))) != workload_tag(args):
+        return None
+    return d.get(kernel_stage)
 
 
 def cpu_baseline(args, scene, bundles, sets, n_envs_sample):
@@ -331,7 +339,7 @@ def blend_roofline(per_stage, dom, pid, w2, args, clk, hbm_peak, peak_kind, n_pi
     ach_f = contribs * BLEND_FLOPS_PER_CONTRIBUTION / (ms / 1e3) / 1e12
     alg = algorithmic_bytes("blend", pid, args.gaussians, n_av, w2, n_pix, args.steps)
     ach_b = alg / (ms / 1e3) / 1e9
-    ncu = committed_ncu(dom)
+    ncu = committed_ncu(dom, args)
     roof = {"bound": "fp32", "kernel": dom, "achieved": ach_f, "peak": peak_f, "unit": "TFLOP/s",
             "frac": ach_f / peak_f, "traffic": None,
             "peak_kind": f"148 SMs x 128 FP32 lanes x 2 x {clk:.0f} MHz (this run's median SM clock)",
@@ -360,7 +368,7 @@ def hbm_roofline(per_stage, dom, sname, pid, w2, args, hbm_peak, peak_kind, n_pi
     roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
             "frac": ach / hbm_peak, "traffic": None, "peak_kind": peak_kind, "alg_bytes_per_step": alg,
             "ms_per_step": ms, "share_of_step": ms / ms_step}
-    ncu = committed_ncu(dom)
+    ncu = committed_ncu(dom, args)
     if ncu is not None:
         roof["traffic"] = ncu["dram_bytes_per_launch"] * ncu["launches_per_step"]
         roof["traffic_source"] = ncu["source"]

@@ -220,6 +220,15 @@ int sn_get_counts(sn_context *ctx, int32_t pass, int32_t env, int64_t *n_visible
 int sn_get_sorted_ids(sn_context *ctx, int32_t pass, int32_t env, int32_t *ids_host, int64_t capacity);
 int sn_get_tile_csr(sn_context *ctx, int32_t pass, int32_t env, int64_t *tile_starts_host, int32_t *pair_splat_host,
                     int64_t capacity);
+/* The tile lists the blend of the last pass actually consumed for env e (HOST): tile_starts (T+1)
+ * and, per tile in depth order, the depth ranks of its splats -- the radix binner's (env, tile)
+ * ranges over pair_vals when that pass built lists, else the streamed lists the blend assembles in
+ * shared memory (exported by the same fill routine, without early termination). They hold the
+ * splats whose TIGHT rectangle (the support ellipse's reach) covers the tile, so each is an
+ * in-order sub-list of the reference list (sn_get_tile_csr) that keeps every splat with a pixel of
+ * the tile inside its support. *n_entries = total entries; ranks_host may be NULL (size query). */
+int sn_get_device_tiles(sn_context *ctx, int32_t pass, int32_t env, int64_t *tile_starts_host, int32_t *ranks_host,
+                        int64_t capacity, int64_t *n_entries);
 /* Depth-sorted per-splat projection outputs of the last pass for env e (HOST, capacity M):
  * means2d (M,2), conics (M,3), depths (M), colors (M,3), alphas (M) -- project_cloud's arrays. */
 int sn_get_projection(sn_context *ctx, int32_t pass, int32_t env, double *means2d, double *conics, double *depths,

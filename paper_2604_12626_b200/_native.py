@@ -65,7 +65,7 @@ STAGES = ("pose", "count", "scan", "emit", "depth_sort", "permute", "pair_scan",
 EXPORTS = (
     "sn_abi_version", "sn_last_error", "sn_context_create", "sn_context_destroy", "sn_context_workspace_bytes",
     "sn_context_sync_stats", "sn_context_kernel_launches", "sn_context_render_retries",
-    "sn_render", "sn_render_async", "sn_render_wait", "sn_get_counts", "sn_get_sorted_ids", "sn_get_tile_csr", "sn_get_projection", "sn_sample_pose",
+    "sn_render", "sn_render_async", "sn_render_wait", "sn_get_counts", "sn_get_sorted_ids", "sn_get_tile_csr", "sn_get_device_tiles", "sn_get_projection", "sn_sample_pose",
     "sn_skin_lbs", "sn_blend_tile_range", "sn_composite", "sn_selftest_fast_exp", "sn_unpack_ply",
     "sn_unpack_bundle", "sn_pack_influences", "sn_quantize_frames", "sn_flip_rows",
 )
@@ -105,6 +105,7 @@ def load():
             "sn_get_sorted_ids": ([P, i32, i32, P, i64], ctypes.c_int),
             "sn_get_tile_csr": ([P, i32, i32, P, P, i64], ctypes.c_int),
             "sn_get_projection": ([P, i32, i32, P, P, P, P, P, i64], ctypes.c_int),
+            "sn_get_device_tiles": ([P, i32, i32, P, P, i64, ctypes.POINTER(i64)], ctypes.c_int),
             "sn_sample_pose": ([P, ctypes.POINTER(SnAvatars), P, i32, P, P, P], ctypes.c_int),
             "sn_skin_lbs": ([P, ctypes.POINTER(SnAvatars), i32, i64, i64, P, P, P, P, P], ctypes.c_int),
             "sn_blend_tile_range": ([i32] * 6 + [P, i64, P, i64, P, P, P, P, P, i64, P, P, P, P], ctypes.c_int),

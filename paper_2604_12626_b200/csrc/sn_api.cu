@@ -1008,6 +1008,82 @@ int sn_get_tile_csr(sn_context *ctx, int32_t pass, int32_t env, int64_t *tile_st
     return SN_OK;
 }
 
+int sn_get_device_tiles(sn_context *ctx, int32_t pass, int32_t env, int64_t *tile_starts_host, int32_t *ranks_host,
+                        int64_t capacity, int64_t *n_entries) {
+    PassWs *w;
+    int el;
+    std::vector<uint64_t> off;
+    int r = pass_env(ctx, pass, env, w, el, off);
+    if (r != SN_OK) return r;
+    SN_CHECK(w->tiled, "last pass was not tiled");
+    SN_CHECK(tile_starts_host && n_entries, "null output");
+    const int n_tiles = w->tiles_x * w->tiles_y;
+    const uint64_t v0 = off[el], v1 = off[el + 1];
+    std::vector<int64_t> ts(n_tiles + 1, 0);
+    std::vector<int32_t> ranks;
+    if (w->binning == 1) {
+        // the radix binner's lists: ranges per (env, tile) into pair_vals (record slots, depth order)
+        std::vector<uint2> rg(n_tiles);
+        SN_CUDA(cudaMemcpy(rg.data(), w->ranges.as<uint2>() + ((size_t)el << w->tile_bits), sizeof(uint2) * n_tiles,
+                           cudaMemcpyDeviceToHost));
+        uint64_t np = 0;
+        SN_CUDA(cudaMemcpy(&np, w->counts.as<uint64_t>() + 1, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        std::vector<uint32_t> pv((size_t)np), order((size_t)(v1 - v0));
+        if (np) SN_CUDA(cudaMemcpy(pv.data(), w->pvals_b.p, sizeof(uint32_t) * np, cudaMemcpyDeviceToHost));
+        if (!order.empty())
+            SN_CUDA(cudaMemcpy(order.data(), w->vals_s.as<uint32_t>() + v0, sizeof(uint32_t) * order.size(),
+                               cudaMemcpyDeviceToHost));
+        std::vector<int32_t> rank_of(order.size(), -1);  // record slot -> depth rank within the env
+        for (size_t i = 0; i < order.size(); ++i) {
+            SN_CHECK(order[i] >= v0 && order[i] < v1, "depth order leaves the env's slots");
+            rank_of[order[i] - v0] = (int32_t)i;
+        }
+        for (int t = 0; t < n_tiles; ++t) {
+            const uint2 q = rg[t];
+            ts[t + 1] = ts[t] + (q.y > q.x ? (int64_t)(q.y - q.x) : 0);
+            for (uint32_t k = q.x; k < q.y; ++k) {
+                SN_CHECK(k < np && pv[k] >= v0 && pv[k] < v1, "tile list entry outside the env");
+                ranks.push_back(rank_of[pv[k] - v0]);
+            }
+        }
+    } else {
+        // the streamed lists the blend builds in shared memory, exported by the same fill routine
+        cudaStream_t st = 0;
+        uint32_t *d_cnt = nullptr, *d_out = nullptr;
+        uint64_t *d_off = nullptr;
+        SN_CUDA(cudaMalloc(&d_cnt, sizeof(uint32_t) * n_tiles));
+        SN_CUDA(cudaMalloc(&d_off, sizeof(uint64_t) * n_tiles));
+        PassView v = view_of(*w);
+        cudaError_t e = launch_tile_queue(v, el, n_tiles, w->tiles_x, d_cnt, nullptr, nullptr, st);
+        std::vector<uint32_t> cnt(n_tiles);
+        if (e == cudaSuccess) e = cudaMemcpy(cnt.data(), d_cnt, sizeof(uint32_t) * n_tiles, cudaMemcpyDeviceToHost);
+        std::vector<uint64_t> o(n_tiles);
+        for (int t = 0; t < n_tiles; ++t) {
+            o[t] = (uint64_t)ts[t];
+            ts[t + 1] = ts[t] + cnt[t];
+        }
+        ranks.resize((size_t)ts[n_tiles]);
+        if (e == cudaSuccess && !ranks.empty()) {
+            e = cudaMalloc(&d_out, sizeof(uint32_t) * ranks.size());
+            if (e == cudaSuccess) e = cudaMemcpy(d_off, o.data(), sizeof(uint64_t) * n_tiles, cudaMemcpyHostToDevice);
+            if (e == cudaSuccess) e = launch_tile_queue(v, el, n_tiles, w->tiles_x, d_cnt, d_off, d_out, st);
+            if (e == cudaSuccess)
+                e = cudaMemcpy(ranks.data(), d_out, sizeof(uint32_t) * ranks.size(), cudaMemcpyDeviceToHost);
+        }
+        cudaFree(d_cnt);
+        cudaFree(d_off);
+        if (d_out) cudaFree(d_out);
+        SN_CUDA(e);
+    }
+    *n_entries = (int64_t)ranks.size();
+    std::copy(ts.begin(), ts.end(), tile_starts_host);
+    if (ranks_host) {
+        SN_CHECK(capacity >= (int64_t)ranks.size(), "ranks buffer too small");
+        std::copy(ranks.begin(), ranks.end(), ranks_host);
+    }
+    return SN_OK;
+}
+
 int sn_get_projection(sn_context *ctx, int32_t pass, int32_t env, double *means2d, double *conics, double *depths,
                       double *colors, double *alphas, int64_t capacity) {
     PassWs *w;

@@ -288,6 +288,71 @@ __device__ __forceinline__ void push_fixup(const BlendArgs &b, bool flag, uint32
     if (flag) b.fix_list[base + __popc(bal & ((1u << lane) - 1u))] = code;
 }
 
+// The streamed tile list of SOURCE 0 (below): appends to s_queue, in depth order, the depth ranks
+// i in [cursor, s1) whose (tight) tile rectangle covers tile (tx, ty), 256 rectangles per step,
+// until at least `cap` entries wait (the queue holds cap + 255) or the env's list ends. Whole
+// 8192-splat super-batches and 256-splat batches whose union rectangles miss the tile are skipped
+// without a barrier (the branch is uniform across the CTA). Used by the blend and by the harness
+// export of the lists the blend consumes (tile_queue_kernel).
+__device__ __forceinline__ void stream_fill(const PassView &v, int tx, int ty, int cap, uint32_t &cursor, uint32_t s1,
+                                            int &q_len, uint32_t &scanned, uint32_t *s_queue, uint32_t *s_wsum) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    while (q_len < cap && cursor < s1) {
+        const uint32_t bi = cursor / kBlock;
+        if (!covers(__ldg(v.super_rects + bi / kSuperBatch), tx, ty)) {
+            cursor = min(s1, (bi / kSuperBatch + 1) * (uint32_t)(kSuperBatch * kBlock));
+            continue;
+        }
+        const uint32_t b_end = min(s1, (bi + 1) * (uint32_t)kBlock);
+        if (!covers(__ldg(v.batch_rects + bi), tx, ty)) {
+            cursor = b_end;
+            continue;
+        }
+        uint32_t i = bi * kBlock + threadIdx.x;
+        const bool hit = i >= cursor && i < b_end && covers(__ldg(v.rects + i), tx, ty);
+        unsigned bal = __ballot_sync(kFull, hit);
+        if (lane == 0) s_wsum[warp] = __popc(bal);
+        __syncthreads();
+        int woff = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < kBlock / 32; ++w) {
+            int c = s_wsum[w];
+            woff += (w < warp) ? c : 0;
+            tot += c;
+        }
+        if (hit) s_queue[q_len + woff + __popc(bal & ((1u << lane) - 1u))] = i;
+        q_len += tot;
+        scanned += b_end - cursor;
+        cursor = b_end;
+        __syncthreads();
+    }
+}
+
+// Harness export (sn_get_device_tiles) of the streamed lists for env `el` of the last pass: one CTA
+// per tile runs stream_fill over the whole env (no early termination) and writes, in order, the
+// depth ranks (relative to the env) it queued: counts first (out == null), then the entries at
+// the caller's offsets.
+__global__ void __launch_bounds__(kBlock) tile_queue_kernel(PassView v, int el, int tiles_x, uint32_t *counts,
+                                                            const uint64_t *offsets, uint32_t *out) {
+    __shared__ uint32_t s_queue[2 * kBlock];
+    __shared__ uint32_t s_wsum[kBlock / 32];
+    if (pass_overflow(v)) return;
+    const int tile = blockIdx.x, tx = tile % tiles_x, ty = tile / tiles_x;
+    const uint32_t e0 = (uint32_t)v.env_off[el];
+    uint32_t cursor = e0, s1 = (uint32_t)v.env_off[el + 1], scanned = 0;
+    uint64_t total = 0;
+    while (true) {
+        int q_len = 0;
+        stream_fill(v, tx, ty, kBlock, cursor, s1, q_len, scanned, s_queue, s_wsum);
+        if (q_len == 0) break;
+        if (out)
+            for (int i = threadIdx.x; i < q_len; i += kBlock) out[offsets[tile] + total + i] = s_queue[i] - e0;
+        total += q_len;
+        __syncthreads();
+    }
+    if (!out && threadIdx.x == 0) counts[tile] = (uint32_t)total;
+}
+
 // SOURCE 0: no tile lists. The CTA streams its env's depth-sorted tile rectangles (8 B each; the
 //           env's 2 MB array stays in L2 while its 1,200 tiles run) and compacts, in depth order,
 //           the splats whose rectangle covers this tile into a shared-memory queue. The walk
@@ -378,37 +443,7 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
         if (__syncthreads_count(dead == 0.0f) == 0) break;  // also guards s_f / s_queue reuse
         int n;
         if (SOURCE == 0) {
-            while (q_len < kBatch && cursor < s1) {
-                // hierarchical cull (uniform across the CTA, no barrier on the skip path):
-                // 8192-splat super-batches, then 256-splat batches, by their union rectangles
-                const uint32_t bi = cursor / kBlock;
-                if (!covers(__ldg(v.super_rects + bi / kSuperBatch), tx, ty)) {
-                    cursor = min(s1, (bi / kSuperBatch + 1) * (uint32_t)(kSuperBatch * kBlock));
-                    continue;
-                }
-                const uint32_t b_end = min(s1, (bi + 1) * (uint32_t)kBlock);
-                if (!covers(__ldg(v.batch_rects + bi), tx, ty)) {
-                    cursor = b_end;
-                    continue;
-                }
-                uint32_t i = bi * kBlock + threadIdx.x;
-                const bool hit = i >= cursor && i < b_end && covers(__ldg(v.rects + i), tx, ty);
-                unsigned bal = __ballot_sync(kFull, hit);
-                if (lane == 0) s_wsum[warp] = __popc(bal);
-                __syncthreads();
-                int woff = 0, tot = 0;
-#pragma unroll
-                for (int w = 0; w < kBlock / 32; ++w) {
-                    int c = s_wsum[w];
-                    woff += (w < warp) ? c : 0;
-                    tot += c;
-                }
-                if (hit) s_queue[q_len + woff + __popc(bal & ((1u << lane) - 1u))] = i;
-                q_len += tot;
-                scanned += b_end - cursor;
-                cursor = b_end;
-                __syncthreads();
-            }
+            stream_fill(v, tx, ty, kBatch, cursor, s1, q_len, scanned, s_queue, s_wsum);
             n = min(q_len, kBatch);
         } else {
             n = (int)min((uint32_t)kBatch, s1 - cursor);
@@ -646,7 +681,13 @@ struct ExactPixel {
     float cr, cg, cb;
     double A, D, T;
     int nc;
+    bool near;  // the cutoff test met a transmittance within 1e-12 (relative) of 1e-4: re-walk with SEQ
 };
+
+// The relative window around 1e-4 inside which the warp prefix product's association (<= ~1e-13
+// relative from the sequential product after hundreds of contributions) could flip `T < 1e-4`.
+constexpr double kNearCut = 1e-12;
+
 
 // A contribution waiting in a warp's queue (float64 alpha and z, colour).
 struct QEntry {
@@ -655,16 +696,52 @@ struct QEntry {
 };
 constexpr int kQueue = 64;  // per-warp queue capacity: < 32 waiting + 32 arriving
 
+// One group's transmittances. Fast mode: a warp prefix product (Hillis-Steele, its association
+// differs from the sequential product's by a few ulps). SEQ mode: lane l multiplies T by
+// (1 - a_j) for j < l itself, in order -- the reference's sequential product (_kernels_cy.pyx:86),
+// bit for bit. Returns T before this lane's contribution; t_after = before * (1 - a).
+template <bool SEQ>
+__device__ __forceinline__ double group_trans_before(double T, double one_minus_a, const QEntry *q, int lane,
+                                                     bool act) {
+    double before = T;
+    if (SEQ) {
+        for (int j = 0; j < lane; ++j) before *= 1.0 - q[j].a;  // q[j], j < lane, are active entries
+    } else {
+        double pp = act ? one_minus_a : 1.0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const double o = __shfl_up_sync(kFull, pp, d);
+            if (lane >= d) pp *= o;
+        }
+        double ex = __shfl_up_sync(kFull, pp, 1);
+        if (lane == 0) ex = 1.0;
+        before = T * ex;
+    }
+    return before;
+}
+
+// exp(-d2 / 2) of a contribution: the table exp (2 ulp), or in SEQ mode the device libm exp (1 ulp)
+// on the reference's own argument -0.5 * d2
+template <bool SEQ>
+__device__ __forceinline__ double exp_neg_half(double d2, const double *s_exp) {
+    if (SEQ) return exp(-0.5 * d2);
+    double ev;
+    SN_EXP_NEG_HALF(d2, s_exp, ev);
+    return ev;
+}
+
 // One pixel of one pass, walked by a whole warp with the reference's float64 arithmetic
 // (_kernels_cy.pyx:64-86: float64 d2 / alpha / transmittance, T tested after each contribution).
 // Lanes gather and test 32 depth-ordered candidates at a time; the contributing ones are queued
 // (in order) and consumed 32 at a time: the transmittance through a group is a warp prefix
-// product (its rounding differs from the sequential product by a few float64 ulps, like the exp),
-// the first member that takes T below 1e-4 is the last contribution, and the accumulators are
+// product (its rounding differs from the sequential product by a few float64 ulps, like the table
+// exp), the first member that takes T below 1e-4 is the last contribution, and the accumulators are
 // per-lane partial sums reduced at the end. Groups are the 1st..32nd, 33rd..64th, ... contributions,
 // so the result depends only on the contribution sequence -- not on how candidates were listed
-// (streamed rectangles, tile lists or every splat of the env give bit-identical pixels).
-template <int kPer>  // candidates per lane per step: their gathers are in flight together
+// (streamed rectangles, tile lists or every splat of the env give bit-identical pixels). When a
+// cutoff test meets a transmittance within kNearCut of 1e-4 the walk reports `near` and the caller
+// re-walks the pixel with SEQ = true: sequential transmittance and libm exp, the reference's order.
+template <int kPer, bool SEQ = false>  // candidates per lane per step: their gathers are in flight together
 __device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_x, int px_i, int py_i,
                                  const double *s_exp, QEntry *q) {
     const int lane = threadIdx.x & 31;
@@ -673,24 +750,18 @@ __device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_
     float cr = 0.0f, cg = 0.0f, cb = 0.0f;  // per-lane partial sums, reduced at the end
     double A = 0.0, D = 0.0, T = 1.0;
     int nc = 0, qn = 0;
-    bool done = false;
+    bool done = false, near = false;
     auto consume = [&](int m) {  // the first m <= 32 queued contributions
         const bool act = lane < m;
         QEntry e{};
         if (act) e = q[lane];
-        double pp = act ? 1.0 - e.a : 1.0;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const double o = __shfl_up_sync(kFull, pp, d);
-            if (lane >= d) pp *= o;
-        }
-        double ex = __shfl_up_sync(kFull, pp, 1);
-        if (lane == 0) ex = 1.0;
-        const double t_after = T * pp;
+        const double before = group_trans_before<SEQ>(T, 1.0 - e.a, q, lane, act);
+        const double t_after = before * (1.0 - e.a);
+        if (!SEQ && __any_sync(kFull, act && fabs(t_after - kTCutoff) <= kNearCut * kTCutoff)) near = true;
         const unsigned cut = __ballot_sync(kFull, act && t_after < kTCutoff);
         const int last = cut ? __ffs(cut) - 1 : m - 1;
         if (act && lane <= last) {
-            const double w = e.a * (T * ex);
+            const double w = e.a * before;
             const float wf = (float)w;
             cr = __fmaf_rn(e.r, wf, cr);
             cg = __fmaf_rn(e.g, wf, cg);
@@ -711,7 +782,7 @@ __device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_
         cur = (uint32_t)v.env_off[el];
         end = (uint32_t)v.env_off[el + 1];
     }
-    while (cur < end && !done) {
+    while (cur < end && !done && !near) {
         uint32_t step;
         uint32_t rid[kPer];
         bool cand[kPer];
@@ -761,9 +832,7 @@ __device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_
                 const double d2 = (s.ca * dx * dx + s.cb2 * dx * dy) + s.cc * dy * dy;
                 if (!(d2 > kSupportD2)) {
                     contrib[i] = true;
-                    double ev;
-                    SN_EXP_NEG_HALF(d2, s_exp, ev);
-                    e[i].a = s.alpha * ev;
+                    e[i].a = s.alpha * exp_neg_half<SEQ>(d2, s_exp);
                     if (e[i].a > kAlphaClip) e[i].a = kAlphaClip;
                     e[i].z = s.z;
                     float rgb[3];
@@ -776,7 +845,7 @@ __device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_
         }
 #pragma unroll
         for (int i = 0; i < kPer; ++i) {
-            if (done) break;
+            if (done || near) break;
             const unsigned bal = __ballot_sync(kFull, contrib[i]);
             if (contrib[i]) q[qn + __popc(bal & ((1u << lane) - 1u))] = e[i];
             qn += __popc(bal);
@@ -794,7 +863,8 @@ __device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_
         }
         cur += step;
     }
-    if (!done && qn > 0) consume(qn);
+    if (!done && !near && qn > 0) consume(qn);
+    __syncwarp();
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
         cr += __shfl_xor_sync(kFull, cr, d);
@@ -803,7 +873,21 @@ __device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_
         A += __shfl_xor_sync(kFull, A, d);
         D += __shfl_xor_sync(kFull, D, d);
     }
-    return ExactPixel{cr, cg, cb, A, D, T, (int)__reduce_add_sync(kFull, (unsigned)nc)};
+    return ExactPixel{cr, cg, cb, A, D, T, (int)__reduce_add_sync(kFull, (unsigned)nc), near};
+}
+
+// exact_walk, then -- only when its cutoff test met a transmittance within kNearCut of 1e-4 -- the
+// same pixel again in SEQ mode (sequential transmittance, libm exp): the reference's decision.
+template <int kPer>
+__device__ __forceinline__ ExactPixel exact_pixel(const PassView &v, int el, int tile, int tiles_x, int px_i, int py_i,
+                                                  const double *s_exp, QEntry *q) {
+    ExactPixel f = exact_walk<kPer, false>(v, el, tile, tiles_x, px_i, py_i, s_exp, q);
+    if (f.near) {
+        __syncwarp();
+        f = exact_walk<kPer, true>(v, el, tile, tiles_x, px_i, py_i, s_exp, q);
+        f.near = true;
+    }
+    return f;
 }
 
 // exact_walk for one pixel by a whole CTA (long, unsaturated lists: avatar-layer fixups). The 8
@@ -816,6 +900,7 @@ __device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_
 #endif
 constexpr int kCtaPer = SN_FIXUP_CTA_PER;
 constexpr int kCtaQueue = kCtaPer * kBlock + 32;
+template <bool SEQ>
 __device__ ExactPixel exact_walk_cta(const PassView &v, int el, int tile, int tiles_x, int px_i, int py_i,
                                      const double *s_exp, QEntry *q, int *s_i) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -824,25 +909,19 @@ __device__ ExactPixel exact_walk_cta(const PassView &v, int el, int tile, int ti
     float cr = 0.0f, cg = 0.0f, cb = 0.0f;
     double A = 0.0, D = 0.0, T = 1.0;
     int nc = 0;
-    bool done = false;  // warp 0's view
+    bool done = false, near = false;  // warp 0's view
     int qn = 0;         // queued contributions (uniform)
     auto consume = [&](int head, int m) {  // warp 0: q[head, head + m), m <= 32
         const bool act = lane < m;
         QEntry e{};
         if (act) e = q[head + lane];
-        double pp = act ? 1.0 - e.a : 1.0;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const double o = __shfl_up_sync(kFull, pp, d);
-            if (lane >= d) pp *= o;
-        }
-        double ex = __shfl_up_sync(kFull, pp, 1);
-        if (lane == 0) ex = 1.0;
-        const double t_after = T * pp;
+        const double before = group_trans_before<SEQ>(T, 1.0 - e.a, q + head, lane, act);
+        const double t_after = before * (1.0 - e.a);
+        if (!SEQ && __any_sync(kFull, act && fabs(t_after - kTCutoff) <= kNearCut * kTCutoff)) near = true;
         const unsigned cut = __ballot_sync(kFull, act && t_after < kTCutoff);
         const int last = cut ? __ffs(cut) - 1 : m - 1;
         if (act && lane <= last) {
-            const double w = e.a * (T * ex);
+            const double w = e.a * before;
             const float wf = (float)w;
             cr = __fmaf_rn(e.r, wf, cr);
             cg = __fmaf_rn(e.g, wf, cg);
@@ -908,9 +987,7 @@ __device__ ExactPixel exact_walk_cta(const PassView &v, int el, int tile, int ti
                     const double d2 = (sr.ca * dx * dx + sr.cb2 * dx * dy) + sr.cc * dy * dy;
                     if (!(d2 > kSupportD2)) {
                         contrib = true;
-                        double ev;
-                        SN_EXP_NEG_HALF(d2, s_exp, ev);
-                        e.a = sr.alpha * ev;
+                        e.a = sr.alpha * exp_neg_half<SEQ>(d2, s_exp);
                         if (e.a > kAlphaClip) e.a = kAlphaClip;
                         e.z = sr.z;
                         float rgb[3];
@@ -938,17 +1015,17 @@ __device__ ExactPixel exact_walk_cta(const PassView &v, int el, int tile, int ti
         // warp 0 consumes whole groups of 32; the remainder moves to the queue's front
         if (warp == 0) {
             int head = 0;
-            while (!done && qn - head >= 32) {
+            while (!done && !near && qn - head >= 32) {
                 consume(head, 32);
                 head += 32;
             }
-            const int rest = done ? 0 : qn - head;
+            const int rest = (done || near) ? 0 : qn - head;
             QEntry t{};
             if (lane < rest) t = q[head + lane];
             __syncwarp();
             if (lane < rest) q[lane] = t;
             if (lane == 0) {
-                s_flag[0] = done;
+                s_flag[0] = done || near;
                 s_cnt[0] = rest;
             }
         }
@@ -960,7 +1037,7 @@ __device__ ExactPixel exact_walk_cta(const PassView &v, int el, int tile, int ti
         cur += step;
     }
     if (warp == 0) {
-        if (!done && qn > 0) consume(0, qn);
+        if (!done && !near && qn > 0) consume(0, qn);
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) {
             cr += __shfl_xor_sync(kFull, cr, d);
@@ -970,9 +1047,23 @@ __device__ ExactPixel exact_walk_cta(const PassView &v, int el, int tile, int ti
             D += __shfl_xor_sync(kFull, D, d);
         }
         nc = (int)__reduce_add_sync(kFull, (unsigned)nc);
+        if (lane == 0) s_flag[2] = near;
     }
     __syncthreads();  // the queue and scratch are reused by the next walk
-    return ExactPixel{cr, cg, cb, A, D, T, nc};
+    near = s_flag[2] != 0;  // uniform across the CTA
+    __syncthreads();
+    return ExactPixel{cr, cg, cb, A, D, T, nc, near};
+}
+
+// exact_walk_cta, re-walked in SEQ mode when the cutoff met a transmittance within kNearCut of 1e-4.
+__device__ __forceinline__ ExactPixel exact_pixel_cta(const PassView &v, int el, int tile, int tiles_x, int px_i,
+                                                      int py_i, const double *s_exp, QEntry *q, int *s_i) {
+    ExactPixel f = exact_walk_cta<false>(v, el, tile, tiles_x, px_i, py_i, s_exp, q, s_i);
+    if (f.near) {
+        f = exact_walk_cta<true>(v, el, tile, tiles_x, px_i, py_i, s_exp, q, s_i);
+        f.near = true;
+    }
+    return f;
 }
 
 // Layer fixups (mode 2): a CTA per listed pixel (their walks are long: near avatars' tile lists
@@ -995,7 +1086,7 @@ __global__ void __launch_bounds__(256) fixup_layer_kernel(BlendArgs b) {
         const int env = b.e0 + el;
         const int tile = (py_i / kTile) * b.tiles_x + px_i / kTile;
         const sn_camera &cam = b.cams[env];
-        const ExactPixel f = exact_walk_cta(b.pv, el, tile, b.tiles_x, px_i, py_i, s_exp, s_q, s_i);
+        const ExactPixel f = exact_pixel_cta(b.pv, el, tile, b.tiles_x, px_i, py_i, s_exp, s_q, s_i);
         const int64_t pix = ((int64_t)env * b.height + py_i) * b.width + px_i;
         const double alpha = f.A < 1.0 ? f.A : 1.0;
         const double depth = f.A > 0.0 ? f.D / f.A : cam.far_;
@@ -1010,7 +1101,7 @@ __global__ void __launch_bounds__(256) fixup_layer_kernel(BlendArgs b) {
         const bool exact_back = s_back != 0;
         __syncthreads();
         ExactPixel k{};
-        if (exact_back) k = exact_walk_cta(b.back, el, tile, b.tiles_x, px_i, py_i, s_exp, s_q, s_i);
+        if (exact_back) k = exact_pixel_cta(b.back, el, tile, b.tiles_x, px_i, py_i, s_exp, s_q, s_i);
         if (threadIdx.x != 0 || !(f.A > 0.0)) continue;  // front depth = far: the back is kept
         float *oc = b.color + 3 * pix;
         float bc[3] = {oc[0], oc[1], oc[2]};
@@ -1069,7 +1160,7 @@ __global__ void __launch_bounds__(256, SN_FIXUP_MIN_BLOCKS) fixup_kernel(BlendAr
         const int tile = (py_i / kTile) * b.tiles_x + px_i / kTile;
         const sn_camera &cam = b.cams[env];
         // mode 2 fixups are few and each walks long, unsaturated lists: more gathers in flight
-        const ExactPixel f = exact_walk<MODE == 2 ? 8 : SN_FIXUP_PER>(b.pv, el, tile, b.tiles_x, px_i, py_i, s_exp, q);
+        const ExactPixel f = exact_pixel<MODE == 2 ? 8 : SN_FIXUP_PER>(b.pv, el, tile, b.tiles_x, px_i, py_i, s_exp, q);
         contribs += (unsigned)f.nc;
         const int64_t pix = ((int64_t)env * b.height + py_i) * b.width + px_i;
         const double alpha = f.A < 1.0 ? f.A : 1.0;
@@ -1084,7 +1175,7 @@ __global__ void __launch_bounds__(256, SN_FIXUP_MIN_BLOCKS) fixup_kernel(BlendAr
             bool exact_back = false;
             ExactPixel k{};
             if (fabs(depth - bd) <= 1.01 * (double)b.derr[pix] + 1e-30) {
-                k = exact_walk<4>(b.back, el, tile, b.tiles_x, px_i, py_i, s_exp, q);
+                k = exact_pixel<4>(b.back, el, tile, b.tiles_x, px_i, py_i, s_exp, q);
                 bd = k.A > 0.0 ? k.D / k.A : cam.far_;
                 exact_back = true;
             }
@@ -1228,6 +1319,12 @@ static void launch_blend_mode(const BlendArgs &b, dim3 grid, cudaStream_t s) {
     else
         blend_kernel<MODE, 2><<<grid, kBlock, 0, s>>>(b);
     if (MODE != 2) fixup_kernel<MODE><<<kFixupBlocks, 256, 0, s>>>(b);  // mode 2: after the composite
+}
+
+cudaError_t launch_tile_queue(const PassView &v, int el, int n_tiles, int tiles_x, uint32_t *counts,
+                              const uint64_t *offsets, uint32_t *out, cudaStream_t s) {
+    tile_queue_kernel<<<n_tiles, kBlock, 0, s>>>(v, el, tiles_x, counts, offsets, out);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_layer_composite(const BlendArgs &b, cudaStream_t s) {

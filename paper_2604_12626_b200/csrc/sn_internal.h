@@ -162,6 +162,9 @@ constexpr int kFixupBlocks = 148 * 4;
 cudaError_t launch_blend(const BlendArgs &b, cudaStream_t s);  // blend (+ fixup for modes 0, 1)
 cudaError_t launch_layer_composite(const BlendArgs &b, cudaStream_t s);  // mode 2: composite + fixup
 cudaError_t fast_exp_selftest(double *max_rel_err);
+// harness export of the streamed (source 0) tile lists of env el: counts (offsets == null) or entries
+cudaError_t launch_tile_queue(const PassView &v, int el, int n_tiles, int tiles_x, uint32_t *counts,
+                              const uint64_t *offsets, uint32_t *out, cudaStream_t s);
 cudaError_t launch_composite64(int64_t npix, const double *fc, const double *fa, const double *fd, const double *bc,
                                const double *ba, const double *bd, double *oc, double *oa, double *od, cudaStream_t s);
 cudaError_t launch_blend_tile_range(int t_begin, int t_end, int tiles_x, int tile_size, int width, int height,

@@ -212,3 +212,18 @@ def tile_csr(n_tiles, pass_id=0, env=0, context=None):
     N.check(lib.sn_get_tile_csr(ctx.handle, pass_id, env, ts.ctypes.data_as(ctypes.c_void_p),
                                 ps.ctypes.data_as(ctypes.c_void_p), npairs.value))
     return ts, ps[:npairs.value]
+
+
+def device_tiles(n_tiles, pass_id=0, env=0, context=None):
+    """The tile lists the last render's blend consumed for `env` (sn_get_device_tiles): tile_starts
+    (T+1) int64 and per-tile depth ranks int32 -- the tight sub-lists of tile_csr's reference lists."""
+    lib = N.load()
+    ctx = context or N.default_context()
+    ts = np.zeros(n_tiles + 1, dtype=np.int64)
+    n = ctypes.c_int64()
+    N.check(lib.sn_get_device_tiles(ctx.handle, pass_id, env, ts.ctypes.data_as(ctypes.c_void_p), None, 0,
+                                    ctypes.byref(n)))
+    ranks = np.zeros(max(n.value, 1), dtype=np.int32)
+    N.check(lib.sn_get_device_tiles(ctx.handle, pass_id, env, ts.ctypes.data_as(ctypes.c_void_p),
+                                    ranks.ctypes.data_as(ctypes.c_void_p), n.value, ctypes.byref(n)))
+    return ts, ranks[:n.value]

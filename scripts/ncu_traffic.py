@@ -1,7 +1,8 @@
 """Extract per-launch DRAM traffic of the bench's kernels from an `ncu --set full` report into
 profiles/ncu_traffic.json (read by bench.py for roofline.traffic) and print a summary.
 
-usage: python scripts/ncu_traffic.py gpurun_out/prof_full.ncu-rep [out.json]
+usage: python scripts/ncu_traffic.py gpurun_out/prof_full.ncu-rep [out.json] [workload tag]
+(the tag is bench.workload_tag of the profiled command; default: bench.py's default workload)
 """
 import csv
 import io
@@ -22,11 +23,14 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
 def main():
     rep = sys.argv[1]
     out = sys.argv[2] if len(sys.argv) > 2 else "profiles/ncu_traffic.json"
+    sys.path.insert(0, ".")
+    import bench
+    tag = sys.argv[3] if len(sys.argv) > 3 else bench.workload_tag(bench.parse([]))
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     col = {h: i for i, h in enumerate(hdr)}
-    result = {}
+    result = {"_workload": tag}
     for r in data:
         name = r[col["Kernel Name"]]
         stage = next((v for k, v in STAGE_OF.items() if k in name), None)
