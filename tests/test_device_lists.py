@@ -73,7 +73,7 @@ def test_scene_streamed_and_radix_lists_match_oracle():
         for binning in (0, 1):
             ctx = N.Context()
             R.render_frames(room, cams, np.ones(3), binning=binning, context=ctx)
-            lists[binning] = [R.device_tiles(100, 0, e, context=ctx) for e in range(5)]
+            lists[binning] = [R.device_tiles(80, 0, e, context=ctx) for e in range(5)]
         for e in (0, 2, 4):
             # both binners hand the blend the same tight lists
             np.testing.assert_array_equal(lists[0][e][0], lists[1][e][0])
@@ -109,7 +109,7 @@ def test_layer_radix_lists_match_oracle():
         clouds = [rig.AvatarRuntime(b, start_offset=0.1 * a).deformed_cloud(float(times[e]))
                   for a, b in enumerate(bundles)]
         layer = concat_clouds(clouds)
-        ts, ranks = R.device_tiles(100, 1, e, context=br.context)
+        ts, ranks = R.device_tiles(80, 1, e, context=br.context)
         kept, total = check_env_lists(ts, ranks, layer, cams[e], f"layer env {e}")
         nonempty += kept > 0
     assert nonempty >= 2
