@@ -547,13 +547,22 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
     const bool amb = inside && (b.force_exact || (cut && (!(T + err < kTLo) || err > 0.0625f * T)));
     PROF(2, amb);
 #ifdef SN_BLEND_PROF
+    const bool prof_live = __syncthreads_or(dead == 0.0f) != 0;
     if (SOURCE == 0 && MODE == 0 && threadIdx.x == 0) {
         const uint32_t st = (uint32_t)v.env_off[el], tot = s1 - st;
         // consumed: the list position the walk had reached (queued-but-unwalked entries excluded)
         const uint32_t used = (cursor - st) - (uint32_t)q_len;
         const unsigned fr = tot ? (unsigned)((1000ull * used) / tot) : 0u;
         atomicMax(&g_env_frac[el & 63], fr);
-        atomicAdd(&g_blend_prof[4 + min(11u, fr * 12u / 1001u)], 1ull);
+        // log-spaced bins of the consumed fraction (1e-5 units): <=0.1%, 0.2, 0.5, 1, 2, 5, 10, 20,
+        // 50, <100%; bin 14: the list ran out with a live (unsaturated) pixel
+        const unsigned f5 = tot ? (unsigned)((100000ull * used) / tot) : 0u;
+        const unsigned edges[9] = {100, 200, 500, 1000, 2000, 5000, 10000, 20000, 50000};
+        unsigned bin = 9;
+        for (int k = 8; k >= 0; --k)
+            if (f5 <= edges[k]) bin = k;
+        if (prof_live && cursor >= s1 && q_len == 0) bin = 10;
+        atomicAdd(&g_blend_prof[4 + bin], 1ull);
     }
     for (int i = 0; i < 16; ++i)
         if (prof[i]) atomicAdd(&g_blend_prof[i], prof[i]);
@@ -724,9 +733,12 @@ __device__ __forceinline__ double group_trans_before(double T, double one_minus_
 // on the reference's own argument -0.5 * d2
 template <bool SEQ>
 __device__ __forceinline__ double exp_neg_half(double d2, const double *s_exp) {
-    if (SEQ) return exp(-0.5 * d2);
     double ev;
-    SN_EXP_NEG_HALF(d2, s_exp, ev);
+    if (SEQ) {
+        ev = exp(-0.5 * d2);
+    } else {
+        SN_EXP_NEG_HALF(d2, s_exp, ev);
+    }
     return ev;
 }
 

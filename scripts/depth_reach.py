@@ -1,6 +1,7 @@
-"""Diagnostic (library built with -DSN_BLEND_PROF): how far into each env's depth-sorted list the
-scene blend's tiles reach before every pixel saturates. Histogram over tiles of the consumed
-fraction, and per env the largest fraction."""
+"""Diagnostic (library built with -DSN_BLEND_PROF, SPLATNAV_B200_LIB pointing at it): how far into
+each env's depth-sorted list the scene blend's tiles reach before every pixel saturates --
+log-spaced histogram over tiles of the consumed fraction, plus the tiles whose list ran out with a
+live pixel -- and per env the largest fraction. Sizes the near slice of the depth-sliced scene pass."""
 import ctypes
 import os
 import sys
@@ -16,11 +17,13 @@ from paper_2604_12626_b200.batch import BatchRenderer
 lib = ctypes.CDLL(N.LIB_PATH)
 hist = (ctypes.c_ulonglong * 16)()
 frac = (ctypes.c_uint * 64)()
-for n, near in ((1_000_000, 0.1), (6_000_000, 0.1), (1_000_000, 0.01)):
+labels = ["<=0.1%", "<=0.2%", "<=0.5%", "<=1%", "<=2%", "<=5%", "<=10%", "<=20%", "<=50%", "<100%", "ran out live"]
+for n, near in ((1_000_000, 0.1), (3_000_000, 0.1), (6_000_000, 0.1), (1_000_000, 0.01)):
     box = S.room_box(n)
     scene = S.make_scene(n, box[0], box[1], seed=0)
     br = BatchRenderer(scene, None, background=(1, 1, 1))
-    for s in range(2):
+    tot = np.zeros(11)
+    for s in range(3):
         cams = S.room_cameras(64, box, seed=10_000 + s, near=near)
         lib.sn_debug_blend_prof(hist, 1)
         lib.sn_debug_env_frac(frac, 1)
@@ -28,7 +31,6 @@ for n, near in ((1_000_000, 0.1), (6_000_000, 0.1), (1_000_000, 0.01)):
         torch.cuda.synchronize()
         lib.sn_debug_blend_prof(hist, 1)
         lib.sn_debug_env_frac(frac, 1)
-        h = np.array(list(hist)[4:16], dtype=np.float64)
-        f = np.array(list(frac)) / 1000.0
-        print(f"N={n} near={near} step {s}: tiles by consumed fraction (12 bins) {np.round(h / h.sum(), 4).tolist()}")
-        print(f"   per-env max fraction: min {f.min():.3f} median {np.median(f):.3f} max {f.max():.3f}")
+        tot += np.array(list(hist)[4:15], dtype=np.float64)
+    cum = np.cumsum(tot) / tot.sum()
+    print(f"N={n} near={near}: cumulative tile fraction " + ", ".join(f"{l} {c:.4f}" for l, c in zip(labels, cum)))
