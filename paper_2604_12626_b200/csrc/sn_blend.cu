@@ -123,18 +123,28 @@ __device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
     return r;
 }
 
-// Shared-memory form of a gathered splat for the float32 chain (64 B): the principal-axis rows as
-// (axis 1, axis 2) pairs, the decision thresholds k (9 -/+ E(9.1)), alpha, the alpha error bound
-// coefficients, colour and z (paired for the FFMA2 accumulation). k = log2(e) / 2: the chain
-// works on h = k d2, so alpha = o 2^-h.
-struct __align__(16) FRec {
-    float a1x, c2x, a1y, c2y;  // (v1, v2) = (a1x, c2x) ox + (a1y, c2y) oy + (V1, V2), h = v1^2 + v2^2,
-    float V1, V2, thr_out, thr_in;  // v_j = sqrt(k l_j) u_j
-    float ka, kb, alpha, pad;  // alpha's relative error bound: eps = ka h + kb
-    float r, g, b, z;
-};
+// The blend CTA: 128 threads per 16 x 16 tile, each thread two pixels -- rows ly and ly + 4 of its
+// warp's 8 x 8 block (warp w: block (w & 1, w >> 1)) -- whose per-contribution chains run as packed
+// float32 pairs (FFMA2 / FMUL2 / FADD2: two IEEE operations per issue slot, each rounded exactly
+// like its scalar form), so the per-splat loads, the loop and the block mask are shared by two
+// pixels and the chain costs about half the issue slots per pixel.
+constexpr int kBT = 128;
+constexpr int kBW = kBT / 32;  // warps (8 x 8 pixel blocks) per tile
 
-// Which of the CTA's eight 8 x 4 warp blocks the splat's support {d2 <= 9} can reach: (mx, my) is
+// Shared-memory form of a gathered splat for the float32 chain (80 B): the principal-axis rows (a
+// pixel's v_k = row_k . o + V_k, h = v1^2 + v2^2), V1 and V2 twice (register pairs for FFMA2), the
+// decision thresholds k (9 -/+ E(9.1)), alpha's error bound coefficients (eps = ka h + kb, kb twice),
+// alpha, z and colour. k = log2(e) / 2: the chain works on h = k d2, so alpha = o 2^-h.
+struct __align__(16) FRec {
+    float a1x, a1y, c2x, c2y;
+    float V1, V1b, V2, V2b;
+    float thr_out, thr_in, kb, kbb;
+    float ka, alpha, z, pad0;
+    float r, g, b, pad1;
+};
+static_assert(sizeof(FRec) == 80, "FRec layout");
+
+// Which of the tile's four 8 x 8 warp blocks the splat's support {d2 <= 9} can reach: (mx, my) is
 // the mean relative to the tile origin, (hx, hy) the support ellipse's bounding-box half-extents
 // (already widened far beyond the float rounding of the reference's d2 test), so a pixel whose
 // d2 <= 9 is never outside a set bit.
@@ -142,14 +152,13 @@ __device__ __forceinline__ unsigned warp_block_mask(float mx, float my, float hx
     const float x0 = mx - hx, x1 = mx + hx, y0 = my - hy, y1 = my + hy;
     unsigned cols = 0, rows = 0;
 #pragma unroll
-    for (int bx = 0; bx < 2; ++bx)  // pixel centres 8 bx + 0.5 .. 8 bx + 7.5
-        cols |= (x1 >= 8 * bx + 0.5f && x0 <= 8 * bx + 7.5f) ? (1u << bx) : 0u;
-#pragma unroll
-    for (int by = 0; by < 4; ++by)  // pixel centres 4 by + 0.5 .. 4 by + 3.5
-        rows |= (y1 >= 4 * by + 0.5f && y0 <= 4 * by + 3.5f) ? (1u << by) : 0u;
+    for (int k = 0; k < 2; ++k) {  // pixel centres 8 k + 0.5 .. 8 k + 7.5 in x and in y
+        cols |= (x1 >= 8 * k + 0.5f && x0 <= 8 * k + 7.5f) ? (1u << k) : 0u;
+        rows |= (y1 >= 8 * k + 0.5f && y0 <= 8 * k + 7.5f) ? (1u << k) : 0u;
+    }
     unsigned m = 0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) m |= (((cols >> (w & 1)) & (rows >> (w >> 1))) & 1u) << w;
+    for (int w = 0; w < kBW; ++w) m |= (((cols >> (w & 1)) & (rows >> (w >> 1))) & 1u) << w;
     return m;
 }
 
@@ -161,7 +170,7 @@ __device__ __forceinline__ unsigned warp_block_mask(float mx, float my, float hx
 //   E(d2) = 1.5 [2 u sqrt(d2) (sqrt(l1) S1 + sqrt(l2) S2) + 7 u d2] + 1e-15 (l1 / l2) 9,
 //   eps(d2) = E(d2) / 2 + kEpsExp <= ka d2 + kb   (sqrt(d2) <= (d2 + 1) / 2),
 // all evaluated in float with a 1% margin. A degenerate conic (l2 <= 0) gets thresholds that send
-// every pixel to the float64 test. Returns the 8-bit warp-block mask (warp_block_mask).
+// every pixel to the float64 test. Returns the 4-bit warp-block mask (warp_block_mask).
 __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1, double p2, float4 gl, float4 gr,
                                                double cx, double cy, FRec &f) {
     const double U1 = fma(e1x, cx, fma(e1y, cy, -p1));
@@ -188,29 +197,29 @@ __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1
     unsigned m = warp_block_mask(mx, my, gr.z * 1.00001f + slack, gr.w * 1.00001f + slack);
     if (ok && m) {
         // Separating axes along the ellipse's own axes (the support's oriented bounding box,
-        // |u_k| <= 3 / sqrt(l_k), against each 8 x 4 block of pixel centres projected on e_k):
+        // |u_k| <= 3 / sqrt(l_k), against each 8 x 8 block of pixel centres projected on e_k):
         // rotated, elongated splats whose axis-aligned box reaches a block often miss it.
         const float ax = fabsf(fe1x), ay = fabsf(fe1y);
         const float marg = 1e-3f + 8.0f * u * (aU1 + aU2 + 16.0f);
-        const float ext1 = 3.0f * rsqrtf(l1) * 1.00001f + marg + (3.5f * ax + 1.5f * ay);
-        const float ext2 = 3.0f * rsqrtf(l2) * 1.00001f + marg + (3.5f * ay + 1.5f * ax);
+        const float ext1 = 3.0f * rsqrtf(l1) * 1.00001f + marg + 3.5f * (ax + ay);
+        const float ext2 = 3.0f * rsqrtf(l2) * 1.00001f + marg + 3.5f * (ay + ax);
         // Two more axes, the diagonals of the support's normalized frame: with v_k = sqrt(l_k) u_k
         // the support is the disc |v| <= 3 and a block is a parallelogram, which misses the disc if
         // its projection on d = (1, +-1)/sqrt(2) stays beyond 3 -- the blocks near the corners of
         // the oriented box, which pass the two tests above without holding a single pixel inside.
         const float s1 = l1 * r1v, s2 = l2 * r2v;  // sqrt(l1), sqrt(l2)
         const float hx1 = s1 * 3.5f * fe1x, hx2 = -s2 * 3.5f * fe1y;  // block half-edges in v space
-        const float hy1 = s1 * 1.5f * fe1y, hy2 = s2 * 1.5f * fe1x;
+        const float hy1 = s1 * 3.5f * fe1y, hy2 = s2 * 3.5f * fe1x;
         const float hwp = (fabsf(hx1 + hx2) + fabsf(hy1 + hy2)) * 0.70710678f;
         const float hwm = (fabsf(hx1 - hx2) + fabsf(hy1 - hy2)) * 0.70710678f;
         const float lim = 3.0f * 1.00001f + (s1 + s2) * marg;
-        // u_k at the block centres (8 bx - 4, 4 by - 6) relative to the tile centre
-        const float u1b = fU1 - 4.0f * fe1x - 6.0f * fe1y, u2b = fU2 + 4.0f * fe1y - 6.0f * fe1x;
+        // u_k at the block centres (8 bx - 4, 8 by - 4) relative to the tile centre
+        const float u1b = fU1 - 4.0f * fe1x - 4.0f * fe1y, u2b = fU2 + 4.0f * fe1y - 4.0f * fe1x;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) {
+        for (int w = 0; w < kBW; ++w) {
             const float bx = (float)(w & 1), by = (float)(w >> 1);
-            const float u1c = u1b + 8.0f * bx * fe1x + 4.0f * by * fe1y;
-            const float u2c = u2b - 8.0f * bx * fe1y + 4.0f * by * fe1x;
+            const float u1c = u1b + 8.0f * bx * fe1x + 8.0f * by * fe1y;
+            const float u2c = u2b - 8.0f * bx * fe1y + 8.0f * by * fe1x;
             const float v1c = s1 * u1c, v2c = s2 * u2c;
             const float slack = lim + 1e-5f * (fabsf(v1c) + fabsf(v2c) + hwp + hwm);
             if (fabsf(u1c) > ext1 || fabsf(u2c) > ext2 || fabsf(v1c + v2c) * 0.70710678f - hwp > slack ||
@@ -218,17 +227,17 @@ __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1
                 m &= ~(1u << w);
         }
     }
-    if (!m) return 0u;  // reaches none of the CTA's warp blocks: the record is never read
+    if (!m) return 0u;  // reaches none of the tile's warp blocks: the record is never read
     // the axes pre-scaled by sqrt(l_k log2(e) / 2) (float64 products, rounded once):
     // h = v1^2 + v2^2 = d2 log2(e) / 2, the exp argument itself; every float error of d2 scales by
     // the same factor, so the d2 bounds carry over with thresholds and ka scaled
     const double sl1 = sqrt((double)l1) * kSqrtHalfLog2e, sl2 = sqrt((double)fmaxf(l2, 0.0f)) * kSqrtHalfLog2e;
     f.a1x = (float)(sl1 * e1x);
     f.a1y = (float)(sl1 * e1y);
-    f.V1 = (float)(sl1 * U1);
+    f.V1 = f.V1b = (float)(sl1 * U1);
     f.c2x = (float)(-sl2 * e1y);
     f.c2y = (float)(sl2 * e1x);
-    f.V2 = (float)(sl2 * U2);
+    f.V2 = f.V2b = (float)(sl2 * U2);
     f.alpha = gl.z;
     f.z = gl.w;
     float rgb[3];
@@ -236,19 +245,19 @@ __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1
     f.r = rgb[0];
     f.g = rgb[1];
     f.b = rgb[2];
-    f.pad = 0.0f;
+    f.pad0 = f.pad1 = 0.0f;
     if (ok) {
         // k (9 -/+ e9) in h units, widened by 1e-6 for the float k and the products' roundings
         const float kf = (float)kHalfLog2e;
         f.thr_in = __fmaf_rn(-kf, e9, kf * 9.0f) - 1.0e-6f;
         f.thr_out = __fmaf_rn(kf, e9, kf * 9.0f) + 1.0e-6f;
         f.ka = 1.4003f * (0.75f * u * sig + 5.25f * u);  // 1.01 / k: eps = ka d2 + kb = ka' h + kb
-        f.kb = 1.01f * (0.75f * u * sig + kEpsExp + 0.5f * kap);
+        f.kb = f.kbb = 1.01f * (0.75f * u * sig + kEpsExp + 0.5f * kap);
     } else {  // every pixel that is not certainly outside takes the float64 test
         f.thr_in = -1.0f;
-        f.thr_out = 3.0e38f;
+        f.thr_out = 1.0e29f;  // below the finished-pixel offset 1e30, above any real h (< 1e15)
         f.ka = 0.0f;
-        f.kb = kEpsExact;
+        f.kb = f.kbb = kEpsExact;
     }
     return m;
 }
@@ -289,11 +298,13 @@ __device__ __forceinline__ void push_fixup(const BlendArgs &b, bool flag, uint32
 }
 
 // The streamed tile list of SOURCE 0 (below): appends to s_queue, in depth order, the depth ranks
-// i in [cursor, s1) whose (tight) tile rectangle covers tile (tx, ty), 256 rectangles per step,
-// until at least `cap` entries wait (the queue holds cap + 255) or the env's list ends. Whole
-// 8192-splat super-batches and 256-splat batches whose union rectangles miss the tile are skipped
-// without a barrier (the branch is uniform across the CTA). Used by the blend and by the harness
-// export of the lists the blend consumes (tile_queue_kernel).
+// i in [cursor, s1) whose (tight) tile rectangle covers tile (tx, ty), one 256-rectangle batch per
+// step (NT threads, 256 / NT rectangles each, in order), until at least `cap` entries wait (the
+// queue holds cap + 255) or the env's list ends. Whole 8192-splat super-batches and 256-splat
+// batches whose union rectangles miss the tile are skipped without a barrier (the branch is
+// uniform across the CTA). Used by the blend and by the harness export of the lists the blend
+// consumes (tile_queue_kernel).
+template <int NT>
 __device__ __forceinline__ void stream_fill(const PassView &v, int tx, int ty, int cap, uint32_t &cursor, uint32_t s1,
                                             int &q_len, uint32_t &scanned, uint32_t *s_queue, uint32_t *s_wsum) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -308,23 +319,26 @@ __device__ __forceinline__ void stream_fill(const PassView &v, int tx, int ty, i
             cursor = b_end;
             continue;
         }
-        uint32_t i = bi * kBlock + threadIdx.x;
-        const bool hit = i >= cursor && i < b_end && covers(__ldg(v.rects + i), tx, ty);
-        unsigned bal = __ballot_sync(kFull, hit);
-        if (lane == 0) s_wsum[warp] = __popc(bal);
-        __syncthreads();
-        int woff = 0, tot = 0;
 #pragma unroll
-        for (int w = 0; w < kBlock / 32; ++w) {
-            int c = s_wsum[w];
-            woff += (w < warp) ? c : 0;
-            tot += c;
+        for (int r = 0; r < kBlock / NT; ++r) {
+            const uint32_t i = bi * kBlock + r * NT + threadIdx.x;
+            const bool hit = i >= cursor && i < b_end && covers(__ldg(v.rects + i), tx, ty);
+            const unsigned bal = __ballot_sync(kFull, hit);
+            if (lane == 0) s_wsum[warp] = __popc(bal);
+            __syncthreads();
+            int woff = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < NT / 32; ++w) {
+                const int c = s_wsum[w];
+                woff += (w < warp) ? c : 0;
+                tot += c;
+            }
+            if (hit) s_queue[q_len + woff + __popc(bal & ((1u << lane) - 1u))] = i;
+            q_len += tot;
+            __syncthreads();
         }
-        if (hit) s_queue[q_len + woff + __popc(bal & ((1u << lane) - 1u))] = i;
-        q_len += tot;
         scanned += b_end - cursor;
         cursor = b_end;
-        __syncthreads();
     }
 }
 
@@ -343,7 +357,7 @@ __global__ void __launch_bounds__(kBlock) tile_queue_kernel(PassView v, int el, 
     uint64_t total = 0;
     while (true) {
         int q_len = 0;
-        stream_fill(v, tx, ty, kBlock, cursor, s1, q_len, scanned, s_queue, s_wsum);
+        stream_fill<kBlock>(v, tx, ty, kBlock, cursor, s1, q_len, scanned, s_queue, s_wsum);
         if (q_len == 0) break;
         if (out)
             for (int i = threadIdx.x; i < q_len; i += kBlock) out[offsets[tile] + total + i] = s_queue[i] - e0;
@@ -362,49 +376,74 @@ __global__ void __launch_bounds__(kBlock) tile_queue_kernel(PassView v, int el, 
 //           record slots, in depth order).
 // SOURCE 2: rasterize_reference -- every splat of the env, in depth order.
 #ifndef SN_BLEND_MIN_BLOCKS
-#define SN_BLEND_MIN_BLOCKS 4
+#define SN_BLEND_MIN_BLOCKS 5
 #endif
 #ifndef SN_LAYER_MIN_BLOCKS
-#define SN_LAYER_MIN_BLOCKS 4
+#define SN_LAYER_MIN_BLOCKS 5
 #endif
+// packed float32 pair helpers (sm_100 FMUL2 / FADD2, each half rounded like the scalar op)
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ float lo_of(f32x2 v) {
+    float a, c;
+    unpack2(v, a, c);
+    return a;
+}
+__device__ __forceinline__ float hi_of(f32x2 v) {
+    float a, c;
+    unpack2(v, a, c);
+    return c;
+}
+
+// One pixel's float32 chain state, packed with the thread's other pixel (lo = row ly, hi = ly + 4).
+struct PixPair {
+    f32x2 T, err, A, cr, cg, cb, D, dead, eps_max, z_last;
+    int nc0, nc1;
+};
+
 template <int MODE, int SOURCE>
-__global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEND_MIN_BLOCKS) blend_kernel(BlendArgs b) {
+__global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEND_MIN_BLOCKS) blend_kernel(BlendArgs b) {
     constexpr bool kBound = MODE != 1;  // depth error bounds feed the compositor
     // the layer tracks each pixel's largest alpha bound (it decides the compositor's depth choice);
     // the scene pass uses the CTA's largest bound over every gathered splat -- looser, one
     // instruction less per contribution
     constexpr bool kPixBound = MODE == 2;
-    // records per batch: tile lists (the avatar layer) take 2 per thread -- their warps' walks are
-    // very uneven (small splats in a few blocks), and fewer, larger batches wait less at barriers
-#ifndef SN_STREAM_PER_THREAD
-#define SN_STREAM_PER_THREAD 1
-#endif
-#ifndef SN_LIST_PER_THREAD
-#define SN_LIST_PER_THREAD 2
-#endif
-    constexpr int kPerT = SOURCE == 1 ? SN_LIST_PER_THREAD : (SOURCE == 0 ? SN_STREAM_PER_THREAD : 1);
-    constexpr int kBatch = kBlock * kPerT;
-    using WlIndex = typename std::conditional<(kBatch > 256), uint16_t, uint8_t>::type;
+    constexpr int kPerT = 2;               // records gathered per thread per batch
+    constexpr int kBatch = kBT * kPerT;    // 256 records per batch
     __shared__ unsigned s_epsmax;
     __shared__ FRec s_f[kBatch];
     __shared__ uint32_t s_slot[kBatch];  // record slot (the boundary band reads its SplatRec)
     __shared__ uint32_t s_queue[SOURCE == 0 ? kBatch + kBlock : 1];
-    __shared__ uint32_t s_wsum[kBlock / 32];
-    __shared__ uint8_t s_mask[kBatch];  // bit w: the splat's support may reach warp w's 8 x 4 block
-    __shared__ WlIndex s_wl[kBlock / 32][kBatch];  // per warp: its batch entries, in depth order
+    __shared__ uint32_t s_wsum[kBW];
+    __shared__ uint8_t s_mask[kBatch];  // bit w: the splat's support may reach warp w's 8 x 8 block
+    __shared__ uint16_t s_wl[kBW][kBatch];  // per warp: byte offsets of its batch entries, in depth order
     const PassView &v = b.pv;
     if (pass_overflow(v)) return;
     if (threadIdx.x == 0) s_epsmax = __float_as_uint(kEpsExact);
     const int tile = blockIdx.x, el = blockIdx.y, env = b.e0 + el;
     const int tx = tile % b.tiles_x, ty = tile / b.tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
+    const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 8 + (lane >> 3);  // rows ly, ly + 4
     const int px_i = tx * kTile + lx;
-    const int py_i = ty * kTile + ly;
-    const bool inside = px_i < b.width && py_i < b.height;
-    const double px = px_i + 0.5, py = py_i + 0.5;
+    const int py0 = ty * kTile + ly, py1 = py0 + 4;
+    const bool in0 = px_i < b.width && py0 < b.height, in1 = px_i < b.width && py1 < b.height;
+    const double px = px_i + 0.5;
     const double x0 = tx * kTile, y0 = ty * kTile;
-    const float oxf = (float)lx - 7.5f, oyf = (float)ly - 7.5f;  // pixel centre - tile centre
+    const float oxf = (float)lx - 7.5f;  // pixel centre - tile centre
+    const f32x2 OX = pack2(oxf, oxf), OY = pack2((float)ly - 7.5f, (float)ly - 3.5f);
 #ifdef SN_BLEND_PROF
     unsigned long long prof[16] = {};
 #define PROF(i, x) (prof[i] += (x))
@@ -428,22 +467,25 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
         s1 = (uint32_t)v.env_off[el + 1];
     }
 
-    float T = 1.0f, A = 0.0f, err = 0.0f;
-    f32x2 crg = 0ull, cbd = 0ull;  // (colour r, g), (colour b, depth sum)
-    const f32x2 o2x = pack2(oxf, oxf), o2y = pack2(oyf, oyf);
-    float eps_max = 0.0f, z_first = 3.0e38f, z_last = 0.0f;
-    int nc = 0;
-    // added to d2: a finished pixel skips every splat. A pixel is finished when it is outside the
+    // added to h: a finished pixel skips every splat. A pixel is finished when it is outside the
     // frame, forced exact, or past the cutoff test (after which T and err never change, so the
-    // cutoff's ambiguity is re-derived from them after the walk)
-    float dead = (!inside || b.force_exact) ? INFINITY : 0.0f;
+    // cutoff's ambiguity is re-derived from them after the walk). 1e30 (not inf) keeps every
+    // product of the chain finite (a finished pixel's alpha is 0 and its eps ~1e24).
+    constexpr float kDead = 1.0e30f;
+    PixPair P;
+    P.T = pack2(1.0f, 1.0f);
+    P.err = P.A = P.cr = P.cg = P.cb = P.D = P.eps_max = P.z_last = 0ull;
+    P.dead = pack2((!in0 || b.force_exact) ? kDead : 0.0f, (!in1 || b.force_exact) ? kDead : 0.0f);
+    P.nc0 = P.nc1 = 0;
+    float z_first = 3.0e38f;
     uint32_t loaded = 0, scanned = 0;
     int q_len = 0;  // SOURCE 0: entries waiting in s_queue (uniform across the CTA)
     while (true) {
-        if (__syncthreads_count(dead == 0.0f) == 0) break;  // also guards s_f / s_queue reuse
+        const bool live = lo_of(P.dead) == 0.0f || hi_of(P.dead) == 0.0f;
+        if (__syncthreads_count(live) == 0) break;  // also guards s_f / s_queue reuse
         int n;
         if (SOURCE == 0) {
-            stream_fill(v, tx, ty, kBatch, cursor, s1, q_len, scanned, s_queue, s_wsum);
+            stream_fill<kBT>(v, tx, ty, kBatch, cursor, s1, q_len, scanned, s_queue, s_wsum);
             n = min(q_len, kBatch);
         } else {
             n = (int)min((uint32_t)kBatch, s1 - cursor);
@@ -452,7 +494,7 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
         loaded += n;
 #pragma unroll
         for (int r = 0; r < kPerT; ++r) {
-            const int jt = threadIdx.x + r * kBlock;
+            const int jt = threadIdx.x + r * kBT;
             if (jt >= n) break;
             // the record slot: tile lists hold slots; streamed / all-splat sources map depth ranks
             const uint32_t rid = SOURCE == 1 ? __ldg(v.pair_vals + cursor + jt)
@@ -470,84 +512,131 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
             s_mask[jt] = (uint8_t)msk;
         }
         __syncthreads();
-        // each warp walks only the batch entries whose support can reach its 8 x 4 pixel block,
+        // each warp walks only the batch entries whose support can reach its 8 x 8 pixel block,
         // in depth order; the per-pixel tests below stay exact, the mask only skips whole warps
         int cnt = 0;
         for (int j0 = 0; j0 < n; j0 += 32) {
             const bool mine = j0 + lane < n && ((s_mask[j0 + lane] >> warp) & 1u);
             const unsigned bal = __ballot_sync(kFull, mine);
-            if (mine) s_wl[warp][cnt + __popc(bal & ((1u << lane) - 1u))] = (WlIndex)(j0 + lane);
+            if (mine) s_wl[warp][cnt + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)((j0 + lane) * sizeof(FRec));
             cnt += __popc(bal);
         }
         __syncwarp();
-        // a lower bound on the pixel's first contribution depth, once per batch instead of per
+        // a lower bound on the pixels' first contribution depth, once per batch instead of per
         // contribution: the warp's entries arrive in depth order, so its first one is the nearest
-        if (kBound && cnt > 0) z_first = fminf(z_first, s_f[s_wl[warp][0]].z);
-        for (int k0 = 0; k0 < cnt && !__all_sync(kFull, dead != 0.0f); k0 += 32) {
+        const char *fbase = reinterpret_cast<const char *>(s_f);
+        if (kBound && cnt > 0) z_first = fminf(z_first, reinterpret_cast<const FRec *>(fbase + s_wl[warp][0])->z);
+        for (int k0 = 0; k0 < cnt; k0 += 32) {
+            if (__all_sync(kFull, !(lo_of(P.dead) == 0.0f || hi_of(P.dead) == 0.0f))) break;
             const int k1 = min(cnt, k0 + 32);
 #pragma unroll kWalkUnroll
             for (int k = k0; k < k1; ++k) {
-                const int j = s_wl[warp][k];
+                const FRec &s = *reinterpret_cast<const FRec *>(fbase + s_wl[warp][k]);
                 PROF(0, lane == 0);
-                const FRec &s = s_f[j];
-                const float4 q0 = *reinterpret_cast<const float4 *>(&s.a1x);
-                const float4 q1 = *reinterpret_cast<const float4 *>(&s.V1);
-                float v1, v2;
-                unpack2(fma2(pack2(q0.x, q0.y), o2x, fma2(pack2(q0.z, q0.w), o2y, pack2(q1.x, q1.y))), v1, v2);
-                // + dead: exact (v2^2 + 0 rounds like v2 * v2), or +inf for a finished pixel
-                float d2 = __fmaf_rn(v1, v1, __fmaf_rn(v2, v2, dead));
-                if (d2 > q1.z) continue;  // saturated (dead = inf), or certainly outside the support
-                const float4 q2 = *reinterpret_cast<const float4 *>(&s.ka);  // (ka, kb, alpha, -): one load
-                float eps;
-                if (d2 < q1.w) {
-                    eps = __fmaf_rn(d2, q2.x, q2.y);
-                } else {  // boundary band: the reference's float64 test (_kernels_cy.pyx:73-75)
-                    PROF(1, 1);
-                    const SplatRec &sd = v.recs[s_slot[j]];
-                    const double ddx = sd.mx - px, ddy = sd.my - py;
-                    const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
-                    if (d2d > kSupportD2) continue;
-                    d2 = (float)(d2d * kHalfLog2e);  // h, rounded once (within kEpsExact)
-                    eps = kEpsExact;
+                const float4 q0 = *reinterpret_cast<const float4 *>(&s.a1x);   // a1x a1y c2x c2y
+                const float4 q1 = *reinterpret_cast<const float4 *>(&s.V1);    // V1 V1 V2 V2
+                const float4 q2 = *reinterpret_cast<const float4 *>(&s.thr_out);  // thr_out thr_in kb kb
+                // v_k for both pixels (same ox, oy and oy + 4), then h = v1^2 + v2^2 (+ dead)
+                const f32x2 v1 = fma2(OY, pack2(q0.y, q0.y), fma2(OX, pack2(q0.x, q0.x), pack2(q1.x, q1.y)));
+                const f32x2 v2 = fma2(OY, pack2(q0.w, q0.w), fma2(OX, pack2(q0.z, q0.z), pack2(q1.z, q1.w)));
+                const f32x2 h = fma2(v1, v1, fma2(v2, v2, P.dead));
+                float h0, h1;
+                unpack2(h, h0, h1);
+                // both pixels certainly outside the support (or finished) for the whole warp: next
+                if (__all_sync(kFull, h0 > q2.x && h1 > q2.x)) continue;
+                bool c0 = h0 <= q2.y, c1 = h1 <= q2.y;  // certainly inside
+                f32x2 hh = h;
+                const float4 q3 = *reinterpret_cast<const float4 *>(&s.ka);  // ka alpha z -
+                f32x2 eps2 = fma2(h, pack2(q3.x, q3.x), pack2(q2.z, q2.w));  // ka h + kb
+                const bool b0 = !c0 && h0 <= q2.x, b1 = !c1 && h1 <= q2.x;
+                if (__any_sync(kFull, b0 || b1)) {
+                    // boundary band: the reference's float64 test (_kernels_cy.pyx:73-75)
+                    PROF(1, (unsigned)b0 + (unsigned)b1);
+                    const int j = (int)((reinterpret_cast<const char *>(&s) - fbase) / sizeof(FRec));
+                    float e0, e1;
+                    unpack2(eps2, e0, e1);
+                    if (b0 || b1) {
+                        const SplatRec &sd = v.recs[s_slot[j]];
+                        const double ddx = sd.mx - px;
+                        if (b0) {
+                            const double ddy = sd.my - (py0 + 0.5);
+                            const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
+                            if (!(d2d > kSupportD2)) {
+                                c0 = true;
+                                h0 = (float)(d2d * kHalfLog2e);  // h, rounded once (within kEpsExact)
+                                e0 = kEpsExact;
+                            }
+                        }
+                        if (b1) {
+                            const double ddy = sd.my - (py1 + 0.5);
+                            const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
+                            if (!(d2d > kSupportD2)) {
+                                c1 = true;
+                                h1 = (float)(d2d * kHalfLog2e);
+                                e1 = kEpsExact;
+                            }
+                        }
+                    }
+                    hh = pack2(h0, h1);
+                    eps2 = pack2(e0, e1);
                 }
-                const float e = ex2_approx(-d2);  // 2^-h: the negation is an operand modifier
-                const float a = fminf(q2.z * e, 0.99f);
-                const float w = a * T;
-                const float Tn = __fmaf_rn(-a, T, T);  // T (1 - a), rounded once
-                const float4 q3 = *reinterpret_cast<const float4 *>(&s.r);
-                crg = fma2(pack2(q3.x, q3.y), pack2(w, w), crg);
-                cbd = fma2(pack2(q3.z, q3.w), pack2(w, w), cbd);
-                A = A + w;
-                err = __fmaf_rn(-a, err, __fmaf_rn(w, eps, __fmaf_rn(Tn, kU125, err)));  // err (1 - a) + ...
-                T = Tn;
-                ++nc;
-                if (kPixBound) eps_max = fmaxf(eps_max, eps);
-                if (kBound) z_last = fmaxf(z_last, q3.w);  // one op into a fixed register (a copy would be two)
+                // alpha = min(o 2^-h, .99) inside the support, 0 outside (T, err and the sums then
+                // stay exactly as they were: w = 0, T (1 - 0) = T)
+                float x0h, x1h;
+                unpack2(hh, x0h, x1h);
+                const f32x2 ee = mul2(pack2(ex2_approx(-x0h), ex2_approx(-x1h)), pack2(q3.y, q3.y));
+                float a0, a1;
+                unpack2(ee, a0, a1);
+                a0 = c0 ? fminf(a0, 0.99f) : 0.0f;
+                a1 = c1 ? fminf(a1, 0.99f) : 0.0f;
+                const f32x2 a = pack2(a0, a1), na = pack2(-a0, -a1);
+                const f32x2 w = mul2(a, P.T);
+                const f32x2 Tn = fma2(na, P.T, P.T);  // T (1 - a), rounded once
+                const float4 q4 = *reinterpret_cast<const float4 *>(&s.r);  // r g b -
+                P.cr = fma2(w, pack2(q4.x, q4.x), P.cr);
+                P.cg = fma2(w, pack2(q4.y, q4.y), P.cg);
+                P.cb = fma2(w, pack2(q4.z, q4.z), P.cb);
+                P.D = fma2(w, pack2(q3.z, q3.z), P.D);
+                P.A = add2(P.A, w);
+                // err (1 - a) + w eps + 1.25 u T' (the last term only where T changed)
+                const f32x2 ku = pack2(c0 ? kU125 : 0.0f, c1 ? kU125 : 0.0f);
+                P.err = fma2(na, P.err, fma2(w, eps2, fma2(Tn, ku, P.err)));
+                P.T = Tn;
+                P.nc0 += c0;
+                P.nc1 += c1;
+                if (kPixBound) {
+                    float m0, m1, s0, s1_;
+                    unpack2(P.eps_max, m0, m1);
+                    unpack2(eps2, s0, s1_);
+                    P.eps_max = pack2(c0 ? fmaxf(m0, s0) : m0, c1 ? fmaxf(m1, s1_) : m1);
+                }
+                if (kBound) {
+                    float z0, z1;
+                    unpack2(P.z_last, z0, z1);
+                    P.z_last = pack2(c0 ? fmaxf(z0, q3.z) : z0, c1 ? fmaxf(z1, q3.z) : z1);
+                }
                 // near the cutoff (_kernels_cy.pyx:65-66): stop; decided or deferred after the walk
-                if (Tn - err <= kTHi) dead = INFINITY;
+                float m0, m1;
+                unpack2(sub2(Tn, P.err), m0, m1);
+                float d0, d1;
+                unpack2(P.dead, d0, d1);
+                P.dead = pack2(m0 <= kTHi ? kDead : d0, m1 <= kTHi ? kDead : d1);
             }
         }
         if (SOURCE == 0) {  // drop the consumed head of the queue
-            int rest = q_len - n;
-            uint32_t qv = threadIdx.x < rest ? s_queue[n + threadIdx.x] : 0u;
+            const int rest = q_len - n;
+            uint32_t qv0 = threadIdx.x < rest ? s_queue[n + threadIdx.x] : 0u;
+            uint32_t qv1 = threadIdx.x + kBT < rest ? s_queue[n + kBT + threadIdx.x] : 0u;
             __syncthreads();
-            if (threadIdx.x < rest) s_queue[threadIdx.x] = qv;
+            if (threadIdx.x < rest) s_queue[threadIdx.x] = qv0;
+            if (threadIdx.x + kBT < rest) s_queue[kBT + threadIdx.x] = qv1;
             q_len = rest;
         } else {
             cursor += n;
         }
     }
-    float cr, cg, cb, D;
-    unpack2(crg, cr, cg);
-    unpack2(cbd, cb, D);
-    // the cutoff fired (T - err <= 1e-4 (1 + 1e-6)) but T < 1e-4 is not certain: float64 fixup.
-    // Also when err > T / 16: the 0.25 u T' margin in kU125 covers the bound's own float roundings
-    // (<= 2u err per step) only while err <= T / 8, and err / T never decreases along the walk.
-    const bool cut = T - err <= kTHi;
-    const bool amb = inside && (b.force_exact || (cut && (!(T + err < kTLo) || err > 0.0625f * T)));
-    PROF(2, amb);
 #ifdef SN_BLEND_PROF
-    const bool prof_live = __syncthreads_or(dead == 0.0f) != 0;
+    const bool prof_live = __syncthreads_or(lo_of(P.dead) == 0.0f || hi_of(P.dead) == 0.0f) != 0;
     if (SOURCE == 0 && MODE == 0 && threadIdx.x == 0) {
         const uint32_t st = (uint32_t)v.env_off[el], tot = s1 - st;
         // consumed: the list position the walk had reached (queued-but-unwalked entries excluded)
@@ -555,7 +644,7 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
         const unsigned fr = tot ? (unsigned)((1000ull * used) / tot) : 0u;
         atomicMax(&g_env_frac[el & 63], fr);
         // log-spaced bins of the consumed fraction (1e-5 units): <=0.1%, 0.2, 0.5, 1, 2, 5, 10, 20,
-        // 50, <100%; bin 14: the list ran out with a live (unsaturated) pixel
+        // 50, <100%; bin 10: the list ran out with a live (unsaturated) pixel
         const unsigned f5 = tot ? (unsigned)((100000ull * used) / tot) : 0u;
         const unsigned edges[9] = {100, 200, 500, 1000, 2000, 5000, 10000, 20000, 50000};
         unsigned bin = 9;
@@ -571,71 +660,100 @@ __global__ void __launch_bounds__(kBlock, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_B
     if (b.loads && threadIdx.x == 0 && loaded) atomicAdd(b.loads, (unsigned long long)loaded);
 
     const sn_camera &cam = b.cams[env];
-    const int64_t pix = ((int64_t)env * b.height + py_i) * b.width + px_i;
-    const uint32_t code = (uint32_t)(((int64_t)el * b.height + py_i) * b.width + px_i);
-    // Error bounds of the outputs the compositor decides on. Every weight w_i = a_i T_(i-1) has
-    // relative error <= rho_w (transmittance bound + largest alpha bound + the product's rounding);
-    // depth = sum z w / sum w then errs by <= rho_w (z_last - z_first) from the weights (z spans the
-    // contributions) plus (2n + 2) u from the float sums and the division; alpha by rho_w + (n + 1) u.
-    if (!kPixBound) eps_max = __uint_as_float(s_epsmax);
-    if (nc == 0) z_first = 3.0e38f;  // no contribution: the empty range, as before any batch
-    const float rho_w = err / T + eps_max + 6.0e-8f;
-    const float alpha = fminf(A, 1.0f);
-    const float depth = A > 0.0f ? D / A : (float)cam.far_;
-    const float d_err = 1.01f * (rho_w * (z_last - z_first) + (float)(2 * nc + 2) * 6.0e-8f * depth);
-    const bool flag = inside && amb;
+    if (!kPixBound) P.eps_max = pack2(__uint_as_float(s_epsmax), __uint_as_float(s_epsmax));
+    float T2[2], E2[2], A2[2], CR[2], CG[2], CB[2], DD[2], EM[2], ZL[2];
+    unpack2(P.T, T2[0], T2[1]);
+    unpack2(P.err, E2[0], E2[1]);
+    unpack2(P.A, A2[0], A2[1]);
+    unpack2(P.cr, CR[0], CR[1]);
+    unpack2(P.cg, CG[0], CG[1]);
+    unpack2(P.cb, CB[0], CB[1]);
+    unpack2(P.D, DD[0], DD[1]);
+    unpack2(P.eps_max, EM[0], EM[1]);
+    unpack2(P.z_last, ZL[0], ZL[1]);
+    const int NC[2] = {P.nc0, P.nc1};
+    const bool IN[2] = {in0, in1};
+    const int PY[2] = {py0, py1};
+    unsigned contrib_sum = 0;
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const float T = T2[p], err = E2[p], A = A2[p];
+        const int nc = NC[p];
+        const bool inside = IN[p];
+        const int py_i = PY[p];
+        // the cutoff fired (T - err <= 1e-4 (1 + 1e-6)) but T < 1e-4 is not certain: float64 fixup.
+        // Also when err > T / 16: the 0.25 u T' margin in kU125 covers the bound's own float
+        // roundings (<= 2u err per step) only while err <= T / 8, and err / T never decreases.
+        const bool cut = T - err <= kTHi;
+        const bool amb = inside && (b.force_exact || (cut && (!(T + err < kTLo) || err > 0.0625f * T)));
+        PROF(2, amb);
+        const int64_t pix = ((int64_t)env * b.height + py_i) * b.width + px_i;
+        const uint32_t code = (uint32_t)(((int64_t)el * b.height + py_i) * b.width + px_i);
+        // Error bounds of the outputs the compositor decides on. Every weight w_i = a_i T_(i-1) has
+        // relative error <= rho_w (transmittance bound + largest alpha bound + the product's
+        // rounding); depth = sum z w / sum w then errs by <= rho_w (z_last - z_first) from the
+        // weights (z spans the contributions) plus (2n + 2) u from the float sums and the division;
+        // alpha by rho_w + (n + 1) u.
+        const float zf = nc == 0 ? 3.0e38f : z_first;  // no contribution: the empty range
+        const float rho_w = err / T + EM[p] + 6.0e-8f;
+        const float alpha = fminf(A, 1.0f);
+        const float depth = A > 0.0f ? DD[p] / A : (float)cam.far_;
+        const float d_err = 1.01f * (rho_w * (ZL[p] - zf) + (float)(2 * nc + 2) * 6.0e-8f * depth);
+        const bool flag = inside && amb;
+        contrib_sum += flag ? 0u : (unsigned)nc;
+        push_fixup(b, flag, code);
+        if (!inside) continue;
+        if (MODE == 2 && SOURCE != 1 && threadIdx.x == 0 && p == 0) b.tile_flag[(int64_t)el * gridDim.x + tile] = 1;
+        if (flag) {
+            if (MODE == 2) b.ldepth[pix] = __int_as_float(0x7fc00000);  // NaN: pending float64 fixup
+            continue;
+        }
+        if (b.contrib) b.contrib[pix] = nc;
+        if (MODE == 0) {
+            float *oc = b.color + 3 * pix;
+            const float o0 = np_clipf(__fmaf_rn((float)cam.background[0], T, CR[p]), 0.0f, 1.0f);
+            const float o1 = np_clipf(__fmaf_rn((float)cam.background[1], T, CG[p]), 0.0f, 1.0f);
+            const float o2 = np_clipf(__fmaf_rn((float)cam.background[2], T, CB[p]), 0.0f, 1.0f);
+            oc[0] = o0;
+            oc[1] = o1;
+            oc[2] = o2;
+            b.alpha[pix] = alpha;
+            b.depth[pix] = depth;
+            if (b.derr) b.derr[pix] = A > 0.0f ? d_err : 0.0f;
+            store_payload(b, pix, o0, o1, o2, depth);
+            continue;
+        }
+        float fc0 = 0.0f, fc1 = 0.0f, fc2 = 0.0f;
+        if (A > 0.0f) {
+            fc0 = np_clipf(CR[p] / A, 0.0f, 1.0f);
+            fc1 = np_clipf(CG[p] / A, 0.0f, 1.0f);
+            fc2 = np_clipf(CB[p] / A, 0.0f, 1.0f);
+        }
+        if (MODE == 1) {
+            float *oc = b.color + 3 * pix;
+            oc[0] = fc0;
+            oc[1] = fc1;
+            oc[2] = fc2;
+            b.alpha[pix] = alpha;
+            b.depth[pix] = depth;
+            store_payload(b, pix, fc0, fc1, fc2, depth);
+            continue;
+        }
+        // MODE 2: the layer frame goes to its own buffers; composite_kernel merges it into the scene
+        // frame once the scene pass is done (so this blend runs concurrently with the scene blend)
+        float *lc = b.lcolor + 3 * pix;
+        lc[0] = fc0;
+        lc[1] = fc1;
+        lc[2] = fc2;
+        b.lalpha[pix] = alpha;
+        b.ldepth[pix] = depth;
+        b.lderr[pix] = d_err;
+        b.laerr[pix] = 1.01f * (rho_w + (float)(nc + 1) * 6.0e-8f) * A + 6.0e-8f;
+    }
     if (b.contribs) {
-        unsigned sum = __reduce_add_sync(kFull, flag ? 0u : (unsigned)nc);
+        const unsigned sum = __reduce_add_sync(kFull, contrib_sum);
         if (lane == 0 && sum) atomicAdd(b.contribs, (unsigned long long)sum);
     }
-    push_fixup(b, flag, code);
-    if (!inside) return;
-    if (MODE == 2 && SOURCE != 1 && threadIdx.x == 0) b.tile_flag[(int64_t)el * gridDim.x + tile] = 1;
-    if (flag) {
-        if (MODE == 2) b.ldepth[pix] = __int_as_float(0x7fc00000);  // NaN: pending float64 fixup
-        return;
-    }
-    if (b.contrib) b.contrib[pix] = nc;
-    if (MODE == 0) {
-        float *oc = b.color + 3 * pix;
-        const float o0 = np_clipf(__fmaf_rn((float)cam.background[0], T, cr), 0.0f, 1.0f);
-        const float o1 = np_clipf(__fmaf_rn((float)cam.background[1], T, cg), 0.0f, 1.0f);
-        const float o2 = np_clipf(__fmaf_rn((float)cam.background[2], T, cb), 0.0f, 1.0f);
-        oc[0] = o0;
-        oc[1] = o1;
-        oc[2] = o2;
-        b.alpha[pix] = alpha;
-        b.depth[pix] = depth;
-        if (b.derr) b.derr[pix] = A > 0.0f ? d_err : 0.0f;
-        store_payload(b, pix, o0, o1, o2, depth);
-        return;
-    }
-    float fc0 = 0.0f, fc1 = 0.0f, fc2 = 0.0f;
-    if (A > 0.0f) {
-        fc0 = np_clipf(cr / A, 0.0f, 1.0f);
-        fc1 = np_clipf(cg / A, 0.0f, 1.0f);
-        fc2 = np_clipf(cb / A, 0.0f, 1.0f);
-    }
-    if (MODE == 1) {
-        float *oc = b.color + 3 * pix;
-        oc[0] = fc0;
-        oc[1] = fc1;
-        oc[2] = fc2;
-        b.alpha[pix] = alpha;
-        b.depth[pix] = depth;
-        store_payload(b, pix, fc0, fc1, fc2, depth);
-        return;
-    }
-    // MODE 2: the layer frame goes to its own buffers; composite_kernel merges it into the scene
-    // frame once the scene pass is done (so this blend runs concurrently with the scene blend)
-    float *lc = b.lcolor + 3 * pix;
-    lc[0] = fc0;
-    lc[1] = fc1;
-    lc[2] = fc2;
-    b.lalpha[pix] = alpha;
-    b.ldepth[pix] = depth;
-    b.lderr[pix] = d_err;
-    b.laerr[pix] = 1.01f * (rho_w + (float)(nc + 1) * 6.0e-8f) * A + 6.0e-8f;
 #undef PROF
 }
 
@@ -1325,11 +1443,11 @@ __global__ void blend_tile_range_kernel(int t_begin, int tiles_x, int tile_size,
 template <int MODE>
 static void launch_blend_mode(const BlendArgs &b, dim3 grid, cudaStream_t s) {
     if (b.pv.source == 0)
-        blend_kernel<MODE, 0><<<grid, kBlock, 0, s>>>(b);
+        blend_kernel<MODE, 0><<<grid, kBT, 0, s>>>(b);
     else if (b.pv.source == 1)
-        blend_kernel<MODE, 1><<<grid, kBlock, 0, s>>>(b);
+        blend_kernel<MODE, 1><<<grid, kBT, 0, s>>>(b);
     else
-        blend_kernel<MODE, 2><<<grid, kBlock, 0, s>>>(b);
+        blend_kernel<MODE, 2><<<grid, kBT, 0, s>>>(b);
     if (MODE != 2) fixup_kernel<MODE><<<kFixupBlocks, 256, 0, s>>>(b);  // mode 2: after the composite
 }
 
