@@ -133,13 +133,14 @@ constexpr int kBW = kBT / 32;  // warps (8 x 8 pixel blocks) per tile
 
 // Shared-memory form of a gathered splat for the float32 chain (80 B): the principal-axis rows (a
 // pixel's v_k = row_k . o + V_k, h = v1^2 + v2^2), V1 and V2 twice (register pairs for FFMA2), the
-// decision thresholds k (9 -/+ E(9.1)), alpha's error bound coefficients (eps = ka h + kb, kb twice),
-// alpha, z and colour. k = log2(e) / 2: the chain works on h = k d2, so alpha = o 2^-h.
+// decision thresholds k (9 -/+ E(9.1)), alpha's error bound coefficients NEGATED (-eps = nka h +
+// nkb, nkb twice: the walk carries negated weights, see blend_kernel), alpha, z and colour.
+// k = log2(e) / 2: the chain works on h = k d2, so alpha = o 2^-h.
 struct __align__(16) FRec {
     float a1x, a1y, c2x, c2y;
     float V1, V1b, V2, V2b;
-    float thr_out, thr_in, kb, kbb;
-    float ka, alpha, z, pad0;
+    float thr_out, thr_in, nkb, nkbb;
+    float nka, alpha, z, pad0;
     float r, g, b, pad1;
 };
 static_assert(sizeof(FRec) == 80, "FRec layout");
@@ -251,13 +252,13 @@ __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1
         const float kf = (float)kHalfLog2e;
         f.thr_in = __fmaf_rn(-kf, e9, kf * 9.0f) - 1.0e-6f;
         f.thr_out = __fmaf_rn(kf, e9, kf * 9.0f) + 1.0e-6f;
-        f.ka = 1.4003f * (0.75f * u * sig + 5.25f * u);  // 1.01 / k: eps = ka d2 + kb = ka' h + kb
-        f.kb = f.kbb = 1.01f * (0.75f * u * sig + kEpsExp + 0.5f * kap);
+        f.nka = -1.4003f * (0.75f * u * sig + 5.25f * u);  // 1.01 / k: eps = ka d2 + kb = ka' h + kb
+        f.nkb = f.nkbb = -1.01f * (0.75f * u * sig + kEpsExp + 0.5f * kap);
     } else {  // every pixel that is not certainly outside takes the float64 test
         f.thr_in = -1.0f;
         f.thr_out = 1.0e29f;  // below the finished-pixel offset 1e30, above any real h (< 1e15)
-        f.ka = 0.0f;
-        f.kb = f.kbb = kEpsExact;
+        f.nka = 0.0f;
+        f.nkb = f.nkbb = -kEpsExact;
     }
     return m;
 }
@@ -410,8 +411,7 @@ __device__ __forceinline__ float hi_of(f32x2 v) {
 
 // One pixel's float32 chain state, packed with the thread's other pixel (lo = row ly, hi = ly + 4).
 struct PixPair {
-    f32x2 T, err, A, cr, cg, cb, D, dead, eps_max, z_last;
-    int nc0, nc1;
+    f32x2 T, err, A, cr, cg, cb, D, dead, eps_max, z_last, nc;  // nc: contributions (exact floats)
 };
 
 template <int MODE, int SOURCE>
@@ -424,15 +424,21 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
     constexpr int kPerT = 2;               // records gathered per thread per batch
     constexpr int kBatch = kBT * kPerT;    // 256 records per batch
     __shared__ unsigned s_epsmax;
-    __shared__ FRec s_f[kBatch];
+    __shared__ FRec s_f[kBatch + 1];     // + a record no pixel is inside of (list padding)
     __shared__ uint32_t s_slot[kBatch];  // record slot (the boundary band reads its SplatRec)
     __shared__ uint32_t s_queue[SOURCE == 0 ? kBatch + kBlock : 1];
     __shared__ uint32_t s_wsum[kBW];
     __shared__ uint8_t s_mask[kBatch];  // bit w: the splat's support may reach warp w's 8 x 8 block
-    __shared__ uint16_t s_wl[kBW][kBatch];  // per warp: byte offsets of its batch entries, in depth order
+    // per warp: byte offsets of its batch entries, in depth order, padded to a multiple of the
+    // walk's unroll with the inert record
+    __shared__ uint16_t s_wl[kBW][kBatch + kWalkUnroll];
     const PassView &v = b.pv;
     if (pass_overflow(v)) return;
     if (threadIdx.x == 0) s_epsmax = __float_as_uint(kEpsExact);
+    if (threadIdx.x < 20) {  // the inert record: h = dead >= 0 > thr_in = thr_out = -1, alpha 0
+        float *d = reinterpret_cast<float *>(&s_f[kBatch]);
+        d[threadIdx.x] = (threadIdx.x == 8 || threadIdx.x == 9) ? -1.0f : 0.0f;
+    }
     const int tile = blockIdx.x, el = blockIdx.y, env = b.e0 + el;
     const int tx = tile % b.tiles_x, ty = tile / b.tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -474,9 +480,8 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
     constexpr float kDead = 1.0e30f;
     PixPair P;
     P.T = pack2(1.0f, 1.0f);
-    P.err = P.A = P.cr = P.cg = P.cb = P.D = P.eps_max = P.z_last = 0ull;
+    P.err = P.A = P.cr = P.cg = P.cb = P.D = P.eps_max = P.z_last = P.nc = 0ull;
     P.dead = pack2((!in0 || b.force_exact) ? kDead : 0.0f, (!in1 || b.force_exact) ? kDead : 0.0f);
-    P.nc0 = P.nc1 = 0;
     float z_first = 3.0e38f;
     uint32_t loaded = 0, scanned = 0;
     int q_len = 0;  // SOURCE 0: entries waiting in s_queue (uniform across the CTA)
@@ -506,7 +511,7 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
             FRec f;
             unsigned msk = tile_entry(ge.x, ge.y, gp.x, gp.y, gl, gr, x0 + 8.0, y0 + 8.0, f);
             if (kBound && !kPixBound && msk)  // eps at the support edge bounds eps inside it
-                atomicMax(&s_epsmax, __float_as_uint(__fmaf_rn(f.ka, fminf(f.thr_out, 7.0f), f.kb)));
+                atomicMax(&s_epsmax, __float_as_uint(-__fmaf_rn(f.nka, fminf(f.thr_out, 7.0f), f.nkb)));
             if (msk) s_f[jt] = f;  // an entry no warp walks is never read
             s_slot[jt] = rid;
             s_mask[jt] = (uint8_t)msk;
@@ -521,106 +526,105 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
             if (mine) s_wl[warp][cnt + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)((j0 + lane) * sizeof(FRec));
             cnt += __popc(bal);
         }
+        const int cnt_pad = (cnt + kWalkUnroll - 1) / kWalkUnroll * kWalkUnroll;
+        if (lane < cnt_pad - cnt) s_wl[warp][cnt + lane] = (uint16_t)(kBatch * sizeof(FRec));
         __syncwarp();
-        // a lower bound on the pixels' first contribution depth, once per batch instead of per
-        // contribution: the warp's entries arrive in depth order, so its first one is the nearest
+        // depth bounds of the contributions, once per batch instead of per contribution: the warp's
+        // entries arrive in depth order, so its first one is a lower bound of every pixel's first
+        // contribution, and its last one an upper bound of any contribution a pixel still live at
+        // the batch's start makes in it
         const char *fbase = reinterpret_cast<const char *>(s_f);
-        if (kBound && cnt > 0) z_first = fminf(z_first, reinterpret_cast<const FRec *>(fbase + s_wl[warp][0])->z);
-        for (int k0 = 0; k0 < cnt; k0 += 32) {
+        if (kBound && cnt > 0) {
+            z_first = fminf(z_first, reinterpret_cast<const FRec *>(fbase + s_wl[warp][0])->z);
+            const float zb = reinterpret_cast<const FRec *>(fbase + s_wl[warp][cnt - 1])->z;
+            float z0, z1, d0, d1;
+            unpack2(P.z_last, z0, z1);
+            unpack2(P.dead, d0, d1);
+            P.z_last = pack2(d0 == 0.0f ? fmaxf(z0, zb) : z0, d1 == 0.0f ? fmaxf(z1, zb) : z1);
+        }
+        // The walk carries NEGATED weights: na = -a (the inside mask m is -1 / 0), so T (1 - a) =
+        // fma(na, T, T) and err (1 - a) = fma(na, err, .) need no negation; nw = -w, and the colour,
+        // depth, A and contribution sums accumulate negated (flipped once in the epilogue).
+        for (int k0 = 0; k0 < cnt_pad; k0 += 32) {
             if (__all_sync(kFull, !(lo_of(P.dead) == 0.0f || hi_of(P.dead) == 0.0f))) break;
-            const int k1 = min(cnt, k0 + 32);
-#pragma unroll kWalkUnroll
-            for (int k = k0; k < k1; ++k) {
-                const FRec &s = *reinterpret_cast<const FRec *>(fbase + s_wl[warp][k]);
+            const int k1 = min(cnt_pad, k0 + 32);
+            for (int k = k0; k < k1; k += kWalkUnroll) {
+#pragma unroll
+            for (int ku = 0; ku < kWalkUnroll; ++ku) {
+                const FRec &s = *reinterpret_cast<const FRec *>(fbase + s_wl[warp][k + ku]);
                 PROF(0, lane == 0);
-                const float4 q0 = *reinterpret_cast<const float4 *>(&s.a1x);   // a1x a1y c2x c2y
-                const float4 q1 = *reinterpret_cast<const float4 *>(&s.V1);    // V1 V1 V2 V2
-                const float4 q2 = *reinterpret_cast<const float4 *>(&s.thr_out);  // thr_out thr_in kb kb
-                // v_k for both pixels (same ox, oy and oy + 4), then h = v1^2 + v2^2 (+ dead)
+                const float4 q0 = *reinterpret_cast<const float4 *>(&s.a1x);      // a1x a1y c2x c2y
+                const float4 q1 = *reinterpret_cast<const float4 *>(&s.V1);       // V1 V1 V2 V2
+                const float4 q2 = *reinterpret_cast<const float4 *>(&s.thr_out);  // thr_out thr_in nkb nkb
+                const float4 q3 = *reinterpret_cast<const float4 *>(&s.nka);      // nka alpha z -
+                // v_k for both pixels (same ox; oy and oy + 4), h = v1^2 + v2^2 (+ the finished offset)
                 const f32x2 v1 = fma2(OY, pack2(q0.y, q0.y), fma2(OX, pack2(q0.x, q0.x), pack2(q1.x, q1.y)));
                 const f32x2 v2 = fma2(OY, pack2(q0.w, q0.w), fma2(OX, pack2(q0.z, q0.z), pack2(q1.z, q1.w)));
                 const f32x2 h = fma2(v1, v1, fma2(v2, v2, P.dead));
+                f32x2 neps = fma2(h, pack2(q3.x, q3.x), pack2(q2.z, q2.w));  // -(alpha's relative bound)
                 float h0, h1;
                 unpack2(h, h0, h1);
-                // both pixels certainly outside the support (or finished) for the whole warp: next
-                if (__all_sync(kFull, h0 > q2.x && h1 > q2.x)) continue;
-                bool c0 = h0 <= q2.y, c1 = h1 <= q2.y;  // certainly inside
-                f32x2 hh = h;
-                const float4 q3 = *reinterpret_cast<const float4 *>(&s.ka);  // ka alpha z -
-                f32x2 eps2 = fma2(h, pack2(q3.x, q3.x), pack2(q2.z, q2.w));  // ka h + kb
-                const bool b0 = !c0 && h0 <= q2.x, b1 = !c1 && h1 <= q2.x;
-                if (__any_sync(kFull, b0 || b1)) {
-                    // boundary band: the reference's float64 test (_kernels_cy.pyx:73-75)
-                    PROF(1, (unsigned)b0 + (unsigned)b1);
+                // -1 where the pixel is certainly inside the support, 0 where outside or finished
+                float m0 = __int_as_float(h0 <= q2.y ? (int)0xbf800000 : 0);
+                float m1 = __int_as_float(h1 <= q2.y ? (int)0xbf800000 : 0);
+                if ((h0 > q2.y && h0 <= q2.x) || (h1 > q2.y && h1 <= q2.x)) {
+                    // boundary band (rare, divergent): the reference's float64 test (_kernels_cy.pyx:73-75)
+                    PROF(1, 1);
                     const int j = (int)((reinterpret_cast<const char *>(&s) - fbase) / sizeof(FRec));
+                    const SplatRec &sd = v.recs[s_slot[j]];
+                    const double ddx = sd.mx - px;
                     float e0, e1;
-                    unpack2(eps2, e0, e1);
-                    if (b0 || b1) {
-                        const SplatRec &sd = v.recs[s_slot[j]];
-                        const double ddx = sd.mx - px;
-                        if (b0) {
-                            const double ddy = sd.my - (py0 + 0.5);
-                            const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
-                            if (!(d2d > kSupportD2)) {
-                                c0 = true;
-                                h0 = (float)(d2d * kHalfLog2e);  // h, rounded once (within kEpsExact)
-                                e0 = kEpsExact;
-                            }
-                        }
-                        if (b1) {
-                            const double ddy = sd.my - (py1 + 0.5);
-                            const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
-                            if (!(d2d > kSupportD2)) {
-                                c1 = true;
-                                h1 = (float)(d2d * kHalfLog2e);
-                                e1 = kEpsExact;
-                            }
+                    unpack2(neps, e0, e1);
+                    if (h0 > q2.y && h0 <= q2.x) {
+                        const double ddy = sd.my - (py0 + 0.5);
+                        const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
+                        if (!(d2d > kSupportD2)) {
+                            m0 = -1.0f;
+                            h0 = (float)(d2d * kHalfLog2e);  // h, rounded once (within kEpsExact)
+                            e0 = -kEpsExact;
                         }
                     }
-                    hh = pack2(h0, h1);
-                    eps2 = pack2(e0, e1);
+                    if (h1 > q2.y && h1 <= q2.x) {
+                        const double ddy = sd.my - (py1 + 0.5);
+                        const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
+                        if (!(d2d > kSupportD2)) {
+                            m1 = -1.0f;
+                            h1 = (float)(d2d * kHalfLog2e);
+                            e1 = -kEpsExact;
+                        }
+                    }
+                    neps = pack2(e0, e1);
                 }
-                // alpha = min(o 2^-h, .99) inside the support, 0 outside (T, err and the sums then
-                // stay exactly as they were: w = 0, T (1 - 0) = T)
-                float x0h, x1h;
-                unpack2(hh, x0h, x1h);
-                const f32x2 ee = mul2(pack2(ex2_approx(-x0h), ex2_approx(-x1h)), pack2(q3.y, q3.y));
-                float a0, a1;
-                unpack2(ee, a0, a1);
-                a0 = c0 ? fminf(a0, 0.99f) : 0.0f;
-                a1 = c1 ? fminf(a1, 0.99f) : 0.0f;
-                const f32x2 a = pack2(a0, a1), na = pack2(-a0, -a1);
-                const f32x2 w = mul2(a, P.T);
+                const f32x2 m = pack2(m0, m1);
+                // alpha = min(o 2^-h, .99) inside the support, 0 outside: T, err and the sums then
+                // stay exactly as they were (w = 0, T (1 - 0) = T, err (1 - 0) + 0)
+                float e0, e1;
+                unpack2(mul2(pack2(ex2_approx(-h0), ex2_approx(-h1)), pack2(q3.y, q3.y)), e0, e1);
+                const f32x2 na = mul2(pack2(fminf(e0, 0.99f), fminf(e1, 0.99f)), m);  // -a
+                const f32x2 nw = mul2(na, P.T);                                       // -w
                 const f32x2 Tn = fma2(na, P.T, P.T);  // T (1 - a), rounded once
                 const float4 q4 = *reinterpret_cast<const float4 *>(&s.r);  // r g b -
-                P.cr = fma2(w, pack2(q4.x, q4.x), P.cr);
-                P.cg = fma2(w, pack2(q4.y, q4.y), P.cg);
-                P.cb = fma2(w, pack2(q4.z, q4.z), P.cb);
-                P.D = fma2(w, pack2(q3.z, q3.z), P.D);
-                P.A = add2(P.A, w);
-                // err (1 - a) + w eps + 1.25 u T' (the last term only where T changed)
-                const f32x2 ku = pack2(c0 ? kU125 : 0.0f, c1 ? kU125 : 0.0f);
-                P.err = fma2(na, P.err, fma2(w, eps2, fma2(Tn, ku, P.err)));
+                P.cr = fma2(nw, pack2(q4.x, q4.x), P.cr);
+                P.cg = fma2(nw, pack2(q4.y, q4.y), P.cg);
+                P.cb = fma2(nw, pack2(q4.z, q4.z), P.cb);
+                P.D = fma2(nw, pack2(q3.z, q3.z), P.D);
+                P.A = add2(P.A, nw);
+                // err (1 - a) + w eps + 1.25 u T' (the rounding term only where T changed)
+                P.err = fma2(na, P.err, fma2(nw, neps, fma2(Tn, mul2(m, pack2(-kU125, -kU125)), P.err)));
                 P.T = Tn;
-                P.nc0 += c0;
-                P.nc1 += c1;
+                P.nc = add2(P.nc, m);
                 if (kPixBound) {
-                    float m0, m1, s0, s1_;
-                    unpack2(P.eps_max, m0, m1);
-                    unpack2(eps2, s0, s1_);
-                    P.eps_max = pack2(c0 ? fmaxf(m0, s0) : m0, c1 ? fmaxf(m1, s1_) : m1);
-                }
-                if (kBound) {
-                    float z0, z1;
-                    unpack2(P.z_last, z0, z1);
-                    P.z_last = pack2(c0 ? fmaxf(z0, q3.z) : z0, c1 ? fmaxf(z1, q3.z) : z1);
+                    float s0, s1_, x0_, x1_;
+                    unpack2(mul2(neps, m), s0, s1_);  // eps inside the support, 0 outside
+                    unpack2(P.eps_max, x0_, x1_);
+                    P.eps_max = pack2(fmaxf(x0_, s0), fmaxf(x1_, s1_));
                 }
                 // near the cutoff (_kernels_cy.pyx:65-66): stop; decided or deferred after the walk
-                float m0, m1;
-                unpack2(sub2(Tn, P.err), m0, m1);
-                float d0, d1;
+                float g0, g1, d0, d1;
+                unpack2(sub2(Tn, P.err), g0, g1);
                 unpack2(P.dead, d0, d1);
-                P.dead = pack2(m0 <= kTHi ? kDead : d0, m1 <= kTHi ? kDead : d1);
+                P.dead = pack2(g0 <= kTHi ? kDead : d0, g1 <= kTHi ? kDead : d1);
+            }
             }
         }
         if (SOURCE == 0) {  // drop the consumed head of the queue
@@ -671,7 +675,17 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
     unpack2(P.D, DD[0], DD[1]);
     unpack2(P.eps_max, EM[0], EM[1]);
     unpack2(P.z_last, ZL[0], ZL[1]);
-    const int NC[2] = {P.nc0, P.nc1};
+    float NCf[2];
+    unpack2(P.nc, NCf[0], NCf[1]);
+    const int NC[2] = {(int)-NCf[0], (int)-NCf[1]};
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {  // the walk accumulated negated sums (exact: negation is exact)
+        A2[p] = -A2[p];
+        CR[p] = -CR[p];
+        CG[p] = -CG[p];
+        CB[p] = -CB[p];
+        DD[p] = -DD[p];
+    }
     const bool IN[2] = {in0, in1};
     const int PY[2] = {py0, py1};
     unsigned contrib_sum = 0;
