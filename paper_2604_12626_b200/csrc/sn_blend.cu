@@ -377,10 +377,10 @@ __global__ void __launch_bounds__(kBlock) tile_queue_kernel(PassView v, int el, 
 //           record slots, in depth order).
 // SOURCE 2: rasterize_reference -- every splat of the env, in depth order.
 #ifndef SN_BLEND_MIN_BLOCKS
-#define SN_BLEND_MIN_BLOCKS 5
+#define SN_BLEND_MIN_BLOCKS 6
 #endif
 #ifndef SN_LAYER_MIN_BLOCKS
-#define SN_LAYER_MIN_BLOCKS 5
+#define SN_LAYER_MIN_BLOCKS 6
 #endif
 // packed float32 pair helpers (sm_100 FMUL2 / FADD2, each half rounded like the scalar op)
 __device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {

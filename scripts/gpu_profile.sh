@@ -1,22 +1,18 @@
 #!/usr/bin/env bash
-# Run on a B200 box via gpurun: GPU parity tests, smoke, the default bench, the ncu launch list of
-# the same bench command, and one full ncu capture of the top kernels. Outputs land in gpurun_out/.
+# Run on a B200 box via gpurun: the default bench, the ncu launch list of the same bench command,
+# and one full ncu capture of the top kernels. Outputs land in gpurun_out/.
 set -u
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 B="python bench.py"
 timeout 900 $B > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
-if [ "${SKIP_NCU:-0}" = "0" ]; then
-  L="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
-  $L > gpurun_out/plain_launch.log 2>&1 && \
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
-      --log-file gpurun_out/launches.csv $L > gpurun_out/ncu_launch.log 2>&1
-  echo "launch rc=$?" >> gpurun_out/ncu_launch.log
-  C="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
-  $C > gpurun_out/plain_full.log 2>&1 && \
-  timeout 1200 ncu --set full --clock-control none --import-source on \
-      -k regex:"blend_kernel|fixup_kernel|scene_emit|scene_count" -s 12 -c 6 -o gpurun_out/prof_full $C \
-      > gpurun_out/ncu_full.log 2>&1
-  echo "full rc=$?" >> gpurun_out/ncu_full.log
-fi
+L="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
+$L > gpurun_out/plain_launch.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
+    --log-file gpurun_out/launches.csv $L > gpurun_out/ncu_launch.log 2>&1
+echo "launch rc=$?" >> gpurun_out/ncu_launch.log
+C="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
+$C > gpurun_out/plain_full.log 2>&1 && \
+timeout 1200 ncu --set full --clock-control none --import-source on \
+    -k regex:"blend_kernel|fixup_kernel|scene_emit|scene_count|avatar_count|sort_downsweep" -s ${NCU_SKIP:-40} -c ${NCU_COUNT:-8} -o gpurun_out/prof_full $C \
+    > gpurun_out/ncu_full.log 2>&1
+echo "full rc=$?" >> gpurun_out/ncu_full.log
