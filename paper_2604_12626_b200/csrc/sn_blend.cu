@@ -263,6 +263,141 @@ __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1
     return m;
 }
 
+// ---- the one-pixel-per-thread blend (256 threads per tile, 8 x 4 warp blocks), kept for the
+// avatar layer: its tile lists hold small splats that reach few pixels of a tile, where the finer
+// 8 x 4 warp blocks walk fewer entries than the two-pixel kernel's 8 x 8 blocks (measured: 2.39 vs
+// 2.55 ms per 64-env layer pass). Same numerics as blend_kernel, scalar chain.
+// Shared-memory form of a gathered splat for the float32 chain (64 B): the principal-axis rows as
+// (axis 1, axis 2) pairs, the decision thresholds k (9 -/+ E(9.1)), alpha, the alpha error bound
+// coefficients, colour and z (paired for the FFMA2 accumulation). k = log2(e) / 2: the chain
+// works on h = k d2, so alpha = o 2^-h.
+struct __align__(16) FRec1 {
+    float a1x, c2x, a1y, c2y;  // (v1, v2) = (a1x, c2x) ox + (a1y, c2y) oy + (V1, V2), h = v1^2 + v2^2,
+    float V1, V2, thr_out, thr_in;  // v_j = sqrt(k l_j) u_j
+    float ka, kb, alpha, pad;  // alpha's relative error bound: eps = ka h + kb
+    float r, g, b, z;
+};
+
+// Which of the CTA's eight 8 x 4 warp blocks the splat's support {d2 <= 9} can reach: (mx, my) is
+// the mean relative to the tile origin, (hx, hy) the support ellipse's bounding-box half-extents
+// (already widened far beyond the float rounding of the reference's d2 test), so a pixel whose
+// d2 <= 9 is never outside a set bit.
+__device__ __forceinline__ unsigned warp_block_mask_8x4(float mx, float my, float hx, float hy) {
+    const float x0 = mx - hx, x1 = mx + hx, y0 = my - hy, y1 = my + hy;
+    unsigned cols = 0, rows = 0;
+#pragma unroll
+    for (int bx = 0; bx < 2; ++bx)  // pixel centres 8 bx + 0.5 .. 8 bx + 7.5
+        cols |= (x1 >= 8 * bx + 0.5f && x0 <= 8 * bx + 7.5f) ? (1u << bx) : 0u;
+#pragma unroll
+    for (int by = 0; by < 4; ++by)  // pixel centres 4 by + 0.5 .. 4 by + 3.5
+        rows |= (y1 >= 4 * by + 0.5f && y0 <= 4 * by + 3.5f) ? (1u << by) : 0u;
+    unsigned m = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) m |= (((cols >> (w & 1)) & (rows >> (w >> 1))) & 1u) << w;
+    return m;
+}
+
+// A gathered splat's float32 blend form for this tile, from its BlendGeo (make_blend_geo): d2 in the
+// conic's principal axes relative to the tile centre (cx, cy), d2(o) = l1 (e1.o + U1)^2 +
+// l2 (e2.o + U2)^2 with U_k = e_k.(centre - mean) formed in float64, the thresholds 9 -/+ E(9.1) and
+// the alpha error coefficients, from the float error of d2 at a pixel with |o| <= 7.5 sqrt(2):
+//   |u_k error| <= u S_k, S_k = 2 |U_k| + 21.3 + 3.02 / sqrt(l_k)   (valid while d2 <= 9.1),
+//   E(d2) = 1.5 [2 u sqrt(d2) (sqrt(l1) S1 + sqrt(l2) S2) + 7 u d2] + 1e-15 (l1 / l2) 9,
+//   eps(d2) = E(d2) / 2 + kEpsExp <= ka d2 + kb   (sqrt(d2) <= (d2 + 1) / 2),
+// all evaluated in float with a 1% margin. A degenerate conic (l2 <= 0) gets thresholds that send
+// every pixel to the float64 test. Returns the 8-bit warp-block mask (warp_block_mask).
+__device__ __forceinline__ unsigned tile_entry_8x4(double e1x, double e1y, double p1, double p2, float4 gl, float4 gr,
+                                               double cx, double cy, FRec1 &f) {
+    const double U1 = fma(e1x, cx, fma(e1y, cy, -p1));
+    const double U2 = fma(-e1y, cx, fma(e1x, cy, -p2));
+    const float l1 = gl.x, l2 = gl.y;
+    const float fU1 = (float)U1, fU2 = (float)U2, fe1x = (float)e1x, fe1y = (float)e1y;
+    const float u = 5.9604644775390625e-08f;  // 2^-24
+    const float aU1 = fabsf(fU1), aU2 = fabsf(fU2);
+    bool ok = l2 > 0.0f;
+    float r1v = 0.0f, r2v = 0.0f, sig = 0.0f, kap = 0.0f, e9 = 0.0f;
+    if (ok) {
+        const float r1 = rsqrtf(l1), r2 = rsqrtf(l2);
+        r1v = r1;
+        r2v = r2;
+        const float s1 = 2.0f * aU1 + 21.3f + 3.02f * r1, s2 = 2.0f * aU2 + 21.3f + 3.02f * r2;
+        sig = (l1 * r1) * s1 + (l2 * r2) * s2;
+        kap = 9.0e-15f * fminf(l1 / l2, 1e30f);
+        e9 = 1.01f * (1.5f * (2.0f * u * 3.0166f * sig + 7.0f * u * 9.1f) + kap);
+        ok = e9 < 0.5f;
+    }
+    // mean - tile origin, from the principal-axis offsets (float error ~ 2u (|U1| + |U2|))
+    const float mx = 8.0f - (fU1 * fe1x - fU2 * fe1y), my = 8.0f - (fU1 * fe1y + fU2 * fe1x);
+    const float slack = 1e-3f + 4.0f * u * (aU1 + aU2);
+    unsigned m = warp_block_mask_8x4(mx, my, gr.z * 1.00001f + slack, gr.w * 1.00001f + slack);
+    if (ok && m) {
+        // Separating axes along the ellipse's own axes (the support's oriented bounding box,
+        // |u_k| <= 3 / sqrt(l_k), against each 8 x 4 block of pixel centres projected on e_k):
+        // rotated, elongated splats whose axis-aligned box reaches a block often miss it.
+        const float ax = fabsf(fe1x), ay = fabsf(fe1y);
+        const float marg = 1e-3f + 8.0f * u * (aU1 + aU2 + 16.0f);
+        const float ext1 = 3.0f * rsqrtf(l1) * 1.00001f + marg + (3.5f * ax + 1.5f * ay);
+        const float ext2 = 3.0f * rsqrtf(l2) * 1.00001f + marg + (3.5f * ay + 1.5f * ax);
+        // Two more axes, the diagonals of the support's normalized frame: with v_k = sqrt(l_k) u_k
+        // the support is the disc |v| <= 3 and a block is a parallelogram, which misses the disc if
+        // its projection on d = (1, +-1)/sqrt(2) stays beyond 3 -- the blocks near the corners of
+        // the oriented box, which pass the two tests above without holding a single pixel inside.
+        const float s1 = l1 * r1v, s2 = l2 * r2v;  // sqrt(l1), sqrt(l2)
+        const float hx1 = s1 * 3.5f * fe1x, hx2 = -s2 * 3.5f * fe1y;  // block half-edges in v space
+        const float hy1 = s1 * 1.5f * fe1y, hy2 = s2 * 1.5f * fe1x;
+        const float hwp = (fabsf(hx1 + hx2) + fabsf(hy1 + hy2)) * 0.70710678f;
+        const float hwm = (fabsf(hx1 - hx2) + fabsf(hy1 - hy2)) * 0.70710678f;
+        const float lim = 3.0f * 1.00001f + (s1 + s2) * marg;
+        // u_k at the block centres (8 bx - 4, 4 by - 6) relative to the tile centre
+        const float u1b = fU1 - 4.0f * fe1x - 6.0f * fe1y, u2b = fU2 + 4.0f * fe1y - 6.0f * fe1x;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            const float bx = (float)(w & 1), by = (float)(w >> 1);
+            const float u1c = u1b + 8.0f * bx * fe1x + 4.0f * by * fe1y;
+            const float u2c = u2b - 8.0f * bx * fe1y + 4.0f * by * fe1x;
+            const float v1c = s1 * u1c, v2c = s2 * u2c;
+            const float slack = lim + 1e-5f * (fabsf(v1c) + fabsf(v2c) + hwp + hwm);
+            if (fabsf(u1c) > ext1 || fabsf(u2c) > ext2 || fabsf(v1c + v2c) * 0.70710678f - hwp > slack ||
+                fabsf(v1c - v2c) * 0.70710678f - hwm > slack)
+                m &= ~(1u << w);
+        }
+    }
+    if (!m) return 0u;  // reaches none of the CTA's warp blocks: the record is never read
+    // the axes pre-scaled by sqrt(l_k log2(e) / 2) (float64 products, rounded once):
+    // h = v1^2 + v2^2 = d2 log2(e) / 2, the exp argument itself; every float error of d2 scales by
+    // the same factor, so the d2 bounds carry over with thresholds and ka scaled
+    const double sl1 = sqrt((double)l1) * kSqrtHalfLog2e, sl2 = sqrt((double)fmaxf(l2, 0.0f)) * kSqrtHalfLog2e;
+    f.a1x = (float)(sl1 * e1x);
+    f.a1y = (float)(sl1 * e1y);
+    f.V1 = (float)(sl1 * U1);
+    f.c2x = (float)(-sl2 * e1y);
+    f.c2y = (float)(sl2 * e1x);
+    f.V2 = (float)(sl2 * U2);
+    f.alpha = gl.z;
+    f.z = gl.w;
+    float rgb[3];
+    unpack_rgb21(((unsigned long long)__float_as_uint(gr.y) << 32) | __float_as_uint(gr.x), rgb);
+    f.r = rgb[0];
+    f.g = rgb[1];
+    f.b = rgb[2];
+    f.pad = 0.0f;
+    if (ok) {
+        // k (9 -/+ e9) in h units, widened by 1e-6 for the float k and the products' roundings
+        const float kf = (float)kHalfLog2e;
+        f.thr_in = __fmaf_rn(-kf, e9, kf * 9.0f) - 1.0e-6f;
+        f.thr_out = __fmaf_rn(kf, e9, kf * 9.0f) + 1.0e-6f;
+        f.ka = 1.4003f * (0.75f * u * sig + 5.25f * u);  // 1.01 / k: eps = ka d2 + kb = ka' h + kb
+        f.kb = 1.01f * (0.75f * u * sig + kEpsExp + 0.5f * kap);
+    } else {  // every pixel that is not certainly outside takes the float64 test
+        f.thr_in = -1.0f;
+        f.thr_out = 3.0e38f;
+        f.ka = 0.0f;
+        f.kb = kEpsExact;
+    }
+    return m;
+}
+
+
 // The observation payload of a finished pixel (sn_render_opts.rgb8 / depth16), from the float32
 // values the frame holds: frame_io.save_color_png's uint8 rule (frame_io.py:13-14: clip, x * 255
 // + 0.5 in float64, truncation) and fp16 depth -- the same bytes sn_quantize_frames writes, fused
@@ -768,6 +903,281 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
         const unsigned sum = __reduce_add_sync(kFull, contrib_sum);
         if (lane == 0 && sum) atomicAdd(b.contribs, (unsigned long long)sum);
     }
+#undef PROF
+}
+
+#ifndef SN_LAYER_PX1_MIN_BLOCKS
+#define SN_LAYER_PX1_MIN_BLOCKS 4
+#endif
+template <int MODE, int SOURCE>
+__global__ void __launch_bounds__(kBlock, SN_LAYER_PX1_MIN_BLOCKS) blend_kernel_px1(BlendArgs b) {
+    constexpr bool kBound = MODE != 1;  // depth error bounds feed the compositor
+    // the layer tracks each pixel's largest alpha bound (it decides the compositor's depth choice);
+    // the scene pass uses the CTA's largest bound over every gathered splat -- looser, one
+    // instruction less per contribution
+    constexpr bool kPixBound = MODE == 2;
+    // records per batch: tile lists (the avatar layer) take 2 per thread -- their warps' walks are
+    // very uneven (small splats in a few blocks), and fewer, larger batches wait less at barriers
+#ifndef SN_STREAM_PER_THREAD
+#define SN_STREAM_PER_THREAD 1
+#endif
+#ifndef SN_LIST_PER_THREAD
+#define SN_LIST_PER_THREAD 2
+#endif
+    constexpr int kPerT = SOURCE == 1 ? SN_LIST_PER_THREAD : (SOURCE == 0 ? SN_STREAM_PER_THREAD : 1);
+    constexpr int kBatch = kBlock * kPerT;
+    using WlIndex = typename std::conditional<(kBatch > 256), uint16_t, uint8_t>::type;
+    __shared__ unsigned s_epsmax;
+    __shared__ FRec1 s_f[kBatch];
+    __shared__ uint32_t s_slot[kBatch];  // record slot (the boundary band reads its SplatRec)
+    __shared__ uint32_t s_queue[SOURCE == 0 ? kBatch + kBlock : 1];
+    __shared__ uint32_t s_wsum[kBlock / 32];
+    __shared__ uint8_t s_mask[kBatch];  // bit w: the splat's support may reach warp w's 8 x 4 block
+    __shared__ WlIndex s_wl[kBlock / 32][kBatch];  // per warp: its batch entries, in depth order
+    const PassView &v = b.pv;
+    if (pass_overflow(v)) return;
+    if (threadIdx.x == 0) s_epsmax = __float_as_uint(kEpsExact);
+    const int tile = blockIdx.x, el = blockIdx.y, env = b.e0 + el;
+    const int tx = tile % b.tiles_x, ty = tile / b.tiles_x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
+    const int px_i = tx * kTile + lx;
+    const int py_i = ty * kTile + ly;
+    const bool inside = px_i < b.width && py_i < b.height;
+    const double px = px_i + 0.5, py = py_i + 0.5;
+    const double x0 = tx * kTile, y0 = ty * kTile;
+    const float oxf = (float)lx - 7.5f, oyf = (float)ly - 7.5f;  // pixel centre - tile centre
+#ifdef SN_BLEND_PROF
+    unsigned long long prof[16] = {};
+#define PROF(i, x) (prof[i] += (x))
+#else
+#define PROF(i, x) ((void)0)
+#endif
+
+    uint32_t cursor, s1;
+    if (SOURCE == 1) {
+        uint2 r = v.ranges[((uint32_t)el << v.tile_bits) | (uint32_t)tile];
+        cursor = r.x;
+        s1 = r.y;
+        // composite of an empty layer tile: front alpha 0 and depth `far`, and the scene depth is a
+        // weighted mean of z < far, so `front.depth < back.depth` never holds -- nothing to do
+        if (MODE == 2) {
+            if (threadIdx.x == 0) b.tile_flag[(int64_t)el * gridDim.x + tile] = cursor != s1;
+            if (cursor == s1) return;
+        }
+    } else {
+        cursor = (uint32_t)v.env_off[el];
+        s1 = (uint32_t)v.env_off[el + 1];
+    }
+
+    float T = 1.0f, A = 0.0f, err = 0.0f;
+    f32x2 crg = 0ull, cbd = 0ull;  // (colour r, g), (colour b, depth sum)
+    const f32x2 o2x = pack2(oxf, oxf), o2y = pack2(oyf, oyf);
+    float eps_max = 0.0f, z_first = 3.0e38f, z_last = 0.0f;
+    int nc = 0;
+    // added to d2: a finished pixel skips every splat. A pixel is finished when it is outside the
+    // frame, forced exact, or past the cutoff test (after which T and err never change, so the
+    // cutoff's ambiguity is re-derived from them after the walk)
+    float dead = (!inside || b.force_exact) ? INFINITY : 0.0f;
+    uint32_t loaded = 0, scanned = 0;
+    int q_len = 0;  // SOURCE 0: entries waiting in s_queue (uniform across the CTA)
+    while (true) {
+        if (__syncthreads_count(dead == 0.0f) == 0) break;  // also guards s_f / s_queue reuse
+        int n;
+        if (SOURCE == 0) {
+            stream_fill<kBlock>(v, tx, ty, kBatch, cursor, s1, q_len, scanned, s_queue, s_wsum);
+            n = min(q_len, kBatch);
+        } else {
+            n = (int)min((uint32_t)kBatch, s1 - cursor);
+        }
+        if (n <= 0) break;
+        loaded += n;
+#pragma unroll
+        for (int r = 0; r < kPerT; ++r) {
+            const int jt = threadIdx.x + r * kBlock;
+            if (jt >= n) break;
+            // the record slot: tile lists hold slots; streamed / all-splat sources map depth ranks
+            const uint32_t rid = SOURCE == 1 ? __ldg(v.pair_vals + cursor + jt)
+                                             : __ldg(v.order + (SOURCE == 0 ? s_queue[jt] : cursor + jt));
+            const double2 *src = reinterpret_cast<const double2 *>(v.geo + rid);
+            const double2 ge = __ldg(src), gp = __ldg(src + 1);
+            const float4 gl = __ldg(reinterpret_cast<const float4 *>(src + 2));
+            const float4 gr = __ldg(reinterpret_cast<const float4 *>(src + 3));
+            FRec1 f;
+            unsigned msk = tile_entry_8x4(ge.x, ge.y, gp.x, gp.y, gl, gr, x0 + 8.0, y0 + 8.0, f);
+            if (kBound && !kPixBound && msk)  // eps at the support edge bounds eps inside it
+                atomicMax(&s_epsmax, __float_as_uint(__fmaf_rn(f.ka, fminf(f.thr_out, 7.0f), f.kb)));
+            if (msk) s_f[jt] = f;  // an entry no warp walks is never read
+            s_slot[jt] = rid;
+            s_mask[jt] = (uint8_t)msk;
+        }
+        __syncthreads();
+        // each warp walks only the batch entries whose support can reach its 8 x 4 pixel block,
+        // in depth order; the per-pixel tests below stay exact, the mask only skips whole warps
+        int cnt = 0;
+        for (int j0 = 0; j0 < n; j0 += 32) {
+            const bool mine = j0 + lane < n && ((s_mask[j0 + lane] >> warp) & 1u);
+            const unsigned bal = __ballot_sync(kFull, mine);
+            if (mine) s_wl[warp][cnt + __popc(bal & ((1u << lane) - 1u))] = (WlIndex)(j0 + lane);
+            cnt += __popc(bal);
+        }
+        __syncwarp();
+        // a lower bound on the pixel's first contribution depth, once per batch instead of per
+        // contribution: the warp's entries arrive in depth order, so its first one is the nearest
+        if (kBound && cnt > 0) z_first = fminf(z_first, s_f[s_wl[warp][0]].z);
+        for (int k0 = 0; k0 < cnt && !__all_sync(kFull, dead != 0.0f); k0 += 32) {
+            const int k1 = min(cnt, k0 + 32);
+#pragma unroll kWalkUnroll
+            for (int k = k0; k < k1; ++k) {
+                const int j = s_wl[warp][k];
+                PROF(0, lane == 0);
+                const FRec1 &s = s_f[j];
+                const float4 q0 = *reinterpret_cast<const float4 *>(&s.a1x);
+                const float4 q1 = *reinterpret_cast<const float4 *>(&s.V1);
+                float v1, v2;
+                unpack2(fma2(pack2(q0.x, q0.y), o2x, fma2(pack2(q0.z, q0.w), o2y, pack2(q1.x, q1.y))), v1, v2);
+                // + dead: exact (v2^2 + 0 rounds like v2 * v2), or +inf for a finished pixel
+                float d2 = __fmaf_rn(v1, v1, __fmaf_rn(v2, v2, dead));
+                if (d2 > q1.z) continue;  // saturated (dead = inf), or certainly outside the support
+                const float4 q2 = *reinterpret_cast<const float4 *>(&s.ka);  // (ka, kb, alpha, -): one load
+                float eps;
+                if (d2 < q1.w) {
+                    eps = __fmaf_rn(d2, q2.x, q2.y);
+                } else {  // boundary band: the reference's float64 test (_kernels_cy.pyx:73-75)
+                    PROF(1, 1);
+                    const SplatRec &sd = v.recs[s_slot[j]];
+                    const double ddx = sd.mx - px, ddy = sd.my - py;
+                    const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
+                    if (d2d > kSupportD2) continue;
+                    d2 = (float)(d2d * kHalfLog2e);  // h, rounded once (within kEpsExact)
+                    eps = kEpsExact;
+                }
+                const float e = ex2_approx(-d2);  // 2^-h: the negation is an operand modifier
+                const float a = fminf(q2.z * e, 0.99f);
+                const float w = a * T;
+                const float Tn = __fmaf_rn(-a, T, T);  // T (1 - a), rounded once
+                const float4 q3 = *reinterpret_cast<const float4 *>(&s.r);
+                crg = fma2(pack2(q3.x, q3.y), pack2(w, w), crg);
+                cbd = fma2(pack2(q3.z, q3.w), pack2(w, w), cbd);
+                A = A + w;
+                err = __fmaf_rn(-a, err, __fmaf_rn(w, eps, __fmaf_rn(Tn, kU125, err)));  // err (1 - a) + ...
+                T = Tn;
+                ++nc;
+                if (kPixBound) eps_max = fmaxf(eps_max, eps);
+                if (kBound) z_last = fmaxf(z_last, q3.w);  // one op into a fixed register (a copy would be two)
+                // near the cutoff (_kernels_cy.pyx:65-66): stop; decided or deferred after the walk
+                if (Tn - err <= kTHi) dead = INFINITY;
+            }
+        }
+        if (SOURCE == 0) {  // drop the consumed head of the queue
+            int rest = q_len - n;
+            uint32_t qv = threadIdx.x < rest ? s_queue[n + threadIdx.x] : 0u;
+            __syncthreads();
+            if (threadIdx.x < rest) s_queue[threadIdx.x] = qv;
+            q_len = rest;
+        } else {
+            cursor += n;
+        }
+    }
+    float cr, cg, cb, D;
+    unpack2(crg, cr, cg);
+    unpack2(cbd, cb, D);
+    // the cutoff fired (T - err <= 1e-4 (1 + 1e-6)) but T < 1e-4 is not certain: float64 fixup.
+    // Also when err > T / 16: the 0.25 u T' margin in kU125 covers the bound's own float roundings
+    // (<= 2u err per step) only while err <= T / 8, and err / T never decreases along the walk.
+    const bool cut = T - err <= kTHi;
+    const bool amb = inside && (b.force_exact || (cut && (!(T + err < kTLo) || err > 0.0625f * T)));
+    PROF(2, amb);
+#ifdef SN_BLEND_PROF
+    const bool prof_live = __syncthreads_or(dead == 0.0f) != 0;
+    if (SOURCE == 0 && MODE == 0 && threadIdx.x == 0) {
+        const uint32_t st = (uint32_t)v.env_off[el], tot = s1 - st;
+        // consumed: the list position the walk had reached (queued-but-unwalked entries excluded)
+        const uint32_t used = (cursor - st) - (uint32_t)q_len;
+        const unsigned fr = tot ? (unsigned)((1000ull * used) / tot) : 0u;
+        atomicMax(&g_env_frac[el & 63], fr);
+        // log-spaced bins of the consumed fraction (1e-5 units): <=0.1%, 0.2, 0.5, 1, 2, 5, 10, 20,
+        // 50, <100%; bin 14: the list ran out with a live (unsaturated) pixel
+        const unsigned f5 = tot ? (unsigned)((100000ull * used) / tot) : 0u;
+        const unsigned edges[9] = {100, 200, 500, 1000, 2000, 5000, 10000, 20000, 50000};
+        unsigned bin = 9;
+        for (int k = 8; k >= 0; --k)
+            if (f5 <= edges[k]) bin = k;
+        if (prof_live && cursor >= s1 && q_len == 0) bin = 10;
+        atomicAdd(&g_blend_prof[4 + bin], 1ull);
+    }
+    for (int i = 0; i < 16; ++i)
+        if (prof[i]) atomicAdd(&g_blend_prof[i], prof[i]);
+#endif
+    if (b.scans && threadIdx.x == 0 && scanned) atomicAdd(b.scans, (unsigned long long)scanned);
+    if (b.loads && threadIdx.x == 0 && loaded) atomicAdd(b.loads, (unsigned long long)loaded);
+
+    const sn_camera &cam = b.cams[env];
+    const int64_t pix = ((int64_t)env * b.height + py_i) * b.width + px_i;
+    const uint32_t code = (uint32_t)(((int64_t)el * b.height + py_i) * b.width + px_i);
+    // Error bounds of the outputs the compositor decides on. Every weight w_i = a_i T_(i-1) has
+    // relative error <= rho_w (transmittance bound + largest alpha bound + the product's rounding);
+    // depth = sum z w / sum w then errs by <= rho_w (z_last - z_first) from the weights (z spans the
+    // contributions) plus (2n + 2) u from the float sums and the division; alpha by rho_w + (n + 1) u.
+    if (!kPixBound) eps_max = __uint_as_float(s_epsmax);
+    if (nc == 0) z_first = 3.0e38f;  // no contribution: the empty range, as before any batch
+    const float rho_w = err / T + eps_max + 6.0e-8f;
+    const float alpha = fminf(A, 1.0f);
+    const float depth = A > 0.0f ? D / A : (float)cam.far_;
+    const float d_err = 1.01f * (rho_w * (z_last - z_first) + (float)(2 * nc + 2) * 6.0e-8f * depth);
+    const bool flag = inside && amb;
+    if (b.contribs) {
+        unsigned sum = __reduce_add_sync(kFull, flag ? 0u : (unsigned)nc);
+        if (lane == 0 && sum) atomicAdd(b.contribs, (unsigned long long)sum);
+    }
+    push_fixup(b, flag, code);
+    if (!inside) return;
+    if (MODE == 2 && SOURCE != 1 && threadIdx.x == 0) b.tile_flag[(int64_t)el * gridDim.x + tile] = 1;
+    if (flag) {
+        if (MODE == 2) b.ldepth[pix] = __int_as_float(0x7fc00000);  // NaN: pending float64 fixup
+        return;
+    }
+    if (b.contrib) b.contrib[pix] = nc;
+    if (MODE == 0) {
+        float *oc = b.color + 3 * pix;
+        const float o0 = np_clipf(__fmaf_rn((float)cam.background[0], T, cr), 0.0f, 1.0f);
+        const float o1 = np_clipf(__fmaf_rn((float)cam.background[1], T, cg), 0.0f, 1.0f);
+        const float o2 = np_clipf(__fmaf_rn((float)cam.background[2], T, cb), 0.0f, 1.0f);
+        oc[0] = o0;
+        oc[1] = o1;
+        oc[2] = o2;
+        b.alpha[pix] = alpha;
+        b.depth[pix] = depth;
+        if (b.derr) b.derr[pix] = A > 0.0f ? d_err : 0.0f;
+        store_payload(b, pix, o0, o1, o2, depth);
+        return;
+    }
+    float fc0 = 0.0f, fc1 = 0.0f, fc2 = 0.0f;
+    if (A > 0.0f) {
+        fc0 = np_clipf(cr / A, 0.0f, 1.0f);
+        fc1 = np_clipf(cg / A, 0.0f, 1.0f);
+        fc2 = np_clipf(cb / A, 0.0f, 1.0f);
+    }
+    if (MODE == 1) {
+        float *oc = b.color + 3 * pix;
+        oc[0] = fc0;
+        oc[1] = fc1;
+        oc[2] = fc2;
+        b.alpha[pix] = alpha;
+        b.depth[pix] = depth;
+        store_payload(b, pix, fc0, fc1, fc2, depth);
+        return;
+    }
+    // MODE 2: the layer frame goes to its own buffers; composite_kernel merges it into the scene
+    // frame once the scene pass is done (so this blend runs concurrently with the scene blend)
+    float *lc = b.lcolor + 3 * pix;
+    lc[0] = fc0;
+    lc[1] = fc1;
+    lc[2] = fc2;
+    b.lalpha[pix] = alpha;
+    b.ldepth[pix] = depth;
+    b.lderr[pix] = d_err;
+    b.laerr[pix] = 1.01f * (rho_w + (float)(nc + 1) * 6.0e-8f) * A + 6.0e-8f;
 #undef PROF
 }
 
@@ -1456,13 +1866,22 @@ __global__ void blend_tile_range_kernel(int t_begin, int tiles_x, int tile_size,
 
 template <int MODE>
 static void launch_blend_mode(const BlendArgs &b, dim3 grid, cudaStream_t s) {
-    if (b.pv.source == 0)
-        blend_kernel<MODE, 0><<<grid, kBT, 0, s>>>(b);
-    else if (b.pv.source == 1)
-        blend_kernel<MODE, 1><<<grid, kBT, 0, s>>>(b);
-    else
-        blend_kernel<MODE, 2><<<grid, kBT, 0, s>>>(b);
-    if (MODE != 2) fixup_kernel<MODE><<<kFixupBlocks, 256, 0, s>>>(b);  // mode 2: after the composite
+    if constexpr (MODE == 2) {  // the avatar layer: one pixel per thread (see blend_kernel_px1)
+        if (b.pv.source == 0)
+            blend_kernel_px1<MODE, 0><<<grid, kBlock, 0, s>>>(b);
+        else if (b.pv.source == 1)
+            blend_kernel_px1<MODE, 1><<<grid, kBlock, 0, s>>>(b);
+        else
+            blend_kernel_px1<MODE, 2><<<grid, kBlock, 0, s>>>(b);
+    } else {
+        if (b.pv.source == 0)
+            blend_kernel<MODE, 0><<<grid, kBT, 0, s>>>(b);
+        else if (b.pv.source == 1)
+            blend_kernel<MODE, 1><<<grid, kBT, 0, s>>>(b);
+        else
+            blend_kernel<MODE, 2><<<grid, kBT, 0, s>>>(b);
+    }
+    if constexpr (MODE != 2) fixup_kernel<MODE><<<kFixupBlocks, 256, 0, s>>>(b);  // mode 2: after the composite
 }
 
 cudaError_t launch_tile_queue(const PassView &v, int el, int n_tiles, int tiles_x, uint32_t *counts,
