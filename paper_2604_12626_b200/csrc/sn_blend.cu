@@ -134,7 +134,7 @@ constexpr int kBW = kBT / 32;  // warps (8 x 8 pixel blocks) per tile
 // Shared-memory form of a gathered splat for the float32 chain (80 B): the principal-axis rows (a
 // pixel's v_k = row_k . o + V_k, h = v1^2 + v2^2), V1 and V2 twice (register pairs for FFMA2), the
 // decision thresholds k (9 -/+ E(9.1)), alpha's error bound coefficients NEGATED (-eps = nka h +
-// nkb, nkb twice: the walk carries negated weights, see blend_kernel), alpha, z and colour.
+// nkb, nkb twice: the walk carries negated weights, see blend_kernel), -alpha, z and colour.
 // k = log2(e) / 2: the chain works on h = k d2, so alpha = o 2^-h.
 struct __align__(16) FRec {
     float a1x, a1y, c2x, c2y;
@@ -239,7 +239,7 @@ __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1
     f.c2x = (float)(-sl2 * e1y);
     f.c2y = (float)(sl2 * e1x);
     f.V2 = f.V2b = (float)(sl2 * U2);
-    f.alpha = gl.z;
+    f.alpha = -gl.z;  // negated: the walk multiplies by -alpha (see blend_kernel)
     f.z = gl.w;
     float rgb[3];
     unpack_rgb21(((unsigned long long)__float_as_uint(gr.y) << 32) | __float_as_uint(gr.x), rgb);
@@ -517,6 +517,12 @@ __global__ void __launch_bounds__(kBlock) tile_queue_kernel(PassView v, int el, 
 #ifndef SN_LAYER_MIN_BLOCKS
 #define SN_LAYER_MIN_BLOCKS 6
 #endif
+// 1.0f when a <= b, else 0.0f (one FSET)
+__device__ __forceinline__ float le_mask(float a, float b) {
+    float r;
+    asm("set.le.f32.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
 // packed float32 pair helpers (sm_100 FMUL2 / FADD2, each half rounded like the scalar op)
 __device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
     f32x2 r;
@@ -555,7 +561,8 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
     // the layer tracks each pixel's largest alpha bound (it decides the compositor's depth choice);
     // the scene pass uses the CTA's largest bound over every gathered splat -- looser, one
     // instruction less per contribution
-    constexpr bool kPixBound = MODE == 2;
+    static_assert(MODE != 2, "the avatar layer (mode 2) runs blend_kernel_px1");
+    constexpr bool kPixBound = false;      // (mode 2's per-pixel alpha bound lives in blend_kernel_px1)
     constexpr int kPerT = 2;               // records gathered per thread per batch
     constexpr int kBatch = kBT * kPerT;    // 256 records per batch
     __shared__ unsigned s_epsmax;
@@ -677,9 +684,9 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
             unpack2(P.dead, d0, d1);
             P.z_last = pack2(d0 == 0.0f ? fmaxf(z0, zb) : z0, d1 == 0.0f ? fmaxf(z1, zb) : z1);
         }
-        // The walk carries NEGATED weights: na = -a (the inside mask m is -1 / 0), so T (1 - a) =
-        // fma(na, T, T) and err (1 - a) = fma(na, err, .) need no negation; nw = -w, and the colour,
-        // depth, A and contribution sums accumulate negated (flipped once in the epilogue).
+        // The walk carries NEGATED weights: na = -a (the record holds -alpha, the inside mask m is
+        // 1 / 0), so T (1 - a) = fma(na, T, T) and err (1 - a) = fma(na, err, .) need no negation;
+        // nw = -w, and the colour, depth and A sums accumulate negated (flipped once in the epilogue).
         for (int k0 = 0; k0 < cnt_pad; k0 += 32) {
             if (__all_sync(kFull, !(lo_of(P.dead) == 0.0f || hi_of(P.dead) == 0.0f))) break;
             const int k1 = min(cnt_pad, k0 + 32);
@@ -699,9 +706,8 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
                 f32x2 neps = fma2(h, pack2(q3.x, q3.x), pack2(q2.z, q2.w));  // -(alpha's relative bound)
                 float h0, h1;
                 unpack2(h, h0, h1);
-                // -1 where the pixel is certainly inside the support, 0 where outside or finished
-                float m0 = __int_as_float(h0 <= q2.y ? (int)0xbf800000 : 0);
-                float m1 = __int_as_float(h1 <= q2.y ? (int)0xbf800000 : 0);
+                // 1 where the pixel is certainly inside the support, 0 where outside or finished
+                float m0 = le_mask(h0, q2.y), m1 = le_mask(h1, q2.y);
                 if ((h0 > q2.y && h0 <= q2.x) || (h1 > q2.y && h1 <= q2.x)) {
                     // boundary band (rare, divergent): the reference's float64 test (_kernels_cy.pyx:73-75)
                     PROF(1, 1);
@@ -714,7 +720,7 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
                         const double ddy = sd.my - (py0 + 0.5);
                         const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
                         if (!(d2d > kSupportD2)) {
-                            m0 = -1.0f;
+                            m0 = 1.0f;
                             h0 = (float)(d2d * kHalfLog2e);  // h, rounded once (within kEpsExact)
                             e0 = -kEpsExact;
                         }
@@ -723,7 +729,7 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
                         const double ddy = sd.my - (py1 + 0.5);
                         const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
                         if (!(d2d > kSupportD2)) {
-                            m1 = -1.0f;
+                            m1 = 1.0f;
                             h1 = (float)(d2d * kHalfLog2e);
                             e1 = -kEpsExact;
                         }
@@ -734,8 +740,8 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
                 // alpha = min(o 2^-h, .99) inside the support, 0 outside: T, err and the sums then
                 // stay exactly as they were (w = 0, T (1 - 0) = T, err (1 - 0) + 0)
                 float e0, e1;
-                unpack2(mul2(pack2(ex2_approx(-h0), ex2_approx(-h1)), pack2(q3.y, q3.y)), e0, e1);
-                const f32x2 na = mul2(pack2(fminf(e0, 0.99f), fminf(e1, 0.99f)), m);  // -a
+                unpack2(mul2(pack2(ex2_approx(-h0), ex2_approx(-h1)), pack2(q3.y, q3.y)), e0, e1);  // -o 2^-h
+                const f32x2 na = mul2(pack2(fmaxf(e0, -0.99f), fmaxf(e1, -0.99f)), m);  // -a
                 const f32x2 nw = mul2(na, P.T);                                       // -w
                 const f32x2 Tn = fma2(na, P.T, P.T);  // T (1 - a), rounded once
                 const float4 q4 = *reinterpret_cast<const float4 *>(&s.r);  // r g b -
@@ -745,15 +751,9 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
                 P.D = fma2(nw, pack2(q3.z, q3.z), P.D);
                 P.A = add2(P.A, nw);
                 // err (1 - a) + w eps + 1.25 u T' (the rounding term only where T changed)
-                P.err = fma2(na, P.err, fma2(nw, neps, fma2(Tn, mul2(m, pack2(-kU125, -kU125)), P.err)));
+                P.err = fma2(na, P.err, fma2(nw, neps, fma2(Tn, mul2(m, pack2(kU125, kU125)), P.err)));
                 P.T = Tn;
                 P.nc = add2(P.nc, m);
-                if (kPixBound) {
-                    float s0, s1_, x0_, x1_;
-                    unpack2(mul2(neps, m), s0, s1_);  // eps inside the support, 0 outside
-                    unpack2(P.eps_max, x0_, x1_);
-                    P.eps_max = pack2(fmaxf(x0_, s0), fmaxf(x1_, s1_));
-                }
                 // near the cutoff (_kernels_cy.pyx:65-66): stop; decided or deferred after the walk
                 float g0, g1, d0, d1;
                 unpack2(sub2(Tn, P.err), g0, g1);
@@ -812,7 +812,7 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
     unpack2(P.z_last, ZL[0], ZL[1]);
     float NCf[2];
     unpack2(P.nc, NCf[0], NCf[1]);
-    const int NC[2] = {(int)-NCf[0], (int)-NCf[1]};
+    const int NC[2] = {(int)NCf[0], (int)NCf[1]};
 #pragma unroll
     for (int p = 0; p < 2; ++p) {  // the walk accumulated negated sums (exact: negation is exact)
         A2[p] = -A2[p];
