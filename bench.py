@@ -417,7 +417,7 @@ def main():
 
     def step(i, instrumented=False, wait=True):
         cams, times = sets[i]
-        kw = dict(stats=False, wait=wait, out=dict(frames_out[i % 2]), payload=payload)
+        kw = dict(stats=False, wait=wait, out=dict(frames_out[i % 2]), payload=payload, views=False)
         if instrumented:  # the layer pass serialized behind the scene pass: stage times add up
             kw.update(stage_ms=stage_ms, work=work, serialize=True)
         return br.render(cams, times, **kw)

@@ -163,6 +163,11 @@ typedef struct sn_render_opts {
                                frame_io.save_color_png's rule (clip, x*255+0.5 in float64, truncation)
                                on the float32 colour the frame holds */
     uint16_t *depth16;      /* device (E,H,W) or NULL: fp16 depth (round to nearest) of the same pixels */
+    int32_t views;          /* 1: keep what the harness views need beyond the render itself (each splat's
+                               gaussian id and reference tile rectangle: sn_get_sorted_ids,
+                               sn_get_tile_csr, sn_get_counts' pair count); 0: the lean throughput path
+                               (12 bytes less written per visible splat), those views then fail */
+    int32_t pad2;
 } sn_render_opts;
 
 typedef struct sn_context sn_context;

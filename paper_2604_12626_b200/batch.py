@@ -32,7 +32,7 @@ class BatchRenderer:
 
     def render(self, cameras, sim_times=None, avatar_active=None, tiled=True, contrib=False, stats=False,
                exact=False, out=None, wait=True, payload=False, serialize=False, stage_ms=None, work=None,
-               binning=-1):
+               binning=-1, views=True):
         """wait=False: queue the render and return (see render_frames); pair every such call with
         a later self.context.render_wait(). payload=True also returns the uint8 / fp16 observation
         payload (rgb8, depth16) written by the render's epilogues."""
@@ -41,7 +41,7 @@ class BatchRenderer:
         return render_frames(self.scene, cameras, self.background, avatars=self.avatars, sim_times=sim_times,
                              tiled=tiled, context=self.context, contrib=contrib, stats=stats,
                              avatar_active=avatar_active, exact=exact, out=out, wait=wait, payload=payload,
-                             serialize=serialize, stage_ms=stage_ms, work=work, binning=binning)
+                             serialize=serialize, stage_ms=stage_ms, work=work, binning=binning, views=views)
 
     def render_to_host(self, cameras, sim_times=None, host_out=None):
         """render() followed by a device->host copy into pinned buffers (the end-to-end path)."""
@@ -102,7 +102,8 @@ class HostPipeline:
                 # the render overwrites this slot's device frames once their download (two submits
                 # back) is done: a device-side wait, so the host keeps queueing ahead of the GPU
                 self.render_stream.wait_event(self.done[slot])
-            out = self.r.render(cameras, sim_times, out=dict(self.dev[slot]), wait=False, payload=self.payload)
+            out = self.r.render(cameras, sim_times, out=dict(self.dev[slot]), wait=False, payload=self.payload,
+                                views=False)
             ready = torch.cuda.Event()
             ready.record(self.render_stream)
         self.dev[slot] = {k: out[k] for k in self.dev[slot]}  # the tensors the render writes
@@ -133,7 +134,7 @@ class HostPipeline:
         self.pending = []
         for s, c, t in redo:
             with torch.cuda.stream(self.render_stream):
-                out = self.r.render(c, t, out=dict(self.dev[s]), payload=self.payload)
+                out = self.r.render(c, t, out=dict(self.dev[s]), payload=self.payload, views=False)
                 self.dev[s] = {k: out[k] for k in self.dev[s]}
                 ev = torch.cuda.Event()
                 ev.record(self.render_stream)

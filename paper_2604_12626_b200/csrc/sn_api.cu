@@ -79,7 +79,7 @@ struct PassWs {
         tiles, pair_off, pkeys_a, pkeys_b, pvals_a, pvals_b, ranges, temp, batch_rects, super_rects, fix, counts;
     uint64_t cap_v = 0, cap_p = 0;  // capacities of the per-splat / per-pair buffers
     // metadata of the last chunk rendered by this pass
-    int32_t e0 = 0, ec = 0, tiles_x = 0, tiles_y = 0, tile_bits = 0, tiled = 1, valid = 0, binning = 0;
+    int32_t e0 = 0, ec = 0, tiles_x = 0, tiles_y = 0, tile_bits = 0, tiled = 1, valid = 0, binning = 0, views = 1;
     int64_t n_vis = 0, n_pairs = 0;
     sn::BlendArgs bl{};        // the last blend's arguments (the deferred composite reuses them)
     int64_t *work = nullptr;   // mode 2: work counters still to be collected after the composite
@@ -282,8 +282,10 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     a.vals = w.vals_un.as<uint32_t>();
     a.recs = w.recs_un.as<SplatRec>();
     a.geo = w.geo_un.as<BlendGeo>();
-    a.gid = w.gid_un.as<uint32_t>();
-    a.rects = w.rects_un.as<ushort4>();
+    // the harness views' extras (gaussian id, reference rectangle per splat) only when requested
+    const int views = opts ? opts->views : 1;
+    a.gid = views ? w.gid_un.as<uint32_t>() : nullptr;
+    a.rects = views ? w.rects_un.as<ushort4>() : nullptr;
     a.rects_tight = w.rects_tun.as<ushort4>();
     a.cap = cap_v;
 
@@ -336,7 +338,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
         // 32-bit keys (env + top z bits), then an exact fix of equal-key runs
         const bool in_s = radix_sort_pairs(w.temp.p, w.keys_un.as<uint32_t>(), w.vals_un.as<uint32_t>(),
                                            w.keys_s.as<uint32_t>(), w.vals_s.as<uint32_t>(), d_nvis, cap_v,
-                                           std::min(key_bits, 32), st, &ctx->launches);
+                                           std::min(key_bits, 32), st, &ctx->launches, /*identity_values=*/true);
         SN_CUDA(cudaGetLastError());
         if (!in_s) {  // even pass count: the sorted arrays are back in the *_un buffers
             std::swap(w.keys_un, w.keys_s);
@@ -393,6 +395,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
 
     w.e0 = e0;
     w.ec = ec;
+    w.views = views;
     w.tiles_x = tiles_x;
     w.tiles_y = tiles_y;
     w.tile_bits = tile_bits;
@@ -924,6 +927,7 @@ static int pass_env(sn_context *ctx, int32_t pass, int32_t env, PassWs *&w, int 
 // rebuilt here from the device's reference rectangles and depth order.
 static int env_tile_csr(PassWs *w, int el, const std::vector<uint64_t> &off, std::vector<int64_t> &ts,
                         std::vector<int32_t> &ps) {
+    SN_CHECK(w->views, "the last render kept no harness views (sn_render_opts.views = 0)");
     const int n_tiles = w->tiles_x * w->tiles_y;
     ts.assign(n_tiles + 1, 0);
     ps.clear();
@@ -980,6 +984,7 @@ int sn_get_sorted_ids(sn_context *ctx, int32_t pass, int32_t env, int32_t *ids_h
     int r = pass_env(ctx, pass, env, w, el, off);
     if (r != SN_OK) return r;
     int64_t m = (int64_t)(off[el + 1] - off[el]);
+    SN_CHECK(w->views, "the last render kept no harness views (sn_render_opts.views = 0)");
     SN_CHECK(capacity >= m, "ids buffer too small");
     if (m) {
         std::vector<uint32_t> order((size_t)m), gid((size_t)m);

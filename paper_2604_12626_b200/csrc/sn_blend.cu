@@ -646,12 +646,9 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
             // the record slot: tile lists hold slots; streamed / all-splat sources map depth ranks
             const uint32_t rid = SOURCE == 1 ? __ldg(v.pair_vals + cursor + jt)
                                              : __ldg(v.order + (SOURCE == 0 ? s_queue[jt] : cursor + jt));
-            const double2 *src = reinterpret_cast<const double2 *>(v.geo + rid);
-            const double2 ge = __ldg(src), gp = __ldg(src + 1);
-            const float4 gl = __ldg(reinterpret_cast<const float4 *>(src + 2));
-            const float4 gr = __ldg(reinterpret_cast<const float4 *>(src + 3));
+            const GatheredSplat gs = gather_splat(v.geo, v.recs, rid);
             FRec f;
-            unsigned msk = tile_entry(ge.x, ge.y, gp.x, gp.y, gl, gr, x0 + 8.0, y0 + 8.0, f);
+            unsigned msk = tile_entry(gs.e1x, gs.e1y, gs.p1, gs.p2, gs.gl, gs.gr, x0 + 8.0, y0 + 8.0, f);
             if (kBound && !kPixBound && msk)  // eps at the support edge bounds eps inside it
                 atomicMax(&s_epsmax, __float_as_uint(-__fmaf_rn(f.nka, fminf(f.thr_out, 7.0f), f.nkb)));
             if (msk) s_f[jt] = f;  // an entry no warp walks is never read
@@ -999,12 +996,9 @@ __global__ void __launch_bounds__(kBlock, SN_LAYER_PX1_MIN_BLOCKS) blend_kernel_
             // the record slot: tile lists hold slots; streamed / all-splat sources map depth ranks
             const uint32_t rid = SOURCE == 1 ? __ldg(v.pair_vals + cursor + jt)
                                              : __ldg(v.order + (SOURCE == 0 ? s_queue[jt] : cursor + jt));
-            const double2 *src = reinterpret_cast<const double2 *>(v.geo + rid);
-            const double2 ge = __ldg(src), gp = __ldg(src + 1);
-            const float4 gl = __ldg(reinterpret_cast<const float4 *>(src + 2));
-            const float4 gr = __ldg(reinterpret_cast<const float4 *>(src + 3));
+            const GatheredSplat gs = gather_splat(v.geo, v.recs, rid);
             FRec1 f;
-            unsigned msk = tile_entry_8x4(ge.x, ge.y, gp.x, gp.y, gl, gr, x0 + 8.0, y0 + 8.0, f);
+            unsigned msk = tile_entry_8x4(gs.e1x, gs.e1y, gs.p1, gs.p2, gs.gl, gs.gr, x0 + 8.0, y0 + 8.0, f);
             if (kBound && !kPixBound && msk)  // eps at the support edge bounds eps inside it
                 atomicMax(&s_epsmax, __float_as_uint(__fmaf_rn(f.ka, fminf(f.thr_out, 7.0f), f.kb)));
             if (msk) s_f[jt] = f;  // an entry no warp walks is never read

@@ -41,22 +41,25 @@ struct __align__(16) SplatRec {
 };
 static_assert(sizeof(SplatRec) == 64, "SplatRec must stay 64 bytes");
 
-// The blend's view of a splat, written next to its SplatRec by the emit stage: the conic in its
-// principal axes (float64 major-axis direction e1 and the projections p1 = e1.mean, p2 = e2.mean,
-// e2 = (-e1y, e1x); eigenvalues l1 >= l2) so a tile only has to form e1.(centre - mean) in
-// float64, plus the support ellipse's bounding-box half-extents and the float blend inputs.
+// The blend's view of a splat, written next to its SplatRec by the emit stage (32 B): the conic's
+// principal axes -- float64 major-axis direction e1 (e2 = (-e1y, e1x)) and the eigenvalues
+// l1 >= l2 -- and the support ellipse's bounding-box half-extents. The blend reads the mean, alpha,
+// z and colour from the SplatRec itself and forms p1 = e1.mean, p2 = e2.mean (blend_geo_p), so a
+// tile only has to form e1.(centre - mean) in float64.
 struct __align__(16) BlendGeo {
     double e1x, e1y;
-    double p1, p2;
     float l1, l2;          // l2 <= 0: degenerate -- the blend tests every pixel in float64
-    float alpha, z;
-    unsigned long long rgb;
     float hx, hy;          // 3 sqrt(e1x^2 / l1 + e1y^2 / l2), 3 sqrt(e1y^2 / l1 + e1x^2 / l2)
 };
-static_assert(sizeof(BlendGeo) == 64, "BlendGeo must stay 64 bytes");
+static_assert(sizeof(BlendGeo) == 32, "BlendGeo must stay 32 bytes");
 
-__device__ __forceinline__ BlendGeo make_blend_geo(double mx, double my, double ca, double cb2, double cc,
-                                                   double alpha, double z, unsigned long long rgb) {
+// p1 = e1.mean, p2 = e2.mean, rounded as products then sum (compiled with -fmad=false)
+__device__ __forceinline__ void blend_geo_p(double e1x, double e1y, double mx, double my, double &p1, double &p2) {
+    p1 = e1x * mx + e1y * my;
+    p2 = e1x * my - e1y * mx;
+}
+
+__device__ __forceinline__ BlendGeo make_blend_geo(double ca, double cb2, double cc) {
     BlendGeo g;
     const double b = 0.5 * cb2;
     const double h = 0.5 * (ca - cc);
@@ -75,19 +78,39 @@ __device__ __forceinline__ BlendGeo make_blend_geo(double mx, double my, double 
     }
     g.e1x = vx;
     g.e1y = vy;
-    g.p1 = vx * mx + vy * my;
-    g.p2 = vx * my - vy * mx;
     const bool ok = det > 0.0 && l2 > 0.0 && l1 < 1e30;
     g.l1 = (float)l1;
     g.l2 = ok ? (float)l2 : 0.0f;
-    g.alpha = (float)alpha;
-    g.z = (float)z;
-    g.rgb = rgb;
     // support half-extents in float (IEEE ops, relative error ~1e-7): the blend widens them by 1e-5
     const float fx2 = (float)(vx * vx), fy2 = (float)(vy * vy);
     const float il1 = __frcp_rn(g.l1), il2 = __frcp_rn(g.l2);
     g.hx = ok ? 3.0f * __fsqrt_rn(__fmaf_rn(fx2, il1, fy2 * il2)) : 3.0e38f;
     g.hy = ok ? 3.0f * __fsqrt_rn(__fmaf_rn(fy2, il1, fx2 * il2)) : 3.0e38f;
+    return g;
+}
+
+// A gathered splat for the blend: (e1x, e1y, p1, p2) in float64, gl = (l1, l2, alpha, z) and
+// gr = (rgb lo bits, rgb hi bits, hx, hy) -- the inputs of the blend's tile_entry -- from the
+// splat's BlendGeo and SplatRec (4 x 16-byte read-only loads, 3 L2 sectors).
+struct GatheredSplat {
+    double e1x, e1y, p1, p2;
+    float4 gl, gr;
+};
+__device__ __forceinline__ GatheredSplat gather_splat(const BlendGeo *geo, const void *recs, uint32_t rid) {
+    GatheredSplat g;
+    const double2 e = __ldg(reinterpret_cast<const double2 *>(geo + rid));
+    const float4 lh = __ldg(reinterpret_cast<const float4 *>(geo + rid) + 1);
+    const double2 *r = reinterpret_cast<const double2 *>(static_cast<const char *>(recs) + 64 * (size_t)rid);
+    const double2 mm = __ldg(r);          // mx, my
+    const double2 ca = __ldg(r + 2);      // cc, alpha
+    const double2 zr = __ldg(r + 3);      // z, rgb bits
+    g.e1x = e.x;
+    g.e1y = e.y;
+    blend_geo_p(e.x, e.y, mm.x, mm.y, g.p1, g.p2);
+    const unsigned long long rgb = (unsigned long long)__double_as_longlong(zr.y);
+    g.gl = make_float4(lh.x, lh.y, (float)ca.y, (float)zr.x);
+    g.gr = make_float4(__uint_as_float((unsigned)(rgb & 0xffffffffull)), __uint_as_float((unsigned)(rgb >> 32)), lh.z,
+                       lh.w);
     return g;
 }
 

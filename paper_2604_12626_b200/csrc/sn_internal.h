@@ -37,12 +37,12 @@ struct PrepArgs {
     const uint64_t *env_off;  // (ec + 1)
     uint32_t *keys;            // 32-bit depth keys: top bits of (env << z_bits | z_bits - z_base)
     int32_t key_shift;         // right shift that turns the 64-bit key into the 32-bit one
-    uint32_t *vals;            // identity positions
+    uint32_t *vals;            // (unused: the depth sort's first pass generates identity values)
     SplatRec *recs;
     BlendGeo *geo;             // the blend's view of each record (same slots as recs)
     ushort4 *rects_tight;      // tiles the support ellipse's bounding box reaches (within rects)
-    uint32_t *gid;
-    ushort4 *rects;
+    uint32_t *gid;             // original gaussian id per slot, or null (harness views off)
+    ushort4 *rects;            // reference tile rectangle per slot, or null (harness views off)
     int32_t tiles_x, tiles_y;
     uint64_t z_base;
     int32_t z_bits;
@@ -106,7 +106,7 @@ cudaError_t launch_publish_counts(const uint64_t *v, const uint64_t *p, uint64_t
 // sn_sort.cu (counts in device memory, grids sized by capacity)
 size_t sort_temp_bytes(uint64_t cap);
 bool radix_sort_pairs(void *temp, uint32_t *k0, uint32_t *v0, uint32_t *k1, uint32_t *v1, const uint64_t *d_n,
-                      uint64_t cap, int bits, cudaStream_t s, int64_t *launches);
+                      uint64_t cap, int bits, cudaStream_t s, int64_t *launches, bool identity_values = false);
 size_t scan_temp_bytes_dev(uint64_t cap);
 cudaError_t scan_u32_to_u64(void *temp, const uint32_t *in, const uint64_t *d_n, uint64_t cap, uint64_t *out,
                             uint64_t *total_out, cudaStream_t s, int64_t *launches);

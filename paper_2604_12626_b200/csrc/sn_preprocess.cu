@@ -141,16 +141,18 @@ __device__ __forceinline__ void write_splat(const PrepArgs &a, int64_t pos, int 
     r.z = geo.z;
     r.rgb = pack_rgb21(rgb);
     a.recs[pos] = r;
-    const BlendGeo bg = make_blend_geo(r.mx, r.my, r.ca, r.cb2, r.cc, r.alpha, r.z, r.rgb);
+    const BlendGeo bg = make_blend_geo(r.ca, r.cb2, r.cc);
     a.geo[pos] = bg;
     unsigned long long zb = (unsigned long long)__double_as_longlong(geo.z);
     a.keys[pos] = (uint32_t)((((unsigned long long)e << a.z_bits) | (zb - a.z_base)) >> a.key_shift);
-    a.vals[pos] = (uint32_t)pos;
-    a.gid[pos] = gid;
+    // (the sort's first pass generates the identity values itself; the gaussian id and the
+    // reference rectangle are written only for the harness views, PrepArgs::gid / rects non-null)
+    if (a.gid) a.gid[pos] = gid;
     int rect[4];
     tile_rect(geo.mx, geo.my, geo.radius, a.tiles_x, a.tiles_y, rect);
-    a.rects[pos] = make_ushort4((unsigned short)rect[0], (unsigned short)rect[1], (unsigned short)rect[2],
-                                (unsigned short)rect[3]);
+    if (a.rects)
+        a.rects[pos] = make_ushort4((unsigned short)rect[0], (unsigned short)rect[1], (unsigned short)rect[2],
+                                    (unsigned short)rect[3]);
     // The tiles whose pixel centres the support {d2 <= 9} can reach: its bounding box mean +- (hx, hy)
     // (BlendGeo, float, widened far beyond its rounding), intersected with the reference rectangle
     // (3 sqrt(lambda_max) circle, renderer.py:83-86, which contains the ellipse). The reference's

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kSortThreads, SN_SORT_MIN_BLOCKS) sort_downswe
         const uint64_t i = seg + (uint64_t)r * 32 + lane;
         const bool valid = i < n;
         k[r] = valid ? __ldg(kin + i) : 0u;
-        v[r] = valid ? __ldg(vin + i) : 0u;
+        v[r] = valid ? (vin ? __ldg(vin + i) : (uint32_t)i) : 0u;  // vin null: identity values
     }
 #pragma unroll
     for (int r = 0; r < kSortRounds; ++r) {
@@ -298,11 +298,12 @@ size_t sort_temp_bytes(uint64_t cap) {
     return sizeof(uint32_t) * (256 * std::max<uint64_t>(tiles, 1) + 256);
 }
 
-// Sorts (keys, values) by the low `bits` key bits, stably; n = min(*d_n, cap). Passes alternate
+// Sorts (keys, values) by the low `bits` key bits, stably; n = min(*d_n, cap) (identity_values: the
+// values are the positions 0..n-1 and v0 is never read). Passes alternate
 // between the two buffer pairs starting with (k0, v0) -> (k1, v1); returns true when the sorted
 // result ends in (k1, v1) (odd pass count), false when it is back in (k0, v0).
 bool radix_sort_pairs(void *temp, uint32_t *k0, uint32_t *v0, uint32_t *k1, uint32_t *v1, const uint64_t *d_n,
-                      uint64_t cap, int bits, cudaStream_t s, int64_t *launches) {
+                      uint64_t cap, int bits, cudaStream_t s, int64_t *launches, bool identity_values) {
     if (cap == 0 || bits <= 0) return false;
     const int passes = (bits + 7) / 8;
     const int dbits = (bits + passes - 1) / passes;
@@ -311,11 +312,12 @@ bool radix_sort_pairs(void *temp, uint32_t *k0, uint32_t *v0, uint32_t *k1, uint
     uint32_t *totals = hist + (size_t)256 * n_tiles;
     uint32_t *ks = k0, *vs = v0, *kd = k1, *vd = v1;
     for (int p = 0; p < passes; ++p) {
+        const uint32_t *vin = (p == 0 && identity_values) ? nullptr : vs;  // pass 0: values = positions
         const int shift = p * dbits;
         const int db = std::min(dbits, bits - shift);
         sort_upsweep<<<n_tiles, kSortThreads, 0, s>>>(ks, d_n, cap, shift, db, hist, n_tiles);
         sort_rowscan<<<1 << db, kRowThreads, 0, s>>>(hist, n_tiles, totals);
-        sort_downsweep<<<n_tiles, kSortThreads, 0, s>>>(ks, vs, kd, vd, d_n, cap, shift, db, hist, totals, n_tiles);
+        sort_downsweep<<<n_tiles, kSortThreads, 0, s>>>(ks, vin, kd, vd, d_n, cap, shift, db, hist, totals, n_tiles);
         if (launches) *launches += 3;
         std::swap(ks, kd);
         std::swap(vs, vd);

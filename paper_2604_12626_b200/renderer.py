@@ -58,7 +58,7 @@ def _nonempty(c):
 
 def render_frames(scene, cameras, background, layer=None, avatars=None, sim_times=None, tiled=True,
                   context=None, contrib=False, stats=True, avatar_active=None, stage_ms=None, work=None,
-                  binning=-1, exact=False, out=None, wait=True, payload=False, serialize=False):
+                  binning=-1, exact=False, out=None, wait=True, payload=False, serialize=False, views=True):
     """One sn_render call over E cameras. Returns a dict of device tensors:
     color (E,H,W,3), alpha (E,H,W), depth (E,H,W) float32; stats (E,5) int64; optionally
     contrib_scene / contrib_layer (E,H,W) int32 and, with payload=True, the observation payload
@@ -66,7 +66,9 @@ def render_frames(scene, cameras, background, layer=None, avatars=None, sim_time
     (frame_io's uint8 rule). The context keeps the pass intermediates for the sn_get_* views.
     wait=False queues the render (sn_render_async) and returns at once: the frames are valid only
     after context.render_wait() for it returns False. serialize=True runs the avatar layer after
-    the scene pass on the same stream (per-stage timers then add up to the render)."""
+    the scene pass on the same stream (per-stage timers then add up to the render). views=False
+    is the lean throughput path: the render keeps nothing for the harness views that need each
+    splat's gaussian id or reference rectangle (pass_intermediates, tile_csr)."""
     lib = N.load()
     ctx = context or N.default_context()
     dscene = DeviceCloud.wrap(scene)
@@ -90,6 +92,7 @@ def render_frames(scene, cameras, background, layer=None, avatars=None, sim_time
     opts.binning = int(binning)
     opts.exact = 1 if exact else 0
     opts.serialize = 1 if serialize else 0
+    opts.views = 1 if views else 0
     if payload:
         opts.rgb8 = out["rgb8"].data_ptr()
         opts.depth16 = out["depth16"].data_ptr()
