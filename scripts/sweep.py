@@ -3,7 +3,8 @@ avatar count'): frames/s and per-stage ms for the scene-complexity sweep (250k..
 envs) and the avatar-count sweep (3M scene, 0..16 avatars x 50k, 1,024 envs), plus config 1 and the
 near=0.01 sensitivity row of config 2. Inputs are seeded synthetic stand-ins (synthetic.py). Each
 point: 2 untimed steps (workspace growth), then 3 timed steps with fresh cameras, CUDA events, renders
-pipelined through sn_render_async / sn_render_wait as in bench.py; stage timers from a separate pass.
+pipelined through sn_render_async / sn_render_wait as in bench.py (lean path, no harness views);
+stage timers from a separate pass with the avatar layer serialized behind the scene pass.
 Prints one JSON line per point."""
 import json
 import os
@@ -38,7 +39,7 @@ def point(config, n, a, e, near=0.1, steps=3, warm=2, seed=0):
     def run(s, wait, **kw):
         cams, times = sets[s]
         return render_frames(br.scene, cams, br.background, avatars=br.avatars, sim_times=times if a else None,
-                             context=br.context, stats=False, out=dict(outs[s % 2]), wait=wait, **kw)
+                             context=br.context, stats=False, out=dict(outs[s % 2]), wait=wait, views=False, **kw)
 
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -58,7 +59,7 @@ def point(config, n, a, e, near=0.1, steps=3, warm=2, seed=0):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     for s in range(warm, warm + steps):  # stage timers and work counters: a separate, untimed pass
-        run(s, True, stage_ms=stage, work=work)
+        run(s, True, stage_ms=stage, work=work, serialize=True)
     br.context.sync_stats()
     st = stage.reshape(2, -1) / steps
     names = list(N.STAGES)
@@ -68,15 +69,18 @@ def point(config, n, a, e, near=0.1, steps=3, warm=2, seed=0):
             "frames_per_s": e / (ms / 1e3), "ms_per_step": ms,
             "stage_ms": {"preprocess": g(0, "count", "scan", "emit"), "sort": g(0, "depth_sort", "permute"),
                          "blend": g(0, "blend"),
-                         "avatar_layer_overlapped": g(1, "pose", "count", "scan", "emit", "depth_sort", "permute",
-                                                      "pair_scan", "bin_count", "bin_scatter", "ranges", "blend"),
+                         "avatar_layer": g(1, "pose", "count", "scan", "emit", "depth_sort", "permute",
+                                           "pair_scan", "bin_count", "bin_scatter", "ranges", "blend"),
+                         "avatar_layer_preprocess": g(1, "pose", "count", "scan", "emit"),
+                         "avatar_layer_blend": g(1, "blend"),
                          "composite": g(1, "composite")},
             "visible_per_env": float(w[0, 0] / e), "contributions_per_pixel": float(w[0, 4] / (e * 640 * 480)),
             "fixup_fraction": float(w[0, 5] / (e * 640 * 480)), "render_retries": br.context.render_retries()}
 
 
 def main():
-    pts = [("config1", 1_000_000, 0, 64, 0.1), ("config2 near=0.01", 1_000_000, 4, 64, 0.01)]
+    pts = [("config1", 1_000_000, 0, 64, 0.1), ("config2", 1_000_000, 4, 64, 0.1),
+           ("config2 near=0.01", 1_000_000, 4, 64, 0.01)]
     pts += [("config3", n, 0, 256, 0.1) for n in (250_000, 1_000_000, 3_000_000, 6_000_000)]
     pts += [("config4", 3_000_000, a, 1024, 0.1) for a in (0, 1, 4, 8, 16)]
     only = sys.argv[1] if len(sys.argv) > 1 else None
