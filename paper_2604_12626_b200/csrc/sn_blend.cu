@@ -1021,33 +1021,18 @@ __global__ void __launch_bounds__(kBlock, SN_LAYER_PX1_MIN_BLOCKS) blend_kernel_
         if (kBound && cnt > 0) z_first = fminf(z_first, s_f[s_wl[warp][0]].z);
         for (int k0 = 0; k0 < cnt && !__all_sync(kFull, dead != 0.0f); k0 += 32) {
             const int k1 = min(cnt, k0 + 32);
-            // Two phases per 32 entries (the layer's splats are small: an entry reaches few of the
-            // warp's pixels): (1) each lane tests d2 <= thr_out for every entry -- a few
-            // instructions each -- and keeps a bit per candidate; (2) each lane runs the
-            // contribution chain over its own candidates only, in depth order, so the warp pays
-            // for its busiest pixel instead of for every entry some pixel needs.
-            unsigned bits = 0;
 #pragma unroll kWalkUnroll
             for (int k = k0; k < k1; ++k) {
-                const FRec1 &s = s_f[s_wl[warp][k]];
-                PROF(0, lane == 0);
-                const float4 q0 = *reinterpret_cast<const float4 *>(&s.a1x);
-                const float4 q1 = *reinterpret_cast<const float4 *>(&s.V1);
-                float v1, v2;
-                unpack2(fma2(pack2(q0.x, q0.y), o2x, fma2(pack2(q0.z, q0.w), o2y, pack2(q1.x, q1.y))), v1, v2);
-                const float d2 = __fmaf_rn(v1, v1, __fmaf_rn(v2, v2, dead));
-                bits |= (d2 <= q1.z ? 1u : 0u) << (k - k0);
-            }
-            while (bits) {
-                const int k = k0 + __ffs(bits) - 1;
-                bits &= bits - 1u;
                 const int j = s_wl[warp][k];
+                PROF(0, lane == 0);
                 const FRec1 &s = s_f[j];
                 const float4 q0 = *reinterpret_cast<const float4 *>(&s.a1x);
                 const float4 q1 = *reinterpret_cast<const float4 *>(&s.V1);
                 float v1, v2;
                 unpack2(fma2(pack2(q0.x, q0.y), o2x, fma2(pack2(q0.z, q0.w), o2y, pack2(q1.x, q1.y))), v1, v2);
-                float d2 = __fmaf_rn(v1, v1, __fmaf_rn(v2, v2, dead));  // the same value as phase 1
+                // + dead: exact (v2^2 + 0 rounds like v2 * v2), or +inf for a finished pixel
+                float d2 = __fmaf_rn(v1, v1, __fmaf_rn(v2, v2, dead));
+                if (d2 > q1.z) continue;  // saturated (dead = inf), or certainly outside the support
                 const float4 q2 = *reinterpret_cast<const float4 *>(&s.ka);  // (ka, kb, alpha, -): one load
                 float eps;
                 if (d2 < q1.w) {
@@ -1075,10 +1060,7 @@ __global__ void __launch_bounds__(kBlock, SN_LAYER_PX1_MIN_BLOCKS) blend_kernel_
                 if (kPixBound) eps_max = fmaxf(eps_max, eps);
                 if (kBound) z_last = fmaxf(z_last, q3.w);  // one op into a fixed register (a copy would be two)
                 // near the cutoff (_kernels_cy.pyx:65-66): stop; decided or deferred after the walk
-                if (Tn - err <= kTHi) {
-                    dead = INFINITY;
-                    break;
-                }
+                if (Tn - err <= kTHi) dead = INFINITY;
             }
         }
         if (SOURCE == 0) {  // drop the consumed head of the queue
