@@ -76,7 +76,8 @@ uint64_t dbits(double d) {
 
 struct PassWs {
     Buf vismask, blk_counts, env_off, keys_un, keys_s, vals_un, vals_s, recs_un, geo_un, gid_un, rects_un, rects_tun, rects,
-        tiles, pair_off, pkeys_a, pkeys_b, pvals_a, pvals_b, ranges, temp, batch_rects, super_rects, fix, counts;
+        tiles, pair_off, pkeys_a, pkeys_b, pvals_a, pvals_b, ranges, temp, batch_rects, super_rects, fix, counts, tlist,
+        tlist_cnt;
     uint64_t cap_v = 0, cap_p = 0;  // capacities of the per-splat / per-pair buffers
     // metadata of the last chunk rendered by this pass
     int32_t e0 = 0, ec = 0, tiles_x = 0, tiles_y = 0, tile_bits = 0, tiled = 1, valid = 0, binning = 0, views = 1;
@@ -207,6 +208,11 @@ PassView view_of(const PassWs &w) {
     v.d_npairs = w.counts.as<uint64_t>() + 1;
     v.cap_v = w.cap_v;
     v.cap_p = w.cap_p;
+    if (v.source == 1 && w.tlist.p && w.tlist_cnt.p) {
+        v.tile_list = w.tlist.as<uint32_t>();
+        v.n_list = w.tlist_cnt.as<uint32_t>();
+        v.list_next = w.tlist_cnt.as<uint32_t>() + 1;
+    }
     return v;
 }
 
@@ -326,6 +332,13 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     SN_ENSURE(w.ranges, sizeof(uint2) * n_ranges);
     b.ranges = w.ranges.as<uint2>();
     SN_CUDA(cudaMemsetAsync(w.ranges.p, 0, sizeof(uint2) * n_ranges, st));
+    if (binning == 1) {  // the non-empty (env, tile) list of the radix binner (listed layer blend)
+        SN_ENSURE(w.tlist, sizeof(uint32_t) * n_ranges);
+        SN_ENSURE(w.tlist_cnt, 4 * sizeof(uint32_t));
+        SN_CUDA(cudaMemsetAsync(w.tlist_cnt.p, 0, 4 * sizeof(uint32_t), st));
+        b.tile_list = w.tlist.as<uint32_t>();
+        b.n_list = w.tlist_cnt.as<uint32_t>();
+    }
     if (n > 0 && cap_v > 0) {
         tm.begin(SN_STAGE_EMIT);
         ctx->launches += 1;
@@ -448,6 +461,8 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
         SN_ENSURE(ctx->lderr, sizeof(float) * npix);
         SN_ENSURE(ctx->laerr, sizeof(float) * npix);
         SN_ENSURE(ctx->tile_flag, (size_t)ec * n_tiles);
+        // listed tiles set their flag; every other tile must read "no layer splats"
+        SN_CUDA(cudaMemsetAsync(ctx->tile_flag.p, 0, (size_t)ec * n_tiles, st));
         bl.lcolor = ctx->lcolor.as<float>();
         bl.lalpha = ctx->lalpha.as<float>();
         bl.ldepth = ctx->ldepth.as<float>();
@@ -559,7 +574,7 @@ int sn_context_destroy(sn_context *ctx) {
         for (Buf *b : {&w.vismask, &w.blk_counts, &w.env_off, &w.keys_un, &w.keys_s, &w.vals_un, &w.vals_s, &w.recs_un, &w.geo_un,
                        &w.gid_un, &w.rects_un, &w.rects_tun, &w.rects, &w.tiles, &w.pair_off, &w.pkeys_a,
                        &w.pkeys_b, &w.pvals_a, &w.pvals_b, &w.ranges, &w.temp, &w.batch_rects, &w.super_rects,
-                       &w.fix, &w.counts})
+                       &w.fix, &w.counts, &w.tlist, &w.tlist_cnt})
             free_buf(*b);
     }
     for (Buf *b : {&ctx->cams, &ctx->times, &ctx->derr, &ctx->jm, &ctx->eq, &ctx->root, &ctx->err, &ctx->pose_q,

@@ -125,7 +125,10 @@ __global__ void __launch_bounds__(kBlock) ranges_kernel(BinArgs b, const uint32_
     if (i >= n) return;
     uint2 *ranges = b.ranges;
     uint32_t k = keys[i];
-    if (i == 0 || keys[i - 1] != k) ranges[k].x = (uint32_t)i;
+    if (i == 0 || keys[i - 1] != k) {
+        ranges[k].x = (uint32_t)i;
+        if (b.tile_list) b.tile_list[atomicAdd(b.n_list, 1u)] = k;  // a non-empty (env, tile)
+    }
     if (i == n - 1 || keys[i + 1] != k) ranges[k].y = (uint32_t)(i + 1);
 }
 

@@ -933,256 +933,277 @@ __global__ void __launch_bounds__(kBlock, SN_LAYER_PX1_MIN_BLOCKS) blend_kernel_
     __shared__ WlIndex s_wl[kBlock / 32][kBatch];  // per warp: its batch entries, in depth order
     const PassView &v = b.pv;
     if (pass_overflow(v)) return;
-    if (threadIdx.x == 0) s_epsmax = __float_as_uint(kEpsExact);
-    const int tile = blockIdx.x, el = blockIdx.y, env = b.e0 + el;
-    const int tx = tile % b.tiles_x, ty = tile / b.tiles_x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
-    const int px_i = tx * kTile + lx;
-    const int py_i = ty * kTile + ly;
-    const bool inside = px_i < b.width && py_i < b.height;
-    const double px = px_i + 0.5, py = py_i + 0.5;
-    const double x0 = tx * kTile, y0 = ty * kTile;
-    const float oxf = (float)lx - 7.5f, oyf = (float)ly - 7.5f;  // pixel centre - tile centre
-#ifdef SN_BLEND_PROF
-    unsigned long long prof[16] = {};
-#define PROF(i, x) (prof[i] += (x))
-#else
-#define PROF(i, x) ((void)0)
-#endif
+    const int n_tiles_all = tiles_of(b.width) * tiles_of(b.height);
+    // one (env, tile): the whole blend of a tile, as a lambda so the listed mode below can loop
+    auto do_tile = [&](const int tile, const int el) {
+        if (threadIdx.x == 0) s_epsmax = __float_as_uint(kEpsExact);
+        const int env = b.e0 + el;
+        const int tx = tile % b.tiles_x, ty = tile / b.tiles_x;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
+        const int px_i = tx * kTile + lx;
+        const int py_i = ty * kTile + ly;
+        const bool inside = px_i < b.width && py_i < b.height;
+        const double px = px_i + 0.5, py = py_i + 0.5;
+        const double x0 = tx * kTile, y0 = ty * kTile;
+        const float oxf = (float)lx - 7.5f, oyf = (float)ly - 7.5f;  // pixel centre - tile centre
+    #ifdef SN_BLEND_PROF
+        unsigned long long prof[16] = {};
+    #define PROF(i, x) (prof[i] += (x))
+    #else
+    #define PROF(i, x) ((void)0)
+    #endif
 
-    uint32_t cursor, s1;
-    if (SOURCE == 1) {
-        uint2 r = v.ranges[((uint32_t)el << v.tile_bits) | (uint32_t)tile];
-        cursor = r.x;
-        s1 = r.y;
-        // composite of an empty layer tile: front alpha 0 and depth `far`, and the scene depth is a
-        // weighted mean of z < far, so `front.depth < back.depth` never holds -- nothing to do
-        if (MODE == 2) {
-            if (threadIdx.x == 0) b.tile_flag[(int64_t)el * gridDim.x + tile] = cursor != s1;
-            if (cursor == s1) return;
-        }
-    } else {
-        cursor = (uint32_t)v.env_off[el];
-        s1 = (uint32_t)v.env_off[el + 1];
-    }
-
-    float T = 1.0f, A = 0.0f, err = 0.0f;
-    f32x2 crg = 0ull, cbd = 0ull;  // (colour r, g), (colour b, depth sum)
-    const f32x2 o2x = pack2(oxf, oxf), o2y = pack2(oyf, oyf);
-    float eps_max = 0.0f, z_first = 3.0e38f, z_last = 0.0f;
-    int nc = 0;
-    // added to d2: a finished pixel skips every splat. A pixel is finished when it is outside the
-    // frame, forced exact, or past the cutoff test (after which T and err never change, so the
-    // cutoff's ambiguity is re-derived from them after the walk)
-    float dead = (!inside || b.force_exact) ? INFINITY : 0.0f;
-    uint32_t loaded = 0, scanned = 0;
-    int q_len = 0;  // SOURCE 0: entries waiting in s_queue (uniform across the CTA)
-    while (true) {
-        if (__syncthreads_count(dead == 0.0f) == 0) break;  // also guards s_f / s_queue reuse
-        int n;
-        if (SOURCE == 0) {
-            stream_fill<kBlock>(v, tx, ty, kBatch, cursor, s1, q_len, scanned, s_queue, s_wsum);
-            n = min(q_len, kBatch);
+        uint32_t cursor, s1;
+        if (SOURCE == 1) {
+            uint2 r = v.ranges[((uint32_t)el << v.tile_bits) | (uint32_t)tile];
+            cursor = r.x;
+            s1 = r.y;
+            // composite of an empty layer tile: front alpha 0 and depth `far`, and the scene depth is a
+            // weighted mean of z < far, so `front.depth < back.depth` never holds -- nothing to do
+            if (MODE == 2) {
+                if (threadIdx.x == 0) b.tile_flag[(int64_t)el * n_tiles_all + tile] = cursor != s1;
+                if (cursor == s1) return;
+            }
         } else {
-            n = (int)min((uint32_t)kBatch, s1 - cursor);
+            cursor = (uint32_t)v.env_off[el];
+            s1 = (uint32_t)v.env_off[el + 1];
         }
-        if (n <= 0) break;
-        loaded += n;
-#pragma unroll
-        for (int r = 0; r < kPerT; ++r) {
-            const int jt = threadIdx.x + r * kBlock;
-            if (jt >= n) break;
-            // the record slot: tile lists hold slots; streamed / all-splat sources map depth ranks
-            const uint32_t rid = SOURCE == 1 ? __ldg(v.pair_vals + cursor + jt)
-                                             : __ldg(v.order + (SOURCE == 0 ? s_queue[jt] : cursor + jt));
-            const GatheredSplat gs = gather_splat(v.geo, v.recs, rid);
-            FRec1 f;
-            unsigned msk = tile_entry_8x4(gs.e1x, gs.e1y, gs.p1, gs.p2, gs.gl, gs.gr, x0 + 8.0, y0 + 8.0, f);
-            if (kBound && !kPixBound && msk)  // eps at the support edge bounds eps inside it
-                atomicMax(&s_epsmax, __float_as_uint(__fmaf_rn(f.ka, fminf(f.thr_out, 7.0f), f.kb)));
-            if (msk) s_f[jt] = f;  // an entry no warp walks is never read
-            s_slot[jt] = rid;
-            s_mask[jt] = (uint8_t)msk;
-        }
-        __syncthreads();
-        // each warp walks only the batch entries whose support can reach its 8 x 4 pixel block,
-        // in depth order; the per-pixel tests below stay exact, the mask only skips whole warps
-        int cnt = 0;
-        for (int j0 = 0; j0 < n; j0 += 32) {
-            const bool mine = j0 + lane < n && ((s_mask[j0 + lane] >> warp) & 1u);
-            const unsigned bal = __ballot_sync(kFull, mine);
-            if (mine) s_wl[warp][cnt + __popc(bal & ((1u << lane) - 1u))] = (WlIndex)(j0 + lane);
-            cnt += __popc(bal);
-        }
-        __syncwarp();
-        // a lower bound on the pixel's first contribution depth, once per batch instead of per
-        // contribution: the warp's entries arrive in depth order, so its first one is the nearest
-        if (kBound && cnt > 0) z_first = fminf(z_first, s_f[s_wl[warp][0]].z);
-        for (int k0 = 0; k0 < cnt && !__all_sync(kFull, dead != 0.0f); k0 += 32) {
-            const int k1 = min(cnt, k0 + 32);
-#pragma unroll kWalkUnroll
-            for (int k = k0; k < k1; ++k) {
-                const int j = s_wl[warp][k];
-                PROF(0, lane == 0);
-                const FRec1 &s = s_f[j];
-                const float4 q0 = *reinterpret_cast<const float4 *>(&s.a1x);
-                const float4 q1 = *reinterpret_cast<const float4 *>(&s.V1);
-                float v1, v2;
-                unpack2(fma2(pack2(q0.x, q0.y), o2x, fma2(pack2(q0.z, q0.w), o2y, pack2(q1.x, q1.y))), v1, v2);
-                // + dead: exact (v2^2 + 0 rounds like v2 * v2), or +inf for a finished pixel
-                float d2 = __fmaf_rn(v1, v1, __fmaf_rn(v2, v2, dead));
-                if (d2 > q1.z) continue;  // saturated (dead = inf), or certainly outside the support
-                const float4 q2 = *reinterpret_cast<const float4 *>(&s.ka);  // (ka, kb, alpha, -): one load
-                float eps;
-                if (d2 < q1.w) {
-                    eps = __fmaf_rn(d2, q2.x, q2.y);
-                } else {  // boundary band: the reference's float64 test (_kernels_cy.pyx:73-75)
-                    PROF(1, 1);
-                    const SplatRec &sd = v.recs[s_slot[j]];
-                    const double ddx = sd.mx - px, ddy = sd.my - py;
-                    const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
-                    if (d2d > kSupportD2) continue;
-                    d2 = (float)(d2d * kHalfLog2e);  // h, rounded once (within kEpsExact)
-                    eps = kEpsExact;
+
+        float T = 1.0f, A = 0.0f, err = 0.0f;
+        f32x2 crg = 0ull, cbd = 0ull;  // (colour r, g), (colour b, depth sum)
+        const f32x2 o2x = pack2(oxf, oxf), o2y = pack2(oyf, oyf);
+        float eps_max = 0.0f, z_first = 3.0e38f, z_last = 0.0f;
+        int nc = 0;
+        // added to d2: a finished pixel skips every splat. A pixel is finished when it is outside the
+        // frame, forced exact, or past the cutoff test (after which T and err never change, so the
+        // cutoff's ambiguity is re-derived from them after the walk)
+        float dead = (!inside || b.force_exact) ? INFINITY : 0.0f;
+        uint32_t loaded = 0, scanned = 0;
+        int q_len = 0;  // SOURCE 0: entries waiting in s_queue (uniform across the CTA)
+        while (true) {
+            if (__syncthreads_count(dead == 0.0f) == 0) break;  // also guards s_f / s_queue reuse
+            int n;
+            if (SOURCE == 0) {
+                stream_fill<kBlock>(v, tx, ty, kBatch, cursor, s1, q_len, scanned, s_queue, s_wsum);
+                n = min(q_len, kBatch);
+            } else {
+                n = (int)min((uint32_t)kBatch, s1 - cursor);
+            }
+            if (n <= 0) break;
+            loaded += n;
+    #pragma unroll
+            for (int r = 0; r < kPerT; ++r) {
+                const int jt = threadIdx.x + r * kBlock;
+                if (jt >= n) break;
+                // the record slot: tile lists hold slots; streamed / all-splat sources map depth ranks
+                const uint32_t rid = SOURCE == 1 ? __ldg(v.pair_vals + cursor + jt)
+                                                 : __ldg(v.order + (SOURCE == 0 ? s_queue[jt] : cursor + jt));
+                const GatheredSplat gs = gather_splat(v.geo, v.recs, rid);
+                FRec1 f;
+                unsigned msk = tile_entry_8x4(gs.e1x, gs.e1y, gs.p1, gs.p2, gs.gl, gs.gr, x0 + 8.0, y0 + 8.0, f);
+                if (kBound && !kPixBound && msk)  // eps at the support edge bounds eps inside it
+                    atomicMax(&s_epsmax, __float_as_uint(__fmaf_rn(f.ka, fminf(f.thr_out, 7.0f), f.kb)));
+                if (msk) s_f[jt] = f;  // an entry no warp walks is never read
+                s_slot[jt] = rid;
+                s_mask[jt] = (uint8_t)msk;
+            }
+            __syncthreads();
+            // each warp walks only the batch entries whose support can reach its 8 x 4 pixel block,
+            // in depth order; the per-pixel tests below stay exact, the mask only skips whole warps
+            int cnt = 0;
+            for (int j0 = 0; j0 < n; j0 += 32) {
+                const bool mine = j0 + lane < n && ((s_mask[j0 + lane] >> warp) & 1u);
+                const unsigned bal = __ballot_sync(kFull, mine);
+                if (mine) s_wl[warp][cnt + __popc(bal & ((1u << lane) - 1u))] = (WlIndex)(j0 + lane);
+                cnt += __popc(bal);
+            }
+            __syncwarp();
+            // a lower bound on the pixel's first contribution depth, once per batch instead of per
+            // contribution: the warp's entries arrive in depth order, so its first one is the nearest
+            if (kBound && cnt > 0) z_first = fminf(z_first, s_f[s_wl[warp][0]].z);
+            for (int k0 = 0; k0 < cnt && !__all_sync(kFull, dead != 0.0f); k0 += 32) {
+                const int k1 = min(cnt, k0 + 32);
+    #pragma unroll kWalkUnroll
+                for (int k = k0; k < k1; ++k) {
+                    const int j = s_wl[warp][k];
+                    PROF(0, lane == 0);
+                    const FRec1 &s = s_f[j];
+                    const float4 q0 = *reinterpret_cast<const float4 *>(&s.a1x);
+                    const float4 q1 = *reinterpret_cast<const float4 *>(&s.V1);
+                    float v1, v2;
+                    unpack2(fma2(pack2(q0.x, q0.y), o2x, fma2(pack2(q0.z, q0.w), o2y, pack2(q1.x, q1.y))), v1, v2);
+                    // + dead: exact (v2^2 + 0 rounds like v2 * v2), or +inf for a finished pixel
+                    float d2 = __fmaf_rn(v1, v1, __fmaf_rn(v2, v2, dead));
+                    if (d2 > q1.z) continue;  // saturated (dead = inf), or certainly outside the support
+                    const float4 q2 = *reinterpret_cast<const float4 *>(&s.ka);  // (ka, kb, alpha, -): one load
+                    float eps;
+                    if (d2 < q1.w) {
+                        eps = __fmaf_rn(d2, q2.x, q2.y);
+                    } else {  // boundary band: the reference's float64 test (_kernels_cy.pyx:73-75)
+                        PROF(1, 1);
+                        const SplatRec &sd = v.recs[s_slot[j]];
+                        const double ddx = sd.mx - px, ddy = sd.my - py;
+                        const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
+                        if (d2d > kSupportD2) continue;
+                        d2 = (float)(d2d * kHalfLog2e);  // h, rounded once (within kEpsExact)
+                        eps = kEpsExact;
+                    }
+                    const float e = ex2_approx(-d2);  // 2^-h: the negation is an operand modifier
+                    const float a = fminf(q2.z * e, 0.99f);
+                    const float w = a * T;
+                    const float Tn = __fmaf_rn(-a, T, T);  // T (1 - a), rounded once
+                    const float4 q3 = *reinterpret_cast<const float4 *>(&s.r);
+                    crg = fma2(pack2(q3.x, q3.y), pack2(w, w), crg);
+                    cbd = fma2(pack2(q3.z, q3.w), pack2(w, w), cbd);
+                    A = A + w;
+                    err = __fmaf_rn(-a, err, __fmaf_rn(w, eps, __fmaf_rn(Tn, kU125, err)));  // err (1 - a) + ...
+                    T = Tn;
+                    ++nc;
+                    if (kPixBound) eps_max = fmaxf(eps_max, eps);
+                    if (kBound) z_last = fmaxf(z_last, q3.w);  // one op into a fixed register (a copy would be two)
+                    // near the cutoff (_kernels_cy.pyx:65-66): stop; decided or deferred after the walk
+                    if (Tn - err <= kTHi) dead = INFINITY;
                 }
-                const float e = ex2_approx(-d2);  // 2^-h: the negation is an operand modifier
-                const float a = fminf(q2.z * e, 0.99f);
-                const float w = a * T;
-                const float Tn = __fmaf_rn(-a, T, T);  // T (1 - a), rounded once
-                const float4 q3 = *reinterpret_cast<const float4 *>(&s.r);
-                crg = fma2(pack2(q3.x, q3.y), pack2(w, w), crg);
-                cbd = fma2(pack2(q3.z, q3.w), pack2(w, w), cbd);
-                A = A + w;
-                err = __fmaf_rn(-a, err, __fmaf_rn(w, eps, __fmaf_rn(Tn, kU125, err)));  // err (1 - a) + ...
-                T = Tn;
-                ++nc;
-                if (kPixBound) eps_max = fmaxf(eps_max, eps);
-                if (kBound) z_last = fmaxf(z_last, q3.w);  // one op into a fixed register (a copy would be two)
-                // near the cutoff (_kernels_cy.pyx:65-66): stop; decided or deferred after the walk
-                if (Tn - err <= kTHi) dead = INFINITY;
+            }
+            if (SOURCE == 0) {  // drop the consumed head of the queue
+                int rest = q_len - n;
+                uint32_t qv = threadIdx.x < rest ? s_queue[n + threadIdx.x] : 0u;
+                __syncthreads();
+                if (threadIdx.x < rest) s_queue[threadIdx.x] = qv;
+                q_len = rest;
+            } else {
+                cursor += n;
             }
         }
-        if (SOURCE == 0) {  // drop the consumed head of the queue
-            int rest = q_len - n;
-            uint32_t qv = threadIdx.x < rest ? s_queue[n + threadIdx.x] : 0u;
-            __syncthreads();
-            if (threadIdx.x < rest) s_queue[threadIdx.x] = qv;
-            q_len = rest;
-        } else {
-            cursor += n;
+        float cr, cg, cb, D;
+        unpack2(crg, cr, cg);
+        unpack2(cbd, cb, D);
+        // the cutoff fired (T - err <= 1e-4 (1 + 1e-6)) but T < 1e-4 is not certain: float64 fixup.
+        // Also when err > T / 16: the 0.25 u T' margin in kU125 covers the bound's own float roundings
+        // (<= 2u err per step) only while err <= T / 8, and err / T never decreases along the walk.
+        const bool cut = T - err <= kTHi;
+        const bool amb = inside && (b.force_exact || (cut && (!(T + err < kTLo) || err > 0.0625f * T)));
+        PROF(2, amb);
+    #ifdef SN_BLEND_PROF
+        const bool prof_live = __syncthreads_or(dead == 0.0f) != 0;
+        if (SOURCE == 0 && MODE == 0 && threadIdx.x == 0) {
+            const uint32_t st = (uint32_t)v.env_off[el], tot = s1 - st;
+            // consumed: the list position the walk had reached (queued-but-unwalked entries excluded)
+            const uint32_t used = (cursor - st) - (uint32_t)q_len;
+            const unsigned fr = tot ? (unsigned)((1000ull * used) / tot) : 0u;
+            atomicMax(&g_env_frac[el & 63], fr);
+            // log-spaced bins of the consumed fraction (1e-5 units): <=0.1%, 0.2, 0.5, 1, 2, 5, 10, 20,
+            // 50, <100%; bin 14: the list ran out with a live (unsaturated) pixel
+            const unsigned f5 = tot ? (unsigned)((100000ull * used) / tot) : 0u;
+            const unsigned edges[9] = {100, 200, 500, 1000, 2000, 5000, 10000, 20000, 50000};
+            unsigned bin = 9;
+            for (int k = 8; k >= 0; --k)
+                if (f5 <= edges[k]) bin = k;
+            if (prof_live && cursor >= s1 && q_len == 0) bin = 10;
+            atomicAdd(&g_blend_prof[4 + bin], 1ull);
         }
-    }
-    float cr, cg, cb, D;
-    unpack2(crg, cr, cg);
-    unpack2(cbd, cb, D);
-    // the cutoff fired (T - err <= 1e-4 (1 + 1e-6)) but T < 1e-4 is not certain: float64 fixup.
-    // Also when err > T / 16: the 0.25 u T' margin in kU125 covers the bound's own float roundings
-    // (<= 2u err per step) only while err <= T / 8, and err / T never decreases along the walk.
-    const bool cut = T - err <= kTHi;
-    const bool amb = inside && (b.force_exact || (cut && (!(T + err < kTLo) || err > 0.0625f * T)));
-    PROF(2, amb);
-#ifdef SN_BLEND_PROF
-    const bool prof_live = __syncthreads_or(dead == 0.0f) != 0;
-    if (SOURCE == 0 && MODE == 0 && threadIdx.x == 0) {
-        const uint32_t st = (uint32_t)v.env_off[el], tot = s1 - st;
-        // consumed: the list position the walk had reached (queued-but-unwalked entries excluded)
-        const uint32_t used = (cursor - st) - (uint32_t)q_len;
-        const unsigned fr = tot ? (unsigned)((1000ull * used) / tot) : 0u;
-        atomicMax(&g_env_frac[el & 63], fr);
-        // log-spaced bins of the consumed fraction (1e-5 units): <=0.1%, 0.2, 0.5, 1, 2, 5, 10, 20,
-        // 50, <100%; bin 14: the list ran out with a live (unsaturated) pixel
-        const unsigned f5 = tot ? (unsigned)((100000ull * used) / tot) : 0u;
-        const unsigned edges[9] = {100, 200, 500, 1000, 2000, 5000, 10000, 20000, 50000};
-        unsigned bin = 9;
-        for (int k = 8; k >= 0; --k)
-            if (f5 <= edges[k]) bin = k;
-        if (prof_live && cursor >= s1 && q_len == 0) bin = 10;
-        atomicAdd(&g_blend_prof[4 + bin], 1ull);
-    }
-    for (int i = 0; i < 16; ++i)
-        if (prof[i]) atomicAdd(&g_blend_prof[i], prof[i]);
-#endif
-    if (b.scans && threadIdx.x == 0 && scanned) atomicAdd(b.scans, (unsigned long long)scanned);
-    if (b.loads && threadIdx.x == 0 && loaded) atomicAdd(b.loads, (unsigned long long)loaded);
+        for (int i = 0; i < 16; ++i)
+            if (prof[i]) atomicAdd(&g_blend_prof[i], prof[i]);
+    #endif
+        if (b.scans && threadIdx.x == 0 && scanned) atomicAdd(b.scans, (unsigned long long)scanned);
+        if (b.loads && threadIdx.x == 0 && loaded) atomicAdd(b.loads, (unsigned long long)loaded);
 
-    const sn_camera &cam = b.cams[env];
-    const int64_t pix = ((int64_t)env * b.height + py_i) * b.width + px_i;
-    const uint32_t code = (uint32_t)(((int64_t)el * b.height + py_i) * b.width + px_i);
-    // Error bounds of the outputs the compositor decides on. Every weight w_i = a_i T_(i-1) has
-    // relative error <= rho_w (transmittance bound + largest alpha bound + the product's rounding);
-    // depth = sum z w / sum w then errs by <= rho_w (z_last - z_first) from the weights (z spans the
-    // contributions) plus (2n + 2) u from the float sums and the division; alpha by rho_w + (n + 1) u.
-    if (!kPixBound) eps_max = __uint_as_float(s_epsmax);
-    if (nc == 0) z_first = 3.0e38f;  // no contribution: the empty range, as before any batch
-    const float rho_w = err / T + eps_max + 6.0e-8f;
-    const float alpha = fminf(A, 1.0f);
-    const float depth = A > 0.0f ? D / A : (float)cam.far_;
-    const float d_err = 1.01f * (rho_w * (z_last - z_first) + (float)(2 * nc + 2) * 6.0e-8f * depth);
-    const bool flag = inside && amb;
-    if (b.contribs) {
-        unsigned sum = __reduce_add_sync(kFull, flag ? 0u : (unsigned)nc);
-        if (lane == 0 && sum) atomicAdd(b.contribs, (unsigned long long)sum);
-    }
-    push_fixup(b, flag, code);
-    if (!inside) return;
-    if (MODE == 2 && SOURCE != 1 && threadIdx.x == 0) b.tile_flag[(int64_t)el * gridDim.x + tile] = 1;
-    if (flag) {
-        if (MODE == 2) b.ldepth[pix] = __int_as_float(0x7fc00000);  // NaN: pending float64 fixup
-        return;
-    }
-    if (b.contrib) b.contrib[pix] = nc;
-    if (MODE == 0) {
-        float *oc = b.color + 3 * pix;
-        const float o0 = np_clipf(__fmaf_rn((float)cam.background[0], T, cr), 0.0f, 1.0f);
-        const float o1 = np_clipf(__fmaf_rn((float)cam.background[1], T, cg), 0.0f, 1.0f);
-        const float o2 = np_clipf(__fmaf_rn((float)cam.background[2], T, cb), 0.0f, 1.0f);
-        oc[0] = o0;
-        oc[1] = o1;
-        oc[2] = o2;
-        b.alpha[pix] = alpha;
-        b.depth[pix] = depth;
-        if (b.derr) b.derr[pix] = A > 0.0f ? d_err : 0.0f;
-        store_payload(b, pix, o0, o1, o2, depth);
-        return;
-    }
-    float fc0 = 0.0f, fc1 = 0.0f, fc2 = 0.0f;
-    if (A > 0.0f) {
-        fc0 = np_clipf(cr / A, 0.0f, 1.0f);
-        fc1 = np_clipf(cg / A, 0.0f, 1.0f);
-        fc2 = np_clipf(cb / A, 0.0f, 1.0f);
-    }
-    if (MODE == 1) {
-        float *oc = b.color + 3 * pix;
-        oc[0] = fc0;
-        oc[1] = fc1;
-        oc[2] = fc2;
-        b.alpha[pix] = alpha;
-        b.depth[pix] = depth;
-        store_payload(b, pix, fc0, fc1, fc2, depth);
-        return;
-    }
-    // MODE 2: the layer frame goes to its own buffers; composite_kernel merges it into the scene
-    // frame once the scene pass is done (so this blend runs concurrently with the scene blend)
-    float *lc = b.lcolor + 3 * pix;
-    lc[0] = fc0;
-    lc[1] = fc1;
-    lc[2] = fc2;
-    b.lalpha[pix] = alpha;
-    b.ldepth[pix] = depth;
-    b.lderr[pix] = d_err;
-    b.laerr[pix] = 1.01f * (rho_w + (float)(nc + 1) * 6.0e-8f) * A + 6.0e-8f;
+        const sn_camera &cam = b.cams[env];
+        const int64_t pix = ((int64_t)env * b.height + py_i) * b.width + px_i;
+        const uint32_t code = (uint32_t)(((int64_t)el * b.height + py_i) * b.width + px_i);
+        // Error bounds of the outputs the compositor decides on. Every weight w_i = a_i T_(i-1) has
+        // relative error <= rho_w (transmittance bound + largest alpha bound + the product's rounding);
+        // depth = sum z w / sum w then errs by <= rho_w (z_last - z_first) from the weights (z spans the
+        // contributions) plus (2n + 2) u from the float sums and the division; alpha by rho_w + (n + 1) u.
+        if (!kPixBound) eps_max = __uint_as_float(s_epsmax);
+        if (nc == 0) z_first = 3.0e38f;  // no contribution: the empty range, as before any batch
+        const float rho_w = err / T + eps_max + 6.0e-8f;
+        const float alpha = fminf(A, 1.0f);
+        const float depth = A > 0.0f ? D / A : (float)cam.far_;
+        const float d_err = 1.01f * (rho_w * (z_last - z_first) + (float)(2 * nc + 2) * 6.0e-8f * depth);
+        const bool flag = inside && amb;
+        if (b.contribs) {
+            unsigned sum = __reduce_add_sync(kFull, flag ? 0u : (unsigned)nc);
+            if (lane == 0 && sum) atomicAdd(b.contribs, (unsigned long long)sum);
+        }
+        push_fixup(b, flag, code);
+        if (!inside) return;
+        if (MODE == 2 && SOURCE != 1 && threadIdx.x == 0) b.tile_flag[(int64_t)el * n_tiles_all + tile] = 1;
+        if (flag) {
+            if (MODE == 2) b.ldepth[pix] = __int_as_float(0x7fc00000);  // NaN: pending float64 fixup
+            return;
+        }
+        if (b.contrib) b.contrib[pix] = nc;
+        if (MODE == 0) {
+            float *oc = b.color + 3 * pix;
+            const float o0 = np_clipf(__fmaf_rn((float)cam.background[0], T, cr), 0.0f, 1.0f);
+            const float o1 = np_clipf(__fmaf_rn((float)cam.background[1], T, cg), 0.0f, 1.0f);
+            const float o2 = np_clipf(__fmaf_rn((float)cam.background[2], T, cb), 0.0f, 1.0f);
+            oc[0] = o0;
+            oc[1] = o1;
+            oc[2] = o2;
+            b.alpha[pix] = alpha;
+            b.depth[pix] = depth;
+            if (b.derr) b.derr[pix] = A > 0.0f ? d_err : 0.0f;
+            store_payload(b, pix, o0, o1, o2, depth);
+            return;
+        }
+        float fc0 = 0.0f, fc1 = 0.0f, fc2 = 0.0f;
+        if (A > 0.0f) {
+            fc0 = np_clipf(cr / A, 0.0f, 1.0f);
+            fc1 = np_clipf(cg / A, 0.0f, 1.0f);
+            fc2 = np_clipf(cb / A, 0.0f, 1.0f);
+        }
+        if (MODE == 1) {
+            float *oc = b.color + 3 * pix;
+            oc[0] = fc0;
+            oc[1] = fc1;
+            oc[2] = fc2;
+            b.alpha[pix] = alpha;
+            b.depth[pix] = depth;
+            store_payload(b, pix, fc0, fc1, fc2, depth);
+            return;
+        }
+        // MODE 2: the layer frame goes to its own buffers; composite_kernel merges it into the scene
+        // frame once the scene pass is done (so this blend runs concurrently with the scene blend)
+        float *lc = b.lcolor + 3 * pix;
+        lc[0] = fc0;
+        lc[1] = fc1;
+        lc[2] = fc2;
+        b.lalpha[pix] = alpha;
+        b.ldepth[pix] = depth;
+        b.lderr[pix] = d_err;
+        b.laerr[pix] = 1.01f * (rho_w + (float)(nc + 1) * 6.0e-8f) * A + 6.0e-8f;
 #undef PROF
+    };
+    if (SOURCE == 1 && MODE == 2 && v.tile_list) {
+        // listed mode: only the (env, tile) pairs that hold layer splats (ranges_kernel's list), taken
+        // dynamically by a grid of a few CTAs per SM -- most of the layer's tiles are empty, and a
+        // CTA per tile would spend the pass launching and retiring them
+        __shared__ int s_item;
+        const uint32_t n_items = *v.n_list;
+        while (true) {
+            if (threadIdx.x == 0) s_item = (int)atomicAdd(v.list_next, 1u);
+            __syncthreads();
+            const int item = s_item;
+            __syncthreads();
+            if ((uint32_t)item >= n_items) break;
+            const uint32_t key = v.tile_list[item];
+            do_tile((int)(key & ((1u << v.tile_bits) - 1u)), (int)(key >> v.tile_bits));
+            __syncthreads();  // the next tile reuses the shared buffers
+        }
+    } else {
+        do_tile(blockIdx.x, blockIdx.y);
+    }
 }
 
 // composite(front = avatar layer, back = scene frame), renderer.py:151-166, for the layer frame the
 // mode-2 blend left in its buffers. Decisions (front.depth < back.depth, alpha >= 0.5) are taken
 // only when the tracked float32 error bounds separate them; other pixels join the fixup list and
 // fixup_kernel<2> recomputes both layers in float64 and composites exactly.
-__global__ void __launch_bounds__(kBlock) composite_kernel(BlendArgs b) {
-    const int tile = blockIdx.x, el = blockIdx.y, env = b.e0 + el;
-    if (pass_overflow(b.pv) || pass_overflow(b.back)) return;
-    if (!b.tile_flag[(int64_t)el * gridDim.x + tile]) return;
+__device__ __forceinline__ void composite_tile(const BlendArgs &b, const int tile, const int el) {
+    const int env = b.e0 + el;
     const int tx = tile % b.tiles_x, ty = tile / b.tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int px_i = tx * kTile + (warp & 1) * 8 + (lane & 7);
@@ -1218,6 +1239,21 @@ __global__ void __launch_bounds__(kBlock) composite_kernel(BlendArgs b) {
     b.alpha[pix] = __fmaf_rn(b.alpha[pix], 1.0f - la, la);
     if (la >= 0.5f) b.depth[pix] = ld;
     store_payload(b, pix, o0, o1, o2, la >= 0.5f ? ld : bd);
+}
+
+__global__ void __launch_bounds__(kBlock) composite_kernel(BlendArgs b) {
+    if (pass_overflow(b.pv) || pass_overflow(b.back)) return;
+    if (b.pv.source == 1 && b.pv.tile_list) {  // listed: only the tiles that hold layer splats
+        const uint32_t n_items = *b.pv.n_list;
+        for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+            const uint32_t key = b.pv.tile_list[item];
+            composite_tile(b, (int)(key & ((1u << b.pv.tile_bits) - 1u)), (int)(key >> b.pv.tile_bits));
+        }
+        return;
+    }
+    const int tile = blockIdx.x, el = blockIdx.y;
+    if (!b.tile_flag[(int64_t)el * gridDim.x + tile]) return;
+    composite_tile(b, tile, el);
 }
 
 // ---- exact (float64) per-pixel walk: the fixup path ----
@@ -1863,6 +1899,8 @@ static void launch_blend_mode(const BlendArgs &b, dim3 grid, cudaStream_t s) {
     if constexpr (MODE == 2) {  // the avatar layer: one pixel per thread (see blend_kernel_px1)
         if (b.pv.source == 0)
             blend_kernel_px1<MODE, 0><<<grid, kBlock, 0, s>>>(b);
+        else if (b.pv.source == 1 && b.pv.tile_list)  // listed: a few CTAs per SM take the non-empty tiles
+            blend_kernel_px1<MODE, 1><<<148 * SN_LAYER_PX1_MIN_BLOCKS, kBlock, 0, s>>>(b);
         else if (b.pv.source == 1)
             blend_kernel_px1<MODE, 1><<<grid, kBlock, 0, s>>>(b);
         else
@@ -1885,8 +1923,12 @@ cudaError_t launch_tile_queue(const PassView &v, int el, int n_tiles, int tiles_
 }
 
 cudaError_t launch_layer_composite(const BlendArgs &b, cudaStream_t s) {
-    dim3 grid((unsigned)(tiles_of(b.width) * tiles_of(b.height)), (unsigned)b.ec);
-    composite_kernel<<<grid, kBlock, 0, s>>>(b);
+    if (b.pv.source == 1 && b.pv.tile_list) {
+        composite_kernel<<<148 * 8, kBlock, 0, s>>>(b);
+    } else {
+        dim3 grid((unsigned)(tiles_of(b.width) * tiles_of(b.height)), (unsigned)b.ec);
+        composite_kernel<<<grid, kBlock, 0, s>>>(b);
+    }
     fixup_layer_kernel<<<kFixupBlocks, 256, 0, s>>>(b);
     return cudaGetLastError();
 }

@@ -91,6 +91,8 @@ struct BinArgs {
     uint32_t *pair_keys;
     uint32_t *pair_vals;
     uint2 *ranges;           // (ec << tile_bits)
+    uint32_t *tile_list;     // (ec << tile_bits) the (env | tile) keys that hold pairs, in any order
+    uint32_t *n_list;        // device count of tile_list (zeroed before ranges_kernel)
 };
 #ifndef SN_SUPER_BATCH
 #define SN_SUPER_BATCH 32
@@ -130,6 +132,11 @@ struct PassView {
     // composite and fixups do nothing (the host re-runs the render with larger buffers)
     const uint64_t *d_nvis, *d_npairs;
     uint64_t cap_v, cap_p;
+    // source 1: the non-empty (env | tile) keys and their count (ranges_kernel), and a work counter
+    // the listed layer blend / composite take tiles from (zeroed with the count); null = grid mode
+    const uint32_t *tile_list;
+    const uint32_t *n_list;
+    uint32_t *list_next;
 };
 __device__ __forceinline__ bool pass_overflow(const PassView &v) {
     return *v.d_nvis > v.cap_v || (v.source == 1 && *v.d_npairs > v.cap_p);
