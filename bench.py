@@ -40,7 +40,7 @@ sys.path.insert(0, REPO)
 
 METRIC = "RGB-D frames/sec (640×480) vs gaussian count & avatar count at 1/2/4/8 B200"
 STAGES = ("pose", "count", "scan", "emit", "depth_sort", "permute", "pair_scan", "bin_count", "bin_scatter", "ranges",
-          "blend", "composite")
+          "blend", "composite", "far")
 CAMERA_BYTES = 208  # sn_camera (include/splatnav_b200.h)
 TIME_BYTES = 8      # one float64 sim time per env
 # FP32-pipe floating-point operations per (pixel, splat) contribution of blend_kernel<0,0>, counted

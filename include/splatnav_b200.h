@@ -133,7 +133,8 @@ enum {
     SN_STAGE_RANGES = 9,
     SN_STAGE_BLEND = 10,
     SN_STAGE_COMPOSITE = 11,   /* layer pass: composite over the scene frame + float64 fixups */
-    SN_N_STAGES = 12
+    SN_STAGE_FAR = 12,         /* depth-sliced scene pass: far buckets, continuation, float64 fixups */
+    SN_N_STAGES = 13
 };
 
 /* Per-call options. Null pointers disable the corresponding output. */
@@ -167,7 +168,15 @@ typedef struct sn_render_opts {
                                gaussian id and reference tile rectangle: sn_get_sorted_ids,
                                sn_get_tile_csr, sn_get_counts' pair count); 0: the lean throughput path
                                (12 bytes less written per visible splat), those views then fail */
-    int32_t pad2;
+    int32_t near_slice;     /* depth slicing of the scene pass: only each env's near depth slice is
+                               sorted and streamed; the few tiles that exhaust it with unsaturated
+                               pixels continue through a per-tile bucket of the far splats, in depth
+                               order (the same frames, counts and stats). -1 auto (scenes of >= 2M
+                               gaussians rendered without harness views), 0 off, 1 on (envs with
+                               too few visible splats stay unsliced), 2..1000: on for every env with
+                               the slice at near_slice / 1000 of its sampled depths (tests, tuning);
+                               never with tiled = 0, exact = 1 or materialized scene lists. A
+                               sliced pass keeps no full depth order: the views that need it fail. */
 } sn_render_opts;
 
 typedef struct sn_context sn_context;

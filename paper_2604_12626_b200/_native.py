@@ -55,11 +55,11 @@ class SnRenderOpts(ctypes.Structure):
     _fields_ = [("tiled", ctypes.c_int32), ("binning", ctypes.c_int32), ("avatar_active", P),
                 ("contrib_scene", P), ("contrib_layer", P), ("stats", P), ("stage_ms", P), ("work", P),
                 ("exact", ctypes.c_int32), ("serialize", ctypes.c_int32), ("rgb8", P), ("depth16", P),
-                ("views", ctypes.c_int32), ("pad2", ctypes.c_int32)]
+                ("views", ctypes.c_int32), ("near_slice", ctypes.c_int32)]
 
 
 STAGES = ("pose", "count", "scan", "emit", "depth_sort", "permute", "pair_scan", "bin_count", "bin_scatter", "ranges",
-          "blend", "composite")
+          "blend", "composite", "far")
 
 
 # every symbol include/splatnav_b200.h declares (tests check the library exports all of them)

@@ -32,7 +32,7 @@ class BatchRenderer:
 
     def render(self, cameras, sim_times=None, avatar_active=None, tiled=True, contrib=False, stats=False,
                exact=False, out=None, wait=True, payload=False, serialize=False, stage_ms=None, work=None,
-               binning=-1, views=True):
+               binning=-1, views=True, near_slice=-1):
         """wait=False: queue the render and return (see render_frames); pair every such call with
         a later self.context.render_wait(). payload=True also returns the uint8 / fp16 observation
         payload (rgb8, depth16) written by the render's epilogues."""
@@ -41,7 +41,8 @@ class BatchRenderer:
         return render_frames(self.scene, cameras, self.background, avatars=self.avatars, sim_times=sim_times,
                              tiled=tiled, context=self.context, contrib=contrib, stats=stats,
                              avatar_active=avatar_active, exact=exact, out=out, wait=wait, payload=payload,
-                             serialize=serialize, stage_ms=stage_ms, work=work, binning=binning, views=views)
+                             serialize=serialize, stage_ms=stage_ms, work=work, binning=binning, views=views,
+                             near_slice=near_slice)
 
     def render_to_host(self, cameras, sim_times=None, host_out=None):
         """render() followed by a device->host copy into pinned buffers (the end-to-end path)."""

@@ -68,6 +68,19 @@ int ensure(Buf &b, size_t bytes) {
 
 int bit_length(uint64_t v) { return v == 0 ? 0 : 64 - __builtin_clzll(v); }
 
+// Depth slicing (sn_render_opts.near_slice): auto-on for scenes of at least this many gaussians
+// (rendered without harness views); the near slice is this quantile of each env's sampled depths
+// (SN_NEAR_FRAC overrides it, for tuning).
+constexpr int64_t kSliceMinGaussians = 2000000;
+double near_frac() {
+    static const double f = [] {
+        const char *e = std::getenv("SN_NEAR_FRAC");
+        const double v = e ? std::atof(e) : 0.0;
+        return v > 0.0 && v <= 1.0 ? v : 0.08;
+    }();
+    return f;
+}
+
 uint64_t dbits(double d) {
     uint64_t u;
     std::memcpy(&u, &d, 8);
@@ -78,6 +91,15 @@ struct PassWs {
     Buf vismask, blk_counts, env_off, keys_un, keys_s, vals_un, vals_s, recs_un, geo_un, gid_un, rects_un, rects_tun, rects,
         tiles, pair_off, pkeys_a, pkeys_b, pvals_a, pvals_b, ranges, temp, batch_rects, super_rects, fix, counts, tlist,
         tlist_cnt;
+    // depth slicing (scene pass): cuts, near bits, far splats, unfinished tiles and their state,
+    // far buckets (offsets, items, re-projected records, sort buffers)
+    Buf zcut, nearmask, far, fctl, unfin_list, bucket_of, state, bcount, boff, bfill, items, item_bucket, brec, bgeo,
+        bkey_a, bkey_b, bval_a, bval_b, ftemp, zk;
+    uint64_t cap_f = 0, cap_b = 0;  // far splats, bucket items
+    uint32_t cap_u = 0;             // unfinished tiles
+    int32_t sliced = 0;
+    uint32_t *far_order = nullptr;  // where the bucket sort left the final item order
+    uint32_t *far_bkeys = nullptr;  // and the matching bucket keys
     uint64_t cap_v = 0, cap_p = 0;  // capacities of the per-splat / per-pair buffers
     // metadata of the last chunk rendered by this pass
     int32_t e0 = 0, ec = 0, tiles_x = 0, tiles_y = 0, tile_bits = 0, tiled = 1, valid = 0, binning = 0, views = 1;
@@ -114,6 +136,7 @@ struct sn_context {
         bool two_pass = false;
         int64_t *work = nullptr;  // the caller's work counters (accumulated when the check passes)
         uint64_t cap_v[2] = {0, 0}, cap_p[2] = {0, 0};  // the capacities the render ran with
+        uint64_t cap_f[2] = {0, 0}, cap_u[2] = {0, 0}, cap_b[2] = {0, 0};
     } slot[2];
     int cur = 0;          // slot of the render being queued
     int64_t seq = 0;      // renders queued so far
@@ -213,6 +236,24 @@ PassView view_of(const PassWs &w) {
         v.n_list = w.tlist_cnt.as<uint32_t>();
         v.list_next = w.tlist_cnt.as<uint32_t>() + 1;
     }
+    v.ec = w.ec;
+    v.n_tiles = w.tiles_x * w.tiles_y;
+    v.sliced = w.sliced;
+    if (w.sliced) {
+        // fctl words: [0] unfinished tiles, [1] bucket items, [2] continuation work counter
+        v.far_bucket_of = w.bucket_of.as<int32_t>();
+        v.far_boff = w.boff.as<uint64_t>();
+        v.far_order = w.far_order;
+        v.far_recs = w.brec.as<SplatRec>();
+        v.far_geo = w.bgeo.as<BlendGeo>();
+        v.far_unfin_list = w.unfin_list.as<uint32_t>();
+        v.far_unfin = w.fctl.as<unsigned long long>();
+        v.far_items = w.fctl.as<uint64_t>() + 1;
+        v.far_next = reinterpret_cast<uint32_t *>(w.fctl.as<uint64_t>() + 2);
+        v.far_cap_u = w.cap_u;
+        v.cap_f = w.cap_f;
+        v.far_cap_b = w.cap_b;
+    }
     return v;
 }
 
@@ -236,11 +277,19 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     // tiles never saturate and have few pairs.
     const int req = opts ? opts->binning : -1;
     const int binning = req == 1 ? 1 : (req == 0 ? 0 : (sp.mode == 2 ? 1 : 0));
+    // depth slicing: the scene pass only (streamed rectangles, tiled, not the all-float64 mode)
+    const int views = opts ? opts->views : 1;
+    const int want_slice = opts ? opts->near_slice : -1;
+    const bool slice = sp.scene && sp.mode != 2 && tiled && binning == 0 && !(opts && opts->exact) &&
+                       (want_slice >= 1 || (want_slice < 0 && !views && n >= kSliceMinGaussians));
+    const double slice_frac = want_slice >= 2 ? std::min(1.0, want_slice / 1000.0) : near_frac();
+    const bool slice_all = want_slice >= 2;  // every env sliced, however few splats it sees
+    const int rows = slice ? 2 * ec : ec;  // per-(env, block) counts: near rows, then far rows
 
     SN_ENSURE(w.vismask, sizeof(uint64_t) * std::max<int64_t>(n, 1));
-    SN_ENSURE(w.blk_counts, sizeof(uint32_t) * (size_t)ec * n_blocks);
-    SN_ENSURE(w.env_off, sizeof(uint64_t) * (ec + 1));
-    SN_CUDA(cudaMemsetAsync(w.env_off.p, 0, sizeof(uint64_t) * (ec + 1), st));
+    SN_ENSURE(w.blk_counts, sizeof(uint32_t) * (size_t)rows * n_blocks);
+    SN_ENSURE(w.env_off, sizeof(uint64_t) * (2 * ec + 1));
+    SN_CUDA(cudaMemsetAsync(w.env_off.p, 0, sizeof(uint64_t) * (2 * ec + 1), st));
 
     PrepArgs a{};
     a.cams = ctx->cams.as<sn_camera>();
@@ -289,15 +338,29 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     a.recs = w.recs_un.as<SplatRec>();
     a.geo = w.geo_un.as<BlendGeo>();
     // the harness views' extras (gaussian id, reference rectangle per splat) only when requested
-    const int views = opts ? opts->views : 1;
     a.gid = views ? w.gid_un.as<uint32_t>() : nullptr;
     a.rects = views ? w.rects_un.as<ushort4>() : nullptr;
     a.rects_tight = w.rects_tun.as<ushort4>();
     a.cap = cap_v;
+    w.sliced = slice ? 1 : 0;
+    if (slice) {
+        if (w.cap_u == 0) w.cap_u = 2048;  // grown (with cap_f, cap_b) by render_check on overflow
+        SN_ENSURE(w.zcut, sizeof(double) * ec);
+        SN_ENSURE(w.nearmask, sizeof(uint64_t) * std::max<int64_t>(n, 1));
+        SN_ENSURE(w.far, sizeof(FarRec) * (w.cap_f + 1));
+        a.z_cut = w.zcut.as<double>();
+        a.nearmask = w.nearmask.as<uint64_t>();
+        a.far = w.far.as<FarRec>();
+        a.cap_f = w.cap_f;
+    }
 
     if (n > 0) {
         tm.begin(SN_STAGE_COUNT);
         ctx->launches += 1;
+        if (slice) {
+            ctx->launches += 1;
+            SN_CUDA(launch_near_cut(*sp.scene, a, slice_frac, slice_all, w.zcut.as<double>(), st));
+        }
         if (sp.scene)
             SN_CUDA(launch_scene_count(*sp.scene, a, st));
         else
@@ -305,7 +368,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
         tm.end();
         tm.begin(SN_STAGE_SCAN);
         ctx->launches += 2;
-        SN_CUDA(launch_block_scan(a.blk_counts, n_blocks, ec, w.env_off.as<uint64_t>(), st));
+        SN_CUDA(launch_block_scan(a.blk_counts, n_blocks, rows, w.env_off.as<uint64_t>(), st));
         tm.end();
     }
 
@@ -470,10 +533,96 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
         bl.laerr = ctx->laerr.as<float>();
         bl.tile_flag = ctx->tile_flag.as<uint8_t>();
     }
+    // the bucket sort's id width and pass parity (both slice blocks below)
+    const int ub = std::max(1, bit_length((uint64_t)w.cap_u));
+    const bool u_odd = ((ub + 7) / 8) % 2 == 1;
+    if (slice) {  // unfinished-tile registry (the blend) and the far-bucket buffers (after it)
+        const size_t cu = w.cap_u, cb = w.cap_b;
+        SN_ENSURE(w.fctl, 4 * sizeof(uint64_t));
+        SN_ENSURE(w.unfin_list, sizeof(uint32_t) * cu);
+        SN_ENSURE(w.bucket_of, sizeof(int32_t) * (size_t)ec * n_tiles);
+        SN_ENSURE(w.state, sizeof(float) * cu * kStateF * kBT);
+        SN_ENSURE(w.bcount, sizeof(uint32_t) * (cu + 1));
+        SN_ENSURE(w.boff, sizeof(uint64_t) * (cu + 1));
+        SN_ENSURE(w.bfill, sizeof(uint32_t) * (cu + 1));
+        SN_ENSURE(w.items, sizeof(uint32_t) * (cb + 1));
+        SN_ENSURE(w.item_bucket, sizeof(uint32_t) * (cb + 1));
+        SN_ENSURE(w.zk, sizeof(uint32_t) * (cb + 1));
+        SN_ENSURE(w.brec, sizeof(SplatRec) * (cb + 1));
+        SN_ENSURE(w.bgeo, sizeof(BlendGeo) * (cb + 1));
+        SN_ENSURE(w.bkey_a, sizeof(uint32_t) * (cb + 1));
+        SN_ENSURE(w.bkey_b, sizeof(uint32_t) * (cb + 1));
+        SN_ENSURE(w.bval_a, sizeof(uint32_t) * (cb + 1));
+        SN_ENSURE(w.bval_b, sizeof(uint32_t) * (cb + 1));
+        SN_ENSURE(w.ftemp, std::max({sort_temp_bytes(cb), scan_temp_bytes_dev(cu)}));
+        SN_CUDA(cudaMemsetAsync(w.fctl.p, 0, 4 * sizeof(uint64_t), st));
+        SN_CUDA(cudaMemsetAsync(w.bucket_of.p, 0xff, sizeof(int32_t) * (size_t)ec * n_tiles, st));
+        SN_CUDA(cudaMemsetAsync(w.bcount.p, 0, sizeof(uint32_t) * (cu + 1), st));
+        SN_CUDA(cudaMemsetAsync(w.bfill.p, 0, sizeof(uint32_t) * (cu + 1), st));
+        // The bucket order: a stable sort by the 32-bit z key (4 passes, ends in (bkey_a, bval_a)),
+        // then a stable sort by bucket id ((bkey_b, bval_a) -> ..., ub bits): the final values are in
+        // bval_b after an odd number of passes, bval_a after an even one.
+        w.far_order = u_odd ? w.bval_b.as<uint32_t>() : w.bval_a.as<uint32_t>();
+        w.far_bkeys = u_odd ? w.bkey_a.as<uint32_t>() : w.bkey_b.as<uint32_t>();
+        bl.pv = view_of(w);
+        bl.unfin_count = w.fctl.as<unsigned long long>();
+        bl.unfin_list = w.unfin_list.as<uint32_t>();
+        bl.bucket_of = w.bucket_of.as<int32_t>();
+        bl.state = w.state.as<float>();
+    }
     tm.begin(SN_STAGE_BLEND);
     ctx->launches += sp.mode == 2 ? 1 : 2;  // blend (+ float64 fixup; mode 2's runs after the composite)
-    SN_CUDA(launch_blend(bl, st));
+    SN_CUDA(launch_blend(bl, st, /*fixup=*/!slice));
     tm.end();
+    if (slice) {
+        // the far buckets of the unfinished tiles, the continuation, then the fixups (sn_far.cu)
+        tm.begin(SN_STAGE_FAR);
+        FarArgs f{};
+        f.e0 = e0;
+        f.ec = ec;
+        f.tiles_x = tiles_x;
+        f.n_tiles = n_tiles;
+        f.env_off = w.env_off.as<uint64_t>();
+        f.far = w.far.as<FarRec>();
+        f.cap_f = w.cap_f;
+        f.bucket_of = w.bucket_of.as<int32_t>();
+        f.bcount = w.bcount.as<uint32_t>();
+        f.boff = w.boff.as<uint64_t>();
+        f.bfill = w.bfill.as<uint32_t>();
+        f.n_items = w.fctl.as<uint64_t>() + 1;
+        f.items = w.items.as<uint32_t>();
+        f.item_bucket = w.item_bucket.as<uint32_t>();
+        f.cap_b = w.cap_b;
+        f.brec = w.brec.as<SplatRec>();
+        f.bgeo = w.bgeo.as<BlendGeo>();
+        f.zkey = w.zk.as<uint32_t>();
+        f.z_base = z_base;
+        f.z_bits = z_bits;
+        ctx->launches += 3;
+        SN_CUDA(launch_far_count(f, st));
+        SN_CUDA(scan_u32_to_u64(w.ftemp.p, w.bcount.as<uint32_t>(), w.fctl.as<uint64_t>(), w.cap_u,
+                                w.boff.as<uint64_t>(), w.fctl.as<uint64_t>() + 1, st, &ctx->launches));
+        SN_CUDA(launch_far_scatter(f, st));
+        SN_CUDA(launch_far_project(*sp.scene, ctx->cams.as<sn_camera>(), f, st));
+        const bool z_odd = radix_sort_pairs(w.ftemp.p, w.bkey_a.as<uint32_t>(), w.bval_a.as<uint32_t>(),
+                                            w.bkey_b.as<uint32_t>(), w.bval_b.as<uint32_t>(), f.n_items, w.cap_b, 32,
+                                            st, &ctx->launches, /*identity_values=*/true, w.zk.as<uint32_t>());
+        SN_CHECK(!z_odd, "far bucket sort: 32-bit keys take an even number of passes");
+        ctx->launches += 2;
+        SN_CUDA(launch_far_bucket_keys(f, w.bval_a.as<uint32_t>(), w.bkey_b.as<uint32_t>(), st));
+        const bool b_odd = radix_sort_pairs(w.ftemp.p, w.bkey_b.as<uint32_t>(), w.bval_a.as<uint32_t>(),
+                                            w.bkey_a.as<uint32_t>(), w.bval_b.as<uint32_t>(), f.n_items, w.cap_b, ub,
+                                            st, &ctx->launches);
+        SN_CHECK(b_odd == u_odd, "far bucket sort parity");
+        SN_CUDA(launch_far_tie_fix(f, w.far_bkeys, w.far_order, st));
+        BlendArgs cb2 = bl;
+        cb2.pv = view_of(w);
+        ctx->launches += 2;
+        SN_CUDA(launch_continue(cb2, st));
+        SN_CUDA(launch_fixup(cb2, st));
+        bl = cb2;
+        tm.end();
+    }
     w.bl = bl;
     w.work = nullptr;
     if (work && sp.mode == 2) {  // collected by finish_layer, after the fixups
@@ -487,8 +636,11 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     }
     // this chunk's (V, P) into mapped host memory: sn_render checks them against the capacities
     ctx->launches += 1;
-    SN_CUDA(launch_publish_counts(d_nvis, w.counts.as<uint64_t>() + 1,
-                                  ctx->slot[ctx->cur].d_counts + 2 * (2 * chunk_idx + pass_id), st));
+    SN_CUDA(launch_publish_counts(
+        d_nvis, w.counts.as<uint64_t>() + 1, slice ? w.env_off.as<uint64_t>() + ec : nullptr,
+        slice ? w.env_off.as<uint64_t>() + 2 * ec : nullptr, slice ? w.fctl.as<unsigned long long>() : nullptr,
+        slice ? w.fctl.as<uint64_t>() + 1 : nullptr,
+        ctx->slot[ctx->cur].d_counts + kCountWords * (2 * chunk_idx + pass_id), st));
     w.valid = 1;
     return SN_OK;
 }
@@ -704,11 +856,11 @@ static int render_queue(sn_context *ctx, const sn_cloud *scene, const sn_cloud *
         if (S.h_counts) cudaFreeHost(S.h_counts);
         S.h_counts = nullptr;
         S.counts_cap = 0;
-        SN_CUDA(cudaHostAlloc(&S.h_counts, sizeof(uint64_t) * 2 * 2 * n_chunks, cudaHostAllocMapped));
+        SN_CUDA(cudaHostAlloc(&S.h_counts, sizeof(uint64_t) * kCountWords * 2 * n_chunks, cudaHostAllocMapped));
         SN_CUDA(cudaHostGetDevicePointer(&S.d_counts, S.h_counts, 0));
         S.counts_cap = 2 * n_chunks;
     }
-    std::memset(S.h_counts, 0, sizeof(uint64_t) * 2 * 2 * n_chunks);
+    std::memset(S.h_counts, 0, sizeof(uint64_t) * kCountWords * 2 * n_chunks);
     S.h_err[0] = 0;
     r = render_once(ctx, scene, layer, avatars, cams, sim_times, n_envs, opts, color, alpha, depth, st, z_lo, z_bits,
                     chunk, tiled, with_layer, with_avatars);
@@ -717,6 +869,9 @@ static int render_queue(sn_context *ctx, const sn_cloud *scene, const sn_cloud *
     for (int p = 0; p < 2; ++p) {
         S.cap_v[p] = ctx->pass[p].cap_v;
         S.cap_p[p] = ctx->pass[p].cap_p;
+        S.cap_f[p] = ctx->pass[p].cap_f;
+        S.cap_u[p] = ctx->pass[p].cap_u;
+        S.cap_b[p] = ctx->pass[p].cap_b;
     }
     S.pending = true;
     S.seq = ctx->seq++;
@@ -742,13 +897,19 @@ static int render_check(sn_context *ctx, int32_t *retry) {
     SN_CHECK(S->h_err[0] == 0, "sample time must be nonnegative");
     bool grow = false;
     for (int p = 0; p < 2; ++p) {
-        uint64_t need_v = 0, need_p = 0, sum_v = 0, sum_p = 0, last_v = 0, last_p = 0;
+        uint64_t need_v = 0, need_p = 0, sum_v = 0, sum_p = 0, last_v = 0, last_p = 0, need_f = 0, need_u = 0,
+                 need_b = 0, sum_f = 0;
         for (int c = 0; c < S->n_chunks; ++c) {
-            const uint64_t v = S->h_counts[2 * (2 * c + p)], q = S->h_counts[2 * (2 * c + p) + 1];
+            const uint64_t *h = S->h_counts + kCountWords * (2 * c + p);
+            const uint64_t v = h[0], q = h[1];
             need_v = std::max(need_v, v);
             need_p = std::max(need_p, q);
+            need_f = std::max(need_f, h[2]);
+            need_u = std::max(need_u, h[3]);
+            need_b = std::max(need_b, h[4]);
             sum_v += v;
             sum_p += q;
+            sum_f += h[2];
             last_v = v;
             last_p = q;
         }
@@ -764,10 +925,24 @@ static int render_check(sn_context *ctx, int32_t *retry) {
             w.cap_p = std::max(w.cap_p, need_p + need_p / 4 + 1024);
             grow = true;
         }
+        // depth slicing: far splats, unfinished tiles (<= one per (env, tile)), far bucket items
+        if (need_f > S->cap_f[p]) {
+            w.cap_f = std::max(w.cap_f, need_f + need_f / 4 + 1024);
+            grow = true;
+        }
+        if (need_u > S->cap_u[p]) {
+            SN_CHECK(need_u < (1u << 16), "too many unfinished tiles in one env chunk (limit 65535)");
+            w.cap_u = (uint32_t)std::min<uint64_t>(65535, std::max<uint64_t>(w.cap_u, need_u + need_u / 4 + 256));
+            grow = true;
+        }
+        if (need_b > S->cap_b[p]) {
+            w.cap_b = std::max(w.cap_b, need_b + need_b / 4 + 1024);
+            grow = true;
+        }
         w.n_vis = (int64_t)last_v;
         w.n_pairs = (int64_t)last_p;
         if (!grow && S->work && (p == 0 || S->two_pass)) {
-            S->work[6 * p] += (int64_t)sum_v;
+            S->work[6 * p] += (int64_t)(sum_v + sum_f);  // near + far visible splats
             S->work[6 * p + 1] += (int64_t)sum_p;
         }
     }
@@ -928,6 +1103,8 @@ static int pass_env(sn_context *ctx, int32_t pass, int32_t env, PassWs *&w, int 
     w = &ctx->pass[pass];
     SN_CHECK(w->valid, "no render recorded for this pass");
     SN_CHECK(env >= w->e0 && env < w->e0 + w->ec, "env not in the last rendered chunk of this pass");
+    SN_CHECK(!w->sliced, "the last pass was depth-sliced (no full depth order kept): render with "
+                         "sn_render_opts.near_slice = 0 for the harness views");
     el = env - w->e0;
     off.resize(w->ec + 1);
     SN_CUDA(cudaDeviceSynchronize());

@@ -205,13 +205,21 @@ __global__ void __launch_bounds__(kBlock) tie_fix_kernel(BinArgs b) {
 
 }  // namespace
 
-__global__ void publish_counts_kernel(const uint64_t *v, const uint64_t *p, volatile uint64_t *dst) {
+// One (chunk, pass)'s sizes into mapped host memory: visible (near) splats, tile pairs and, for a
+// depth-sliced pass, far splats (f_hi - f_lo), unfinished tiles and far bucket items.
+__global__ void publish_counts_kernel(const uint64_t *v, const uint64_t *p, const uint64_t *f_lo, const uint64_t *f_hi,
+                                      const unsigned long long *u, const uint64_t *b, volatile uint64_t *dst) {
     dst[0] = *v;
     dst[1] = *p;
+    dst[2] = f_lo ? *f_hi - *f_lo : 0ull;
+    dst[3] = u ? *u : 0ull;
+    dst[4] = b ? *b : 0ull;
 }
 
-cudaError_t launch_publish_counts(const uint64_t *v, const uint64_t *p, uint64_t *mapped_dst, cudaStream_t s) {
-    publish_counts_kernel<<<1, 1, 0, s>>>(v, p, mapped_dst);
+cudaError_t launch_publish_counts(const uint64_t *v, const uint64_t *p, const uint64_t *f_lo, const uint64_t *f_hi,
+                                  const unsigned long long *u, const uint64_t *b, uint64_t *mapped_dst,
+                                  cudaStream_t s) {
+    publish_counts_kernel<<<1, 1, 0, s>>>(v, p, f_lo, f_hi, u, b, mapped_dst);
     return cudaGetLastError();
 }
 

@@ -128,8 +128,7 @@ __device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
 // float32 pairs (FFMA2 / FMUL2 / FADD2: two IEEE operations per issue slot, each rounded exactly
 // like its scalar form), so the per-splat loads, the loop and the block mask are shared by two
 // pixels and the chain costs about half the issue slots per pixel.
-constexpr int kBT = 128;
-constexpr int kBW = kBT / 32;  // warps (8 x 8 pixel blocks) per tile
+constexpr int kBW = kBT / 32;  // warps (8 x 8 pixel blocks) per tile (kBT: sn_internal.h)
 
 // Shared-memory form of a gathered splat for the float32 chain (80 B): the principal-axis rows (a
 // pixel's v_k = row_k . o + V_k, h = v1^2 + v2^2), V1 and V2 twice (register pairs for FFMA2), the
@@ -569,6 +568,7 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
     __shared__ FRec s_f[kBatch + 1];     // + a record no pixel is inside of (list padding)
     __shared__ uint32_t s_slot[kBatch];  // record slot (the boundary band reads its SplatRec)
     __shared__ uint32_t s_queue[SOURCE == 0 ? kBatch + kBlock : 1];
+    __shared__ int s_u;  // sliced pass: this tile's unfinished index (-1: none / overflow)
     __shared__ uint32_t s_wsum[kBW];
     __shared__ uint8_t s_mask[kBatch];  // bit w: the splat's support may reach warp w's 8 x 8 block
     // per warp: byte offsets of its batch entries, in depth order, padded to a multiple of the
@@ -576,331 +576,415 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
     __shared__ uint16_t s_wl[kBW][kBatch + kWalkUnroll];
     const PassView &v = b.pv;
     if (pass_overflow(v)) return;
-    if (threadIdx.x == 0) s_epsmax = __float_as_uint(kEpsExact);
-    if (threadIdx.x < 20) {  // the inert record: h = dead >= 0 > thr_in = thr_out = -1, alpha 0
-        float *d = reinterpret_cast<float *>(&s_f[kBatch]);
-        d[threadIdx.x] = (threadIdx.x == 8 || threadIdx.x == 9) ? -1.0f : 0.0f;
-    }
-    const int tile = blockIdx.x, el = blockIdx.y, env = b.e0 + el;
-    const int tx = tile % b.tiles_x, ty = tile / b.tiles_x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 8 + (lane >> 3);  // rows ly, ly + 4
-    const int px_i = tx * kTile + lx;
-    const int py0 = ty * kTile + ly, py1 = py0 + 4;
-    const bool in0 = px_i < b.width && py0 < b.height, in1 = px_i < b.width && py1 < b.height;
-    const double px = px_i + 0.5;
-    const double x0 = tx * kTile, y0 = ty * kTile;
-    const float oxf = (float)lx - 7.5f;  // pixel centre - tile centre
-    const f32x2 OX = pack2(oxf, oxf), OY = pack2((float)ly - 7.5f, (float)ly - 3.5f);
-#ifdef SN_BLEND_PROF
-    unsigned long long prof[16] = {};
-#define PROF(i, x) (prof[i] += (x))
-#else
-#define PROF(i, x) ((void)0)
-#endif
+    if (SOURCE == 3 && far_overflow(v)) return;
+    // one (env, tile); u: its unfinished index (the continuation, SOURCE 3), else -1
+    auto do_tile = [&](const int tile, const int el, const int u) {
+        if (threadIdx.x == 0) s_epsmax = __float_as_uint(kEpsExact);
+        if (threadIdx.x < 20) {  // the inert record: h = dead >= 0 > thr_in = thr_out = -1, alpha 0
+            float *d = reinterpret_cast<float *>(&s_f[kBatch]);
+            d[threadIdx.x] = (threadIdx.x == 8 || threadIdx.x == 9) ? -1.0f : 0.0f;
+        }
+        const int env = b.e0 + el;
+        const int tx = tile % b.tiles_x, ty = tile / b.tiles_x;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 8 + (lane >> 3);  // rows ly, ly + 4
+        const int px_i = tx * kTile + lx;
+        const int py0 = ty * kTile + ly, py1 = py0 + 4;
+        const bool in0 = px_i < b.width && py0 < b.height, in1 = px_i < b.width && py1 < b.height;
+        const double px = px_i + 0.5;
+        const double x0 = tx * kTile, y0 = ty * kTile;
+        const float oxf = (float)lx - 7.5f;  // pixel centre - tile centre
+        const f32x2 OX = pack2(oxf, oxf), OY = pack2((float)ly - 7.5f, (float)ly - 3.5f);
+    #ifdef SN_BLEND_PROF
+        unsigned long long prof[16] = {};
+    #define PROF(i, x) (prof[i] += (x))
+    #else
+    #define PROF(i, x) ((void)0)
+    #endif
 
-    uint32_t cursor, s1;
-    if (SOURCE == 1) {
-        uint2 r = v.ranges[((uint32_t)el << v.tile_bits) | (uint32_t)tile];
-        cursor = r.x;
-        s1 = r.y;
-        // composite of an empty layer tile: front alpha 0 and depth `far`, and the scene depth is a
-        // weighted mean of z < far, so `front.depth < back.depth` never holds -- nothing to do
-        if (MODE == 2) {
-            if (threadIdx.x == 0) b.tile_flag[(int64_t)el * gridDim.x + tile] = cursor != s1;
-            if (cursor == s1) return;
+        uint32_t cursor, s1;
+        if (SOURCE == 1) {
+            uint2 r = v.ranges[((uint32_t)el << v.tile_bits) | (uint32_t)tile];
+            cursor = r.x;
+            s1 = r.y;
+            // composite of an empty layer tile: front alpha 0 and depth `far`, and the scene depth is a
+            // weighted mean of z < far, so `front.depth < back.depth` never holds -- nothing to do
+            if (MODE == 2) {
+                if (threadIdx.x == 0) b.tile_flag[(int64_t)el * (tiles_of(b.width) * tiles_of(b.height)) + tile] = cursor != s1;
+                if (cursor == s1) return;
+            }
+        } else if (SOURCE == 3) {  // continuation of an unfinished tile: its far bucket, in depth order
+            cursor = (uint32_t)v.far_boff[u];
+            s1 = (uint32_t)v.far_boff[u + 1];
+        } else {
+            cursor = (uint32_t)v.env_off[el];
+            s1 = (uint32_t)v.env_off[el + 1];
+        }
+
+        // added to h: a finished pixel skips every splat. A pixel is finished when it is outside the
+        // frame, forced exact, or past the cutoff test (after which T and err never change, so the
+        // cutoff's ambiguity is re-derived from them after the walk). 1e30 (not inf) keeps every
+        // product of the chain finite (a finished pixel's alpha is 0 and its eps ~1e24).
+        constexpr float kDead = 1.0e30f;
+        PixPair P;
+        P.T = pack2(1.0f, 1.0f);
+        P.err = P.A = P.cr = P.cg = P.cb = P.D = P.eps_max = P.z_last = P.nc = 0ull;
+        P.dead = pack2((!in0 || b.force_exact) ? kDead : 0.0f, (!in1 || b.force_exact) ? kDead : 0.0f);
+        float z_first = 3.0e38f;
+        bool entry_live0 = true, entry_live1 = true;  // SOURCE 3: pixels still live when the tile resumed
+        if (SOURCE == 3) {  // the state the near walk saved (save_state below)
+            const float *st = b.state + (size_t)u * kStateF * kBT + threadIdx.x;
+            f32x2 *f[10] = {&P.T, &P.err, &P.A, &P.cr, &P.cg, &P.cb, &P.D, &P.dead, &P.z_last, &P.nc};
+    #pragma unroll
+            for (int q = 0; q < 10; ++q) *f[q] = pack2(st[(2 * q) * kBT], st[(2 * q + 1) * kBT]);
+            z_first = st[20 * kBT];
+            if (threadIdx.x == 0) s_epsmax = __float_as_uint(st[21 * kBT]);
+            entry_live0 = lo_of(P.dead) == 0.0f;
+            entry_live1 = hi_of(P.dead) == 0.0f;
+        }
+        uint32_t loaded = 0, scanned = 0;
+        int q_len = 0;  // SOURCE 0: entries waiting in s_queue (uniform across the CTA)
+        while (true) {
+            const bool live = lo_of(P.dead) == 0.0f || hi_of(P.dead) == 0.0f;
+            if (__syncthreads_count(live) == 0) break;  // also guards s_f / s_queue reuse
+            int n;
+            if (SOURCE == 0) {
+                stream_fill<kBT>(v, tx, ty, kBatch, cursor, s1, q_len, scanned, s_queue, s_wsum);
+                n = min(q_len, kBatch);
+            } else {
+                n = (int)min((uint32_t)kBatch, s1 - cursor);
+            }
+            if (n <= 0) break;
+            loaded += n;
+    #pragma unroll
+            for (int r = 0; r < kPerT; ++r) {
+                const int jt = threadIdx.x + r * kBT;
+                if (jt >= n) break;
+                // the record slot: tile lists hold slots; streamed / all-splat sources map depth ranks
+                const uint32_t rid = SOURCE == 1   ? __ldg(v.pair_vals + cursor + jt)
+                                     : SOURCE == 3 ? __ldg(v.far_order + cursor + jt)
+                                                   : __ldg(v.order + (SOURCE == 0 ? s_queue[jt] : cursor + jt));
+                const GatheredSplat gs = SOURCE == 3 ? gather_splat(v.far_geo, v.far_recs, rid) : gather_splat(v.geo, v.recs, rid);
+                FRec f;
+                unsigned msk = tile_entry(gs.e1x, gs.e1y, gs.p1, gs.p2, gs.gl, gs.gr, x0 + 8.0, y0 + 8.0, f);
+                if (kBound && !kPixBound && msk)  // eps at the support edge bounds eps inside it
+                    atomicMax(&s_epsmax, __float_as_uint(-__fmaf_rn(f.nka, fminf(f.thr_out, 7.0f), f.nkb)));
+                if (msk) s_f[jt] = f;  // an entry no warp walks is never read
+                s_slot[jt] = rid;
+                s_mask[jt] = (uint8_t)msk;
+            }
+            __syncthreads();
+            // each warp walks only the batch entries whose support can reach its 8 x 8 pixel block,
+            // in depth order; the per-pixel tests below stay exact, the mask only skips whole warps
+            int cnt = 0;
+            for (int j0 = 0; j0 < n; j0 += 32) {
+                const bool mine = j0 + lane < n && ((s_mask[j0 + lane] >> warp) & 1u);
+                const unsigned bal = __ballot_sync(kFull, mine);
+                if (mine) s_wl[warp][cnt + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)((j0 + lane) * sizeof(FRec));
+                cnt += __popc(bal);
+            }
+            const int cnt_pad = (cnt + kWalkUnroll - 1) / kWalkUnroll * kWalkUnroll;
+            if (lane < cnt_pad - cnt) s_wl[warp][cnt + lane] = (uint16_t)(kBatch * sizeof(FRec));
+            __syncwarp();
+            // depth bounds of the contributions, once per batch instead of per contribution: the warp's
+            // entries arrive in depth order, so its first one is a lower bound of every pixel's first
+            // contribution, and its last one an upper bound of any contribution a pixel still live at
+            // the batch's start makes in it
+            const char *fbase = reinterpret_cast<const char *>(s_f);
+            if (kBound && cnt > 0) {
+                z_first = fminf(z_first, reinterpret_cast<const FRec *>(fbase + s_wl[warp][0])->z);
+                const float zb = reinterpret_cast<const FRec *>(fbase + s_wl[warp][cnt - 1])->z;
+                float z0, z1, d0, d1;
+                unpack2(P.z_last, z0, z1);
+                unpack2(P.dead, d0, d1);
+                P.z_last = pack2(d0 == 0.0f ? fmaxf(z0, zb) : z0, d1 == 0.0f ? fmaxf(z1, zb) : z1);
+            }
+            // The walk carries NEGATED weights: na = -a (the record holds -alpha, the inside mask m is
+            // 1 / 0), so T (1 - a) = fma(na, T, T) and err (1 - a) = fma(na, err, .) need no negation;
+            // nw = -w, and the colour, depth and A sums accumulate negated (flipped once in the epilogue).
+            for (int k0 = 0; k0 < cnt_pad; k0 += 32) {
+                if (__all_sync(kFull, !(lo_of(P.dead) == 0.0f || hi_of(P.dead) == 0.0f))) break;
+                const int k1 = min(cnt_pad, k0 + 32);
+                for (int k = k0; k < k1; k += kWalkUnroll) {
+    #pragma unroll
+                for (int ku = 0; ku < kWalkUnroll; ++ku) {
+                    const FRec &s = *reinterpret_cast<const FRec *>(fbase + s_wl[warp][k + ku]);
+                    PROF(0, lane == 0);
+                    const float4 q0 = *reinterpret_cast<const float4 *>(&s.a1x);      // a1x a1y c2x c2y
+                    const float4 q1 = *reinterpret_cast<const float4 *>(&s.V1);       // V1 V1 V2 V2
+                    const float4 q2 = *reinterpret_cast<const float4 *>(&s.thr_out);  // thr_out thr_in nkb nkb
+                    const float4 q3 = *reinterpret_cast<const float4 *>(&s.nka);      // nka alpha z -
+                    // v_k for both pixels (same ox; oy and oy + 4), h = v1^2 + v2^2 (+ the finished offset)
+                    const f32x2 v1 = fma2(OY, pack2(q0.y, q0.y), fma2(OX, pack2(q0.x, q0.x), pack2(q1.x, q1.y)));
+                    const f32x2 v2 = fma2(OY, pack2(q0.w, q0.w), fma2(OX, pack2(q0.z, q0.z), pack2(q1.z, q1.w)));
+                    const f32x2 h = fma2(v1, v1, fma2(v2, v2, P.dead));
+                    f32x2 neps = fma2(h, pack2(q3.x, q3.x), pack2(q2.z, q2.w));  // -(alpha's relative bound)
+                    float h0, h1;
+                    unpack2(h, h0, h1);
+                    // 1 where the pixel is certainly inside the support, 0 where outside or finished
+                    float m0 = le_mask(h0, q2.y), m1 = le_mask(h1, q2.y);
+                    if ((h0 > q2.y && h0 <= q2.x) || (h1 > q2.y && h1 <= q2.x)) {
+                        // boundary band (rare, divergent): the reference's float64 test (_kernels_cy.pyx:73-75)
+                        PROF(1, 1);
+                        const int j = (int)((reinterpret_cast<const char *>(&s) - fbase) / sizeof(FRec));
+                        const SplatRec &sd = (SOURCE == 3 ? v.far_recs : v.recs)[s_slot[j]];
+                        const double ddx = sd.mx - px;
+                        float e0, e1;
+                        unpack2(neps, e0, e1);
+                        if (h0 > q2.y && h0 <= q2.x) {
+                            const double ddy = sd.my - (py0 + 0.5);
+                            const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
+                            if (!(d2d > kSupportD2)) {
+                                m0 = 1.0f;
+                                h0 = (float)(d2d * kHalfLog2e);  // h, rounded once (within kEpsExact)
+                                e0 = -kEpsExact;
+                            }
+                        }
+                        if (h1 > q2.y && h1 <= q2.x) {
+                            const double ddy = sd.my - (py1 + 0.5);
+                            const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
+                            if (!(d2d > kSupportD2)) {
+                                m1 = 1.0f;
+                                h1 = (float)(d2d * kHalfLog2e);
+                                e1 = -kEpsExact;
+                            }
+                        }
+                        neps = pack2(e0, e1);
+                    }
+                    const f32x2 m = pack2(m0, m1);
+                    // alpha = min(o 2^-h, .99) inside the support, 0 outside: T, err and the sums then
+                    // stay exactly as they were (w = 0, T (1 - 0) = T, err (1 - 0) + 0)
+                    float e0, e1;
+                    unpack2(mul2(pack2(ex2_approx(-h0), ex2_approx(-h1)), pack2(q3.y, q3.y)), e0, e1);  // -o 2^-h
+                    const f32x2 na = mul2(pack2(fmaxf(e0, -0.99f), fmaxf(e1, -0.99f)), m);  // -a
+                    const f32x2 nw = mul2(na, P.T);                                       // -w
+                    const f32x2 Tn = fma2(na, P.T, P.T);  // T (1 - a), rounded once
+                    const float4 q4 = *reinterpret_cast<const float4 *>(&s.r);  // r g b -
+                    P.cr = fma2(nw, pack2(q4.x, q4.x), P.cr);
+                    P.cg = fma2(nw, pack2(q4.y, q4.y), P.cg);
+                    P.cb = fma2(nw, pack2(q4.z, q4.z), P.cb);
+                    P.D = fma2(nw, pack2(q3.z, q3.z), P.D);
+                    P.A = add2(P.A, nw);
+                    // err (1 - a) + w eps + 1.25 u T' (the rounding term only where T changed)
+                    P.err = fma2(na, P.err, fma2(nw, neps, fma2(Tn, mul2(m, pack2(kU125, kU125)), P.err)));
+                    P.T = Tn;
+                    P.nc = add2(P.nc, m);
+                    // near the cutoff (_kernels_cy.pyx:65-66): stop; decided or deferred after the walk
+                    float g0, g1, d0, d1;
+                    unpack2(sub2(Tn, P.err), g0, g1);
+                    unpack2(P.dead, d0, d1);
+                    P.dead = pack2(g0 <= kTHi ? kDead : d0, g1 <= kTHi ? kDead : d1);
+                }
+                }
+            }
+            if (SOURCE == 0) {  // drop the consumed head of the queue
+                const int rest = q_len - n;
+                uint32_t qv0 = threadIdx.x < rest ? s_queue[n + threadIdx.x] : 0u;
+                uint32_t qv1 = threadIdx.x + kBT < rest ? s_queue[n + kBT + threadIdx.x] : 0u;
+                __syncthreads();
+                if (threadIdx.x < rest) s_queue[threadIdx.x] = qv0;
+                if (threadIdx.x + kBT < rest) s_queue[kBT + threadIdx.x] = qv1;
+                q_len = rest;
+            } else {
+                cursor += n;
+            }
+        }
+    #ifdef SN_BLEND_PROF
+        const bool prof_live = __syncthreads_or(lo_of(P.dead) == 0.0f || hi_of(P.dead) == 0.0f) != 0;
+        if (SOURCE == 0 && MODE == 0 && threadIdx.x == 0) {
+            const uint32_t st = (uint32_t)v.env_off[el], tot = s1 - st;
+            // consumed: the list position the walk had reached (queued-but-unwalked entries excluded)
+            const uint32_t used = (cursor - st) - (uint32_t)q_len;
+            const unsigned fr = tot ? (unsigned)((1000ull * used) / tot) : 0u;
+            atomicMax(&g_env_frac[el & 63], fr);
+            // log-spaced bins of the consumed fraction (1e-5 units): <=0.1%, 0.2, 0.5, 1, 2, 5, 10, 20,
+            // 50, <100%; bin 10: the list ran out with a live (unsaturated) pixel
+            const unsigned f5 = tot ? (unsigned)((100000ull * used) / tot) : 0u;
+            const unsigned edges[9] = {100, 200, 500, 1000, 2000, 5000, 10000, 20000, 50000};
+            unsigned bin = 9;
+            for (int k = 8; k >= 0; --k)
+                if (f5 <= edges[k]) bin = k;
+            if (prof_live && cursor >= s1 && q_len == 0) bin = 10;
+            atomicAdd(&g_blend_prof[4 + bin], 1ull);
+        }
+        for (int i = 0; i < 16; ++i)
+            if (prof[i]) atomicAdd(&g_blend_prof[i], prof[i]);
+    #endif
+        if (b.scans && threadIdx.x == 0 && scanned) atomicAdd(b.scans, (unsigned long long)scanned);
+        if (b.loads && threadIdx.x == 0 && loaded) atomicAdd(b.loads, (unsigned long long)loaded);
+
+        // Depth-sliced pass: the near list ran out. A tile with a live pixel (or one whose cutoff is
+        // undecided: its float64 walk may need to go on) and far splats in its env registers as
+        // unfinished, saves its pixels' state and leaves the live pixels to the continuation (source 3).
+        bool saved = false;
+        if (SOURCE == 0 && v.sliced) {
+            float Tq[2], Eq[2], Dq[2];
+            unpack2(P.T, Tq[0], Tq[1]);
+            unpack2(P.err, Eq[0], Eq[1]);
+            unpack2(P.dead, Dq[0], Dq[1]);
+            bool need = false;
+    #pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                const bool cutq = Tq[p] - Eq[p] <= kTHi;
+                const bool ambq = cutq && (!(Tq[p] + Eq[p] < kTLo) || Eq[p] > 0.0625f * Tq[p]);
+                need |= (p ? in1 : in0) && (Dq[p] == 0.0f || ambq);
+            }
+            const bool has_far = v.env_off[v.ec + el + 1] > v.env_off[v.ec + el];
+            if (__syncthreads_or(need) && has_far) {
+                if (threadIdx.x == 0) {
+                    const unsigned long long uu = atomicAdd(b.unfin_count, 1ull);
+                    s_u = uu < v.far_cap_u ? (int)uu : -1;
+                    if (s_u >= 0) {
+                        b.unfin_list[s_u] = ((uint32_t)el << 16) | (uint32_t)tile;
+                        b.bucket_of[(int64_t)el * (tiles_of(b.width) * tiles_of(b.height)) + tile] = s_u;
+                    }
+                }
+                __syncthreads();
+                const int us = s_u;
+                if (us >= 0) {
+                    float *st = b.state + (size_t)us * kStateF * kBT + threadIdx.x;
+                    const f32x2 f[10] = {P.T, P.err, P.A, P.cr, P.cg, P.cb, P.D, P.dead, P.z_last, P.nc};
+    #pragma unroll
+                    for (int q = 0; q < 10; ++q) {
+                        st[(2 * q) * kBT] = lo_of(f[q]);
+                        st[(2 * q + 1) * kBT] = hi_of(f[q]);
+                    }
+                    st[20 * kBT] = z_first;
+                    st[21 * kBT] = __uint_as_float(s_epsmax);
+                }
+                saved = true;  // (on overflow the render is re-run: these pixels' outputs do not matter)
+            }
+        }
+
+        const sn_camera &cam = b.cams[env];
+        if (!kPixBound) P.eps_max = pack2(__uint_as_float(s_epsmax), __uint_as_float(s_epsmax));
+        float T2[2], E2[2], A2[2], CR[2], CG[2], CB[2], DD[2], EM[2], ZL[2];
+        unpack2(P.T, T2[0], T2[1]);
+        unpack2(P.err, E2[0], E2[1]);
+        unpack2(P.A, A2[0], A2[1]);
+        unpack2(P.cr, CR[0], CR[1]);
+        unpack2(P.cg, CG[0], CG[1]);
+        unpack2(P.cb, CB[0], CB[1]);
+        unpack2(P.D, DD[0], DD[1]);
+        unpack2(P.eps_max, EM[0], EM[1]);
+        unpack2(P.z_last, ZL[0], ZL[1]);
+        float NCf[2];
+        unpack2(P.nc, NCf[0], NCf[1]);
+        const int NC[2] = {(int)NCf[0], (int)NCf[1]};
+    #pragma unroll
+        for (int p = 0; p < 2; ++p) {  // the walk accumulated negated sums (exact: negation is exact)
+            A2[p] = -A2[p];
+            CR[p] = -CR[p];
+            CG[p] = -CG[p];
+            CB[p] = -CB[p];
+            DD[p] = -DD[p];
+        }
+        float DL[2];
+        unpack2(P.dead, DL[0], DL[1]);
+        // the pixels this launch finishes: every pixel, but a saved tile's live ones (the continuation
+        // finishes them) and, in the continuation, only the pixels that were live when it resumed
+        const bool FIN[2] = {SOURCE == 3 ? entry_live0 : !(saved && DL[0] == 0.0f),
+                             SOURCE == 3 ? entry_live1 : !(saved && DL[1] == 0.0f)};
+        const bool IN[2] = {in0, in1};
+        const int PY[2] = {py0, py1};
+        unsigned contrib_sum = 0;
+    #pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const float T = T2[p], err = E2[p], A = A2[p];
+            const int nc = NC[p];
+            const bool inside = IN[p];
+            const int py_i = PY[p];
+            // the cutoff fired (T - err <= 1e-4 (1 + 1e-6)) but T < 1e-4 is not certain: float64 fixup.
+            // Also when err > T / 16: the 0.25 u T' margin in kU125 covers the bound's own float
+            // roundings (<= 2u err per step) only while err <= T / 8, and err / T never decreases.
+            const bool cut = T - err <= kTHi;
+            const bool amb = inside && (b.force_exact || (cut && (!(T + err < kTLo) || err > 0.0625f * T)));
+            PROF(2, amb);
+            const int64_t pix = ((int64_t)env * b.height + py_i) * b.width + px_i;
+            const uint32_t code = (uint32_t)(((int64_t)el * b.height + py_i) * b.width + px_i);
+            // Error bounds of the outputs the compositor decides on. Every weight w_i = a_i T_(i-1) has
+            // relative error <= rho_w (transmittance bound + largest alpha bound + the product's
+            // rounding); depth = sum z w / sum w then errs by <= rho_w (z_last - z_first) from the
+            // weights (z spans the contributions) plus (2n + 2) u from the float sums and the division;
+            // alpha by rho_w + (n + 1) u.
+            const float zf = nc == 0 ? 3.0e38f : z_first;  // no contribution: the empty range
+            const float rho_w = err / T + EM[p] + 6.0e-8f;
+            const float alpha = fminf(A, 1.0f);
+            const float depth = A > 0.0f ? DD[p] / A : (float)cam.far_;
+            const float d_err = 1.01f * (rho_w * (ZL[p] - zf) + (float)(2 * nc + 2) * 6.0e-8f * depth);
+            const bool fin = FIN[p];
+            const bool flag = inside && amb && fin;
+            contrib_sum += (flag || !fin) ? 0u : (unsigned)nc;
+            push_fixup(b, flag, code);
+            if (!inside || !fin) continue;
+            if (MODE == 2 && SOURCE != 1 && threadIdx.x == 0 && p == 0) b.tile_flag[(int64_t)el * (tiles_of(b.width) * tiles_of(b.height)) + tile] = 1;
+            if (flag) {
+                if (MODE == 2) b.ldepth[pix] = __int_as_float(0x7fc00000);  // NaN: pending float64 fixup
+                continue;
+            }
+            if (b.contrib) b.contrib[pix] = nc;
+            if (MODE == 0) {
+                float *oc = b.color + 3 * pix;
+                const float o0 = np_clipf(__fmaf_rn((float)cam.background[0], T, CR[p]), 0.0f, 1.0f);
+                const float o1 = np_clipf(__fmaf_rn((float)cam.background[1], T, CG[p]), 0.0f, 1.0f);
+                const float o2 = np_clipf(__fmaf_rn((float)cam.background[2], T, CB[p]), 0.0f, 1.0f);
+                oc[0] = o0;
+                oc[1] = o1;
+                oc[2] = o2;
+                b.alpha[pix] = alpha;
+                b.depth[pix] = depth;
+                if (b.derr) b.derr[pix] = A > 0.0f ? d_err : 0.0f;
+                store_payload(b, pix, o0, o1, o2, depth);
+                continue;
+            }
+            float fc0 = 0.0f, fc1 = 0.0f, fc2 = 0.0f;
+            if (A > 0.0f) {
+                fc0 = np_clipf(CR[p] / A, 0.0f, 1.0f);
+                fc1 = np_clipf(CG[p] / A, 0.0f, 1.0f);
+                fc2 = np_clipf(CB[p] / A, 0.0f, 1.0f);
+            }
+            if (MODE == 1) {
+                float *oc = b.color + 3 * pix;
+                oc[0] = fc0;
+                oc[1] = fc1;
+                oc[2] = fc2;
+                b.alpha[pix] = alpha;
+                b.depth[pix] = depth;
+                store_payload(b, pix, fc0, fc1, fc2, depth);
+                continue;
+            }
+            // MODE 2: the layer frame goes to its own buffers; composite_kernel merges it into the scene
+            // frame once the scene pass is done (so this blend runs concurrently with the scene blend)
+            float *lc = b.lcolor + 3 * pix;
+            lc[0] = fc0;
+            lc[1] = fc1;
+            lc[2] = fc2;
+            b.lalpha[pix] = alpha;
+            b.ldepth[pix] = depth;
+            b.lderr[pix] = d_err;
+            b.laerr[pix] = 1.01f * (rho_w + (float)(nc + 1) * 6.0e-8f) * A + 6.0e-8f;
+        }
+        if (b.contribs) {
+            const unsigned sum = __reduce_add_sync(kFull, contrib_sum);
+            if (lane == 0 && sum) atomicAdd(b.contribs, (unsigned long long)sum);
+        }
+#undef PROF
+    };
+    if (SOURCE == 3) {  // the unfinished tiles, taken dynamically by a few CTAs per SM
+        const uint32_t n_items = (uint32_t)min(*v.far_unfin, (unsigned long long)v.far_cap_u);
+        while (true) {
+            if (threadIdx.x == 0) s_u = (int)atomicAdd(v.far_next, 1u);
+            __syncthreads();
+            const int item = s_u;
+            __syncthreads();
+            if ((uint32_t)item >= n_items) break;
+            const uint32_t key = v.far_unfin_list[item];
+            do_tile((int)(key & 0xffffu), (int)(key >> 16), item);
+            __syncthreads();  // the next tile reuses the shared buffers
         }
     } else {
-        cursor = (uint32_t)v.env_off[el];
-        s1 = (uint32_t)v.env_off[el + 1];
+        do_tile(blockIdx.x, blockIdx.y, -1);
     }
-
-    // added to h: a finished pixel skips every splat. A pixel is finished when it is outside the
-    // frame, forced exact, or past the cutoff test (after which T and err never change, so the
-    // cutoff's ambiguity is re-derived from them after the walk). 1e30 (not inf) keeps every
-    // product of the chain finite (a finished pixel's alpha is 0 and its eps ~1e24).
-    constexpr float kDead = 1.0e30f;
-    PixPair P;
-    P.T = pack2(1.0f, 1.0f);
-    P.err = P.A = P.cr = P.cg = P.cb = P.D = P.eps_max = P.z_last = P.nc = 0ull;
-    P.dead = pack2((!in0 || b.force_exact) ? kDead : 0.0f, (!in1 || b.force_exact) ? kDead : 0.0f);
-    float z_first = 3.0e38f;
-    uint32_t loaded = 0, scanned = 0;
-    int q_len = 0;  // SOURCE 0: entries waiting in s_queue (uniform across the CTA)
-    while (true) {
-        const bool live = lo_of(P.dead) == 0.0f || hi_of(P.dead) == 0.0f;
-        if (__syncthreads_count(live) == 0) break;  // also guards s_f / s_queue reuse
-        int n;
-        if (SOURCE == 0) {
-            stream_fill<kBT>(v, tx, ty, kBatch, cursor, s1, q_len, scanned, s_queue, s_wsum);
-            n = min(q_len, kBatch);
-        } else {
-            n = (int)min((uint32_t)kBatch, s1 - cursor);
-        }
-        if (n <= 0) break;
-        loaded += n;
-#pragma unroll
-        for (int r = 0; r < kPerT; ++r) {
-            const int jt = threadIdx.x + r * kBT;
-            if (jt >= n) break;
-            // the record slot: tile lists hold slots; streamed / all-splat sources map depth ranks
-            const uint32_t rid = SOURCE == 1 ? __ldg(v.pair_vals + cursor + jt)
-                                             : __ldg(v.order + (SOURCE == 0 ? s_queue[jt] : cursor + jt));
-            const GatheredSplat gs = gather_splat(v.geo, v.recs, rid);
-            FRec f;
-            unsigned msk = tile_entry(gs.e1x, gs.e1y, gs.p1, gs.p2, gs.gl, gs.gr, x0 + 8.0, y0 + 8.0, f);
-            if (kBound && !kPixBound && msk)  // eps at the support edge bounds eps inside it
-                atomicMax(&s_epsmax, __float_as_uint(-__fmaf_rn(f.nka, fminf(f.thr_out, 7.0f), f.nkb)));
-            if (msk) s_f[jt] = f;  // an entry no warp walks is never read
-            s_slot[jt] = rid;
-            s_mask[jt] = (uint8_t)msk;
-        }
-        __syncthreads();
-        // each warp walks only the batch entries whose support can reach its 8 x 8 pixel block,
-        // in depth order; the per-pixel tests below stay exact, the mask only skips whole warps
-        int cnt = 0;
-        for (int j0 = 0; j0 < n; j0 += 32) {
-            const bool mine = j0 + lane < n && ((s_mask[j0 + lane] >> warp) & 1u);
-            const unsigned bal = __ballot_sync(kFull, mine);
-            if (mine) s_wl[warp][cnt + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)((j0 + lane) * sizeof(FRec));
-            cnt += __popc(bal);
-        }
-        const int cnt_pad = (cnt + kWalkUnroll - 1) / kWalkUnroll * kWalkUnroll;
-        if (lane < cnt_pad - cnt) s_wl[warp][cnt + lane] = (uint16_t)(kBatch * sizeof(FRec));
-        __syncwarp();
-        // depth bounds of the contributions, once per batch instead of per contribution: the warp's
-        // entries arrive in depth order, so its first one is a lower bound of every pixel's first
-        // contribution, and its last one an upper bound of any contribution a pixel still live at
-        // the batch's start makes in it
-        const char *fbase = reinterpret_cast<const char *>(s_f);
-        if (kBound && cnt > 0) {
-            z_first = fminf(z_first, reinterpret_cast<const FRec *>(fbase + s_wl[warp][0])->z);
-            const float zb = reinterpret_cast<const FRec *>(fbase + s_wl[warp][cnt - 1])->z;
-            float z0, z1, d0, d1;
-            unpack2(P.z_last, z0, z1);
-            unpack2(P.dead, d0, d1);
-            P.z_last = pack2(d0 == 0.0f ? fmaxf(z0, zb) : z0, d1 == 0.0f ? fmaxf(z1, zb) : z1);
-        }
-        // The walk carries NEGATED weights: na = -a (the record holds -alpha, the inside mask m is
-        // 1 / 0), so T (1 - a) = fma(na, T, T) and err (1 - a) = fma(na, err, .) need no negation;
-        // nw = -w, and the colour, depth and A sums accumulate negated (flipped once in the epilogue).
-        for (int k0 = 0; k0 < cnt_pad; k0 += 32) {
-            if (__all_sync(kFull, !(lo_of(P.dead) == 0.0f || hi_of(P.dead) == 0.0f))) break;
-            const int k1 = min(cnt_pad, k0 + 32);
-            for (int k = k0; k < k1; k += kWalkUnroll) {
-#pragma unroll
-            for (int ku = 0; ku < kWalkUnroll; ++ku) {
-                const FRec &s = *reinterpret_cast<const FRec *>(fbase + s_wl[warp][k + ku]);
-                PROF(0, lane == 0);
-                const float4 q0 = *reinterpret_cast<const float4 *>(&s.a1x);      // a1x a1y c2x c2y
-                const float4 q1 = *reinterpret_cast<const float4 *>(&s.V1);       // V1 V1 V2 V2
-                const float4 q2 = *reinterpret_cast<const float4 *>(&s.thr_out);  // thr_out thr_in nkb nkb
-                const float4 q3 = *reinterpret_cast<const float4 *>(&s.nka);      // nka alpha z -
-                // v_k for both pixels (same ox; oy and oy + 4), h = v1^2 + v2^2 (+ the finished offset)
-                const f32x2 v1 = fma2(OY, pack2(q0.y, q0.y), fma2(OX, pack2(q0.x, q0.x), pack2(q1.x, q1.y)));
-                const f32x2 v2 = fma2(OY, pack2(q0.w, q0.w), fma2(OX, pack2(q0.z, q0.z), pack2(q1.z, q1.w)));
-                const f32x2 h = fma2(v1, v1, fma2(v2, v2, P.dead));
-                f32x2 neps = fma2(h, pack2(q3.x, q3.x), pack2(q2.z, q2.w));  // -(alpha's relative bound)
-                float h0, h1;
-                unpack2(h, h0, h1);
-                // 1 where the pixel is certainly inside the support, 0 where outside or finished
-                float m0 = le_mask(h0, q2.y), m1 = le_mask(h1, q2.y);
-                if ((h0 > q2.y && h0 <= q2.x) || (h1 > q2.y && h1 <= q2.x)) {
-                    // boundary band (rare, divergent): the reference's float64 test (_kernels_cy.pyx:73-75)
-                    PROF(1, 1);
-                    const int j = (int)((reinterpret_cast<const char *>(&s) - fbase) / sizeof(FRec));
-                    const SplatRec &sd = v.recs[s_slot[j]];
-                    const double ddx = sd.mx - px;
-                    float e0, e1;
-                    unpack2(neps, e0, e1);
-                    if (h0 > q2.y && h0 <= q2.x) {
-                        const double ddy = sd.my - (py0 + 0.5);
-                        const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
-                        if (!(d2d > kSupportD2)) {
-                            m0 = 1.0f;
-                            h0 = (float)(d2d * kHalfLog2e);  // h, rounded once (within kEpsExact)
-                            e0 = -kEpsExact;
-                        }
-                    }
-                    if (h1 > q2.y && h1 <= q2.x) {
-                        const double ddy = sd.my - (py1 + 0.5);
-                        const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
-                        if (!(d2d > kSupportD2)) {
-                            m1 = 1.0f;
-                            h1 = (float)(d2d * kHalfLog2e);
-                            e1 = -kEpsExact;
-                        }
-                    }
-                    neps = pack2(e0, e1);
-                }
-                const f32x2 m = pack2(m0, m1);
-                // alpha = min(o 2^-h, .99) inside the support, 0 outside: T, err and the sums then
-                // stay exactly as they were (w = 0, T (1 - 0) = T, err (1 - 0) + 0)
-                float e0, e1;
-                unpack2(mul2(pack2(ex2_approx(-h0), ex2_approx(-h1)), pack2(q3.y, q3.y)), e0, e1);  // -o 2^-h
-                const f32x2 na = mul2(pack2(fmaxf(e0, -0.99f), fmaxf(e1, -0.99f)), m);  // -a
-                const f32x2 nw = mul2(na, P.T);                                       // -w
-                const f32x2 Tn = fma2(na, P.T, P.T);  // T (1 - a), rounded once
-                const float4 q4 = *reinterpret_cast<const float4 *>(&s.r);  // r g b -
-                P.cr = fma2(nw, pack2(q4.x, q4.x), P.cr);
-                P.cg = fma2(nw, pack2(q4.y, q4.y), P.cg);
-                P.cb = fma2(nw, pack2(q4.z, q4.z), P.cb);
-                P.D = fma2(nw, pack2(q3.z, q3.z), P.D);
-                P.A = add2(P.A, nw);
-                // err (1 - a) + w eps + 1.25 u T' (the rounding term only where T changed)
-                P.err = fma2(na, P.err, fma2(nw, neps, fma2(Tn, mul2(m, pack2(kU125, kU125)), P.err)));
-                P.T = Tn;
-                P.nc = add2(P.nc, m);
-                // near the cutoff (_kernels_cy.pyx:65-66): stop; decided or deferred after the walk
-                float g0, g1, d0, d1;
-                unpack2(sub2(Tn, P.err), g0, g1);
-                unpack2(P.dead, d0, d1);
-                P.dead = pack2(g0 <= kTHi ? kDead : d0, g1 <= kTHi ? kDead : d1);
-            }
-            }
-        }
-        if (SOURCE == 0) {  // drop the consumed head of the queue
-            const int rest = q_len - n;
-            uint32_t qv0 = threadIdx.x < rest ? s_queue[n + threadIdx.x] : 0u;
-            uint32_t qv1 = threadIdx.x + kBT < rest ? s_queue[n + kBT + threadIdx.x] : 0u;
-            __syncthreads();
-            if (threadIdx.x < rest) s_queue[threadIdx.x] = qv0;
-            if (threadIdx.x + kBT < rest) s_queue[kBT + threadIdx.x] = qv1;
-            q_len = rest;
-        } else {
-            cursor += n;
-        }
-    }
-#ifdef SN_BLEND_PROF
-    const bool prof_live = __syncthreads_or(lo_of(P.dead) == 0.0f || hi_of(P.dead) == 0.0f) != 0;
-    if (SOURCE == 0 && MODE == 0 && threadIdx.x == 0) {
-        const uint32_t st = (uint32_t)v.env_off[el], tot = s1 - st;
-        // consumed: the list position the walk had reached (queued-but-unwalked entries excluded)
-        const uint32_t used = (cursor - st) - (uint32_t)q_len;
-        const unsigned fr = tot ? (unsigned)((1000ull * used) / tot) : 0u;
-        atomicMax(&g_env_frac[el & 63], fr);
-        // log-spaced bins of the consumed fraction (1e-5 units): <=0.1%, 0.2, 0.5, 1, 2, 5, 10, 20,
-        // 50, <100%; bin 10: the list ran out with a live (unsaturated) pixel
-        const unsigned f5 = tot ? (unsigned)((100000ull * used) / tot) : 0u;
-        const unsigned edges[9] = {100, 200, 500, 1000, 2000, 5000, 10000, 20000, 50000};
-        unsigned bin = 9;
-        for (int k = 8; k >= 0; --k)
-            if (f5 <= edges[k]) bin = k;
-        if (prof_live && cursor >= s1 && q_len == 0) bin = 10;
-        atomicAdd(&g_blend_prof[4 + bin], 1ull);
-    }
-    for (int i = 0; i < 16; ++i)
-        if (prof[i]) atomicAdd(&g_blend_prof[i], prof[i]);
-#endif
-    if (b.scans && threadIdx.x == 0 && scanned) atomicAdd(b.scans, (unsigned long long)scanned);
-    if (b.loads && threadIdx.x == 0 && loaded) atomicAdd(b.loads, (unsigned long long)loaded);
-
-    const sn_camera &cam = b.cams[env];
-    if (!kPixBound) P.eps_max = pack2(__uint_as_float(s_epsmax), __uint_as_float(s_epsmax));
-    float T2[2], E2[2], A2[2], CR[2], CG[2], CB[2], DD[2], EM[2], ZL[2];
-    unpack2(P.T, T2[0], T2[1]);
-    unpack2(P.err, E2[0], E2[1]);
-    unpack2(P.A, A2[0], A2[1]);
-    unpack2(P.cr, CR[0], CR[1]);
-    unpack2(P.cg, CG[0], CG[1]);
-    unpack2(P.cb, CB[0], CB[1]);
-    unpack2(P.D, DD[0], DD[1]);
-    unpack2(P.eps_max, EM[0], EM[1]);
-    unpack2(P.z_last, ZL[0], ZL[1]);
-    float NCf[2];
-    unpack2(P.nc, NCf[0], NCf[1]);
-    const int NC[2] = {(int)NCf[0], (int)NCf[1]};
-#pragma unroll
-    for (int p = 0; p < 2; ++p) {  // the walk accumulated negated sums (exact: negation is exact)
-        A2[p] = -A2[p];
-        CR[p] = -CR[p];
-        CG[p] = -CG[p];
-        CB[p] = -CB[p];
-        DD[p] = -DD[p];
-    }
-    const bool IN[2] = {in0, in1};
-    const int PY[2] = {py0, py1};
-    unsigned contrib_sum = 0;
-#pragma unroll
-    for (int p = 0; p < 2; ++p) {
-        const float T = T2[p], err = E2[p], A = A2[p];
-        const int nc = NC[p];
-        const bool inside = IN[p];
-        const int py_i = PY[p];
-        // the cutoff fired (T - err <= 1e-4 (1 + 1e-6)) but T < 1e-4 is not certain: float64 fixup.
-        // Also when err > T / 16: the 0.25 u T' margin in kU125 covers the bound's own float
-        // roundings (<= 2u err per step) only while err <= T / 8, and err / T never decreases.
-        const bool cut = T - err <= kTHi;
-        const bool amb = inside && (b.force_exact || (cut && (!(T + err < kTLo) || err > 0.0625f * T)));
-        PROF(2, amb);
-        const int64_t pix = ((int64_t)env * b.height + py_i) * b.width + px_i;
-        const uint32_t code = (uint32_t)(((int64_t)el * b.height + py_i) * b.width + px_i);
-        // Error bounds of the outputs the compositor decides on. Every weight w_i = a_i T_(i-1) has
-        // relative error <= rho_w (transmittance bound + largest alpha bound + the product's
-        // rounding); depth = sum z w / sum w then errs by <= rho_w (z_last - z_first) from the
-        // weights (z spans the contributions) plus (2n + 2) u from the float sums and the division;
-        // alpha by rho_w + (n + 1) u.
-        const float zf = nc == 0 ? 3.0e38f : z_first;  // no contribution: the empty range
-        const float rho_w = err / T + EM[p] + 6.0e-8f;
-        const float alpha = fminf(A, 1.0f);
-        const float depth = A > 0.0f ? DD[p] / A : (float)cam.far_;
-        const float d_err = 1.01f * (rho_w * (ZL[p] - zf) + (float)(2 * nc + 2) * 6.0e-8f * depth);
-        const bool flag = inside && amb;
-        contrib_sum += flag ? 0u : (unsigned)nc;
-        push_fixup(b, flag, code);
-        if (!inside) continue;
-        if (MODE == 2 && SOURCE != 1 && threadIdx.x == 0 && p == 0) b.tile_flag[(int64_t)el * gridDim.x + tile] = 1;
-        if (flag) {
-            if (MODE == 2) b.ldepth[pix] = __int_as_float(0x7fc00000);  // NaN: pending float64 fixup
-            continue;
-        }
-        if (b.contrib) b.contrib[pix] = nc;
-        if (MODE == 0) {
-            float *oc = b.color + 3 * pix;
-            const float o0 = np_clipf(__fmaf_rn((float)cam.background[0], T, CR[p]), 0.0f, 1.0f);
-            const float o1 = np_clipf(__fmaf_rn((float)cam.background[1], T, CG[p]), 0.0f, 1.0f);
-            const float o2 = np_clipf(__fmaf_rn((float)cam.background[2], T, CB[p]), 0.0f, 1.0f);
-            oc[0] = o0;
-            oc[1] = o1;
-            oc[2] = o2;
-            b.alpha[pix] = alpha;
-            b.depth[pix] = depth;
-            if (b.derr) b.derr[pix] = A > 0.0f ? d_err : 0.0f;
-            store_payload(b, pix, o0, o1, o2, depth);
-            continue;
-        }
-        float fc0 = 0.0f, fc1 = 0.0f, fc2 = 0.0f;
-        if (A > 0.0f) {
-            fc0 = np_clipf(CR[p] / A, 0.0f, 1.0f);
-            fc1 = np_clipf(CG[p] / A, 0.0f, 1.0f);
-            fc2 = np_clipf(CB[p] / A, 0.0f, 1.0f);
-        }
-        if (MODE == 1) {
-            float *oc = b.color + 3 * pix;
-            oc[0] = fc0;
-            oc[1] = fc1;
-            oc[2] = fc2;
-            b.alpha[pix] = alpha;
-            b.depth[pix] = depth;
-            store_payload(b, pix, fc0, fc1, fc2, depth);
-            continue;
-        }
-        // MODE 2: the layer frame goes to its own buffers; composite_kernel merges it into the scene
-        // frame once the scene pass is done (so this blend runs concurrently with the scene blend)
-        float *lc = b.lcolor + 3 * pix;
-        lc[0] = fc0;
-        lc[1] = fc1;
-        lc[2] = fc2;
-        b.lalpha[pix] = alpha;
-        b.ldepth[pix] = depth;
-        b.lderr[pix] = d_err;
-        b.laerr[pix] = 1.01f * (rho_w + (float)(nc + 1) * 6.0e-8f) * A + 6.0e-8f;
-    }
-    if (b.contribs) {
-        const unsigned sum = __reduce_add_sync(kFull, contrib_sum);
-        if (lane == 0 && sum) atomicAdd(b.contribs, (unsigned long long)sum);
-    }
-#undef PROF
 }
 
 #ifndef SN_LAYER_PX1_MIN_BLOCKS
@@ -1242,7 +1326,7 @@ __device__ __forceinline__ void composite_tile(const BlendArgs &b, const int til
 }
 
 __global__ void __launch_bounds__(kBlock) composite_kernel(BlendArgs b) {
-    if (pass_overflow(b.pv) || pass_overflow(b.back)) return;
+    if (pass_overflow(b.pv) || pass_overflow(b.back) || far_overflow(b.back)) return;
     if (b.pv.source == 1 && b.pv.tile_list) {  // listed: only the tiles that hold layer splats
         const uint32_t n_items = *b.pv.n_list;
         for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
@@ -1366,11 +1450,22 @@ __device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_
         cur = (uint32_t)v.env_off[el];
         end = (uint32_t)v.env_off[el + 1];
     }
+    // two segments: the pass's own list, then -- a depth-sliced pass's unfinished tile -- its far
+    // bucket (every far z is beyond every near one: the concatenation is the tile's depth order)
+    for (int sgm = 0; sgm < 2; ++sgm) {
+    const bool far = sgm == 1;
+    if (far) {
+        if (!v.sliced || done || near) break;
+        const int32_t ub = v.far_bucket_of[(int64_t)el * v.n_tiles + tile];
+        if (ub < 0) break;
+        cur = (uint32_t)v.far_boff[ub];
+        end = (uint32_t)v.far_boff[ub + 1];
+    }
     while (cur < end && !done && !near) {
         uint32_t step;
         uint32_t rid[kPer];
         bool cand[kPer];
-        if (v.source == 0) {
+        if (!far && v.source == 0) {
             const uint32_t bi = cur / kBlock;
             if (cur % kBlock == 0 || !covers(__ldg(v.batch_rects + bi), tx, ty)) {
                 // find the next 256-splat batch whose union rectangle covers the tile, 32 batches
@@ -1401,7 +1496,7 @@ __device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_
             for (int i = 0; i < kPer; ++i) {
                 const uint32_t k = cur + 32 * i + lane;
                 cand[i] = k < cur + step;
-                rid[i] = cand[i] ? (v.source == 1 ? __ldg(v.pair_vals + k) : k) : 0u;
+                rid[i] = cand[i] ? (far ? __ldg(v.far_order + k) : v.source == 1 ? __ldg(v.pair_vals + k) : k) : 0u;
             }
         }
         QEntry e[kPer];
@@ -1411,7 +1506,7 @@ __device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_
             contrib[i] = false;
             e[i] = QEntry{};
             if (cand[i]) {
-                const SplatRec &s = v.recs[v.source == 1 ? rid[i] : __ldg(v.order + rid[i])];
+                const SplatRec &s = far ? v.far_recs[rid[i]] : v.recs[v.source == 1 ? rid[i] : __ldg(v.order + rid[i])];
                 const double dx = s.mx - px, dy = s.my - py;
                 const double d2 = (s.ca * dx * dx + s.cb2 * dx * dy) + s.cc * dy * dy;
                 if (!(d2 > kSupportD2)) {
@@ -1446,6 +1541,7 @@ __device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_
             }
         }
         cur += step;
+    }
     }
     if (!done && !near && qn > 0) consume(qn);
     __syncwarp();
@@ -1528,10 +1624,22 @@ __device__ ExactPixel exact_walk_cta(const PassView &v, int el, int tile, int ti
     }
     int *s_cnt = s_i;           // [8] per-warp counts
     int *s_flag = s_i + 8;      // [0] done, [1] next cursor (source 0 batch search)
+    if (threadIdx.x == 0) s_flag[0] = 0;
+    __syncthreads();
+    // two segments: the pass's own list, then a depth-sliced pass's far bucket (see exact_walk)
+    for (int sgm = 0; sgm < 2; ++sgm) {
+    const bool far = sgm == 1;
+    if (far) {
+        if (!v.sliced || s_flag[0]) break;  // s_flag[0]: the walk already stopped (uniform)
+        const int32_t ub = v.far_bucket_of[(int64_t)el * v.n_tiles + tile];
+        if (ub < 0) break;
+        cur = (uint32_t)v.far_boff[ub];
+        end = (uint32_t)v.far_boff[ub + 1];
+    }
     while (cur < end) {
         uint32_t step;
         int per;
-        if (v.source == 0) {  // one 256-splat batch per step; warp 0 finds the next covering batch
+        if (!far && v.source == 0) {  // one 256-splat batch per step; warp 0 finds the next covering batch
             if (warp == 0) {
                 uint32_t c = cur;
                 while (c < end) {
@@ -1563,10 +1671,11 @@ __device__ ExactPixel exact_walk_cta(const PassView &v, int el, int tile, int ti
             if (k < cur + step) {
                 uint32_t rid = k;
                 bool cand = true;
-                if (v.source == 0) cand = covers(__ldg(v.rects + k), tx, ty);
+                if (far) rid = __ldg(v.far_order + k);
+                else if (v.source == 0) cand = covers(__ldg(v.rects + k), tx, ty);
                 else if (v.source == 1) rid = __ldg(v.pair_vals + k);
                 if (cand) {
-                    const SplatRec &sr = v.recs[v.source == 1 ? rid : __ldg(v.order + rid)];
+                    const SplatRec &sr = far ? v.far_recs[rid] : v.recs[v.source == 1 ? rid : __ldg(v.order + rid)];
                     const double dx = sr.mx - px, dy = sr.my - py;
                     const double d2 = (sr.ca * dx * dx + sr.cb2 * dx * dy) + sr.cc * dy * dy;
                     if (!(d2 > kSupportD2)) {
@@ -1620,6 +1729,7 @@ __device__ ExactPixel exact_walk_cta(const PassView &v, int el, int tile, int ti
         if (stop) break;
         cur += step;
     }
+    }
     if (warp == 0) {
         if (!done && !near && qn > 0) consume(0, qn);
 #pragma unroll
@@ -1659,7 +1769,7 @@ __global__ void __launch_bounds__(256) fixup_layer_kernel(BlendArgs b) {
     __shared__ int s_back;
     if (threadIdx.x < 64) s_exp[threadIdx.x] = kExp2Tbl[threadIdx.x];
     __syncthreads();
-    if (pass_overflow(b.pv) || pass_overflow(b.back)) return;
+    if (pass_overflow(b.pv) || pass_overflow(b.back) || far_overflow(b.back)) return;
     const unsigned n_fix = *b.fix_count;
     const unsigned hw = (unsigned)b.width * (unsigned)b.height;
     unsigned long long contribs = 0;
@@ -1732,7 +1842,8 @@ __global__ void __launch_bounds__(256, SN_FIXUP_MIN_BLOCKS) fixup_kernel(BlendAr
     __syncthreads();
     const int lane = threadIdx.x & 31;
     QEntry *q = s_q[threadIdx.x >> 5];
-    if (pass_overflow(b.pv) || (MODE == 2 && pass_overflow(b.back))) return;
+    if (pass_overflow(b.pv) || far_overflow(b.pv) || (MODE == 2 && (pass_overflow(b.back) || far_overflow(b.back))))
+        return;
     const unsigned n_fix = *b.fix_count;
     const unsigned hw = (unsigned)b.width * (unsigned)b.height;
     unsigned long long contribs = 0;
@@ -1895,7 +2006,7 @@ __global__ void blend_tile_range_kernel(int t_begin, int tiles_x, int tile_size,
 }  // namespace
 
 template <int MODE>
-static void launch_blend_mode(const BlendArgs &b, dim3 grid, cudaStream_t s) {
+static void launch_blend_mode(const BlendArgs &b, dim3 grid, cudaStream_t s, bool fixup) {
     if constexpr (MODE == 2) {  // the avatar layer: one pixel per thread (see blend_kernel_px1)
         if (b.pv.source == 0)
             blend_kernel_px1<MODE, 0><<<grid, kBlock, 0, s>>>(b);
@@ -1912,8 +2023,8 @@ static void launch_blend_mode(const BlendArgs &b, dim3 grid, cudaStream_t s) {
             blend_kernel<MODE, 1><<<grid, kBT, 0, s>>>(b);
         else
             blend_kernel<MODE, 2><<<grid, kBT, 0, s>>>(b);
+        if (fixup) fixup_kernel<MODE><<<kFixupBlocks, 256, 0, s>>>(b);  // mode 2: after the composite
     }
-    if constexpr (MODE != 2) fixup_kernel<MODE><<<kFixupBlocks, 256, 0, s>>>(b);  // mode 2: after the composite
 }
 
 cudaError_t launch_tile_queue(const PassView &v, int el, int n_tiles, int tiles_x, uint32_t *counts,
@@ -1933,14 +2044,32 @@ cudaError_t launch_layer_composite(const BlendArgs &b, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_blend(const BlendArgs &b, cudaStream_t s) {
+cudaError_t launch_blend(const BlendArgs &b, cudaStream_t s, bool fixup) {
     dim3 grid((unsigned)(tiles_of(b.width) * tiles_of(b.height)), (unsigned)b.ec);
     if (b.mode == 0)
-        launch_blend_mode<0>(b, grid, s);
+        launch_blend_mode<0>(b, grid, s, fixup);
     else if (b.mode == 1)
-        launch_blend_mode<1>(b, grid, s);
+        launch_blend_mode<1>(b, grid, s, fixup);
     else
-        launch_blend_mode<2>(b, grid, s);
+        launch_blend_mode<2>(b, grid, s, fixup);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_continue(const BlendArgs &b, cudaStream_t s) {
+    BlendArgs c = b;
+    c.pv.source = 3;
+    if (b.mode == 0)
+        blend_kernel<0, 3><<<148 * SN_BLEND_MIN_BLOCKS, kBT, 0, s>>>(c);
+    else if (b.mode == 1)
+        blend_kernel<1, 3><<<148 * SN_BLEND_MIN_BLOCKS, kBT, 0, s>>>(c);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fixup(const BlendArgs &b, cudaStream_t s) {
+    if (b.mode == 0)
+        fixup_kernel<0><<<kFixupBlocks, 256, 0, s>>>(b);
+    else if (b.mode == 1)
+        fixup_kernel<1><<<kFixupBlocks, 256, 0, s>>>(b);
     return cudaGetLastError();
 }
 

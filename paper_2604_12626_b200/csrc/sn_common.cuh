@@ -114,6 +114,16 @@ __device__ __forceinline__ GatheredSplat gather_splat(const BlendGeo *geo, const
     return g;
 }
 
+// A far splat of a depth-sliced scene pass (sn_render_opts.near_slice): its gaussian, its env in
+// the chunk and the tiles its support can reach. Only the tiles whose near list ran out with live
+// pixels ever look at it (the far buckets); it is re-projected there.
+struct __align__(16) FarRec {
+    uint32_t gid;
+    uint32_t env;
+    ushort4 rect;  // tight rectangle (x0, x1, y0, y1), or (0xffff, 0, 0xffff, 0) when it reaches no pixel
+};
+static_assert(sizeof(FarRec) == 16, "FarRec must stay 16 bytes");
+
 __host__ __device__ inline int tiles_of(int px) { return (px + kTile - 1) / kTile; }
 
 // numpy.maximum(x, 0.0) / numpy.clip: NaN propagates (fmax would drop it)

@@ -47,9 +47,21 @@ struct PrepArgs {
     uint64_t z_base;
     int32_t z_bits;
     uint64_t cap;              // capacity of the per-splat buffers (writes past it are dropped)
+    // depth slicing (scene pass, sn_render_opts.near_slice): z_cut (ec, device) per env -- visible
+    // items with z < z_cut are near (full records, depth-sorted, streamed by the blend), the rest
+    // far (FarRec, bucketed by tile only for tiles whose near list runs out); null = no slicing.
+    // blk_counts then has 2 ec rows (near, far) and env_off 2 ec + 1 entries.
+    const double *z_cut;
+    uint64_t *nearmask;        // (n) bit e: visible and near in env e0 + e
+    FarRec *far;
+    uint64_t cap_f;
 };
 
 // sn_preprocess.cu
+// per-env depth cuts of a sliced scene pass: z_cut[e] = the `frac` quantile of the z of a strided
+// sample of the gaussians inside env e's view cone (+inf: no slicing for that env)
+cudaError_t launch_near_cut(const sn_cloud &c, const PrepArgs &a, double frac, bool all_envs, double *z_cut,
+                            cudaStream_t s);
 cudaError_t launch_scene_count(const sn_cloud &c, const PrepArgs &a, cudaStream_t s);
 cudaError_t launch_scene_emit(const sn_cloud &c, const PrepArgs &a, cudaStream_t s);
 cudaError_t launch_avatar_count(const sn_avatars &av, const PoseView &pv, const PrepArgs &a, cudaStream_t s);
@@ -71,6 +83,32 @@ cudaError_t launch_avatar_cull(const sn_avatars &av, const PoseView &pv, const d
                                int32_t n_envs, unsigned long long *ext, uint8_t *codes, cudaStream_t s);
 cudaError_t launch_joint_prep(const sn_avatars &av, int32_t avatar, const double *pose_q, const double *pose_t,
                               double *joint_mats, double *eff_q, double *root, cudaStream_t s);
+
+// sn_far.cu (+ launch_far_project in sn_preprocess.cu): the far buckets of a depth-sliced pass
+struct FarArgs {
+    int32_t e0, ec, tiles_x, n_tiles;
+    const uint64_t *env_off;   // (2 ec + 1): far items are [env_off[ec], env_off[2 ec]) (relative)
+    const FarRec *far;
+    uint64_t cap_f;
+    const int32_t *bucket_of;  // (ec * n_tiles): unfinished-tile index, or -1
+    uint32_t *bcount;          // (cap_u) bucket sizes
+    uint64_t *boff;            // (cap_u + 1) bucket offsets (exclusive scan of bcount)
+    uint32_t *bfill;           // (cap_u) scatter cursors
+    const uint64_t *n_items;   // device: total bucket items (boff[U])
+    uint32_t *items;           // (cap_b) far index per bucket item
+    uint32_t *item_bucket;     // (cap_b) bucket per item
+    uint64_t cap_b;
+    SplatRec *brec;            // (cap_b) the re-projected splat per item
+    BlendGeo *bgeo;            // (cap_b)
+    uint32_t *zkey;            // (cap_b) top 32 bits of (bits(z) - z_base)
+    uint64_t z_base;
+    int32_t z_bits;
+};
+cudaError_t launch_far_count(const FarArgs &f, cudaStream_t s);
+cudaError_t launch_far_scatter(const FarArgs &f, cudaStream_t s);
+cudaError_t launch_far_project(const sn_cloud &c, const sn_camera *cams, const FarArgs &f, cudaStream_t s);
+cudaError_t launch_far_bucket_keys(const FarArgs &f, const uint32_t *order, uint32_t *keys, cudaStream_t s);
+cudaError_t launch_far_tie_fix(const FarArgs &f, const uint32_t *bkeys, uint32_t *order, cudaStream_t s);
 
 // sn_bin.cu
 struct BinArgs {
@@ -103,12 +141,16 @@ cudaError_t launch_depth_tie_fix(const BinArgs &b, cudaStream_t s);
 cudaError_t launch_super_rects(const BinArgs &b, ushort4 *super_rects, cudaStream_t s);
 cudaError_t launch_duplicate(const BinArgs &b, cudaStream_t s);
 cudaError_t launch_ranges(const BinArgs &b, const uint32_t *keys_sorted, cudaStream_t s);
-cudaError_t launch_publish_counts(const uint64_t *v, const uint64_t *p, uint64_t *mapped_dst, cudaStream_t s);
+constexpr int kCountWords = 5;  // published per (chunk, pass): visible, pairs, far, unfinished, bucket items
+cudaError_t launch_publish_counts(const uint64_t *v, const uint64_t *p, const uint64_t *f_lo, const uint64_t *f_hi,
+                                  const unsigned long long *u, const uint64_t *b, uint64_t *mapped_dst,
+                                  cudaStream_t s);
 
 // sn_sort.cu (counts in device memory, grids sized by capacity)
 size_t sort_temp_bytes(uint64_t cap);
 bool radix_sort_pairs(void *temp, uint32_t *k0, uint32_t *v0, uint32_t *k1, uint32_t *v1, const uint64_t *d_n,
-                      uint64_t cap, int bits, cudaStream_t s, int64_t *launches, bool identity_values = false);
+                      uint64_t cap, int bits, cudaStream_t s, int64_t *launches, bool identity_values = false,
+                      const uint32_t *k_in = nullptr);
 size_t scan_temp_bytes_dev(uint64_t cap);
 cudaError_t scan_u32_to_u64(void *temp, const uint32_t *in, const uint64_t *d_n, uint64_t cap, uint64_t *out,
                             uint64_t *total_out, cudaStream_t s, int64_t *launches);
@@ -137,7 +179,29 @@ struct PassView {
     const uint32_t *tile_list;
     const uint32_t *n_list;
     uint32_t *list_next;
+    // depth slicing (scene pass, source 0): env_off has 2 ec + 1 entries (near rows, then far rows);
+    // the tiles whose near list ran out with live / undecided pixels continue in their far bucket
+    int32_t ec;
+    int32_t sliced;
+    int32_t n_tiles;
+    const int32_t *far_bucket_of;           // (ec * n_tiles): bucket (unfinished tile) index, or -1
+    const uint64_t *far_boff;               // (cap_u + 1)
+    const uint32_t *far_order;              // bucket items in depth order (item index)
+    const SplatRec *far_recs;               // per item
+    const BlendGeo *far_geo;                // per item
+    const uint32_t *far_unfin_list;         // (cap_u): el << 16 | tile
+    const unsigned long long *far_unfin;    // unfinished tiles registered (device)
+    const uint64_t *far_items;              // bucket items (device)
+    uint32_t far_cap_u;
+    uint64_t cap_f, far_cap_b;
+    uint32_t *far_next;                     // the continuation's work counter
 };
+// A sliced pass whose far half outgrew its buffers (far items, unfinished tiles or bucket items): the
+// continuation and the fixups do nothing (the host re-runs the render with larger buffers).
+__device__ __forceinline__ bool far_overflow(const PassView &v) {
+    return v.sliced && (v.env_off[2 * v.ec] - v.env_off[v.ec] > v.cap_f || *v.far_unfin > v.far_cap_u ||
+                        *v.far_items > v.far_cap_b);
+}
 __device__ __forceinline__ bool pass_overflow(const PassView &v) {
     return *v.d_nvis > v.cap_v || (v.source == 1 && *v.d_npairs > v.cap_p);
 }
@@ -164,9 +228,18 @@ struct BlendArgs {
     unsigned long long *loads;  // device counter: records gathered into shared memory (may be null)
     unsigned long long *scans;  // device counter: rectangles examined by source-0 tiles (may be null)
     unsigned long long *contribs;  // device counter: (pixel, splat) contributions (may be null)
+    // depth slicing: where an unfinished tile registers and saves its pixels' state (source 0 blend)
+    unsigned long long *unfin_count;
+    uint32_t *unfin_list;
+    int32_t *bucket_of;
+    float *state;           // (cap_u, kStateF, kBT)
 };
+constexpr int kBT = 128;     // scene blend threads per tile (two pixels each, sn_blend.cu)
+constexpr int kStateF = 22;  // floats per blend thread of a saved tile (2 pixels)
 constexpr int kFixupBlocks = 148 * 4;
-cudaError_t launch_blend(const BlendArgs &b, cudaStream_t s);  // blend (+ fixup for modes 0, 1)
+cudaError_t launch_blend(const BlendArgs &b, cudaStream_t s, bool fixup = true);  // blend (+ fixup, modes 0, 1)
+cudaError_t launch_continue(const BlendArgs &b, cudaStream_t s);  // sliced pass: the unfinished tiles' far walk
+cudaError_t launch_fixup(const BlendArgs &b, cudaStream_t s);     // modes 0, 1: the float64 fixups
 cudaError_t launch_layer_composite(const BlendArgs &b, cudaStream_t s);  // mode 2: composite + fixup
 cudaError_t fast_exp_selftest(double *max_rel_err);
 // harness export of the streamed (source 0) tile lists of env el: counts (offsets == null) or entries

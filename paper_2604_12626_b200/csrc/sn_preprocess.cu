@@ -81,10 +81,17 @@ __device__ __forceinline__ void tally(unsigned (*s_cnt)[5], int e, int code, boo
     }
 }
 
-__device__ __forceinline__ void flush_counts(unsigned (*s_cnt)[5], const PrepArgs &a) {
+__device__ __forceinline__ void flush_counts(unsigned (*s_cnt)[5], const PrepArgs &a, const unsigned *s_near = nullptr) {
     __syncthreads();
     int t = threadIdx.x;
-    if (t < a.ec) a.blk_counts[(int64_t)t * a.n_blocks + blockIdx.x] = s_cnt[t][4];
+    if (t < a.ec) {
+        if (s_near) {  // depth-sliced: rows e (near) and ec + e (far)
+            a.blk_counts[(int64_t)t * a.n_blocks + blockIdx.x] = s_near[t];
+            a.blk_counts[(int64_t)(a.ec + t) * a.n_blocks + blockIdx.x] = s_cnt[t][4] - s_near[t];
+        } else {
+            a.blk_counts[(int64_t)t * a.n_blocks + blockIdx.x] = s_cnt[t][4];
+        }
+    }
     if (a.stats != nullptr) {
         for (int i = t; i < a.ec * 5; i += blockDim.x) {  // ec * 5 can exceed the block (64 envs: 320)
             int e = i / 5, f = i % 5;  // sn_stats field order: input, depth, frame, degenerate, drawn
@@ -128,6 +135,26 @@ __device__ __forceinline__ void warp_offsets(uint64_t mask, int ec, unsigned (*s
     __syncthreads();
 }
 
+// The tiles whose pixel centres the support {d2 <= 9} can reach: its bounding box mean +- (hx, hy)
+// (BlendGeo, float, widened far beyond its rounding), intersected with the reference rectangle
+// (3 sqrt(lambda_max) circle, renderer.py:83-86, which contains the ellipse). The reference's
+// tile lists hold the other tiles of the rectangle too, but no pixel there passes d2 <= 9, so the
+// blend and the exact walks skip them; the harness CSR views still report the reference lists.
+__device__ __forceinline__ ushort4 tight_rect(const Geo &geo, const BlendGeo &bg, const int rect[4]) {
+    int t0 = rect[0], t1 = rect[1], t2 = rect[2], t3 = rect[3];
+    if (bg.hx < 1e30f && bg.hy < 1e30f) {
+        const double ex = (double)bg.hx * (1.0 + 1e-5) + 1e-3, ey = (double)bg.hy * (1.0 + 1e-5) + 1e-3;
+        // pixel p has its centre p + 0.5 inside [m - e, m + e] iff p in [m - e - 0.5, m + e - 0.5]
+        t0 = max(t0, (int)floor((geo.mx - ex - 0.5) / kTile));
+        t1 = min(t1, (int)floor((geo.mx + ex - 0.5) / kTile));
+        t2 = max(t2, (int)floor((geo.my - ey - 0.5) / kTile));
+        t3 = min(t3, (int)floor((geo.my + ey - 0.5) / kTile));
+    }
+    return t0 <= t1 && t2 <= t3 ? make_ushort4((unsigned short)t0, (unsigned short)t1, (unsigned short)t2,
+                                               (unsigned short)t3)
+                                : make_ushort4(0xffff, 0, 0xffff, 0);  // reaches no pixel
+}
+
 __device__ __forceinline__ void write_splat(const PrepArgs &a, int64_t pos, int e, const Geo &geo, double alpha,
                                             const float rgb[3], uint32_t gid) {
     if ((uint64_t)pos >= a.cap) return;  // overflow: the host re-runs the pass with larger buffers
@@ -153,23 +180,7 @@ __device__ __forceinline__ void write_splat(const PrepArgs &a, int64_t pos, int 
     if (a.rects)
         a.rects[pos] = make_ushort4((unsigned short)rect[0], (unsigned short)rect[1], (unsigned short)rect[2],
                                     (unsigned short)rect[3]);
-    // The tiles whose pixel centres the support {d2 <= 9} can reach: its bounding box mean +- (hx, hy)
-    // (BlendGeo, float, widened far beyond its rounding), intersected with the reference rectangle
-    // (3 sqrt(lambda_max) circle, renderer.py:83-86, which contains the ellipse). The reference's
-    // tile lists hold the other tiles of the rectangle too, but no pixel there passes d2 <= 9, so the
-    // blend and the exact walks skip them; the harness CSR views still report the reference lists.
-    int t0 = rect[0], t1 = rect[1], t2 = rect[2], t3 = rect[3];
-    if (bg.hx < 1e30f && bg.hy < 1e30f) {
-        const double ex = (double)bg.hx * (1.0 + 1e-5) + 1e-3, ey = (double)bg.hy * (1.0 + 1e-5) + 1e-3;
-        // pixel p has its centre p + 0.5 inside [m - e, m + e] iff p in [m - e - 0.5, m + e - 0.5]
-        t0 = max(t0, (int)floor((geo.mx - ex - 0.5) / kTile));
-        t1 = min(t1, (int)floor((geo.mx + ex - 0.5) / kTile));
-        t2 = max(t2, (int)floor((geo.my - ey - 0.5) / kTile));
-        t3 = min(t3, (int)floor((geo.my + ey - 0.5) / kTile));
-    }
-    a.rects_tight[pos] = t0 <= t1 && t2 <= t3 ? make_ushort4((unsigned short)t0, (unsigned short)t1, (unsigned short)t2,
-                                                             (unsigned short)t3)
-                                              : make_ushort4(0xffff, 0, 0xffff, 0);  // reaches no pixel
+    a.rects_tight[pos] = tight_rect(geo, bg, rect);
 }
 
 // ------------------------------------------------------------------------------- scene
@@ -232,7 +243,15 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
     __shared__ unsigned long long s_vis[kBlock];
     __shared__ uint16_t s_q[kBlock / 32][32 * kCountRound];
     __shared__ sn_camera s_cam[kMaxEnvChunk];
+    __shared__ unsigned long long s_nearbits[kBlock];  // depth slicing: visible and z < z_cut
+    __shared__ unsigned s_near[kMaxEnvChunk];
+    __shared__ double s_zcut[kMaxEnvChunk];
     stage_cams(a, s_cam);
+    if (threadIdx.x < a.ec) {
+        s_near[threadIdx.x] = 0u;
+        s_zcut[threadIdx.x] = a.z_cut ? a.z_cut[threadIdx.x] : INFINITY;
+    }
+    s_nearbits[threadIdx.x] = 0ull;
     init_counts(s_cnt, a.ec);  // (synchronizes)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
@@ -284,30 +303,47 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
             // field: 2 frame, 3 degenerate, 4 drawn (sn_stats order)
             const int field = code == kKeep ? 4 : (code == kDegenerate ? 3 : 2);
             tally_item(s_cnt, active, e, field);
-            if (code == kKeep) atomicOr(&s_vis[warp * 32 + l], 1ull << e);
+            if (code == kKeep) {
+                atomicOr(&s_vis[warp * 32 + l], 1ull << e);
+                if (geo.z < s_zcut[e]) atomicOr(&s_nearbits[warp * 32 + l], 1ull << e);
+            }
         }
         __syncwarp();
     }
     __syncthreads();
     if (valid) a.vismask[g] = s_vis[threadIdx.x];
     (void)g0;
-    flush_counts(s_cnt, a);
+    if (a.z_cut) {  // near items per env of this block
+        const uint64_t nb = s_nearbits[threadIdx.x];
+        if (valid) a.nearmask[g] = nb;
+        for (int e = 0; e < a.ec; ++e) {
+            const unsigned bal = __ballot_sync(kFull, (nb >> e) & 1ull);
+            if (lane == 0 && bal) atomicAdd(&s_near[e], __popc(bal));
+        }
+        flush_counts(s_cnt, a, s_near);
+    } else {
+        flush_counts(s_cnt, a);
+    }
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kBlock, SN_EMIT_MIN_BLOCKS) scene_emit_kernel(sn_cloud c, PrepArgs a) {
     __shared__ unsigned s_woff[kMaxEnvChunk][kBlock / 32];
+    __shared__ unsigned s_woff_far[kMaxEnvChunk][kBlock / 32];
     __shared__ double s_geo[kBlock][10];  // position (3), cov3d (6), alpha
     __shared__ uint16_t s_q[kBlock / 32][32 * kEmitRound];
     __shared__ sn_camera s_cam[kMaxEnvChunk];
     stage_cams(a, s_cam);
     int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     bool valid = g < c.n;
-    uint64_t mask = valid ? a.vismask[g] : 0ull;
+    const uint64_t vis = valid ? a.vismask[g] : 0ull;
+    const uint64_t near_bits = (valid && a.z_cut) ? a.nearmask[g] : ~0ull;
+    const uint64_t mask = vis & near_bits, mask_far = vis & ~near_bits;
     warp_offsets(mask, a.ec, s_woff);  // (synchronizes)
-    if (!__any_sync(kFull, mask != 0)) return;
+    if (a.z_cut) warp_offsets(mask_far, a.ec, s_woff_far);
+    if (!__any_sync(kFull, vis != 0)) return;
     const int warp = threadIdx.x >> 5;
-    if (mask) {
+    if (vis) {
         double p[3], ls[3], q[4], opacity, cov[6];
         load_scene<T>(c, g, p, ls, q, opacity);
         build_cov3d(ls, q, cov);
@@ -338,6 +374,34 @@ __global__ void __launch_bounds__(kBlock, SN_EMIT_MIN_BLOCKS) scene_emit_kernel(
             view_dir(p, cam, dir);
             eval_sh_f32(c.sh, c.n, g0 + l, c.sh_k, dir[0], dir[1], dir[2], rgb);
             write_splat(a, pos, e, geo, d[9], rgb, (uint32_t)(g0 + l));
+        }
+        __syncwarp();
+    }
+    if (!a.z_cut) return;
+    // far items (depth-sliced pass): the gaussian, its env and its tight rectangle -- no colour, no
+    // 64-byte records, no sort; re-projected only by the tiles whose near list runs out
+    const uint64_t far_base = a.env_off[a.ec];
+    for (int eb = 0; eb < a.ec; eb += kEmitRound) {
+        const int n = build_round(mask_far, eb, min(eb + kEmitRound, a.ec), q);
+        for (int k = threadIdx.x & 31; k < n; k += 32) {
+            const unsigned it = q[k];
+            const int l = it & 31, e = (it >> 5) & 63, rank = it >> 11;
+            const double *d = s_geo[warp * 32 + l];
+            const double p[3] = {d[0], d[1], d[2]};
+            const double cov[6] = {d[3], d[4], d[5], d[6], d[7], d[8]};
+            const uint64_t pos = a.env_off[a.ec + e] - far_base +
+                                 a.blk_counts[(int64_t)(a.ec + e) * a.n_blocks + blockIdx.x] + s_woff_far[e][warp] + rank;
+            if (pos >= a.cap_f) continue;  // overflow: the host re-runs with larger buffers
+            Geo geo;
+            project_geo(p, cov, s_cam[e], geo);
+            const BlendGeo bg = make_blend_geo(geo.ca, 2.0 * geo.cb, geo.cc);  // as write_splat
+            int rect[4];
+            tile_rect(geo.mx, geo.my, geo.radius, a.tiles_x, a.tiles_y, rect);
+            FarRec fr;
+            fr.gid = (uint32_t)(g0 + l);
+            fr.env = (uint32_t)e;
+            fr.rect = tight_rect(geo, bg, rect);
+            a.far[pos] = fr;
         }
         __syncwarp();
     }
@@ -628,6 +692,92 @@ __global__ void __launch_bounds__(kBlock) skin_kernel(sn_avatars av, int64_t g0,
     out_rot[4 * i + 3] = q[3];
 }
 
+// ------------------------------------------------------------------------------- depth slicing
+
+// z_cut per env of the chunk: the `frac` quantile of the depth of a strided sample of the gaussians
+// inside the env's view cone (camera-space |x| <= z (cx + 64) / fx, same for y, near < z < far: a
+// cheap stand-in for the visible set), from a 64-bins-per-octave log histogram. Envs with too few
+// expected visible splats for slicing to pay get +inf (everything near).
+constexpr int kCutBins = 1024;
+constexpr int kCutPerOctave = 64;
+constexpr double kMinSliced = 131072.0;  // expected visible splats below which an env is not sliced
+template <typename T>
+__global__ void __launch_bounds__(kBlock) near_cut_kernel(sn_cloud c, PrepArgs a, int64_t stride, double frac,
+                                                         double min_visible, double *z_cut) {
+    __shared__ unsigned s_h[kCutBins];
+    const sn_camera cam = a.cams[a.e0 + blockIdx.x];
+    for (int i = threadIdx.x; i < kCutBins; i += kBlock) s_h[i] = 0u;
+    __syncthreads();
+    const double lnear = log2(cam.near_);
+    const double mx = (cam.cx + 64.0) / cam.fx, my = (cam.cy + 64.0) / cam.fy;
+    for (int64_t g = (int64_t)threadIdx.x * stride; g < c.n; g += (int64_t)kBlock * stride) {
+        double v[4];
+        load4<T>(static_cast<const T *>(c.pos_opacity) + 4 * g, v);
+        const double p[3] = {v[0], v[1], v[2]};
+        const double *w = cam.rot;
+        const double z = dot3_fma(p[0], p[1], p[2], w[6], w[7], w[8]) + cam.trans[2];
+        if (!(z > cam.near_ && z < cam.far_)) continue;
+        const double x = dot3_fma(p[0], p[1], p[2], w[0], w[1], w[2]) + cam.trans[0];
+        const double y = dot3_fma(p[0], p[1], p[2], w[3], w[4], w[5]) + cam.trans[1];
+        if (fabs(x) > z * mx || fabs(y) > z * my) continue;
+        const int bin = min(kCutBins - 1, max(0, (int)((log2(z) - lnear) * kCutPerOctave)));
+        atomicAdd(&s_h[bin], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t tot = 0;
+        for (int i = 0; i < kCutBins; ++i) tot += s_h[i];
+        double cut = INFINITY;
+        if (tot > 0 && (double)tot * (double)stride >= min_visible) {
+            const double target = frac * (double)tot;
+            uint64_t run = 0;
+            for (int i = 0; i < kCutBins; ++i) {
+                run += s_h[i];
+                if ((double)run >= target) {
+                    cut = exp2(lnear + (double)(i + 1) / kCutPerOctave);
+                    break;
+                }
+            }
+            if (!(cut < cam.far_)) cut = INFINITY;
+        }
+        z_cut[blockIdx.x] = cut;
+    }
+}
+
+// One bucket item of a sliced pass (sn_far.cu): the far splat re-projected exactly as the emit
+// projects a near one -- SplatRec, BlendGeo and its 32-bit depth key.
+template <typename T>
+__global__ void __launch_bounds__(kBlock, SN_EMIT_MIN_BLOCKS) far_project_kernel(sn_cloud c, const sn_camera *cams,
+                                                                                FarArgs f) {
+    const uint64_t n = min(*f.n_items, f.cap_b);
+    const uint64_t i = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n) return;
+    const FarRec fr = f.far[f.items[i]];
+    const int64_t g = fr.gid;
+    double p[3], ls[3], q[4], opacity, cov[6];
+    load_scene<T>(c, g, p, ls, q, opacity);
+    build_cov3d(ls, q, cov);
+    const sn_camera &cam = cams[f.e0 + (int)fr.env];
+    Geo geo;
+    project_geo(p, cov, cam, geo);  // kKeep: the same computation the count kernel kept it with
+    float dir[3], rgb[3];
+    view_dir(p, cam, dir);
+    eval_sh_f32(c.sh, c.n, g, c.sh_k, dir[0], dir[1], dir[2], rgb);
+    SplatRec r;
+    r.mx = geo.mx;
+    r.my = geo.my;
+    r.ca = geo.ca;
+    r.cb2 = 2.0 * geo.cb;
+    r.cc = geo.cc;
+    r.alpha = sigmoid(opacity);
+    r.z = geo.z;
+    r.rgb = pack_rgb21(rgb);
+    f.brec[i] = r;
+    f.bgeo[i] = make_blend_geo(r.ca, r.cb2, r.cc);
+    const unsigned long long off = (unsigned long long)__double_as_longlong(geo.z) - f.z_base;
+    f.zkey[i] = (uint32_t)(f.z_bits > 32 ? off >> (f.z_bits - 32) : off << (32 - f.z_bits));
+}
+
 // Per-env exclusive scan of the per-block visible counts (in place), then env offsets.
 constexpr int kScanThreads = 1024;
 __global__ void __launch_bounds__(kScanThreads) block_scan_kernel(uint32_t *blk_counts, int32_t n_blocks,
@@ -715,6 +865,27 @@ cudaError_t launch_avatar_count(const sn_avatars &av, const PoseView &pv, const 
 
 cudaError_t launch_avatar_emit(const sn_avatars &av, const PoseView &pv, const PrepArgs &a, cudaStream_t s) {
     avatar_emit_kernel<<<a.n_blocks, kBlock, 0, s>>>(av, pv, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_near_cut(const sn_cloud &c, const PrepArgs &a, double frac, bool all_envs, double *z_cut,
+                            cudaStream_t s) {
+    const int64_t stride = std::max<int64_t>(1, c.n / 65536);  // ~64k samples per env
+    const double min_visible = all_envs ? 0.0 : kMinSliced;
+    if (c.dtype == SN_FLOAT64)
+        near_cut_kernel<double><<<a.ec, kBlock, 0, s>>>(c, a, stride, frac, min_visible, z_cut);
+    else
+        near_cut_kernel<float><<<a.ec, kBlock, 0, s>>>(c, a, stride, frac, min_visible, z_cut);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_far_project(const sn_cloud &c, const sn_camera *cams, const FarArgs &f, cudaStream_t s) {
+    if (f.cap_b == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, (f.cap_b + kBlock - 1) / kBlock);
+    if (c.dtype == SN_FLOAT64)
+        far_project_kernel<double><<<grid, kBlock, 0, s>>>(c, cams, f);
+    else
+        far_project_kernel<float><<<grid, kBlock, 0, s>>>(c, cams, f);
     return cudaGetLastError();
 }
 

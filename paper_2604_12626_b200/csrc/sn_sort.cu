@@ -299,11 +299,13 @@ size_t sort_temp_bytes(uint64_t cap) {
 }
 
 // Sorts (keys, values) by the low `bits` key bits, stably; n = min(*d_n, cap) (identity_values: the
-// values are the positions 0..n-1 and v0 is never read). Passes alternate
+// values are the positions 0..n-1 and v0 is never read; k_in: pass 0 reads the keys there and k0 is
+// scratch). Passes alternate
 // between the two buffer pairs starting with (k0, v0) -> (k1, v1); returns true when the sorted
 // result ends in (k1, v1) (odd pass count), false when it is back in (k0, v0).
 bool radix_sort_pairs(void *temp, uint32_t *k0, uint32_t *v0, uint32_t *k1, uint32_t *v1, const uint64_t *d_n,
-                      uint64_t cap, int bits, cudaStream_t s, int64_t *launches, bool identity_values) {
+                      uint64_t cap, int bits, cudaStream_t s, int64_t *launches, bool identity_values,
+                      const uint32_t *k_in) {
     if (cap == 0 || bits <= 0) return false;
     const int passes = (bits + 7) / 8;
     const int dbits = (bits + passes - 1) / passes;
@@ -313,11 +315,12 @@ bool radix_sort_pairs(void *temp, uint32_t *k0, uint32_t *v0, uint32_t *k1, uint
     uint32_t *ks = k0, *vs = v0, *kd = k1, *vd = v1;
     for (int p = 0; p < passes; ++p) {
         const uint32_t *vin = (p == 0 && identity_values) ? nullptr : vs;  // pass 0: values = positions
+        const uint32_t *kin = (p == 0 && k_in) ? k_in : ks;  // pass 0 may read the keys from elsewhere
         const int shift = p * dbits;
         const int db = std::min(dbits, bits - shift);
-        sort_upsweep<<<n_tiles, kSortThreads, 0, s>>>(ks, d_n, cap, shift, db, hist, n_tiles);
+        sort_upsweep<<<n_tiles, kSortThreads, 0, s>>>(kin, d_n, cap, shift, db, hist, n_tiles);
         sort_rowscan<<<1 << db, kRowThreads, 0, s>>>(hist, n_tiles, totals);
-        sort_downsweep<<<n_tiles, kSortThreads, 0, s>>>(ks, vin, kd, vd, d_n, cap, shift, db, hist, totals, n_tiles);
+        sort_downsweep<<<n_tiles, kSortThreads, 0, s>>>(kin, vin, kd, vd, d_n, cap, shift, db, hist, totals, n_tiles);
         if (launches) *launches += 3;
         std::swap(ks, kd);
         std::swap(vs, vd);

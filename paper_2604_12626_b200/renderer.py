@@ -58,7 +58,8 @@ def _nonempty(c):
 
 def render_frames(scene, cameras, background, layer=None, avatars=None, sim_times=None, tiled=True,
                   context=None, contrib=False, stats=True, avatar_active=None, stage_ms=None, work=None,
-                  binning=-1, exact=False, out=None, wait=True, payload=False, serialize=False, views=True):
+                  binning=-1, exact=False, out=None, wait=True, payload=False, serialize=False, views=True,
+                  near_slice=-1):
     """One sn_render call over E cameras. Returns a dict of device tensors:
     color (E,H,W,3), alpha (E,H,W), depth (E,H,W) float32; stats (E,5) int64; optionally
     contrib_scene / contrib_layer (E,H,W) int32 and, with payload=True, the observation payload
@@ -68,7 +69,9 @@ def render_frames(scene, cameras, background, layer=None, avatars=None, sim_time
     after context.render_wait() for it returns False. serialize=True runs the avatar layer after
     the scene pass on the same stream (per-stage timers then add up to the render). views=False
     is the lean throughput path: the render keeps nothing for the harness views that need each
-    splat's gaussian id or reference rectangle (pass_intermediates, tile_csr)."""
+    splat's gaussian id or reference rectangle (pass_intermediates, tile_csr). near_slice: depth
+    slicing of the scene pass (-1 auto: scenes of >= 2M gaussians without views; 0 off; 1 on) --
+    the same frames, only each env's near depth slice sorted (see include/splatnav_b200.h)."""
     lib = N.load()
     ctx = context or N.default_context()
     dscene = DeviceCloud.wrap(scene)
@@ -93,6 +96,7 @@ def render_frames(scene, cameras, background, layer=None, avatars=None, sim_time
     opts.exact = 1 if exact else 0
     opts.serialize = 1 if serialize else 0
     opts.views = 1 if views else 0
+    opts.near_slice = int(near_slice)
     if payload:
         opts.rgb8 = out["rgb8"].data_ptr()
         opts.depth16 = out["depth16"].data_ptr()

@@ -20,6 +20,9 @@ from paper_2604_12626_b200.batch import BatchRenderer
 from paper_2604_12626_b200.renderer import render_frames
 
 
+NEAR_SLICE = int(os.environ.get("SN_SWEEP_NEAR_SLICE", "-1"))  # -1 auto, 0 off, 1 on, 2..1000 forced fraction
+
+
 def point(config, n, a, e, near=0.1, steps=3, warm=2, seed=0):
     box = S.room_box(n)
     scene = S.make_scene(n, box[0], box[1], seed=seed)
@@ -31,7 +34,7 @@ def point(config, n, a, e, near=0.1, steps=3, warm=2, seed=0):
     stage = np.zeros(2 * len(N.STAGES))
     work = np.zeros(12, dtype=np.int64)
     for s in range(warm + steps):  # untimed: grows the workspace to fit every timed step's views
-        br.render(*sets[s])
+        br.render(*sets[s], views=False, near_slice=NEAR_SLICE)
     torch.cuda.synchronize()
     shapes = {"color": (e, 480, 640, 3), "alpha": (e, 480, 640), "depth": (e, 480, 640)}
     outs = [{k: torch.empty(v, device="cuda") for k, v in shapes.items()} for _ in range(2)]
@@ -39,7 +42,8 @@ def point(config, n, a, e, near=0.1, steps=3, warm=2, seed=0):
     def run(s, wait, **kw):
         cams, times = sets[s]
         return render_frames(br.scene, cams, br.background, avatars=br.avatars, sim_times=times if a else None,
-                             context=br.context, stats=False, out=dict(outs[s % 2]), wait=wait, views=False, **kw)
+                             context=br.context, stats=False, out=dict(outs[s % 2]), wait=wait, views=False,
+                             near_slice=NEAR_SLICE, **kw)
 
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -65,10 +69,10 @@ def point(config, n, a, e, near=0.1, steps=3, warm=2, seed=0):
     names = list(N.STAGES)
     g = lambda p, *ks: float(sum(st[p, names.index(k)] for k in ks))
     w = work.reshape(2, 6) / steps
-    return {"config": config, "n_gaussians": n, "n_avatars": a, "envs": e, "near": near,
+    return {"config": config, "n_gaussians": n, "n_avatars": a, "envs": e, "near": near, "near_slice": NEAR_SLICE,
             "frames_per_s": e / (ms / 1e3), "ms_per_step": ms,
             "stage_ms": {"preprocess": g(0, "count", "scan", "emit"), "sort": g(0, "depth_sort", "permute"),
-                         "blend": g(0, "blend"),
+                         "blend": g(0, "blend"), "far": g(0, "far"),
                          "avatar_layer": g(1, "pose", "count", "scan", "emit", "depth_sort", "permute",
                                            "pair_scan", "bin_count", "bin_scatter", "ranges", "blend"),
                          "avatar_layer_preprocess": g(1, "pose", "count", "scan", "emit"),
