@@ -71,7 +71,14 @@ int bit_length(uint64_t v) { return v == 0 ? 0 : 64 - __builtin_clzll(v); }
 // Depth slicing (sn_render_opts.near_slice): auto-on for scenes of at least this many gaussians
 // (rendered without harness views); the near slice is this quantile of each env's sampled depths
 // (SN_NEAR_FRAC overrides it, for tuning).
-constexpr int64_t kSliceMinGaussians = 2000000;
+// auto slicing (near_slice = -1) from this scene size up; SN_SLICE_MIN overrides (tuning)
+int64_t slice_min_gaussians() {
+    static const int64_t m = [] {
+        const char *e = std::getenv("SN_SLICE_MIN");
+        return e ? (int64_t)std::atoll(e) : (int64_t)500000;
+    }();
+    return m;
+}
 double near_frac() {
     static const double f = [] {
         const char *e = std::getenv("SN_NEAR_FRAC");
@@ -91,15 +98,14 @@ struct PassWs {
     Buf vismask, blk_counts, env_off, keys_un, keys_s, vals_un, vals_s, recs_un, geo_un, gid_un, rects_un, rects_tun, rects,
         tiles, pair_off, pkeys_a, pkeys_b, pvals_a, pvals_b, ranges, temp, batch_rects, super_rects, fix, counts, tlist,
         tlist_cnt;
-    // depth slicing (scene pass): cuts, near bits, far splats, unfinished tiles and their state,
-    // far buckets (offsets, items, re-projected records, sort buffers)
-    Buf zcut, nearmask, far, fctl, unfin_list, bucket_of, state, bcount, boff, bfill, items, item_bucket, brec, bgeo,
-        bkey_a, bkey_b, bval_a, bval_b, ftemp, zk;
-    uint64_t cap_f = 0, cap_b = 0;  // far splats, bucket items
+    // depth slicing (scene pass): cuts, near bits, control words, unfinished tiles and their state,
+    // far records of the splats reaching them, bucket items (sort buffers) and bucket ranges
+    Buf zcut, nearmask, fctl, unfin_list, bucket_of, state, frec, fgeo, fgid, franges, bkey_a, bkey_b, bval_a,
+        bval_b, ftemp;
+    uint64_t cap_f = 0, cap_b = 0;  // far records, bucket items
     uint32_t cap_u = 0;             // unfinished tiles
     int32_t sliced = 0;
-    uint32_t *far_order = nullptr;  // where the bucket sort left the final item order
-    uint32_t *far_bkeys = nullptr;  // and the matching bucket keys
+    uint32_t *far_order = nullptr;  // where the bucket sort left the item order (far record indices)
     uint64_t cap_v = 0, cap_p = 0;  // capacities of the per-splat / per-pair buffers
     // metadata of the last chunk rendered by this pass
     int32_t e0 = 0, ec = 0, tiles_x = 0, tiles_y = 0, tile_bits = 0, tiled = 1, valid = 0, binning = 0, views = 1;
@@ -151,6 +157,8 @@ struct sn_context {
     cudaEvent_t ev_inputs = nullptr, ev_scene = nullptr, ev_layer = nullptr;
     int64_t launches = 0;  // kernels of this library launched through the context
     int64_t retries = 0;   // renders re-run because a pass outgrew its buffers
+    bool slice_off_next = false;  // renders run unsliced until one goes through (a sliced one set far_short)
+    int64_t slice_fallbacks = 0;  // sliced renders re-run unsliced that way
     double *ms_dst[2][SN_N_STAGES] = {};
     int64_t *work_dst[2] = {};
     bool have_events = false;
@@ -240,16 +248,18 @@ PassView view_of(const PassWs &w) {
     v.n_tiles = w.tiles_x * w.tiles_y;
     v.sliced = w.sliced;
     if (w.sliced) {
-        // fctl words: [0] unfinished tiles, [1] bucket items, [2] continuation work counter
+        // control words: see kFarCtl (sn_internal.h)
         v.far_bucket_of = w.bucket_of.as<int32_t>();
-        v.far_boff = w.boff.as<uint64_t>();
+        v.far_ranges = w.franges.as<uint2>();
         v.far_order = w.far_order;
-        v.far_recs = w.brec.as<SplatRec>();
-        v.far_geo = w.bgeo.as<BlendGeo>();
+        v.far_recs = w.frec.as<SplatRec>();
+        v.far_geo = w.fgeo.as<BlendGeo>();
         v.far_unfin_list = w.unfin_list.as<uint32_t>();
         v.far_unfin = w.fctl.as<unsigned long long>();
-        v.far_items = w.fctl.as<uint64_t>() + 1;
+        v.far_items = w.fctl.as<unsigned long long>() + 1;
+        v.far_nrec = w.fctl.as<unsigned long long>() + 4;
         v.far_next = reinterpret_cast<uint32_t *>(w.fctl.as<uint64_t>() + 2);
+        v.far_short = w.fctl.as<unsigned long long>() + 3;
         v.far_cap_u = w.cap_u;
         v.cap_f = w.cap_f;
         v.far_cap_b = w.cap_b;
@@ -281,7 +291,8 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     const int views = opts ? opts->views : 1;
     const int want_slice = opts ? opts->near_slice : -1;
     const bool slice = sp.scene && sp.mode != 2 && tiled && binning == 0 && !(opts && opts->exact) &&
-                       (want_slice >= 1 || (want_slice < 0 && !views && n >= kSliceMinGaussians));
+                       !ctx->slice_off_next &&
+                       (want_slice >= 1 || (want_slice < 0 && !views && n >= slice_min_gaussians()));
     const double slice_frac = want_slice >= 2 ? std::min(1.0, want_slice / 1000.0) : near_frac();
     const bool slice_all = want_slice >= 2;  // every env sliced, however few splats it sees
     const int rows = slice ? 2 * ec : ec;  // per-(env, block) counts: near rows, then far rows
@@ -344,14 +355,15 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     a.cap = cap_v;
     w.sliced = slice ? 1 : 0;
     if (slice) {
-        if (w.cap_u == 0) w.cap_u = 2048;  // grown (with cap_f, cap_b) by render_check on overflow
+        // starting capacities of the far half (~70 MB), grown by render_check on overflow: sized so the
+        // occasional unfinished tiles of a fresh camera set do not cost a re-render
+        if (w.cap_u == 0) w.cap_u = 4096;
+        if (w.cap_f == 0) w.cap_f = 1u << 18;
+        if (w.cap_b == 0) w.cap_b = 1u << 20;
         SN_ENSURE(w.zcut, sizeof(double) * ec);
         SN_ENSURE(w.nearmask, sizeof(uint64_t) * std::max<int64_t>(n, 1));
-        SN_ENSURE(w.far, sizeof(FarRec) * (w.cap_f + 1));
         a.z_cut = w.zcut.as<double>();
         a.nearmask = w.nearmask.as<uint64_t>();
-        a.far = w.far.as<FarRec>();
-        a.cap_f = w.cap_f;
     }
 
     if (n > 0) {
@@ -477,8 +489,9 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     w.tile_bits = tile_bits;
     w.tiled = tiled;
     w.binning = binning;
-    SN_ENSURE(w.fix, sizeof(uint32_t) * (size_t)ec * width * height);
-    SN_ENSURE(ctx->fixcnt, 2 * sizeof(unsigned));
+    // (a sliced pass may queue a pixel twice: the first fixup pass defers the ones needing a far bucket)
+    SN_ENSURE(w.fix, sizeof(uint32_t) * (size_t)ec * width * height * (slice ? 2 : 1));
+    SN_ENSURE(ctx->fixcnt, 4 * sizeof(unsigned));  // per pass: count, then [2 + pass] the second pass's start
     BlendArgs bl{};
     bl.cams = ctx->cams.as<sn_camera>();
     bl.e0 = e0;
@@ -533,39 +546,30 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
         bl.laerr = ctx->laerr.as<float>();
         bl.tile_flag = ctx->tile_flag.as<uint8_t>();
     }
-    // the bucket sort's id width and pass parity (both slice blocks below)
-    const int ub = std::max(1, bit_length((uint64_t)w.cap_u));
-    const bool u_odd = ((ub + 7) / 8) % 2 == 1;
-    if (slice) {  // unfinished-tile registry (the blend) and the far-bucket buffers (after it)
-        const size_t cu = w.cap_u, cb = w.cap_b;
-        SN_ENSURE(w.fctl, 4 * sizeof(uint64_t));
+    const int ub = std::max(1, bit_length((uint64_t)w.cap_u));  // bucket-id bits of the far item keys
+    if (slice) {  // unfinished-tile registry (the blend) and the far buffers (after it)
+        const size_t cu = w.cap_u, cb = w.cap_b, cf = w.cap_f;
+        SN_ENSURE(w.fctl, kFarCtl * sizeof(uint64_t));
         SN_ENSURE(w.unfin_list, sizeof(uint32_t) * cu);
         SN_ENSURE(w.bucket_of, sizeof(int32_t) * (size_t)ec * n_tiles);
         SN_ENSURE(w.state, sizeof(float) * cu * kStateF * kBT);
-        SN_ENSURE(w.bcount, sizeof(uint32_t) * (cu + 1));
-        SN_ENSURE(w.boff, sizeof(uint64_t) * (cu + 1));
-        SN_ENSURE(w.bfill, sizeof(uint32_t) * (cu + 1));
-        SN_ENSURE(w.items, sizeof(uint32_t) * (cb + 1));
-        SN_ENSURE(w.item_bucket, sizeof(uint32_t) * (cb + 1));
-        SN_ENSURE(w.zk, sizeof(uint32_t) * (cb + 1));
-        SN_ENSURE(w.brec, sizeof(SplatRec) * (cb + 1));
-        SN_ENSURE(w.bgeo, sizeof(BlendGeo) * (cb + 1));
+        SN_ENSURE(w.franges, sizeof(uint2) * cu);
+        SN_ENSURE(w.frec, sizeof(SplatRec) * (cf + 1));
+        SN_ENSURE(w.fgeo, sizeof(BlendGeo) * (cf + 1));
+        SN_ENSURE(w.fgid, sizeof(uint32_t) * (cf + 1));
         SN_ENSURE(w.bkey_a, sizeof(uint32_t) * (cb + 1));
         SN_ENSURE(w.bkey_b, sizeof(uint32_t) * (cb + 1));
         SN_ENSURE(w.bval_a, sizeof(uint32_t) * (cb + 1));
         SN_ENSURE(w.bval_b, sizeof(uint32_t) * (cb + 1));
-        SN_ENSURE(w.ftemp, std::max({sort_temp_bytes(cb), scan_temp_bytes_dev(cu)}));
-        SN_CUDA(cudaMemsetAsync(w.fctl.p, 0, 4 * sizeof(uint64_t), st));
+        SN_ENSURE(w.ftemp, sort_temp_bytes(cb));
+        SN_CUDA(cudaMemsetAsync(w.fctl.p, 0, kFarCtl * sizeof(uint64_t), st));
         SN_CUDA(cudaMemsetAsync(w.bucket_of.p, 0xff, sizeof(int32_t) * (size_t)ec * n_tiles, st));
-        SN_CUDA(cudaMemsetAsync(w.bcount.p, 0, sizeof(uint32_t) * (cu + 1), st));
-        SN_CUDA(cudaMemsetAsync(w.bfill.p, 0, sizeof(uint32_t) * (cu + 1), st));
-        // The bucket order: a stable sort by the 32-bit z key (4 passes, ends in (bkey_a, bval_a)),
-        // then a stable sort by bucket id ((bkey_b, bval_a) -> ..., ub bits): the final values are in
-        // bval_b after an odd number of passes, bval_a after an even one.
-        w.far_order = u_odd ? w.bval_b.as<uint32_t>() : w.bval_a.as<uint32_t>();
-        w.far_bkeys = u_odd ? w.bkey_a.as<uint32_t>() : w.bkey_b.as<uint32_t>();
+        SN_CUDA(cudaMemsetAsync(w.franges.p, 0, sizeof(uint2) * cu, st));
+        // the item sort is 4 radix passes of 8 bits: the order ends where it started (bkey_a, bval_a)
+        w.far_order = w.bval_a.as<uint32_t>();
         bl.pv = view_of(w);
         bl.unfin_count = w.fctl.as<unsigned long long>();
+        bl.unfin_envs = w.fctl.as<unsigned long long>() + 5;
         bl.unfin_list = w.unfin_list.as<uint32_t>();
         bl.bucket_of = w.bucket_of.as<int32_t>();
         bl.state = w.state.as<float>();
@@ -577,49 +581,53 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     if (slice) {
         // the far buckets of the unfinished tiles, the continuation, then the fixups (sn_far.cu)
         tm.begin(SN_STAGE_FAR);
+        // first fixup pass over the near lists (the buckets do not exist yet): a pixel whose float64
+        // walk needs its tile's far bucket registers the tile (if the blend did not) and is queued
+        // again for the second pass below
+        // (the second pass starts where the blend's entries end: the deferred ones come after them)
+        unsigned *fix_start = ctx->fixcnt.as<unsigned>() + 2 + pass_id;
+        SN_CUDA(cudaMemcpyAsync(fix_start, bl.fix_count, sizeof(unsigned), cudaMemcpyDeviceToDevice, st));
+        BlendArgs fa = bl;
+        fa.pv.far_phase = 1;
+        ctx->launches += 1;
+        SN_CUDA(launch_fixup(fa, st));
         FarArgs f{};
         f.e0 = e0;
         f.ec = ec;
         f.tiles_x = tiles_x;
         f.n_tiles = n_tiles;
-        f.env_off = w.env_off.as<uint64_t>();
-        f.far = w.far.as<FarRec>();
-        f.cap_f = w.cap_f;
+        f.ub = ub;
+        f.vismask = w.vismask.as<uint64_t>();
+        f.nearmask = w.nearmask.as<uint64_t>();
+        f.cams = ctx->cams.as<sn_camera>();
         f.bucket_of = w.bucket_of.as<int32_t>();
-        f.bcount = w.bcount.as<uint32_t>();
-        f.boff = w.boff.as<uint64_t>();
-        f.bfill = w.bfill.as<uint32_t>();
-        f.n_items = w.fctl.as<uint64_t>() + 1;
-        f.items = w.items.as<uint32_t>();
-        f.item_bucket = w.item_bucket.as<uint32_t>();
+        f.fctl = w.fctl.as<unsigned long long>();
+        f.recs = w.frec.as<SplatRec>();
+        f.geo = w.fgeo.as<BlendGeo>();
+        f.gid = w.fgid.as<uint32_t>();
+        f.cap_f = w.cap_f;
+        f.keys = w.bkey_a.as<uint32_t>();
+        f.vals = w.bval_a.as<uint32_t>();
         f.cap_b = w.cap_b;
-        f.brec = w.brec.as<SplatRec>();
-        f.bgeo = w.bgeo.as<BlendGeo>();
-        f.zkey = w.zk.as<uint32_t>();
+        f.ranges = w.franges.as<uint2>();
         f.z_base = z_base;
         f.z_bits = z_bits;
-        ctx->launches += 3;
-        SN_CUDA(launch_far_count(f, st));
-        SN_CUDA(scan_u32_to_u64(w.ftemp.p, w.bcount.as<uint32_t>(), w.fctl.as<uint64_t>(), w.cap_u,
-                                w.boff.as<uint64_t>(), w.fctl.as<uint64_t>() + 1, st, &ctx->launches));
-        SN_CUDA(launch_far_scatter(f, st));
-        SN_CUDA(launch_far_project(*sp.scene, ctx->cams.as<sn_camera>(), f, st));
-        const bool z_odd = radix_sort_pairs(w.ftemp.p, w.bkey_a.as<uint32_t>(), w.bval_a.as<uint32_t>(),
-                                            w.bkey_b.as<uint32_t>(), w.bval_b.as<uint32_t>(), f.n_items, w.cap_b, 32,
-                                            st, &ctx->launches, /*identity_values=*/true, w.zk.as<uint32_t>());
-        SN_CHECK(!z_odd, "far bucket sort: 32-bit keys take an even number of passes");
+        ctx->launches += 1;
+        SN_CUDA(launch_far_collect(*sp.scene, f, n, st));
+        const bool odd = radix_sort_pairs(w.ftemp.p, w.bkey_a.as<uint32_t>(), w.bval_a.as<uint32_t>(),
+                                          w.bkey_b.as<uint32_t>(), w.bval_b.as<uint32_t>(),
+                                          w.fctl.as<uint64_t>() + 1, w.cap_b, 32, st, &ctx->launches);
+        SN_CHECK(!odd, "far item sort: 32-bit keys take an even number of passes");
         ctx->launches += 2;
-        SN_CUDA(launch_far_bucket_keys(f, w.bval_a.as<uint32_t>(), w.bkey_b.as<uint32_t>(), st));
-        const bool b_odd = radix_sort_pairs(w.ftemp.p, w.bkey_b.as<uint32_t>(), w.bval_a.as<uint32_t>(),
-                                            w.bkey_a.as<uint32_t>(), w.bval_b.as<uint32_t>(), f.n_items, w.cap_b, ub,
-                                            st, &ctx->launches);
-        SN_CHECK(b_odd == u_odd, "far bucket sort parity");
-        SN_CUDA(launch_far_tie_fix(f, w.far_bkeys, w.far_order, st));
+        SN_CUDA(launch_far_tie_fix(f, w.bkey_a.as<uint32_t>(), w.bval_a.as<uint32_t>(), st));
+        SN_CUDA(launch_far_ranges(f, w.bkey_a.as<uint32_t>(), st));
         BlendArgs cb2 = bl;
         cb2.pv = view_of(w);
         ctx->launches += 2;
         SN_CUDA(launch_continue(cb2, st));
-        SN_CUDA(launch_fixup(cb2, st));
+        BlendArgs fb = cb2;  // the second fixup pass: the continuation's pixels and the deferred ones
+        fb.fix_start = fix_start;
+        SN_CUDA(launch_fixup(fb, st));
         bl = cb2;
         tm.end();
     }
@@ -636,11 +644,9 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     }
     // this chunk's (V, P) into mapped host memory: sn_render checks them against the capacities
     ctx->launches += 1;
-    SN_CUDA(launch_publish_counts(
-        d_nvis, w.counts.as<uint64_t>() + 1, slice ? w.env_off.as<uint64_t>() + ec : nullptr,
-        slice ? w.env_off.as<uint64_t>() + 2 * ec : nullptr, slice ? w.fctl.as<unsigned long long>() : nullptr,
-        slice ? w.fctl.as<uint64_t>() + 1 : nullptr,
-        ctx->slot[ctx->cur].d_counts + kCountWords * (2 * chunk_idx + pass_id), st));
+    SN_CUDA(launch_publish_counts(d_nvis, w.counts.as<uint64_t>() + 1,
+                                  slice ? w.fctl.as<unsigned long long>() : nullptr,
+                                  ctx->slot[ctx->cur].d_counts + kCountWords * (2 * chunk_idx + pass_id), st));
     w.valid = 1;
     return SN_OK;
 }
@@ -904,6 +910,11 @@ static int render_check(sn_context *ctx, int32_t *retry) {
             const uint64_t v = h[0], q = h[1];
             need_v = std::max(need_v, v);
             need_p = std::max(need_p, q);
+            if (h[5]) {  // a float64 walk ran out of a near list with no far bucket: re-run unsliced
+                if (!ctx->slice_off_next) ctx->slice_fallbacks += 1;
+                ctx->slice_off_next = true;
+                grow = true;
+            }
             need_f = std::max(need_f, h[2]);
             need_u = std::max(need_u, h[3]);
             need_b = std::max(need_b, h[4]);
@@ -931,8 +942,11 @@ static int render_check(sn_context *ctx, int32_t *retry) {
             grow = true;
         }
         if (need_u > S->cap_u[p]) {
-            SN_CHECK(need_u < (1u << 16), "too many unfinished tiles in one env chunk (limit 65535)");
-            w.cap_u = (uint32_t)std::min<uint64_t>(65535, std::max<uint64_t>(w.cap_u, need_u + need_u / 4 + 256));
+            // <= one per (env, tile) of the chunk, so this bounds itself; the state is 11 KB per tile
+            SN_CHECK(need_u < (1u << 24), "too many unfinished tiles in one env chunk (limit 2^24)");
+            w.cap_u = (uint32_t)std::max<uint64_t>(w.cap_u, need_u + need_u / 4 + 256);
+            // the bucket items were counted for the registered tiles only: scale the estimate
+            if (S->cap_u[p] > 0) need_b = need_b / S->cap_u[p] * need_u + need_b % S->cap_u[p] * need_u / S->cap_u[p];
             grow = true;
         }
         if (need_b > S->cap_b[p]) {
@@ -946,6 +960,7 @@ static int render_check(sn_context *ctx, int32_t *retry) {
             S->work[6 * p + 1] += (int64_t)sum_p;
         }
     }
+    if (!grow) ctx->slice_off_next = false;  // (a far-short fallback holds until a render goes through)
     if (grow) {
         // larger buffers: drop the partial work counters of the failed attempt
         resolve_all(ctx);
@@ -972,7 +987,9 @@ int sn_render(sn_context *ctx, const sn_cloud *scene, const sn_cloud *layer, con
     SN_CHECK(ctx != nullptr, "null context");
     SN_CHECK(!ctx->slot[0].pending && !ctx->slot[1].pending,
              "renders queued with sn_render_async are in flight: call sn_render_wait first");
-    for (int attempt = 0; attempt < 3; ++attempt) {
+    // a sliced pass can discover its capacities in stages (splats and pairs, then the unfinished
+    // tiles, then their bucket items): a few re-runs at most
+    for (int attempt = 0; attempt < 6; ++attempt) {
         int r = render_queue(ctx, scene, layer, avatars, cams, sim_times, n_envs, opts, color, alpha, depth, stream);
         if (r != SN_OK) return r;
         int32_t retry = 0;
@@ -1463,3 +1480,26 @@ int sn_composite(int64_t npix, const double *front_color, const double *front_al
 }
 
 }  // extern "C"
+
+// Diagnostic (not part of the ABI): the last scene pass's depth-slicing control words -- unfinished
+// tiles registered, far bucket items -- read synchronously, and the sliced renders re-run unsliced.
+extern "C" int sn_debug_slice_counts(sn_context *ctx, uint64_t *out) {
+    SN_CHECK(ctx != nullptr && out != nullptr, "null argument");
+    out[0] = out[1] = 0;
+    out[2] = (uint64_t)ctx->slice_fallbacks;
+    const PassWs &w = ctx->pass[0];
+    if (!w.sliced || !w.fctl.p) return SN_OK;
+    SN_CUDA(cudaDeviceSynchronize());
+    SN_CUDA(cudaMemcpy(out, w.fctl.p, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    return SN_OK;
+}
+
+// Test hook (not part of the ABI): the starting capacities of the scene pass's far half (unfinished
+// tiles, far records, bucket items), so a test can force their growth path.
+extern "C" int sn_debug_far_caps(sn_context *ctx, uint32_t cap_u, uint64_t cap_f, uint64_t cap_b) {
+    SN_CHECK(ctx != nullptr && cap_u > 0 && cap_f > 0 && cap_b > 0, "bad argument");
+    ctx->pass[0].cap_u = cap_u;
+    ctx->pass[0].cap_f = cap_f;
+    ctx->pass[0].cap_b = cap_b;
+    return SN_OK;
+}

@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(kBlock) duplicate_kernel(BinArgs b) {
         uint32_t span = (uint32_t)(r.y - r.x + 1);
         uint32_t tx = r.x + local % span, ty = r.z + local / span;
         uint32_t tile = ty * (uint32_t)b.tiles_x + tx;
+        SN_ASSERT(gk < b.cap_p && tile < (uint32_t)(b.tiles_x * b.tiles_y));
         b.pair_keys[gk] = (s_env[lo] << b.tile_bits) | tile;
         b.pair_vals[gk] = b.vals_sorted[i0 + lo];  // the record slot: the blend gathers it directly
     }
@@ -207,19 +208,20 @@ __global__ void __launch_bounds__(kBlock) tie_fix_kernel(BinArgs b) {
 
 // One (chunk, pass)'s sizes into mapped host memory: visible (near) splats, tile pairs and, for a
 // depth-sliced pass, far splats (f_hi - f_lo), unfinished tiles and far bucket items.
-__global__ void publish_counts_kernel(const uint64_t *v, const uint64_t *p, const uint64_t *f_lo, const uint64_t *f_hi,
-                                      const unsigned long long *u, const uint64_t *b, volatile uint64_t *dst) {
+__global__ void publish_counts_kernel(const uint64_t *v, const uint64_t *p, const unsigned long long *fctl,
+                                      volatile uint64_t *dst) {
     dst[0] = *v;
     dst[1] = *p;
-    dst[2] = f_lo ? *f_hi - *f_lo : 0ull;
-    dst[3] = u ? *u : 0ull;
-    dst[4] = b ? *b : 0ull;
+    // a sliced scene pass (control words, kFarCtl): far records, unfinished tiles, bucket items, far-short
+    dst[2] = fctl ? fctl[4] : 0ull;
+    dst[3] = fctl ? fctl[0] : 0ull;
+    dst[4] = fctl ? fctl[1] : 0ull;
+    dst[5] = fctl ? fctl[3] : 0ull;
 }
 
-cudaError_t launch_publish_counts(const uint64_t *v, const uint64_t *p, const uint64_t *f_lo, const uint64_t *f_hi,
-                                  const unsigned long long *u, const uint64_t *b, uint64_t *mapped_dst,
-                                  cudaStream_t s) {
-    publish_counts_kernel<<<1, 1, 0, s>>>(v, p, f_lo, f_hi, u, b, mapped_dst);
+cudaError_t launch_publish_counts(const uint64_t *v, const uint64_t *p, const unsigned long long *fctl,
+                                  uint64_t *mapped_dst, cudaStream_t s) {
+    publish_counts_kernel<<<1, 1, 0, s>>>(v, p, fctl, mapped_dst);
     return cudaGetLastError();
 }
 

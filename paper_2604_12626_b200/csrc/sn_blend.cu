@@ -42,6 +42,8 @@ __device__ unsigned g_env_frac[64];  // per env: largest fraction (1/1000) of th
 
 namespace sn {
 
+__device__ int g_slice_hooks = 0;  // test hooks, see sn_debug_slice_hooks
+
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -429,6 +431,7 @@ __device__ __forceinline__ void push_fixup(const BlendArgs &b, bool flag, uint32
     unsigned base = 0;
     if (lane == __ffs(bal) - 1) base = atomicAdd(b.fix_count, (unsigned)__popc(bal));
     base = __shfl_sync(kFull, base, __ffs(bal) - 1);
+    SN_ASSERT(!flag || base + __popc(bal) <= (unsigned)(b.ec * b.width * b.height));
     if (flag) b.fix_list[base + __popc(bal & ((1u << lane) - 1u))] = code;
 }
 
@@ -468,6 +471,7 @@ __device__ __forceinline__ void stream_fill(const PassView &v, int tx, int ty, i
                 woff += (w < warp) ? c : 0;
                 tot += c;
             }
+            SN_ASSERT(q_len + tot < cap + kBlock);  // callers size the queue cap + kBlock
             if (hit) s_queue[q_len + woff + __popc(bal & ((1u << lane) - 1u))] = i;
             q_len += tot;
             __syncthreads();
@@ -614,8 +618,9 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
                 if (cursor == s1) return;
             }
         } else if (SOURCE == 3) {  // continuation of an unfinished tile: its far bucket, in depth order
-            cursor = (uint32_t)v.far_boff[u];
-            s1 = (uint32_t)v.far_boff[u + 1];
+            const uint2 r = v.far_ranges[u];
+            cursor = r.x;
+            s1 = r.y;
         } else {
             cursor = (uint32_t)v.env_off[el];
             s1 = (uint32_t)v.env_off[el + 1];
@@ -633,6 +638,7 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
         float z_first = 3.0e38f;
         bool entry_live0 = true, entry_live1 = true;  // SOURCE 3: pixels still live when the tile resumed
         if (SOURCE == 3) {  // the state the near walk saved (save_state below)
+            SN_ASSERT(u >= 0 && (uint32_t)u < v.far_cap_u);
             const float *st = b.state + (size_t)u * kStateF * kBT + threadIdx.x;
             f32x2 *f[10] = {&P.T, &P.err, &P.A, &P.cr, &P.cg, &P.cb, &P.D, &P.dead, &P.z_last, &P.nc};
     #pragma unroll
@@ -664,6 +670,7 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
                 const uint32_t rid = SOURCE == 1   ? __ldg(v.pair_vals + cursor + jt)
                                      : SOURCE == 3 ? __ldg(v.far_order + cursor + jt)
                                                    : __ldg(v.order + (SOURCE == 0 ? s_queue[jt] : cursor + jt));
+                SN_ASSERT(SOURCE == 3 ? (uint64_t)rid < v.cap_f : (uint64_t)rid < v.cap_v);
                 const GatheredSplat gs = SOURCE == 3 ? gather_splat(v.far_geo, v.far_recs, rid) : gather_splat(v.geo, v.recs, rid);
                 FRec f;
                 unsigned msk = tile_entry(gs.e1x, gs.e1y, gs.p1, gs.p2, gs.gl, gs.gr, x0 + 8.0, y0 + 8.0, f);
@@ -684,6 +691,7 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
                 cnt += __popc(bal);
             }
             const int cnt_pad = (cnt + kWalkUnroll - 1) / kWalkUnroll * kWalkUnroll;
+            SN_ASSERT(cnt_pad <= kBatch + kWalkUnroll);
             if (lane < cnt_pad - cnt) s_wl[warp][cnt + lane] = (uint16_t)(kBatch * sizeof(FRec));
             __syncwarp();
             // depth bounds of the contributions, once per batch instead of per contribution: the warp's
@@ -817,7 +825,10 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
         // undecided: its float64 walk may need to go on) and far splats in its env registers as
         // unfinished, saves its pixels' state and leaves the live pixels to the continuation (source 3).
         bool saved = false;
-        if (SOURCE == 0 && v.sliced) {
+        // (Only tiles that reached the end of the near list: a tile whose pixels all stopped before it
+        // leaves its undecided pixels' float64 walks the rest of the near list, which ends them but
+        // for a pathological few -- those set far_short and the render is re-run unsliced.)
+        if (SOURCE == 0 && v.sliced && cursor >= s1 && q_len == 0) {
             float Tq[2], Eq[2], Dq[2];
             unpack2(P.T, Tq[0], Tq[1]);
             unpack2(P.err, Eq[0], Eq[1]);
@@ -827,7 +838,7 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
             for (int p = 0; p < 2; ++p) {
                 const bool cutq = Tq[p] - Eq[p] <= kTHi;
                 const bool ambq = cutq && (!(Tq[p] + Eq[p] < kTLo) || Eq[p] > 0.0625f * Tq[p]);
-                need |= (p ? in1 : in0) && (Dq[p] == 0.0f || ambq);
+                need |= (p ? in1 : in0) && (Dq[p] == 0.0f || (ambq && !(g_slice_hooks & 2)));
             }
             const bool has_far = v.env_off[v.ec + el + 1] > v.env_off[v.ec + el];
             if (__syncthreads_or(need) && has_far) {
@@ -835,6 +846,7 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
                     const unsigned long long uu = atomicAdd(b.unfin_count, 1ull);
                     s_u = uu < v.far_cap_u ? (int)uu : -1;
                     if (s_u >= 0) {
+                        atomicOr(b.unfin_envs, 1ull << el);
                         b.unfin_list[s_u] = ((uint32_t)el << 16) | (uint32_t)tile;
                         b.bucket_of[(int64_t)el * (tiles_of(b.width) * tiles_of(b.height)) + tile] = s_u;
                     }
@@ -979,7 +991,8 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
             __syncthreads();
             if ((uint32_t)item >= n_items) break;
             const uint32_t key = v.far_unfin_list[item];
-            do_tile((int)(key & 0xffffu), (int)(key >> 16), item);
+            if (key & kLateTile) continue;  // registered by the first fixup pass: no live pixels
+            do_tile((int)(key & 0xffffu), (int)((key >> 16) & 0xffu), item);
             __syncthreads();  // the next tile reuses the shared buffers
         }
     } else {
@@ -1347,6 +1360,7 @@ struct ExactPixel {
     double A, D, T;
     int nc;
     bool near;  // the cutoff test met a transmittance within 1e-12 (relative) of 1e-4: re-walk with SEQ
+    bool out;   // (far_phase 1) the walk needs the tile's far bucket, not built yet: defer the pixel
 };
 
 // The relative window around 1e-4 inside which the warp prefix product's association (<= ~1e-13
@@ -1418,7 +1432,7 @@ __device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_
     float cr = 0.0f, cg = 0.0f, cb = 0.0f;  // per-lane partial sums, reduced at the end
     double A = 0.0, D = 0.0, T = 1.0;
     int nc = 0, qn = 0;
-    bool done = false, near = false;
+    bool done = false, near = false, out = false;
     auto consume = [&](int m) {  // the first m <= 32 queued contributions
         const bool act = lane < m;
         QEntry e{};
@@ -1456,10 +1470,17 @@ __device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_
     const bool far = sgm == 1;
     if (far) {
         if (!v.sliced || done || near) break;
+        if (v.far_phase == 1) {  // first fixup pass: the buckets come later -- defer (if there is a far half)
+            out = v.env_off[v.ec + el + 1] > v.env_off[v.ec + el];
+            break;
+        }
         const int32_t ub = v.far_bucket_of[(int64_t)el * v.n_tiles + tile];
-        if (ub < 0) break;
-        cur = (uint32_t)v.far_boff[ub];
-        end = (uint32_t)v.far_boff[ub + 1];
+        if (ub < 0) {  // unregistered: the env has no far splats, or the tile stopped inside its near list
+            if (lane == 0 && v.env_off[v.ec + el + 1] > v.env_off[v.ec + el]) atomicExch(v.far_short, 1ull);
+            break;
+        }
+        cur = v.far_ranges[ub].x;
+        end = v.far_ranges[ub].y;
     }
     while (cur < end && !done && !near) {
         uint32_t step;
@@ -1553,7 +1574,8 @@ __device__ ExactPixel exact_walk(const PassView &v, int el, int tile, int tiles_
         A += __shfl_xor_sync(kFull, A, d);
         D += __shfl_xor_sync(kFull, D, d);
     }
-    return ExactPixel{cr, cg, cb, A, D, T, (int)__reduce_add_sync(kFull, (unsigned)nc), near};
+    if (v.sliced && (g_slice_hooks & 1) && lane == 0) atomicExch(v.far_short, 1ull);
+    return ExactPixel{cr, cg, cb, A, D, T, (int)__reduce_add_sync(kFull, (unsigned)nc), near, out};
 }
 
 // exact_walk, then -- only when its cutoff test met a transmittance within kNearCut of 1e-4 -- the
@@ -1632,9 +1654,12 @@ __device__ ExactPixel exact_walk_cta(const PassView &v, int el, int tile, int ti
     if (far) {
         if (!v.sliced || s_flag[0]) break;  // s_flag[0]: the walk already stopped (uniform)
         const int32_t ub = v.far_bucket_of[(int64_t)el * v.n_tiles + tile];
-        if (ub < 0) break;
-        cur = (uint32_t)v.far_boff[ub];
-        end = (uint32_t)v.far_boff[ub + 1];
+        if (ub < 0) {  // as in exact_walk
+            if (threadIdx.x == 0 && v.env_off[v.ec + el + 1] > v.env_off[v.ec + el]) atomicExch(v.far_short, 1ull);
+            break;
+        }
+        cur = v.far_ranges[ub].x;
+        end = v.far_ranges[ub].y;
     }
     while (cur < end) {
         uint32_t step;
@@ -1844,10 +1869,11 @@ __global__ void __launch_bounds__(256, SN_FIXUP_MIN_BLOCKS) fixup_kernel(BlendAr
     QEntry *q = s_q[threadIdx.x >> 5];
     if (pass_overflow(b.pv) || far_overflow(b.pv) || (MODE == 2 && (pass_overflow(b.back) || far_overflow(b.back))))
         return;
-    const unsigned n_fix = *b.fix_count;
+    const unsigned n_fix = *b.fix_count, i0 = b.fix_start ? *b.fix_start : 0u;
     const unsigned hw = (unsigned)b.width * (unsigned)b.height;
     unsigned long long contribs = 0;
-    for (unsigned i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_fix; i += (gridDim.x * blockDim.x) >> 5) {
+    for (unsigned i = i0 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < n_fix;
+         i += (gridDim.x * blockDim.x) >> 5) {
         const uint32_t code = b.fix_list[i];
         const int el = (int)(code / hw), p = (int)(code % hw);
         const int py_i = p / b.width, px_i = p % b.width;
@@ -1856,6 +1882,26 @@ __global__ void __launch_bounds__(256, SN_FIXUP_MIN_BLOCKS) fixup_kernel(BlendAr
         const sn_camera &cam = b.cams[env];
         // mode 2 fixups are few and each walks long, unsaturated lists: more gathers in flight
         const ExactPixel f = exact_pixel<MODE == 2 ? 8 : SN_FIXUP_PER>(b.pv, el, tile, b.tiles_x, px_i, py_i, s_exp, q);
+        if (MODE != 2 && f.out) {
+            // (sliced pass, first fixup pass) the walk needs the tile's far bucket: register the tile
+            // if the blend did not (late: no saved state, the continuation skips it) and queue the
+            // pixel again for the second fixup pass, which walks near list + bucket
+            if (lane == 0) {
+                int32_t *bo = b.bucket_of + (int64_t)el * b.pv.n_tiles + tile;
+                if (atomicCAS(bo, -1, -2) == -1) {
+                    const unsigned long long u = atomicAdd(b.unfin_count, 1ull);
+                    if (u < b.pv.far_cap_u) {
+                        b.unfin_list[u] = kLateTile | ((uint32_t)el << 16) | (uint32_t)tile;
+                        atomicOr(b.unfin_envs, 1ull << el);
+                        atomicExch(bo, (int32_t)u);
+                    }  // (overflow: the render is re-run with more room)
+                }
+                const unsigned slot = atomicAdd(b.fix_count, 1u);
+                SN_ASSERT(slot < 2u * (unsigned)b.ec * hw);
+                b.fix_list[slot] = code;
+            }
+            continue;
+        }
         contribs += (unsigned)f.nc;
         const int64_t pix = ((int64_t)env * b.height + py_i) * b.width + px_i;
         const double alpha = f.A < 1.0 ? f.A : 1.0;
@@ -2106,6 +2152,15 @@ cudaError_t fast_exp_selftest(double *max_rel_err) {
 }
 
 }  // namespace sn
+
+// Test hooks (not part of the ABI) for the rare paths of a sliced pass, which the tests check give
+// identical frames: bit 0 -- every float64 walk sets far_short as if it had run out of a near list
+// with no bucket, so the render is re-run unsliced; bit 1 -- the blend does not register tiles for
+// their undecided pixels alone, so those pixels' walks are deferred by the first fixup pass, which
+// registers their tiles late.
+extern "C" int sn_debug_slice_hooks(int bits) {
+    return cudaMemcpyToSymbol(sn::g_slice_hooks, &bits, sizeof(int)) == cudaSuccess ? 0 : 1;
+}
 
 #ifdef SN_BLEND_PROF
 extern "C" int sn_debug_blend_prof(unsigned long long *out, int reset) {

@@ -9,10 +9,27 @@
 
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cstdio>
 
 #include "../../include/splatnav_b200.h"
 
 namespace sn {
+
+// Device-side bounds checks of the build variant compiled with -DSN_CHECKS (the sanitizer tools are
+// unavailable on the GPU pool): a failed check prints its location and traps the kernel, which
+// surfaces as a CUDA error from the render. Compiled out otherwise.
+#ifdef SN_CHECKS
+#define SN_ASSERT(cond)                                                                               \
+    do {                                                                                              \
+        if (!(cond)) {                                                                                \
+            printf("SN_ASSERT failed: %s at %s:%d (block %d,%d thread %d)\n", #cond, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)blockIdx.y, (int)threadIdx.x);                               \
+            __trap();                                                                                 \
+        }                                                                                             \
+    } while (0)
+#else
+#define SN_ASSERT(cond) ((void)0)
+#endif
 
 constexpr int kTile = 16;
 constexpr int kBlock = 256;
@@ -113,16 +130,6 @@ __device__ __forceinline__ GatheredSplat gather_splat(const BlendGeo *geo, const
                        lh.w);
     return g;
 }
-
-// A far splat of a depth-sliced scene pass (sn_render_opts.near_slice): its gaussian, its env in
-// the chunk and the tiles its support can reach. Only the tiles whose near list ran out with live
-// pixels ever look at it (the far buckets); it is re-projected there.
-struct __align__(16) FarRec {
-    uint32_t gid;
-    uint32_t env;
-    ushort4 rect;  // tight rectangle (x0, x1, y0, y1), or (0xffff, 0, 0xffff, 0) when it reaches no pixel
-};
-static_assert(sizeof(FarRec) == 16, "FarRec must stay 16 bytes");
 
 __host__ __device__ inline int tiles_of(int px) { return (px + kTile - 1) / kTile; }
 

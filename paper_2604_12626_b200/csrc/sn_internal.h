@@ -49,12 +49,11 @@ struct PrepArgs {
     uint64_t cap;              // capacity of the per-splat buffers (writes past it are dropped)
     // depth slicing (scene pass, sn_render_opts.near_slice): z_cut (ec, device) per env -- visible
     // items with z < z_cut are near (full records, depth-sorted, streamed by the blend), the rest
-    // far (FarRec, bucketed by tile only for tiles whose near list runs out); null = no slicing.
-    // blk_counts then has 2 ec rows (near, far) and env_off 2 ec + 1 entries.
+    // far (not emitted: projected again by far_collect, and only where a tile's near list runs out
+    // with live pixels); null = no slicing. blk_counts then has 2 ec rows (near, far) and env_off
+    // 2 ec + 1 entries.
     const double *z_cut;
     uint64_t *nearmask;        // (n) bit e: visible and near in env e0 + e
-    FarRec *far;
-    uint64_t cap_f;
 };
 
 // sn_preprocess.cu
@@ -84,31 +83,32 @@ cudaError_t launch_avatar_cull(const sn_avatars &av, const PoseView &pv, const d
 cudaError_t launch_joint_prep(const sn_avatars &av, int32_t avatar, const double *pose_q, const double *pose_t,
                               double *joint_mats, double *eff_q, double *root, cudaStream_t s);
 
-// sn_far.cu (+ launch_far_project in sn_preprocess.cu): the far buckets of a depth-sliced pass
+// sn_far.cu (+ launch_far_collect in sn_preprocess.cu): the far buckets of a depth-sliced pass.
+// Control words of a sliced pass (u64, PassWs::fctl): [0] unfinished tiles registered, [1] bucket
+// items, [2] the continuation's work counter, [3] far-short flag, [4] far records written, [5] mask
+// of the envs (in chunk) with unfinished tiles.
+constexpr int kFarCtl = 8;
 struct FarArgs {
     int32_t e0, ec, tiles_x, n_tiles;
-    const uint64_t *env_off;   // (2 ec + 1): far items are [env_off[ec], env_off[2 ec]) (relative)
-    const FarRec *far;
+    int32_t ub;                     // bucket-id bits at the top of the 32-bit item keys
+    const uint64_t *vismask;        // (n) visible envs per gaussian
+    const uint64_t *nearmask;       // (n) of those, the envs where it is in the near slice
+    const sn_camera *cams;
+    const int32_t *bucket_of;       // (ec * n_tiles): unfinished-tile index, or -1
+    unsigned long long *fctl;       // control words (above)
+    SplatRec *recs;                 // (cap_f) far splats that reach an unfinished tile: records,
+    BlendGeo *geo;                  //   blend geometry
+    uint32_t *gid;                  //   and gaussian index (the tie fix's second key)
     uint64_t cap_f;
-    const int32_t *bucket_of;  // (ec * n_tiles): unfinished-tile index, or -1
-    uint32_t *bcount;          // (cap_u) bucket sizes
-    uint64_t *boff;            // (cap_u + 1) bucket offsets (exclusive scan of bcount)
-    uint32_t *bfill;           // (cap_u) scatter cursors
-    const uint64_t *n_items;   // device: total bucket items (boff[U])
-    uint32_t *items;           // (cap_b) far index per bucket item
-    uint32_t *item_bucket;     // (cap_b) bucket per item
+    uint32_t *keys, *vals;          // (cap_b) bucket items: bucket << (32 - ub) | z key >> ub, far record
     uint64_t cap_b;
-    SplatRec *brec;            // (cap_b) the re-projected splat per item
-    BlendGeo *bgeo;            // (cap_b)
-    uint32_t *zkey;            // (cap_b) top 32 bits of (bits(z) - z_base)
+    uint2 *ranges;                  // (cap_u) each bucket's item range after the sort (zeroed)
     uint64_t z_base;
     int32_t z_bits;
 };
-cudaError_t launch_far_count(const FarArgs &f, cudaStream_t s);
-cudaError_t launch_far_scatter(const FarArgs &f, cudaStream_t s);
-cudaError_t launch_far_project(const sn_cloud &c, const sn_camera *cams, const FarArgs &f, cudaStream_t s);
-cudaError_t launch_far_bucket_keys(const FarArgs &f, const uint32_t *order, uint32_t *keys, cudaStream_t s);
-cudaError_t launch_far_tie_fix(const FarArgs &f, const uint32_t *bkeys, uint32_t *order, cudaStream_t s);
+cudaError_t launch_far_collect(const sn_cloud &c, const FarArgs &f, int64_t n, cudaStream_t s);
+cudaError_t launch_far_tie_fix(const FarArgs &f, const uint32_t *keys, uint32_t *vals, cudaStream_t s);
+cudaError_t launch_far_ranges(const FarArgs &f, const uint32_t *keys, cudaStream_t s);
 
 // sn_bin.cu
 struct BinArgs {
@@ -141,10 +141,10 @@ cudaError_t launch_depth_tie_fix(const BinArgs &b, cudaStream_t s);
 cudaError_t launch_super_rects(const BinArgs &b, ushort4 *super_rects, cudaStream_t s);
 cudaError_t launch_duplicate(const BinArgs &b, cudaStream_t s);
 cudaError_t launch_ranges(const BinArgs &b, const uint32_t *keys_sorted, cudaStream_t s);
-constexpr int kCountWords = 5;  // published per (chunk, pass): visible, pairs, far, unfinished, bucket items
-cudaError_t launch_publish_counts(const uint64_t *v, const uint64_t *p, const uint64_t *f_lo, const uint64_t *f_hi,
-                                  const unsigned long long *u, const uint64_t *b, uint64_t *mapped_dst,
-                                  cudaStream_t s);
+constexpr int kCountWords = 6;  // published per (chunk, pass): visible, pairs, far records, unfinished
+                                // tiles, bucket items, far-short flag
+cudaError_t launch_publish_counts(const uint64_t *v, const uint64_t *p, const unsigned long long *fctl,
+                                  uint64_t *mapped_dst, cudaStream_t s);
 
 // sn_sort.cu (counts in device memory, grids sized by capacity)
 size_t sort_temp_bytes(uint64_t cap);
@@ -181,26 +181,32 @@ struct PassView {
     uint32_t *list_next;
     // depth slicing (scene pass, source 0): env_off has 2 ec + 1 entries (near rows, then far rows);
     // the tiles whose near list ran out with live / undecided pixels continue in their far bucket
+    // (the far splats reaching the tile, projected by far_collect, sorted by (z, gaussian index))
     int32_t ec;
     int32_t sliced;
     int32_t n_tiles;
     const int32_t *far_bucket_of;           // (ec * n_tiles): bucket (unfinished tile) index, or -1
-    const uint64_t *far_boff;               // (cap_u + 1)
-    const uint32_t *far_order;              // bucket items in depth order (item index)
-    const SplatRec *far_recs;               // per item
-    const BlendGeo *far_geo;                // per item
+    const uint2 *far_ranges;                // (cap_u) bucket -> item range in far_order
+    const uint32_t *far_order;              // bucket items in depth order (far record index)
+    const SplatRec *far_recs;               // (cap_f) far records
+    const BlendGeo *far_geo;                // (cap_f)
     const uint32_t *far_unfin_list;         // (cap_u): el << 16 | tile
     const unsigned long long *far_unfin;    // unfinished tiles registered (device)
-    const uint64_t *far_items;              // bucket items (device)
+    const unsigned long long *far_items;    // bucket items (device)
+    const unsigned long long *far_nrec;     // far records (device)
     uint32_t far_cap_u;
     uint64_t cap_f, far_cap_b;
     uint32_t *far_next;                     // the continuation's work counter
+    int32_t far_phase;                      // 1: the buckets are not built yet (the first fixup pass):
+                                            // a float64 walk that needs its tile's bucket reports `out`
+    unsigned long long *far_short;          // set by a float64 walk that ran out of a tile's near list
+                                            // with no far bucket to continue in (the render is re-run
+                                            // unsliced)
 };
 // A sliced pass whose far half outgrew its buffers (far items, unfinished tiles or bucket items): the
 // continuation and the fixups do nothing (the host re-runs the render with larger buffers).
 __device__ __forceinline__ bool far_overflow(const PassView &v) {
-    return v.sliced && (v.env_off[2 * v.ec] - v.env_off[v.ec] > v.cap_f || *v.far_unfin > v.far_cap_u ||
-                        *v.far_items > v.far_cap_b);
+    return v.sliced && (*v.far_nrec > v.cap_f || *v.far_unfin > v.far_cap_u || *v.far_items > v.far_cap_b);
 }
 __device__ __forceinline__ bool pass_overflow(const PassView &v) {
     return *v.d_nvis > v.cap_v || (v.source == 1 && *v.d_npairs > v.cap_p);
@@ -220,8 +226,9 @@ struct BlendArgs {
     // splats" flag, all indexed like the outputs
     float *lcolor, *lalpha, *ldepth, *lderr, *laerr;
     uint8_t *tile_flag;
-    uint32_t *fix_list;     // (ec*H*W) pixels deferred to the float64 fixup (el*H*W + pixel)
+    uint32_t *fix_list;     // (ec*H*W, x2 when sliced) pixels deferred to the float64 fixup (el*H*W + pixel)
     unsigned *fix_count;    // device counter, zeroed before the blend
+    const unsigned *fix_start;  // the first entry this fixup pass takes (null: 0; a sliced pass's second)
     int32_t force_exact;    // every pixel to the float64 fixup (sn_render_opts.exact)
     uint8_t *rgb8;          // (E,H,W,3) observation payload colour, or null (written where a pixel is final)
     uint16_t *depth16;      // (E,H,W) fp16 payload depth, or null
@@ -230,10 +237,12 @@ struct BlendArgs {
     unsigned long long *contribs;  // device counter: (pixel, splat) contributions (may be null)
     // depth slicing: where an unfinished tile registers and saves its pixels' state (source 0 blend)
     unsigned long long *unfin_count;
+    unsigned long long *unfin_envs;  // bit el: env el has an unfinished tile
     uint32_t *unfin_list;
     int32_t *bucket_of;
     float *state;           // (cap_u, kStateF, kBT)
 };
+constexpr uint32_t kLateTile = 1u << 31;  // unfinished-list flag: registered by the first fixup pass (no state)
 constexpr int kBT = 128;     // scene blend threads per tile (two pixels each, sn_blend.cu)
 constexpr int kStateF = 22;  // floats per blend thread of a saved tile (2 pixels)
 constexpr int kFixupBlocks = 148 * 4;

@@ -329,7 +329,6 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
 template <typename T>
 __global__ void __launch_bounds__(kBlock, SN_EMIT_MIN_BLOCKS) scene_emit_kernel(sn_cloud c, PrepArgs a) {
     __shared__ unsigned s_woff[kMaxEnvChunk][kBlock / 32];
-    __shared__ unsigned s_woff_far[kMaxEnvChunk][kBlock / 32];
     __shared__ double s_geo[kBlock][10];  // position (3), cov3d (6), alpha
     __shared__ uint16_t s_q[kBlock / 32][32 * kEmitRound];
     __shared__ sn_camera s_cam[kMaxEnvChunk];
@@ -338,12 +337,11 @@ __global__ void __launch_bounds__(kBlock, SN_EMIT_MIN_BLOCKS) scene_emit_kernel(
     bool valid = g < c.n;
     const uint64_t vis = valid ? a.vismask[g] : 0ull;
     const uint64_t near_bits = (valid && a.z_cut) ? a.nearmask[g] : ~0ull;
-    const uint64_t mask = vis & near_bits, mask_far = vis & ~near_bits;
+    const uint64_t mask = vis & near_bits;
     warp_offsets(mask, a.ec, s_woff);  // (synchronizes)
-    if (a.z_cut) warp_offsets(mask_far, a.ec, s_woff_far);
-    if (!__any_sync(kFull, vis != 0)) return;
+    if (!__any_sync(kFull, mask != 0)) return;
     const int warp = threadIdx.x >> 5;
-    if (vis) {
+    if (mask) {
         double p[3], ls[3], q[4], opacity, cov[6];
         load_scene<T>(c, g, p, ls, q, opacity);
         build_cov3d(ls, q, cov);
@@ -377,34 +375,8 @@ __global__ void __launch_bounds__(kBlock, SN_EMIT_MIN_BLOCKS) scene_emit_kernel(
         }
         __syncwarp();
     }
-    if (!a.z_cut) return;
-    // far items (depth-sliced pass): the gaussian, its env and its tight rectangle -- no colour, no
-    // 64-byte records, no sort; re-projected only by the tiles whose near list runs out
-    const uint64_t far_base = a.env_off[a.ec];
-    for (int eb = 0; eb < a.ec; eb += kEmitRound) {
-        const int n = build_round(mask_far, eb, min(eb + kEmitRound, a.ec), q);
-        for (int k = threadIdx.x & 31; k < n; k += 32) {
-            const unsigned it = q[k];
-            const int l = it & 31, e = (it >> 5) & 63, rank = it >> 11;
-            const double *d = s_geo[warp * 32 + l];
-            const double p[3] = {d[0], d[1], d[2]};
-            const double cov[6] = {d[3], d[4], d[5], d[6], d[7], d[8]};
-            const uint64_t pos = a.env_off[a.ec + e] - far_base +
-                                 a.blk_counts[(int64_t)(a.ec + e) * a.n_blocks + blockIdx.x] + s_woff_far[e][warp] + rank;
-            if (pos >= a.cap_f) continue;  // overflow: the host re-runs with larger buffers
-            Geo geo;
-            project_geo(p, cov, s_cam[e], geo);
-            const BlendGeo bg = make_blend_geo(geo.ca, 2.0 * geo.cb, geo.cc);  // as write_splat
-            int rect[4];
-            tile_rect(geo.mx, geo.my, geo.radius, a.tiles_x, a.tiles_y, rect);
-            FarRec fr;
-            fr.gid = (uint32_t)(g0 + l);
-            fr.env = (uint32_t)e;
-            fr.rect = tight_rect(geo, bg, rect);
-            a.far[pos] = fr;
-        }
-        __syncwarp();
-    }
+    // (depth-sliced pass: the far items are not emitted -- far_collect projects them again, and only
+    // for the envs with a tile whose near list ran out with live pixels)
 }
 
 // ------------------------------------------------------------------------------- avatars
@@ -744,38 +716,121 @@ __global__ void __launch_bounds__(kBlock) near_cut_kernel(sn_cloud c, PrepArgs a
     }
 }
 
-// One bucket item of a sliced pass (sn_far.cu): the far splat re-projected exactly as the emit
-// projects a near one -- SplatRec, BlendGeo and its 32-bit depth key.
+// The far half of a depth-sliced scene pass, for the envs with unfinished tiles (a tile whose near
+// list ran out with a live or undecided pixel, fctl[5]): every visible far (gaussian, env) item of
+// those envs is projected again exactly as the emit projects a near one; one that reaches an
+// unfinished tile of its env gets a far record (SplatRec, BlendGeo, gaussian index) and a bucket
+// item per such tile, keyed (bucket << (32 - ub)) | (32-bit depth key >> ub). The items are sorted
+// next (sn_far.cu). Reservations are warp-aggregated.
 template <typename T>
-__global__ void __launch_bounds__(kBlock, SN_EMIT_MIN_BLOCKS) far_project_kernel(sn_cloud c, const sn_camera *cams,
-                                                                                FarArgs f) {
-    const uint64_t n = min(*f.n_items, f.cap_b);
-    const uint64_t i = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
-    if (i >= n) return;
-    const FarRec fr = f.far[f.items[i]];
-    const int64_t g = fr.gid;
-    double p[3], ls[3], q[4], opacity, cov[6];
-    load_scene<T>(c, g, p, ls, q, opacity);
-    build_cov3d(ls, q, cov);
-    const sn_camera &cam = cams[f.e0 + (int)fr.env];
-    Geo geo;
-    project_geo(p, cov, cam, geo);  // kKeep: the same computation the count kernel kept it with
-    float dir[3], rgb[3];
-    view_dir(p, cam, dir);
-    eval_sh_f32(c.sh, c.n, g, c.sh_k, dir[0], dir[1], dir[2], rgb);
-    SplatRec r;
-    r.mx = geo.mx;
-    r.my = geo.my;
-    r.ca = geo.ca;
-    r.cb2 = 2.0 * geo.cb;
-    r.cc = geo.cc;
-    r.alpha = sigmoid(opacity);
-    r.z = geo.z;
-    r.rgb = pack_rgb21(rgb);
-    f.brec[i] = r;
-    f.bgeo[i] = make_blend_geo(r.ca, r.cb2, r.cc);
-    const unsigned long long off = (unsigned long long)__double_as_longlong(geo.z) - f.z_base;
-    f.zkey[i] = (uint32_t)(f.z_bits > 32 ? off >> (f.z_bits - 32) : off << (32 - f.z_bits));
+__global__ void __launch_bounds__(kBlock, SN_EMIT_MIN_BLOCKS) far_collect_kernel(sn_cloud c, FarArgs f) {
+    __shared__ double s_geo[kBlock][10];  // position (3), cov3d (6), alpha
+    __shared__ uint16_t s_q[kBlock / 32][32 * kEmitRound];
+    __shared__ sn_camera s_cam[kMaxEnvChunk];
+    const uint64_t envs = *(volatile unsigned long long *)(f.fctl + 5);
+    if (envs == 0) return;  // no unfinished tile anywhere (uniform)
+    {
+        const double *src = reinterpret_cast<const double *>(f.cams + f.e0);
+        double *dst = reinterpret_cast<double *>(s_cam);
+        const int nd = f.ec * (int)(sizeof(sn_camera) / sizeof(double));
+        for (int i = threadIdx.x; i < nd; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+    const int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    const uint64_t mask = g < c.n ? (f.vismask[g] & ~f.nearmask[g] & envs) : 0ull;
+    if (!__syncthreads_or(mask != 0ull)) return;  // (also the barrier after the camera staging)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (mask) {
+        double p[3], ls[3], q[4], opacity, cov[6];
+        load_scene<T>(c, g, p, ls, q, opacity);
+        build_cov3d(ls, q, cov);
+        double *d = s_geo[threadIdx.x];
+        d[0] = p[0];
+        d[1] = p[1];
+        d[2] = p[2];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) d[3 + k] = cov[k];
+        d[9] = sigmoid(opacity);
+    }
+    const int64_t g0 = (int64_t)blockIdx.x * kBlock + warp * 32;
+    uint16_t *qq = s_q[warp];
+    const uint32_t lt = (1u << lane) - 1u;
+    for (int eb = 0; eb < f.ec; eb += kEmitRound) {
+        const int n = build_round(mask, eb, min(eb + kEmitRound, f.ec), qq);  // (warp-uniform n)
+        for (int k0 = 0; k0 < n; k0 += 32) {
+            const int k = k0 + lane;
+            int e = 0, l = 0;
+            Geo geo;
+            ushort4 r = make_ushort4(0xffff, 0, 0xffff, 0);
+            unsigned hits = 0;
+            if (k < n) {
+                const unsigned it = qq[k];
+                l = it & 31;
+                e = (it >> 5) & 63;
+                const double *d = s_geo[warp * 32 + l];
+                const double p[3] = {d[0], d[1], d[2]};
+                const double cov[6] = {d[3], d[4], d[5], d[6], d[7], d[8]};
+                project_geo(p, cov, s_cam[e], geo);  // kKeep: as the count kernel kept it
+                const BlendGeo bg = make_blend_geo(geo.ca, 2.0 * geo.cb, geo.cc);  // as write_splat
+                int rect[4];
+                tile_rect(geo.mx, geo.my, geo.radius, f.tiles_x, f.n_tiles / f.tiles_x, rect);
+                r = tight_rect(geo, bg, rect);
+                const int32_t *bo = f.bucket_of + (int64_t)e * f.n_tiles;
+                for (int ty = r.z; ty <= (int)r.w && r.x <= r.y; ++ty)
+                    for (int tx = r.x; tx <= (int)r.y; ++tx) hits += __ldg(bo + ty * f.tiles_x + tx) >= 0;
+            }
+            const unsigned hm = __ballot_sync(kFull, hits > 0);
+            if (!hm) continue;
+            unsigned incl = hits;  // inclusive warp scan of the item counts
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned o = __shfl_up_sync(kFull, incl, d);
+                if (lane >= d) incl += o;
+            }
+            unsigned long long jb = 0, ib = 0;
+            if (lane == 31) {
+                jb = atomicAdd(f.fctl + 4, (unsigned long long)__popc(hm));
+                ib = atomicAdd(f.fctl + 1, (unsigned long long)incl);
+            }
+            jb = __shfl_sync(kFull, jb, 31);
+            ib = __shfl_sync(kFull, ib, 31);
+            if (!hits) continue;
+            const uint64_t j = jb + __popc(hm & lt);
+            if (j >= f.cap_f) continue;  // overflow: the host re-runs with larger buffers
+            const double *d = s_geo[warp * 32 + l];
+            const double p[3] = {d[0], d[1], d[2]};
+            float dir[3], rgb[3];
+            view_dir(p, s_cam[e], dir);
+            eval_sh_f32(c.sh, c.n, g0 + l, c.sh_k, dir[0], dir[1], dir[2], rgb);
+            SplatRec rec;
+            rec.mx = geo.mx;
+            rec.my = geo.my;
+            rec.ca = geo.ca;
+            rec.cb2 = 2.0 * geo.cb;
+            rec.cc = geo.cc;
+            rec.alpha = d[9];
+            rec.z = geo.z;
+            rec.rgb = pack_rgb21(rgb);
+            f.recs[j] = rec;
+            f.geo[j] = make_blend_geo(rec.ca, rec.cb2, rec.cc);
+            f.gid[j] = (uint32_t)(g0 + l);
+            const unsigned long long off = (unsigned long long)__double_as_longlong(geo.z) - f.z_base;
+            const uint32_t zkey = (uint32_t)(f.z_bits > 32 ? off >> (f.z_bits - 32) : off << (32 - f.z_bits));
+            const uint32_t zlo = zkey >> f.ub;
+            uint64_t pos = ib + incl - hits;
+            const int32_t *bo = f.bucket_of + (int64_t)e * f.n_tiles;
+            for (int ty = r.z; ty <= (int)r.w; ++ty)
+                for (int tx = r.x; tx <= (int)r.y; ++tx) {
+                    const int32_t u = __ldg(bo + ty * f.tiles_x + tx);
+                    if (u < 0) continue;
+                    if (pos < f.cap_b) {
+                        f.keys[pos] = ((uint32_t)u << (32 - f.ub)) | zlo;
+                        f.vals[pos] = (uint32_t)j;
+                    }
+                    ++pos;
+                }
+        }
+        __syncwarp();
+    }
 }
 
 // Per-env exclusive scan of the per-block visible counts (in place), then env offsets.
@@ -879,13 +934,13 @@ cudaError_t launch_near_cut(const sn_cloud &c, const PrepArgs &a, double frac, b
     return cudaGetLastError();
 }
 
-cudaError_t launch_far_project(const sn_cloud &c, const sn_camera *cams, const FarArgs &f, cudaStream_t s) {
-    if (f.cap_b == 0) return cudaSuccess;
-    const unsigned grid = (unsigned)std::max<uint64_t>(1, (f.cap_b + kBlock - 1) / kBlock);
+cudaError_t launch_far_collect(const sn_cloud &c, const FarArgs &f, int64_t n, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const unsigned grid = (unsigned)((n + kBlock - 1) / kBlock);
     if (c.dtype == SN_FLOAT64)
-        far_project_kernel<double><<<grid, kBlock, 0, s>>>(c, cams, f);
+        far_collect_kernel<double><<<grid, kBlock, 0, s>>>(c, f);
     else
-        far_project_kernel<float><<<grid, kBlock, 0, s>>>(c, cams, f);
+        far_collect_kernel<float><<<grid, kBlock, 0, s>>>(c, f);
     return cudaGetLastError();
 }
 

@@ -70,7 +70,7 @@ def render_frames(scene, cameras, background, layer=None, avatars=None, sim_time
     the scene pass on the same stream (per-stage timers then add up to the render). views=False
     is the lean throughput path: the render keeps nothing for the harness views that need each
     splat's gaussian id or reference rectangle (pass_intermediates, tile_csr). near_slice: depth
-    slicing of the scene pass (-1 auto: scenes of >= 2M gaussians without views; 0 off; 1 on) --
+    slicing of the scene pass (-1 auto: scenes of >= 500k gaussians without views; 0 off; 1 on) --
     the same frames, only each env's near depth slice sorted (see include/splatnav_b200.h)."""
     lib = N.load()
     ctx = context or N.default_context()

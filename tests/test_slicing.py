@@ -91,13 +91,72 @@ def test_sliced_capacity_growth_and_exact_mode():
     cams = S.room_cameras(5, box, seed=183, width=320, height=240)
     bg = np.ones(3)
     ref, _ = _render(big, cams, bg, 0)
+    import ctypes
     ctx = N.Context()
     R.render_frames(small, cams, bg, views=False, near_slice=20, context=ctx)
+    lib = ctypes.CDLL(N.LIB_PATH)
+    lib.sn_debug_far_caps.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64]
+    assert lib.sn_debug_far_caps(ctx.handle, 4, 16, 16) == 0  # tiny far-half capacities
     r0 = ctx.render_retries()
     got = R.render_frames(big, cams, bg, contrib=True, stats=True, views=False, near_slice=20, context=ctx)
-    assert ctx.render_retries() > r0  # the far / bucket / unfinished capacities grew
+    assert ctx.render_retries() >= r0 + 2  # the unfinished / far-record / bucket capacities grew
     for k in KEYS:
         assert torch.equal(got[k], ref[k]), k
     # the all-float64 mode never slices (its walk needs the whole list): same counts
     ex = R.render_frames(big, cams, bg, contrib=True, stats=True, views=False, near_slice=20, exact=True, context=ctx)
     assert torch.equal(ex["contrib_scene"], ref["contrib_scene"])
+
+
+def test_far_short_fallback_rerenders_unsliced():
+    """A tile whose pixels all stop inside its near list does not register for the far buckets; an
+    undecided pixel's float64 walk that nevertheless runs out of the near list sets far_short and
+    the render is re-run unsliced. The test hook makes every float64 walk of a sliced pass set the
+    flag, so the fallback fires; the frames must still equal the unsliced render."""
+    import ctypes
+    from paper_2604_12626_b200 import _native as N
+    lib = ctypes.CDLL(N.LIB_PATH)
+    box = S.room_box(1_000_000)
+    scene = S.make_scene(300_000, box[0], box[1], seed=191)
+    cams = S.room_cameras(9, box, seed=192, width=320, height=240)
+    bg = np.array([0.3, 0.3, 0.3])
+    ref, _ = _render(scene, cams, bg, 0)
+    counts = (ctypes.c_uint64 * 3)()
+    assert lib.sn_debug_slice_hooks(1) == 0
+    try:
+        got, ctx = _render(scene, cams, bg, 10)
+        assert lib.sn_debug_slice_counts(ctx.handle, counts) == 0
+    finally:
+        lib.sn_debug_slice_hooks(0)
+    assert counts[2] > 0  # the fallback fired
+    for k in KEYS:
+        assert torch.equal(got[k], ref[k]), k
+    # and without the hook, the same sliced render runs through (the near lists end the walks)
+    got, ctx = _render(scene, cams, bg, 10)
+    for k in KEYS:
+        assert torch.equal(got[k], ref[k]), k
+
+
+def test_late_registration_by_the_first_fixup_pass():
+    """An undecided pixel whose float64 walk needs its tile's far bucket when the blend did not
+    register the tile: the first fixup pass registers it late and defers the pixel to the second.
+    The test hook stops the blend from registering tiles for undecided pixels alone, so with a 1%
+    near slice this path carries many pixels; frames, counts and stats must equal the unsliced render."""
+    import ctypes
+    from paper_2604_12626_b200 import _native as N
+    lib = ctypes.CDLL(N.LIB_PATH)
+    box = S.room_box(1_000_000)
+    scene = S.make_scene(300_000, box[0], box[1], seed=201)
+    cams = S.room_cameras(9, box, seed=202, width=320, height=240, near=0.01)
+    bg = np.array([0.6, 0.5, 0.4])
+    ref, _ = _render(scene, cams, bg, 0)
+    counts = (ctypes.c_uint64 * 3)()
+    assert lib.sn_debug_slice_hooks(2) == 0
+    try:
+        for frac in (10, 40):
+            got, ctx = _render(scene, cams, bg, frac)
+            assert lib.sn_debug_slice_counts(ctx.handle, counts) == 0
+            assert counts[2] == 0  # no unsliced fallback
+            for k in KEYS:
+                assert torch.equal(got[k], ref[k]), (frac, k)
+    finally:
+        lib.sn_debug_slice_hooks(0)
