@@ -673,16 +673,19 @@ __global__ void __launch_bounds__(kBlock) skin_kernel(sn_avatars av, int64_t g0,
 constexpr int kCutBins = 1024;
 constexpr int kCutPerOctave = 64;
 constexpr double kMinSliced = 131072.0;  // expected visible splats below which an env is not sliced
+constexpr int kCutThreads = kCutBins;  // one histogram bin per thread for the scan
 template <typename T>
-__global__ void __launch_bounds__(kBlock) near_cut_kernel(sn_cloud c, PrepArgs a, int64_t stride, double frac,
-                                                         double min_visible, double *z_cut) {
+__global__ void __launch_bounds__(kCutThreads) near_cut_kernel(sn_cloud c, PrepArgs a, int64_t stride, double frac,
+                                                              double min_visible, double *z_cut) {
+    using Scan = cub::BlockScan<unsigned, kCutThreads>;
+    __shared__ typename Scan::TempStorage tmp;
     __shared__ unsigned s_h[kCutBins];
     const sn_camera cam = a.cams[a.e0 + blockIdx.x];
-    for (int i = threadIdx.x; i < kCutBins; i += kBlock) s_h[i] = 0u;
+    s_h[threadIdx.x] = 0u;
     __syncthreads();
     const double lnear = log2(cam.near_);
     const double mx = (cam.cx + 64.0) / cam.fx, my = (cam.cy + 64.0) / cam.fy;
-    for (int64_t g = (int64_t)threadIdx.x * stride; g < c.n; g += (int64_t)kBlock * stride) {
+    for (int64_t g = (int64_t)threadIdx.x * stride; g < c.n; g += (int64_t)kCutThreads * stride) {
         double v[4];
         load4<T>(static_cast<const T *>(c.pos_opacity) + 4 * g, v);
         const double p[3] = {v[0], v[1], v[2]};
@@ -696,23 +699,17 @@ __global__ void __launch_bounds__(kBlock) near_cut_kernel(sn_cloud c, PrepArgs a
         atomicAdd(&s_h[bin], 1u);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint64_t tot = 0;
-        for (int i = 0; i < kCutBins; ++i) tot += s_h[i];
-        double cut = INFINITY;
-        if (tot > 0 && (double)tot * (double)stride >= min_visible) {
-            const double target = frac * (double)tot;
-            uint64_t run = 0;
-            for (int i = 0; i < kCutBins; ++i) {
-                run += s_h[i];
-                if ((double)run >= target) {
-                    cut = exp2(lnear + (double)(i + 1) / kCutPerOctave);
-                    break;
-                }
-            }
-            if (!(cut < cam.far_)) cut = INFINITY;
-        }
-        z_cut[blockIdx.x] = cut;
+    // inclusive prefix over the bins: the cut is the upper edge of the first bin reaching frac
+    const unsigned h = s_h[threadIdx.x];
+    unsigned excl, tot;
+    Scan(tmp).ExclusiveSum(h, excl, tot);
+    const bool slice = tot > 0 && (double)tot * (double)stride >= min_visible;
+    const double target = frac * (double)tot;
+    if (threadIdx.x == 0) z_cut[blockIdx.x] = INFINITY;  // (no bin reaches the target, or no slicing)
+    __syncthreads();
+    if (slice && (double)(excl + h) >= target && (double)excl < target) {  // exactly one thread
+        const double cut = exp2(lnear + (double)(threadIdx.x + 1) / kCutPerOctave);
+        z_cut[blockIdx.x] = cut < cam.far_ ? cut : INFINITY;
     }
 }
 
@@ -928,9 +925,9 @@ cudaError_t launch_near_cut(const sn_cloud &c, const PrepArgs &a, double frac, b
     const int64_t stride = std::max<int64_t>(1, c.n / 65536);  // ~64k samples per env
     const double min_visible = all_envs ? 0.0 : kMinSliced;
     if (c.dtype == SN_FLOAT64)
-        near_cut_kernel<double><<<a.ec, kBlock, 0, s>>>(c, a, stride, frac, min_visible, z_cut);
+        near_cut_kernel<double><<<a.ec, kCutThreads, 0, s>>>(c, a, stride, frac, min_visible, z_cut);
     else
-        near_cut_kernel<float><<<a.ec, kBlock, 0, s>>>(c, a, stride, frac, min_visible, z_cut);
+        near_cut_kernel<float><<<a.ec, kCutThreads, 0, s>>>(c, a, stride, frac, min_visible, z_cut);
     return cudaGetLastError();
 }
 
