@@ -131,6 +131,9 @@ __device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
 // like its scalar form), so the per-splat loads, the loop and the block mask are shared by two
 // pixels and the chain costs about half the issue slots per pixel.
 constexpr int kBW = kBT / 32;  // warps (8 x 8 pixel blocks) per tile (kBT: sn_internal.h)
+#ifndef SN_EXACT_BLOCK
+X
+#endif
 
 // Shared-memory form of a gathered splat for the float32 chain (80 B): the principal-axis rows (a
 // pixel's v_k = row_k . o + V_k, h = v1^2 + v2^2), V1 and V2 twice (register pairs for FFMA2), the
@@ -217,6 +220,45 @@ __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1
         const float lim = 3.0f * 1.00001f + (s1 + s2) * marg;
         // u_k at the block centres (8 bx - 4, 8 by - 4) relative to the tile centre
         const float u1b = fU1 - 4.0f * fe1x - 4.0f * fe1y, u2b = fU2 + 4.0f * fe1y - 4.0f * fe1x;
+#if SN_EXACT_BLOCK
+        // Exact: the distance from the disc's centre to the block's parallelogram {C + s A + t B,
+        // |s|, |t| <= 1} in v space, against 3 (with the same slack). The parallelogram's minimum is
+        // its interior point when the unconstrained minimiser lies inside, else on one of its four
+        // edges (a clamped 1-D minimum each); the float errors (~1e-6 of |C|^2) stay far inside the
+        // slack's 2e-5 |C| R. Subsumes the four separating axes below.
+        const float AA = hx1 * hx1 + hx2 * hx2, BB = hy1 * hy1 + hy2 * hy2, AB = hx1 * hy1 + hx2 * hy2;
+        const float rdet = 1.0f / (AA * BB - AB * AB), rAA = 1.0f / AA, rBB = 1.0f / BB;
+        (void)ext1;
+        (void)ext2;
+#pragma unroll
+        for (int w = 0; w < kBW; ++w) {
+            const float bx = (float)(w & 1), by = (float)(w >> 1);
+            const float u1c = u1b + 8.0f * bx * fe1x + 8.0f * by * fe1y;
+            const float u2c = u2b - 8.0f * bx * fe1y + 8.0f * by * fe1x;
+            const float v1c = s1 * u1c, v2c = s2 * u2c;
+            const float rad = lim + 1e-5f * (fabsf(v1c) + fabsf(v2c) + hwp + hwm);
+            const float AC = hx1 * v1c + hx2 * v2c, BC = hy1 * v1c + hy2 * v2c;
+            const float ss = (AB * BC - BB * AC) * rdet, tt = (AB * AC - AA * BC) * rdet;
+            if (fabsf(ss) <= 1.0f && fabsf(tt) <= 1.0f) continue;  // the centre projects inside
+            float d2m = 3.0e38f;
+#pragma unroll
+            for (int sg = -1; sg <= 1; sg += 2) {
+                {  // edge s = sg
+                    const float cx = v1c + sg * hx1, cy = v2c + sg * hx2;
+                    const float t = fminf(1.0f, fmaxf(-1.0f, -(hy1 * cx + hy2 * cy) * rBB));
+                    const float ex = cx + t * hy1, ey = cy + t * hy2;
+                    d2m = fminf(d2m, ex * ex + ey * ey);
+                }
+                {  // edge t = sg
+                    const float cx = v1c + sg * hy1, cy = v2c + sg * hy2;
+                    const float t = fminf(1.0f, fmaxf(-1.0f, -(hx1 * cx + hx2 * cy) * rAA));
+                    const float ex = cx + t * hx1, ey = cy + t * hx2;
+                    d2m = fminf(d2m, ex * ex + ey * ey);
+                }
+            }
+            if (d2m > rad * rad) m &= ~(1u << w);
+        }
+#else
 #pragma unroll
         for (int w = 0; w < kBW; ++w) {
             const float bx = (float)(w & 1), by = (float)(w >> 1);
@@ -228,6 +270,7 @@ __device__ __forceinline__ unsigned tile_entry(double e1x, double e1y, double p1
                 fabsf(v1c - v2c) * 0.70710678f - hwm > slack)
                 m &= ~(1u << w);
         }
+#endif
     }
     if (!m) return 0u;  // reaches none of the tile's warp blocks: the record is never read
     // the axes pre-scaled by sqrt(l_k log2(e) / 2) (float64 products, rounded once):
@@ -729,6 +772,13 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
                     f32x2 neps = fma2(h, pack2(q3.x, q3.x), pack2(q2.z, q2.w));  // -(alpha's relative bound)
                     float h0, h1;
                     unpack2(h, h0, h1);
+    #ifdef SN_BLEND_PROF
+                    {  // walk iterations where no pixel of the warp's block (live or not) is inside
+                        float g0, g1;
+                        unpack2(fma2(v1, v1, mul2(v2, v2)), g0, g1);
+                        PROF(3, lane == 0 && !__any_sync(kFull, g0 <= q2.x || g1 <= q2.x));
+                    }
+    #endif
                     // 1 where the pixel is certainly inside the support, 0 where outside or finished
                     float m0 = le_mask(h0, q2.y), m1 = le_mask(h1, q2.y);
                     if ((h0 > q2.y && h0 <= q2.x) || (h1 > q2.y && h1 <= q2.x)) {
