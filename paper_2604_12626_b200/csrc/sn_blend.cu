@@ -132,7 +132,10 @@ __device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
 // pixels and the chain costs about half the issue slots per pixel.
 constexpr int kBW = kBT / 32;  // warps (8 x 8 pixel blocks) per tile (kBT: sn_internal.h)
 #ifndef SN_EXACT_BLOCK
-X
+// tile_entry's warp-block test: separating axes (0), or the exact disc-vs-parallelogram distance (1),
+// which removes more empty walk iterations but was measured slower (scene blend 6.04 vs 5.83 ms at
+// config 2: its per-record cost exceeds the walk it saves)
+#define SN_EXACT_BLOCK 0
 #endif
 
 // Shared-memory form of a gathered splat for the float32 chain (80 B): the principal-axis rows (a
