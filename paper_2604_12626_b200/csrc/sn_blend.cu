@@ -724,16 +724,19 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
                     atomicMax(&s_epsmax, __float_as_uint(-__fmaf_rn(f.nka, fminf(f.thr_out, 7.0f), f.nkb)));
                 if (msk) s_f[jt] = f;  // an entry no warp walks is never read
                 s_slot[jt] = rid;
-                s_mask[jt] = (uint8_t)msk;
+                s_mask[jt] = (uint8_t)(msk | (msk && gs.gl.z > 0.99f ? 0x80u : 0u));  // bit 7: opacity > .99
             }
             __syncthreads();
             // each warp walks only the batch entries whose support can reach its 8 x 8 pixel block,
             // in depth order; the per-pixel tests below stay exact, the mask only skips whole warps
             int cnt = 0;
+            bool hi_op = false;  // an entry of this warp's list has opacity > .99 (mask bit 7)
             for (int j0 = 0; j0 < n; j0 += 32) {
-                const bool mine = j0 + lane < n && ((s_mask[j0 + lane] >> warp) & 1u);
+                const unsigned mk = j0 + lane < n ? s_mask[j0 + lane] : 0u;
+                const bool mine = (mk >> warp) & 1u;
                 const unsigned bal = __ballot_sync(kFull, mine);
                 if (mine) s_wl[warp][cnt + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)((j0 + lane) * sizeof(FRec));
+                hi_op |= __any_sync(kFull, mine && (mk & 0x80u));
                 cnt += __popc(bal);
             }
             const int cnt_pad = (cnt + kWalkUnroll - 1) / kWalkUnroll * kWalkUnroll;
@@ -756,88 +759,98 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
             // The walk carries NEGATED weights: na = -a (the record holds -alpha, the inside mask m is
             // 1 / 0), so T (1 - a) = fma(na, T, T) and err (1 - a) = fma(na, err, .) need no negation;
             // nw = -w, and the colour, depth and A sums accumulate negated (flipped once in the epilogue).
-            for (int k0 = 0; k0 < cnt_pad; k0 += 32) {
-                if (__all_sync(kFull, !(lo_of(P.dead) == 0.0f || hi_of(P.dead) == 0.0f))) break;
-                const int k1 = min(cnt_pad, k0 + 32);
-                for (int k = k0; k < k1; k += kWalkUnroll) {
-    #pragma unroll
-                for (int ku = 0; ku < kWalkUnroll; ++ku) {
-                    const FRec &s = *reinterpret_cast<const FRec *>(fbase + s_wl[warp][k + ku]);
-                    PROF(0, lane == 0);
-                    const float4 q0 = *reinterpret_cast<const float4 *>(&s.a1x);      // a1x a1y c2x c2y
-                    const float4 q1 = *reinterpret_cast<const float4 *>(&s.V1);       // V1 V1 V2 V2
-                    const float4 q2 = *reinterpret_cast<const float4 *>(&s.thr_out);  // thr_out thr_in nkb nkb
-                    const float4 q3 = *reinterpret_cast<const float4 *>(&s.nka);      // nka alpha z -
-                    // v_k for both pixels (same ox; oy and oy + 4), h = v1^2 + v2^2 (+ the finished offset)
-                    const f32x2 v1 = fma2(OY, pack2(q0.y, q0.y), fma2(OX, pack2(q0.x, q0.x), pack2(q1.x, q1.y)));
-                    const f32x2 v2 = fma2(OY, pack2(q0.w, q0.w), fma2(OX, pack2(q0.z, q0.z), pack2(q1.z, q1.w)));
-                    const f32x2 h = fma2(v1, v1, fma2(v2, v2, P.dead));
-                    f32x2 neps = fma2(h, pack2(q3.x, q3.x), pack2(q2.z, q2.w));  // -(alpha's relative bound)
-                    float h0, h1;
-                    unpack2(h, h0, h1);
-    #ifdef SN_BLEND_PROF
-                    {  // walk iterations where no pixel of the warp's block (live or not) is inside
-                        float g0, g1;
-                        unpack2(fma2(v1, v1, mul2(v2, v2)), g0, g1);
-                        PROF(3, lane == 0 && !__any_sync(kFull, g0 <= q2.x || g1 <= q2.x));
-                    }
-    #endif
-                    // 1 where the pixel is certainly inside the support, 0 where outside or finished
-                    float m0 = le_mask(h0, q2.y), m1 = le_mask(h1, q2.y);
-                    if ((h0 > q2.y && h0 <= q2.x) || (h1 > q2.y && h1 <= q2.x)) {
-                        // boundary band (rare, divergent): the reference's float64 test (_kernels_cy.pyx:73-75)
-                        PROF(1, 1);
-                        const int j = (int)((reinterpret_cast<const char *>(&s) - fbase) / sizeof(FRec));
-                        const SplatRec &sd = (SOURCE == 3 ? v.far_recs : v.recs)[s_slot[j]];
-                        const double ddx = sd.mx - px;
+            auto walk = [&](auto clamp_tag) {
+                constexpr bool kClamp = decltype(clamp_tag)::value;
+                for (int k0 = 0; k0 < cnt_pad; k0 += 32) {
+                    if (__all_sync(kFull, !(lo_of(P.dead) == 0.0f || hi_of(P.dead) == 0.0f))) break;
+                    const int k1 = min(cnt_pad, k0 + 32);
+                    for (int k = k0; k < k1; k += kWalkUnroll) {
+        #pragma unroll
+                    for (int ku = 0; ku < kWalkUnroll; ++ku) {
+                        const FRec &s = *reinterpret_cast<const FRec *>(fbase + s_wl[warp][k + ku]);
+                        PROF(0, lane == 0);
+                        const float4 q0 = *reinterpret_cast<const float4 *>(&s.a1x);      // a1x a1y c2x c2y
+                        const float4 q1 = *reinterpret_cast<const float4 *>(&s.V1);       // V1 V1 V2 V2
+                        const float4 q2 = *reinterpret_cast<const float4 *>(&s.thr_out);  // thr_out thr_in nkb nkb
+                        const float4 q3 = *reinterpret_cast<const float4 *>(&s.nka);      // nka alpha z -
+                        // v_k for both pixels (same ox; oy and oy + 4), h = v1^2 + v2^2 (+ the finished offset)
+                        const f32x2 v1 = fma2(OY, pack2(q0.y, q0.y), fma2(OX, pack2(q0.x, q0.x), pack2(q1.x, q1.y)));
+                        const f32x2 v2 = fma2(OY, pack2(q0.w, q0.w), fma2(OX, pack2(q0.z, q0.z), pack2(q1.z, q1.w)));
+                        const f32x2 h = fma2(v1, v1, fma2(v2, v2, P.dead));
+                        f32x2 neps = fma2(h, pack2(q3.x, q3.x), pack2(q2.z, q2.w));  // -(alpha's relative bound)
+                        float h0, h1;
+                        unpack2(h, h0, h1);
+        #ifdef SN_BLEND_PROF
+                        {  // walk iterations where no pixel of the warp's block (live or not) is inside
+                            float g0, g1;
+                            unpack2(fma2(v1, v1, mul2(v2, v2)), g0, g1);
+                            PROF(3, lane == 0 && !__any_sync(kFull, g0 <= q2.x || g1 <= q2.x));
+                        }
+        #endif
+                        // 1 where the pixel is certainly inside the support, 0 where outside or finished
+                        float m0 = le_mask(h0, q2.y), m1 = le_mask(h1, q2.y);
+                        if ((h0 > q2.y && h0 <= q2.x) || (h1 > q2.y && h1 <= q2.x)) {
+                            // boundary band (rare, divergent): the reference's float64 test (_kernels_cy.pyx:73-75)
+                            PROF(1, 1);
+                            const int j = (int)((reinterpret_cast<const char *>(&s) - fbase) / sizeof(FRec));
+                            const SplatRec &sd = (SOURCE == 3 ? v.far_recs : v.recs)[s_slot[j]];
+                            const double ddx = sd.mx - px;
+                            float e0, e1;
+                            unpack2(neps, e0, e1);
+                            if (h0 > q2.y && h0 <= q2.x) {
+                                const double ddy = sd.my - (py0 + 0.5);
+                                const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
+                                if (!(d2d > kSupportD2)) {
+                                    m0 = 1.0f;
+                                    h0 = (float)(d2d * kHalfLog2e);  // h, rounded once (within kEpsExact)
+                                    e0 = -kEpsExact;
+                                }
+                            }
+                            if (h1 > q2.y && h1 <= q2.x) {
+                                const double ddy = sd.my - (py1 + 0.5);
+                                const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
+                                if (!(d2d > kSupportD2)) {
+                                    m1 = 1.0f;
+                                    h1 = (float)(d2d * kHalfLog2e);
+                                    e1 = -kEpsExact;
+                                }
+                            }
+                            neps = pack2(e0, e1);
+                        }
+                        const f32x2 m = pack2(m0, m1);
+                        // alpha = min(o 2^-h, .99) inside the support, 0 outside: T, err and the sums then
+                        // stay exactly as they were (w = 0, T (1 - 0) = T, err (1 - 0) + 0)
                         float e0, e1;
-                        unpack2(neps, e0, e1);
-                        if (h0 > q2.y && h0 <= q2.x) {
-                            const double ddy = sd.my - (py0 + 0.5);
-                            const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
-                            if (!(d2d > kSupportD2)) {
-                                m0 = 1.0f;
-                                h0 = (float)(d2d * kHalfLog2e);  // h, rounded once (within kEpsExact)
-                                e0 = -kEpsExact;
-                            }
-                        }
-                        if (h1 > q2.y && h1 <= q2.x) {
-                            const double ddy = sd.my - (py1 + 0.5);
-                            const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
-                            if (!(d2d > kSupportD2)) {
-                                m1 = 1.0f;
-                                h1 = (float)(d2d * kHalfLog2e);
-                                e1 = -kEpsExact;
-                            }
-                        }
-                        neps = pack2(e0, e1);
+                        unpack2(mul2(pack2(ex2_approx(-h0), ex2_approx(-h1)), pack2(q3.y, q3.y)), e0, e1);  // -o 2^-h
+                        // min(., .99) only matters for opacities above .99 (o 2^-h <= o): batches without one skip it
+                        const f32x2 na = kClamp ? mul2(pack2(fmaxf(e0, -0.99f), fmaxf(e1, -0.99f)), m)
+                                                : mul2(pack2(e0, e1), m);  // -a
+                        const f32x2 nw = mul2(na, P.T);                                       // -w
+                        const f32x2 Tn = fma2(na, P.T, P.T);  // T (1 - a), rounded once
+                        const float4 q4 = *reinterpret_cast<const float4 *>(&s.r);  // r g b -
+                        P.cr = fma2(nw, pack2(q4.x, q4.x), P.cr);
+                        P.cg = fma2(nw, pack2(q4.y, q4.y), P.cg);
+                        P.cb = fma2(nw, pack2(q4.z, q4.z), P.cb);
+                        P.D = fma2(nw, pack2(q3.z, q3.z), P.D);
+                        P.A = add2(P.A, nw);
+                        // err (1 - a) + w eps + 1.25 u T' (the rounding term only where T changed)
+                        P.err = fma2(na, P.err, fma2(nw, neps, fma2(Tn, mul2(m, pack2(kU125, kU125)), P.err)));
+                        P.T = Tn;
+                        P.nc = add2(P.nc, m);
+                        // near the cutoff (_kernels_cy.pyx:65-66): stop; decided or deferred after the walk
+                        // (+ kDead once per step past it: a finished pixel's offset only grows, ~1e30 per
+                        // walked entry, far from overflow; liveness is dead == 0)
+                        float g0, g1;
+                        unpack2(sub2(Tn, P.err), g0, g1);
+                        P.dead = fma2(pack2(le_mask(g0, kTHi), le_mask(g1, kTHi)), pack2(kDead, kDead), P.dead);
                     }
-                    const f32x2 m = pack2(m0, m1);
-                    // alpha = min(o 2^-h, .99) inside the support, 0 outside: T, err and the sums then
-                    // stay exactly as they were (w = 0, T (1 - 0) = T, err (1 - 0) + 0)
-                    float e0, e1;
-                    unpack2(mul2(pack2(ex2_approx(-h0), ex2_approx(-h1)), pack2(q3.y, q3.y)), e0, e1);  // -o 2^-h
-                    const f32x2 na = mul2(pack2(fmaxf(e0, -0.99f), fmaxf(e1, -0.99f)), m);  // -a
-                    const f32x2 nw = mul2(na, P.T);                                       // -w
-                    const f32x2 Tn = fma2(na, P.T, P.T);  // T (1 - a), rounded once
-                    const float4 q4 = *reinterpret_cast<const float4 *>(&s.r);  // r g b -
-                    P.cr = fma2(nw, pack2(q4.x, q4.x), P.cr);
-                    P.cg = fma2(nw, pack2(q4.y, q4.y), P.cg);
-                    P.cb = fma2(nw, pack2(q4.z, q4.z), P.cb);
-                    P.D = fma2(nw, pack2(q3.z, q3.z), P.D);
-                    P.A = add2(P.A, nw);
-                    // err (1 - a) + w eps + 1.25 u T' (the rounding term only where T changed)
-                    P.err = fma2(na, P.err, fma2(nw, neps, fma2(Tn, mul2(m, pack2(kU125, kU125)), P.err)));
-                    P.T = Tn;
-                    P.nc = add2(P.nc, m);
-                    // near the cutoff (_kernels_cy.pyx:65-66): stop; decided or deferred after the walk
-                    float g0, g1, d0, d1;
-                    unpack2(sub2(Tn, P.err), g0, g1);
-                    unpack2(P.dead, d0, d1);
-                    P.dead = pack2(g0 <= kTHi ? kDead : d0, g1 <= kTHi ? kDead : d1);
+                    }
                 }
-                }
-            }
+            };
+            if (hi_op)
+                walk(std::true_type{});
+            else
+                walk(std::false_type{});
             if (SOURCE == 0) {  // drop the consumed head of the queue
                 const int rest = q_len - n;
                 uint32_t qv0 = threadIdx.x < rest ? s_queue[n + threadIdx.x] : 0u;
