@@ -364,6 +364,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
         SN_ENSURE(w.nearmask, sizeof(uint64_t) * std::max<int64_t>(n, 1));
         a.z_cut = w.zcut.as<double>();
         a.nearmask = w.nearmask.as<uint64_t>();
+        a.lazy_far = a.stats == nullptr ? 1 : 0;  // RenderStats need every item's frame cull
     }
 
     if (n > 0) {

@@ -54,6 +54,10 @@ struct PrepArgs {
     // 2 ec + 1 entries.
     const double *z_cut;
     uint64_t *nearmask;        // (n) bit e: visible and near in env e0 + e
+    // lazy far (sliced, no RenderStats requested): in-depth items at z >= z_cut are classified far
+    // without their projection -- vismask holds them as in-depth, far rows count them, and
+    // far_collect applies the frame cull if a tile ever needs them
+    int32_t lazy_far;
 };
 
 // sn_preprocess.cu

@@ -81,13 +81,14 @@ __device__ __forceinline__ void tally(unsigned (*s_cnt)[5], int e, int code, boo
     }
 }
 
-__device__ __forceinline__ void flush_counts(unsigned (*s_cnt)[5], const PrepArgs &a, const unsigned *s_near = nullptr) {
+__device__ __forceinline__ void flush_counts(unsigned (*s_cnt)[5], const PrepArgs &a, const unsigned *s_near = nullptr,
+                                             const unsigned *s_farz = nullptr) {
     __syncthreads();
     int t = threadIdx.x;
     if (t < a.ec) {
-        if (s_near) {  // depth-sliced: rows e (near) and ec + e (far)
+        if (s_near) {  // depth-sliced: rows e (near) and ec + e (far: visible, or in-depth when lazy)
             a.blk_counts[(int64_t)t * a.n_blocks + blockIdx.x] = s_near[t];
-            a.blk_counts[(int64_t)(a.ec + t) * a.n_blocks + blockIdx.x] = s_cnt[t][4] - s_near[t];
+            a.blk_counts[(int64_t)(a.ec + t) * a.n_blocks + blockIdx.x] = s_farz ? s_farz[t] : s_cnt[t][4] - s_near[t];
         } else {
             a.blk_counts[(int64_t)t * a.n_blocks + blockIdx.x] = s_cnt[t][4];
         }
@@ -245,10 +246,12 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
     __shared__ sn_camera s_cam[kMaxEnvChunk];
     __shared__ unsigned long long s_nearbits[kBlock];  // depth slicing: visible and z < z_cut
     __shared__ unsigned s_near[kMaxEnvChunk];
+    __shared__ unsigned s_farz[kMaxEnvChunk];  // lazy far: in-depth items at z >= z_cut
     __shared__ double s_zcut[kMaxEnvChunk];
     stage_cams(a, s_cam);
     if (threadIdx.x < a.ec) {
         s_near[threadIdx.x] = 0u;
+        s_farz[threadIdx.x] = 0u;
         s_zcut[threadIdx.x] = a.z_cut ? a.z_cut[threadIdx.x] : INFINITY;
     }
     s_nearbits[threadIdx.x] = 0ull;
@@ -269,20 +272,26 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
         for (int k = 0; k < 6; ++k) d[3 + k] = cov[k];
     }
     s_vis[threadIdx.x] = 0ull;
-    // depth cull for every env (4 fp64 ops per env), then full geometry only for in-depth items
-    uint64_t in_depth = 0;
+    // depth cull for every env (4 fp64 ops per env), then full geometry only for in-depth items --
+    // with a.lazy_far, only for the near ones: an in-depth item at z >= z_cut is far whatever its
+    // frame cull, and far items are projected again (and culled) only if a tile needs them
+    uint64_t in_depth = 0, far_z = 0;
     for (int e = 0; e < a.ec; ++e) {
-        bool in = false;
+        bool in = false, fz = false;
         if (valid) {
             const sn_camera &cam = s_cam[e];
             double z = cam_z(p, cam);
             in = (z > cam.near_) && (z < cam.far_);
+            fz = a.lazy_far && in && !(z < s_zcut[e]);
         }
-        in_depth |= (uint64_t)in << e;
+        in_depth |= (uint64_t)(in && !fz) << e;
+        far_z |= (uint64_t)fz << e;
         unsigned b_in = __ballot_sync(kFull, valid), b_out = __ballot_sync(kFull, valid && !in);
+        const unsigned b_fz = __ballot_sync(kFull, fz);
         if (lane == 0) {
             if (b_in) atomicAdd(&s_cnt[e][0], __popc(b_in));
             if (b_out) atomicAdd(&s_cnt[e][1], __popc(b_out));
+            if (b_fz) atomicAdd(&s_farz[e], __popc(b_fz));
         }
     }
     const int64_t g0 = (int64_t)blockIdx.x * kBlock + warp * 32;
@@ -311,7 +320,8 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
         __syncwarp();
     }
     __syncthreads();
-    if (valid) a.vismask[g] = s_vis[threadIdx.x];
+    // (lazy far: the far bits are the in-depth far items, not yet frame-culled)
+    if (valid) a.vismask[g] = s_vis[threadIdx.x] | far_z;
     (void)g0;
     if (a.z_cut) {  // near items per env of this block
         const uint64_t nb = s_nearbits[threadIdx.x];
@@ -320,7 +330,7 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
             const unsigned bal = __ballot_sync(kFull, (nb >> e) & 1ull);
             if (lane == 0 && bal) atomicAdd(&s_near[e], __popc(bal));
         }
-        flush_counts(s_cnt, a, s_near);
+        flush_counts(s_cnt, a, s_near, a.lazy_far ? s_farz : nullptr);
     } else {
         flush_counts(s_cnt, a);
     }
@@ -766,14 +776,17 @@ __global__ void __launch_bounds__(kBlock, SN_EMIT_MIN_BLOCKS) far_collect_kernel
                 const double *d = s_geo[warp * 32 + l];
                 const double p[3] = {d[0], d[1], d[2]};
                 const double cov[6] = {d[3], d[4], d[5], d[6], d[7], d[8]};
-                project_geo(p, cov, s_cam[e], geo);  // kKeep: as the count kernel kept it
-                const BlendGeo bg = make_blend_geo(geo.ca, 2.0 * geo.cb, geo.cc);  // as write_splat
-                int rect[4];
-                tile_rect(geo.mx, geo.my, geo.radius, f.tiles_x, f.n_tiles / f.tiles_x, rect);
-                r = tight_rect(geo, bg, rect);
-                const int32_t *bo = f.bucket_of + (int64_t)e * f.n_tiles;
-                for (int ty = r.z; ty <= (int)r.w && r.x <= r.y; ++ty)
-                    for (int tx = r.x; tx <= (int)r.y; ++tx) hits += __ldg(bo + ty * f.tiles_x + tx) >= 0;
+                // kKeep as the count kernel kept it -- or, lazily classified far items (in depth, not
+                // yet frame-culled), whatever the reference's cull decides
+                if (project_geo(p, cov, s_cam[e], geo) == kKeep) {
+                    const BlendGeo bg = make_blend_geo(geo.ca, 2.0 * geo.cb, geo.cc);  // as write_splat
+                    int rect[4];
+                    tile_rect(geo.mx, geo.my, geo.radius, f.tiles_x, f.n_tiles / f.tiles_x, rect);
+                    r = tight_rect(geo, bg, rect);
+                    const int32_t *bo = f.bucket_of + (int64_t)e * f.n_tiles;
+                    for (int ty = r.z; ty <= (int)r.w && r.x <= r.y; ++ty)
+                        for (int tx = r.x; tx <= (int)r.y; ++tx) hits += __ldg(bo + ty * f.tiles_x + tx) >= 0;
+                }
             }
             const unsigned hm = __ballot_sync(kFull, hits > 0);
             if (!hm) continue;

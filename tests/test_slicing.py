@@ -17,13 +17,13 @@ pytestmark = pytest.mark.gpu
 KEYS = ("color", "alpha", "depth", "contrib_scene", "stats")
 
 
-def _render(scene, cams, bg, near_slice, **kw):
+def _render(scene, cams, bg, near_slice, stats=True, **kw):
     from paper_2604_12626_b200 import _native as N
     from paper_2604_12626_b200 import renderer as R
     ctx = N.Context()
     out = None
     for _ in range(2):  # the second render runs on grown buffers (the first may retry inside)
-        out = R.render_frames(scene, cams, bg, contrib=True, stats=True, views=False, near_slice=near_slice,
+        out = R.render_frames(scene, cams, bg, contrib=True, stats=stats, views=False, near_slice=near_slice,
                               context=ctx, **kw)
     torch.cuda.synchronize()
     return out, ctx
@@ -160,3 +160,31 @@ def test_late_registration_by_the_first_fixup_pass():
                 assert torch.equal(got[k], ref[k]), (frac, k)
     finally:
         lib.sn_debug_slice_hooks(0)
+
+
+def test_lazy_far_classification_without_stats():
+    """Without RenderStats the count kernel classifies in-depth items beyond the cut as far without
+    projecting them (their frame cull waits for far_collect, if a tile ever needs them): frames and
+    contributor counts must still equal the unsliced render, alone and under the avatar layer."""
+    from paper_2604_12626_b200.batch import BatchRenderer
+    box = S.room_box(1_000_000)
+    scene = S.make_scene(300_000, box[0], box[1], seed=211)
+    cams = S.room_cameras(9, box, seed=212, width=320, height=240)
+    bg = np.array([0.9, 0.8, 0.7])
+    ref, _ = _render(scene, cams, bg, 0)
+    for frac in (10, 50, 200):
+        got, _ = _render(scene, cams, bg, frac, stats=False, payload=True)
+        for k in ("color", "alpha", "depth", "contrib_scene"):
+            assert torch.equal(got[k], ref[k]), (frac, k)
+    bundles = [S.make_avatar(4000, seed=213 + i, n_frames=12, floor_lo=(2.0, 2.0), floor_hi=(6.0, 6.0))
+               for i in range(3)]
+    times = np.linspace(0.0, 0.37, 9)
+    outs = []
+    for ns in (0, 20, 120):
+        br = BatchRenderer(scene, bundles, start_offsets=[0.0, 0.1, 0.2], background=(0.5, 0.5, 0.5))
+        for _ in range(2):
+            o = br.render(cams, times, contrib=True, stats=ns == 0, views=False, near_slice=ns, payload=True)
+        outs.append(o)
+    for o in outs[1:]:
+        for k in ("color", "alpha", "depth", "contrib_scene", "contrib_layer", "rgb8", "depth16"):
+            assert torch.equal(o[k], outs[0][k]), k
