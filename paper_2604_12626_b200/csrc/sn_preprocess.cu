@@ -82,9 +82,11 @@ __device__ __forceinline__ void tally(unsigned (*s_cnt)[5], int e, int code, boo
 }
 
 __device__ __forceinline__ void flush_counts(unsigned (*s_cnt)[5], const PrepArgs &a, const unsigned *s_near = nullptr,
-                                             const unsigned *s_farz = nullptr) {
-    __syncthreads();
+                                             const unsigned *s_farz = nullptr, int n_input = -1) {
     int t = threadIdx.x;
+    // (the input count is the block's gaussians, the same for every env, when the caller passes it)
+    if (n_input >= 0 && t < a.ec) s_cnt[t][0] = (unsigned)n_input;
+    __syncthreads();
     if (t < a.ec) {
         if (s_near) {  // depth-sliced: rows e (near) and ec + e (far: visible, or in-depth when lazy)
             a.blk_counts[(int64_t)t * a.n_blocks + blockIdx.x] = s_near[t];
@@ -259,6 +261,7 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     bool valid = g < c.n;
+    const int n_input = (int)min((int64_t)kBlock, c.n - (int64_t)blockIdx.x * kBlock);
     double p[3] = {0.0, 0.0, 0.0};
     if (valid) {
         double ls[3], q[4], opacity, cov[6];
@@ -275,24 +278,48 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
     // depth cull for every env (4 fp64 ops per env), then full geometry only for in-depth items --
     // with a.lazy_far, only for the near ones: an in-depth item at z >= z_cut is far whatever its
     // frame cull, and far items are projected again (and culled) only if a tile needs them
-    uint64_t in_depth = 0, far_z = 0;
-    for (int e = 0; e < a.ec; ++e) {
-        bool in = false, fz = false;
-        if (valid) {
-            const sn_camera &cam = s_cam[e];
-            double z = cam_z(p, cam);
-            in = (z > cam.near_) && (z < cam.far_);
-            fz = a.lazy_far && in && !(z < s_zcut[e]);
+    // Per-env warp counts are accumulated in registers, lane e & 31 holding env e's (lo: e < 32,
+    // hi: e >= 32), and added to shared memory once per warp after the loop: a ballot and a popc
+    // per env instead of a shared atomic per env and counter. The depth-culled count is for
+    // RenderStats only; the in-depth far count for the lazy far rows only.
+    unsigned out_lo = 0, out_hi = 0, fz_lo = 0, fz_hi = 0;
+    const bool want_out = a.stats != nullptr;
+    // one half (32 envs) of the chunk: 32-bit masks, no 64-bit variable shifts in the loop
+    auto depth_half = [&](const int e0, const int e1, unsigned &in_m, unsigned &fz_m, unsigned &out_c,
+                          unsigned &fz_c) {
+        in_m = fz_m = 0u;
+        for (int e = e0; e < e1; ++e) {
+            bool in = false, fz = false;
+            if (valid) {
+                const sn_camera &cam = s_cam[e];
+                double z = cam_z(p, cam);
+                in = (z > cam.near_) && (z < cam.far_);
+                fz = a.lazy_far && in && !(z < s_zcut[e]);
+            }
+            in_m |= (unsigned)(in && !fz) << (e - e0);
+            fz_m |= (unsigned)fz << (e - e0);
+            const bool mine = lane == e - e0;
+            if (want_out) {
+                const unsigned c = __popc(__ballot_sync(kFull, valid && !in));
+                if (mine) out_c = c;
+            }
+            if (a.lazy_far) {
+                const unsigned c = __popc(__ballot_sync(kFull, fz));
+                if (mine) fz_c = c;
+            }
         }
-        in_depth |= (uint64_t)(in && !fz) << e;
-        far_z |= (uint64_t)fz << e;
-        unsigned b_in = __ballot_sync(kFull, valid), b_out = __ballot_sync(kFull, valid && !in);
-        const unsigned b_fz = __ballot_sync(kFull, fz);
-        if (lane == 0) {
-            if (b_in) atomicAdd(&s_cnt[e][0], __popc(b_in));
-            if (b_out) atomicAdd(&s_cnt[e][1], __popc(b_out));
-            if (b_fz) atomicAdd(&s_farz[e], __popc(b_fz));
-        }
+    };
+    unsigned in_lo, in_hi = 0u, far_lo, far_hi = 0u;
+    depth_half(0, min(a.ec, 32), in_lo, far_lo, out_lo, fz_lo);
+    if (a.ec > 32) depth_half(32, a.ec, in_hi, far_hi, out_hi, fz_hi);
+    const uint64_t in_depth = ((uint64_t)in_hi << 32) | in_lo, far_z = ((uint64_t)far_hi << 32) | far_lo;
+    if (lane < a.ec) {
+        if (want_out && out_lo) atomicAdd(&s_cnt[lane][1], out_lo);
+        if (fz_lo) atomicAdd(&s_farz[lane], fz_lo);
+    }
+    if (lane + 32 < a.ec) {
+        if (want_out && out_hi) atomicAdd(&s_cnt[lane + 32][1], out_hi);
+        if (fz_hi) atomicAdd(&s_farz[lane + 32], fz_hi);
     }
     const int64_t g0 = (int64_t)blockIdx.x * kBlock + warp * 32;
     uint16_t *qq = s_q[warp];
@@ -309,9 +336,10 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
             const double cov[6] = {d[3], d[4], d[5], d[6], d[7], d[8]};
             Geo geo;
             const int code = project_geo(pp, cov, s_cam[e], geo);
-            // field: 2 frame, 3 degenerate, 4 drawn (sn_stats order)
+            // field: 2 frame, 3 degenerate, 4 drawn (sn_stats order); the lazy sliced pass counts its
+            // near items below and needs none of these
             const int field = code == kKeep ? 4 : (code == kDegenerate ? 3 : 2);
-            tally_item(s_cnt, active, e, field);
+            if (!a.lazy_far) tally_item(s_cnt, active, e, field);
             if (code == kKeep) {
                 atomicOr(&s_vis[warp * 32 + l], 1ull << e);
                 if (geo.z < s_zcut[e]) atomicOr(&s_nearbits[warp * 32 + l], 1ull << e);
@@ -323,16 +351,19 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
     // (lazy far: the far bits are the in-depth far items, not yet frame-culled)
     if (valid) a.vismask[g] = s_vis[threadIdx.x] | far_z;
     (void)g0;
-    if (a.z_cut) {  // near items per env of this block
+    if (a.z_cut) {  // near items per env of this block (register-accumulated as above)
         const uint64_t nb = s_nearbits[threadIdx.x];
         if (valid) a.nearmask[g] = nb;
+        unsigned n_lo = 0, n_hi = 0;
         for (int e = 0; e < a.ec; ++e) {
-            const unsigned bal = __ballot_sync(kFull, (nb >> e) & 1ull);
-            if (lane == 0 && bal) atomicAdd(&s_near[e], __popc(bal));
+            const unsigned c = __popc(__ballot_sync(kFull, (nb >> e) & 1ull));
+            if (lane == (e & 31)) (e < 32 ? n_lo : n_hi) = c;
         }
-        flush_counts(s_cnt, a, s_near, a.lazy_far ? s_farz : nullptr);
+        if (lane < a.ec && n_lo) atomicAdd(&s_near[lane], n_lo);
+        if (lane + 32 < a.ec && n_hi) atomicAdd(&s_near[lane + 32], n_hi);
+        flush_counts(s_cnt, a, s_near, a.lazy_far ? s_farz : nullptr, n_input);
     } else {
-        flush_counts(s_cnt, a);
+        flush_counts(s_cnt, a, nullptr, nullptr, n_input);
     }
 }
 
