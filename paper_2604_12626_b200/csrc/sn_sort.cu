@@ -25,6 +25,9 @@ constexpr int kSortThreads = 256;
 #define SN_SORT_ROUNDS 8
 #endif
 constexpr int kSortRounds = SN_SORT_ROUNDS;  // items per thread
+#ifndef SN_SORT_MATCH
+#define SN_SORT_MATCH 0  // downsweep ranks: __match_any_sync peers (1) or digit-bit ballots (0)
+#endif
 constexpr int kSortTile = kSortThreads * kSortRounds;
 constexpr int kRowThreads = 1024;
 constexpr unsigned kAll = 0xffffffffu;
@@ -140,6 +143,7 @@ __global__ void __launch_bounds__(kSortThreads, SN_SORT_MIN_BLOCKS) sort_downswe
         k[r] = valid ? __ldg(kin + i) : 0u;
         v[r] = valid ? (vin ? __ldg(vin + i) : (uint32_t)i) : 0u;  // vin null: identity values
     }
+#if SN_SORT_MATCH
 #pragma unroll
     for (int r = 0; r < kSortRounds; ++r) {
         const uint64_t i = seg + (uint64_t)r * 32 + lane;
@@ -153,6 +157,30 @@ __global__ void __launch_bounds__(kSortThreads, SN_SORT_MIN_BLOCKS) sort_downswe
         __syncwarp();
         pos[r] = before + rank;
     }
+#else
+    // Peers (lanes with the same digit) from one ballot per digit bit, and the warp's running count
+    // per digit from a returning shared atomic by each peer group's first lane, broadcast by a
+    // shuffle: no shared-memory read-modify-write chain between rounds, so they pipeline.
+#pragma unroll
+    for (int r = 0; r < kSortRounds; ++r) {
+        const uint64_t i = seg + (uint64_t)r * 32 + lane;
+        const bool valid = i < n;
+        const uint32_t d = (k[r] >> shift) & mask;
+        unsigned peers = __ballot_sync(kAll, valid);
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            if (b < dbits) {
+                const unsigned bal = __ballot_sync(kAll, (d >> b) & 1u);
+                peers &= ((d >> b) & 1u) ? bal : ~bal;
+            }
+        }
+        const int leader = __ffs(peers) - 1;  // (invalid lanes: any; their result is unused)
+        uint32_t before = 0u;
+        if (valid && lane == leader) before = atomicAdd(&s_cnt[warp][d], (uint32_t)__popc(peers));
+        before = __shfl_sync(kAll, before, leader < 0 ? lane : leader);
+        pos[r] = before + __popc(peers & ((1u << lane) - 1u));
+    }
+#endif
     __syncthreads();
     uint32_t tile_cnt = 0;
     if (threadIdx.x < bins) {  // per digit: prefix over the tile's warps, and the tile's count
