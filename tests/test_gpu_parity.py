@@ -295,15 +295,17 @@ def test_blend_tile_range_plugin():
 
 
 def test_streaming_and_list_binners_agree():
-    """Rect streaming (no lists) and materialized radix lists give the same CSR and frames."""
+    """Rect streaming (no lists) and materialized radix lists: the tile lists the blend actually
+    consumes (sn_get_device_tiles -- the streamed per-tile queues vs the radix-sorted pairs) and the
+    frames are identical."""
     box = S.room_box(1_000_000)
     scene = S.make_scene(120_000, box[0], box[1], seed=71)
     cams = S.room_cameras(5, box, seed=72, near=0.01)
     r = R()
     a = r.render_frames(scene, cams, np.ones(3), contrib=True, binning=0)
-    csr_a = [r.tile_csr(1200, 0, e) for e in range(5)]
+    csr_a = [r.device_tiles(1200, 0, e) for e in range(5)]
     b = r.render_frames(scene, cams, np.ones(3), contrib=True, binning=1)
-    csr_b = [r.tile_csr(1200, 0, e) for e in range(5)]
+    csr_b = [r.device_tiles(1200, 0, e) for e in range(5)]
     for (ta, pa), (tb, pb) in zip(csr_a, csr_b):
         np.testing.assert_array_equal(ta, tb)
         np.testing.assert_array_equal(pa, pb)
