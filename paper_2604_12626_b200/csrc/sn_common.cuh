@@ -45,6 +45,8 @@ constexpr double kSupportD2 = 9.0;
 constexpr double kAlphaClip = 0.99;
 
 enum { kKeep = 0, kCullDepth = 1, kDegenerate = 2, kCullFrame = 3 };
+// whole-avatar cull code (avatar_cull_kernel): every gaussian of the avatar is visible in the env
+constexpr int kWholeVisible = 4;
 
 // One depth-sorted splat as the blend reads it: 64 bytes, one gather of four 16-byte vectors.
 // The decision chain (mean, conic, alpha) stays float64; colour is 3 x 21-bit unorm (error

@@ -613,7 +613,9 @@ __global__ void __launch_bounds__(kBlock, SN_AVATAR_COUNT_MIN_BLOCKS) avatar_cou
         bool input = valid && avatar_on(a, av.n_avatars, env, avatar);
         int code = -1;
         if (input && cull && cull[avatar]) {
-            code = cull[avatar];  // the whole avatar is depth- or frame-culled in this env
+            // the whole avatar is depth- or frame-culled in this env, or wholly visible
+            code = cull[avatar] == kWholeVisible ? kKeep : cull[avatar];
+            if (code == kKeep) mask |= 1ull << e;
         } else if (input) {
             double p[3], q[4];
             const bool staged = avatar == a_lo || avatar == a_hi;

@@ -199,7 +199,11 @@ __global__ void __launch_bounds__(256) avatar_extent_kernel(sn_avatars av, unsig
         unsigned long long *e = s_ext + (a == a_lo ? 0 : slots);
         const double *p = av.pos_opacity + 4 * g, *l = av.log_scales + 4 * g;
         const double r = sqrt((p[0] * p[0] + p[1] * p[1]) + p[2] * p[2]);
-        const double sm = exp(fmax(fmax(l[0], l[1]), l[2]));
+        // (a non-finite rotation poisons the scale bound too: its covariance, hence the reference's
+        // degenerate test, cannot be bounded)
+        const double *qq = av.rotations + 4 * g;
+        const bool q_ok = isfinite(qq[0]) && isfinite(qq[1]) && isfinite(qq[2]) && isfinite(qq[3]);
+        const double sm = q_ok ? exp(fmax(fmax(l[0], l[1]), l[2])) : INFINITY;
         // non-negative doubles order like their bit patterns; NaN/inf poison the bound (no culling)
         atomicMax(e, (unsigned long long)__double_as_longlong(r == r ? r : INFINITY));
         atomicMax(e + 1, (unsigned long long)__double_as_longlong(sm == sm ? sm : INFINITY));
@@ -237,6 +241,10 @@ __global__ void __launch_bounds__(256) avatar_extent_kernel(sn_avatars av, unsig
 // kCullFrame: the ball is strictly inside (near, far), every covariance is finite (so det > 1e-12:
 // cov2d >= 0.3 I), and even with the largest projected radius 3 sqrt(||J||_F^2 s_max^2 + 0.3)
 // (>= 3 sqrt(lambda_max)) every mean misses the frame on one side (projection.py:160-166).
+// kWholeVisible: the ball is strictly inside (near, far), every mean lands inside the frame (so the
+// inclusive 3-sigma frame test passes whatever the radius), and that radius bound stays below
+// 3000 px, so the cov2d entries stay below 1e6 and the float64 determinant cannot fall to the
+// degenerate threshold (>= 0.09 - 1e-4): every gaussian is kept without being skinned.
 // 0: test every gaussian.
 __global__ void avatar_cull_kernel(sn_avatars av, PoseView pv, const double *pose_t, const sn_camera *cams,
                                    const unsigned long long *ext, int n_envs, uint8_t *codes) {
@@ -290,6 +298,9 @@ __global__ void avatar_cull_kernel(sn_avatars av, PoseView pv, const double *pos
             if (mx_hi + r < -mw || mx_lo - r > (double)c.width + mw || my_hi + r < -mw ||
                 my_lo - r > (double)c.height + mw)
                 code = kCullFrame;
+            else if (r < 3000.0 && mx_lo > mw && mx_hi < (double)c.width - mw && my_lo > mw &&
+                     my_hi < (double)c.height - mw)
+                code = kWholeVisible;
         }
     }
     codes[ea] = code;
