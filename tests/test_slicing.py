@@ -17,6 +17,25 @@ pytestmark = pytest.mark.gpu
 KEYS = ("color", "alpha", "depth", "contrib_scene", "stats")
 
 
+def _same_layer_render(got, ref, keys_exact=("contrib_scene", "contrib_layer", "stats")):
+    """Sliced vs unsliced renders with the avatar layer: discrete outputs identical; the continuous
+    ones equal up to float32 rounding. (The composite recomputes a scene pixel in float64 when the
+    layer's exact depth falls inside the scene depth's error band, and that bound depends on which
+    splats the CTA gathered -- the batch structure, which slicing changes -- so a handful of pixels
+    can take the exact recompute in one render and the certified float32 value in the other: the
+    same decisions, colours differing in the last bits.)"""
+    for k in keys_exact:
+        if k in ref:
+            assert torch.equal(got[k], ref[k]), k
+    for k in ("color", "alpha"):  # (observed <= 8.4e-7 on ~50 pixels of 80 envs)
+        assert (got[k] - ref[k]).abs().max().item() <= 2e-6, k
+    assert ((got["depth"] - ref["depth"]).abs() <= 5e-6 * ref["depth"].abs()).all()
+    if "rgb8" in ref:
+        assert (got["rgb8"].int() - ref["rgb8"].int()).abs().max().item() <= 1
+        d16 = got["depth16"].view(torch.float16).float(), ref["depth16"].view(torch.float16).float()
+        assert ((d16[0] - d16[1]).abs() <= 1e-3 * d16[1].abs()).all()
+
+
 def _render(scene, cams, bg, near_slice, stats=True, **kw):
     from paper_2604_12626_b200 import _native as N
     from paper_2604_12626_b200 import renderer as R
@@ -63,7 +82,7 @@ def test_sliced_render_matches_oracle():
 
 def test_sliced_scene_under_avatar_layer():
     """The layer's float64 fixups recompute scene pixels (the composite's back layer) through the
-    sliced pass's near list and far buckets."""
+    sliced pass's near list and far buckets (same decisions; see _same_layer_render)."""
     from paper_2604_12626_b200.batch import BatchRenderer
     box = S.room_box(1_000_000)
     scene = S.make_scene(250_000, box[0], box[1], seed=171)
@@ -78,8 +97,7 @@ def test_sliced_scene_under_avatar_layer():
             o = br.render(cams, times, contrib=True, stats=True, views=False, near_slice=ns, payload=True)
         outs.append(o)
     for o in outs[1:]:
-        for k in ("color", "alpha", "depth", "contrib_scene", "contrib_layer", "stats", "rgb8", "depth16"):
-            assert torch.equal(o[k], outs[0][k]), k
+        _same_layer_render(o, outs[0])
 
 
 def test_sliced_capacity_growth_and_exact_mode():
@@ -186,5 +204,23 @@ def test_lazy_far_classification_without_stats():
             o = br.render(cams, times, contrib=True, stats=ns == 0, views=False, near_slice=ns, payload=True)
         outs.append(o)
     for o in outs[1:]:
-        for k in ("color", "alpha", "depth", "contrib_scene", "contrib_layer", "rgb8", "depth16"):
-            assert torch.equal(o[k], outs[0][k]), k
+        _same_layer_render(o, outs[0], keys_exact=("contrib_scene", "contrib_layer"))
+
+
+def test_sliced_multi_chunk_with_avatars():
+    """More envs than one chunk (64): every chunk's slice, far buckets and fixup passes use the
+    chunk's own buffers -- frames, counts and stats equal the unsliced render, with the avatar layer."""
+    from paper_2604_12626_b200.batch import BatchRenderer
+    box = S.room_box(1_000_000)
+    scene = S.make_scene(150_000, box[0], box[1], seed=221)
+    bundles = [S.make_avatar(2000, seed=222 + i, n_frames=8, floor_lo=(2.0, 2.0), floor_hi=(6.0, 6.0))
+               for i in range(2)]
+    cams = S.room_cameras(80, box, seed=223, width=96, height=64)
+    times = np.linspace(0.0, 0.5, 80)
+    outs = []
+    for ns in (0, 30):
+        br = BatchRenderer(scene, bundles, start_offsets=[0.0, 0.2], background=(0.4, 0.5, 0.6))
+        for _ in range(2):
+            o = br.render(cams, times, contrib=True, stats=True, views=False, near_slice=ns)
+        outs.append(o)
+    _same_layer_render(outs[1], outs[0])
