@@ -171,7 +171,8 @@ typedef struct sn_render_opts {
     int32_t near_slice;     /* depth slicing of the scene pass: only each env's near depth slice is
                                sorted and streamed; the few tiles that exhaust it with unsaturated
                                pixels continue through a per-tile bucket of the far splats, in depth
-                               order (the same frames, counts and stats). -1 auto (scenes of >= 500k
+                               order (the same decisions, counts and stats; frames bit-identical
+                               without an avatar layer, within float32 rounding with one). -1 auto (scenes of >= 500k
                                gaussians rendered without harness views), 0 off, 1 on (envs with
                                too few visible splats stay unsliced), 2..1000: on for every env with
                                the slice at near_slice / 1000 of its sampled depths (tests, tuning);
