@@ -83,7 +83,7 @@ double near_frac() {
     static const double f = [] {
         const char *e = std::getenv("SN_NEAR_FRAC");
         const double v = e ? std::atof(e) : 0.0;
-        return v > 0.0 && v <= 1.0 ? v : 0.08;
+        return v > 0.0 && v <= 1.0 ? v : 0.05;
     }();
     return f;
 }
