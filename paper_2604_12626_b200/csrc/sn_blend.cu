@@ -1361,6 +1361,214 @@ __global__ void __launch_bounds__(kBlock, SN_LAYER_PX1_MIN_BLOCKS) blend_kernel_
     }
 }
 
+// The avatar layer's listed blend with TWO 8 x 4 pixel blocks per warp (SN_LAYER_LP2): 128-thread
+// CTAs, warp w owning blocks w and 7 - w of the tile (opposite corners: a cluster of small splats
+// loads one corner, so the pair evens out what a warp per block leaves to the slowest warp at each
+// barrier). Per batch the CTA gathers the tile list's records once, each warp builds a list per
+// block and walks them one after the other with that block's pixel state (no lane idles for the
+// other block, unlike a paired-pixel chain). Numerics, outputs and fixups are blend_kernel_px1's
+// (MODE 2, SOURCE 1): the same per-pixel float32 chain, in the same order.
+#ifndef SN_LAYER_LP2
+#define SN_LAYER_LP2 1
+#endif
+#ifndef SN_LAYER_LP2_MIN_BLOCKS
+#define SN_LAYER_LP2_MIN_BLOCKS 8
+#endif
+#ifndef SN_LAYER_LP2_PER_THREAD
+#define SN_LAYER_LP2_PER_THREAD 2  // records per thread per batch
+#endif
+constexpr int kLT = 128;           // threads per layer CTA
+constexpr int kLWarps = kLT / 32;  // 4 warps x 2 blocks = the tile's 8 blocks
+__global__ void __launch_bounds__(kLT, SN_LAYER_LP2_MIN_BLOCKS) blend_kernel_lp2(BlendArgs b) {
+    constexpr int kPerT = SN_LAYER_LP2_PER_THREAD;
+    constexpr int kBatch = kLT * kPerT;
+    __shared__ FRec1 s_f[kBatch];
+    __shared__ uint32_t s_slot[kBatch];
+    __shared__ uint8_t s_mask[kBatch];  // bit k: the splat's support may reach block k (8 x 4)
+    __shared__ uint16_t s_wl[kLWarps][2][kBatch];
+    __shared__ int s_item;
+    const PassView &v = b.pv;
+    if (pass_overflow(v)) return;
+    const int n_tiles_all = tiles_of(b.width) * tiles_of(b.height);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int blk[2] = {warp, 7 - warp};
+    const uint32_t n_items = *v.n_list;
+    while (true) {
+        if (threadIdx.x == 0) s_item = (int)atomicAdd(v.list_next, 1u);
+        __syncthreads();
+        const int item = s_item;
+        __syncthreads();
+        if ((uint32_t)item >= n_items) break;
+        const uint32_t key = v.tile_list[item];
+        const int tile = (int)(key & ((1u << v.tile_bits) - 1u)), el = (int)(key >> v.tile_bits);
+        const int env = b.e0 + el;
+        const int tx = tile % b.tiles_x, ty = tile / b.tiles_x;
+        const uint2 rg = v.ranges[((uint32_t)el << v.tile_bits) | (uint32_t)tile];
+        uint32_t cursor = rg.x;
+        const uint32_t s1 = rg.y;
+        if (threadIdx.x == 0) b.tile_flag[(int64_t)el * n_tiles_all + tile] = cursor != s1;
+        const double x0 = tx * kTile, y0 = ty * kTile;
+        int px_i[2], py_i[2];
+        bool inside[2];
+        float T[2], A[2], err[2], eps_max[2], z_first[2], z_last[2], dead[2];
+        f32x2 crg[2], cbd[2], o2x[2], o2y[2];
+        int nc[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int lx = (blk[q] & 1) * 8 + (lane & 7), ly = (blk[q] >> 1) * 4 + (lane >> 3);
+            px_i[q] = tx * kTile + lx;
+            py_i[q] = ty * kTile + ly;
+            inside[q] = px_i[q] < b.width && py_i[q] < b.height;
+            const float oxf = (float)lx - 7.5f, oyf = (float)ly - 7.5f;
+            o2x[q] = pack2(oxf, oxf);
+            o2y[q] = pack2(oyf, oyf);
+            T[q] = 1.0f;
+            A[q] = err[q] = eps_max[q] = z_last[q] = 0.0f;
+            z_first[q] = 3.0e38f;
+            crg[q] = cbd[q] = 0ull;
+            nc[q] = 0;
+            dead[q] = (!inside[q] || b.force_exact) ? INFINITY : 0.0f;
+        }
+        uint32_t loaded = 0;
+        while (true) {
+            if (__syncthreads_count(dead[0] == 0.0f || dead[1] == 0.0f) == 0) break;  // guards s_f reuse
+            const int n = (int)min((uint32_t)kBatch, s1 - cursor);
+            if (n <= 0) break;
+            loaded += n;
+#pragma unroll
+            for (int r = 0; r < kPerT; ++r) {
+                const int jt = threadIdx.x + r * kLT;
+                if (jt >= n) break;
+                const uint32_t rid = __ldg(v.pair_vals + cursor + jt);
+                const GatheredSplat gs = gather_splat(v.geo, v.recs, rid);
+                FRec1 f;
+                const unsigned msk = tile_entry_8x4(gs.e1x, gs.e1y, gs.p1, gs.p2, gs.gl, gs.gr, x0 + 8.0, y0 + 8.0, f);
+                if (msk) s_f[jt] = f;
+                s_slot[jt] = rid;
+                s_mask[jt] = (uint8_t)msk;
+            }
+            __syncthreads();
+            int cnt[2] = {0, 0};
+            for (int j0 = 0; j0 < n; j0 += 32) {
+                const unsigned mk = j0 + lane < n ? s_mask[j0 + lane] : 0u;
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const bool mine = (mk >> blk[q]) & 1u;
+                    const unsigned bal = __ballot_sync(kFull, mine);
+                    if (mine) s_wl[warp][q][cnt[q] + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)(j0 + lane);
+                    cnt[q] += __popc(bal);
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const uint16_t *wl = s_wl[warp][q];
+                if (cnt[q] > 0) z_first[q] = fminf(z_first[q], s_f[wl[0]].z);
+                const double px = px_i[q] + 0.5, py = py_i[q] + 0.5;
+                float Tq = T[q], Aq = A[q], errq = err[q], em = eps_max[q], zl = z_last[q], dq = dead[q];
+                f32x2 crgq = crg[q], cbdq = cbd[q];
+                int ncq = nc[q];
+                for (int k0 = 0; k0 < cnt[q] && !__all_sync(kFull, dq != 0.0f); k0 += 32) {
+                    const int k1 = min(cnt[q], k0 + 32);
+#pragma unroll kWalkUnroll
+                    for (int k = k0; k < k1; ++k) {
+                        const int j = wl[k];
+                        const FRec1 &sr = s_f[j];
+                        const float4 q0 = *reinterpret_cast<const float4 *>(&sr.a1x);
+                        const float4 q1 = *reinterpret_cast<const float4 *>(&sr.V1);
+                        float v1, v2;
+                        unpack2(fma2(pack2(q0.x, q0.y), o2x[q], fma2(pack2(q0.z, q0.w), o2y[q], pack2(q1.x, q1.y))), v1,
+                                v2);
+                        float d2 = __fmaf_rn(v1, v1, __fmaf_rn(v2, v2, dq));
+                        if (d2 > q1.z) continue;
+                        const float4 q2 = *reinterpret_cast<const float4 *>(&sr.ka);
+                        float eps;
+                        if (d2 < q1.w) {
+                            eps = __fmaf_rn(d2, q2.x, q2.y);
+                        } else {  // boundary band: the reference's float64 test (_kernels_cy.pyx:73-75)
+                            const SplatRec &sd = v.recs[s_slot[j]];
+                            const double ddx = sd.mx - px, ddy = sd.my - py;
+                            const double d2d = (sd.ca * ddx * ddx + sd.cb2 * ddx * ddy) + sd.cc * ddy * ddy;
+                            if (d2d > kSupportD2) continue;
+                            d2 = (float)(d2d * kHalfLog2e);
+                            eps = kEpsExact;
+                        }
+                        const float e = ex2_approx(-d2);
+                        const float a = fminf(q2.z * e, 0.99f);
+                        const float w = a * Tq;
+                        const float Tn = __fmaf_rn(-a, Tq, Tq);
+                        const float4 q3 = *reinterpret_cast<const float4 *>(&sr.r);
+                        crgq = fma2(pack2(q3.x, q3.y), pack2(w, w), crgq);
+                        cbdq = fma2(pack2(q3.z, q3.w), pack2(w, w), cbdq);
+                        Aq = Aq + w;
+                        errq = __fmaf_rn(-a, errq, __fmaf_rn(w, eps, __fmaf_rn(Tn, kU125, errq)));
+                        Tq = Tn;
+                        ++ncq;
+                        em = fmaxf(em, eps);
+                        zl = fmaxf(zl, q3.w);
+                        if (Tn - errq <= kTHi) dq = INFINITY;
+                    }
+                }
+                T[q] = Tq;
+                A[q] = Aq;
+                err[q] = errq;
+                eps_max[q] = em;
+                z_last[q] = zl;
+                dead[q] = dq;
+                crg[q] = crgq;
+                cbd[q] = cbdq;
+                nc[q] = ncq;
+            }
+            cursor += n;
+        }
+        if (b.loads && threadIdx.x == 0 && loaded) atomicAdd(b.loads, (unsigned long long)loaded);
+        const sn_camera &cam = b.cams[env];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {  // blend_kernel_px1's MODE 2 epilogue, per block
+            float cr, cg, cb, D;
+            unpack2(crg[q], cr, cg);
+            unpack2(cbd[q], cb, D);
+            const float Tq = T[q], errq = err[q], Aq = A[q];
+            const bool cut = Tq - errq <= kTHi;
+            const bool amb = inside[q] && (b.force_exact || (cut && (!(Tq + errq < kTLo) || errq > 0.0625f * Tq)));
+            const int64_t pix = ((int64_t)env * b.height + py_i[q]) * b.width + px_i[q];
+            const uint32_t code = (uint32_t)(((int64_t)el * b.height + py_i[q]) * b.width + px_i[q]);
+            const float zf = nc[q] == 0 ? 3.0e38f : z_first[q];
+            const float rho_w = errq / Tq + eps_max[q] + 6.0e-8f;
+            const float alpha = fminf(Aq, 1.0f);
+            const float depth = Aq > 0.0f ? D / Aq : (float)cam.far_;
+            const float d_err = 1.01f * (rho_w * (z_last[q] - zf) + (float)(2 * nc[q] + 2) * 6.0e-8f * depth);
+            const bool flag = inside[q] && amb;
+            if (b.contribs) {
+                const unsigned sum = __reduce_add_sync(kFull, flag ? 0u : (unsigned)nc[q]);
+                if (lane == 0 && sum) atomicAdd(b.contribs, (unsigned long long)sum);
+            }
+            push_fixup(b, flag, code);
+            if (!inside[q]) continue;
+            if (flag) {
+                b.ldepth[pix] = __int_as_float(0x7fc00000);  // NaN: pending float64 fixup
+                continue;
+            }
+            if (b.contrib) b.contrib[pix] = nc[q];
+            float fc0 = 0.0f, fc1 = 0.0f, fc2 = 0.0f;
+            if (Aq > 0.0f) {
+                fc0 = np_clipf(cr / Aq, 0.0f, 1.0f);
+                fc1 = np_clipf(cg / Aq, 0.0f, 1.0f);
+                fc2 = np_clipf(cb / Aq, 0.0f, 1.0f);
+            }
+            float *lc = b.lcolor + 3 * pix;
+            lc[0] = fc0;
+            lc[1] = fc1;
+            lc[2] = fc2;
+            b.lalpha[pix] = alpha;
+            b.ldepth[pix] = depth;
+            b.lderr[pix] = d_err;
+            b.laerr[pix] = 1.01f * (rho_w + (float)(nc[q] + 1) * 6.0e-8f) * Aq + 6.0e-8f;
+        }
+        __syncthreads();  // the next tile reuses the shared buffers
+    }
+}
+
 // composite(front = avatar layer, back = scene frame), renderer.py:151-166, for the layer frame the
 // mode-2 blend left in its buffers. Decisions (front.depth < back.depth, alpha >= 0.5) are taken
 // only when the tracked float32 error bounds separate them; other pixels join the fixup list and
@@ -2122,6 +2330,8 @@ static void launch_blend_mode(const BlendArgs &b, dim3 grid, cudaStream_t s, boo
     if constexpr (MODE == 2) {  // the avatar layer: one pixel per thread (see blend_kernel_px1)
         if (b.pv.source == 0)
             blend_kernel_px1<MODE, 0><<<grid, kBlock, 0, s>>>(b);
+        else if (b.pv.source == 1 && b.pv.tile_list && SN_LAYER_LP2)  // listed, two blocks per warp
+            blend_kernel_lp2<<<148 * SN_LAYER_LP2_MIN_BLOCKS, kLT, 0, s>>>(b);
         else if (b.pv.source == 1 && b.pv.tile_list)  // listed: a few CTAs per SM take the non-empty tiles
             blend_kernel_px1<MODE, 1><<<148 * SN_LAYER_PX1_MIN_BLOCKS, kBlock, 0, s>>>(b);
         else if (b.pv.source == 1)
