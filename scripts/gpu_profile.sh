@@ -13,6 +13,6 @@ echo "launch rc=$?" >> gpurun_out/ncu_launch.log
 C="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
 $C > gpurun_out/plain_full.log 2>&1 && \
 timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k regex:"${NCU_REGEX:-blend_kernel<0, 0>|blend_kernel_px1|scene_emit|scene_count|avatar_count|avatar_emit|fixup_kernel<0>}" -s ${NCU_SKIP:-21} -c ${NCU_COUNT:-8} -o gpurun_out/prof_full $C \
+    -k regex:"${NCU_REGEX:-blend_kernel<\(int\)0, \(int\)0>|blend_kernel_lp2|scene_emit|scene_count|avatar_count|avatar_emit|fixup_kernel<\(int\)0>}" -s ${NCU_SKIP:-21} -c ${NCU_COUNT:-8} -o gpurun_out/prof_full $C \
     > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?" >> gpurun_out/ncu_full.log

@@ -10,7 +10,7 @@ import json
 import subprocess
 import sys
 
-STAGE_OF = {"blend_kernel<0, 0>": "scene.blend", "blend_kernel_px1<2, 1>": "layer.blend",
+STAGE_OF = {"blend_kernel<0, 0>": "scene.blend", "blend_kernel_lp2": "layer.blend",
             "scene_emit_kernel": "scene.emit", "scene_count_kernel": "scene.count",
             "fixup_kernel<0>": "scene.fixup", "fixup_kernel<2>": "layer.fixup"}
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
