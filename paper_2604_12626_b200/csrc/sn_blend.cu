@@ -1374,6 +1374,10 @@ __global__ void __launch_bounds__(kBlock, SN_LAYER_PX1_MIN_BLOCKS) blend_kernel_
 #ifndef SN_LAYER_LP2_MIN_BLOCKS
 #define SN_LAYER_LP2_MIN_BLOCKS 8
 #endif
+#ifndef SN_LP2_UNROLL
+#define SN_LP2_UNROLL 1  // the walk's unroll (measured: 1 > 2, 4 -- smaller code beside the scene blend)
+#endif
+constexpr int kLp2Unroll = SN_LP2_UNROLL;
 #ifndef SN_LAYER_LP2_PER_THREAD
 #define SN_LAYER_LP2_PER_THREAD 2  // records per thread per batch
 #endif
@@ -1470,7 +1474,7 @@ __global__ void __launch_bounds__(kLT, SN_LAYER_LP2_MIN_BLOCKS) blend_kernel_lp2
                 int ncq = nc[q];
                 for (int k0 = 0; k0 < cnt[q] && !__all_sync(kFull, dq != 0.0f); k0 += 32) {
                     const int k1 = min(cnt[q], k0 + 32);
-#pragma unroll kWalkUnroll
+#pragma unroll kLp2Unroll
                     for (int k = k0; k < k1; ++k) {
                         const int j = wl[k];
                         const FRec1 &sr = s_f[j];
