@@ -95,7 +95,7 @@ constexpr float kTLo = 9.99999e-05f;   // 1e-4 (1 - 1e-6): below it (with the bo
 constexpr float kTHi = 1.000001e-04f;  // 1e-4 (1 + 1e-6)
 constexpr float kNegHalfLog2e = -0.72134752044448170f;
 #ifndef SN_WALK_UNROLL
-#define SN_WALK_UNROLL 4
+#define SN_WALK_UNROLL 8
 #endif
 constexpr int kWalkUnroll = SN_WALK_UNROLL;  // walk loop unroll (entries per iteration)
 // the blend works on h = d2 log2(e) / 2 (so e^(-d2/2) = 2^-h): its axes carry sqrt(log2(e) / 2)
