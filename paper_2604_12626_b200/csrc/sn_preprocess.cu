@@ -212,7 +212,7 @@ __device__ __forceinline__ void load_scene(const sn_cloud &c, int64_t g, double 
 #define SN_EMIT_ROUND 16
 #endif
 #ifndef SN_COUNT_ROUND
-#define SN_COUNT_ROUND 8
+#define SN_COUNT_ROUND 16
 #endif
 constexpr int kEmitRound = SN_EMIT_ROUND;
 constexpr int kCountRound = SN_COUNT_ROUND;  // the count kernel's rounds (in-depth items)
