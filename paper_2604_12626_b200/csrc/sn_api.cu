@@ -1504,3 +1504,13 @@ extern "C" int sn_debug_far_caps(sn_context *ctx, uint32_t cap_u, uint64_t cap_f
     ctx->pass[0].cap_b = cap_b;
     return SN_OK;
 }
+
+// Diagnostic (not part of the ABI): the whole-avatar codes of the last render with an avatar set,
+// (env, avatar) row-major: 0 test every gaussian, kCullDepth / kCullFrame, kWholeVisible (4).
+extern "C" int sn_debug_avatar_codes(sn_context *ctx, uint8_t *out, int64_t n) {
+    SN_CHECK(ctx != nullptr && out != nullptr && n >= 0, "bad argument");
+    SN_CHECK(ctx->av_cull.p != nullptr, "no render with an avatar set yet");
+    SN_CUDA(cudaDeviceSynchronize());
+    SN_CUDA(cudaMemcpy(out, ctx->av_cull.p, (size_t)n, cudaMemcpyDeviceToHost));
+    return SN_OK;
+}

@@ -581,3 +581,35 @@ def test_random_scale_spread_against_oracle(seed):
                         o.color, o.alpha, o.depth, cams[e].far)
             assert out["stats"][e].tolist() == [o.stats[k] for k in ("n_input", "n_culled_depth", "n_culled_frame",
                                                                      "n_degenerate", "n_drawn")]
+
+
+def test_whole_avatar_visibility_code():
+    """An avatar whose bounding ball projects strictly inside the frame and depth range is kept
+    without per-gaussian skinning in the count (code kWholeVisible = 4): the layer's kept set,
+    order and contributor counts must still be the oracle's."""
+    import ctypes
+    from paper_2604_12626_b200 import _native as N
+    from paper_2604_12626_b200 import rig
+    from paper_2604_12626_b200.batch import BatchRenderer
+    from paper_2604_12626_b200.camera import Camera, pose_world_to_camera
+    from paper_2604_12626_b200.cloud import concat_clouds
+    box = S.room_box(1_000_000)
+    scene = S.make_scene(30_000, box[0], box[1], seed=301)
+    bundles = [S.make_avatar(3000, seed=302, n_frames=6, floor_lo=(4.0, 4.0), floor_hi=(4.0, 4.0))]
+    cams = [Camera.from_hfov(320, 240, 90.0, 0.1, 100.0, pose_world_to_camera(np.array([x, 4.0, 1.25]), 0.0))
+            for x in (0.5, 1.0, 0.0)]
+    times = np.array([0.0, 0.05, 0.1])
+    br = BatchRenderer(scene, bundles, background=(0.5, 0.5, 0.5))
+    out = br.render(cams, times, contrib=True, stats=True)
+    codes = (ctypes.c_uint8 * 3)()
+    lib = ctypes.CDLL(N.LIB_PATH)
+    assert lib.sn_debug_avatar_codes(br.context.handle, codes, ctypes.c_int64(3)) == 0
+    assert 4 in list(codes), list(codes)  # the whole-visible path was taken
+    for e in range(3):
+        clouds = [rig.AvatarRuntime(bundles[0]).deformed_cloud(float(times[e]))]
+        layer = concat_clouds(clouds)
+        lo = O.rasterize(layer, cams[e], None)
+        np.testing.assert_array_equal(out["contrib_layer"][e].cpu().numpy(), lo.contrib)
+        proj = O.project_cloud(layer, cams[e])
+        inter = R().pass_intermediates(1, e, context=br.context)
+        np.testing.assert_array_equal(inter["ids"], proj.ids.astype(np.int32))
