@@ -17,6 +17,8 @@
 #include "sn_common.cuh"
 #include "sn_internal.h"
 
+#include <type_traits>
+
 namespace sn {
 
 namespace {
@@ -285,33 +287,42 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
     unsigned out_lo = 0, out_hi = 0, fz_lo = 0, fz_hi = 0;
     const bool want_out = a.stats != nullptr;
     // one half (32 envs) of the chunk: 32-bit masks, no 64-bit variable shifts in the loop
-    auto depth_half = [&](const int e0, const int e1, unsigned &in_m, unsigned &fz_m, unsigned &out_c,
-                          unsigned &fz_c) {
+    // (branch-free per env: an invalid thread's p is 0, its z finite and masked by `valid`; the
+    // counters wanted are compile-time variants of the loop)
+    auto depth_half = [&](auto lazy_tag, auto out_tag, const int e0, const int e1, unsigned &in_m, unsigned &fz_m,
+                          unsigned &out_c, unsigned &fz_c) {
+        constexpr bool kLazy = decltype(lazy_tag)::value, kOut = decltype(out_tag)::value;
         in_m = fz_m = 0u;
         for (int e = e0; e < e1; ++e) {
-            bool in = false, fz = false;
-            if (valid) {
-                const sn_camera &cam = s_cam[e];
-                double z = cam_z(p, cam);
-                in = (z > cam.near_) && (z < cam.far_);
-                fz = a.lazy_far && in && !(z < s_zcut[e]);
-            }
+            const sn_camera &cam = s_cam[e];
+            const double z = cam_z(p, cam);
+            const bool in = valid && (z > cam.near_) && (z < cam.far_);
+            const bool fz = kLazy && in && !(z < s_zcut[e]);
             in_m |= (unsigned)(in && !fz) << (e - e0);
             fz_m |= (unsigned)fz << (e - e0);
             const bool mine = lane == e - e0;
-            if (want_out) {
+            if (kOut) {
                 const unsigned c = __popc(__ballot_sync(kFull, valid && !in));
                 if (mine) out_c = c;
             }
-            if (a.lazy_far) {
+            if (kLazy) {
                 const unsigned c = __popc(__ballot_sync(kFull, fz));
                 if (mine) fz_c = c;
             }
         }
     };
-    unsigned in_lo, in_hi = 0u, far_lo, far_hi = 0u;
-    depth_half(0, min(a.ec, 32), in_lo, far_lo, out_lo, fz_lo);
-    if (a.ec > 32) depth_half(32, a.ec, in_hi, far_hi, out_hi, fz_hi);
+    auto depth_all = [&](auto lazy_tag, auto out_tag, unsigned &in_lo, unsigned &in_hi, unsigned &far_lo,
+                         unsigned &far_hi) {
+        depth_half(lazy_tag, out_tag, 0, min(a.ec, 32), in_lo, far_lo, out_lo, fz_lo);
+        if (a.ec > 32) depth_half(lazy_tag, out_tag, 32, a.ec, in_hi, far_hi, out_hi, fz_hi);
+    };
+    unsigned in_lo = 0u, in_hi = 0u, far_lo = 0u, far_hi = 0u;
+    if (a.lazy_far)
+        depth_all(std::true_type{}, std::false_type{}, in_lo, in_hi, far_lo, far_hi);  // (lazy: no RenderStats)
+    else if (want_out)
+        depth_all(std::false_type{}, std::true_type{}, in_lo, in_hi, far_lo, far_hi);
+    else
+        depth_all(std::false_type{}, std::false_type{}, in_lo, in_hi, far_lo, far_hi);
     const uint64_t in_depth = ((uint64_t)in_hi << 32) | in_lo, far_z = ((uint64_t)far_hi << 32) | far_lo;
     if (lane < a.ec) {
         if (want_out && out_lo) atomicAdd(&s_cnt[lane][1], out_lo);
