@@ -55,6 +55,14 @@ def test_config3_6m_256_envs():
         if e == 255:
             proj = O.project_cloud(scene, cams[e])
             np.testing.assert_array_equal(R.pass_intermediates(0, e, context=ctx)["ids"], proj.ids.astype(np.int32))
+    # the throughput path at this scale: depth-sliced (auto), with RenderStats and without them (the
+    # lazy far classification) -- bit-identical to the unsliced render above, every env
+    for stats in (True, False):
+        for _ in range(2):  # (the first may grow the far capacities)
+            sl = R.render_frames(scene, cams, bg, contrib=True, stats=stats, views=False, context=ctx)
+        torch.cuda.synchronize()
+        for k in ("color", "alpha", "depth", "contrib_scene") + (("stats",) if stats else ()):
+            assert torch.equal(sl[k], out[k]), (stats, k)
 
 
 def _layer_checks(out, br, bundles, offs, scene, cams, times, envs, bg):
