@@ -101,6 +101,18 @@ def test_config4_shape_1024_envs_16_avatars():
     out = br.render(cams, times, contrib=True, stats=True)
     _layer_checks(out, br, bundles, offs, scene, cams, times, (0, 511, 1023), bg)
     assert int(out["contrib_layer"].sum()) > 0  # the layer is not empty across the batch
+    # the throughput path over all 1,024 envs: lean views and a forced 5% depth slice, with and
+    # without RenderStats -- the same decisions (contributor counts, stats), colours within float32
+    # rounding of the composite's float64 recomputes (see tests/test_slicing.py)
+    for stats in (True, False):
+        for _ in range(2):
+            sl = br.render(cams, times, contrib=True, stats=stats, views=False, near_slice=50)
+        torch.cuda.synchronize()
+        for k in ("contrib_scene", "contrib_layer") + (("stats",) if stats else ()):
+            assert torch.equal(sl[k], out[k]), (stats, k)
+        for k in ("color", "alpha"):
+            assert (sl[k] - out[k]).abs().max().item() <= 2e-6, (stats, k)
+        assert ((sl["depth"] - out["depth"]).abs() <= 5e-6 * out["depth"].abs()).all()
 
 
 def test_avatars_smaller_than_a_block():
