@@ -60,7 +60,8 @@ def defaults_for(config):
 def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=60)
+    p.add_argument("--steps", type=int, default=None,
+                   help="timed steps (default 60; the --impl reference arm, whose step is ~4 s of host work, 20)")
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", type=int, default=2, choices=[2, 4],
@@ -79,6 +80,8 @@ def parse(argv=None):
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-envs", type=int, default=0, help="env sample for the CPU baseline (0 = auto)")
     a = p.parse_args(argv)
+    if a.steps is None:
+        a.steps = 20 if a.impl == "reference" else 60
     d = defaults_for(a.config)
     for k, v in d.items():
         if getattr(a, k) is None:
