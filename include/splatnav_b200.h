@@ -228,7 +228,8 @@ int sn_render_async(sn_context *ctx, const sn_cloud *scene, const sn_cloud *laye
 int sn_render_wait(sn_context *ctx, int32_t *retry);
 
 /* Intermediates of the last sn_render pass (0 = scene, 1 = avatar layer) for env e, copied to
- * HOST buffers. sn_get_counts: visible splats and tile pairs. sorted_ids: original gaussian
+ * HOST buffers. The workspace holds one env chunk (<= 64 envs): e must lie in the last chunk the
+ * render processed (SN_ERR_INVALID otherwise); render a smaller batch to inspect other envs. sn_get_counts: visible splats and tile pairs. sorted_ids: original gaussian
  * index per depth rank (projection.py:184). tile_starts (T+1) / pair_splat (P): the tile CSR
  * with depth ranks as values (renderer.py:80-101). */
 int sn_get_counts(sn_context *ctx, int32_t pass, int32_t env, int64_t *n_visible, int64_t *n_pairs);
