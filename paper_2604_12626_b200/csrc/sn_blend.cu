@@ -1,10 +1,19 @@
 // sn_blend.cu -- K7/K8: per-tile front-to-back compositing with fused finalize / composite.
 //
-// One 256-thread CTA per (tile, env); thread = pixel, warp = 8 x 4 pixel block. The tile's
-// depth-ordered splats are walked in batches of 256: each thread gathers one 64-byte record into
-// shared memory, then every warp walks the batch entries whose support can reach its block
-// (a conservative per-warp mask), reading them as shared-memory broadcasts. A CTA-wide vote
-// (__syncthreads_count) stops the walk once every pixel is saturated.
+// Kernels (a tile is 16 x 16 pixels):
+//   blend_kernel      -- the scene pass: one 128-thread CTA per (tile, env), two pixels per thread
+//                        (rows ly, ly + 4 of the warp's 8 x 8 block) on packed float32-pair chains.
+//                        Sources: 0 the env's depth-sorted rectangles streamed with batch culling,
+//                        1 materialized tile lists, 2 every splat (rasterize_reference), 3 the
+//                        continuation of a depth-sliced pass's unfinished tiles over their far
+//                        buckets (sn_far.cu).
+//   blend_kernel_lp2  -- the avatar layer's listed blend: 128-thread CTAs taking the non-empty
+//                        (env, tile) pairs dynamically, each warp walking two 8 x 4 blocks.
+//   blend_kernel_px1  -- the layer's other sources: 256 threads, one pixel per thread.
+//   fixup_kernel / fixup_layer_kernel / composite_kernel -- float64 walks, the deferred composite.
+// Per batch the CTA gathers the next depth-ordered records into shared memory (their float32
+// principal-axis form and a per-warp block mask), each warp walks the entries whose support can
+// reach its block, and a CTA-wide vote (__syncthreads_count) stops once every pixel is saturated.
 //
 // Numerics (the reference is float64, _kernels_cy.pyx:64-86): the per-contribution chain runs in
 // float32 with a rigorous running error bound, and every discrete decision is either certain or
