@@ -1,10 +1,14 @@
 // sn_api.cu -- the C ABI (include/splatnav_b200.h): context/workspace and pass orchestration.
 //
 // A pass (scene, or the concatenated avatar layer) over a chunk of <= 64 envs is:
-//   count -> per-env block scan -> [sync: visible total] -> emit -> depth sort -> permute
-//   -> pair-offset scan -> [sync: pair total] -> duplicate -> pair sort -> ranges -> blend.
-// The two host syncs size the workspace; buffers only grow, so a steady-state batch loop
-// allocates nothing.
+//   [near cut] -> count -> per-env block scan -> emit -> depth sort + tie fix -> permute
+//   -> (avatar layer: pair-offset scan -> duplicate -> pair sort -> ranges) -> blend
+//   -> (sliced scene pass: fixups over the near lists -> far collect -> item sort -> continuation)
+//   -> fixups, and the layer's deferred composite on the scene stream.
+// No host round trip inside a render: buffers are sized by host-side capacities, the counts stay
+// on the device and are published to mapped host memory; sn_render_wait checks them afterwards
+// and a render that outgrew its buffers is re-run with larger ones (buffers only grow, so a
+// steady-state batch loop allocates nothing).
 #include <algorithm>
 #include <cstdlib>
 #include <cstdio>

@@ -4,10 +4,10 @@
 // Order contract (renderer.py:80-101 + projection.py:184): within each (env, tile) the splats
 // appear in (z, original index) order. The emit stage writes records env-major in index order;
 // a stable radix sort on the 64-bit key (env | z_bits - z_base) therefore yields the exact
-// lexsort order. Pairs are then emitted in (env, depth-rank) order and a stable sort on the
-// (env | tile) key alone (17 bits at 64 envs x 1,200 tiles) keeps depth order inside each tile,
-// which is the semantics of a 64-bit (env | tile | depth) key without sorting the depth bits
-// twice.
+// lexsort order (the sort runs on the top 32 bits; tie_fix orders equal-key runs by the float64 z
+// and index). Pairs are then emitted in (env, depth-rank) order and a stable sort on the tile bits
+// alone keeps every (env, tile) group contiguous and in depth order -- the semantics of a 64-bit
+// (env | tile | depth) key without sorting the env or depth bits again.
 #include "sn_common.cuh"
 #include "sn_internal.h"
 

@@ -6,8 +6,13 @@
 //   count: visibility bitmask per gaussian + per-(env, block) visible counts + RenderStats
 //          (warp ballots, aggregated in shared memory, one global atomic per block and field);
 //   emit:  recomputes geometry only for visible (gaussian, env) pairs and writes 64-byte splat
-//          records at order-preserving positions (env-major, gaussian index order within env),
-//          so a stable depth sort reproduces np.lexsort((idx, z)) (projection.py:184).
+//          records + 32-byte blend geometry at order-preserving positions (env-major, gaussian
+//          index order within env), so a stable depth sort reproduces np.lexsort((idx, z))
+//          (projection.py:184).
+// A depth-sliced scene pass (sn_render_opts.near_slice) adds near_cut (each env's depth cut), marks
+// the near items in the count and emits only those; the far ones are projected again, and only
+// where a tile needs them, by far_collect (sn_far.cu). Without RenderStats the count classifies
+// in-depth items beyond the cut as far from their depth alone (the lazy far classification).
 // Avatars (sn_avatars) run the same pipeline with LBS skinning fused in front of the
 // projection (rig.py:107-146): skinned positions/rotations never touch HBM.
 #include <cub/block/block_scan.cuh>

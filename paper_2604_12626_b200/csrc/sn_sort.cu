@@ -5,9 +5,11 @@
 // Sort, per digit pass (digit width <= 8 bits, passes = ceil(bits / 8)):
 //   upsweep   -- each 2048-item tile builds its digit histogram (per-warp shared-memory counters);
 //   rowscan   -- one CTA per digit scans that digit's per-tile counts (exclusive) and its total;
-//   downsweep -- each tile ranks its items stably (warp __match_any_sync peers + per-warp running
-//                counts, then a prefix over the tile's warps), stages them in digit order in shared
-//                memory and writes each digit's run to digit base + tile offset, coalesced.
+//   downsweep -- each tile ranks its items stably (warp peers from one ballot per digit bit, the
+//                warp's running count per digit from a returning shared atomic by each peer
+//                group's first lane, then a prefix over the tile's warps), stages them in digit
+//                order in shared memory and writes each digit's run to digit base + tile offset,
+//                coalesced.
 // Stable at every level (lane order within a round, round order within a warp's 256-item segment,
 // warp order within a tile, tile order in the scan), hence a stable LSD sort. Traffic per pass:
 // 4 B/item read (upsweep) + 8 B read + 8 B written (downsweep).
