@@ -224,3 +224,28 @@ def test_sliced_multi_chunk_with_avatars():
             o = br.render(cams, times, contrib=True, stats=True, views=False, near_slice=ns)
         outs.append(o)
     _same_layer_render(outs[1], outs[0])
+
+
+def test_slicing_edge_cases():
+    """near_slice = 1 (on, with the per-env size threshold: small envs stay unsliced), an empty
+    scene, and envs that see nothing (cameras looking out of the room) -- all equal to unsliced."""
+    box = S.room_box(1_000_000)
+    scene = S.make_scene(120_000, box[0], box[1], seed=231)
+    cams = S.room_cameras(6, box, seed=232, width=160, height=120)
+    from paper_2604_12626_b200.camera import Camera, pose_world_to_camera
+    # two cameras outside the box looking away from it: no visible splat at all
+    for x in (-50.0, 60.0):
+        cams.append(Camera.from_hfov(160, 120, 90.0, 0.1, 100.0,
+                                     pose_world_to_camera(np.array([x, 4.0, 1.25]), 0.0 if x > 0 else np.pi)))
+    bg = np.array([0.3, 0.6, 0.9])
+    ref, _ = _render(scene, cams, bg, 0)
+    for ns in (1, 20):
+        got, _ = _render(scene, cams, bg, ns)
+        for k in KEYS:
+            assert torch.equal(got[k], ref[k]), (ns, k)
+    assert int(ref["stats"][6:, 4].sum()) == 0  # (the outward cameras really see nothing)
+    empty = S.make_scene(0, box[0], box[1], seed=233)
+    ref, _ = _render(empty, cams, bg, 0)
+    got, _ = _render(empty, cams, bg, 20)
+    for k in KEYS:
+        assert torch.equal(got[k], ref[k]), ("empty", k)
