@@ -249,3 +249,46 @@ def test_slicing_edge_cases():
     got, _ = _render(empty, cams, bg, 20)
     for k in KEYS:
         assert torch.equal(got[k], ref[k]), ("empty", k)
+
+
+def test_pipelined_sliced_renders_retry_and_fall_back():
+    """sn_render_async / sn_render_wait with a sliced pass: a render that outgrew the far-half
+    capacities (tiny, set by the test hook) and one that set far_short (the fallback hook) both
+    report a retry; re-queued, they produce the unsliced frames."""
+    import ctypes
+    from paper_2604_12626_b200 import _native as N
+    from paper_2604_12626_b200 import renderer as R
+    lib = ctypes.CDLL(N.LIB_PATH)
+    lib.sn_debug_far_caps.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64]
+    box = S.room_box(1_000_000)
+    scene = S.make_scene(200_000, box[0], box[1], seed=241)
+    cams = S.room_cameras(6, box, seed=242, width=200, height=150)
+    bg = np.array([0.8, 0.7, 0.6])
+    ref, _ = _render(scene, cams, bg, 0)
+    ctx = N.Context()
+    kw = dict(contrib=True, stats=True, views=False, near_slice=20, context=ctx)
+    R.render_frames(scene, cams, bg, **kw)  # sizes the near buffers
+    assert lib.sn_debug_far_caps(ctx.handle, 2, 8, 8) == 0
+    out = R.render_frames(scene, cams, bg, wait=False, **kw)
+    assert ctx.render_wait()  # the far half outgrew its buffers
+    out = R.render_frames(scene, cams, bg, wait=False, **kw)
+    retried = ctx.render_wait()
+    if retried:  # (growth in stages: unfinished tiles, then their records and items)
+        out = R.render_frames(scene, cams, bg, wait=False, **kw)
+        assert not ctx.render_wait()
+    for k in KEYS:
+        assert torch.equal(out[k], ref[k]), k
+    assert lib.sn_debug_slice_hooks(1) == 0
+    try:
+        out = R.render_frames(scene, cams, bg, wait=False, **kw)
+        assert ctx.render_wait()  # far_short: re-run unsliced
+        for _ in range(3):  # (the unsliced re-run may first grow the near buffers to the full set)
+            out = R.render_frames(scene, cams, bg, wait=False, **kw)
+            if not ctx.render_wait():
+                break
+        else:
+            raise AssertionError("the unsliced re-run did not go through")
+    finally:
+        lib.sn_debug_slice_hooks(0)
+    for k in KEYS:
+        assert torch.equal(out[k], ref[k]), k
