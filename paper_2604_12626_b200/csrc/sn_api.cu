@@ -934,11 +934,11 @@ static int render_check(sn_context *ctx, int32_t *retry) {
         // against the capacities this render ran with (a later check may have grown them already)
         PassWs &w = ctx->pass[p];
         if (need_v > S->cap_v[p]) {
-            w.cap_v = std::max(w.cap_v, need_v + need_v / 4 + 1024);
+            w.cap_v = std::max(w.cap_v, need_v + need_v / 2 + 1024);  // (+50%: fresh camera sets vary)
             grow = true;
         }
         if (need_p > S->cap_p[p]) {
-            w.cap_p = std::max(w.cap_p, need_p + need_p / 4 + 1024);
+            w.cap_p = std::max(w.cap_p, need_p + need_p / 2 + 1024);
             grow = true;
         }
         // depth slicing: far splats, unfinished tiles (<= one per (env, tile)), far bucket items
