@@ -737,7 +737,9 @@ int sn_context_destroy(sn_context *ctx) {
         for (Buf *b : {&w.vismask, &w.blk_counts, &w.env_off, &w.keys_un, &w.keys_s, &w.vals_un, &w.vals_s, &w.recs_un, &w.geo_un,
                        &w.gid_un, &w.rects_un, &w.rects_tun, &w.rects, &w.tiles, &w.pair_off, &w.pkeys_a,
                        &w.pkeys_b, &w.pvals_a, &w.pvals_b, &w.ranges, &w.temp, &w.batch_rects, &w.super_rects,
-                       &w.fix, &w.counts, &w.tlist, &w.tlist_cnt})
+                       &w.fix, &w.counts, &w.tlist, &w.tlist_cnt, &w.zcut, &w.nearmask, &w.fctl, &w.unfin_list,
+                       &w.bucket_of, &w.state, &w.frec, &w.fgeo, &w.fgid, &w.franges, &w.bkey_a, &w.bkey_b,
+                       &w.bval_a, &w.bval_b, &w.ftemp})
             free_buf(*b);
     }
     for (Buf *b : {&ctx->cams, &ctx->times, &ctx->derr, &ctx->jm, &ctx->eq, &ctx->root, &ctx->err, &ctx->pose_q,
