@@ -75,6 +75,14 @@ int bit_length(uint64_t v) { return v == 0 ? 0 : 64 - __builtin_clzll(v); }
 // Depth slicing (sn_render_opts.near_slice): auto-on for scenes of at least this many gaussians
 // (rendered without harness views); the near slice is this quantile of each env's sampled depths
 // (SN_NEAR_FRAC overrides it, for tuning).
+// the far pipeline as a conditional graph (SN_FAR_GRAPH=0: plain launches)
+bool far_graphs_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("SN_FAR_GRAPH");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 // auto slicing (near_slice = -1) from this scene size up; SN_SLICE_MIN overrides (tuning)
 int64_t slice_min_gaussians() {
     static const int64_t m = [] {
@@ -158,6 +166,21 @@ struct sn_context {
     cudaEvent_t ev_work[2] = {};
     // side stream for the layer pass: its preprocessing overlaps the scene blend
     cudaStream_t side = nullptr;
+    // The far pipeline of a sliced pass as a small graph whose body runs only when the render
+    // registered an unfinished tile (a conditional node): the dozen kernels it launches are skipped
+    // on the device in the common case. Instantiated per distinct set of launch parameters (the
+    // graph bakes them in): a few cached, captured on a private stream.
+    struct FarGraph {
+        std::vector<unsigned char> shape, key;  // kernels + device-resident control words; all parameters
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        std::vector<cudaGraphNode_t> body;  // the body's kernel nodes in launch order
+    };
+    FarGraph far_graph[4];
+    int far_graph_next = 0;
+    int64_t far_graph_builds = 0, far_graph_updates = 0;  // instantiations / in-place parameter updates
+    int64_t far_body_launches = 0;  // kernels of the body (counted by render_check when it ran)
+    cudaStream_t cap_stream = nullptr;
     cudaEvent_t ev_inputs = nullptr, ev_scene = nullptr, ev_layer = nullptr;
     int64_t launches = 0;  // kernels of this library launched through the context
     int64_t retries = 0;   // renders re-run because a pass outgrew its buffers
@@ -596,7 +619,8 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
         fa.pv.far_phase = 1;
         ctx->launches += 1;
         SN_CUDA(launch_fixup(fa, st));
-        FarArgs f{};
+        FarArgs f;
+        std::memset(&f, 0, sizeof f);  // (the graph key compares bytes: padding too)
         f.e0 = e0;
         f.ec = ec;
         f.tiles_x = tiles_x;
@@ -617,22 +641,150 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
         f.ranges = w.franges.as<uint2>();
         f.z_base = z_base;
         f.z_bits = z_bits;
-        ctx->launches += 1;
-        SN_CUDA(launch_far_collect(*sp.scene, f, n, st));
-        const bool odd = radix_sort_pairs(w.ftemp.p, w.bkey_a.as<uint32_t>(), w.bval_a.as<uint32_t>(),
-                                          w.bkey_b.as<uint32_t>(), w.bval_b.as<uint32_t>(),
-                                          w.fctl.as<uint64_t>() + 1, w.cap_b, 32, st, &ctx->launches);
-        SN_CHECK(!odd, "far item sort: 32-bit keys take an even number of passes");
-        ctx->launches += 2;
-        SN_CUDA(launch_far_tie_fix(f, w.bkey_a.as<uint32_t>(), w.bval_a.as<uint32_t>(), st));
-        SN_CUDA(launch_far_ranges(f, w.bkey_a.as<uint32_t>(), st));
         BlendArgs cb2 = bl;
         cb2.pv = view_of(w);
-        ctx->launches += 2;
-        SN_CUDA(launch_continue(cb2, st));
         BlendArgs fb = cb2;  // the second fixup pass: the continuation's pixels and the deferred ones
         fb.fix_start = fix_start;
-        SN_CUDA(launch_fixup(fb, st));
+        const sn_cloud scene_c = *sp.scene;
+        // the far pipeline: far_collect, the item sort, tie fix, ranges, the continuation, fixup pass 2
+        int64_t body_launches = 0;
+        auto far_body = [&](cudaStream_t fs) -> int {
+            body_launches += 1;
+            SN_CUDA(launch_far_collect(scene_c, f, n, fs));
+            const bool odd = radix_sort_pairs(w.ftemp.p, w.bkey_a.as<uint32_t>(), w.bval_a.as<uint32_t>(),
+                                              w.bkey_b.as<uint32_t>(), w.bval_b.as<uint32_t>(),
+                                              w.fctl.as<uint64_t>() + 1, w.cap_b, 32, fs, &body_launches);
+            SN_CHECK(!odd, "far item sort: 32-bit keys take an even number of passes");
+            body_launches += 4;
+            SN_CUDA(launch_far_tie_fix(f, w.bkey_a.as<uint32_t>(), w.bval_a.as<uint32_t>(), fs));
+            SN_CUDA(launch_far_ranges(f, w.bkey_a.as<uint32_t>(), fs));
+            SN_CUDA(launch_continue(cb2, fs));
+            SN_CUDA(launch_fixup(fb, fs));
+            return SN_OK;
+        };
+        if (!far_graphs_enabled()) {
+            SN_CHECK(far_body(st) == SN_OK, sn_last_error());
+            ctx->launches += body_launches;
+        } else {
+            // shape: what fixes the graph's kernels (a cached graph of the same shape takes new
+            // parameters in place); key: every launch parameter the graph bakes in
+            const uint64_t shape_words[5] = {(uint64_t)(uintptr_t)w.fctl.p, (uint64_t)scene_c.dtype,
+                                             (uint64_t)cb2.mode, (uint64_t)(n > 0), (uint64_t)(w.cap_b > 0)};
+            std::vector<unsigned char> shape(sizeof shape_words);
+            std::memcpy(shape.data(), shape_words, sizeof shape_words);
+            std::vector<unsigned char> key(sizeof f + 2 * sizeof(BlendArgs) + sizeof(sn_cloud) + 8 * sizeof(uint64_t));
+            {
+                unsigned char *k = key.data();
+                std::memcpy(k, &f, sizeof f);
+                k += sizeof f;
+                std::memcpy(k, &cb2, sizeof cb2);
+                k += sizeof cb2;
+                std::memcpy(k, &fb, sizeof fb);
+                k += sizeof fb;
+                std::memcpy(k, &scene_c, sizeof scene_c);
+                k += sizeof scene_c;
+                const uint64_t extra[8] = {(uint64_t)n, (uint64_t)(uintptr_t)w.ftemp.p, (uint64_t)(uintptr_t)w.bkey_b.p,
+                                           (uint64_t)(uintptr_t)w.bval_b.p, w.cap_b, 0, 0, 0};
+                std::memcpy(k, extra, sizeof extra);
+            }
+            if (!ctx->cap_stream) SN_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+            cudaStream_t cs = ctx->cap_stream;
+            // the kernel nodes of a captured linear chain, in launch order
+            auto chain = [](cudaGraph_t g, std::vector<cudaGraphNode_t> &out) -> bool {
+                out.clear();
+                size_t nr = 1;
+                cudaGraphNode_t node = nullptr;
+                if (cudaGraphGetRootNodes(g, &node, &nr) != cudaSuccess || nr != 1) return false;
+                while (node) {
+                    cudaGraphNodeType t;
+                    if (cudaGraphNodeGetType(node, &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) return false;
+                    out.push_back(node);
+                    size_t nd = 0;
+                    if (cudaGraphNodeGetDependentNodes(node, nullptr, &nd) != cudaSuccess || nd > 1) return false;
+                    cudaGraphNode_t next = nullptr;
+                    if (nd == 1 && cudaGraphNodeGetDependentNodes(node, &next, &nd) != cudaSuccess) return false;
+                    node = nd == 1 ? next : nullptr;
+                }
+                return true;
+            };
+            sn_context::FarGraph *fg = nullptr;
+            for (auto &c : ctx->far_graph)
+                if (c.exec && c.key == key) fg = &c;
+            if (!fg) {  // same shape: capture the body alone and move its parameters into the cached graph
+                for (auto &c : ctx->far_graph)
+                    if (!fg && c.exec && c.shape == shape) fg = &c;
+                bool updated = false;
+                if (fg) {
+                    SN_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+                    body_launches = 0;
+                    const int rb = far_body(cs);
+                    cudaGraph_t tmp = nullptr;
+                    const cudaError_t ec2 = cudaStreamEndCapture(cs, &tmp);
+                    SN_CHECK(rb == SN_OK, sn_last_error());
+                    SN_CUDA(ec2);
+                    std::vector<cudaGraphNode_t> nodes;
+                    updated = chain(tmp, nodes) && nodes.size() == fg->body.size();
+                    for (size_t i = 0; updated && i < nodes.size(); ++i) {
+                        cudaKernelNodeParams kp;
+                        updated = cudaGraphKernelNodeGetParams(nodes[i], &kp) == cudaSuccess &&
+                                  cudaGraphExecKernelNodeSetParams(fg->exec, fg->body[i], &kp) == cudaSuccess;
+                    }
+                    cudaGraphDestroy(tmp);
+                    cudaGetLastError();  // (a refused update falls back to a new instantiation)
+                    if (updated) {
+                        fg->key = std::move(key);
+                        ctx->far_graph_updates += 1;
+                    }
+                }
+                if (!updated) {
+                    if (!fg) {
+                        fg = &ctx->far_graph[ctx->far_graph_next];
+                        ctx->far_graph_next = (ctx->far_graph_next + 1) % 4;
+                    }
+                    if (fg->exec) cudaGraphExecDestroy(fg->exec);
+                    if (fg->graph) cudaGraphDestroy(fg->graph);
+                    fg->exec = nullptr;
+                    fg->graph = nullptr;
+                    cudaGraph_t g = nullptr;
+                    SN_CUDA(cudaGraphCreate(&g, 0));
+                    fg->graph = g;
+                    cudaGraphConditionalHandle h;
+                    SN_CUDA(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
+                    SN_CUDA(cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+                    SN_CUDA(launch_far_cond(h, w.fctl.as<unsigned long long>(), cs));
+                    cudaStreamCaptureStatus cst;
+                    const cudaGraphNode_t *deps = nullptr;
+                    size_t n_deps = 0;
+                    SN_CUDA(cudaStreamGetCaptureInfo(cs, &cst, nullptr, nullptr, &deps, &n_deps));
+                    cudaGraphNodeParams cp = {};
+                    cp.type = cudaGraphNodeTypeConditional;
+                    cp.conditional.handle = h;
+                    cp.conditional.type = cudaGraphCondTypeIf;
+                    cp.conditional.size = 1;
+                    cudaGraphNode_t cn;
+                    SN_CUDA(cudaGraphAddNode(&cn, g, deps, n_deps, &cp));
+                    SN_CUDA(cudaStreamUpdateCaptureDependencies(cs, &cn, 1, cudaStreamSetCaptureDependencies));
+                    cudaGraph_t g_out = nullptr;
+                    SN_CUDA(cudaStreamEndCapture(cs, &g_out));
+                    cudaGraph_t body = cp.conditional.phGraph_out[0];
+                    SN_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+                    body_launches = 0;
+                    const int rb = far_body(cs);
+                    cudaGraph_t b_out = nullptr;
+                    const cudaError_t ec2 = cudaStreamEndCapture(cs, &b_out);
+                    SN_CHECK(rb == SN_OK, sn_last_error());
+                    SN_CUDA(ec2);
+                    SN_CHECK(chain(body, fg->body), "far pipeline graph: the body is not a chain of kernels");
+                    SN_CUDA(cudaGraphInstantiate(&fg->exec, g, 0));
+                    fg->shape = std::move(shape);
+                    fg->key = std::move(key);
+                    ctx->far_graph_builds += 1;
+                }
+            }
+            if (body_launches) ctx->far_body_launches = body_launches;
+            SN_CUDA(cudaGraphLaunch(fg->exec, st));
+            ctx->launches += 1;  // the condition kernel (the body's kernels run only when needed)
+        }
         bl = cb2;
         tm.end();
     }
@@ -752,6 +904,11 @@ int sn_context_destroy(sn_context *ctx) {
                 for (auto &ev : st2) cudaEventDestroy(ev);
         for (auto &ev : ctx->ev_work) cudaEventDestroy(ev);
     }
+    for (auto &g : ctx->far_graph) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        if (g.graph) cudaGraphDestroy(g.graph);
+    }
+    if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     if (ctx->h_work) cudaFreeHost(ctx->h_work);
     for (auto &S : ctx->slot) {
         if (S.h_stage) cudaFreeHost(S.h_stage);
@@ -922,6 +1079,7 @@ static int render_check(sn_context *ctx, int32_t *retry) {
                 ctx->slice_off_next = true;
                 grow = true;
             }
+            if (h[3] && far_graphs_enabled()) ctx->launches += ctx->far_body_launches;  // the body ran
             need_f = std::max(need_f, h[2]);
             need_u = std::max(need_u, h[3]);
             need_b = std::max(need_b, h[4]);
@@ -1503,6 +1661,14 @@ extern "C" int sn_debug_slice_counts(sn_context *ctx, uint64_t *out) {
 
 // Test hook (not part of the ABI): the starting capacities of the scene pass's far half (unfinished
 // tiles, far records, bucket items), so a test can force their growth path.
+// test hook: far-pipeline graph instantiations and in-place updates so far (0 with SN_FAR_GRAPH=0)
+extern "C" int sn_debug_far_graph_builds(sn_context *ctx, int64_t *builds, int64_t *updates) {
+    SN_CHECK(ctx != nullptr && builds != nullptr && updates != nullptr, "bad argument");
+    *builds = ctx->far_graph_builds;
+    *updates = ctx->far_graph_updates;
+    return SN_OK;
+}
+
 extern "C" int sn_debug_far_caps(sn_context *ctx, uint32_t cap_u, uint64_t cap_f, uint64_t cap_b) {
     SN_CHECK(ctx != nullptr && cap_u > 0 && cap_f > 0 && cap_b > 0, "bad argument");
     ctx->pass[0].cap_u = cap_u;

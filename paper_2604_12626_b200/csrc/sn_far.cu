@@ -71,7 +71,17 @@ __global__ void __launch_bounds__(kBlock) far_ranges_kernel(FarArgs f, const uin
 
 unsigned grid_of(uint64_t cap) { return (unsigned)std::max<uint64_t>(1, (cap + kBlock - 1) / kBlock); }
 
+// The far pipeline runs only when the render registered an unfinished tile (a conditional graph node).
+__global__ void far_cond_kernel(cudaGraphConditionalHandle h, const unsigned long long *fctl) {
+    cudaGraphSetConditional(h, fctl[0] != 0ull ? 1u : 0u);
+}
+
 }  // namespace
+
+cudaError_t launch_far_cond(cudaGraphConditionalHandle h, const unsigned long long *fctl, cudaStream_t s) {
+    far_cond_kernel<<<1, 1, 0, s>>>(h, fctl);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_far_tie_fix(const FarArgs &f, const uint32_t *keys, uint32_t *vals, cudaStream_t s) {
     if (f.cap_b == 0) return cudaSuccess;

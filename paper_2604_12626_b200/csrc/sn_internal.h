@@ -113,6 +113,8 @@ struct FarArgs {
 cudaError_t launch_far_collect(const sn_cloud &c, const FarArgs &f, int64_t n, cudaStream_t s);
 cudaError_t launch_far_tie_fix(const FarArgs &f, const uint32_t *keys, uint32_t *vals, cudaStream_t s);
 cudaError_t launch_far_ranges(const FarArgs &f, const uint32_t *keys, cudaStream_t s);
+// sets the conditional handle to (unfinished tiles registered != 0)
+cudaError_t launch_far_cond(cudaGraphConditionalHandle h, const unsigned long long *fctl, cudaStream_t s);
 
 // sn_bin.cu
 struct BinArgs {
