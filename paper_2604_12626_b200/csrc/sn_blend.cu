@@ -48,6 +48,9 @@
 __device__ unsigned long long g_blend_prof[16];
 __device__ unsigned g_env_frac[64];  // per env: largest fraction (1/1000) of the depth list a tile consumed
 #endif
+#ifdef SN_FIX_PROF
+__device__ unsigned long long g_fix_prof[16];  // why the scene blend deferred pixels (scripts/blend_prof.py)
+#endif
 
 namespace sn {
 
@@ -987,6 +990,18 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
             const bool cut = T - err <= kTHi;
             const bool amb = inside && (b.force_exact || (cut && (!(T + err < kTLo) || err > 0.0625f * T)));
             PROF(2, amb);
+    #ifdef SN_FIX_PROF
+            if (MODE == 0 && amb) {
+                atomicAdd(&g_fix_prof[0], 1ull);
+                if (b.force_exact) atomicAdd(&g_fix_prof[13], 1ull);
+                if (err > 0.0625f * T) atomicAdd(&g_fix_prof[1], 1ull);
+                atomicAdd(&g_fix_prof[T >= kTHi ? 2 : T >= kTLo ? 3 : 4], 1ull);
+                const float lr = T > 0.0f && err > 0.0f ? log10f(err / T) : -9.0f;
+                atomicAdd(&g_fix_prof[5 + min(7, max(0, (int)floorf(lr) + 8))], 1ull);
+                if (fabsf(T - 1.0e-4f) <= 1.0e-9f) atomicAdd(&g_fix_prof[14], 1ull);
+                if (nc <= 4) atomicAdd(&g_fix_prof[15], 1ull);
+            }
+    #endif
             const int64_t pix = ((int64_t)env * b.height + py_i) * b.width + px_i;
             const uint32_t code = (uint32_t)(((int64_t)el * b.height + py_i) * b.width + px_i);
             // Error bounds of the outputs the compositor decides on. Every weight w_i = a_i T_(i-1) has
@@ -2451,6 +2466,17 @@ extern "C" int sn_debug_slice_hooks(int bits) {
     return cudaMemcpyToSymbol(sn::g_slice_hooks, &bits, sizeof(int)) == cudaSuccess ? 0 : 1;
 }
 
+#ifdef SN_FIX_PROF
+extern "C" int sn_debug_fix_prof(unsigned long long *out, int reset) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_fix_prof, sizeof(unsigned long long) * 16);
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(g_fix_prof, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
 #ifdef SN_BLEND_PROF
 extern "C" int sn_debug_blend_prof(unsigned long long *out, int reset) {
     cudaDeviceSynchronize();

@@ -608,21 +608,19 @@ __global__ void __launch_bounds__(kBlock, SN_AVATAR_COUNT_MIN_BLOCKS) avatar_cou
         if (gs == 0) {  // stage the group's pose blocks (skipping envs whose two avatars are culled whole)
             __syncthreads();
             const int ge = min(group, a.ec - e);
-            for (int k = threadIdx.x; k < ge * 2 * pb; k += kBlock) {
-                const int eg = k / (2 * pb), kk = k % (2 * pb);
+            // (segment by segment: contiguous copies, no per-element index divisions)
+            for (int eg = 0; eg < ge; ++eg) {
                 const int env_k = env + eg;
                 const uint8_t *cull_k = a.avatar_cull ? a.avatar_cull + (int64_t)env_k * av.n_avatars : nullptr;
                 if (cull_k && cull_k[a_lo] && cull_k[a_hi]) continue;
-                const int slot = kk / pb, o = kk % pb, av_id = slot ? a_hi : a_lo;
-                const int64_t ea = (int64_t)env_k * pv.n_avatars + av_id;
-                double v;
-                if (o < 12 * J)
-                    v = pv.joint_mats[ea * J * 12 + o];
-                else if (o < 16 * J)
-                    v = pv.eff_q[ea * J * 4 + (o - 12 * J)];
-                else
-                    v = pv.root[ea * 12 + (o - 16 * J)];
-                s_pose[k] = v;
+                for (int slot = 0; slot < (a_hi == a_lo ? 1 : 2); ++slot) {  // (one avatar: slot 1 is never read)
+                    const int64_t ea = (int64_t)env_k * pv.n_avatars + (slot ? a_hi : a_lo);
+                    double *dst = s_pose + (size_t)(eg * 2 + slot) * pb;
+                    const double *jm = pv.joint_mats + ea * J * 12, *eq = pv.eff_q + ea * J * 4;
+                    for (int o = threadIdx.x; o < 12 * J; o += kBlock) dst[o] = __ldg(jm + o);
+                    for (int o = threadIdx.x; o < 4 * J; o += kBlock) dst[12 * J + o] = __ldg(eq + o);
+                    if (threadIdx.x < 12) dst[16 * J + threadIdx.x] = __ldg(pv.root + ea * 12 + threadIdx.x);
+                }
             }
             __syncthreads();
         }

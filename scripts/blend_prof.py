@@ -25,10 +25,22 @@ print("rendering", flush=True)
 br.render(cams, views=False, near_slice=ns)
 torch.cuda.synchronize()
 print("warm", flush=True)
-lib.sn_debug_blend_prof(hist, 1)
-br.render(cams, views=False, near_slice=ns)
-torch.cuda.synchronize()
-lib.sn_debug_blend_prof(hist, 1)
-h = list(hist)
-print(f"warp iterations {h[0]}, boundary-band {h[1]} ({h[1] / max(h[0], 1):.4f}), no pixel inside {h[3]} "
+if hasattr(lib, "sn_debug_blend_prof"):
+  lib.sn_debug_blend_prof(hist, 1)
+  br.render(cams, views=False, near_slice=ns)
+  torch.cuda.synchronize()
+  lib.sn_debug_blend_prof(hist, 1)
+  h = list(hist)
+  print(f"warp iterations {h[0]}, boundary-band {h[1]} ({h[1] / max(h[0], 1):.4f}), no pixel inside {h[3]} "
       f"({h[3] / max(h[0], 1):.4f})")
+
+if hasattr(lib, "sn_debug_fix_prof"):
+    fx = (ctypes.c_ulonglong * 16)()
+    lib.sn_debug_fix_prof(fx, 1)
+    br.render(cams, views=False, near_slice=ns)
+    torch.cuda.synchronize()
+    lib.sn_debug_fix_prof(fx, 1)
+    f = list(fx)
+    print(f"deferred pixels {f[0]}: err > T/16 {f[1]}, T >= 1e-4(1+1e-6) {f[2]}, T within 1e-6 rel {f[3]}, "
+          f"T below {f[4]}, forced {f[13]}, |T - 1e-4| <= 1e-9 {f[14]}, <= 4 contributions {f[15]}")
+    print("log10(err / T) bins [<-7, -7, -6, -5, -4, -3, -2, >=-1]:", f[5:13])
