@@ -603,8 +603,11 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
         bl.state = w.state.as<float>();
     }
     tm.begin(SN_STAGE_BLEND);
-    ctx->launches += sp.mode == 2 ? 1 : 2;  // blend (+ float64 fixup; mode 2's runs after the composite)
-    SN_CUDA(launch_blend(bl, st, /*fixup=*/!slice));
+    // the streamed scene blend resolves its deferred pixels itself (SN_INCTA_FIXUP)
+    const bool incta = SN_INCTA_FIXUP && sp.mode == 0 && bl.pv.source == 0;
+    const bool fix_after = !slice && !incta && sp.mode != 2;
+    ctx->launches += fix_after ? 2 : 1;  // blend (+ float64 fixup; mode 2's runs after the composite)
+    SN_CUDA(launch_blend(bl, st, /*fixup=*/fix_after));
     tm.end();
     if (slice) {
         // the far buckets of the unfinished tiles, the continuation, then the fixups (sn_far.cu)
@@ -613,12 +616,16 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
         // walk needs its tile's far bucket registers the tile (if the blend did not) and is queued
         // again for the second pass below
         // (the second pass starts where the blend's entries end: the deferred ones come after them)
-        unsigned *fix_start = ctx->fixcnt.as<unsigned>() + 2 + pass_id;
-        SN_CUDA(cudaMemcpyAsync(fix_start, bl.fix_count, sizeof(unsigned), cudaMemcpyDeviceToDevice, st));
-        BlendArgs fa = bl;
-        fa.pv.far_phase = 1;
-        ctx->launches += 1;
-        SN_CUDA(launch_fixup(fa, st));
+        // (with in-CTA fixups the blend did this pass itself: the list holds only deferred pixels)
+        unsigned *fix_start = nullptr;
+        if (!incta) {
+            fix_start = ctx->fixcnt.as<unsigned>() + 2 + pass_id;
+            SN_CUDA(cudaMemcpyAsync(fix_start, bl.fix_count, sizeof(unsigned), cudaMemcpyDeviceToDevice, st));
+            BlendArgs fa = bl;
+            fa.pv.far_phase = 1;
+            ctx->launches += 1;
+            SN_CUDA(launch_fixup(fa, st));
+        }
         FarArgs f;
         std::memset(&f, 0, sizeof f);  // (the graph key compares bytes: padding too)
         f.e0 = e0;
@@ -1679,6 +1686,20 @@ extern "C" int sn_debug_far_caps(sn_context *ctx, uint32_t cap_u, uint64_t cap_f
 
 // Diagnostic (not part of the ABI): the whole-avatar codes of the last render with an avatar set,
 // (env, avatar) row-major: 0 test every gaussian, kCullDepth / kCullFrame, kWholeVisible (4).
+// diagnostic: the last render's float64 fixup list of a pass (el * H * W + pixel codes, the last
+// env chunk); returns the count in *n (at most cap entries copied)
+extern "C" int sn_debug_fix_list(sn_context *ctx, int pass, uint32_t *out, int64_t cap, int64_t *n) {
+    SN_CHECK(ctx != nullptr && out != nullptr && n != nullptr && (pass == 0 || pass == 1), "bad argument");
+    SN_CHECK(ctx->fixcnt.p != nullptr && ctx->pass[pass].fix.p != nullptr, "no render yet");
+    SN_CUDA(cudaDeviceSynchronize());
+    unsigned c = 0;
+    SN_CUDA(cudaMemcpy(&c, ctx->fixcnt.as<unsigned>() + pass, sizeof c, cudaMemcpyDeviceToHost));
+    *n = c;
+    SN_CUDA(cudaMemcpy(out, ctx->pass[pass].fix.p, sizeof(uint32_t) * (size_t)std::min<int64_t>(c, cap),
+                       cudaMemcpyDeviceToHost));
+    return SN_OK;
+}
+
 extern "C" int sn_debug_avatar_codes(sn_context *ctx, uint8_t *out, int64_t n) {
     SN_CHECK(ctx != nullptr && out != nullptr && n >= 0, "bad argument");
     SN_CHECK(ctx->av_cull.p != nullptr, "no render with an avatar set yet");

@@ -616,6 +616,38 @@ struct PixPair {
     f32x2 T, err, A, cr, cg, cb, D, dead, eps_max, z_last, nc;  // nc: contributions (exact floats)
 };
 
+// ---- exact (float64) per-pixel walk: the fixup path (defined below) ----
+
+struct ExactPixel {
+    float cr, cg, cb;
+    double A, D, T;
+    int nc;
+    bool near;  // the cutoff test met a transmittance within 1e-12 (relative) of 1e-4: re-walk with SEQ
+    bool out;   // (far_phase 1) the walk needs the tile's far bucket, not built yet: defer the pixel
+};
+
+// The relative window around 1e-4 inside which the warp prefix product's association (<= ~1e-13
+// relative from the sequential product after hundreds of contributions) could flip `T < 1e-4`.
+constexpr double kNearCut = 1e-12;
+
+
+// A contribution waiting in a warp's queue (float64 alpha and z, colour).
+struct QEntry {
+    double a, z;
+    float r, g, b, pad;
+};
+constexpr int kQueue = 64;  // per-warp queue capacity: < 32 waiting + 32 arriving
+
+#ifndef SN_FIXUP_PER
+#define SN_FIXUP_PER 2
+#endif
+template <int kPer>
+__device__ __forceinline__ ExactPixel exact_pixel(const PassView &v, int el, int tile, int tiles_x, int px_i, int py_i,
+                                                  const double *s_exp, QEntry *q);
+__device__ __forceinline__ void write_exact_scene(const BlendArgs &b, const ExactPixel &f, int64_t pix,
+                                                  const sn_camera &cam);
+__device__ __forceinline__ void defer_to_far(const BlendArgs &b, int el, int tile, uint32_t code);
+
 template <int MODE, int SOURCE>
 __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEND_MIN_BLOCKS) blend_kernel(BlendArgs b) {
     constexpr bool kBound = MODE != 1;  // depth error bounds feed the compositor
@@ -636,12 +668,21 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
     // per warp: byte offsets of its batch entries, in depth order, padded to a multiple of the
     // walk's unroll with the inert record
     __shared__ uint16_t s_wl[kBW][kBatch + kWalkUnroll];
+    // the scene pass resolves its deferred pixels itself, after the tile's walk (a warp per pixel,
+    // the float64 walk of fixup_kernel): their latency-bound list walks overlap the other CTAs' blends
+    constexpr bool kInCta = MODE == 0 && SOURCE == 0 && SN_INCTA_FIXUP;
+    __shared__ uint32_t s_fixpix[kInCta ? 2 * kBT : 1];
+    __shared__ unsigned s_nfix;
+    static_assert(sizeof(s_f) >= 64 * sizeof(double) + kBW * kQueue * sizeof(QEntry), "fixup scratch in s_f");
     const PassView &v = b.pv;
     if (pass_overflow(v)) return;
     if (SOURCE == 3 && far_overflow(v)) return;
     // one (env, tile); u: its unfinished index (the continuation, SOURCE 3), else -1
     auto do_tile = [&](const int tile, const int el, const int u) {
-        if (threadIdx.x == 0) s_epsmax = __float_as_uint(kEpsExact);
+        if (threadIdx.x == 0) {
+            s_epsmax = __float_as_uint(kEpsExact);
+            s_nfix = 0u;
+        }
         if (threadIdx.x < 20) {  // the inert record: h = dead >= 0 > thr_in = thr_out = -1, alpha 0
             float *d = reinterpret_cast<float *>(&s_f[kBatch]);
             d[threadIdx.x] = (threadIdx.x == 8 || threadIdx.x == 9) ? -1.0f : 0.0f;
@@ -1017,7 +1058,15 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
             const bool fin = FIN[p];
             const bool flag = inside && amb && fin;
             contrib_sum += (flag || !fin) ? 0u : (unsigned)nc;
-            push_fixup(b, flag, code);
+            if (kInCta) {
+                if (flag) {
+                    const unsigned k = atomicAdd(&s_nfix, 1u);
+                    SN_ASSERT(k < 2u * kBT);
+                    s_fixpix[k] = code;
+                }
+            } else {
+                push_fixup(b, flag, code);
+            }
             if (!inside || !fin) continue;
             if (MODE == 2 && SOURCE != 1 && threadIdx.x == 0 && p == 0) b.tile_flag[(int64_t)el * (tiles_of(b.width) * tiles_of(b.height)) + tile] = 1;
             if (flag) {
@@ -1069,6 +1118,33 @@ __global__ void __launch_bounds__(kBT, MODE == 2 ? SN_LAYER_MIN_BLOCKS : SN_BLEN
         if (b.contribs) {
             const unsigned sum = __reduce_add_sync(kFull, contrib_sum);
             if (lane == 0 && sum) atomicAdd(b.contribs, (unsigned long long)sum);
+        }
+        if (kInCta) {
+            __syncthreads();
+            const unsigned nfix = s_nfix;
+            if (nfix) {
+                double *s_exp = reinterpret_cast<double *>(s_f);  // (the batch buffers are free now)
+                QEntry *q = reinterpret_cast<QEntry *>(s_exp + 64) + warp * kQueue;
+                if (threadIdx.x < 64) s_exp[threadIdx.x] = kExp2Tbl[threadIdx.x];
+                __syncthreads();
+                PassView fv = v;
+                fv.far_phase = v.sliced ? 1 : 0;  // a walk that needs the far bucket goes to the fixup pass
+                const unsigned hw = (unsigned)b.width * (unsigned)b.height;
+                unsigned long long nc_sum = 0;
+                for (unsigned i = warp; i < nfix; i += kBW) {
+                    const uint32_t code = s_fixpix[i];
+                    const int pp = (int)(code % hw);
+                    const int fy = pp / b.width, fx = pp % b.width;
+                    const ExactPixel f = exact_pixel<SN_FIXUP_PER>(fv, el, tile, b.tiles_x, fx, fy, s_exp, q);
+                    if (f.out) {
+                        defer_to_far(b, el, tile, code);
+                        continue;
+                    }
+                    nc_sum += (unsigned)f.nc;
+                    if (lane == 0) write_exact_scene(b, f, ((int64_t)env * b.height + fy) * b.width + fx, cam);
+                }
+                if (b.contribs && lane == 0 && nc_sum) atomicAdd(b.contribs, nc_sum);
+            }
         }
 #undef PROF
     };
@@ -1657,26 +1733,6 @@ __global__ void __launch_bounds__(kBlock) composite_kernel(BlendArgs b) {
 
 // ---- exact (float64) per-pixel walk: the fixup path ----
 
-struct ExactPixel {
-    float cr, cg, cb;
-    double A, D, T;
-    int nc;
-    bool near;  // the cutoff test met a transmittance within 1e-12 (relative) of 1e-4: re-walk with SEQ
-    bool out;   // (far_phase 1) the walk needs the tile's far bucket, not built yet: defer the pixel
-};
-
-// The relative window around 1e-4 inside which the warp prefix product's association (<= ~1e-13
-// relative from the sequential product after hundreds of contributions) could flip `T < 1e-4`.
-constexpr double kNearCut = 1e-12;
-
-
-// A contribution waiting in a warp's queue (float64 alpha and z, colour).
-struct QEntry {
-    double a, z;
-    float r, g, b, pad;
-};
-constexpr int kQueue = 64;  // per-warp queue capacity: < 32 waiting + 32 arriving
-
 // One group's transmittances. Fast mode: a warp prefix product (Hillis-Steele, its association
 // differs from the sequential product's by a few ulps). SEQ mode: lane l multiplies T by
 // (1 - a_j) for j < l itself, in order -- the reference's sequential product (_kernels_cy.pyx:86),
@@ -2155,12 +2211,48 @@ __global__ void __launch_bounds__(256) fixup_layer_kernel(BlendArgs b) {
 // Recomputes the listed pixels exactly (warp per pixel, grid-stride over the device-side count)
 // and writes the same outputs the float64 blend epilogue writes. Mode 2 also recomputes the scene
 // pixel (the back layer) so the composite's comparisons see float64 depths.
+// A scene pixel's float64 result into the frame (fixup_kernel<0> and the blend's in-CTA fixups).
+__device__ __forceinline__ void write_exact_scene(const BlendArgs &b, const ExactPixel &f, int64_t pix,
+                                                  const sn_camera &cam) {
+    const double alpha = f.A < 1.0 ? f.A : 1.0;
+    const double depth = f.A > 0.0 ? f.D / f.A : cam.far_;
+    if (b.contrib) b.contrib[pix] = f.nc;
+    float *oc = b.color + 3 * pix;
+    oc[0] = (float)np_clip((double)f.cr + cam.background[0] * f.T, 0.0, 1.0);
+    oc[1] = (float)np_clip((double)f.cg + cam.background[1] * f.T, 0.0, 1.0);
+    oc[2] = (float)np_clip((double)f.cb + cam.background[2] * f.T, 0.0, 1.0);
+    b.alpha[pix] = (float)alpha;
+    b.depth[pix] = (float)depth;
+    store_payload(b, pix, oc[0], oc[1], oc[2], (float)depth);
+    // the stored depth is the float64 walk's rounded to float32 (and the walk's prefix-product
+    // transmittance / table exp differ from the sequential reference by a few float64 ulps):
+    // a band of ~2 float ulps makes a layer fixup whose exact front depth falls inside it
+    // recompute this pixel in float64 (fixup_layer_kernel / fixup_kernel<2>)
+    if (b.derr) b.derr[pix] = f.A > 0.0 ? (float)(2.5e-7 * fabs(depth)) : 0.0f;
+}
+
+// (sliced pass, far_phase 1) a float64 walk needs the tile's far bucket: register the tile if the
+// blend did not (late: no saved state, the continuation skips it) and queue the pixel for the
+// fixup pass after the buckets, which walks near list + bucket. Lane 0 acts.
+__device__ __forceinline__ void defer_to_far(const BlendArgs &b, int el, int tile, uint32_t code) {
+    if ((threadIdx.x & 31) != 0) return;
+    int32_t *bo = b.bucket_of + (int64_t)el * b.pv.n_tiles + tile;
+    if (atomicCAS(bo, -1, -2) == -1) {
+        const unsigned long long u = atomicAdd(b.unfin_count, 1ull);
+        if (u < b.pv.far_cap_u) {
+            b.unfin_list[u] = kLateTile | ((uint32_t)el << 16) | (uint32_t)tile;
+            atomicOr(b.unfin_envs, 1ull << el);
+            atomicExch(bo, (int32_t)u);
+        }  // (overflow: the render is re-run with more room)
+    }
+    const unsigned slot = atomicAdd(b.fix_count, 1u);
+    SN_ASSERT(slot < 2u * (unsigned)b.ec * (unsigned)b.width * (unsigned)b.height);
+    b.fix_list[slot] = code;
+}
+
 template <int MODE>
 #ifndef SN_FIXUP_MIN_BLOCKS
 #define SN_FIXUP_MIN_BLOCKS 4
-#endif
-#ifndef SN_FIXUP_PER
-#define SN_FIXUP_PER 2
 #endif
 __global__ void __launch_bounds__(256, SN_FIXUP_MIN_BLOCKS) fixup_kernel(BlendArgs b) {
     __shared__ double s_exp[64];
@@ -2185,23 +2277,7 @@ __global__ void __launch_bounds__(256, SN_FIXUP_MIN_BLOCKS) fixup_kernel(BlendAr
         // mode 2 fixups are few and each walks long, unsaturated lists: more gathers in flight
         const ExactPixel f = exact_pixel<MODE == 2 ? 8 : SN_FIXUP_PER>(b.pv, el, tile, b.tiles_x, px_i, py_i, s_exp, q);
         if (MODE != 2 && f.out) {
-            // (sliced pass, first fixup pass) the walk needs the tile's far bucket: register the tile
-            // if the blend did not (late: no saved state, the continuation skips it) and queue the
-            // pixel again for the second fixup pass, which walks near list + bucket
-            if (lane == 0) {
-                int32_t *bo = b.bucket_of + (int64_t)el * b.pv.n_tiles + tile;
-                if (atomicCAS(bo, -1, -2) == -1) {
-                    const unsigned long long u = atomicAdd(b.unfin_count, 1ull);
-                    if (u < b.pv.far_cap_u) {
-                        b.unfin_list[u] = kLateTile | ((uint32_t)el << 16) | (uint32_t)tile;
-                        atomicOr(b.unfin_envs, 1ull << el);
-                        atomicExch(bo, (int32_t)u);
-                    }  // (overflow: the render is re-run with more room)
-                }
-                const unsigned slot = atomicAdd(b.fix_count, 1u);
-                SN_ASSERT(slot < 2u * (unsigned)b.ec * hw);
-                b.fix_list[slot] = code;
-            }
+            defer_to_far(b, el, tile, code);
             continue;
         }
         contribs += (unsigned)f.nc;
@@ -2248,22 +2324,12 @@ __global__ void __launch_bounds__(256, SN_FIXUP_MIN_BLOCKS) fixup_kernel(BlendAr
             continue;
         }
         if (lane != 0) continue;
-        if (b.contrib) b.contrib[pix] = f.nc;
-        float *oc = b.color + 3 * pix;
         if (MODE == 0) {
-            oc[0] = (float)np_clip((double)f.cr + cam.background[0] * f.T, 0.0, 1.0);
-            oc[1] = (float)np_clip((double)f.cg + cam.background[1] * f.T, 0.0, 1.0);
-            oc[2] = (float)np_clip((double)f.cb + cam.background[2] * f.T, 0.0, 1.0);
-            b.alpha[pix] = (float)alpha;
-            b.depth[pix] = (float)depth;
-            store_payload(b, pix, oc[0], oc[1], oc[2], (float)depth);
-            // the stored depth is the float64 walk's rounded to float32 (and the walk's prefix-product
-            // transmittance / table exp differ from the sequential reference by a few float64 ulps):
-            // a band of ~2 float ulps makes a layer fixup whose exact front depth falls inside it
-            // recompute this pixel in float64 (fixup_layer_kernel / fixup_kernel<2>)
-            if (b.derr) b.derr[pix] = f.A > 0.0 ? (float)(2.5e-7 * fabs(depth)) : 0.0f;
+            write_exact_scene(b, f, pix, cam);
             continue;
         }
+        if (b.contrib) b.contrib[pix] = f.nc;
+        float *oc = b.color + 3 * pix;
         double fc[3] = {0.0, 0.0, 0.0};
         if (f.A > 0.0) {
             fc[0] = np_clip((double)f.cr / f.A, 0.0, 1.0);

@@ -248,6 +248,13 @@ struct BlendArgs {
     int32_t *bucket_of;
     float *state;           // (cap_u, kStateF, kBT)
 };
+// 1: the scene blend (streamed source) resolves its deferred pixels in the same CTA after the tile's
+// walk, and a sliced pass needs only the fixup pass after the far buckets. Off: a CTA holding its
+// slot for a latency-bound float64 walk (45% of tiles have one) costs the blend more than the
+// separate fixup kernel (6,366 vs 6,460 frames/s at config 2)
+#ifndef SN_INCTA_FIXUP
+#define SN_INCTA_FIXUP 0
+#endif
 constexpr uint32_t kLateTile = 1u << 31;  // unfinished-list flag: registered by the first fixup pass (no state)
 constexpr int kBT = 128;     // scene blend threads per tile (two pixels each, sn_blend.cu)
 constexpr int kStateF = 22;  // floats per blend thread of a saved tile (2 pixels)
