@@ -2251,9 +2251,6 @@ __device__ __forceinline__ void defer_to_far(const BlendArgs &b, int el, int til
 }
 
 template <int MODE>
-#ifndef SN_FIXUP_MIN_BLOCKS
-#define SN_FIXUP_MIN_BLOCKS 4
-#endif
 __global__ void __launch_bounds__(256, SN_FIXUP_MIN_BLOCKS) fixup_kernel(BlendArgs b) {
     __shared__ double s_exp[64];
     __shared__ QEntry s_q[8][kQueue];

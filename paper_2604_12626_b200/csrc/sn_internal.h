@@ -258,7 +258,10 @@ struct BlendArgs {
 constexpr uint32_t kLateTile = 1u << 31;  // unfinished-list flag: registered by the first fixup pass (no state)
 constexpr int kBT = 128;     // scene blend threads per tile (two pixels each, sn_blend.cu)
 constexpr int kStateF = 22;  // floats per blend thread of a saved tile (2 pixels)
-constexpr int kFixupBlocks = 148 * 4;
+#ifndef SN_FIXUP_MIN_BLOCKS
+#define SN_FIXUP_MIN_BLOCKS 4  // fixup CTAs (256 threads) per SM
+#endif
+constexpr int kFixupBlocks = 148 * SN_FIXUP_MIN_BLOCKS;
 cudaError_t launch_blend(const BlendArgs &b, cudaStream_t s, bool fixup = true);  // blend (+ fixup, modes 0, 1)
 cudaError_t launch_continue(const BlendArgs &b, cudaStream_t s);  // sliced pass: the unfinished tiles' far walk
 cudaError_t launch_fixup(const BlendArgs &b, cudaStream_t s);     // modes 0, 1: the float64 fixups
