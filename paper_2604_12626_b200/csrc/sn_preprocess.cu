@@ -438,29 +438,24 @@ __global__ void __launch_bounds__(kBlock, SN_EMIT_MIN_BLOCKS) scene_emit_kernel(
 
 // ------------------------------------------------------------------------------- avatars
 
-// lbs_deform (rig.py:107-146) for one gaussian under one (env, avatar) pose. Sparse influences
-// in ascending joint order reproduce the dense N x J sums exactly: zero weights add +-0.
-template <bool NC>
-__device__ __forceinline__ double ldp(const double *p) {
-    if (NC) return __ldg(p);
-    return *p;
-}
-template <bool NC>
-__device__ __forceinline__ void ld4p(const double *p, double o[4]) {
-    if (NC) {
-        load4<double>(p, o);
-    } else {
-        o[0] = p[0];
-        o[1] = p[1];
-        o[2] = p[2];
-        o[3] = p[3];
-    }
-}
-
 // lbs_deform's per-gaussian sums over one influence list (get(k, j, w): the k-th nonzero influence,
 // ascending joint order). NC = true: pose data in global memory (read-only path); false: generic
 // loads (shared memory). ROT = false: the position only (q_out untouched) -- the count kernel's
 // visibility test needs the rotation only for the few items its float32 prefilter cannot decide.
+// 16-byte loads of pose data (joint matrices, quaternions and the root block are 16-byte aligned in
+// global memory and in the count kernel's shared staging): half the load instructions
+template <bool NC, int K>
+__device__ __forceinline__ void ldp2(const double *p, double o[K]) {
+    static_assert(K % 2 == 0, "pairs");
+    const double2 *q = reinterpret_cast<const double2 *>(p);
+#pragma unroll
+    for (int i = 0; i < K / 2; ++i) {
+        const double2 v = NC ? __ldg(q + i) : q[i];
+        o[2 * i] = v.x;
+        o[2 * i + 1] = v.y;
+    }
+}
+
 template <bool NC, bool ROT, typename Get>
 __device__ __forceinline__ void skin_core(int n, Get get, const double P[4], const double Q[4], const double *jm,
                                           const double *eq, const double *root, double p_out[3], double q_out[4]) {
@@ -473,12 +468,13 @@ __device__ __forceinline__ void skin_core(int n, Get get, const double P[4], con
         double w;
         get(k, j, w);
         if (w == 0.0) continue;
-        const double *M = jm + 12 * j;
+        double M[12];
+        ldp2<NC, 12>(jm + 12 * j, M);
         // einsum("jab,nb->jna") as numpy evaluates it: (r0 p0 + r2 p2) + r1 p1, then + offset;
         // einsum("nj,jnc->nc") accumulates over j sequentially, unfused (measured)
-        double t0 = ((ldp<NC>(M + 0) * P[0] + ldp<NC>(M + 2) * P[2]) + ldp<NC>(M + 1) * P[1]) + ldp<NC>(M + 3);
-        double t1 = ((ldp<NC>(M + 4) * P[0] + ldp<NC>(M + 6) * P[2]) + ldp<NC>(M + 5) * P[1]) + ldp<NC>(M + 7);
-        double t2 = ((ldp<NC>(M + 8) * P[0] + ldp<NC>(M + 10) * P[2]) + ldp<NC>(M + 9) * P[1]) + ldp<NC>(M + 11);
+        double t0 = ((M[0] * P[0] + M[2] * P[2]) + M[1] * P[1]) + M[3];
+        double t1 = ((M[4] * P[0] + M[6] * P[2]) + M[5] * P[1]) + M[7];
+        double t2 = ((M[8] * P[0] + M[10] * P[2]) + M[9] * P[1]) + M[11];
         acc0 = acc0 + w * (t0 - P[0]);
         acc1 = acc1 + w * (t1 - P[1]);
         acc2 = acc2 + w * (t2 - P[2]);
@@ -489,13 +485,15 @@ __device__ __forceinline__ void skin_core(int n, Get get, const double P[4], con
     }
     if (dom < 0) dom = 0;  // all-zero row: np.argmax picks joint 0
     double b0 = P[0] + acc0, b1 = P[1] + acc1, b2 = P[2] + acc2;
-    p_out[0] = dot3_fma(b0, b1, b2, ldp<NC>(root + 0), ldp<NC>(root + 1), ldp<NC>(root + 2)) + ldp<NC>(root + 9);
-    p_out[1] = dot3_fma(b0, b1, b2, ldp<NC>(root + 3), ldp<NC>(root + 4), ldp<NC>(root + 5)) + ldp<NC>(root + 10);
-    p_out[2] = dot3_fma(b0, b1, b2, ldp<NC>(root + 6), ldp<NC>(root + 7), ldp<NC>(root + 8)) + ldp<NC>(root + 11);
+    double R[12];
+    ldp2<NC, 12>(root, R);
+    p_out[0] = dot3_fma(b0, b1, b2, R[0], R[1], R[2]) + R[9];
+    p_out[1] = dot3_fma(b0, b1, b2, R[3], R[4], R[5]) + R[10];
+    p_out[2] = dot3_fma(b0, b1, b2, R[6], R[7], R[8]) + R[11];
     if (!ROT) return;
 
     double qd[4];
-    ld4p<NC>(eq + 4 * dom, qd);
+    ldp2<NC, 4>(eq + 4 * dom, qd);
     double bq[4] = {0.0, 0.0, 0.0, 0.0};
     // (weights * signs) @ eff_quats: an FMA chain over j (OpenBLAS at production sizes; for
     // K >= 16 and up to ~1k rows OpenBLAS interleaves 8 accumulators instead -- a few-ulp
@@ -507,7 +505,7 @@ __device__ __forceinline__ void skin_core(int n, Get get, const double P[4], con
         get(k, j, w);
         if (w == 0.0) continue;
         double qj[4];
-        ld4p<NC>(eq + 4 * j, qj);
+        ldp2<NC, 4>(eq + 4 * j, qj);
         double dot = fma(qj[3], qd[3], fma(qj[2], qd[2], fma(qj[1], qd[1], qj[0] * qd[0])));
         double ws = w * (dot < 0.0 ? -1.0 : 1.0);
         bq[0] = fma(ws, qj[0], bq[0]);
