@@ -95,7 +95,7 @@ double near_frac() {
     static const double f = [] {
         const char *e = std::getenv("SN_NEAR_FRAC");
         const double v = e ? std::atof(e) : 0.0;
-        return v > 0.0 && v <= 1.0 ? v : 0.05;
+        return v > 0.0 && v <= 1.0 ? v : 0.02;
     }();
     return f;
 }
@@ -382,11 +382,11 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     a.cap = cap_v;
     w.sliced = slice ? 1 : 0;
     if (slice) {
-        // starting capacities of the far half (~70 MB), grown by render_check on overflow: sized so the
-        // occasional unfinished tiles of a fresh camera set do not cost a re-render
-        if (w.cap_u == 0) w.cap_u = 4096;
-        if (w.cap_f == 0) w.cap_f = 1u << 18;
-        if (w.cap_b == 0) w.cap_b = 1u << 20;
+        // starting capacities of the far half (~300 MB), grown by render_check on overflow: sized so
+        // the occasional unfinished tiles of a fresh camera set do not cost a re-render
+        if (w.cap_u == 0) w.cap_u = 16384;
+        if (w.cap_f == 0) w.cap_f = 1u << 20;
+        if (w.cap_b == 0) w.cap_b = 1u << 22;
         SN_ENSURE(w.zcut, sizeof(double) * ec);
         SN_ENSURE(w.nearmask, sizeof(uint64_t) * std::max<int64_t>(n, 1));
         a.z_cut = w.zcut.as<double>();
@@ -1110,19 +1110,19 @@ static int render_check(sn_context *ctx, int32_t *retry) {
         }
         // depth slicing: far splats, unfinished tiles (<= one per (env, tile)), far bucket items
         if (need_f > S->cap_f[p]) {
-            w.cap_f = std::max(w.cap_f, need_f + need_f / 4 + 1024);
+            w.cap_f = std::max(w.cap_f, need_f + need_f / 2 + 1024);  // (+50%: fresh camera sets vary)
             grow = true;
         }
         if (need_u > S->cap_u[p]) {
             // <= one per (env, tile) of the chunk, so this bounds itself; the state is 11 KB per tile
             SN_CHECK(need_u < (1u << 24), "too many unfinished tiles in one env chunk (limit 2^24)");
-            w.cap_u = (uint32_t)std::max<uint64_t>(w.cap_u, need_u + need_u / 4 + 256);
+            w.cap_u = (uint32_t)std::max<uint64_t>(w.cap_u, need_u + need_u / 2 + 256);
             // the bucket items were counted for the registered tiles only: scale the estimate
             if (S->cap_u[p] > 0) need_b = need_b / S->cap_u[p] * need_u + need_b % S->cap_u[p] * need_u / S->cap_u[p];
             grow = true;
         }
         if (need_b > S->cap_b[p]) {
-            w.cap_b = std::max(w.cap_b, need_b + need_b / 4 + 1024);
+            w.cap_b = std::max(w.cap_b, need_b + need_b / 2 + 1024);
             grow = true;
         }
         w.n_vis = (int64_t)last_v;
