@@ -339,27 +339,52 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
     }
     const int64_t g0 = (int64_t)blockIdx.x * kBlock + warp * 32;
     uint16_t *qq = s_q[warp];
+    // an in-depth item's frame cull: the float32 prefilter decides it where certain (a kept item's
+    // radius bound < 3000 px also rules out the degenerate case); the undecided ones are queued at
+    // the end of this warp's round list and take the float64 projection with full lanes
+    auto resolve = [&](const unsigned it, const unsigned active, const int code) {
+        const int l = it & 31, e = (it >> 5) & 63;
+        // field: 2 frame, 3 degenerate, 4 drawn (sn_stats order); the lazy sliced pass counts its
+        // near items below and needs none of these
+        const int field = code == kKeep ? 4 : (code == kDegenerate ? 3 : 2);
+        if (!a.lazy_far) tally_item(s_cnt, active, e, field);
+        if (code == kKeep) {
+            atomicOr(&s_vis[warp * 32 + l], 1ull << e);
+            if (cam_z(s_geo[warp * 32 + l], s_cam[e]) < s_zcut[e]) atomicOr(&s_nearbits[warp * 32 + l], 1ull << e);
+        }
+    };
     for (int eb = 0; eb < a.ec; eb += kCountRound) {
         const int n = build_round(in_depth, eb, min(eb + kCountRound, a.ec), qq);
+        int nu = 0;  // undecided items, compacted over the list's consumed head (nu <= k0 + 32)
         for (int k0 = 0; k0 < n; k0 += 32) {
             const int k = k0 + lane;
-            const unsigned active = __ballot_sync(kFull, k < n);
-            if (k >= n) continue;
+            unsigned it = 0;
+            int code = -2;
+            if (k < n) {
+                it = qq[k];
+                const int l = it & 31, e = (it >> 5) & 63;
+                const double *d = s_geo[warp * 32 + l];
+                code = frame_prefilter(d, (d[3] + d[6]) + d[8], s_cam[e]);
+            }
+            const unsigned und = __ballot_sync(kFull, code == -1);
+            __syncwarp();  // (every lane has read its entry before the head is overwritten)
+            if (code == -1) qq[nu + __popc(und & ((1u << lane) - 1u))] = (uint16_t)it;
+            nu += __popc(und);
+            const unsigned dec = __ballot_sync(kFull, code >= 0);
+            if (code >= 0) resolve(it, dec, code);
+        }
+        __syncwarp();
+        for (int k0 = 0; k0 < nu; k0 += 32) {
+            const int k = k0 + lane;
+            const unsigned active = __ballot_sync(kFull, k < nu);
+            if (k >= nu) continue;
             const unsigned it = qq[k];
             const int l = it & 31, e = (it >> 5) & 63;
             const double *d = s_geo[warp * 32 + l];
             const double pp[3] = {d[0], d[1], d[2]};
             const double cov[6] = {d[3], d[4], d[5], d[6], d[7], d[8]};
             Geo geo;
-            const int code = project_geo(pp, cov, s_cam[e], geo);
-            // field: 2 frame, 3 degenerate, 4 drawn (sn_stats order); the lazy sliced pass counts its
-            // near items below and needs none of these
-            const int field = code == kKeep ? 4 : (code == kDegenerate ? 3 : 2);
-            if (!a.lazy_far) tally_item(s_cnt, active, e, field);
-            if (code == kKeep) {
-                atomicOr(&s_vis[warp * 32 + l], 1ull << e);
-                if (geo.z < s_zcut[e]) atomicOr(&s_nearbits[warp * 32 + l], 1ull << e);
-            }
+            resolve(it, active, project_geo(pp, cov, s_cam[e], geo));
         }
         __syncwarp();
     }
