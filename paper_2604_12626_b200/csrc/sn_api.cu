@@ -1700,6 +1700,24 @@ extern "C" int sn_debug_fix_list(sn_context *ctx, int pass, uint32_t *out, int64
     return SN_OK;
 }
 
+// diagnostic: the pair-list lengths of the listed (env, tile)s of a pass (the last env chunk)
+extern "C" int sn_debug_tile_lens(sn_context *ctx, int pass, uint32_t *out, int64_t cap, int64_t *n) {
+    SN_CHECK(ctx != nullptr && out != nullptr && n != nullptr && (pass == 0 || pass == 1), "bad argument");
+    PassWs &w = ctx->pass[pass];
+    SN_CHECK(w.tlist.p && w.tlist_cnt.p && w.ranges.p, "no listed pass yet");
+    SN_CUDA(cudaDeviceSynchronize());
+    uint32_t cnt = 0;
+    SN_CUDA(cudaMemcpy(&cnt, w.tlist_cnt.p, sizeof cnt, cudaMemcpyDeviceToHost));
+    const size_t n_ranges = (size_t)w.ec << w.tile_bits;
+    std::vector<uint32_t> keys(cnt);
+    std::vector<uint2> rg(n_ranges);
+    SN_CUDA(cudaMemcpy(keys.data(), w.tlist.p, sizeof(uint32_t) * cnt, cudaMemcpyDeviceToHost));
+    SN_CUDA(cudaMemcpy(rg.data(), w.ranges.p, sizeof(uint2) * n_ranges, cudaMemcpyDeviceToHost));
+    *n = cnt;
+    for (uint32_t i = 0; i < cnt && (int64_t)i < cap; ++i) out[i] = rg[keys[i]].y - rg[keys[i]].x;
+    return SN_OK;
+}
+
 extern "C" int sn_debug_avatar_codes(sn_context *ctx, uint8_t *out, int64_t n) {
     SN_CHECK(ctx != nullptr && out != nullptr && n >= 0, "bad argument");
     SN_CHECK(ctx->av_cull.p != nullptr, "no render with an avatar set yet");
