@@ -8,4 +8,4 @@ SPLATNAV_B200_LIB=build_variants/libsn_checks.so timeout 1500 python -m pytest t
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log; tail -2 gpurun_out/smoke.log
 timeout 900 python bench.py --impl reference > gpurun_out/bench_reference.log 2>&1; echo "reference rc=$?" >> gpurun_out/bench_reference.log; tail -c 600 gpurun_out/bench_reference.log
 bash scripts/gpu_profile.sh
-tail -c 1500 gpurun_out/bench.log; tail -2 gpurun_out/ncu_launch.log gpurun_out/ncu_full.log
+tail -c 1500 gpurun_out/bench.log; tail -n 2 gpurun_out/ncu_launch.log; tail -n 2 gpurun_out/ncu_full.log
