@@ -320,4 +320,8 @@ def test_far_graph_reused_across_renders():
         for k in KEYS:  # (new output addresses reach the cached graph through in-place updates)
             assert torch.equal(outs[ns][k], ref[k]), (i, k)
     assert lib.sn_debug_far_graph_builds(ctx.handle, ctypes.byref(builds), ctypes.byref(updates)) == 0
-    assert 1 <= builds.value <= 3, builds.value  # (first render; the buffers may grow once or twice)
+    import os
+    if os.environ.get("SN_FAR_GRAPH") == "0":  # (plain launches: no graph)
+        assert builds.value == 0
+    else:
+        assert 1 <= builds.value <= 3, builds.value  # (first render; the buffers may grow once or twice)
