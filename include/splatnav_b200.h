@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SN_ABI_VERSION 2
+#define SN_ABI_VERSION 3
 
 enum {
     SN_OK = 0,
@@ -67,7 +67,13 @@ typedef struct sn_stats {
  *   pos_opacity (n,4): x, y, z, opacity logit      -- float or double (dtype)
  *   log_scales  (n,4): s0, s1, s2, unused          -- dtype
  *   rotations   (n,4): w, x, y, z (raw, renormalized on use like build_cov3d)  -- dtype
- *   sh          (K*3, n) float32, structure-of-arrays (coefficient k, channel c at row 3k+c) */
+ *   sh          (K*3, n) float32, structure-of-arrays (coefficient k, channel c at row 3k+c)
+ * Optionally (ABI 3) the rows are a spatially ordered copy of the reference's cloud:
+ *   index        (n) uint32: the reference (original) index of each row -- depth ties, gaussian ids
+ *                and every order-dependent output use it, so results are those of the original order
+ *   block_bounds (ceil(n / 256), 8) float32 per 256-row block: min x y z, max x y z, 0, 0 of the
+ *                positions -- the count kernel decides whole blocks per env where the box allows
+ * Both NULL: rows in the original order, no block decisions. */
 typedef struct sn_cloud {
     int64_t n;
     int32_t sh_k;
@@ -76,6 +82,8 @@ typedef struct sn_cloud {
     const void *log_scales;
     const void *rotations;
     const float *sh;
+    const uint32_t *index;
+    const float *block_bounds;
 } sn_cloud;
 
 /* Device-resident avatar set: A avatars concatenated (render_observation's concat_clouds

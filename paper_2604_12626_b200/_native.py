@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("SPLATNAV_B200_LIB") or os.path.join(_HERE, "libsplatn
 
 SN_OK, SN_ERR_INVALID, SN_ERR_CUDA, SN_ERR_NOMEM = 0, 1, 2, 3
 SN_FLOAT32, SN_FLOAT64 = 0, 1
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 c_double_p = ctypes.POINTER(ctypes.c_double)
 P = ctypes.c_void_p
@@ -39,7 +39,8 @@ class SnStats(ctypes.Structure):
 
 class SnCloud(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("sh_k", ctypes.c_int32), ("dtype", ctypes.c_int32),
-                ("pos_opacity", P), ("log_scales", P), ("rotations", P), ("sh", P)]
+                ("pos_opacity", P), ("log_scales", P), ("rotations", P), ("sh", P), ("index", P),
+                ("block_bounds", P)]
 
 
 class SnAvatars(ctypes.Structure):

@@ -6,6 +6,8 @@ skin->project avatar-layer pass, compositor in the blend epilogue. Outputs stay 
 torch tensors (E,H,W,3) / (E,H,W) / (E,H,W).
 """
 
+import os
+
 import numpy as np
 import torch
 
@@ -16,8 +18,15 @@ from .renderer import render_frames
 
 class BatchRenderer:
     def __init__(self, scene, avatars=None, start_offsets=None, loops=None, background=(1.0, 1.0, 1.0), device=None,
-                 context=None):
+                 context=None, spatial=None):
+        """spatial: keep the scene as a spatially ordered copy (DeviceCloud.spatially_ordered; the same
+        frames, ids and stats as the original order, fewer per-(gaussian, env) depth tests); default
+        on (SPLATNAV_SPATIAL=0 turns the default off)."""
+        if spatial is None:
+            spatial = os.environ.get("SPLATNAV_SPATIAL", "1") != "0"
         self.scene = DeviceCloud.wrap(scene, device)
+        if spatial:
+            self.scene = self.scene.spatially_ordered()
         if avatars is None or isinstance(avatars, DeviceAvatars):
             self.avatars = avatars
         else:

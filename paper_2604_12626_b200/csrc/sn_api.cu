@@ -376,7 +376,9 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     a.recs = w.recs_un.as<SplatRec>();
     a.geo = w.geo_un.as<BlendGeo>();
     // the harness views' extras (gaussian id, reference rectangle per splat) only when requested
-    a.gid = views ? w.gid_un.as<uint32_t>() : nullptr;
+    // (a spatially reordered scene always keeps the original ids: its depth ties compare them)
+    const bool reordered = sp.scene && sp.scene->index;
+    a.gid = (views || reordered) ? w.gid_un.as<uint32_t>() : nullptr;
     a.rects = views ? w.rects_un.as<ushort4>() : nullptr;
     a.rects_tight = w.rects_tun.as<ushort4>();
     a.cap = cap_v;
@@ -423,6 +425,7 @@ int run_pass(sn_context *ctx, int pass_id, const PassSpec &sp, int e0, int ec, i
     b.d_npairs = w.counts.as<uint64_t>() + 1;
     b.cap_p = cap_p;
     b.recs_un = w.recs_un.as<SplatRec>();
+    b.gid_un = reordered ? w.gid_un.as<uint32_t>() : nullptr;
     b.rects_in = w.rects_tun.as<ushort4>();  // the blend's (tight) rectangles into depth order
     b.env_off = w.env_off.as<uint64_t>();
     b.rects_out = w.rects.as<ushort4>();

@@ -148,9 +148,11 @@ __global__ void __launch_bounds__(kBlock) super_rects_kernel(BinArgs b, ushort4 
 // re-ordered here by the full float64 z, then by slot (= original index, the emit writes in index
 // order): the exact np.lexsort((idx, z)) order. Runs are almost always 1-3 long; long runs
 // (pathological exact-depth planes) fall back to an in-place heap sort.
-__device__ __forceinline__ bool z_less(const SplatRec *recs, uint32_t a, uint32_t c) {
+// (a spatially reordered scene, sn_cloud.index: the slot order is not the original order -- ties
+// compare the original ids the emit wrote, gid)
+__device__ __forceinline__ bool z_less(const SplatRec *recs, const uint32_t *gid, uint32_t a, uint32_t c) {
     double za = recs[a].z, zc = recs[c].z;
-    return za < zc || (za == zc && a < c);
+    return za < zc || (za == zc && (gid ? gid[a] < gid[c] : a < c));
 }
 
 // Sorts the run of equal 32-bit keys starting at i by (exact z, index).
@@ -165,7 +167,7 @@ __device__ __forceinline__ void tie_fix_run(const BinArgs &b, int64_t i, int64_t
         for (int64_t x = 1; x < L; ++x) {  // insertion sort
             uint32_t cur = v[x];
             int64_t y = x - 1;
-            while (y >= 0 && z_less(b.recs_un, cur, v[y])) {
+            while (y >= 0 && z_less(b.recs_un, b.gid_un, cur, v[y])) {
                 v[y + 1] = v[y];
                 --y;
             }
@@ -177,8 +179,8 @@ __device__ __forceinline__ void tie_fix_run(const BinArgs &b, int64_t i, int64_t
     auto sift = [&](int64_t root, int64_t end) {
         while (2 * root + 1 < end) {
             int64_t c = 2 * root + 1;
-            if (c + 1 < end && z_less(b.recs_un, v[c], v[c + 1])) ++c;
-            if (!z_less(b.recs_un, v[root], v[c])) return;
+            if (c + 1 < end && z_less(b.recs_un, b.gid_un, v[c], v[c + 1])) ++c;
+            if (!z_less(b.recs_un, b.gid_un, v[root], v[c])) return;
             uint32_t t = v[root];
             v[root] = v[c];
             v[c] = t;

@@ -126,6 +126,8 @@ struct BinArgs {
     const uint32_t *keys_sorted;   // 32-bit depth keys after the sort
     uint32_t *vals_sorted;         // depth order -> unsorted record slot (tie-fixed in place)
     const SplatRec *recs_un;       // unsorted records (z for the tie fix)
+    const uint32_t *gid_un;        // original ids per slot when the slot order is not the original
+                                   // order (spatially reordered scene), else null
     const ushort4 *rects_in;
     const uint64_t *env_off;
     ushort4 *rects_out;

@@ -257,6 +257,7 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
     __shared__ unsigned s_near[kMaxEnvChunk];
     __shared__ unsigned s_farz[kMaxEnvChunk];  // lazy far: in-depth items at z >= z_cut
     __shared__ double s_zcut[kMaxEnvChunk];
+    __shared__ uint8_t s_bcode[kMaxEnvChunk];  // per env, the whole block: 0 test, 1 out of depth, 2 far
     stage_cams(a, s_cam);
     if (threadIdx.x < a.ec) {
         s_near[threadIdx.x] = 0u;
@@ -265,6 +266,33 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
     }
     s_nearbits[threadIdx.x] = 0ull;
     init_counts(s_cnt, a.ec);  // (synchronizes)
+    if (threadIdx.x < a.ec) {
+        // A spatially ordered scene's 256-row block is decided per env from its bounding box where
+        // the box is entirely out of (near, far), or (lazy far) entirely in depth at or beyond the
+        // cut: the items' float64 z lies within the box's z range (plus a margin far above the
+        // rounding of their dot products), so every item's depth test has the block's answer.
+        uint8_t code = 0;
+        if (c.block_bounds) {
+            const float *bb = c.block_bounds + 8 * (int64_t)blockIdx.x;
+            const sn_camera &cam = s_cam[threadIdx.x];
+            const double cx = 0.5 * ((double)bb[0] + (double)bb[3]), cy = 0.5 * ((double)bb[1] + (double)bb[4]),
+                         cz = 0.5 * ((double)bb[2] + (double)bb[5]);
+            const double hx = 0.5 * ((double)bb[3] - (double)bb[0]), hy = 0.5 * ((double)bb[4] - (double)bb[1]),
+                         hz = 0.5 * ((double)bb[5] - (double)bb[2]);
+            const double zc = (cam.rot[6] * cx + cam.rot[7] * cy) + cam.rot[8] * cz + cam.trans[2];
+            const double zr = fabs(cam.rot[6]) * hx + fabs(cam.rot[7]) * hy + fabs(cam.rot[8]) * hz;
+            const double tol = 1e-9 * (1.0 + fabs(zc) + zr + fabs(cam.trans[2]));
+            const double zmin = zc - zr - tol, zmax = zc + zr + tol;
+            if (hx >= 0.0 && hy >= 0.0 && hz >= 0.0 && zmin == zmin && zmax == zmax) {  // (NaN: test)
+                if (zmax < cam.near_ || zmin > cam.far_)
+                    code = 1;
+                else if (a.lazy_far && zmin > cam.near_ && zmax < cam.far_ && zmin > s_zcut[threadIdx.x])
+                    code = 2;
+            }
+        }
+        s_bcode[threadIdx.x] = code;
+    }
+    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     bool valid = g < c.n;
@@ -300,9 +328,17 @@ __global__ void __launch_bounds__(kBlock, SN_COUNT_MIN_BLOCKS) scene_count_kerne
         in_m = fz_m = 0u;
         for (int e = e0; e < e1; ++e) {
             const sn_camera &cam = s_cam[e];
-            const double z = cam_z(p, cam);
-            const bool in = valid && (z > cam.near_) && (z < cam.far_);
-            const bool fz = kLazy && in && !(z < s_zcut[e]);
+            const int bc = s_bcode[e];  // (uniform)
+            bool in, fz;
+            if (bc == 1) {
+                in = fz = false;
+            } else if (kLazy && bc == 2) {
+                in = fz = valid;
+            } else {
+                const double z = cam_z(p, cam);
+                in = valid && (z > cam.near_) && (z < cam.far_);
+                fz = kLazy && in && !(z < s_zcut[e]);
+            }
             in_m |= (unsigned)(in && !fz) << (e - e0);
             fz_m |= (unsigned)fz << (e - e0);
             const bool mine = lane == e - e0;
@@ -453,7 +489,7 @@ __global__ void __launch_bounds__(kBlock, SN_EMIT_MIN_BLOCKS) scene_emit_kernel(
             float dir[3], rgb[3];
             view_dir(p, cam, dir);
             eval_sh_f32(c.sh, c.n, g0 + l, c.sh_k, dir[0], dir[1], dir[2], rgb);
-            write_splat(a, pos, e, geo, d[9], rgb, (uint32_t)(g0 + l));
+            write_splat(a, pos, e, geo, d[9], rgb, c.index ? __ldg(c.index + g0 + l) : (uint32_t)(g0 + l));
         }
         __syncwarp();
     }
@@ -892,7 +928,7 @@ __global__ void __launch_bounds__(kBlock, SN_EMIT_MIN_BLOCKS) far_collect_kernel
             rec.rgb = pack_rgb21(rgb);
             f.recs[j] = rec;
             f.geo[j] = make_blend_geo(rec.ca, rec.cb2, rec.cc);
-            f.gid[j] = (uint32_t)(g0 + l);
+            f.gid[j] = c.index ? __ldg(c.index + g0 + l) : (uint32_t)(g0 + l);
             const unsigned long long off = (unsigned long long)__double_as_longlong(geo.z) - f.z_base;
             const uint32_t zkey = (uint32_t)(f.z_bits > 32 ? off >> (f.z_bits - 32) : off << (32 - f.z_bits));
             const uint32_t zlo = zkey >> f.ub;

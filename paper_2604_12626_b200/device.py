@@ -62,8 +62,9 @@ class DeviceCloud:
         self.log_scales = torch.from_numpy(_pack4(cloud.log_scales, 3, dt)).to(dev)
         self.rotations = torch.from_numpy(_pack4(cloud.rotations, 4, dt)).to(dev)
         self.sh = torch.from_numpy(sh).to(dev)
+        self.index = self.block_bounds = None
         self._struct = N.SnCloud(n, k, self.dtype, self.pos_opacity.data_ptr(), self.log_scales.data_ptr(),
-                                 self.rotations.data_ptr(), self.sh.data_ptr())
+                                 self.rotations.data_ptr(), self.sh.data_ptr(), None, None)
 
     @classmethod
     def wrap(cls, cloud, device=None):
@@ -78,15 +79,70 @@ class DeviceCloud:
         self.dtype = dtype
         self.device = device
         self.pos_opacity, self.log_scales, self.rotations, self.sh = pos_opacity, log_scales, rotations, sh
+        self.index = self.block_bounds = None
         self._struct = N.SnCloud(self.n, self.sh_k, dtype, pos_opacity.data_ptr(), log_scales.data_ptr(),
-                                 rotations.data_ptr(), sh.data_ptr())
+                                 rotations.data_ptr(), sh.data_ptr(), None, None)
         return self
 
+    def spatially_ordered(self):
+        """A copy with the rows in Morton (Z-curve) order of the positions, carrying each row's
+        original index and the bounding box of every 256-row block (sn_cloud ABI 3): the count
+        kernel decides whole blocks per env where the box allows, and every order-dependent output
+        (depth ties, ids) uses the original index, so renders equal the original order's."""
+        if self.index is not None:
+            return self
+        pos = self.pos_opacity[:, :3].double()
+        n = self.n
+        lo = pos.amin(0) if n else torch.zeros(3, dtype=torch.float64, device=pos.device)
+        hi = pos.amax(0) if n else lo
+        span = (hi - lo).clamp_min(1e-30)
+        q = ((pos - lo) / span * 1023.0).clamp(0, 1023).long()
+
+        def spread(v):  # 10 bits -> every third bit
+            v = (v | (v << 16)) & 0x030000FF
+            v = (v | (v << 8)) & 0x0300F00F
+            v = (v | (v << 4)) & 0x030C30C3
+            return (v | (v << 2)) & 0x09249249
+
+        code = spread(q[:, 0]) | (spread(q[:, 1]) << 1) | (spread(q[:, 2]) << 2)
+        perm = torch.sort(code, stable=True).indices
+        out = DeviceCloud.__new__(DeviceCloud)
+        out.n, out.sh_k, out.dtype, out.device = n, self.sh_k, self.dtype, self.device
+        out.pos_opacity = self.pos_opacity[perm].contiguous()
+        out.log_scales = self.log_scales[perm].contiguous()
+        out.rotations = self.rotations[perm].contiguous()
+        out.sh = self.sh[:, perm].contiguous()
+        out.index = perm.to(torch.int32).contiguous()
+        nb = (n + 255) // 256
+        p = out.pos_opacity[:, :3].double()
+        pmin = torch.full((nb * 256, 3), float("inf"), dtype=torch.float64, device=p.device)
+        pmax = torch.full((nb * 256, 3), float("-inf"), dtype=torch.float64, device=p.device)
+        pmin[:n] = p
+        pmax[:n] = p
+        bmin = pmin.view(nb, 256, 3).amin(1)
+        bmax = pmax.view(nb, 256, 3).amax(1)
+        # float32 bounds rounded outward (exact for float32 positions)
+        lo32, hi32 = bmin.float(), bmax.float()
+        lo32 = torch.where(lo32.double() > bmin, torch.nextafter(lo32, torch.full_like(lo32, -float("inf"))), lo32)
+        hi32 = torch.where(hi32.double() < bmax, torch.nextafter(hi32, torch.full_like(hi32, float("inf"))), hi32)
+        out.block_bounds = torch.cat([lo32, hi32, torch.zeros(nb, 2, dtype=torch.float32, device=p.device)],
+                                     dim=1).contiguous()
+        out._struct = N.SnCloud(n, out.sh_k, out.dtype, out.pos_opacity.data_ptr(), out.log_scales.data_ptr(),
+                                out.rotations.data_ptr(), out.sh.data_ptr(), out.index.data_ptr(),
+                                out.block_bounds.data_ptr())
+        return out
+
     def to_host(self):
-        """(positions (n,3), sh_coeffs (n,K,3), opacities (n,), log_scales (n,3), rotations (n,4))"""
+        """(positions (n,3), sh_coeffs (n,K,3), opacities (n,), log_scales (n,3), rotations (n,4)), in
+        the original row order"""
         po = self.pos_opacity.cpu().numpy()
         sh = self.sh.cpu().numpy().T.reshape(self.n, self.sh_k, 3)
-        return po[:, :3], sh, po[:, 3], self.log_scales.cpu().numpy()[:, :3], self.rotations.cpu().numpy()
+        ls, rot = self.log_scales.cpu().numpy()[:, :3], self.rotations.cpu().numpy()
+        if self.index is not None:
+            inv = np.empty(self.n, dtype=np.int64)
+            inv[self.index.cpu().numpy()] = np.arange(self.n)
+            po, sh, ls, rot = po[inv], sh[inv], ls[inv], rot[inv]
+        return po[:, :3], sh, po[:, 3], ls, rot
 
     def struct(self):
         return self._struct

@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
     missing = [s for s in declared_functions() if not hasattr(lib, s)]
     assert not missing, missing
     assert sorted(N.EXPORTS) == declared_functions()
-    assert N.load().sn_abi_version() == N.ABI_VERSION == 2
+    assert N.load().sn_abi_version() == N.ABI_VERSION == 3
 
 
 def _c_layout(struct, fields):
