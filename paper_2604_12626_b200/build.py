@@ -36,15 +36,18 @@ def up_to_date():
     return all(os.path.getmtime(f) <= t for f in sources() + headers())
 
 
-def build(force=False, verbose=False, extra_flags=()):
-    if not force and not extra_flags and up_to_date():
+def build(force=False, verbose=False, extra_flags=(), lib=LIB, obj_dir=OBJ):
+    """Compile csrc/*.cu into `lib`; `extra_flags` / `lib` / `obj_dir` build a variant (e.g. the
+    bounds-checked -DSN_CHECKS library under build_variants/) without touching the product library."""
+    if not force and not extra_flags and lib == LIB and up_to_date():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(obj_dir, exist_ok=True)
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
     flags = NVCC_FLAGS + list(extra_flags)
 
     def compile_one(src):
-        obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+        obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
         cmd = [nvcc] + flags + ["-c", "-o", obj, src]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
@@ -53,12 +56,23 @@ def build(force=False, verbose=False, extra_flags=()):
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, sources()))
-    cmd = [nvcc] + ARCH + ["-shared", "-o", LIB] + objs
+    cmd = [nvcc] + ARCH + ["-shared", "-o", lib] + objs
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True, cwd=CSRC)
-    return LIB
+    return lib
+
+
+def build_checks(verbose=False):
+    """The bounds-checked variant (SN_ASSERT on every shared-memory queue, gather and pair write)."""
+    root = os.path.dirname(HERE)
+    return build(force=True, verbose=verbose, extra_flags=["-DSN_CHECKS"],
+                 lib=os.path.join(root, "build_variants", "libsn_checks.so"),
+                 obj_dir=os.path.join(root, "build", "obj_checks"))
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    if "--checks" in sys.argv:
+        build_checks(verbose=True)
+    else:
+        build(force="--force" in sys.argv, verbose=True)
