@@ -16,6 +16,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "sn_common.cuh"
 #include "sn_internal.h"
 
@@ -220,13 +222,27 @@ struct StageTimer {
     double *ms;  // host (SN_N_STAGES) for this pass, or null
     int pass;
     int open = -1;
+    bool nvtx_open = false;
     void begin(int stage) {
+        // NVTX range per stage (host side: it brackets the stage's launches; free with no tool attached)
+        static const char *const kNames[2][13] = {
+            {"scene.pose", "scene.count", "scene.scan", "scene.emit", "scene.depth_sort", "scene.permute",
+             "scene.pair_scan", "scene.bin_count", "scene.bin_scatter", "scene.ranges", "scene.blend",
+             "scene.composite", "scene.far"},
+            {"layer.pose", "layer.count", "layer.scan", "layer.emit", "layer.depth_sort", "layer.permute",
+             "layer.pair_scan", "layer.bin_count", "layer.bin_scatter", "layer.ranges", "layer.blend",
+             "layer.composite", "layer.far"}};
+        if (nvtx_open) nvtxRangePop();
+        nvtxRangePushA(kNames[pass ? 1 : 0][stage >= 0 && stage < 13 ? stage : 0]);
+        nvtx_open = true;
         if (!ms) return;
         resolve_stage(ctx, pass, stage);  // the event pair is about to be reused (multi-chunk renders)
         open = stage;
         cudaEventRecord(ctx->ev[pass][stage][0], st);
     }
     void end() {
+        if (nvtx_open) nvtxRangePop();
+        nvtx_open = false;
         if (!ms || open < 0) return;
         cudaEventRecord(ctx->ev[pass][open][1], st);
         ctx->ms_dst[pass][open] = ms + open;
